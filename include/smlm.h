@@ -1,0 +1,185 @@
+/*
+ * smlm.h -- C ABI of the B200-native Segmented Multi-LoRA Multiplication (SMLM) library.
+ *
+ * What the library computes (§3.3 "Unified computation flow management
+ * and SMLM kernel"): for one linear layer ("we adapt the Punica kernel to process LoRA weights
+ * one linear layer at a time"), a single call computes, for every row of a packed mixed
+ * batch, the base projection plus the LoRA term of the adapter assigned to the row's segment,
+ * for all four request kinds ("fine-tuning (training), evaluation, prefilling, and decoding",
+ * P:384), with a static per-adapter scale and an optional dynamic per-request scale.
+ * The backward covers fine-tune rows only ("a shared backward pass") and masks
+ * gradients per adapter (MixedLoRAModelForTrainer).  The adapter pool mirrors the
+ * paper's Virtualized Module contract: adapters are loaded and unloaded at runtime without
+ * re-splicing and the base weight is shared, never copied.
+ *
+ * Math (row t in segment g, adapter a = seg_slot[g], s = slot_scale[a] * seg_scale[g]):
+ *     V[t]  = A_a x_t                         (rank-r intermediate)
+ *     y_t   = W x_t + s B_a V[t]              (a == -1: y_t = W x_t)
+ *   fine-tune rows only:
+ *     U[t]  = B_a^T dy_t
+ *     dx_t  = W^T dy_t + s A_a^T U[t]
+ *     dA_a  = s sum_t U[t] x_t^T     dB_a = s sum_t dy_t V[t]^T
+ *
+ * Layout: row-major everywhere (nn.Linear / PEFT convention).
+ *     X [S,in]   W [out,in]   A_a [r,in]   B_a [out,r]   Y [S,out]   V_save [S,r]
+ *     dY [S,out] dX [S,in]    dA_a [r,in] (fp32)         dB_a [out,r] (fp32)
+ * Element type of every tensor is the pool dtype (SMLM_BF16, or SMLM_FP32 test mode) except
+ * dA/dB, which are always fp32.  All tensor pointers are DEVICE pointers unless marked "host".
+ *
+ * Ownership: the caller owns every tensor (X, W, Y, A, B, V_save, dY, dX, dA, dB, workspace).
+ * smlm_adapter_register BORROWS A and B (zero copy): they must stay alive and unchanged in
+ * shape until smlm_adapter_unregister has been ordered on the stream; their VALUES may be
+ * updated in place (e.g. by an optimizer) between calls.  The pool owns only its slot table.
+ *
+ * Errors: every entry point validates on the host before anything is enqueued; on error no
+ * output is touched and a status below is returned; smlm_last_error() gives a thread-local
+ * message.  Asynchronous CUDA faults surface as SMLM_E_CUDA from a later call.
+ * There is no CPU fallback: a device that is not sm_100 gives SMLM_E_UNSUPPORTED.
+ *
+ * Threading: all work is stream-ordered on the given stream with no host synchronisation
+ * (the plan is staged through a pinned ring buffer).  A pool must be used by one host thread
+ * at a time.
+ */
+#ifndef SMLM_H_
+#define SMLM_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define SMLM_API __attribute__((visibility("default")))
+#else
+#define SMLM_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct smlm_pool_s *smlm_pool; /* one pool per (layer, projection) */
+
+enum smlm_status {
+    SMLM_OK = 0,
+    SMLM_E_INVALID = 1,     /* malformed offsets, mode outside 0..3, bad scale, null pointer */
+    SMLM_E_SHAPE = 2,       /* shape or dtype mismatch */
+    SMLM_E_SLOT = 3,        /* slot not registered / out of range */
+    SMLM_E_CAPACITY = 4,    /* pool full */
+    SMLM_E_CUDA = 5,        /* a CUDA runtime/driver error (sticky device errors included) */
+    SMLM_E_UNSUPPORTED = 6, /* not an sm_100 device, or a shape/rank the dtype path lacks */
+    SMLM_E_WORKSPACE = 7    /* workspace smaller than smlm_workspace_size() */
+};
+
+/* Request kinds, PAPER.md P:384 ("fine-tuning (training), evaluation, prefilling, and decoding") */
+enum smlm_mode { SMLM_FINETUNE = 0, SMLM_EVAL = 1, SMLM_PREFILL = 2, SMLM_DECODE = 3 };
+
+/* SMLM_BF16: bf16 tensors, fp32 accumulation on tcgen05 tensor cores (production path).
+ * SMLM_FP32: fp32 tensors, fp32 SIMT kernels with chunked accumulation (1e-5 parity mode). */
+enum smlm_dtype { SMLM_BF16 = 0, SMLM_FP32 = 1 };
+
+/* Options for smlm_pool_set_option */
+enum smlm_option {
+    SMLM_OPT_L_LONG = 0 /* segments with >= L_long rows take the long (per-segment tile) path; default 64 */
+};
+
+/*
+ * Create a pool for one (layer, projection) of shape (in_features -> out_features) with LoRA
+ * rank `rank` and room for `capacity` adapters, on CUDA device `device`.
+ * bf16: rank in {8,16,32,64}; in/out multiples of 64.  fp32: 1 <= rank <= 64; in/out >= 1.
+ * Errors: SMLM_E_INVALID (capacity < 1, null out), SMLM_E_UNSUPPORTED (device not sm_100,
+ * rank/shape not supported by the dtype path), SMLM_E_CUDA.
+ */
+SMLM_API int smlm_pool_create(int device, int in_features, int out_features, int rank, int capacity,
+                     int dtype, smlm_pool *out);
+SMLM_API int smlm_pool_destroy(smlm_pool pool);
+SMLM_API int smlm_pool_set_option(smlm_pool pool, int option, int value);
+
+/*
+ * Register (load) an adapter: A [rank,in], B [out,rank] (device, pool dtype, row-major,
+ * 16-byte aligned, borrowed).  `scale` is the static slot scale alpha/r (> 0, finite; pass 1 if
+ * the caller baked the scale into B).  The device slot table update is ordered on
+ * `stream` (a cudaStream_t; NULL = legacy default stream).  Writes the slot index to *slot_out.
+ * Errors: SMLM_E_INVALID, SMLM_E_CAPACITY (no free slot), SMLM_E_CUDA.
+ */
+SMLM_API int smlm_adapter_register(smlm_pool pool, const void *A, const void *B, float scale, void *stream,
+                          int *slot_out);
+/* Bind fp32 gradient buffers dA [rank,in], dB [out,rank] (device) to a slot; NULL = frozen
+ * (masked).  Takes effect for calls issued after it.  Errors: SMLM_E_SLOT. */
+SMLM_API int smlm_adapter_set_grad(smlm_pool pool, int slot, float *dA, float *dB);
+/* Unload an adapter; the slot may be reused by a later register.  Errors: SMLM_E_SLOT. */
+SMLM_API int smlm_adapter_unregister(smlm_pool pool, int slot, void *stream);
+
+/*
+ * A segmented mixed batch (Alg. 1 Require P:326-329: rows packed over all requests).
+ * All arrays are HOST memory, read during the call only.
+ *   seg_offsets [G+1]: 0 = off[0] <= off[1] <= ... <= off[G] = S; empty segments allowed
+ *   seg_slot    [G]  : -1 = base only, else a registered slot
+ *   seg_mode    [G]  : SMLM_FINETUNE .. SMLM_DECODE
+ *   seg_scale   [G]  : dynamic per-request scale (finite, > 0) or NULL (= 1); multiplies the
+ *                      slot scale ("applied on a per-request basis during the forward pass")
+ */
+typedef struct {
+    int S;
+    int G;
+    const int32_t *seg_offsets;
+    const int32_t *seg_slot;
+    const int8_t *seg_mode;
+    const float *seg_scale;
+} smlm_batch;
+
+/* Bytes of device workspace a forward (backward = 0) or backward (backward = 1) call needs. */
+SMLM_API size_t smlm_workspace_size(smlm_pool pool, const smlm_batch *batch, int backward);
+
+/*
+ * Forward: Y = W X + s B_a (A_a X) per segment.
+ *   X [S,in]; W [out,in] or NULL (then Y holds the base output on entry and only the LoRA term
+ *   is added in place); Y [S,out]; V_save [S,rank] or NULL: receives the unscaled V = A_a x_t of
+ *   every FINETUNE row that has an adapter (other rows untouched).
+ *   ws: device workspace of ws_bytes >= smlm_workspace_size(pool, batch, 0).
+ * Errors: SMLM_E_INVALID / SMLM_E_SLOT / SMLM_E_WORKSPACE / SMLM_E_CUDA; S == 0 or G == 0 is a
+ * no-op returning SMLM_OK.
+ */
+SMLM_API int smlm_forward(smlm_pool pool, const smlm_batch *batch, const void *X, const void *W, void *Y,
+                 void *V_save, void *ws, size_t ws_bytes, void *stream);
+
+/*
+ * Backward over FINETUNE rows.
+ *   X [S,in], W [out,in] (required when dX != NULL), dY [S,out];
+ *   V_save [S,rank] from the forward, or NULL (V is then recomputed from X);
+ *   dX [S,in] or NULL: FINETUNE rows written, other rows untouched;
+ *   dA/dB of every slot that has grad buffers AND fine-tune rows in this batch are overwritten
+ *   (accumulate = 0) or incremented (accumulate = 1) with the sum over all of that slot's
+ *   fine-tune rows, reduced in the fixed canonical order (bitwise deterministic).  Slots with
+ *   grad buffers but no fine-tune rows are untouched; slots without grad buffers get none.
+ */
+SMLM_API int smlm_backward(smlm_pool pool, const smlm_batch *batch, const void *X, const void *W,
+                  const void *dY, const void *V_save, void *dX, int accumulate, void *ws,
+                  size_t ws_bytes, void *stream);
+
+/*
+ * The canonical work plan (segment scheduler output), as int32
+ * records of 6 words, written to HOST memory `items` (capacity max_items records);
+ * *n_items receives the record count (also when the buffer is too small: SMLM_E_WORKSPACE).
+ * smlm_plan is a pure host function (no device needed): slot_registered [capacity] host flags.
+ */
+SMLM_API int smlm_plan(const smlm_batch *batch, int capacity, const uint8_t *slot_registered, int l_long,
+              int backward, int32_t *items, int max_items, int *n_items);
+SMLM_API int smlm_plan_export(smlm_pool pool, const smlm_batch *batch, int backward, int32_t *items,
+                     int max_items, int *n_items);
+
+SMLM_API const char *smlm_status_string(int status);
+SMLM_API const char *smlm_last_error(void);
+
+/* ---- instrumentation (used by bench.py; not needed for correctness) ---- */
+/* Number of kernels this library has launched in this process. */
+SMLM_API uint64_t smlm_launch_count(void);
+/* When enabled, the library records CUDA events around its main GEMM kernels on the launching
+ * stream; smlm_profile_read synchronises those events and returns the summed milliseconds and
+ * launch count for kernel class `kind` (0 = forward GEMM, 1 = backward dX GEMM, 2 = short-row
+ * shrink, 3 = dA/dB) since the last reset, then resets that class. */
+SMLM_API int smlm_profile_enable(int on);
+SMLM_API int smlm_profile_read(int kind, double *total_ms, int *count);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SMLM_H_ */

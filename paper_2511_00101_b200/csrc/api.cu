@@ -1,0 +1,714 @@
+// api.cu -- the C ABI (include/smlm.h): adapter pools, validation, plan staging, dispatch.
+//
+// PAPER.md mapping:
+//   * per-(layer, projection) pool, adapters loaded/unloaded at runtime
+//   * shared base weight passed per call, never copied ("no additional GPU memory overhead")
+//   * static slot scale x dynamic per-request scale
+//   * backward for fine-tune rows only, gradients masked per adapter
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+#include <math.h>
+#include <string.h>
+
+#include <atomic>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/smlm.h"
+#include "device_types.h"
+#include "plan.h"
+
+namespace smlm {
+int gemm_stages(int r_pad, size_t *smem_bytes);
+int launch_gemm(const GemmArgs &a, bool bwd, int num_sms, cudaStream_t st);
+int launch_shrink_short(const __nv_bfloat16 *X, const SlotDev *slots, const DevBlock *blocks,
+                        const DevShortRow *srows, int n_blocks, int in_f, int r, int r_pad, __nv_bfloat16 *Vbd,
+                        __nv_bfloat16 *Vsave, cudaStream_t st);
+template <typename T>
+int launch_rows_shrink(const DevTile *tiles, int n_tiles, const SlotDev *slots, const T *X, int in_f, int r,
+                       float *Vf, T *Vsave, int ft_only, cudaStream_t st);
+template <typename T>
+int launch_rows_u(const DevTile *tiles, int n_tiles, const SlotDev *slots, const T *dY, int out_f, int r, float *Uf,
+                  cudaStream_t st);
+size_t grad_group_bytes();
+void fill_grad_group(void *dst, int slot, int tile_begin, int n_tiles, float *dA, float *dB);
+template <typename T, typename TV>
+int launch_dadb(const DevTile *tiles, const void *groups, int n_groups, const T *X, const T *dY, const float *Uf,
+                const TV *V, int in_f, int out_f, int r, int accumulate, cudaStream_t st);
+int launch_f32_fwd(const DevTile *tiles, int n_tiles, const SlotDev *slots, const float *X, const float *W, float *Y,
+                   const float *Vf, int in_f, int out_f, int r, cudaStream_t st);
+int launch_f32_dx(const DevTile *tiles, int n_tiles, const SlotDev *slots, const float *dY, const float *W, float *dX,
+                  const float *Uf, int in_f, int out_f, int r, cudaStream_t st);
+}  // namespace smlm
+
+using namespace smlm;
+
+// ------------------------------------------------------------------------------------------
+// error reporting, instrumentation
+// ------------------------------------------------------------------------------------------
+static thread_local std::string g_last_error;
+static std::atomic<uint64_t> g_launches{0};
+
+static int set_err(int code, const std::string &msg) {
+    g_last_error = msg;
+    return code;
+}
+static int cuda_err(cudaError_t e, const char *where) {
+    return set_err(SMLM_E_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+#define CK(call)                                                   \
+    do {                                                           \
+        cudaError_t _e = (call);                                   \
+        if (_e != cudaSuccess) return cuda_err(_e, #call);         \
+    } while (0)
+#define CKL(expr, n)                                               \
+    do {                                                           \
+        int _e = (expr);                                           \
+        if (_e != 0) return cuda_err((cudaError_t)_e, #expr);      \
+        g_launches += (n);                                         \
+    } while (0)
+
+namespace {
+
+struct Profiler {
+    std::mutex mu;
+    bool on = false;
+    struct Rec { cudaEvent_t a, b; int kind; };
+    std::vector<Rec> recs;
+    std::vector<cudaEvent_t> pool;
+    cudaEvent_t get() {
+        if (!pool.empty()) { cudaEvent_t e = pool.back(); pool.pop_back(); return e; }
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        return e;
+    }
+} g_prof;
+
+struct ProfScope {
+    cudaEvent_t a = nullptr;
+    int kind;
+    cudaStream_t st;
+    ProfScope(int k, cudaStream_t s) : kind(k), st(s) {
+        if (g_prof.on) {
+            std::lock_guard<std::mutex> lk(g_prof.mu);
+            a = g_prof.get();
+            cudaEventRecord(a, st);
+        }
+    }
+    ~ProfScope() {
+        if (a) {
+            std::lock_guard<std::mutex> lk(g_prof.mu);
+            cudaEvent_t b = g_prof.get();
+            cudaEventRecord(b, st);
+            g_prof.recs.push_back({a, b, kind});
+        }
+    }
+};
+
+// ------------------------------------------------------------------------------------------
+// TMA descriptor encoding through the driver entry point (no -lcuda link dependency)
+// ------------------------------------------------------------------------------------------
+PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+
+int get_encode() {
+    if (g_encode) return SMLM_OK;
+    void *fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
+    if (e != cudaSuccess || !fn) return set_err(SMLM_E_CUDA, "cuTensorMapEncodeTiled entry point unavailable");
+    g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    return SMLM_OK;
+}
+
+CUtensorMapSwizzle swizzle_for(int row_bytes) {
+    return row_bytes >= 128 ? CU_TENSOR_MAP_SWIZZLE_128B
+                            : (row_bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B);
+}
+
+// 2-D bf16 tensor [outer, inner] row-major
+int make_map(CUtensorMap *m, const void *ptr, uint64_t inner, uint64_t outer, uint32_t box_inner,
+             uint32_t box_outer, CUtensorMapSwizzle swz) {
+    if (get_encode() != SMLM_OK) return SMLM_E_CUDA;
+    cuuint64_t dims[2] = {inner, outer};
+    cuuint64_t strides[1] = {inner * 2};
+    cuuint32_t box[2] = {box_inner, box_outer};
+    cuuint32_t es[2] = {1, 1};
+    CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void *>(ptr), dims, strides, box, es,
+                          CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return set_err(SMLM_E_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+    return SMLM_OK;
+}
+
+// ------------------------------------------------------------------------------------------
+// pinned staging ring (plan uploads and slot-table updates stay stream-ordered, no host sync)
+// ------------------------------------------------------------------------------------------
+struct Ring {
+    struct Ent {
+        void *host = nullptr;
+        size_t cap = 0;
+        cudaEvent_t ev = nullptr;
+        bool pending = false;
+    };
+    Ent e[8];
+    int next = 0;
+    ~Ring() {
+        for (auto &x : e) {
+            if (x.pending) cudaEventSynchronize(x.ev);
+            if (x.host) cudaFreeHost(x.host);
+            if (x.ev) cudaEventDestroy(x.ev);
+        }
+    }
+    // returns index of a free pinned buffer with >= bytes capacity
+    int acquire(size_t bytes, void **host) {
+        Ent &x = e[next];
+        if (x.pending) {
+            cudaEventSynchronize(x.ev);
+            x.pending = false;
+        }
+        if (x.cap < bytes) {
+            if (x.host) cudaFreeHost(x.host);
+            x.host = nullptr;
+            size_t cap = bytes < 65536 ? 65536 : bytes * 2;
+            if (cudaMallocHost(&x.host, cap) != cudaSuccess) return -1;
+            x.cap = cap;
+        }
+        if (!x.ev) cudaEventCreateWithFlags(&x.ev, cudaEventDisableTiming);
+        *host = x.host;
+        int idx = next;
+        next = (next + 1) % 8;
+        return idx;
+    }
+    void release(int idx, cudaStream_t st) {
+        cudaEventRecord(e[idx].ev, st);
+        e[idx].pending = true;
+    }
+};
+
+struct SlotHost {
+    bool used = false;
+    const void *A = nullptr;
+    const void *B = nullptr;
+    float scale = 1.f;
+    float *dA = nullptr;
+    float *dB = nullptr;
+};
+
+size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+}  // namespace
+
+struct smlm_pool_s {
+    int device = 0;
+    int in = 0, out = 0, r = 0, r_pad = 16, cap = 0, dtype = 0;
+    int l_long = 64;
+    int num_sms = 148;
+    std::vector<SlotHost> slots;
+    std::vector<uint8_t> ok;
+    std::vector<float> scales;
+    SlotDev *d_slots = nullptr;
+    Ring ring;
+};
+
+namespace {
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev);
+        if (prev != dev) cudaSetDevice(dev);
+    }
+    ~DeviceGuard() {
+        int cur;
+        cudaGetDevice(&cur);
+        if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+int check_sticky() {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_err(e, "pending CUDA error");
+    return SMLM_OK;
+}
+
+// Sizes of the workspace sections for a planned call.
+struct WsLayout {
+    size_t plan_off = 0, plan_bytes = 0;
+    size_t vbd_off = 0, vbd_bytes = 0;     // bf16 fwd: block-diagonal s*V of short tiles
+    size_t u_off = 0, u_bytes = 0;         // bwd: U fp32 [S,r]
+    size_t vf_off = 0, vf_bytes = 0;       // fp32 V [S,r] (fp32 mode, or bwd recompute)
+    size_t total = 0;
+};
+
+int plan_for(smlm_pool p, const smlm_batch *b, bool bwd, Plan &plan) {
+    std::string msg;
+    // fp32 test mode consumes segment-aligned tiles for every row (L_long = 1)
+    int l_long = p->dtype == SMLM_FP32 ? 1 : p->l_long;
+    int rc = build_plan(b, p->cap, p->ok.data(), p->scales.data(), l_long, bwd, plan, msg);
+    if (rc != SMLM_OK) return set_err(rc, msg);
+    return SMLM_OK;
+}
+
+WsLayout layout_for(smlm_pool p, const smlm_batch *b, const Plan &plan, bool bwd, bool need_vf) {
+    WsLayout L;
+    size_t off = 0;
+    if (!bwd) {
+        L.plan_bytes = (plan.long_tiles.size() + plan.short_tiles.size()) * sizeof(DevTile) +
+                       plan.blocks.size() * sizeof(DevBlock) + plan.short_rows.size() * sizeof(DevShortRow);
+    } else {
+        L.plan_bytes = plan.bwd_tiles.size() * sizeof(DevTile) + plan.groups.size() * grad_group_bytes();
+    }
+    L.plan_off = off;
+    off = align256(off + L.plan_bytes + 16);
+    if (!bwd && p->dtype == SMLM_BF16) {
+        L.vbd_off = off;
+        L.vbd_bytes = plan.blocks.size() * 128 * (size_t)p->r_pad * 2;
+        off = align256(off + L.vbd_bytes);
+    }
+    if (bwd) {
+        L.u_off = off;
+        L.u_bytes = (size_t)b->S * p->r * 4;
+        off = align256(off + L.u_bytes);
+    }
+    if (need_vf) {
+        L.vf_off = off;
+        L.vf_bytes = (size_t)b->S * p->r * 4;
+        off = align256(off + L.vf_bytes);
+    }
+    L.total = off;
+    return L;
+}
+
+// Copy a host byte vector into the workspace through the pinned ring (stream ordered).
+int stage_upload(smlm_pool p, const std::vector<uint8_t> &bytes, void *dst, cudaStream_t st) {
+    if (bytes.empty()) return SMLM_OK;
+    void *h = nullptr;
+    int idx = p->ring.acquire(bytes.size(), &h);
+    if (idx < 0) return set_err(SMLM_E_CUDA, "cudaMallocHost failed");
+    memcpy(h, bytes.data(), bytes.size());
+    cudaError_t e = cudaMemcpyAsync(dst, h, bytes.size(), cudaMemcpyHostToDevice, st);
+    p->ring.release(idx, st);
+    if (e != cudaSuccess) return cuda_err(e, "plan upload");
+    return SMLM_OK;
+}
+
+template <typename T> void append(std::vector<uint8_t> &v, const std::vector<T> &x) {
+    const uint8_t *s = reinterpret_cast<const uint8_t *>(x.data());
+    v.insert(v.end(), s, s + x.size() * sizeof(T));
+}
+
+}  // namespace
+
+// ==========================================================================================
+// C ABI
+// ==========================================================================================
+extern "C" {
+
+const char *smlm_status_string(int s) {
+    switch (s) {
+        case SMLM_OK: return "SMLM_OK";
+        case SMLM_E_INVALID: return "SMLM_E_INVALID";
+        case SMLM_E_SHAPE: return "SMLM_E_SHAPE";
+        case SMLM_E_SLOT: return "SMLM_E_SLOT";
+        case SMLM_E_CAPACITY: return "SMLM_E_CAPACITY";
+        case SMLM_E_CUDA: return "SMLM_E_CUDA";
+        case SMLM_E_UNSUPPORTED: return "SMLM_E_UNSUPPORTED";
+        case SMLM_E_WORKSPACE: return "SMLM_E_WORKSPACE";
+    }
+    return "SMLM_E_UNKNOWN";
+}
+
+const char *smlm_last_error(void) { return g_last_error.c_str(); }
+
+uint64_t smlm_launch_count(void) { return g_launches.load(); }
+
+int smlm_profile_enable(int on) {
+    std::lock_guard<std::mutex> lk(g_prof.mu);
+    g_prof.on = on != 0;
+    return SMLM_OK;
+}
+
+int smlm_profile_read(int kind, double *total_ms, int *count) {
+    std::lock_guard<std::mutex> lk(g_prof.mu);
+    double tot = 0;
+    int n = 0;
+    std::vector<Profiler::Rec> keep;
+    for (auto &r : g_prof.recs) {
+        if (r.kind != kind) { keep.push_back(r); continue; }
+        cudaEventSynchronize(r.b);
+        float ms = 0;
+        cudaEventElapsedTime(&ms, r.a, r.b);
+        tot += ms;
+        ++n;
+        g_prof.pool.push_back(r.a);
+        g_prof.pool.push_back(r.b);
+    }
+    g_prof.recs.swap(keep);
+    if (total_ms) *total_ms = tot;
+    if (count) *count = n;
+    return SMLM_OK;
+}
+
+int smlm_pool_create(int device, int in_features, int out_features, int rank, int capacity, int dtype,
+                     smlm_pool *out) {
+    if (!out) return set_err(SMLM_E_INVALID, "out is NULL");
+    *out = nullptr;
+    if (capacity < 1) return set_err(SMLM_E_INVALID, "capacity must be >= 1");
+    if (in_features < 1 || out_features < 1 || rank < 1) return set_err(SMLM_E_INVALID, "bad shape");
+    if (dtype == SMLM_BF16) {
+        if (!(rank == 8 || rank == 16 || rank == 32 || rank == 64))
+            return set_err(SMLM_E_UNSUPPORTED, "bf16 path supports rank in {8,16,32,64}");
+        if (in_features % 64 || out_features % 64)
+            return set_err(SMLM_E_UNSUPPORTED, "bf16 path needs in/out multiples of 64");
+    } else if (dtype == SMLM_FP32) {
+        if (rank > 64) return set_err(SMLM_E_UNSUPPORTED, "fp32 path supports rank <= 64");
+    } else {
+        return set_err(SMLM_E_INVALID, "unknown dtype");
+    }
+    int ndev = 0;
+    cudaError_t e = cudaGetDeviceCount(&ndev);
+    if (e != cudaSuccess || device < 0 || device >= ndev)
+        return set_err(SMLM_E_UNSUPPORTED, "no such CUDA device (there is no CPU fallback)");
+    cudaDeviceProp prop;
+    CK(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10 || prop.minor != 0)
+        return set_err(SMLM_E_UNSUPPORTED, "device is not sm_100 (B200); this library is sm_100a-only");
+    DeviceGuard dg(device);
+    auto *p = new smlm_pool_s();
+    p->device = device;
+    p->in = in_features;
+    p->out = out_features;
+    p->r = rank;
+    p->r_pad = rank <= 16 ? 16 : (rank <= 32 ? 32 : 64);
+    p->cap = capacity;
+    p->dtype = dtype;
+    p->num_sms = prop.multiProcessorCount;
+    p->slots.resize(capacity);
+    p->ok.assign(capacity, 0);
+    p->scales.assign(capacity, 0.f);
+    e = cudaMalloc(&p->d_slots, sizeof(SlotDev) * capacity);
+    if (e != cudaSuccess) {
+        delete p;
+        return cuda_err(e, "cudaMalloc(slot table)");
+    }
+    e = cudaMemset(p->d_slots, 0, sizeof(SlotDev) * capacity);
+    if (e != cudaSuccess) {
+        cudaFree(p->d_slots);
+        delete p;
+        return cuda_err(e, "cudaMemset(slot table)");
+    }
+    *out = p;
+    return SMLM_OK;
+}
+
+int smlm_pool_destroy(smlm_pool p) {
+    if (!p) return SMLM_OK;
+    {
+        DeviceGuard dg(p->device);
+        cudaDeviceSynchronize();
+        if (p->d_slots) cudaFree(p->d_slots);
+    }
+    delete p;
+    return SMLM_OK;
+}
+
+int smlm_pool_set_option(smlm_pool p, int option, int value) {
+    if (!p) return set_err(SMLM_E_INVALID, "pool is NULL");
+    if (option == SMLM_OPT_L_LONG) {
+        if (value < 1) return set_err(SMLM_E_INVALID, "L_long must be >= 1");
+        p->l_long = value;
+        return SMLM_OK;
+    }
+    return set_err(SMLM_E_INVALID, "unknown option");
+}
+
+static int upload_slot(smlm_pool p, int slot, cudaStream_t st) {
+    SlotDev d;
+    memset(&d, 0, sizeof(d));
+    const SlotHost &h = p->slots[slot];
+    if (h.used) {
+        d.A = h.A;
+        d.B = h.B;
+        d.dA = h.dA;
+        d.dB = h.dB;
+        d.scale = h.scale;
+        d.used = 1;
+        if (p->dtype == SMLM_BF16) {
+            const int rb = p->r_pad * 2;
+            int rc;
+            if ((rc = make_map(&d.tmA, h.A, p->in, p->r, 64, p->r_pad, CU_TENSOR_MAP_SWIZZLE_128B))) return rc;
+            if ((rc = make_map(&d.tmBn, h.B, p->r, p->out, p->r_pad, 256, swizzle_for(rb)))) return rc;
+            if ((rc = make_map(&d.tmBk, h.B, p->r, p->out, p->r_pad, 64, swizzle_for(rb)))) return rc;
+        }
+    }
+    std::vector<uint8_t> bytes(sizeof(SlotDev));
+    memcpy(bytes.data(), &d, sizeof(SlotDev));
+    return stage_upload(p, bytes, p->d_slots + slot, st);
+}
+
+int smlm_adapter_register(smlm_pool p, const void *A, const void *B, float scale, void *stream, int *slot_out) {
+    if (!p || !A || !B || !slot_out) return set_err(SMLM_E_INVALID, "NULL argument");
+    if (!(scale > 0.f) || !isfinite(scale)) return set_err(SMLM_E_INVALID, "scale must be finite and > 0");
+    if (p->dtype == SMLM_BF16 && (((uintptr_t)A & 15) || ((uintptr_t)B & 15)))
+        return set_err(SMLM_E_INVALID, "A/B must be 16-byte aligned");
+    int slot = -1;
+    for (int i = 0; i < p->cap; ++i)
+        if (!p->slots[i].used) { slot = i; break; }
+    if (slot < 0) return set_err(SMLM_E_CAPACITY, "adapter pool is full");
+    DeviceGuard dg(p->device);
+    int rc = check_sticky();
+    if (rc) return rc;
+    SlotHost &h = p->slots[slot];
+    h.used = true;
+    h.A = A;
+    h.B = B;
+    h.scale = scale;
+    h.dA = h.dB = nullptr;
+    rc = upload_slot(p, slot, (cudaStream_t)stream);
+    if (rc) {
+        h = SlotHost();
+        return rc;
+    }
+    p->ok[slot] = 1;
+    p->scales[slot] = scale;
+    *slot_out = slot;
+    return SMLM_OK;
+}
+
+int smlm_adapter_set_grad(smlm_pool p, int slot, float *dA, float *dB) {
+    if (!p) return set_err(SMLM_E_INVALID, "pool is NULL");
+    if (slot < 0 || slot >= p->cap || !p->slots[slot].used) return set_err(SMLM_E_SLOT, "slot not registered");
+    p->slots[slot].dA = dA;
+    p->slots[slot].dB = dB;
+    return SMLM_OK;
+}
+
+int smlm_adapter_unregister(smlm_pool p, int slot, void *stream) {
+    if (!p) return set_err(SMLM_E_INVALID, "pool is NULL");
+    if (slot < 0 || slot >= p->cap || !p->slots[slot].used) return set_err(SMLM_E_SLOT, "slot not registered");
+    DeviceGuard dg(p->device);
+    p->slots[slot] = SlotHost();
+    p->ok[slot] = 0;
+    p->scales[slot] = 0.f;
+    return upload_slot(p, slot, (cudaStream_t)stream);
+}
+
+int smlm_plan(const smlm_batch *batch, int capacity, const uint8_t *slot_registered, int l_long, int backward,
+              int32_t *items, int max_items, int *n_items) {
+    if (!n_items) return set_err(SMLM_E_INVALID, "n_items is NULL");
+    Plan plan;
+    std::string msg;
+    int rc = build_plan(batch, capacity, slot_registered, nullptr, l_long, backward != 0, plan, msg);
+    if (rc) return set_err(rc, msg);
+    std::vector<int32_t> rec;
+    export_plan(plan, batch, backward != 0, rec);
+    int n = (int)(rec.size() / 6);
+    *n_items = n;
+    if (n > max_items || (n > 0 && !items)) return set_err(SMLM_E_WORKSPACE, "items buffer too small");
+    if (n) memcpy(items, rec.data(), rec.size() * sizeof(int32_t));
+    return SMLM_OK;
+}
+
+int smlm_plan_export(smlm_pool p, const smlm_batch *batch, int backward, int32_t *items, int max_items,
+                     int *n_items) {
+    if (!p) return set_err(SMLM_E_INVALID, "pool is NULL");
+    return smlm_plan(batch, p->cap, p->ok.data(), p->l_long, backward, items, max_items, n_items);
+}
+
+size_t smlm_workspace_size(smlm_pool p, const smlm_batch *batch, int backward) {
+    if (!p) return 0;
+    Plan plan;
+    if (plan_for(p, batch, backward != 0, plan) != SMLM_OK) return 0;
+    bool need_vf = p->dtype == SMLM_FP32 || backward;  // conservative: bwd may recompute V
+    return layout_for(p, batch, plan, backward != 0, need_vf).total;
+}
+
+int smlm_forward(smlm_pool p, const smlm_batch *b, const void *X, const void *W, void *Y, void *V_save, void *ws,
+                 size_t ws_bytes, void *stream) {
+    if (!p || !b) return set_err(SMLM_E_INVALID, "NULL pool/batch");
+    Plan plan;
+    int rc = plan_for(p, b, false, plan);
+    if (rc) return rc;
+    if (b->S == 0 || b->G == 0) return SMLM_OK;
+    if (!X || !Y) return set_err(SMLM_E_INVALID, "X and Y must be non-NULL");
+    const bool need_vf = p->dtype == SMLM_FP32;
+    WsLayout L = layout_for(p, b, plan, false, need_vf);
+    if (!ws || ws_bytes < L.total) return set_err(SMLM_E_WORKSPACE, "workspace too small");
+    DeviceGuard dg(p->device);
+    if ((rc = check_sticky())) return rc;
+    cudaStream_t st = (cudaStream_t)stream;
+    uint8_t *wsb = reinterpret_cast<uint8_t *>(ws);
+
+    if (p->dtype == SMLM_FP32) {
+        std::vector<uint8_t> bytes;
+        append(bytes, plan.long_tiles);
+        if ((rc = stage_upload(p, bytes, wsb + L.plan_off, st))) return rc;
+        const DevTile *tiles = reinterpret_cast<const DevTile *>(wsb + L.plan_off);
+        const int nt = (int)plan.long_tiles.size();
+        float *Vf = reinterpret_cast<float *>(wsb + L.vf_off);
+        CKL(launch_rows_shrink<float>(tiles, nt, p->d_slots, (const float *)X, p->in, p->r, Vf, (float *)V_save, 1,
+                                      st), 1);
+        CKL(launch_f32_fwd(tiles, nt, p->d_slots, (const float *)X, (const float *)W, (float *)Y, Vf, p->in, p->out,
+                           p->r, st), 1);
+        return SMLM_OK;
+    }
+
+    // ---------------- bf16 tensor-core path ----------------
+    const bool has_w = W != nullptr;
+    std::vector<DevTile> tiles;
+    tiles.reserve(plan.long_tiles.size() + plan.short_tiles.size());
+    for (auto &t : plan.long_tiles)
+        if (has_w || (t.flags & kTileLora)) tiles.push_back(t);
+    for (auto &t : plan.short_tiles)
+        if (has_w || t.nblk > 0) tiles.push_back(t);
+    std::vector<uint8_t> bytes;
+    append(bytes, tiles);
+    const size_t blk_off = bytes.size();
+    append(bytes, plan.blocks);
+    const size_t srow_off = bytes.size();
+    append(bytes, plan.short_rows);
+    if ((rc = stage_upload(p, bytes, wsb + L.plan_off, st))) return rc;
+    const DevTile *d_tiles = reinterpret_cast<const DevTile *>(wsb + L.plan_off);
+    const DevBlock *d_blocks = reinterpret_cast<const DevBlock *>(wsb + L.plan_off + blk_off);
+    const DevShortRow *d_srows = reinterpret_cast<const DevShortRow *>(wsb + L.plan_off + srow_off);
+    __nv_bfloat16 *Vbd = reinterpret_cast<__nv_bfloat16 *>(wsb + L.vbd_off);
+
+    if (!plan.blocks.empty()) {
+        ProfScope ps(2, st);
+        CKL(launch_shrink_short((const __nv_bfloat16 *)X, p->d_slots, d_blocks, d_srows, (int)plan.blocks.size(),
+                                p->in, p->r, p->r_pad, Vbd, (__nv_bfloat16 *)V_save, st), 1);
+    }
+    if (tiles.empty()) return SMLM_OK;
+    GemmArgs a;
+    memset(&a, 0, sizeof(a));
+    if ((rc = make_map(&a.tmA, X, p->in, b->S, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B))) return rc;
+    if (has_w && (rc = make_map(&a.tmB, W, p->in, p->out, 64, 256, CU_TENSOR_MAP_SWIZZLE_128B))) return rc;
+    if (!plan.blocks.empty() &&
+        (rc = make_map(&a.tmV, Vbd, p->r_pad, plan.blocks.size() * 128, p->r_pad, 128, swizzle_for(p->r_pad * 2))))
+        return rc;
+    a.slots = p->d_slots;
+    a.tiles = d_tiles;
+    a.blocks = d_blocks;
+    a.n_tiles = (int)tiles.size();
+    a.K = p->in;
+    a.N = p->out;
+    a.n_ntiles = (p->out + kBN - 1) / kBN;
+    a.r = p->r;
+    a.r_pad = p->r_pad;
+    a.stages = gemm_stages(p->r_pad, nullptr);
+    a.has_w = has_w ? 1 : 0;
+    a.Y = Y;
+    a.Vsave = V_save;
+    a.Usave = nullptr;
+    a.S = b->S;
+    {
+        ProfScope ps(0, st);
+        CKL(launch_gemm(a, false, p->num_sms, st), 1);
+    }
+    return SMLM_OK;
+}
+
+int smlm_backward(smlm_pool p, const smlm_batch *b, const void *X, const void *W, const void *dY, const void *V_save,
+                  void *dX, int accumulate, void *ws, size_t ws_bytes, void *stream) {
+    if (!p || !b) return set_err(SMLM_E_INVALID, "NULL pool/batch");
+    Plan plan;
+    int rc = plan_for(p, b, true, plan);
+    if (rc) return rc;
+    if (b->S == 0 || b->G == 0 || plan.bwd_tiles.empty()) return SMLM_OK;
+    if (!X || !dY) return set_err(SMLM_E_INVALID, "X and dY must be non-NULL");
+    if (dX && !W) return set_err(SMLM_E_INVALID, "W is required when dX is requested");
+    WsLayout L = layout_for(p, b, plan, true, true);
+    if (!ws || ws_bytes < L.total) return set_err(SMLM_E_WORKSPACE, "workspace too small");
+    DeviceGuard dg(p->device);
+    if ((rc = check_sticky())) return rc;
+    cudaStream_t st = (cudaStream_t)stream;
+    uint8_t *wsb = reinterpret_cast<uint8_t *>(ws);
+
+    // grad groups with the current grad bindings (masking: NULL => no dA/dB for that slot)
+    std::vector<uint8_t> gbytes(plan.groups.size() * grad_group_bytes());
+    int n_grad = 0;
+    for (auto &g : plan.groups) {
+        const SlotHost &h = p->slots[g.slot];
+        if (!h.dA && !h.dB) continue;
+        fill_grad_group(gbytes.data() + n_grad * grad_group_bytes(), g.slot, g.tile_begin, g.n_tiles, h.dA, h.dB);
+        ++n_grad;
+    }
+    gbytes.resize(n_grad * grad_group_bytes());
+    std::vector<uint8_t> bytes;
+    append(bytes, plan.bwd_tiles);
+    const size_t grp_off = bytes.size();
+    bytes.insert(bytes.end(), gbytes.begin(), gbytes.end());
+    if ((rc = stage_upload(p, bytes, wsb + L.plan_off, st))) return rc;
+    const DevTile *d_tiles = reinterpret_cast<const DevTile *>(wsb + L.plan_off);
+    const void *d_groups = wsb + L.plan_off + grp_off;
+    const int nt = (int)plan.bwd_tiles.size();
+    float *Uf = reinterpret_cast<float *>(wsb + L.u_off);
+    float *Vf = reinterpret_cast<float *>(wsb + L.vf_off);
+
+    if (p->dtype == SMLM_FP32) {
+        CKL(launch_rows_u<float>(d_tiles, nt, p->d_slots, (const float *)dY, p->out, p->r, Uf, st), 1);
+        if (dX)
+            CKL(launch_f32_dx(d_tiles, nt, p->d_slots, (const float *)dY, (const float *)W, (float *)dX, Uf, p->in,
+                              p->out, p->r, st), 1);
+        if (n_grad) {
+            const float *V = (const float *)V_save;
+            if (!V) {
+                CKL(launch_rows_shrink<float>(d_tiles, nt, p->d_slots, (const float *)X, p->in, p->r, Vf, nullptr,
+                                              0, st), 1);
+                V = Vf;
+            }
+            CKL((launch_dadb<float, float>(d_tiles, d_groups, n_grad, (const float *)X, (const float *)dY, Uf, V,
+                                           p->in, p->out, p->r, accumulate, st)), 2);
+        }
+        return SMLM_OK;
+    }
+
+    // ---------------- bf16 path ----------------
+    if (dX) {
+        GemmArgs a;
+        memset(&a, 0, sizeof(a));
+        if ((rc = make_map(&a.tmA, dY, p->out, b->S, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B))) return rc;
+        if ((rc = make_map(&a.tmB, W, p->in, p->out, 64, 64, CU_TENSOR_MAP_SWIZZLE_128B))) return rc;
+        a.slots = p->d_slots;
+        a.tiles = d_tiles;
+        a.blocks = nullptr;
+        a.n_tiles = nt;
+        a.K = p->out;
+        a.N = p->in;
+        a.n_ntiles = (p->in + kBN - 1) / kBN;
+        a.r = p->r;
+        a.r_pad = p->r_pad;
+        a.stages = gemm_stages(p->r_pad, nullptr);
+        a.has_w = 1;
+        a.Y = dX;
+        a.Vsave = nullptr;
+        a.Usave = Uf;
+        a.S = b->S;
+        ProfScope ps(1, st);
+        CKL(launch_gemm(a, true, p->num_sms, st), 1);
+    } else if (n_grad) {
+        CKL(launch_rows_u<__nv_bfloat16>(d_tiles, nt, p->d_slots, (const __nv_bfloat16 *)dY, p->out, p->r, Uf, st),
+            1);
+    }
+    if (n_grad) {
+        ProfScope ps(3, st);
+        if (V_save) {
+            CKL((launch_dadb<__nv_bfloat16, __nv_bfloat16>(d_tiles, d_groups, n_grad, (const __nv_bfloat16 *)X,
+                                                           (const __nv_bfloat16 *)dY, Uf,
+                                                           (const __nv_bfloat16 *)V_save, p->in, p->out, p->r,
+                                                           accumulate, st)), 2);
+        } else {
+            CKL(launch_rows_shrink<__nv_bfloat16>(d_tiles, nt, p->d_slots, (const __nv_bfloat16 *)X, p->in, p->r, Vf,
+                                                  nullptr, 0, st), 1);
+            CKL((launch_dadb<__nv_bfloat16, float>(d_tiles, d_groups, n_grad, (const __nv_bfloat16 *)X,
+                                                   (const __nv_bfloat16 *)dY, Uf, Vf, p->in, p->out, p->r,
+                                                   accumulate, st)), 2);
+        }
+    }
+    return SMLM_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,423 @@
+// kernels_tc.cu -- the fused SMLM GEMM on 5th-generation tensor cores (tcgen05 + TMEM + TMA).
+//
+// One persistent, warp-specialised kernel serves both directions:
+//   forward  (a2/a3): Y[tile, n-tile] = X_tile W^T  +  (s V) B_a^T,   V = X_tile A_a^T on-chip
+//   backward (a4)   : dX[tile, n-tile] = dY_tile W  +  (s U) A_a,     U = dY_tile B_a  on-chip
+// PAPER.md P:379-384 (§3.3): all input-LoRA pairs of one linear layer in a single kernel call,
+// per-request scale applied "during the forward pass"; P:415 / P:696: the LoRA backward, which
+// the paper left to per-linear autograd calls, is fused here.
+//
+// Work item = (128-row tile, 256-column n-tile).  Long tiles (one segment, one adapter) compute
+// the rank-r intermediate with an extra N=r_pad MMA that reuses the X (dY) tile already staged
+// in shared memory; the epilogue warps scale it by s, round to bf16 into shared memory, and the
+// MMA warp folds it in as one more K-block of depth r (the rank-r intermediate never leaves the
+// SM).  Short tiles (rows of many decode/short segments) fold each distinct adapter
+// in as a K=r_pad block whose A operand is the block-diagonal s*V prepared by the shrink kernel.
+//
+// Warp roles (256 threads): warp 0 TMA producer, warp 1 MMA issuer, warp 2 TMEM allocator,
+// warps 4..7 epilogue (TMEM lanes 32*(warp%4) ...).  TMEM: accumulator columns [0,256),
+// rank-r accumulator columns [256, 256+r_pad).
+#include <cuda_runtime.h>
+
+#include "device_types.h"
+#include "sm100.cuh"
+
+namespace smlm {
+using namespace sm100;
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kGroupM = 8;  // m-tiles per raster group (L2 reuse of W n-tiles and X m-tiles)
+constexpr uint32_t kABytes = 128 * 128;   // X/dY tile: 128 rows x 64 bf16
+constexpr uint32_t kBBytes = 256 * 128;   // W tile: 256 x 64 bf16
+
+__device__ __forceinline__ void decode_work(int w, int n_tiles, int n_nt, int &ti, int &nt) {
+    const int gsz = kGroupM * n_nt;
+    const int g = w / gsz;
+    const int first = g * kGroupM;
+    const int gm = min(kGroupM, n_tiles - first);
+    const int local = w - g * gsz;
+    ti = first + local % gm;
+    nt = local / gm;
+}
+
+template <bool BWD, int RP>
+__global__ void __launch_bounds__(kThreads, 1) smlm_gemm_kernel(const __grid_constant__ GemmArgs args) {
+    extern __shared__ uint8_t smem_raw[];
+    const uint32_t raw = smem_u32(smem_raw);
+    const uint32_t base = (raw + 1023u) & ~1023u;
+    uint8_t *base_ptr = smem_raw + (base - raw);
+
+    constexpr uint32_t RB = RP * 2;             // bytes per row of an r_pad-wide bf16 tile
+    constexpr uint32_t kAaBytes = RP * 128;     // shrink/U operand per stage
+    constexpr uint32_t kStage = kABytes + kBBytes + kAaBytes;
+    constexpr uint32_t kSwR = RB >= 128 ? kSw128 : (RB == 64 ? kSw64 : kSw32);
+    const int stages = args.stages;
+    const uint32_t sv_addr = base + stages * kStage;
+    const uint32_t bar = sv_addr + 128 * RB;
+    auto full_bar = [&](int s) { return bar + 8u * s; };
+    auto empty_bar = [&](int s) { return bar + 8u * (stages + s); };
+    const uint32_t acc_full = bar + 16u * stages;
+    const uint32_t acc_empty = acc_full + 8;
+    const uint32_t v_full = acc_full + 16;
+    const uint32_t sv_ready = acc_full + 24;
+    const uint32_t tmem_slot = acc_full + 32;
+    auto a_addr = [&](int s) { return base + s * kStage; };
+    auto b_addr = [&](int s) { return base + s * kStage + kABytes; };
+    auto aa_addr = [&](int s) { return base + s * kStage + kABytes + kBBytes; };
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < stages; ++s) {
+            mbar_init(full_bar(s), 1);
+            mbar_init(empty_bar(s), 1);
+        }
+        mbar_init(acc_full, 1);
+        mbar_init(acc_empty, 128);
+        mbar_init(v_full, 1);
+        mbar_init(sv_ready, 128);
+        fence_mbar_init();
+        tma_prefetch_desc(&args.tmA);
+        tma_prefetch_desc(&args.tmB);
+        if (!BWD) tma_prefetch_desc(&args.tmV);
+    }
+    if (warp == 2) tmem_alloc(tmem_slot, 512);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *reinterpret_cast<volatile uint32_t *>(base_ptr + (tmem_slot - base));
+    const uint32_t acc_tmem = tmem_base;
+    const uint32_t v_tmem = tmem_base + 256;
+
+    const int total = args.n_tiles * args.n_ntiles;
+    const int nkb = args.K / kBK;
+
+    if (warp == 0) {
+        // ============================ TMA producer ============================
+        int stage = 0;
+        uint32_t phase = 0;
+        auto advance = [&]() {
+            if (++stage == stages) { stage = 0; phase ^= 1; }
+        };
+        for (int w = blockIdx.x; w < total; w += gridDim.x) {
+            int ti, nt;
+            decode_work(w, args.n_tiles, args.n_ntiles, ti, nt);
+            const DevTile t = args.tiles[ti];
+            const int n0 = nt * kBN;
+            const bool is_short = (t.flags & kTileShort) != 0;
+            const bool lora = (t.flags & kTileLora) != 0;
+            const SlotDev *sd = lora ? args.slots + t.slot : nullptr;
+            if (!is_short || args.has_w) {
+                for (int kb = 0; kb < nkb; ++kb) {
+                    mbar_wait(empty_bar(stage), phase ^ 1);
+                    if (lane == 0) {
+                        uint32_t bytes = kABytes;
+                        if (args.has_w) {
+                            if (BWD) {
+                                int nb = 0;
+                                for (int i = 0; i < 4; ++i) nb += (n0 + 64 * i < args.N);
+                                bytes += 8192u * nb;
+                            } else {
+                                bytes += kBBytes;
+                            }
+                        }
+                        if (lora) bytes += kAaBytes;
+                        mbar_expect_tx(full_bar(stage), bytes);
+                        tma_load_2d(a_addr(stage), &args.tmA, full_bar(stage), kb * kBK, t.row0);
+                        if (args.has_w) {
+                            if (BWD) {
+                                for (int i = 0; i < 4; ++i)
+                                    if (n0 + 64 * i < args.N)
+                                        tma_load_2d(b_addr(stage) + 8192u * i, &args.tmB, full_bar(stage),
+                                                    n0 + 64 * i, kb * kBK);
+                            } else {
+                                tma_load_2d(b_addr(stage), &args.tmB, full_bar(stage), kb * kBK, n0);
+                            }
+                        }
+                        if (lora) {
+                            if (BWD)  // B_a rows [kb*64, +64) x r_pad  (MN-major U operand)
+                                tma_load_2d(aa_addr(stage), &sd->tmBk, full_bar(stage), 0, kb * kBK);
+                            else      // A_a [r_pad rows] x 64 k      (K-major shrink operand)
+                                tma_load_2d(aa_addr(stage), &sd->tmA, full_bar(stage), kb * kBK, 0);
+                        }
+                    }
+                    __syncwarp();
+                    advance();
+                }
+            }
+            if (lora) {
+                mbar_wait(empty_bar(stage), phase ^ 1);
+                if (lane == 0) {
+                    mbar_expect_tx(full_bar(stage), 256u * RB);
+                    if (BWD) {  // A_a [r_pad rows, n0 + 64 i ...] MN-major expand operand
+                        for (int i = 0; i < 4; ++i)
+                            tma_load_2d(b_addr(stage) + (uint32_t)RP * 128u * i, &sd->tmA, full_bar(stage),
+                                        n0 + 64 * i, 0);
+                    } else {    // B_a [n0.., r_pad] K-major expand operand
+                        tma_load_2d(b_addr(stage), &sd->tmBn, full_bar(stage), 0, n0);
+                    }
+                }
+                __syncwarp();
+                advance();
+            } else if (is_short) {
+                for (int b = 0; b < t.nblk; ++b) {
+                    const DevBlock blk = args.blocks[t.blk0 + b];
+                    const SlotDev *bs = args.slots + blk.slot;
+                    mbar_wait(empty_bar(stage), phase ^ 1);
+                    if (lane == 0) {
+                        mbar_expect_tx(full_bar(stage), 128u * RB + 256u * RB);
+                        tma_load_2d(a_addr(stage), &args.tmV, full_bar(stage), 0, (t.blk0 + b) * 128);
+                        tma_load_2d(b_addr(stage), &bs->tmBn, full_bar(stage), 0, n0);
+                    }
+                    __syncwarp();
+                    advance();
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ============================ MMA issuer ============================
+        int stage = 0;
+        uint32_t phase = 0;
+        auto advance = [&]() {
+            if (++stage == stages) { stage = 0; phase ^= 1; }
+        };
+        constexpr uint32_t idesc_main = idesc_bf16(128, kBN, 0, BWD ? 1 : 0);
+        constexpr uint32_t idesc_v = idesc_bf16(128, RP, 0, BWD ? 1 : 0);
+        uint32_t it = 0, lora_it = 0;
+        for (int w = blockIdx.x; w < total; w += gridDim.x) {
+            int ti, nt;
+            decode_work(w, args.n_tiles, args.n_ntiles, ti, nt);
+            const DevTile t = args.tiles[ti];
+            const bool is_short = (t.flags & kTileShort) != 0;
+            const bool lora = (t.flags & kTileLora) != 0;
+            mbar_wait(acc_empty, (it & 1) ^ 1);
+            tc_fence_after();
+            uint32_t acc_on = 0;  // 1 once the accumulator holds data
+            if (!is_short || args.has_w) {
+                for (int kb = 0; kb < nkb; ++kb) {
+                    mbar_wait(full_bar(stage), phase);
+                    tc_fence_after();
+                    if (lane == 0) {
+                        const uint32_t ab = a_addr(stage), bb = b_addr(stage), vb = aa_addr(stage);
+#pragma unroll
+                        for (int k = 0; k < kBK / 16; ++k) {
+                            const uint64_t ad = smem_desc(ab + 32u * k, 16, 1024, kSw128);
+                            if (args.has_w) {
+                                const uint64_t bd = BWD ? smem_desc(bb + 2048u * k, 8192, 1024, kSw128)
+                                                        : smem_desc(bb + 32u * k, 16, 1024, kSw128);
+                                mma_bf16(acc_tmem, ad, bd, idesc_main, (kb | k) != 0);
+                            }
+                            if (lora) {
+                                const uint64_t vd = BWD ? smem_desc(vb + 16u * RB * k, 64u * RB, 8u * RB, kSwR)
+                                                        : smem_desc(vb + 32u * k, 16, 1024, kSw128);
+                                mma_bf16(v_tmem, ad, vd, idesc_v, (kb | k) != 0);
+                            }
+                        }
+                        mma_commit(empty_bar(stage));
+                    }
+                    __syncwarp();
+                    advance();
+                }
+                acc_on = args.has_w ? 1u : 0u;
+            }
+            if (lora) {
+                if (lane == 0) mma_commit(v_full);
+                __syncwarp();
+                mbar_wait(full_bar(stage), phase);
+                mbar_wait(sv_ready, lora_it & 1);
+                tc_fence_after();
+                if (lane == 0) {
+                    const uint32_t bb = b_addr(stage);
+#pragma unroll
+                    for (int kk = 0; kk < RP / 16; ++kk) {
+                        const uint64_t ad = smem_desc(sv_addr + 32u * kk, 16, 8u * RB, kSwR);
+                        const uint64_t bd = BWD ? smem_desc(bb + 2048u * kk, (uint32_t)RP * 128u, 1024, kSw128)
+                                                : smem_desc(bb + 32u * kk, 16, 8u * RB, kSwR);
+                        mma_bf16(acc_tmem, ad, bd, idesc_main, acc_on | (kk != 0));
+                    }
+                    mma_commit(empty_bar(stage));
+                }
+                __syncwarp();
+                advance();
+                ++lora_it;
+            } else if (is_short) {
+                for (int b = 0; b < t.nblk; ++b) {
+                    mbar_wait(full_bar(stage), phase);
+                    tc_fence_after();
+                    if (lane == 0) {
+                        const uint32_t ab = a_addr(stage), bb = b_addr(stage);
+#pragma unroll
+                        for (int kk = 0; kk < RP / 16; ++kk) {
+                            const uint64_t ad = smem_desc(ab + 32u * kk, 16, 8u * RB, kSwR);
+                            const uint64_t bd = smem_desc(bb + 32u * kk, 16, 8u * RB, kSwR);
+                            mma_bf16(acc_tmem, ad, bd, idesc_main, acc_on | (uint32_t)(b | kk));
+                        }
+                        mma_commit(empty_bar(stage));
+                    }
+                    __syncwarp();
+                    advance();
+                }
+            }
+            if (lane == 0) mma_commit(acc_full);
+            __syncwarp();
+            ++it;
+        }
+    } else if (warp >= 4) {
+        // ============================ epilogue ============================
+        const int q = warp - 4;
+        const int m = q * 32 + lane;
+        const uint32_t lane_base = (uint32_t)(q * 32) << 16;
+        uint32_t it = 0, lora_it = 0;
+        __nv_bfloat16 *Y = reinterpret_cast<__nv_bfloat16 *>(args.Y);
+        for (int w = blockIdx.x; w < total; w += gridDim.x) {
+            int ti, nt;
+            decode_work(w, args.n_tiles, args.n_ntiles, ti, nt);
+            const DevTile t = args.tiles[ti];
+            const int n0 = nt * kBN;
+            const bool lora = (t.flags & kTileLora) != 0;
+            const bool row_ok = m < t.rows;
+            const int row = t.row0 + m;
+            if (lora) {
+                mbar_wait(v_full, lora_it & 1);
+                tc_fence_after();
+                uint32_t v[RP];
+#pragma unroll
+                for (int c = 0; c < RP; c += 16) {
+                    uint32_t tmp[16];
+                    tmem_ld16(v_tmem + lane_base + c, tmp);
+                    tmem_wait_ld();
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) v[c + j] = tmp[j];
+                }
+                if (nt == 0 && row_ok) {
+                    if (BWD) {
+                        if (args.Usave) {
+                            float *u = args.Usave + (size_t)row * args.r;
+#pragma unroll
+                            for (int j = 0; j < RP; ++j)
+                                if (j < args.r) u[j] = __uint_as_float(v[j]);
+                        }
+                    } else if ((t.flags & kTileFT) && args.Vsave) {
+                        __nv_bfloat16 *vs = reinterpret_cast<__nv_bfloat16 *>(args.Vsave) + (size_t)row * args.r;
+#pragma unroll
+                        for (int j = 0; j < RP; ++j)
+                            if (j < args.r) vs[j] = __float2bfloat16_rn(__uint_as_float(v[j]));
+                    }
+                }
+                const float s = t.scale;
+                uint8_t *sv = base_ptr + (sv_addr - base);
+#pragma unroll
+                for (int c = 0; c < RP / 8; ++c) {
+                    uint4 pk;
+                    pk.x = pack_bf16x2(s * __uint_as_float(v[8 * c + 0]), s * __uint_as_float(v[8 * c + 1]));
+                    pk.y = pack_bf16x2(s * __uint_as_float(v[8 * c + 2]), s * __uint_as_float(v[8 * c + 3]));
+                    pk.z = pack_bf16x2(s * __uint_as_float(v[8 * c + 4]), s * __uint_as_float(v[8 * c + 5]));
+                    pk.w = pack_bf16x2(s * __uint_as_float(v[8 * c + 6]), s * __uint_as_float(v[8 * c + 7]));
+                    *reinterpret_cast<uint4 *>(sv + swz((uint32_t)m * RB + 16u * c, RB)) = pk;
+                }
+                fence_proxy_async_smem();
+                tc_fence_before();
+                mbar_arrive(sv_ready);
+                ++lora_it;
+            }
+            mbar_wait(acc_full, it & 1);
+            tc_fence_after();
+#pragma unroll 1
+            for (int c = 0; c < kBN / 32; ++c) {
+                uint32_t r[32];
+                tmem_ld32(acc_tmem + lane_base + 32u * c, r);
+                tmem_wait_ld();
+                const int col = n0 + 32 * c;
+                if (row_ok && col < args.N) {
+                    uint4 *dst = reinterpret_cast<uint4 *>(Y + (size_t)row * args.N + col);
+                    if (!BWD && !args.has_w) {
+#pragma unroll
+                        for (int q4 = 0; q4 < 4; ++q4) {
+                            uint4 old = dst[q4];
+                            const __nv_bfloat162 *o2 = reinterpret_cast<const __nv_bfloat162 *>(&old);
+                            uint4 pk;
+                            uint32_t *pw = reinterpret_cast<uint32_t *>(&pk);
+#pragma unroll
+                            for (int e = 0; e < 4; ++e) {
+                                float2 f = __bfloat1622float2(o2[e]);
+                                pw[e] = pack_bf16x2(f.x + __uint_as_float(r[8 * q4 + 2 * e]),
+                                                    f.y + __uint_as_float(r[8 * q4 + 2 * e + 1]));
+                            }
+                            dst[q4] = pk;
+                        }
+                    } else {
+#pragma unroll
+                        for (int q4 = 0; q4 < 4; ++q4) {
+                            uint4 pk;
+                            pk.x = pack_bf16x2(__uint_as_float(r[8 * q4 + 0]), __uint_as_float(r[8 * q4 + 1]));
+                            pk.y = pack_bf16x2(__uint_as_float(r[8 * q4 + 2]), __uint_as_float(r[8 * q4 + 3]));
+                            pk.z = pack_bf16x2(__uint_as_float(r[8 * q4 + 4]), __uint_as_float(r[8 * q4 + 5]));
+                            pk.w = pack_bf16x2(__uint_as_float(r[8 * q4 + 6]), __uint_as_float(r[8 * q4 + 7]));
+                            dst[q4] = pk;
+                        }
+                    }
+                }
+            }
+            tc_fence_before();
+            mbar_arrive(acc_empty);
+            ++it;
+        }
+    }
+    __syncthreads();
+    if (warp == 2) {
+        tc_fence_after();
+        tmem_dealloc(tmem_base, 512);
+    }
+}
+
+template <bool BWD, int RP>
+int launch_impl(const GemmArgs &a, int num_sms, size_t smem, cudaStream_t st) {
+    auto kern = smlm_gemm_kernel<BWD, RP>;
+    static bool attr_done = false;
+    if (!attr_done) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
+        if (e != cudaSuccess) return (int)e;
+        attr_done = true;
+    }
+    const int total = a.n_tiles * a.n_ntiles;
+    const int grid = total < num_sms ? total : num_sms;
+    kern<<<grid, kThreads, smem, st>>>(a);
+    return (int)cudaGetLastError();
+}
+
+}  // namespace
+
+// Shared-memory bytes and pipeline depth for a given r_pad.
+int gemm_stages(int r_pad, size_t *smem_bytes) {
+    const size_t stage = kABytes + kBBytes + (size_t)r_pad * 128;
+    const size_t fixed = 1024 + (size_t)128 * r_pad * 2 + 256;
+    int stages = (int)((232448 - fixed) / stage);
+    if (stages > 6) stages = 6;
+    if (smem_bytes) *smem_bytes = fixed + stage * stages;
+    return stages;
+}
+
+int launch_gemm(const GemmArgs &a, bool bwd, int num_sms, cudaStream_t st) {
+    size_t smem = 0;
+    gemm_stages(a.r_pad, &smem);
+    if (a.n_tiles == 0 || a.n_ntiles == 0) return 0;
+    if (bwd) {
+        switch (a.r_pad) {
+            case 16: return launch_impl<true, 16>(a, num_sms, smem, st);
+            case 32: return launch_impl<true, 32>(a, num_sms, smem, st);
+            case 64: return launch_impl<true, 64>(a, num_sms, smem, st);
+        }
+    } else {
+        switch (a.r_pad) {
+            case 16: return launch_impl<false, 16>(a, num_sms, smem, st);
+            case 32: return launch_impl<false, 32>(a, num_sms, smem, st);
+            case 64: return launch_impl<false, 64>(a, num_sms, smem, st);
+        }
+    }
+    return (int)cudaErrorInvalidValue;
+}
+
+}  // namespace smlm

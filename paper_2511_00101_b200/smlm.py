@@ -1,0 +1,275 @@
+"""Thin ctypes binding of libsmlm.so (include/smlm.h).  Argument marshalling only: every step
+of the SMLM path runs in the library's CUDA kernels.  PyTorch supplies device memory and streams.
+
+Function names mirror the C ABI (smlm_pool_create, smlm_adapter_register, smlm_forward, ...);
+`Pool` is a convenience owner that keeps borrowed adapter tensors alive.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import Optional
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libsmlm.so")
+
+SMLM_OK, SMLM_E_INVALID, SMLM_E_SHAPE, SMLM_E_SLOT, SMLM_E_CAPACITY, SMLM_E_CUDA, SMLM_E_UNSUPPORTED, \
+    SMLM_E_WORKSPACE = range(8)
+SMLM_FINETUNE, SMLM_EVAL, SMLM_PREFILL, SMLM_DECODE = range(4)
+SMLM_BF16, SMLM_FP32 = 0, 1
+SMLM_OPT_L_LONG = 0
+PROF_FWD_GEMM, PROF_BWD_GEMM, PROF_SHRINK, PROF_DADB = range(4)
+
+EXPORTED = [
+    "smlm_pool_create", "smlm_pool_destroy", "smlm_pool_set_option", "smlm_adapter_register",
+    "smlm_adapter_set_grad", "smlm_adapter_unregister", "smlm_workspace_size", "smlm_forward",
+    "smlm_backward", "smlm_plan", "smlm_plan_export", "smlm_status_string", "smlm_last_error",
+    "smlm_launch_count", "smlm_profile_enable", "smlm_profile_read",
+]
+
+
+class SmlmError(RuntimeError):
+    def __init__(self, code: int, where: str, msg: str):
+        super().__init__(f"{where}: {_status_name(code)}: {msg}")
+        self.code = code
+
+
+class smlm_batch(ctypes.Structure):
+    _fields_ = [("S", ctypes.c_int), ("G", ctypes.c_int), ("seg_offsets", ctypes.c_void_p),
+                ("seg_slot", ctypes.c_void_p), ("seg_mode", ctypes.c_void_p), ("seg_scale", ctypes.c_void_p)]
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"libsmlm.so not built at {LIB_PATH}: run `python -m paper_2511_00101_b200.build` "
+                          "(there is no CPU fallback)")
+    lib = ctypes.CDLL(LIB_PATH)
+    P, I, Z = ctypes.c_void_p, ctypes.c_int, ctypes.c_size_t
+    BP = ctypes.POINTER(smlm_batch)
+    sig = {
+        "smlm_pool_create": ([I, I, I, I, I, I, ctypes.POINTER(P)], I),
+        "smlm_pool_destroy": ([P], I),
+        "smlm_pool_set_option": ([P, I, I], I),
+        "smlm_adapter_register": ([P, P, P, ctypes.c_float, P, ctypes.POINTER(I)], I),
+        "smlm_adapter_set_grad": ([P, I, P, P], I),
+        "smlm_adapter_unregister": ([P, I, P], I),
+        "smlm_workspace_size": ([P, BP, I], Z),
+        "smlm_forward": ([P, BP, P, P, P, P, P, Z, P], I),
+        "smlm_backward": ([P, BP, P, P, P, P, P, I, P, Z, P], I),
+        "smlm_plan": ([BP, I, P, I, I, P, I, ctypes.POINTER(I)], I),
+        "smlm_plan_export": ([P, BP, I, P, I, ctypes.POINTER(I)], I),
+        "smlm_status_string": ([I], ctypes.c_char_p),
+        "smlm_last_error": ([], ctypes.c_char_p),
+        "smlm_launch_count": ([], ctypes.c_uint64),
+        "smlm_profile_enable": ([I], I),
+        "smlm_profile_read": ([I, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(I)], I),
+    }
+    for name, (args, res) in sig.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = res
+    return lib
+
+
+_lib = _load()
+
+
+def _status_name(code: int) -> str:
+    return _lib.smlm_status_string(code).decode()
+
+
+def _check(code: int, where: str):
+    if code != SMLM_OK:
+        raise SmlmError(code, where, _lib.smlm_last_error().decode())
+
+
+def _ptr(t) -> Optional[int]:
+    if t is None:
+        return None
+    return t.data_ptr()
+
+
+def _stream(stream, device) -> int:
+    import torch
+    if stream is None:
+        stream = torch.cuda.current_stream(device)
+    return stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+
+
+class Batch:
+    """Host-side segment arrays kept alive for the duration of the calls."""
+
+    def __init__(self, offsets, slots, modes, seg_scale=None):
+        self.offsets = np.ascontiguousarray(offsets, np.int32)
+        self.slots = np.ascontiguousarray(slots, np.int32)
+        self.modes = np.ascontiguousarray(modes, np.int8)
+        self.seg_scale = None if seg_scale is None else np.ascontiguousarray(seg_scale, np.float32)
+        self.c = smlm_batch(int(self.offsets[-1]) if len(self.offsets) else 0, len(self.slots),
+                            self.offsets.ctypes.data, self.slots.ctypes.data, self.modes.ctypes.data,
+                            None if self.seg_scale is None else self.seg_scale.ctypes.data)
+
+    @classmethod
+    def from_synth(cls, b):
+        return cls(b.offsets, b.slots, b.modes, b.seg_scale)
+
+    @property
+    def S(self):
+        return self.c.S
+
+
+# ------------------------------ C-ABI mirrors ------------------------------
+def smlm_pool_create(device: int, in_features: int, out_features: int, rank: int, capacity: int,
+                     dtype: int = SMLM_BF16) -> int:
+    h = ctypes.c_void_p()
+    _check(_lib.smlm_pool_create(device, in_features, out_features, rank, capacity, dtype, ctypes.byref(h)),
+           "smlm_pool_create")
+    return h.value
+
+
+def smlm_pool_destroy(pool: int):
+    _check(_lib.smlm_pool_destroy(pool), "smlm_pool_destroy")
+
+
+def smlm_pool_set_option(pool: int, option: int, value: int):
+    _check(_lib.smlm_pool_set_option(pool, option, value), "smlm_pool_set_option")
+
+
+def smlm_adapter_register(pool: int, A, B, scale: float, stream=None) -> int:
+    s = ctypes.c_int(-1)
+    _check(_lib.smlm_adapter_register(pool, _ptr(A), _ptr(B), float(scale), _stream(stream, A.device),
+                                      ctypes.byref(s)), "smlm_adapter_register")
+    return s.value
+
+
+def smlm_adapter_set_grad(pool: int, slot: int, dA=None, dB=None):
+    _check(_lib.smlm_adapter_set_grad(pool, slot, _ptr(dA), _ptr(dB)), "smlm_adapter_set_grad")
+
+
+def smlm_adapter_unregister(pool: int, slot: int, stream=None, device=None):
+    _check(_lib.smlm_adapter_unregister(pool, slot, _stream(stream, device)), "smlm_adapter_unregister")
+
+
+def smlm_workspace_size(pool: int, batch: Batch, backward: bool) -> int:
+    return int(_lib.smlm_workspace_size(pool, ctypes.byref(batch.c), int(backward)))
+
+
+def smlm_forward(pool: int, batch: Batch, X, W, Y, V_save=None, ws=None, stream=None):
+    _check(_lib.smlm_forward(pool, ctypes.byref(batch.c), _ptr(X), _ptr(W), _ptr(Y), _ptr(V_save), _ptr(ws),
+                             0 if ws is None else ws.numel() * ws.element_size(), _stream(stream, X.device)),
+           "smlm_forward")
+
+
+def smlm_backward(pool: int, batch: Batch, X, W, dY, V_save=None, dX=None, accumulate=False, ws=None,
+                  stream=None):
+    _check(_lib.smlm_backward(pool, ctypes.byref(batch.c), _ptr(X), _ptr(W), _ptr(dY), _ptr(V_save), _ptr(dX),
+                              int(bool(accumulate)), _ptr(ws), 0 if ws is None else ws.numel() * ws.element_size(),
+                              _stream(stream, X.device)), "smlm_backward")
+
+
+def smlm_plan(batch: Batch, capacity: int, registered, l_long: int = 64, backward: bool = False):
+    reg = np.ascontiguousarray(registered, np.uint8)
+    n = ctypes.c_int(0)
+    code = _lib.smlm_plan(ctypes.byref(batch.c), capacity, reg.ctypes.data, l_long, int(backward), None, 0,
+                          ctypes.byref(n))
+    if code not in (SMLM_OK, SMLM_E_WORKSPACE):
+        _check(code, "smlm_plan")
+    buf = np.zeros((max(n.value, 1), 6), np.int32)
+    _check(_lib.smlm_plan(ctypes.byref(batch.c), capacity, reg.ctypes.data, l_long, int(backward),
+                          buf.ctypes.data, n.value, ctypes.byref(n)), "smlm_plan")
+    return buf[:n.value].tolist()
+
+
+def smlm_plan_export(pool: int, batch: Batch, backward: bool = False):
+    n = ctypes.c_int(0)
+    code = _lib.smlm_plan_export(pool, ctypes.byref(batch.c), int(backward), None, 0, ctypes.byref(n))
+    if code not in (SMLM_OK, SMLM_E_WORKSPACE):
+        _check(code, "smlm_plan_export")
+    buf = np.zeros((max(n.value, 1), 6), np.int32)
+    _check(_lib.smlm_plan_export(pool, ctypes.byref(batch.c), int(backward), buf.ctypes.data, n.value,
+                                 ctypes.byref(n)), "smlm_plan_export")
+    return buf[:n.value].tolist()
+
+
+def smlm_launch_count() -> int:
+    return int(_lib.smlm_launch_count())
+
+
+def smlm_profile_enable(on: bool):
+    _lib.smlm_profile_enable(int(bool(on)))
+
+
+def smlm_profile_read(kind: int):
+    ms = ctypes.c_double(0)
+    n = ctypes.c_int(0)
+    _lib.smlm_profile_read(kind, ctypes.byref(ms), ctypes.byref(n))
+    return ms.value, n.value
+
+
+# ------------------------------ convenience owner ------------------------------
+class Pool:
+    """One adapter pool per (layer, projection).  Keeps borrowed adapter tensors alive."""
+
+    def __init__(self, in_features: int, out_features: int, rank: int, capacity: int, dtype: int = SMLM_BF16,
+                 device: int = 0):
+        import torch
+        self.device = torch.device("cuda", device)
+        self.in_features, self.out_features, self.rank, self.capacity = in_features, out_features, rank, capacity
+        self.dtype = dtype
+        self.h = smlm_pool_create(device, in_features, out_features, rank, capacity, dtype)
+        self._keep = {}
+        self._ws = None
+
+    def close(self):
+        if self.h:
+            smlm_pool_destroy(self.h)
+            self.h = None
+            self._keep.clear()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def register(self, A, B, scale: float, stream=None) -> int:
+        slot = smlm_adapter_register(self.h, A, B, scale, stream)
+        self._keep[slot] = [A, B, None, None]
+        return slot
+
+    def set_grad(self, slot: int, dA=None, dB=None):
+        smlm_adapter_set_grad(self.h, slot, dA, dB)
+        self._keep[slot][2:] = [dA, dB]
+
+    def unregister(self, slot: int, stream=None):
+        smlm_adapter_unregister(self.h, slot, stream, self.device)
+        self._keep.pop(slot, None)
+
+    def set_option(self, option: int, value: int):
+        smlm_pool_set_option(self.h, option, value)
+
+    def workspace(self, batch: Batch, backward: bool = False):
+        import torch
+        n = smlm_workspace_size(self.h, batch, backward)
+        if self._ws is None or self._ws.numel() < n:
+            self._ws = torch.empty(max(n, 256), dtype=torch.uint8, device=self.device)
+        return self._ws
+
+    def forward(self, batch: Batch, X, W, Y=None, V_save=None, ws=None, stream=None):
+        import torch
+        if Y is None:
+            Y = torch.empty(X.shape[0], self.out_features, dtype=X.dtype, device=X.device)
+        if ws is None:
+            ws = self.workspace(batch, False)
+        smlm_forward(self.h, batch, X, W, Y, V_save, ws, stream)
+        return Y
+
+    def backward(self, batch: Batch, X, W, dY, V_save=None, dX=None, accumulate=False, ws=None, stream=None):
+        if ws is None:
+            ws = self.workspace(batch, True)
+        smlm_backward(self.h, batch, X, W, dY, V_save, dX, accumulate, ws, stream)
+        return dX
+
+    def plan(self, batch: Batch, backward: bool = False):
+        return smlm_plan_export(self.h, batch, backward)

@@ -1,0 +1,223 @@
+"""GPU parity: the CUDA path (through the C ABI) against the fp64 oracle on identical seeded inputs.
+
+Bar (BASELINE.json north_star): plan/index bookkeeping bit-exact; floating outputs within 2e-2
+(bf16 inputs, fp32 accumulate) and 1e-5 (fp32 test mode) under the rms-floored relative metric
+of tests/util.parity_err (reading R4).
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+from oracle import plan as plan_oracle
+from synth import DECODE, EVAL, FINETUNE, PREFILL
+from tests.smlm_run import run_smlm
+from tests.util import BF16_TOL, FP32_TOL, parity_err
+
+pytestmark = pytest.mark.gpu
+
+
+def _oracle_all(batch, w, X, dY, rows=None, has_grad=None, base_in=None, w_null=False):
+    Y, V = oracle.forward(batch, None if w_null else w.W, w.A, w.B, w.slot_scale, X, rows=rows, Y_in=base_in)
+    dX, dA, dB = oracle.backward(batch, w.W, w.A, w.B, w.slot_scale, X, dY, has_grad=has_grad, rows=rows)
+    return Y, V, dX, dA, dB
+
+
+def _check(res, batch, w, X, dY, tol, rows=None, has_grad=None, check_v=True, base_in=None, w_null=False):
+    Y, V, dX, dA, dB = _oracle_all(batch, w, X, dY, rows, has_grad, base_in, w_null)
+    sel = np.arange(batch.S) if rows is None else np.asarray(rows)
+    errs = {"Y": parity_err(res.Y.double().numpy()[sel], Y[sel])}
+    ft = batch.ft_rows()
+    ftsel = np.intersect1d(ft, sel)
+    rs = batch.row_slot()
+    ft_lora = ftsel[rs[ftsel] >= 0]
+    if check_v and res.V is not None and len(ft_lora):
+        errs["V"] = parity_err(res.V.double().numpy()[ft_lora], V[ft_lora])
+    if res.dX is not None and len(ftsel):
+        errs["dX"] = parity_err(res.dX.double().numpy()[ftsel], dX[ftsel])
+    for a in range(len(w.A)):
+        if np.any(rs[ft] == a) and (has_grad is None or has_grad[a]):
+            errs[f"dA{a}"] = parity_err(res.dA[a].double().numpy(), dA[a])
+            errs[f"dB{a}"] = parity_err(res.dB[a].double().numpy(), dB[a])
+        else:
+            assert torch.all(res.dA[a] == 0) and torch.all(res.dB[a] == 0), f"slot {a} must stay untouched"
+    bad = {k: v for k, v in errs.items() if not v <= tol}
+    assert not bad, f"parity failures {bad} (all: {errs})"
+    return errs
+
+
+# ------------------------------------------------------------------------------------------
+# fp32 test mode (1e-5)
+# ------------------------------------------------------------------------------------------
+def test_c1_fp32(golden_dir):
+    batch, w, X, dY = synth.c1_inputs()
+    res = run_smlm(batch, w, X, dY)
+    _check(res, batch, w, X, dY, FP32_TOL)
+    ref = json.load(open(os.path.join(golden_dir, "c1_checksums.json")))
+    ft = batch.ft_rows()
+    assert abs(res.Y.double().sum().item() - ref["sum_Y"]) <= 1e-4 * abs(ref["sum_Y"]) + 1e-3
+    assert abs(res.dA[0].double().sum().item() - ref["sum_dA0"]) <= 1e-4 * abs(ref["sum_dA0"])
+    assert abs(res.dX[ft].double().sum().item() - ref["sum_dX_ft"]) <= 1e-4 * abs(ref["sum_dX_ft"])
+    assert torch.all(res.dA[1:] == 0) and torch.all(res.dB[1:] == 0)
+
+
+def _worked(golden_dir, dtype, pad_in=None, pad_out=None, pad_r=None):
+    d = json.load(open(os.path.join(golden_dir, "worked_example.json")))
+    in_f, out_f, r = d["in"], d["out"], d["rank"]
+    pin, pout, pr = pad_in or in_f, pad_out or out_f, pad_r or r
+    W = torch.zeros(pout, pin); W[:out_f, :in_f] = torch.tensor(d["W"], dtype=torch.float32)
+    A = [torch.zeros(pr, pin) for _ in d["A"]]
+    B = [torch.zeros(pout, pr) for _ in d["B"]]
+    for i in range(len(A)):
+        A[i][:r, :in_f] = torch.tensor(d["A"][i], dtype=torch.float32)
+        B[i][:out_f, :r] = torch.tensor(d["B"][i], dtype=torch.float32)
+    X = torch.zeros(4, pin); X[:, :in_f] = torch.tensor(d["X"], dtype=torch.float32)
+    dY = torch.zeros(4, pout); dY[:, :out_f] = torch.tensor(d["dY"], dtype=torch.float32)
+    w = synth.Weights(W.to(dtype), [a.to(dtype) for a in A], [b.to(dtype) for b in B], d["slot_scale"])
+    batch = synth.batch_from_lengths(np.diff(d["offsets"]).tolist(), d["slots"], d["modes"], d["seg_scale"])
+    return d, batch, w, X.to(dtype), dY.to(dtype), in_f, out_f, r
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+def test_worked_example_exact(golden_dir, dtype):
+    pads = (None, None, None) if dtype == torch.float32 else (64, 64, 8)
+    d, batch, w, X, dY, in_f, out_f, r = _worked(golden_dir, dtype, *pads)
+    res = run_smlm(batch, w, X, dY)
+    e = d["expect"]
+    assert torch.equal(res.Y[:, :out_f].float(), torch.tensor(e["Y"], dtype=torch.float32))
+    assert torch.all(res.Y[:, out_f:] == 0)
+    assert torch.equal(res.V[0, :r].float(), torch.tensor(e["V_ft"]["0"], dtype=torch.float32))
+    assert torch.equal(res.dX[0, :in_f].float(), torch.tensor(e["dX_ft"]["0"], dtype=torch.float32))
+    assert torch.all(res.dX[1:] == 0)  # non fine-tune rows untouched
+    assert torch.equal(res.dA[:, :r, :in_f], torch.tensor(e["dA"], dtype=torch.float32))
+    assert torch.equal(res.dB[:, :out_f, :r], torch.tensor(e["dB"], dtype=torch.float32))
+
+
+# ------------------------------------------------------------------------------------------
+# bf16 tensor-core path at sizes the oracle finishes quickly (several tiles + ragged tails)
+# ------------------------------------------------------------------------------------------
+MIXED_LENGTHS = [300, 5, 1, 1, 64, 2, 130, 0, 63, 1, 200, 3, 1]
+MIXED_MODES = [FINETUNE, DECODE, DECODE, DECODE, EVAL, DECODE, FINETUNE, DECODE, PREFILL, DECODE, PREFILL,
+               FINETUNE, DECODE]
+
+
+@pytest.mark.parametrize("r", [8, 16, 32, 64])
+@pytest.mark.parametrize("shape", [(256, 320), (512, 192)])
+def test_bf16_mixed(r, shape):
+    in_f, out_f = shape
+    slots = [0, 1, 2, 1, 3, -1, 2, 0, 3, 4, -1, 4, 0]
+    scale = [1.0, 0.5, 1.0, 2.0, 1.0, 1.0, 0.75, 1.0, 1.0, 1.0, 1.0, 1.5, 1.0]
+    batch, w, X, dY = synth.random_case(1000 + r, in_f, out_f, r, 5, MIXED_LENGTHS, MIXED_MODES, slots, scale)
+    res = run_smlm(batch, w, X, dY)
+    assert res.plan_fwd == plan_oracle.forward_plan(batch.offsets, batch.slots, batch.modes)
+    assert res.plan_bwd == plan_oracle.backward_plan(batch.offsets, batch.slots, batch.modes)
+    _check(res, batch, w, X, dY, BF16_TOL)
+
+
+@pytest.mark.parametrize("l_long", [1, 16, 1000])
+def test_bf16_path_choice(l_long):
+    """All-long, mostly-long and all-short decompositions all match the oracle."""
+    batch, w, X, dY = synth.random_case(77, 192, 256, 16, 5, MIXED_LENGTHS, MIXED_MODES)
+    res = run_smlm(batch, w, X, dY, l_long=l_long)
+    _check(res, batch, w, X, dY, BF16_TOL)
+
+
+def test_bf16_inplace_base_and_no_vsave():
+    batch, w, X, dY = synth.random_case(5, 256, 256, 16, 5, MIXED_LENGTHS, MIXED_MODES)
+    base = (X.float() @ w.W.float().T).to(torch.bfloat16)
+    res = run_smlm(batch, w, X, dY, w_null=True, base_in=base, vsave=False)
+    _check(res, batch, w, X, dY, BF16_TOL, base_in=base, w_null=True, check_v=False)
+
+
+def test_bf16_accumulate_mask_and_no_dx():
+    batch, w, X, dY = synth.random_case(6, 256, 192, 16, 5, MIXED_LENGTHS, MIXED_MODES)
+    dA0 = torch.randn(5, 16, 256)
+    dB0 = torch.randn(5, 192, 16)
+    grads = [1, 0, 1, 1, 0]
+    res = run_smlm(batch, w, X, dY, accumulate=True, dA0=dA0, dB0=dB0, grads=grads, want_dx=False)
+    _, _, _, dA, dB = _oracle_all(batch, w, X, dY)
+    rs, ft = batch.row_slot(), batch.ft_rows()
+    for a in range(5):
+        has_ft = np.any(rs[ft] == a)
+        if grads[a] and has_ft:
+            assert parity_err(res.dA[a].double() - dA0[a].double(), dA[a]) <= BF16_TOL
+            assert parity_err(res.dB[a].double() - dB0[a].double(), dB[a]) <= BF16_TOL
+        else:
+            assert torch.equal(res.dA[a], dA0[a]) and torch.equal(res.dB[a], dB0[a])
+
+
+def test_bf16_b_zero_identical_to_base_only():
+    batch, w, X, dY = synth.random_case(8, 256, 256, 16, 5, MIXED_LENGTHS, MIXED_MODES)
+    wz = synth.Weights(w.W, w.A, [torch.zeros_like(b) for b in w.B], w.slot_scale)
+    r1 = run_smlm(batch, wz, X, dY, backward=False)
+    nb = synth.Batch(batch.offsets, np.full_like(batch.slots, -1), batch.modes, None)
+    r2 = run_smlm(nb, wz, X, dY, backward=False)
+    assert torch.equal(r1.Y.float(), r2.Y.float())  # value equality (-0 == +0)
+    ref = X.double() @ w.W.double().T
+    assert parity_err(r1.Y, ref) <= BF16_TOL
+
+
+def test_bf16_permutation_bit_exact():
+    lengths = [300, 5, 1, 1, 64, 2, 130, 63, 1, 200]
+    modes = [FINETUNE, DECODE, DECODE, DECODE, EVAL, DECODE, FINETUNE, PREFILL, DECODE, PREFILL]
+    slots = [0, 1, 2, 1, 3, -1, 2, 3, 4, -1]
+    batch, w, X, dY = synth.random_case(9, 256, 320, 16, 5, lengths, modes, slots)
+    r1 = run_smlm(batch, w, X, dY)
+    perm = [6, 2, 0, 9, 4, 1, 8, 3, 7, 5]
+    rows = np.concatenate([np.arange(batch.offsets[g], batch.offsets[g + 1]) for g in perm])
+    pb = synth.batch_from_lengths([lengths[g] for g in perm], [slots[g] for g in perm], [modes[g] for g in perm])
+    r2 = run_smlm(pb, w, X[rows], dY[rows])
+    assert torch.equal(r2.Y.float(), r1.Y[rows].float())
+    ft = batch.ft_rows()
+    pft = pb.ft_rows()
+    assert torch.equal(r2.dX[pft].float(), r1.dX[rows][pft].float())
+    for a in range(5):
+        assert parity_err(r2.dA[a], r1.dA[a].double()) <= 1e-5 or (torch.all(r1.dA[a] == 0) and torch.all(r2.dA[a] == 0))
+
+
+def test_bf16_dy_zero_and_determinism():
+    batch, w, X, dY = synth.random_case(10, 256, 192, 16, 5, MIXED_LENGTHS, MIXED_MODES)
+    r0 = run_smlm(batch, w, X, torch.zeros_like(dY))
+    assert torch.all(r0.dA == 0) and torch.all(r0.dB == 0) and torch.all(r0.dX == 0)
+    r1 = run_smlm(batch, w, X, dY)
+    r2 = run_smlm(batch, w, X, dY)
+    assert torch.equal(r1.dA, r2.dA) and torch.equal(r1.dB, r2.dB) and torch.equal(r1.Y, r2.Y)
+
+
+def test_empty_batch():
+    batch = synth.batch_from_lengths([], [], [])
+    w = synth.draw_weights(torch.Generator().manual_seed(0), 64, 64, 16, 1)
+    X = torch.zeros(0, 64, dtype=torch.bfloat16)
+    res = run_smlm(batch, w, X, torch.zeros(0, 64, dtype=torch.bfloat16))
+    assert res.Y.shape == (0, 64)
+
+
+# ------------------------------------------------------------------------------------------
+# full BASELINE.json shapes, sampled rows (plus exact-property checks at full size)
+# ------------------------------------------------------------------------------------------
+def _full_case(k, proj, rank=0):
+    batch = synth.config_batch(k, rank)
+    w = synth.config_weights(k, proj)
+    X, dY = synth.config_activations(k, proj, batch.S, rank)
+    return batch, w, X, dY
+
+
+@pytest.mark.parametrize("k,proj", [(2, "q"), (2, "k"), (3, "down"), (4, "gate"), (4, "v")])
+def test_full_config_sampled(k, proj):
+    batch, w, X, dY = _full_case(k, proj)
+    res = run_smlm(batch, w, X, dY)
+    rows = synth.sample_rows(batch, every=97)
+    _check(res, batch, w, X, dY, BF16_TOL, rows=rows)
+    # Euler identities at full size (no oracle): <dA_a, A_a> = <dB_a, B_a> = <dY, Y_lora_a>
+    if len(batch.ft_rows()):
+        rs, ft = batch.row_slot(), batch.ft_rows()
+        for a in sorted(set(rs[ft].tolist())):
+            if a < 0:
+                continue
+            lhsA = float((res.dA[a].double() * w.A[a].double()).sum())
+            lhsB = float((res.dB[a].double() * w.B[a].double()).sum())
+            assert abs(lhsA - lhsB) <= 2e-2 * (abs(lhsA) + abs(lhsB))
