@@ -1,0 +1,491 @@
+#!/usr/bin/env python
+"""SMLM benchmark (BASELINE.json metric: "SMLM tokens/s at Llama-3-8B r=16 mixed batch; % of
+HBM/tensor roofline").
+
+One step = one SMLM layer-step of the unified workload (BASELINE.json configs[3], "C4"):
+forward of all 7 Llama-3-8B projections (q,k,v,o,gate,up,down) over the mixed batch of
+4 fine-tune segments x 1024 rows + 8 prefill requests + 128 decode rows over a 64-adapter pool
+(r = 16), then the fine-tune backward (dX, dA, dB) of all 7 projections in reverse order.
+tokens/s = rows in the batch / step time (the per-layer throughput of SURVEY.md §8(d)).
+With --gpus N > 1 (torchrun, one process per GPU, NCCL): configs[4] "C5" -- every rank runs its
+own C4-shaped batch over a replicated 256-adapter pool and the fine-tune dA/dB of every
+projection are SUM all-reduced over NCCL on a side stream, overlapping the next projection's
+backward; value = all ranks' rows / max-over-ranks step time (weak scaling).
+
+`--impl reference` times the fp64 CPU oracle (oracle/, test infrastructure) on a bounded row
+sample of the same workload on this box's host cores (rank 0 only).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import synth  # noqa: E402
+
+METRIC = "SMLM tokens/s at Llama-3-8B r=16 mixed batch; % of HBM/tensor roofline"
+UNIT = "tokens/s"
+N_LAYER_SETS = 3          # distinct weight sets rotated across steps (each 416 MiB > 126 MB L2)
+FT_SLOTS = [0, 1, 2, 3]   # fine-tune adapters (C4/C5)
+GROUP_OF = {"q": "attn", "k": "attn", "v": "attn", "o": "o", "gate": "mlp", "up": "mlp", "down": "down"}
+
+
+def _peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return {"hbm": d["hbm_gbs"], "bf16": d["bf16_tflops"], "bf16_sustained": d.get("bf16_tflops_sustained"),
+                "source": "measured (MEASURED_PEAKS.json)"}
+    return {"hbm": 6650.0, "bf16": 1590.0, "bf16_sustained": 1400.0, "source": "fallback (B200_PROFILING.md)"}
+
+
+# ------------------------------------------------------------------------------------------
+# clocks sampler (nvidia-smi during the timed region)
+# ------------------------------------------------------------------------------------------
+class ClockSampler:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax = float(f[2])
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        busy = [s for s in sm if smax and s > 0.5 * smax] or sm
+        return {"sm_mhz": statistics.median(busy) if busy else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------------------------------
+# workload
+# ------------------------------------------------------------------------------------------
+class Workload:
+    def __init__(self, k: int, rank: int, dev: torch.device):
+        from paper_2511_00101_b200 import smlm as S
+        self.S = S
+        self.k = k
+        self.spec = synth.CONFIGS[k]
+        self.dev = dev
+        self.batch = synth.config_batch(k, rank)
+        self.b = S.Batch.from_synth(self.batch)
+        self.rows = self.batch.S
+        self.ft_rows = len(self.batch.ft_rows())
+        r = self.spec.rank
+        U = self.spec.n_adapters
+        g = torch.Generator(device=dev)
+        g.manual_seed(1234 + k)
+        # activations: one input per projection group (q/k/v share X, gate/up share X)
+        self.X = {}
+        for grp, in_f in (("attn", 4096), ("o", 4096), ("mlp", 4096), ("down", 14336)):
+            self.X[grp] = torch.randn(self.rows, in_f, generator=g, device=dev).to(torch.bfloat16)
+        self.dY, self.Y, self.dX, self.V = {}, {}, {}, {}
+        for p in synth.PROJECTIONS:
+            in_f, out_f = synth.PROJ_SHAPES[p]
+            self.dY[p] = torch.randn(self.rows, out_f, generator=g, device=dev).to(torch.bfloat16)
+            self.Y[p] = torch.empty(self.rows, out_f, dtype=torch.bfloat16, device=dev)
+            self.dX[p] = torch.empty(self.rows, in_f, dtype=torch.bfloat16, device=dev)
+            self.V[p] = torch.zeros(self.rows, r, dtype=torch.bfloat16, device=dev)
+        # layer sets: base weights + adapter pools (replicated across ranks: same seeds)
+        self.layers = []
+        for L in range(N_LAYER_SETS):
+            gw = torch.Generator(device=dev)
+            gw.manual_seed(1000 + 10 * k + 100 * L)
+            layer = {}
+            for p in synth.PROJECTIONS:
+                in_f, out_f = synth.PROJ_SHAPES[p]
+                W = (torch.randn(out_f, in_f, generator=gw, device=dev) / math.sqrt(in_f)).to(torch.bfloat16)
+                A = (torch.randn(U, r, in_f, generator=gw, device=dev) / math.sqrt(in_f)).to(torch.bfloat16)
+                B = (torch.randn(U, out_f, r, generator=gw, device=dev) / (4 * math.sqrt(r))).to(torch.bfloat16)
+                pool = S.Pool(in_f, out_f, r, U, S.SMLM_BF16, dev.index)
+                for a in range(U):
+                    assert pool.register(A[a], B[a], 2.0) == a
+                # fine-tune adapters' grads in one flat fp32 bucket per projection (all-reduce unit)
+                nA, nB = r * in_f, out_f * r
+                flat = torch.zeros(len(FT_SLOTS) * (nA + nB), dtype=torch.float32, device=dev)
+                for i, a in enumerate(FT_SLOTS):
+                    dA = flat[i * nA:(i + 1) * nA].view(r, in_f)
+                    dB = flat[len(FT_SLOTS) * nA + i * nB: len(FT_SLOTS) * nA + (i + 1) * nB].view(out_f, r)
+                    pool.set_grad(a, dA, dB)
+                wsf = pool.workspace(self.b, False)
+                wsf = torch.empty_like(wsf)
+                wsb = torch.empty(S.smlm_workspace_size(pool.h, self.b, True) + 256, dtype=torch.uint8, device=dev)
+                layer[p] = dict(W=W, A=A, B=B, pool=pool, grad=flat, wsf=wsf, wsb=wsb)
+            self.layers.append(layer)
+
+    def flops(self):
+        """Algorithmic flops of one layer-step: forward 2 in out + 2 r (in+out)
+        per row; fine-tune backward 2 in out + 4 r (in+out) per fine-tune row (no dW)."""
+        r = self.spec.rank
+        f = b = 0.0
+        for p in synth.PROJECTIONS:
+            in_f, out_f = synth.PROJ_SHAPES[p]
+            f += self.rows * (2.0 * in_f * out_f + 2.0 * r * (in_f + out_f))
+            b += self.ft_rows * (2.0 * in_f * out_f + 4.0 * r * (in_f + out_f))
+        return f, b
+
+    def fwd_gemm_flops(self, p):
+        """Algorithmic flops of one forward tensor-core launch for projection p: the base product
+        for every row, plus the on-chip shrink of long-tile rows that have an adapter, plus the
+        expand of every row that has an adapter (short-row shrink runs in the SIMT kernel)."""
+        r = self.spec.rank
+        in_f, out_f = synth.PROJ_SHAPES[p]
+        lens = np.diff(self.batch.offsets)
+        lora = self.batch.slots >= 0
+        long_ = lens >= 64
+        rows_lora = int(lens[lora].sum())
+        rows_long_lora = int(lens[lora & long_].sum())
+        return 2.0 * self.rows * in_f * out_f + 2.0 * rows_long_lora * r * in_f + 2.0 * rows_lora * r * out_f
+
+    def step(self, L: int, stream, comm=None):
+        S = self.S
+        layer = self.layers[L]
+        for p in synth.PROJECTIONS:
+            e = layer[p]
+            S.smlm_forward(e["pool"].h, self.b, self.X[GROUP_OF[p]], e["W"], self.Y[p], self.V[p], e["wsf"], stream)
+        for p in reversed(synth.PROJECTIONS):
+            e = layer[p]
+            S.smlm_backward(e["pool"].h, self.b, self.X[GROUP_OF[p]], e["W"], self.dY[p], self.V[p], self.dX[p],
+                            0, e["wsb"], stream)
+            if comm is not None:
+                comm(e["grad"])
+
+
+def _device_timed(fn, steps, stream):
+    start = torch.cuda.Event(enable_timing=True)
+    end = torch.cuda.Event(enable_timing=True)
+    start.record(stream)
+    for i in range(steps):
+        fn(i)
+    end.record(stream)
+    end.synchronize()
+    return start.elapsed_time(end)
+
+
+# ------------------------------------------------------------------------------------------
+# oracle (reference arm / cpu_baseline) on a bounded row sample
+# ------------------------------------------------------------------------------------------
+def oracle_sample(k: int, n_sample: int, rank: int = 0):
+    """Sub-batch of `n_sample` rows spread evenly over the workload's rows, keeping each row's
+    segment (slot, mode); the oracle then runs forward over all 7 projections and the fine-tune
+    backward (dX, dA, dB) over the sub-batch."""
+    bt = synth.config_batch(k, rank)
+    rs, rm = bt.row_slot(), bt.row_mode()
+    idx = np.unique(np.linspace(0, bt.S - 1, n_sample).round().astype(np.int64))
+    # segments of the sub-batch: consecutive sampled rows that came from the same segment
+    seg_of = np.repeat(np.arange(bt.G), np.diff(bt.offsets))
+    lengths, slots, modes = [], [], []
+    for t in idx:
+        g = seg_of[t]
+        if lengths and seg_prev == g:
+            lengths[-1] += 1
+        else:
+            lengths.append(1)
+            slots.append(int(rs[t]))
+            modes.append(int(rm[t]))
+        seg_prev = g
+    return synth.batch_from_lengths(lengths, slots, modes), idx
+
+
+def run_oracle_step(sub, k, weights_cache):
+    import oracle
+    g = torch.Generator().manual_seed(77)
+    n = sub.S
+    for p in synth.PROJECTIONS:
+        w = weights_cache[p]
+        in_f, out_f = synth.PROJ_SHAPES[p]
+        X = torch.randn(n, in_f, generator=g).to(torch.bfloat16)
+        dY = torch.randn(n, out_f, generator=g).to(torch.bfloat16)
+        oracle.forward(sub, w.W, w.A, w.B, w.slot_scale, X)
+        if len(sub.ft_rows()):
+            oracle.backward(sub, w.W, w.A, w.B, w.slot_scale, X, dY)
+
+
+def oracle_weights(k):
+    """Oracle-side weights: only the adapters the sample uses need values; shapes are full."""
+    spec = synth.CONFIGS[k]
+    cache = {}
+    for p in synth.PROJECTIONS:
+        in_f, out_f = synth.PROJ_SHAPES[p]
+        g = torch.Generator().manual_seed(1000 + 10 * k + synth.PROJECTIONS.index(p))
+        cache[p] = synth.draw_weights(g, in_f, out_f, spec.rank, spec.n_adapters)
+    return cache
+
+
+def time_oracle(k, n_sample, steps=1):
+    import oracle
+    sub, _ = oracle_sample(k, n_sample)
+    wc = oracle_weights(k)
+    run_oracle_step(synth.batch_from_lengths([1], [0], [0]), k, wc)  # build + warm
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        run_oracle_step(sub, k, wc)
+    dt = time.perf_counter() - t0
+    return sub.S * steps / dt, dt, sub, oracle.num_threads()
+
+
+# ------------------------------------------------------------------------------------------
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--oracle-rows", type=int, default=24, help="cpu_baseline sample rows (~20 s)")
+    ap.add_argument("--ref-rows", type=int, default=8, help="--impl reference sample rows per step")
+    args = ap.parse_args()
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    n = max(args.gpus, world)
+    k = 4 if n == 1 else 5
+    spec = synth.CONFIGS[k]
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        import oracle
+        sub, _ = oracle_sample(k, args.ref_rows)
+        wc = oracle_weights(k)
+        for _ in range(args.warmup):
+            run_oracle_step(sub, k, wc)
+        samples = []
+        for _ in range(args.steps):
+            t0 = time.perf_counter()
+            run_oracle_step(sub, k, wc)
+            samples.append(time.perf_counter() - t0)
+        ms = 1000.0 * statistics.median(samples)
+        val = sub.S / (ms / 1000.0)
+        threads = oracle.num_threads()
+        out = {"impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": n,
+               "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+               "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+               "config": {"workload": spec.name, "sample_rows_per_step": sub.S},
+               "cpu_baseline": {"value": val, "unit": UNIT, "cores": threads, "kind": "oracle",
+                                "sample": f"{sub.S} rows evenly spread over the {spec.name} batch "
+                                          f"(fp64 forward of 7 projections + fine-tune backward dX/dA/dB)"},
+               "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(out))
+        return
+
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    from paper_2511_00101_b200 import smlm as S
+
+    wl = Workload(k, rank, dev)
+    stream = torch.cuda.current_stream(dev)
+    comm = None
+    comm_stream = None
+    if dist is not None:
+        comm_stream = torch.cuda.Stream(dev)
+
+        def comm(buf):
+            ev = torch.cuda.Event()
+            ev.record(stream)
+            comm_stream.wait_event(ev)
+            with torch.cuda.stream(comm_stream):
+                dist.all_reduce(buf, op=dist.ReduceOp.SUM)
+
+    def one_step(i):
+        wl.step(i % N_LAYER_SETS, stream, comm)
+        if comm_stream is not None:
+            stream.wait_stream(comm_stream)
+
+    for i in range(args.warmup):
+        one_step(i)
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    S.smlm_profile_enable(True)
+    for kind in range(4):
+        S.smlm_profile_read(kind)
+    launches0 = S.smlm_launch_count()
+    clocks = ClockSampler(dev.index if dev.index is not None else 0)
+    clocks.start()
+    time.sleep(0.3)
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    ms_total = _device_timed(one_step, args.steps, stream)
+    torch.cuda.synchronize()
+    launches = S.smlm_launch_count() - launches0
+    prof = {kind: S.smlm_profile_read(kind) for kind in range(4)}
+    S.smlm_profile_enable(False)
+    clk = clocks.stop()
+    if dist is not None:
+        t = torch.tensor([ms_total], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_total = float(t.item())
+        dist.barrier()
+    ms = ms_total / args.steps
+    value = n * wl.rows / (ms / 1000.0)
+
+    # ---- roofline of the dominant kernel: the forward tensor-core GEMM ----
+    peaks = _peaks()
+    fwd_ms, fwd_n = prof[0]
+    bwd_ms, bwd_n = prof[1]
+    fwd_flops = sum(wl.fwd_gemm_flops(p) for p in synth.PROJECTIONS) * args.steps
+    achieved = fwd_flops / (fwd_ms / 1000.0) / 1e12 if fwd_ms > 0 else 0.0
+    peak = peaks["bf16_sustained"] or peaks["bf16"]
+    traffic = None
+    ncu_sum = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(ncu_sum):
+        try:
+            with open(ncu_sum) as f:
+                traffic = json.load(f).get("fwd_gemm_dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    f_alg, b_alg = wl.flops()
+    step_tflops = (f_alg + b_alg) / (ms / 1000.0) / 1e12
+    roofline = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                "frac": achieved / peak if peak else None, "traffic": traffic,
+                "kernel": "smlm_gemm_kernel<fwd> (tcgen05 fused base+shrink+expand)",
+                "peak_source": peaks["source"] + " bf16_tflops_sustained",
+                "launches": fwd_n, "avg_launch_ms": fwd_ms / max(fwd_n, 1),
+                "share_of_step": fwd_ms / ms_total if ms_total else None,
+                "bwd_gemm": {"launches": bwd_n, "ms": bwd_ms, "share_of_step": bwd_ms / ms_total if ms_total else None},
+                "step_alg_tflops": step_tflops, "step_frac": step_tflops / peak}
+
+    # ---- end to end: host buffers through the public API ----
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(wl, stream, max(2, min(args.steps, 5)), n, dist)
+
+    cpu = None
+    if rank == 0 and n == 1 and not args.no_cpu_baseline:
+        v, dt, sub, threads = time_oracle(k, args.oracle_rows, 1)
+        cpu = {"value": v, "unit": UNIT, "cores": threads, "kind": "oracle",
+               "sample": f"{sub.S} rows evenly spread over the {spec.name} batch; fp64 forward of 7 projections "
+                         f"+ fine-tune backward (dX, dA, dB); {dt:.1f} s"}
+
+    if rank == 0:
+        out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": n, "steps": args.steps,
+               "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+               "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+               "config": {"workload": spec.name + ": Llama-3-8B projections q,k,v,o,gate,up,down; r=16; "
+                          f"{spec.n_adapters} adapters; 4 fine-tune x 1024 rows (fwd+bwd) + 8 prefill "
+                          "(512-2048) + 128 decode rows",
+                          "rows_per_step_per_gpu": wl.rows, "finetune_rows": wl.ft_rows, "rank": spec.rank,
+                          "adapters": spec.n_adapters, "parallelism": f"dp{n}",
+                          "l2": f"inputs larger than L2: {N_LAYER_SETS} rotated layer weight sets of 416 MiB",
+                          "step": "1 layer-step = forward 7 projections + fine-tune backward 7 projections"
+                                  + (" + NCCL all-reduce of fine-tune dA/dB" if n > 1 else "")},
+               "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
+               "clocks": clk}
+        print(json.dumps(out))
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def run_e2e(wl, stream, steps, n, dist):
+    """Same step through the public API with HOST buffers: every step copies the step's inputs
+    (X per projection group; dY rows of the fine-tune segments) from pinned host memory and reads
+    back the results (Y of every projection, dX of fine-tune rows, the fine-tune dA/dB)."""
+    S = wl.S
+    ft = wl.ft_rows  # fine-tune segments come first (row order F, E, P, D)
+    hX = {g: torch.empty_like(x, device="cpu").pin_memory() for g, x in wl.X.items()}
+    hdY = {p: torch.empty(ft, y.shape[1], dtype=y.dtype).pin_memory() for p, y in wl.dY.items()}
+    hY = {p: torch.empty_like(y, device="cpu").pin_memory() for p, y in wl.Y.items()}
+    hdX = {p: torch.empty(ft, x.shape[1], dtype=x.dtype).pin_memory() for p, x in wl.dX.items()}
+    hG = {p: torch.empty_like(wl.layers[0][p]["grad"], device="cpu").pin_memory() for p in synth.PROJECTIONS}
+    for g in hX:
+        hX[g].copy_(wl.X[g].cpu())
+    for p in hdY:
+        hdY[p].copy_(wl.dY[p][:ft].cpu())
+    h2d = sum(t.numel() * t.element_size() for t in hX.values()) + sum(t.numel() * t.element_size() for t in hdY.values())
+    d2h = sum(t.numel() * t.element_size() for t in hY.values()) + \
+        sum(t.numel() * t.element_size() for t in hdX.values()) + sum(t.numel() * t.element_size() for t in hG.values())
+
+    def e2e_step(i):
+        L = i % N_LAYER_SETS
+        layer = wl.layers[L]
+        for g in hX:
+            wl.X[g].copy_(hX[g], non_blocking=True)
+        for p in hdY:
+            wl.dY[p][:ft].copy_(hdY[p], non_blocking=True)
+        for p in synth.PROJECTIONS:
+            e = layer[p]
+            S.smlm_forward(e["pool"].h, wl.b, wl.X[GROUP_OF[p]], e["W"], wl.Y[p], wl.V[p], e["wsf"], stream)
+            hY[p].copy_(wl.Y[p], non_blocking=True)
+        for p in reversed(synth.PROJECTIONS):
+            e = layer[p]
+            S.smlm_backward(e["pool"].h, wl.b, wl.X[GROUP_OF[p]], e["W"], wl.dY[p], wl.V[p], wl.dX[p], 0,
+                            e["wsb"], stream)
+            if dist is not None:
+                dist.all_reduce(e["grad"], op=dist.ReduceOp.SUM)
+            hdX[p].copy_(wl.dX[p][:ft], non_blocking=True)
+            hG[p].copy_(e["grad"], non_blocking=True)
+
+    e2e_step(0)
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    ms = _device_timed(e2e_step, steps, stream) / steps
+    if dist is not None:
+        t = torch.tensor([ms], device=wl.dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    return {"value": n * wl.rows / (ms / 1000.0), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+            "d2h_bytes_per_step": int(d2h), "ms_per_step": ms}
+
+
+if __name__ == "__main__":
+    main()

@@ -32,7 +32,11 @@ int launch_rows_shrink(const DevTile *tiles, int n_tiles, const SlotDev *slots, 
                        float *Vf, T *Vsave, int ft_only, cudaStream_t st);
 template <typename T>
 int launch_rows_u(const DevTile *tiles, int n_tiles, const SlotDev *slots, const T *dY, int out_f, int r, float *Uf,
-                  cudaStream_t st);
+                  __nv_bfloat16 *sUt, int r_pad, cudaStream_t st);
+template <typename TV>
+int launch_prep_sv(const DevTile *tiles, int n_tiles, const TV *V, int r, int r_pad, __nv_bfloat16 *sVt,
+                   cudaStream_t st);
+int launch_tok(const TokArgs &a, int num_sms, cudaStream_t st);
 size_t grad_group_bytes();
 void fill_grad_group(void *dst, int slot, int tile_begin, int n_tiles, float *dA, float *dB);
 template <typename T, typename TV>
@@ -238,7 +242,8 @@ int check_sticky() {
 struct WsLayout {
     size_t plan_off = 0, plan_bytes = 0;
     size_t vbd_off = 0, vbd_bytes = 0;     // bf16 fwd: block-diagonal s*V of short tiles
-    size_t u_off = 0, u_bytes = 0;         // bwd: U fp32 [S,r]
+    size_t u_off = 0, u_bytes = 0;         // bwd fp32 mode: U fp32 [S,r]
+    size_t sut_off = 0, svt_off = 0, st_bytes = 0;  // bwd bf16: tile-compact s*U, s*V [tiles*128, r_pad]
     size_t vf_off = 0, vf_bytes = 0;       // fp32 V [S,r] (fp32 mode, or bwd recompute)
     size_t total = 0;
 };
@@ -268,10 +273,17 @@ WsLayout layout_for(smlm_pool p, const smlm_batch *b, const Plan &plan, bool bwd
         L.vbd_bytes = plan.blocks.size() * 128 * (size_t)p->r_pad * 2;
         off = align256(off + L.vbd_bytes);
     }
-    if (bwd) {
+    if (bwd && p->dtype == SMLM_FP32) {
         L.u_off = off;
         L.u_bytes = (size_t)b->S * p->r * 4;
         off = align256(off + L.u_bytes);
+    }
+    if (bwd && p->dtype == SMLM_BF16) {
+        L.st_bytes = plan.bwd_tiles.size() * 128 * (size_t)p->r_pad * 2;
+        L.sut_off = off;
+        off = align256(off + L.st_bytes);
+        L.svt_off = off;
+        off = align256(off + L.st_bytes);
     }
     if (need_vf) {
         L.vf_off = off;
@@ -522,7 +534,7 @@ size_t smlm_workspace_size(smlm_pool p, const smlm_batch *batch, int backward) {
     if (!p) return 0;
     Plan plan;
     if (plan_for(p, batch, backward != 0, plan) != SMLM_OK) return 0;
-    bool need_vf = p->dtype == SMLM_FP32 || backward;  // conservative: bwd may recompute V
+    bool need_vf = p->dtype == SMLM_FP32 || backward;  // conservative: bwd may recompute V (V_save NULL)
     return layout_for(p, batch, plan, backward != 0, need_vf).total;
 }
 
@@ -602,7 +614,7 @@ int smlm_forward(smlm_pool p, const smlm_batch *b, const void *X, const void *W,
     a.has_w = has_w ? 1 : 0;
     a.Y = Y;
     a.Vsave = V_save;
-    a.Usave = nullptr;
+    a.sUt = nullptr;
     a.S = b->S;
     {
         ProfScope ps(0, st);
@@ -620,7 +632,7 @@ int smlm_backward(smlm_pool p, const smlm_batch *b, const void *X, const void *W
     if (b->S == 0 || b->G == 0 || plan.bwd_tiles.empty()) return SMLM_OK;
     if (!X || !dY) return set_err(SMLM_E_INVALID, "X and dY must be non-NULL");
     if (dX && !W) return set_err(SMLM_E_INVALID, "W is required when dX is requested");
-    WsLayout L = layout_for(p, b, plan, true, true);
+    WsLayout L = layout_for(p, b, plan, true, p->dtype == SMLM_FP32 || V_save == nullptr);
     if (!ws || ws_bytes < L.total) return set_err(SMLM_E_WORKSPACE, "workspace too small");
     DeviceGuard dg(p->device);
     if ((rc = check_sticky())) return rc;
@@ -649,7 +661,8 @@ int smlm_backward(smlm_pool p, const smlm_batch *b, const void *X, const void *W
     float *Vf = reinterpret_cast<float *>(wsb + L.vf_off);
 
     if (p->dtype == SMLM_FP32) {
-        CKL(launch_rows_u<float>(d_tiles, nt, p->d_slots, (const float *)dY, p->out, p->r, Uf, st), 1);
+        CKL(launch_rows_u<float>(d_tiles, nt, p->d_slots, (const float *)dY, p->out, p->r, Uf, nullptr, p->r_pad,
+                                 st), 1);
         if (dX)
             CKL(launch_f32_dx(d_tiles, nt, p->d_slots, (const float *)dY, (const float *)W, (float *)dX, Uf, p->in,
                               p->out, p->r, st), 1);
@@ -667,6 +680,8 @@ int smlm_backward(smlm_pool p, const smlm_batch *b, const void *X, const void *W
     }
 
     // ---------------- bf16 path ----------------
+    __nv_bfloat16 *sUt = reinterpret_cast<__nv_bfloat16 *>(wsb + L.sut_off);
+    __nv_bfloat16 *sVt = reinterpret_cast<__nv_bfloat16 *>(wsb + L.svt_off);
     if (dX) {
         GemmArgs a;
         memset(&a, 0, sizeof(a));
@@ -685,28 +700,41 @@ int smlm_backward(smlm_pool p, const smlm_batch *b, const void *X, const void *W
         a.has_w = 1;
         a.Y = dX;
         a.Vsave = nullptr;
-        a.Usave = Uf;
+        a.sUt = n_grad ? sUt : nullptr;
         a.S = b->S;
         ProfScope ps(1, st);
         CKL(launch_gemm(a, true, p->num_sms, st), 1);
     } else if (n_grad) {
-        CKL(launch_rows_u<__nv_bfloat16>(d_tiles, nt, p->d_slots, (const __nv_bfloat16 *)dY, p->out, p->r, Uf, st),
-            1);
+        CKL(launch_rows_u<__nv_bfloat16>(d_tiles, nt, p->d_slots, (const __nv_bfloat16 *)dY, p->out, p->r, nullptr,
+                                         sUt, p->r_pad, st), 1);
     }
     if (n_grad) {
         ProfScope ps(3, st);
         if (V_save) {
-            CKL((launch_dadb<__nv_bfloat16, __nv_bfloat16>(d_tiles, d_groups, n_grad, (const __nv_bfloat16 *)X,
-                                                           (const __nv_bfloat16 *)dY, Uf,
-                                                           (const __nv_bfloat16 *)V_save, p->in, p->out, p->r,
-                                                           accumulate, st)), 2);
+            CKL(launch_prep_sv<__nv_bfloat16>(d_tiles, nt, (const __nv_bfloat16 *)V_save, p->r, p->r_pad, sVt, st), 1);
         } else {
             CKL(launch_rows_shrink<__nv_bfloat16>(d_tiles, nt, p->d_slots, (const __nv_bfloat16 *)X, p->in, p->r, Vf,
                                                   nullptr, 0, st), 1);
-            CKL((launch_dadb<__nv_bfloat16, float>(d_tiles, d_groups, n_grad, (const __nv_bfloat16 *)X,
-                                                   (const __nv_bfloat16 *)dY, Uf, Vf, p->in, p->out, p->r,
-                                                   accumulate, st)), 2);
+            CKL(launch_prep_sv<float>(d_tiles, nt, Vf, p->r, p->r_pad, sVt, st), 1);
         }
+        TokArgs ta;
+        memset(&ta, 0, sizeof(ta));
+        const int rb = p->r_pad * 2;
+        if ((rc = make_map(&ta.tmX, X, p->in, b->S, 64, 64, CU_TENSOR_MAP_SWIZZLE_128B))) return rc;
+        if ((rc = make_map(&ta.tmDY, dY, p->out, b->S, 64, 64, CU_TENSOR_MAP_SWIZZLE_128B))) return rc;
+        if ((rc = make_map(&ta.tmSU, sUt, p->r_pad, (uint64_t)nt * 128, p->r_pad, 64, swizzle_for(rb)))) return rc;
+        if ((rc = make_map(&ta.tmSV, sVt, p->r_pad, (uint64_t)nt * 128, p->r_pad, 64, swizzle_for(rb)))) return rc;
+        ta.tiles = d_tiles;
+        ta.groups = reinterpret_cast<const GradGroup *>(d_groups);
+        ta.n_groups = n_grad;
+        ta.in_f = p->in;
+        ta.out_f = p->out;
+        ta.r = p->r;
+        ta.r_pad = p->r_pad;
+        ta.mt_a = (p->in + 127) / 128;
+        ta.mt_b = (p->out + 127) / 128;
+        ta.accumulate = accumulate ? 1 : 0;
+        CKL(launch_tok(ta, p->num_sms, st), 1);
     }
     return SMLM_OK;
 }

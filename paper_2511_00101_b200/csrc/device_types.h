@@ -44,8 +44,37 @@ struct GemmArgs {
     int has_w;      // fwd: 0 => Y holds the base output, only the LoRA term is added (RMW)
     void *Y;        // fwd: Y [S,out]; bwd: dX [S,in]
     void *Vsave;    // fwd: bf16 [S,r] (FT rows of long tiles, written by n-tile 0)
-    float *Usave;   // bwd: fp32 [S,r] (FT rows, written by n-tile 0)
+    void *sUt;      // bwd: bf16 s*U, tile-compact [n_tiles*128, r_pad] (written by n-tile 0)
     int S;
+};
+
+// backward: one adapter with fine-tune rows and bound gradient buffers (PAPER.md P:422 masking)
+struct GradGroup {
+    int slot;
+    int tile_begin;  // into the backward tile list (canonical reduction order)
+    int n_tiles;
+    int pad;
+    float *dA;       // [r,in] fp32 or NULL
+    float *dB;       // [out,r] fp32 or NULL
+};
+
+// token-contraction GEMM (a5): dA_a^T = X^T (sU) and dB_a = dY^T (sV) over a's fine-tune tiles
+struct TokArgs {
+    CUtensorMap tmX;    // X  [S,in]  box {64,64} SW128 (MN-major A operand)
+    CUtensorMap tmDY;   // dY [S,out] box {64,64} SW128
+    CUtensorMap tmSU;   // s*U tile-compact [n_tiles*128, r_pad] box {r_pad,64}
+    CUtensorMap tmSV;   // s*V tile-compact [n_tiles*128, r_pad] box {r_pad,64}
+    const DevTile *tiles;
+    const GradGroup *groups;
+    int n_groups;
+    int in_f;
+    int out_f;
+    int r;
+    int r_pad;
+    int mt_a;           // ceil(in/128)
+    int mt_b;           // ceil(out/128)
+    int accumulate;
+    int stages;
 };
 
 }  // namespace smlm

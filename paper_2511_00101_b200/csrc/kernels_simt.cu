@@ -184,16 +184,22 @@ __global__ void __launch_bounds__(256) rows_shrink_kernel(const DevTile *__restr
 }
 
 // U[t][j] = sum_o dy[t][o] B[o][j]   (tiles with slot >= 0)
+// Writes fp32 U [S,r] (Uf) and/or the tile-compact bf16 s*U [n_tiles*128, RP] (sUt, zero-padded).
 template <typename T, int RP>
 __global__ void __launch_bounds__(256) rows_u_kernel(const DevTile *__restrict__ tiles,
                                                      const SlotDev *__restrict__ slots,
                                                      const T *__restrict__ dY, int out_f, int r,
-                                                     float *__restrict__ Uf) {
+                                                     float *__restrict__ Uf, __nv_bfloat16 *__restrict__ sUt) {
     const DevTile t = tiles[blockIdx.x];
     if (t.slot < 0) return;
     const T *B = reinterpret_cast<const T *>(slots[t.slot].B);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    for (int m = blockIdx.y * 8 + warp; m < t.rows; m += gridDim.y * 8) {
+    for (int m = blockIdx.y * 8 + warp; m < 128; m += gridDim.y * 8) {
+        if (m >= t.rows) {
+            if (sUt)
+                for (int j = lane; j < RP; j += 32) sUt[((size_t)blockIdx.x * 128 + m) * RP + j] = __float2bfloat16_rn(0.f);
+            continue;
+        }
         const int row = t.row0 + m;
         const T *dy = dY + (size_t)row * out_f;
         float acc[RP];
@@ -208,8 +214,26 @@ __global__ void __launch_bounds__(256) rows_u_kernel(const DevTile *__restrict__
 #pragma unroll
         for (int j = 0; j < RP; ++j) {
             float s = warp_sum(acc[j]);
-            if (lane == 0 && j < r) Uf[(size_t)row * r + j] = s;
+            if (lane == 0) {
+                if (Uf && j < r) Uf[(size_t)row * r + j] = s;
+                if (sUt) sUt[((size_t)blockIdx.x * 128 + m) * RP + j] = __float2bfloat16_rn(j < r ? t.scale * s : 0.f);
+            }
         }
+    }
+}
+
+// tile-compact bf16 s*V [n_tiles*128, RP] from V_save (bf16) or the fp32 recompute, zero-padded
+template <typename TV, int RP>
+__global__ void __launch_bounds__(128) prep_sv_kernel(const DevTile *__restrict__ tiles, const TV *__restrict__ V,
+                                                      int r, __nv_bfloat16 *__restrict__ sVt) {
+    const DevTile t = tiles[blockIdx.x];
+    const int m = threadIdx.x;
+    __nv_bfloat16 *dst = sVt + ((size_t)blockIdx.x * 128 + m) * RP;
+#pragma unroll
+    for (int j = 0; j < RP; ++j) {
+        float v = 0.f;
+        if (t.slot >= 0 && m < t.rows && j < r) v = t.scale * ld_f(V + (size_t)(t.row0 + m) * r + j);
+        dst[j] = __float2bfloat16_rn(v);
     }
 }
 
@@ -217,15 +241,6 @@ __global__ void __launch_bounds__(256) rows_u_kernel(const DevTile *__restrict__
 // dA_a[j][k] = sum over a's fine-tune tiles (canonical order) and rows: (s U[t][j]) x[t][k]
 // grid (ceil(in/128), n_groups), 128 threads; thread owns column k.
 // --------------------------------------------------------------------------------------
-struct GradGroup {
-    int slot;
-    int tile_begin;
-    int n_tiles;
-    int pad;
-    float *dA;
-    float *dB;
-};
-
 template <typename T, int RP>
 __global__ void __launch_bounds__(128) dA_kernel(const DevTile *__restrict__ tiles,
                                                  const GradGroup *__restrict__ groups,
@@ -404,20 +419,35 @@ template int launch_rows_shrink<__nv_bfloat16>(const DevTile *, int, const SlotD
 
 template <typename T>
 int launch_rows_u(const DevTile *tiles, int n_tiles, const SlotDev *slots, const T *dY, int out_f, int r, float *Uf,
-                  cudaStream_t st) {
+                  __nv_bfloat16 *sUt, int r_pad, cudaStream_t st) {
     if (n_tiles == 0) return 0;
     dim3 grid(n_tiles, 16);
-    switch (rp_of(r)) {
-        case 16: rows_u_kernel<T, 16><<<grid, 256, 0, st>>>(tiles, slots, dY, out_f, r, Uf); break;
-        case 32: rows_u_kernel<T, 32><<<grid, 256, 0, st>>>(tiles, slots, dY, out_f, r, Uf); break;
-        default: rows_u_kernel<T, 64><<<grid, 256, 0, st>>>(tiles, slots, dY, out_f, r, Uf); break;
+    switch (sUt ? r_pad : rp_of(r)) {
+        case 16: rows_u_kernel<T, 16><<<grid, 256, 0, st>>>(tiles, slots, dY, out_f, r, Uf, sUt); break;
+        case 32: rows_u_kernel<T, 32><<<grid, 256, 0, st>>>(tiles, slots, dY, out_f, r, Uf, sUt); break;
+        default: rows_u_kernel<T, 64><<<grid, 256, 0, st>>>(tiles, slots, dY, out_f, r, Uf, sUt); break;
     }
     return (int)cudaGetLastError();
 }
 template int launch_rows_u<float>(const DevTile *, int, const SlotDev *, const float *, int, int, float *,
-                                  cudaStream_t);
+                                  __nv_bfloat16 *, int, cudaStream_t);
 template int launch_rows_u<__nv_bfloat16>(const DevTile *, int, const SlotDev *, const __nv_bfloat16 *, int, int,
-                                          float *, cudaStream_t);
+                                          float *, __nv_bfloat16 *, int, cudaStream_t);
+
+template <typename TV>
+int launch_prep_sv(const DevTile *tiles, int n_tiles, const TV *V, int r, int r_pad, __nv_bfloat16 *sVt,
+                   cudaStream_t st) {
+    if (n_tiles == 0) return 0;
+    switch (r_pad) {
+        case 16: prep_sv_kernel<TV, 16><<<n_tiles, 128, 0, st>>>(tiles, V, r, sVt); break;
+        case 32: prep_sv_kernel<TV, 32><<<n_tiles, 128, 0, st>>>(tiles, V, r, sVt); break;
+        default: prep_sv_kernel<TV, 64><<<n_tiles, 128, 0, st>>>(tiles, V, r, sVt); break;
+    }
+    return (int)cudaGetLastError();
+}
+template int launch_prep_sv<float>(const DevTile *, int, const float *, int, int, __nv_bfloat16 *, cudaStream_t);
+template int launch_prep_sv<__nv_bfloat16>(const DevTile *, int, const __nv_bfloat16 *, int, int, __nv_bfloat16 *,
+                                           cudaStream_t);
 
 size_t grad_group_bytes() { return sizeof(GradGroup); }
 void fill_grad_group(void *dst, int slot, int tile_begin, int n_tiles, float *dA, float *dB) {

@@ -292,23 +292,20 @@ __global__ void __launch_bounds__(kThreads, 1) smlm_gemm_kernel(const __grid_con
 #pragma unroll
                     for (int j = 0; j < 16; ++j) v[c + j] = tmp[j];
                 }
-                if (nt == 0 && row_ok) {
-                    if (BWD) {
-                        if (args.Usave) {
-                            float *u = args.Usave + (size_t)row * args.r;
+                if (!BWD && nt == 0 && row_ok && (t.flags & kTileFT) && args.Vsave) {
+                    __nv_bfloat16 *vs = reinterpret_cast<__nv_bfloat16 *>(args.Vsave) + (size_t)row * args.r;
 #pragma unroll
-                            for (int j = 0; j < RP; ++j)
-                                if (j < args.r) u[j] = __uint_as_float(v[j]);
-                        }
-                    } else if ((t.flags & kTileFT) && args.Vsave) {
-                        __nv_bfloat16 *vs = reinterpret_cast<__nv_bfloat16 *>(args.Vsave) + (size_t)row * args.r;
-#pragma unroll
-                        for (int j = 0; j < RP; ++j)
-                            if (j < args.r) vs[j] = __float2bfloat16_rn(__uint_as_float(v[j]));
-                    }
+                    for (int j = 0; j < RP; ++j)
+                        if (j < args.r) vs[j] = __float2bfloat16_rn(__uint_as_float(v[j]));
                 }
                 const float s = t.scale;
                 uint8_t *sv = base_ptr + (sv_addr - base);
+                // backward: n-tile 0 also stores s*U (bf16, tile-compact, zero rows past the segment)
+                // for the token-contraction dA kernel
+                uint4 *su_g = (BWD && nt == 0 && args.sUt)
+                                  ? reinterpret_cast<uint4 *>(reinterpret_cast<__nv_bfloat16 *>(args.sUt) +
+                                                              ((size_t)ti * 128 + m) * RP)
+                                  : nullptr;
 #pragma unroll
                 for (int c = 0; c < RP / 8; ++c) {
                     uint4 pk;
@@ -317,6 +314,7 @@ __global__ void __launch_bounds__(kThreads, 1) smlm_gemm_kernel(const __grid_con
                     pk.z = pack_bf16x2(s * __uint_as_float(v[8 * c + 4]), s * __uint_as_float(v[8 * c + 5]));
                     pk.w = pack_bf16x2(s * __uint_as_float(v[8 * c + 6]), s * __uint_as_float(v[8 * c + 7]));
                     *reinterpret_cast<uint4 *>(sv + swz((uint32_t)m * RB + 16u * c, RB)) = pk;
+                    if (su_g) su_g[c] = row_ok ? pk : make_uint4(0, 0, 0, 0);
                 }
                 fence_proxy_async_smem();
                 tc_fence_before();
@@ -388,6 +386,220 @@ int launch_impl(const GemmArgs &a, int num_sms, size_t smem, cudaStream_t st) {
     return (int)cudaGetLastError();
 }
 
+
+// ==========================================================================================
+// Token-contraction GEMM (a5): for every adapter with fine-tune rows and bound gradients,
+//   dA_a^T [in x r]  = X^T (s U)   and   dB_a [out x r] = dY^T (s V)
+// contracted over the adapter's fine-tune tokens, visiting its tiles in the canonical order
+// (bitwise deterministic, no atomics; PAPER.md P:420 shared backward, P:422 masking).
+// Work item = (adapter, 128-row M tile of in or out).  A operand = 64 tokens x 128 columns of
+// X or dY (MN-major, two 64-column SW128 boxes); B operand = 64 tokens x r_pad of the
+// tile-compact s*U / s*V (MN-major).  Token rows past a segment's end are zeroed in shared
+// memory before the MMA (isolation from other requests' rows).  Two TMEM accumulators of r_pad
+// columns let the epilogue of one item overlap the main loop of the next.
+// ==========================================================================================
+constexpr int kTokStages = 6;
+
+__device__ __forceinline__ bool tok_item(const TokArgs &a, int w, int &g, int &mt, bool &is_b) {
+    const int na = a.n_groups * a.mt_a;
+    if (w < na) {
+        g = w / a.mt_a;
+        mt = w % a.mt_a;
+        is_b = false;
+        return a.groups[g].dA != nullptr;
+    }
+    w -= na;
+    g = w / a.mt_b;
+    mt = w % a.mt_b;
+    is_b = true;
+    return a.groups[g].dB != nullptr;
+}
+
+template <int RP>
+__global__ void __launch_bounds__(kThreads, 1) smlm_tok_kernel(const __grid_constant__ TokArgs args) {
+    extern __shared__ uint8_t smem_raw[];
+    const uint32_t raw = smem_u32(smem_raw);
+    const uint32_t base = (raw + 1023u) & ~1023u;
+    uint8_t *base_ptr = smem_raw + (base - raw);
+    constexpr uint32_t RB = RP * 2;
+    constexpr uint32_t kA = 16384;              // 64 tokens x 128 columns bf16 (2 boxes of 8 KB)
+    constexpr uint32_t kB = 64 * RB;            // 64 tokens x r_pad
+    constexpr uint32_t kStage = kA + ((kB + 1023u) & ~1023u);
+    constexpr uint32_t kSwR = RB >= 128 ? kSw128 : (RB == 64 ? kSw64 : kSw32);
+    constexpr int ST = kTokStages;
+    const uint32_t bar = base + ST * kStage;
+    auto full_bar = [&](int s) { return bar + 8u * s; };
+    auto empty_bar = [&](int s) { return bar + 8u * (ST + s); };
+    const uint32_t accf0 = bar + 16u * ST;      // acc_full[2], acc_empty[2]
+    const uint32_t tmem_slot = accf0 + 32;
+    auto a_addr = [&](int s) { return base + s * kStage; };
+    auto b_addr = [&](int s) { return base + s * kStage + kA; };
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < ST; ++s) {
+            mbar_init(full_bar(s), 1);
+            mbar_init(empty_bar(s), 1);
+        }
+        mbar_init(accf0 + 0, 1);
+        mbar_init(accf0 + 8, 1);
+        mbar_init(accf0 + 16, 128);
+        mbar_init(accf0 + 24, 128);
+        fence_mbar_init();
+    }
+    if (warp == 2) tmem_alloc(tmem_slot, 128);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *reinterpret_cast<volatile uint32_t *>(base_ptr + (tmem_slot - base));
+    const int total = args.n_groups * (args.mt_a + args.mt_b);
+
+    if (warp == 0) {
+        int stage = 0;
+        uint32_t phase = 0;
+        for (int w = blockIdx.x; w < total; w += gridDim.x) {
+            int g, mt;
+            bool is_b;
+            if (!tok_item(args, w, g, mt, is_b)) continue;
+            const GradGroup grp = args.groups[g];
+            const int M = is_b ? args.out_f : args.in_f;
+            const int m0 = mt * 128;
+            const bool two = m0 + 64 < M;
+            const CUtensorMap *ma = is_b ? &args.tmDY : &args.tmX;
+            const CUtensorMap *mb = is_b ? &args.tmSV : &args.tmSU;
+            for (int ti = 0; ti < grp.n_tiles; ++ti) {
+                const int tix = grp.tile_begin + ti;
+                const DevTile t = args.tiles[tix];
+                for (int kb = 0; kb * 64 < t.rows; ++kb) {
+                    mbar_wait(empty_bar(stage), phase ^ 1);
+                    if (lane == 0) {
+                        mbar_expect_tx(full_bar(stage), (two ? kA : kA / 2) + kB);
+                        tma_load_2d(a_addr(stage), ma, full_bar(stage), m0, t.row0 + 64 * kb);
+                        if (two) tma_load_2d(a_addr(stage) + 8192, ma, full_bar(stage), m0 + 64, t.row0 + 64 * kb);
+                        tma_load_2d(b_addr(stage), mb, full_bar(stage), 0, tix * 128 + 64 * kb);
+                    }
+                    __syncwarp();
+                    if (++stage == ST) { stage = 0; phase ^= 1; }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        int stage = 0;
+        uint32_t phase = 0;
+        uint32_t it = 0;
+        constexpr uint32_t idesc = idesc_bf16(128, RP, 1, 1);
+        for (int w = blockIdx.x; w < total; w += gridDim.x) {
+            int g, mt;
+            bool is_b;
+            if (!tok_item(args, w, g, mt, is_b)) continue;
+            const GradGroup grp = args.groups[g];
+            const uint32_t buf = it & 1;
+            mbar_wait(accf0 + 16 + 8 * buf, ((it >> 1) & 1) ^ 1);
+            tc_fence_after();
+            const uint32_t acc = tmem_base + buf * RP;
+            uint32_t acc_on = 0;
+            for (int ti = 0; ti < grp.n_tiles; ++ti) {
+                const DevTile t = args.tiles[grp.tile_begin + ti];
+                for (int kb = 0; kb * 64 < t.rows; ++kb) {
+                    mbar_wait(full_bar(stage), phase);
+                    const int valid = min(64, t.rows - 64 * kb);
+                    if (valid < 64) {
+                        // zero token rows past the segment end in both 64-column boxes
+                        uint8_t *ap = base_ptr + (a_addr(stage) - base);
+                        for (int e = lane; e < (64 - valid) * 16; e += 32) {
+                            const int row = valid + (e >> 4), box = (e >> 3) & 1, ch = e & 7;
+                            *reinterpret_cast<uint4 *>(ap + box * 8192 + row * 128 + ch * 16) = make_uint4(0, 0, 0, 0);
+                        }
+                        fence_proxy_async_smem();
+                        __syncwarp();
+                    }
+                    tc_fence_after();
+                    if (lane == 0) {
+                        const uint32_t ab = a_addr(stage), bb = b_addr(stage);
+                        for (int k = 0; k * 16 < valid; ++k) {
+                            const uint64_t ad = smem_desc(ab + 2048u * k, 8192, 1024, kSw128);
+                            const uint64_t bd = smem_desc(bb + 16u * RB * k, 64u * RB, 8u * RB, kSwR);
+                            mma_bf16(acc, ad, bd, idesc, acc_on);
+                            acc_on = 1;
+                        }
+                        mma_commit(empty_bar(stage));
+                    }
+                    __syncwarp();
+                    if (++stage == ST) { stage = 0; phase ^= 1; }
+                }
+            }
+            if (lane == 0) mma_commit(accf0 + 8 * buf);
+            __syncwarp();
+            ++it;
+        }
+    } else if (warp >= 4) {
+        const int q = warp - 4;
+        const int m = q * 32 + lane;
+        const uint32_t lane_base = (uint32_t)(q * 32) << 16;
+        uint32_t it = 0;
+        for (int w = blockIdx.x; w < total; w += gridDim.x) {
+            int g, mt;
+            bool is_b;
+            if (!tok_item(args, w, g, mt, is_b)) continue;
+            const GradGroup grp = args.groups[g];
+            const uint32_t buf = it & 1;
+            mbar_wait(accf0 + 8 * buf, (it >> 1) & 1);
+            tc_fence_after();
+            uint32_t v[RP];
+#pragma unroll
+            for (int c = 0; c < RP; c += 16) {
+                uint32_t tmp[16];
+                tmem_ld16(tmem_base + buf * RP + lane_base + c, tmp);
+                tmem_wait_ld();
+#pragma unroll
+                for (int j = 0; j < 16; ++j) v[c + j] = tmp[j];
+            }
+            tc_fence_before();
+            mbar_arrive(accf0 + 16 + 8 * buf);
+            const int M = is_b ? args.out_f : args.in_f;
+            const int col = mt * 128 + m;
+            if (col < M) {
+                if (is_b) {
+                    float *p = grp.dB + (size_t)col * args.r;
+#pragma unroll
+                    for (int j = 0; j < RP; ++j)
+                        if (j < args.r) p[j] = args.accumulate ? p[j] + __uint_as_float(v[j]) : __uint_as_float(v[j]);
+                } else {
+#pragma unroll
+                    for (int j = 0; j < RP; ++j)
+                        if (j < args.r) {
+                            float *p = grp.dA + (size_t)j * args.in_f + col;
+                            *p = args.accumulate ? *p + __uint_as_float(v[j]) : __uint_as_float(v[j]);
+                        }
+                }
+            }
+            ++it;
+        }
+    }
+    __syncthreads();
+    if (warp == 2) {
+        tc_fence_after();
+        tmem_dealloc(tmem_base, 128);
+    }
+}
+
+template <int RP>
+int launch_tok_impl(const TokArgs &a, int num_sms, cudaStream_t st) {
+    auto kern = smlm_tok_kernel<RP>;
+    constexpr size_t kStage = 16384 + ((64 * RP * 2 + 1023) & ~1023);
+    const size_t smem = 1024 + kTokStages * kStage + 256;
+    static bool attr_done = false;
+    if (!attr_done) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return (int)e;
+        attr_done = true;
+    }
+    const int total = a.n_groups * (a.mt_a + a.mt_b);
+    const int grid = total < num_sms ? total : num_sms;
+    kern<<<grid, kThreads, smem, st>>>(a);
+    return (int)cudaGetLastError();
+}
+
 }  // namespace
 
 // Shared-memory bytes and pipeline depth for a given r_pad.
@@ -398,6 +610,16 @@ int gemm_stages(int r_pad, size_t *smem_bytes) {
     if (stages > 6) stages = 6;
     if (smem_bytes) *smem_bytes = fixed + stage * stages;
     return stages;
+}
+
+int launch_tok(const TokArgs &a, int num_sms, cudaStream_t st) {
+    if (a.n_groups == 0) return 0;
+    switch (a.r_pad) {
+        case 16: return launch_tok_impl<16>(a, num_sms, st);
+        case 32: return launch_tok_impl<32>(a, num_sms, st);
+        case 64: return launch_tok_impl<64>(a, num_sms, st);
+    }
+    return (int)cudaErrorInvalidValue;
 }
 
 int launch_gemm(const GemmArgs &a, bool bwd, int num_sms, cudaStream_t st) {
