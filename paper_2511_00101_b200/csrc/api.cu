@@ -203,6 +203,16 @@ struct SlotHost {
 
 size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
+// m-tiles per raster group: the group's 128-row A tiles (128 x K bf16) stay L2-resident while
+// the CTAs sweep every n-tile, so each W n-tile is fetched from HBM once per group (~48 MB budget)
+int raster_group(int K) {
+    const long tile = 128L * K * 2;
+    long g = (48L << 20) / tile;
+    if (g < 4) g = 4;
+    if (g > 64) g = 64;
+    return (int)g;
+}
+
 }  // namespace
 
 struct smlm_pool_s {
@@ -452,7 +462,8 @@ static int upload_slot(smlm_pool p, int slot, cudaStream_t st) {
             const int rb = p->r_pad * 2;
             int rc;
             if ((rc = make_map(&d.tmA, h.A, p->in, p->r, 64, p->r_pad, CU_TENSOR_MAP_SWIZZLE_128B))) return rc;
-            if ((rc = make_map(&d.tmBn, h.B, p->r, p->out, p->r_pad, 256, swizzle_for(rb)))) return rc;
+            // forward n-tile = 256 - r_pad output columns (the shrink rides in the same N=256 MMA)
+            if ((rc = make_map(&d.tmBn, h.B, p->r, p->out, p->r_pad, 256 - p->r_pad, swizzle_for(rb)))) return rc;
             if ((rc = make_map(&d.tmBk, h.B, p->r, p->out, p->r_pad, 64, swizzle_for(rb)))) return rc;
         }
     }
@@ -597,7 +608,8 @@ int smlm_forward(smlm_pool p, const smlm_batch *b, const void *X, const void *W,
     GemmArgs a;
     memset(&a, 0, sizeof(a));
     if ((rc = make_map(&a.tmA, X, p->in, b->S, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B))) return rc;
-    if (has_w && (rc = make_map(&a.tmB, W, p->in, p->out, 64, 256, CU_TENSOR_MAP_SWIZZLE_128B))) return rc;
+    const int bnw = kBN - p->r_pad;
+    if (has_w && (rc = make_map(&a.tmB, W, p->in, p->out, 64, bnw, CU_TENSOR_MAP_SWIZZLE_128B))) return rc;
     if (!plan.blocks.empty() &&
         (rc = make_map(&a.tmV, Vbd, p->r_pad, plan.blocks.size() * 128, p->r_pad, 128, swizzle_for(p->r_pad * 2))))
         return rc;
@@ -607,10 +619,11 @@ int smlm_forward(smlm_pool p, const smlm_batch *b, const void *X, const void *W,
     a.n_tiles = (int)tiles.size();
     a.K = p->in;
     a.N = p->out;
-    a.n_ntiles = (p->out + kBN - 1) / kBN;
+    a.n_ntiles = (p->out + bnw - 1) / bnw;
     a.r = p->r;
     a.r_pad = p->r_pad;
     a.stages = gemm_stages(p->r_pad, nullptr);
+    a.group_m = raster_group(p->in);
     a.has_w = has_w ? 1 : 0;
     a.Y = Y;
     a.Vsave = V_save;
@@ -697,6 +710,7 @@ int smlm_backward(smlm_pool p, const smlm_batch *b, const void *X, const void *W
         a.r = p->r;
         a.r_pad = p->r_pad;
         a.stages = gemm_stages(p->r_pad, nullptr);
+        a.group_m = raster_group(p->out);
         a.has_w = 1;
         a.Y = dX;
         a.Vsave = nullptr;

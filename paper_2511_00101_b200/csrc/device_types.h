@@ -41,6 +41,7 @@ struct GemmArgs {
     int r;
     int r_pad;
     int stages;
+    int group_m;    // m-tiles per raster group (L2 reuse)
     int has_w;      // fwd: 0 => Y holds the base output, only the LoRA term is added (RMW)
     void *Y;        // fwd: Y [S,out]; bwd: dX [S,in]
     void *Vsave;    // fwd: bf16 [S,r] (FT rows of long tiles, written by n-tile 0)

@@ -32,11 +32,11 @@ constexpr int kGroupM = 8;  // m-tiles per raster group (L2 reuse of W n-tiles a
 constexpr uint32_t kABytes = 128 * 128;   // X/dY tile: 128 rows x 64 bf16
 constexpr uint32_t kBBytes = 256 * 128;   // W tile: 256 x 64 bf16
 
-__device__ __forceinline__ void decode_work(int w, int n_tiles, int n_nt, int &ti, int &nt) {
-    const int gsz = kGroupM * n_nt;
+__device__ __forceinline__ void decode_work(int w, int n_tiles, int n_nt, int group_m, int &ti, int &nt) {
+    const int gsz = group_m * n_nt;
     const int g = w / gsz;
-    const int first = g * kGroupM;
-    const int gm = min(kGroupM, n_tiles - first);
+    const int first = g * group_m;
+    const int gm = min(group_m, n_tiles - first);
     const int local = w - g * gsz;
     ti = first + local % gm;
     nt = local / gm;
@@ -50,7 +50,14 @@ __global__ void __launch_bounds__(kThreads, 1) smlm_gemm_kernel(const __grid_con
     uint8_t *base_ptr = smem_raw + (base - raw);
 
     constexpr uint32_t RB = RP * 2;             // bytes per row of an r_pad-wide bf16 tile
-    constexpr uint32_t kAaBytes = RP * 128;     // shrink/U operand per stage
+    // Forward: the shrink is fused into the main MMA.  The B operand of one N=256 MMA is the W
+    // n-tile (BNW = 256 - RP rows) stacked on A_a (RP rows), so the accumulator columns
+    // [BNW, 256) receive V = X_tile A_a^T while [0, BNW) receive X_tile W^T, and the X tile is
+    // read from shared memory once per K-step.  Backward: dY W needs W as an MN-major operand,
+    // which cannot be stacked with B_a in one swizzle row, so U = dY B_a is a separate N=RP MMA
+    // whose accumulator lives in the top RP columns of the other TMEM buffer.
+    constexpr int BNW = BWD ? kBN : kBN - RP;   // output columns per n-tile
+    constexpr uint32_t kAaBytes = BWD ? RP * 128 : 0;
     constexpr uint32_t kStage = kABytes + kBBytes + kAaBytes;
     constexpr uint32_t kSwR = RB >= 128 ? kSw128 : (RB == 64 ? kSw64 : kSw32);
     const int stages = args.stages;
@@ -58,11 +65,12 @@ __global__ void __launch_bounds__(kThreads, 1) smlm_gemm_kernel(const __grid_con
     const uint32_t bar = sv_addr + 128 * RB;
     auto full_bar = [&](int s) { return bar + 8u * s; };
     auto empty_bar = [&](int s) { return bar + 8u * (stages + s); };
-    const uint32_t acc_full = bar + 16u * stages;
-    const uint32_t acc_empty = acc_full + 8;
-    const uint32_t v_full = acc_full + 16;
-    const uint32_t sv_ready = acc_full + 24;
-    const uint32_t tmem_slot = acc_full + 32;
+    const uint32_t acc_full0 = bar + 16u * stages;   // acc_full[2]
+    const uint32_t acc_empty0 = acc_full0 + 16;      // acc_empty[2]
+    const uint32_t vfree0 = acc_full0 + 32;          // vfree[2] (backward)
+    const uint32_t v_full = acc_full0 + 48;
+    const uint32_t sv_ready = acc_full0 + 56;
+    const uint32_t tmem_slot = acc_full0 + 64;
     auto a_addr = [&](int s) { return base + s * kStage; };
     auto b_addr = [&](int s) { return base + s * kStage + kABytes; };
     auto aa_addr = [&](int s) { return base + s * kStage + kABytes + kBBytes; };
@@ -75,8 +83,11 @@ __global__ void __launch_bounds__(kThreads, 1) smlm_gemm_kernel(const __grid_con
             mbar_init(full_bar(s), 1);
             mbar_init(empty_bar(s), 1);
         }
-        mbar_init(acc_full, 1);
-        mbar_init(acc_empty, 128);
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(acc_full0 + 8 * b, 1);
+            mbar_init(acc_empty0 + 8 * b, 128);
+            mbar_init(vfree0 + 8 * b, 128);
+        }
         mbar_init(v_full, 1);
         mbar_init(sv_ready, 128);
         fence_mbar_init();
@@ -89,8 +100,11 @@ __global__ void __launch_bounds__(kThreads, 1) smlm_gemm_kernel(const __grid_con
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *reinterpret_cast<volatile uint32_t *>(base_ptr + (tmem_slot - base));
-    const uint32_t acc_tmem = tmem_base;
-    const uint32_t v_tmem = tmem_base + 256;
+    // two accumulator buffers ACC_b = TMEM columns [256 b, 256 b + 256)
+    auto acc_col = [&](uint32_t b) { return tmem_base + 256u * b; };
+    auto v_col = [&](uint32_t b) {
+        return BWD ? tmem_base + 256u * (1u - b) + 256u - RP : tmem_base + 256u * b + BNW;
+    };
 
     const int total = args.n_tiles * args.n_ntiles;
     const int nkb = args.K / kBK;
@@ -104,9 +118,9 @@ __global__ void __launch_bounds__(kThreads, 1) smlm_gemm_kernel(const __grid_con
         };
         for (int w = blockIdx.x; w < total; w += gridDim.x) {
             int ti, nt;
-            decode_work(w, args.n_tiles, args.n_ntiles, ti, nt);
+            decode_work(w, args.n_tiles, args.n_ntiles, args.group_m, ti, nt);
             const DevTile t = args.tiles[ti];
-            const int n0 = nt * kBN;
+            const int n0 = nt * BNW;
             const bool is_short = (t.flags & kTileShort) != 0;
             const bool lora = (t.flags & kTileLora) != 0;
             const SlotDev *sd = lora ? args.slots + t.slot : nullptr;
@@ -121,10 +135,10 @@ __global__ void __launch_bounds__(kThreads, 1) smlm_gemm_kernel(const __grid_con
                                 for (int i = 0; i < 4; ++i) nb += (n0 + 64 * i < args.N);
                                 bytes += 8192u * nb;
                             } else {
-                                bytes += kBBytes;
+                                bytes += BNW * 128u;
                             }
                         }
-                        if (lora) bytes += kAaBytes;
+                        if (lora) bytes += RP * 128u;
                         mbar_expect_tx(full_bar(stage), bytes);
                         tma_load_2d(a_addr(stage), &args.tmA, full_bar(stage), kb * kBK, t.row0);
                         if (args.has_w) {
@@ -140,8 +154,8 @@ __global__ void __launch_bounds__(kThreads, 1) smlm_gemm_kernel(const __grid_con
                         if (lora) {
                             if (BWD)  // B_a rows [kb*64, +64) x r_pad  (MN-major U operand)
                                 tma_load_2d(aa_addr(stage), &sd->tmBk, full_bar(stage), 0, kb * kBK);
-                            else      // A_a [r_pad rows] x 64 k      (K-major shrink operand)
-                                tma_load_2d(aa_addr(stage), &sd->tmA, full_bar(stage), kb * kBK, 0);
+                            else      // A_a [r_pad rows] x 64 k, stacked under the W rows
+                                tma_load_2d(b_addr(stage) + BNW * 128u, &sd->tmA, full_bar(stage), kb * kBK, 0);
                         }
                     }
                     __syncwarp();
@@ -151,25 +165,26 @@ __global__ void __launch_bounds__(kThreads, 1) smlm_gemm_kernel(const __grid_con
             if (lora) {
                 mbar_wait(empty_bar(stage), phase ^ 1);
                 if (lane == 0) {
-                    mbar_expect_tx(full_bar(stage), 256u * RB);
                     if (BWD) {  // A_a [r_pad rows, n0 + 64 i ...] MN-major expand operand
+                        mbar_expect_tx(full_bar(stage), 256u * RB);
                         for (int i = 0; i < 4; ++i)
                             tma_load_2d(b_addr(stage) + (uint32_t)RP * 128u * i, &sd->tmA, full_bar(stage),
                                         n0 + 64 * i, 0);
-                    } else {    // B_a [n0.., r_pad] K-major expand operand
+                    } else {    // B_a [n0 .. n0 + BNW, r_pad] K-major expand operand
+                        mbar_expect_tx(full_bar(stage), (uint32_t)BNW * RB);
                         tma_load_2d(b_addr(stage), &sd->tmBn, full_bar(stage), 0, n0);
                     }
                 }
                 __syncwarp();
                 advance();
             } else if (is_short) {
-                for (int b = 0; b < t.nblk; ++b) {
-                    const DevBlock blk = args.blocks[t.blk0 + b];
+                for (int bi = 0; bi < t.nblk; ++bi) {
+                    const DevBlock blk = args.blocks[t.blk0 + bi];
                     const SlotDev *bs = args.slots + blk.slot;
                     mbar_wait(empty_bar(stage), phase ^ 1);
                     if (lane == 0) {
-                        mbar_expect_tx(full_bar(stage), 128u * RB + 256u * RB);
-                        tma_load_2d(a_addr(stage), &args.tmV, full_bar(stage), 0, (t.blk0 + b) * 128);
+                        mbar_expect_tx(full_bar(stage), 128u * RB + (uint32_t)BNW * RB);
+                        tma_load_2d(a_addr(stage), &args.tmV, full_bar(stage), 0, (t.blk0 + bi) * 128);
                         tma_load_2d(b_addr(stage), &bs->tmBn, full_bar(stage), 0, n0);
                     }
                     __syncwarp();
@@ -184,16 +199,20 @@ __global__ void __launch_bounds__(kThreads, 1) smlm_gemm_kernel(const __grid_con
         auto advance = [&]() {
             if (++stage == stages) { stage = 0; phase ^= 1; }
         };
-        constexpr uint32_t idesc_main = idesc_bf16(128, kBN, 0, BWD ? 1 : 0);
-        constexpr uint32_t idesc_v = idesc_bf16(128, RP, 0, BWD ? 1 : 0);
+        constexpr uint32_t idesc_full = idesc_bf16(128, kBN, 0, BWD ? 1 : 0);   // W (+ stacked A_a)
+        constexpr uint32_t idesc_out = idesc_bf16(128, BNW, 0, BWD ? 1 : 0);    // output columns only
+        constexpr uint32_t idesc_v = idesc_bf16(128, RP, 0, 1);                 // backward U
         uint32_t it = 0, lora_it = 0;
         for (int w = blockIdx.x; w < total; w += gridDim.x) {
             int ti, nt;
-            decode_work(w, args.n_tiles, args.n_ntiles, ti, nt);
+            decode_work(w, args.n_tiles, args.n_ntiles, args.group_m, ti, nt);
             const DevTile t = args.tiles[ti];
             const bool is_short = (t.flags & kTileShort) != 0;
             const bool lora = (t.flags & kTileLora) != 0;
-            mbar_wait(acc_empty, (it & 1) ^ 1);
+            const uint32_t b = it & 1, u = it >> 1;
+            const uint32_t acc_tmem = acc_col(b), v_tmem = v_col(b);
+            mbar_wait(acc_empty0 + 8 * b, (u & 1) ^ 1);
+            if (BWD && lora && it >= 1) mbar_wait(vfree0 + 8 * (1 - b), ((it - 1) >> 1) & 1);
             tc_fence_after();
             uint32_t acc_on = 0;  // 1 once the accumulator holds data
             if (!is_short || args.has_w) {
@@ -205,15 +224,20 @@ __global__ void __launch_bounds__(kThreads, 1) smlm_gemm_kernel(const __grid_con
 #pragma unroll
                         for (int k = 0; k < kBK / 16; ++k) {
                             const uint64_t ad = smem_desc(ab + 32u * k, 16, 1024, kSw128);
-                            if (args.has_w) {
-                                const uint64_t bd = BWD ? smem_desc(bb + 2048u * k, 8192, 1024, kSw128)
-                                                        : smem_desc(bb + 32u * k, 16, 1024, kSw128);
-                                mma_bf16(acc_tmem, ad, bd, idesc_main, (kb | k) != 0);
-                            }
-                            if (lora) {
-                                const uint64_t vd = BWD ? smem_desc(vb + 16u * RB * k, 64u * RB, 8u * RB, kSwR)
-                                                        : smem_desc(vb + 32u * k, 16, 1024, kSw128);
-                                mma_bf16(v_tmem, ad, vd, idesc_v, (kb | k) != 0);
+                            if (BWD) {
+                                const uint64_t bd = smem_desc(bb + 2048u * k, 8192, 1024, kSw128);
+                                mma_bf16(acc_tmem, ad, bd, idesc_full, (kb | k) != 0);
+                                if (lora) {
+                                    const uint64_t vd = smem_desc(vb + 16u * RB * k, 64u * RB, 8u * RB, kSwR);
+                                    mma_bf16(v_tmem, ad, vd, idesc_v, (kb | k) != 0);
+                                }
+                            } else if (args.has_w) {
+                                const uint64_t bd = smem_desc(bb + 32u * k, 16, 1024, kSw128);
+                                mma_bf16(acc_tmem, ad, bd, lora ? idesc_full : idesc_out, (kb | k) != 0);
+                            } else {
+                                // delta-only forward: only the stacked A_a rows (V columns)
+                                const uint64_t vd = smem_desc(bb + BNW * 128u + 32u * k, 16, 1024, kSw128);
+                                mma_bf16(v_tmem, ad, vd, idesc_bf16(128, RP, 0, 0), (kb | k) != 0);
                             }
                         }
                         mma_commit(empty_bar(stage));
@@ -236,7 +260,7 @@ __global__ void __launch_bounds__(kThreads, 1) smlm_gemm_kernel(const __grid_con
                         const uint64_t ad = smem_desc(sv_addr + 32u * kk, 16, 8u * RB, kSwR);
                         const uint64_t bd = BWD ? smem_desc(bb + 2048u * kk, (uint32_t)RP * 128u, 1024, kSw128)
                                                 : smem_desc(bb + 32u * kk, 16, 8u * RB, kSwR);
-                        mma_bf16(acc_tmem, ad, bd, idesc_main, acc_on | (kk != 0));
+                        mma_bf16(acc_tmem, ad, bd, idesc_out, acc_on | (kk != 0));
                     }
                     mma_commit(empty_bar(stage));
                 }
@@ -244,7 +268,7 @@ __global__ void __launch_bounds__(kThreads, 1) smlm_gemm_kernel(const __grid_con
                 advance();
                 ++lora_it;
             } else if (is_short) {
-                for (int b = 0; b < t.nblk; ++b) {
+                for (int bi = 0; bi < t.nblk; ++bi) {
                     mbar_wait(full_bar(stage), phase);
                     tc_fence_after();
                     if (lane == 0) {
@@ -253,7 +277,7 @@ __global__ void __launch_bounds__(kThreads, 1) smlm_gemm_kernel(const __grid_con
                         for (int kk = 0; kk < RP / 16; ++kk) {
                             const uint64_t ad = smem_desc(ab + 32u * kk, 16, 8u * RB, kSwR);
                             const uint64_t bd = smem_desc(bb + 32u * kk, 16, 8u * RB, kSwR);
-                            mma_bf16(acc_tmem, ad, bd, idesc_main, acc_on | (uint32_t)(b | kk));
+                            mma_bf16(acc_tmem, ad, bd, idesc_out, acc_on | (uint32_t)(bi | kk));
                         }
                         mma_commit(empty_bar(stage));
                     }
@@ -261,7 +285,7 @@ __global__ void __launch_bounds__(kThreads, 1) smlm_gemm_kernel(const __grid_con
                     advance();
                 }
             }
-            if (lane == 0) mma_commit(acc_full);
+            if (lane == 0) mma_commit(acc_full0 + 8 * b);
             __syncwarp();
             ++it;
         }
@@ -274,12 +298,13 @@ __global__ void __launch_bounds__(kThreads, 1) smlm_gemm_kernel(const __grid_con
         __nv_bfloat16 *Y = reinterpret_cast<__nv_bfloat16 *>(args.Y);
         for (int w = blockIdx.x; w < total; w += gridDim.x) {
             int ti, nt;
-            decode_work(w, args.n_tiles, args.n_ntiles, ti, nt);
+            decode_work(w, args.n_tiles, args.n_ntiles, args.group_m, ti, nt);
             const DevTile t = args.tiles[ti];
-            const int n0 = nt * kBN;
+            const int n0 = nt * BNW;
             const bool lora = (t.flags & kTileLora) != 0;
             const bool row_ok = m < t.rows;
             const int row = t.row0 + m;
+            const uint32_t b = it & 1, u = it >> 1;
             if (lora) {
                 mbar_wait(v_full, lora_it & 1);
                 tc_fence_after();
@@ -287,7 +312,7 @@ __global__ void __launch_bounds__(kThreads, 1) smlm_gemm_kernel(const __grid_con
 #pragma unroll
                 for (int c = 0; c < RP; c += 16) {
                     uint32_t tmp[16];
-                    tmem_ld16(v_tmem + lane_base + c, tmp);
+                    tmem_ld16(v_col(b) + lane_base + c, tmp);
                     tmem_wait_ld();
 #pragma unroll
                     for (int j = 0; j < 16; ++j) v[c + j] = tmp[j];
@@ -321,19 +346,25 @@ __global__ void __launch_bounds__(kThreads, 1) smlm_gemm_kernel(const __grid_con
                 mbar_arrive(sv_ready);
                 ++lora_it;
             }
-            mbar_wait(acc_full, it & 1);
+            mbar_wait(acc_full0 + 8 * b, u & 1);
             tc_fence_after();
+            // drain the accumulator top-down in 16-column chunks (the backward's next V lands in
+            // the top columns, released early through vfree)
 #pragma unroll 1
-            for (int c = 0; c < kBN / 32; ++c) {
-                uint32_t r[32];
-                tmem_ld32(acc_tmem + lane_base + 32u * c, r);
+            for (int c = BNW / 16 - 1; c >= 0; --c) {
+                uint32_t r[16];
+                tmem_ld16(acc_col(b) + lane_base + 16u * c, r);
                 tmem_wait_ld();
-                const int col = n0 + 32 * c;
+                if (BWD && c == BNW / 16 - 4) {
+                    tc_fence_before();
+                    mbar_arrive(vfree0 + 8 * b);
+                }
+                const int col = n0 + 16 * c;
                 if (row_ok && col < args.N) {
                     uint4 *dst = reinterpret_cast<uint4 *>(Y + (size_t)row * args.N + col);
                     if (!BWD && !args.has_w) {
 #pragma unroll
-                        for (int q4 = 0; q4 < 4; ++q4) {
+                        for (int q4 = 0; q4 < 2; ++q4) {
                             uint4 old = dst[q4];
                             const __nv_bfloat162 *o2 = reinterpret_cast<const __nv_bfloat162 *>(&old);
                             uint4 pk;
@@ -348,7 +379,7 @@ __global__ void __launch_bounds__(kThreads, 1) smlm_gemm_kernel(const __grid_con
                         }
                     } else {
 #pragma unroll
-                        for (int q4 = 0; q4 < 4; ++q4) {
+                        for (int q4 = 0; q4 < 2; ++q4) {
                             uint4 pk;
                             pk.x = pack_bf16x2(__uint_as_float(r[8 * q4 + 0]), __uint_as_float(r[8 * q4 + 1]));
                             pk.y = pack_bf16x2(__uint_as_float(r[8 * q4 + 2]), __uint_as_float(r[8 * q4 + 3]));
@@ -359,8 +390,12 @@ __global__ void __launch_bounds__(kThreads, 1) smlm_gemm_kernel(const __grid_con
                     }
                 }
             }
+            if (!BWD) {  // keep vfree phases in step for symmetry (unused in the forward)
+                tc_fence_before();
+                mbar_arrive(vfree0 + 8 * b);
+            }
             tc_fence_before();
-            mbar_arrive(acc_empty);
+            mbar_arrive(acc_empty0 + 8 * b);
             ++it;
         }
     }
@@ -604,7 +639,7 @@ int launch_tok_impl(const TokArgs &a, int num_sms, cudaStream_t st) {
 
 // Shared-memory bytes and pipeline depth for a given r_pad.
 int gemm_stages(int r_pad, size_t *smem_bytes) {
-    const size_t stage = kABytes + kBBytes + (size_t)r_pad * 128;
+    const size_t stage = kABytes + kBBytes + (size_t)r_pad * 128;  // backward layout (forward is smaller)
     const size_t fixed = 1024 + (size_t)128 * r_pad * 2 + 256;
     int stages = (int)((232448 - fixed) / stage);
     if (stages > 6) stages = 6;
