@@ -34,6 +34,7 @@ import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
 import synth  # noqa: E402
+from paper_2511_00101_b200.dp import AllReduce, GradBucket  # noqa: E402
 
 METRIC = "SMLM tokens/s at Llama-3-8B r=16 mixed batch; % of HBM/tensor roofline"
 UNIT = "tokens/s"
@@ -150,16 +151,12 @@ class Workload:
                 for a in range(U):
                     assert pool.register(A[a], B[a], 2.0) == a
                 # fine-tune adapters' grads in one flat fp32 bucket per projection (all-reduce unit)
-                nA, nB = r * in_f, out_f * r
-                flat = torch.zeros(len(FT_SLOTS) * (nA + nB), dtype=torch.float32, device=dev)
-                for i, a in enumerate(FT_SLOTS):
-                    dA = flat[i * nA:(i + 1) * nA].view(r, in_f)
-                    dB = flat[len(FT_SLOTS) * nA + i * nB: len(FT_SLOTS) * nA + (i + 1) * nB].view(out_f, r)
-                    pool.set_grad(a, dA, dB)
+                bucket = GradBucket(FT_SLOTS, r, in_f, out_f, dev)
+                bucket.bind(pool)
                 wsf = pool.workspace(self.b, False)
                 wsf = torch.empty_like(wsf)
                 wsb = torch.empty(S.smlm_workspace_size(pool.h, self.b, True) + 256, dtype=torch.uint8, device=dev)
-                layer[p] = dict(W=W, A=A, B=B, pool=pool, grad=flat, wsf=wsf, wsb=wsb)
+                layer[p] = dict(W=W, A=A, B=B, pool=pool, grad=bucket, wsf=wsf, wsb=wsb)
             self.layers.append(layer)
 
     def flops(self):
@@ -281,6 +278,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--dist-backend", default="nccl", help="nccl (production); gloo only to exercise the N>1 "
+                    "path on a single-GPU box")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--oracle-rows", type=int, default=24, help="cpu_baseline sample rows (~20 s)")
     ap.add_argument("--ref-rows", type=int, default=8, help="--impl reference sample rows per step")
@@ -321,10 +320,14 @@ def main():
         return
 
     dist = None
+    local = local % max(torch.cuda.device_count(), 1)
     if world > 1:
         import torch.distributed as dist
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(args.dist_backend)
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
     from paper_2511_00101_b200 import smlm as S
@@ -332,21 +335,16 @@ def main():
     wl = Workload(k, rank, dev)
     stream = torch.cuda.current_stream(dev)
     comm = None
-    comm_stream = None
     if dist is not None:
-        comm_stream = torch.cuda.Stream(dev)
+        allreduce = AllReduce(dist, dev)
 
-        def comm(buf):
-            ev = torch.cuda.Event()
-            ev.record(stream)
-            comm_stream.wait_event(ev)
-            with torch.cuda.stream(comm_stream):
-                dist.all_reduce(buf, op=dist.ReduceOp.SUM)
+        def comm(bucket):
+            allreduce(bucket, stream)
 
     def one_step(i):
         wl.step(i % N_LAYER_SETS, stream, comm)
-        if comm_stream is not None:
-            stream.wait_stream(comm_stream)
+        if comm is not None:
+            allreduce.join(stream)
 
     for i in range(args.warmup):
         one_step(i)
@@ -445,7 +443,7 @@ def run_e2e(wl, stream, steps, n, dist):
     hdY = {p: torch.empty(ft, y.shape[1], dtype=y.dtype).pin_memory() for p, y in wl.dY.items()}
     hY = {p: torch.empty_like(y, device="cpu").pin_memory() for p, y in wl.Y.items()}
     hdX = {p: torch.empty(ft, x.shape[1], dtype=x.dtype).pin_memory() for p, x in wl.dX.items()}
-    hG = {p: torch.empty_like(wl.layers[0][p]["grad"], device="cpu").pin_memory() for p in synth.PROJECTIONS}
+    hG = {p: torch.empty_like(wl.layers[0][p]["grad"].flat, device="cpu").pin_memory() for p in synth.PROJECTIONS}
     for g in hX:
         hX[g].copy_(wl.X[g].cpu())
     for p in hdY:
@@ -470,9 +468,9 @@ def run_e2e(wl, stream, steps, n, dist):
             S.smlm_backward(e["pool"].h, wl.b, wl.X[GROUP_OF[p]], e["W"], wl.dY[p], wl.V[p], wl.dX[p], 0,
                             e["wsb"], stream)
             if dist is not None:
-                dist.all_reduce(e["grad"], op=dist.ReduceOp.SUM)
+                dist.all_reduce(e["grad"].flat, op=dist.ReduceOp.SUM)
             hdX[p].copy_(wl.dX[p][:ft], non_blocking=True)
-            hG[p].copy_(e["grad"], non_blocking=True)
+            hG[p].copy_(e["grad"].flat, non_blocking=True)
 
     e2e_step(0)
     torch.cuda.synchronize()

@@ -1,0 +1,63 @@
+"""Data-parallel plumbing for SMLM (BASELINE.json north_star).
+
+Request batches are independent per GPU; base weights and adapters are replicated; the only
+exchange is a SUM all-reduce of the fine-tune adapters' fp32 dA/dB (PAPER.md P:422 masking: only
+fine-tune adapters carry gradients).  One flat bucket per (layer, projection) holds the dA/dB of
+the fine-tune slots so that a single NCCL call reduces them; on CUDA the call is issued on a
+side stream that waits on an event recorded after the projection's backward, so it overlaps the
+next projection's backward.  Pure plumbing: no SMLM arithmetic lives here.
+"""
+from __future__ import annotations
+
+from typing import Sequence
+
+import torch
+
+
+class GradBucket:
+    """Flat fp32 buffer [ |slots| * r*in  |  |slots| * out*r ] with per-slot dA/dB views."""
+
+    def __init__(self, slots: Sequence[int], r: int, in_f: int, out_f: int, device="cpu"):
+        self.slots = list(slots)
+        self.r, self.in_f, self.out_f = r, in_f, out_f
+        self.nA, self.nB = r * in_f, out_f * r
+        self.flat = torch.zeros(len(self.slots) * (self.nA + self.nB), dtype=torch.float32, device=device)
+
+    def dA(self, i: int) -> torch.Tensor:
+        return self.flat[i * self.nA:(i + 1) * self.nA].view(self.r, self.in_f)
+
+    def dB(self, i: int) -> torch.Tensor:
+        o = len(self.slots) * self.nA
+        return self.flat[o + i * self.nB:o + (i + 1) * self.nB].view(self.out_f, self.r)
+
+    def bind(self, pool):
+        """Bind the views as the pool's gradient buffers of the fine-tune slots."""
+        for i, s in enumerate(self.slots):
+            pool.set_grad(s, self.dA(i), self.dB(i))
+
+
+class AllReduce:
+    """SUM all-reduce of gradient buckets; on CUDA overlapped on a side stream."""
+
+    def __init__(self, dist, device):
+        self.dist = dist
+        self.cuda = torch.device(device).type == "cuda"
+        self.stream = torch.cuda.Stream(device) if self.cuda else None
+
+    def __call__(self, bucket: GradBucket, main_stream=None):
+        if self.dist is None:
+            return
+        if not self.cuda:
+            self.dist.all_reduce(bucket.flat, op=self.dist.ReduceOp.SUM)
+            return
+        main = main_stream or torch.cuda.current_stream(bucket.flat.device)
+        ev = torch.cuda.Event()
+        ev.record(main)
+        self.stream.wait_event(ev)
+        with torch.cuda.stream(self.stream):
+            self.dist.all_reduce(bucket.flat, op=self.dist.ReduceOp.SUM)
+
+    def join(self, main_stream=None):
+        """Make the main stream wait for every issued all-reduce."""
+        if self.cuda and self.dist is not None:
+            (main_stream or torch.cuda.current_stream()).wait_stream(self.stream)
