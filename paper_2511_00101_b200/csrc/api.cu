@@ -37,6 +37,12 @@ template <typename TV>
 int launch_prep_sv(const DevTile *tiles, int n_tiles, const TV *V, int r, int r_pad, __nv_bfloat16 *sVt,
                    cudaStream_t st);
 int launch_tok(const TokArgs &a, int num_sms, cudaStream_t st);
+int dec_stages();
+int dec_chunks(int in_f);
+int launch_shrink_split(const __nv_bfloat16 *X, const SlotDev *slots, const DevBlock *blocks,
+                        const DevShortRow *srows, int n_blocks, int in_f, int r, int r_pad, float *part,
+                        __nv_bfloat16 *Vbd, __nv_bfloat16 *Vsave, cudaStream_t st);
+int launch_dec(const DecArgs &a, int num_sms, cudaStream_t st);
 size_t grad_group_bytes();
 void fill_grad_group(void *dst, int slot, int tile_begin, int n_tiles, float *dA, float *dB);
 template <typename T, typename TV>
@@ -255,6 +261,10 @@ struct WsLayout {
     size_t u_off = 0, u_bytes = 0;         // bwd fp32 mode: U fp32 [S,r]
     size_t sut_off = 0, svt_off = 0, st_bytes = 0;  // bwd bf16: tile-compact s*U, s*V [tiles*128, r_pad]
     size_t vf_off = 0, vf_bytes = 0;       // fp32 V [S,r] (fp32 mode, or bwd recompute)
+    size_t spart_off = 0, spart_bytes = 0; // bf16 fwd: K-split shrink partials
+    size_t dpart_off = 0, dpart_bytes = 0; // bf16 fwd decode GEMM: split-K partials
+    size_t dcnt_off = 0, dcnt_bytes = 0;   // bf16 fwd decode GEMM: split counters
+    int dec_items = 0, dec_ksplit = 0;     // > 0: pure-decode batch takes the transposed split-K kernel
     size_t total = 0;
 };
 
@@ -282,6 +292,31 @@ WsLayout layout_for(smlm_pool p, const smlm_batch *b, const Plan &plan, bool bwd
         L.vbd_off = off;
         L.vbd_bytes = plan.blocks.size() * 128 * (size_t)p->r_pad * 2;
         off = align256(off + L.vbd_bytes);
+        const int nch = dec_chunks(p->in);
+        if (nch > 0) {
+            L.spart_off = off;
+            L.spart_bytes = plan.blocks.size() * (size_t)nch * 128 * p->r_pad * 4;
+            off = align256(off + L.spart_bytes);
+        }
+        // pure decode / short batches (<= 512 rows in <= 4 short tiles): transposed split-K GEMM
+        const int nst = (int)plan.short_tiles.size();
+        if (plan.long_tiles.empty() && nst > 0 && nst <= 4) {
+            const int items = ((p->out + 127) / 128) * ((nst + 1) / 2);
+            if (items <= p->num_sms) {
+                int ks = p->num_sms / items;
+                const int nkb = p->in / 64;
+                if (ks > nkb / 2) ks = nkb / 2 > 0 ? nkb / 2 : 1;
+                if (ks < 1) ks = 1;
+                L.dec_items = items;
+                L.dec_ksplit = ks;
+                L.dpart_off = off;
+                L.dpart_bytes = (size_t)items * ks * 256 * 128 * 4;
+                off = align256(off + L.dpart_bytes);
+                L.dcnt_off = off;
+                L.dcnt_bytes = (size_t)items * 4;
+                off = align256(off + L.dcnt_bytes);
+            }
+        }
     }
     if (bwd && p->dtype == SMLM_FP32) {
         L.u_off = off;
@@ -601,10 +636,46 @@ int smlm_forward(smlm_pool p, const smlm_batch *b, const void *X, const void *W,
 
     if (!plan.blocks.empty()) {
         ProfScope ps(2, st);
-        CKL(launch_shrink_short((const __nv_bfloat16 *)X, p->d_slots, d_blocks, d_srows, (int)plan.blocks.size(),
-                                p->in, p->r, p->r_pad, Vbd, (__nv_bfloat16 *)V_save, st), 1);
+        if (L.spart_bytes) {
+            CKL(launch_shrink_split((const __nv_bfloat16 *)X, p->d_slots, d_blocks, d_srows, (int)plan.blocks.size(),
+                                    p->in, p->r, p->r_pad, reinterpret_cast<float *>(wsb + L.spart_off), Vbd,
+                                    (__nv_bfloat16 *)V_save, st), 2);
+        } else {
+            CKL(launch_shrink_short((const __nv_bfloat16 *)X, p->d_slots, d_blocks, d_srows,
+                                    (int)plan.blocks.size(), p->in, p->r, p->r_pad, Vbd, (__nv_bfloat16 *)V_save,
+                                    st), 1);
+        }
     }
     if (tiles.empty()) return SMLM_OK;
+    if (has_w && L.dec_items > 0) {
+        // pure decode batch: W streamed once at HBM rate by the transposed split-K kernel
+        DecArgs d;
+        memset(&d, 0, sizeof(d));
+        if ((rc = make_map(&d.tmW, W, p->in, p->out, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B))) return rc;
+        if ((rc = make_map(&d.tmX, X, p->in, b->S, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B))) return rc;
+        if (!plan.blocks.empty() &&
+            (rc = make_map(&d.tmV, Vbd, p->r_pad, plan.blocks.size() * 128, p->r_pad, 128,
+                           swizzle_for(p->r_pad * 2))))
+            return rc;
+        d.slots = p->d_slots;
+        d.tiles = d_tiles;  // only short tiles remain (no long tiles in a pure decode batch)
+        d.blocks = d_blocks;
+        d.n_tiles = (int)tiles.size();
+        d.n_groups = (d.n_tiles + 1) / 2;
+        d.n_nt = (p->out + 127) / 128;
+        d.ksplit = L.dec_ksplit;
+        d.K = p->in;
+        d.N = p->out;
+        d.r_pad = p->r_pad;
+        d.stages = dec_stages();
+        d.Y = Y;
+        d.part = reinterpret_cast<float *>(wsb + L.dpart_off);
+        d.counters = reinterpret_cast<int *>(wsb + L.dcnt_off);
+        CK(cudaMemsetAsync(d.counters, 0, L.dcnt_bytes, st));
+        ProfScope ps(0, st);
+        CKL(launch_dec(d, p->num_sms, st), 1);
+        return SMLM_OK;
+    }
     GemmArgs a;
     memset(&a, 0, sizeof(a));
     if ((rc = make_map(&a.tmA, X, p->in, b->S, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B))) return rc;

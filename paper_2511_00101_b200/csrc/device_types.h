@@ -78,4 +78,25 @@ struct TokArgs {
     int stages;
 };
 
+// decode / short-row GEMM (transposed, split K)
+struct DecArgs {
+    CUtensorMap tmW;    // W  [out,in] box {64,128} SW128  (A operand: 128 W rows)
+    CUtensorMap tmX;    // X  [S,in]   box {64,128} SW128  (B operand: decode rows)
+    CUtensorMap tmV;    // block-diagonal s*V [n_blocks*128, r_pad] box {r_pad,128}
+    const SlotDev *slots;
+    const DevTile *tiles;    // the short tiles (<= 4)
+    const DevBlock *blocks;
+    int n_tiles;
+    int n_groups;       // ceil(n_tiles / 2): <= 256 decode rows per MMA
+    int n_nt;           // ceil(out / 128)
+    int ksplit;
+    int K;
+    int N;
+    int r_pad;
+    int stages;
+    void *Y;
+    float *part;        // [n_nt*n_groups][ksplit][256][128] fp32 partials
+    int *counters;      // [n_nt*n_groups], zeroed before the launch
+};
+
 }  // namespace smlm

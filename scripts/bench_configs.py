@@ -1,0 +1,100 @@
+"""Per-config measurements beside the main bench line (BASELINE.json configs[1], configs[2]):
+
+  C2 decode : q,k,v,o forward over 256 one-row decode requests, 32 adapters r=16 (HBM-bound)
+  C3 prefill: gate,up,down forward over 8 prefill segments of 512-2048 rows, 8 adapters r=64
+
+Rotates 8 distinct weight sets so consecutive calls do not hit L2.  Reports per projection the
+device time (CUDA events on the launching stream, median of iterations), the algorithmic bytes /
+flops (SURVEY.md §8(d) rules) and the fraction of the measured HBM / bf16 peak.
+"""
+import json
+import math
+import os
+import statistics
+import sys
+
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import synth  # noqa: E402
+from paper_2511_00101_b200 import smlm as S  # noqa: E402
+
+PEAKS = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+    os.path.join(ROOT, "MEASURED_PEAKS.json")) else {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}
+NSETS = 8
+
+
+def run_config(k, iters=30, graphs=False):
+    spec = synth.CONFIGS[k]
+    dev = torch.device("cuda", 0)
+    batch = synth.config_batch(k)
+    b = S.Batch.from_synth(batch)
+    r, U = spec.rank, spec.n_adapters
+    slots = batch.slots
+    uniq = sorted(set(int(s) for s in slots if s >= 0))
+    out = []
+    g = torch.Generator(device=dev)
+    g.manual_seed(7 + k)
+    total_ms = 0.0
+    for p in spec.projections:
+        in_f, out_f = synth.PROJ_SHAPES[p]
+        X = torch.randn(batch.S, in_f, generator=g, device=dev).to(torch.bfloat16)
+        Y = torch.empty(batch.S, out_f, dtype=torch.bfloat16, device=dev)
+        sets = []
+        for _ in range(NSETS):
+            W = (torch.randn(out_f, in_f, generator=g, device=dev) / math.sqrt(in_f)).to(torch.bfloat16)
+            A = (torch.randn(U, r, in_f, generator=g, device=dev) / math.sqrt(in_f)).to(torch.bfloat16)
+            B = (torch.randn(U, out_f, r, generator=g, device=dev) / (4 * math.sqrt(r))).to(torch.bfloat16)
+            pool = S.Pool(in_f, out_f, r, U, S.SMLM_BF16, 0)
+            for a in range(U):
+                pool.register(A[a], B[a], 2.0)
+            ws = torch.empty(S.smlm_workspace_size(pool.h, b, False) + 256, dtype=torch.uint8, device=dev)
+            sets.append((W, A, B, pool, ws))
+        st = torch.cuda.current_stream()
+
+        def call(i):
+            W, _, _, pool, ws = sets[i % NSETS]
+            S.smlm_forward(pool.h, b, X, W, Y, None, ws, st)
+        for i in range(2 * NSETS):
+            call(i)
+        torch.cuda.synchronize()
+        times = []
+        for i in range(iters):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(st)
+            call(i)
+            e1.record(st)
+            e1.synchronize()
+            times.append(e0.elapsed_time(e1))
+        ms = statistics.median(times)
+        total_ms += ms
+        Sx = batch.S
+        nbytes = in_f * out_f * 2 + len(uniq) * r * (in_f + out_f) * 2 + Sx * (in_f + out_f) * 2
+        lens = [int(batch.offsets[i + 1] - batch.offsets[i]) for i in range(batch.G)]
+        rows_lora = sum(l for l, s in zip(lens, slots) if s >= 0)
+        flops = 2.0 * Sx * in_f * out_f + 2.0 * rows_lora * r * (in_f + out_f)
+        t_hbm = nbytes / (PEAKS["hbm_gbs"] * 1e9) * 1e3
+        t_tc = flops / (PEAKS["bf16_tflops"] * 1e12) * 1e3
+        out.append({"config": spec.name, "proj": p, "S": Sx, "ms": ms, "p10": sorted(times)[len(times) // 10],
+                    "alg_MiB": nbytes / 2**20, "alg_GFLOP": flops / 1e9,
+                    "hbm_GBs": nbytes / ms / 1e6, "hbm_frac": nbytes / ms / 1e6 / PEAKS["hbm_gbs"],
+                    "tflops": flops / ms / 1e9, "tensor_frac": flops / ms / 1e9 / PEAKS["bf16_tflops"],
+                    "roofline_ms": max(t_hbm, t_tc), "roofline_frac": max(t_hbm, t_tc) / ms})
+        for s_ in sets:
+            s_[3].close()
+    return out, total_ms
+
+
+def main():
+    for k in (2, 3):
+        rows, tot = run_config(k)
+        for r in rows:
+            print(json.dumps(r), flush=True)
+        print(json.dumps({"config": synth.CONFIGS[k].name, "total_ms": tot,
+                          "rows_per_s": synth.config_batch(k).S / (tot / 1e3),
+                          "roofline_frac": sum(r["roofline_ms"] for r in rows) / tot}), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -221,3 +221,26 @@ def test_full_config_sampled(k, proj):
             lhsA = float((res.dA[a].double() * w.A[a].double()).sum())
             lhsB = float((res.dB[a].double() * w.B[a].double()).sum())
             assert abs(lhsA - lhsB) <= 2e-2 * (abs(lhsA) + abs(lhsB))
+
+
+@pytest.mark.parametrize("rows,in_f,out_f,r", [(200, 512, 320, 16), (64, 1024, 256, 8), (450, 512, 192, 32),
+                                               (300, 192, 256, 16), (512, 1024, 128, 64)])
+def test_bf16_decode_batches(rows, in_f, out_f, r):
+    """Pure decode batches (the transposed split-K kernel path): one-row DECODE segments, random
+    slots including base-only rows, unsorted."""
+    g = torch.Generator().manual_seed(rows + in_f)
+    slots = torch.randint(-1, 6, (rows,), generator=g).tolist()
+    batch, w, X, dY = synth.random_case(rows * 7 + r, in_f, out_f, r, 6, [1] * rows, [DECODE] * rows, slots)
+    res = run_smlm(batch, w, X, dY, backward=False)
+    assert res.plan_fwd == plan_oracle.forward_plan(batch.offsets, batch.slots, batch.modes)
+    Y, _ = oracle.forward(batch, w.W, w.A, w.B, w.slot_scale, X)
+    assert parity_err(res.Y, Y) <= BF16_TOL
+
+
+def test_bf16_decode_grouped_with_finetune_short_rows():
+    """Short fine-tune segments inside a pure-short batch: V_save and the backward still match."""
+    lengths = [3, 1, 5, 1, 2, 7, 1, 1]
+    modes = [FINETUNE, DECODE, FINETUNE, DECODE, EVAL, FINETUNE, DECODE, PREFILL]
+    batch, w, X, dY = synth.random_case(31, 1024, 384, 16, 4, lengths, modes, [0, 1, 2, 1, 3, 0, -1, 2])
+    res = run_smlm(batch, w, X, dY)
+    _check(res, batch, w, X, dY, BF16_TOL)
