@@ -78,7 +78,8 @@ enum smlm_dtype { SMLM_BF16 = 0, SMLM_FP32 = 1 };
 
 /* Options for smlm_pool_set_option */
 enum smlm_option {
-    SMLM_OPT_L_LONG = 0 /* segments with >= L_long rows take the long (per-segment tile) path; default 64 */
+    SMLM_OPT_L_LONG = 0,  /* segments with >= L_long rows take the long (per-segment tile) path; default 64 */
+    SMLM_OPT_CTA_PAIR = 1 /* 1 (default): forward long tiles on CTA pairs (tcgen05 cta_group::2); 0: one CTA */
 };
 
 /*

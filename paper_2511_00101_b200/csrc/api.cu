@@ -12,6 +12,7 @@
 #include <math.h>
 #include <string.h>
 
+#include <algorithm>
 #include <atomic>
 #include <mutex>
 #include <string>
@@ -24,6 +25,8 @@
 namespace smlm {
 int gemm_stages(int r_pad, size_t *smem_bytes);
 int launch_gemm(const GemmArgs &a, bool bwd, int num_sms, cudaStream_t st);
+int gemm2_stages(int r_pad);
+int launch_gemm2(const Gemm2Args &a, int num_sms, cudaStream_t st);
 int launch_shrink_short(const __nv_bfloat16 *X, const SlotDev *slots, const DevBlock *blocks,
                         const DevShortRow *srows, int n_blocks, int in_f, int r, int r_pad, __nv_bfloat16 *Vbd,
                         __nv_bfloat16 *Vsave, cudaStream_t st);
@@ -225,6 +228,7 @@ struct smlm_pool_s {
     int device = 0;
     int in = 0, out = 0, r = 0, r_pad = 16, cap = 0, dtype = 0;
     int l_long = 64;
+    int cta_pair = 1;   // forward long tiles on CTA pairs (cta_group::2)
     int num_sms = 148;
     std::vector<SlotHost> slots;
     std::vector<uint8_t> ok;
@@ -263,8 +267,8 @@ struct WsLayout {
     size_t vf_off = 0, vf_bytes = 0;       // fp32 V [S,r] (fp32 mode, or bwd recompute)
     size_t spart_off = 0, spart_bytes = 0; // bf16 fwd: K-split shrink partials
     size_t dpart_off = 0, dpart_bytes = 0; // bf16 fwd decode GEMM: split-K partials
-    size_t dcnt_off = 0, dcnt_bytes = 0;   // bf16 fwd decode GEMM: split counters
     int dec_items = 0, dec_ksplit = 0;     // > 0: pure-decode batch takes the transposed split-K kernel
+    std::vector<int> dec_uniq;             // distinct adapter slots of the decode batch
     size_t total = 0;
 };
 
@@ -282,7 +286,10 @@ WsLayout layout_for(smlm_pool p, const smlm_batch *b, const Plan &plan, bool bwd
     size_t off = 0;
     if (!bwd) {
         L.plan_bytes = (plan.long_tiles.size() + plan.short_tiles.size()) * sizeof(DevTile) +
-                       plan.blocks.size() * sizeof(DevBlock) + plan.short_rows.size() * sizeof(DevShortRow);
+                       plan.blocks.size() * sizeof(DevBlock) + plan.short_rows.size() * sizeof(DevShortRow) +
+                       // decode-path extras: distinct slots + per-row records (<= 4 short tiles)
+                       (size_t)p->cap * 4 + 4 * 128 * sizeof(DecRow) + 64 +
+                       plan.long_tiles.size() * sizeof(DevPair) + 16;
     } else {
         L.plan_bytes = plan.bwd_tiles.size() * sizeof(DevTile) + plan.groups.size() * grad_group_bytes();
     }
@@ -301,21 +308,26 @@ WsLayout layout_for(smlm_pool p, const smlm_batch *b, const Plan &plan, bool bwd
         // pure decode / short batches (<= 512 rows in <= 4 short tiles): transposed split-K GEMM
         const int nst = (int)plan.short_tiles.size();
         if (plan.long_tiles.empty() && nst > 0 && nst <= 4) {
-            const int items = ((p->out + 127) / 128) * ((nst + 1) / 2);
-            if (items <= p->num_sms) {
-                int ks = p->num_sms / items;
-                const int nkb = p->in / 64;
-                if (ks > nkb / 2) ks = nkb / 2 > 0 ? nkb / 2 : 1;
-                if (ks < 1) ks = 1;
-                L.dec_items = items;
-                L.dec_ksplit = ks;
-                L.dpart_off = off;
-                L.dpart_bytes = (size_t)items * ks * 256 * 128 * 4;
-                off = align256(off + L.dpart_bytes);
-                L.dcnt_off = off;
-                L.dcnt_bytes = (size_t)items * 4;
-                off = align256(off + L.dcnt_bytes);
-            }
+            std::vector<int> uniq;
+            for (auto &bk : plan.blocks) uniq.push_back(bk.slot);
+            std::sort(uniq.begin(), uniq.end());
+            uniq.erase(std::unique(uniq.begin(), uniq.end()), uniq.end());
+            const int groups = (nst + 1) / 2;
+            const int n_nt = (p->out + 127) / 128;
+            const int n_vt = ((int)uniq.size() * p->r_pad + 127) / 128;
+            const int items = (n_nt + n_vt) * groups;
+            int ks = p->num_sms / items;        // one wave
+            const int nkb = p->in / 64;
+            const int ks_bytes = p->in / 256;   // partials <= ~2x the W bytes
+            if (ks > ks_bytes) ks = ks_bytes;
+            if (ks > nkb / 2) ks = nkb / 2;
+            if (ks < 1) ks = 1;
+            L.dec_items = items;
+            L.dec_ksplit = ks;
+            L.dec_uniq = uniq;
+            L.dpart_off = off;
+            L.dpart_bytes = (size_t)items * ks * 256 * 128 * 4;
+            off = align256(off + L.dpart_bytes);
         }
     }
     if (bwd && p->dtype == SMLM_FP32) {
@@ -479,6 +491,10 @@ int smlm_pool_set_option(smlm_pool p, int option, int value) {
         p->l_long = value;
         return SMLM_OK;
     }
+    if (option == SMLM_OPT_CTA_PAIR) {
+        p->cta_pair = value != 0;
+        return SMLM_OK;
+    }
     return set_err(SMLM_E_INVALID, "unknown option");
 }
 
@@ -622,18 +638,97 @@ int smlm_forward(smlm_pool p, const smlm_batch *b, const void *X, const void *W,
         if (has_w || (t.flags & kTileLora)) tiles.push_back(t);
     for (auto &t : plan.short_tiles)
         if (has_w || t.nblk > 0) tiles.push_back(t);
+    // pairs of long tiles (same segment) for the CTA-pair kernel
+    int n_long_kept = 0;
+    for (auto &t : tiles)
+        if (!(t.flags & kTileShort)) ++n_long_kept;
+    std::vector<DevPair> pairs;
+    if (has_w && p->cta_pair) {
+        for (int i = 0; i < n_long_kept;) {
+            const DevTile &t0 = tiles[i];
+            DevPair pr{};
+            pr.row0 = t0.row0;
+            pr.slot = t0.slot;
+            pr.ft = (t0.flags & kTileFT) ? 1 : 0;
+            pr.scale = t0.scale;
+            int rows = t0.rows;
+            if (i + 1 < n_long_kept && tiles[i + 1].seg == t0.seg) {
+                rows = 128 + tiles[i + 1].rows;
+                i += 2;
+            } else {
+                i += 1;
+            }
+            pr.rows = rows;
+            pairs.push_back(pr);
+        }
+    }
     std::vector<uint8_t> bytes;
     append(bytes, tiles);
     const size_t blk_off = bytes.size();
     append(bytes, plan.blocks);
     const size_t srow_off = bytes.size();
     append(bytes, plan.short_rows);
-    if ((rc = stage_upload(p, bytes, wsb + L.plan_off, st))) return rc;
+    while (bytes.size() % 16) bytes.push_back(0);
+    const size_t pair_off = bytes.size();
+    append(bytes, pairs);
     const DevTile *d_tiles = reinterpret_cast<const DevTile *>(wsb + L.plan_off);
     const DevBlock *d_blocks = reinterpret_cast<const DevBlock *>(wsb + L.plan_off + blk_off);
     const DevShortRow *d_srows = reinterpret_cast<const DevShortRow *>(wsb + L.plan_off + srow_off);
     __nv_bfloat16 *Vbd = reinterpret_cast<__nv_bfloat16 *>(wsb + L.vbd_off);
 
+    if (has_w && L.dec_items > 0) {
+        // pure decode batch: one streaming pass over [W ; A_u] (base rows + rank-r rows of every
+        // adapter in the batch) with split K, then a wide reduce + expand pass
+        const int groups = ((int)tiles.size() + 1) / 2;
+        std::vector<DecRow> drows((size_t)groups * 256, DecRow{-1, -1, 0.f, 0});
+        std::vector<int> uidx_of(p->cap, -1);
+        for (size_t i = 0; i < L.dec_uniq.size(); ++i) uidx_of[L.dec_uniq[i]] = (int)i;
+        for (size_t t = 0; t < tiles.size(); ++t) {
+            const DevTile &tl = tiles[t];
+            for (int m = 0; m < tl.rows; ++m) drows[t * 128 + m] = DecRow{tl.row0 + m, -1, 0.f, 0};
+            for (int bi = 0; bi < tl.nblk; ++bi) {
+                const DevBlock &bk = plan.blocks[tl.blk0 + bi];
+                for (int i = 0; i < bk.nrows; ++i) {
+                    const DevShortRow &sr = plan.short_rows[bk.row_begin + i];
+                    drows[t * 128 + sr.pos] = DecRow{sr.row, uidx_of[bk.slot], sr.scale, sr.ft};
+                }
+            }
+        }
+        std::vector<uint8_t> extra;
+        const size_t vt_off = bytes.size();
+        append(extra, L.dec_uniq);
+        while (extra.size() % 16) extra.push_back(0);
+        const size_t rows_off = vt_off + extra.size();
+        append(extra, drows);
+        bytes.insert(bytes.end(), extra.begin(), extra.end());
+        if ((rc = stage_upload(p, bytes, wsb + L.plan_off, st))) return rc;
+        DecArgs d;
+        memset(&d, 0, sizeof(d));
+        if ((rc = make_map(&d.tmW, W, p->in, p->out, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B))) return rc;
+        if ((rc = make_map(&d.tmX, X, p->in, b->S, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B))) return rc;
+        d.slots = p->d_slots;
+        d.tiles = d_tiles;  // only short tiles (no long tiles in a pure decode batch)
+        d.vt_slots = reinterpret_cast<const int *>(wsb + L.plan_off + vt_off);
+        d.rows = reinterpret_cast<const DecRow *>(wsb + L.plan_off + rows_off);
+        d.n_tiles = (int)tiles.size();
+        d.n_groups = groups;
+        d.n_nt = (p->out + 127) / 128;
+        d.n_uniq = (int)L.dec_uniq.size();
+        d.n_vt = (d.n_uniq * p->r_pad + 127) / 128;
+        d.ksplit = L.dec_ksplit;
+        d.K = p->in;
+        d.N = p->out;
+        d.r = p->r;
+        d.r_pad = p->r_pad;
+        d.stages = dec_stages();
+        d.Y = Y;
+        d.Vsave = V_save;
+        d.part = reinterpret_cast<float *>(wsb + L.dpart_off);
+        ProfScope ps(0, st);
+        CKL(launch_dec(d, p->num_sms, st), 2);
+        return SMLM_OK;
+    }
+    if ((rc = stage_upload(p, bytes, wsb + L.plan_off, st))) return rc;
     if (!plan.blocks.empty()) {
         ProfScope ps(2, st);
         if (L.spart_bytes) {
@@ -647,47 +742,43 @@ int smlm_forward(smlm_pool p, const smlm_batch *b, const void *X, const void *W,
         }
     }
     if (tiles.empty()) return SMLM_OK;
-    if (has_w && L.dec_items > 0) {
-        // pure decode batch: W streamed once at HBM rate by the transposed split-K kernel
-        DecArgs d;
-        memset(&d, 0, sizeof(d));
-        if ((rc = make_map(&d.tmW, W, p->in, p->out, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B))) return rc;
-        if ((rc = make_map(&d.tmX, X, p->in, b->S, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B))) return rc;
-        if (!plan.blocks.empty() &&
-            (rc = make_map(&d.tmV, Vbd, p->r_pad, plan.blocks.size() * 128, p->r_pad, 128,
-                           swizzle_for(p->r_pad * 2))))
-            return rc;
-        d.slots = p->d_slots;
-        d.tiles = d_tiles;  // only short tiles remain (no long tiles in a pure decode batch)
-        d.blocks = d_blocks;
-        d.n_tiles = (int)tiles.size();
-        d.n_groups = (d.n_tiles + 1) / 2;
-        d.n_nt = (p->out + 127) / 128;
-        d.ksplit = L.dec_ksplit;
-        d.K = p->in;
-        d.N = p->out;
-        d.r_pad = p->r_pad;
-        d.stages = dec_stages();
-        d.Y = Y;
-        d.part = reinterpret_cast<float *>(wsb + L.dpart_off);
-        d.counters = reinterpret_cast<int *>(wsb + L.dcnt_off);
-        CK(cudaMemsetAsync(d.counters, 0, L.dcnt_bytes, st));
+    const int bnw = kBN - p->r_pad;
+    // long tiles on CTA pairs: consecutive tiles of one segment (same adapter) share one M=256 MMA
+    int first_1cta = 0;  // tiles[first_1cta ..] go to the 1-CTA kernel
+    if (has_w && p->cta_pair && !pairs.empty()) {
+        Gemm2Args g2;
+        memset(&g2, 0, sizeof(g2));
+        if ((rc = make_map(&g2.tmX, X, p->in, b->S, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B))) return rc;
+        if ((rc = make_map(&g2.tmW0, W, p->in, p->out, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B))) return rc;
+        if ((rc = make_map(&g2.tmW1, W, p->in, p->out, 64, bnw - 128, CU_TENSOR_MAP_SWIZZLE_128B))) return rc;
+        g2.slots = p->d_slots;
+        g2.pairs = reinterpret_cast<const DevPair *>(wsb + L.plan_off + pair_off);
+        g2.n_pairs = (int)pairs.size();
+        g2.n_ntiles = (p->out + bnw - 1) / bnw;
+        g2.group_m = (raster_group(p->in) + 1) / 2;
+        g2.K = p->in;
+        g2.N = p->out;
+        g2.r = p->r;
+        g2.r_pad = p->r_pad;
+        g2.stages = gemm2_stages(p->r_pad);
+        g2.Y = Y;
+        g2.Vsave = V_save;
         ProfScope ps(0, st);
-        CKL(launch_dec(d, p->num_sms, st), 1);
-        return SMLM_OK;
+        CKL(launch_gemm2(g2, p->num_sms, st), 1);
+        first_1cta = n_long_kept;
     }
+    if ((int)tiles.size() == first_1cta) return SMLM_OK;
     GemmArgs a;
     memset(&a, 0, sizeof(a));
     if ((rc = make_map(&a.tmA, X, p->in, b->S, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B))) return rc;
-    const int bnw = kBN - p->r_pad;
     if (has_w && (rc = make_map(&a.tmB, W, p->in, p->out, 64, bnw, CU_TENSOR_MAP_SWIZZLE_128B))) return rc;
     if (!plan.blocks.empty() &&
         (rc = make_map(&a.tmV, Vbd, p->r_pad, plan.blocks.size() * 128, p->r_pad, 128, swizzle_for(p->r_pad * 2))))
         return rc;
     a.slots = p->d_slots;
-    a.tiles = d_tiles;
+    a.tiles = d_tiles + first_1cta;
     a.blocks = d_blocks;
-    a.n_tiles = (int)tiles.size();
+    a.n_tiles = (int)tiles.size() - first_1cta;
     a.K = p->in;
     a.N = p->out;
     a.n_ntiles = (p->out + bnw - 1) / bnw;

@@ -49,6 +49,34 @@ struct GemmArgs {
     int S;
 };
 
+// a pair of 128-row tiles of one segment processed by a CTA pair (cta_group::2)
+struct alignas(16) DevPair {
+    int row0;     // first row of the pair (CTA 0: [row0, row0+128), CTA 1: [row0+128, row0+256))
+    int rows;     // valid rows of the pair (<= 256; past a segment end rows are masked)
+    int slot;     // adapter or -1
+    int ft;       // FINETUNE segment (V_save)
+    float scale;
+    int pad[3];
+};
+
+struct Gemm2Args {
+    CUtensorMap tmX;    // X [S,in] box {64,128} SW128
+    CUtensorMap tmW0;   // W [out,in] box {64,128}           (CTA 0's half of the B tile)
+    CUtensorMap tmW1;   // W [out,in] box {64,256-r_pad-128} (CTA 1's W rows; A_a stacked below)
+    const SlotDev *slots;
+    const DevPair *pairs;
+    int n_pairs;
+    int n_ntiles;
+    int group_m;
+    int K;
+    int N;
+    int r;
+    int r_pad;
+    int stages;
+    void *Y;
+    void *Vsave;
+};
+
 // backward: one adapter with fine-tune rows and bound gradient buffers (PAPER.md P:422 masking)
 struct GradGroup {
     int slot;
@@ -78,25 +106,34 @@ struct TokArgs {
     int stages;
 };
 
-// decode / short-row GEMM (transposed, split K)
+// decode / short-row GEMM (transposed, split K over the stacked rows [W ; A_u of the batch])
+struct DecRow {        // one decode row, indexed by group*256 + m (m = position in the group)
+    int row;           // batch row, -1 for padding
+    int uidx;          // index of its adapter in vt_slots, -1 = base only
+    float scale;       // effective s
+    int ft;            // FINETUNE row (V_save)
+};
 struct DecArgs {
-    CUtensorMap tmW;    // W  [out,in] box {64,128} SW128  (A operand: 128 W rows)
-    CUtensorMap tmX;    // X  [S,in]   box {64,128} SW128  (B operand: decode rows)
-    CUtensorMap tmV;    // block-diagonal s*V [n_blocks*128, r_pad] box {r_pad,128}
+    CUtensorMap tmW;    // W [out,in] box {64,128} SW128 (A operand: 128 W rows)
+    CUtensorMap tmX;    // X [S,in]   box {64,128} SW128 (B operand: decode rows)
     const SlotDev *slots;
     const DevTile *tiles;    // the short tiles (<= 4)
-    const DevBlock *blocks;
+    const int *vt_slots;     // distinct adapter slots of the batch, ascending
+    const DecRow *rows;      // [n_groups*256]
     int n_tiles;
     int n_groups;       // ceil(n_tiles / 2): <= 256 decode rows per MMA
-    int n_nt;           // ceil(out / 128)
+    int n_nt;           // ceil(out / 128) W row tiles
+    int n_vt;           // ceil(n_uniq * r_pad / 128) stacked-adapter row tiles
+    int n_uniq;
     int ksplit;
     int K;
     int N;
+    int r;
     int r_pad;
     int stages;
     void *Y;
-    float *part;        // [n_nt*n_groups][ksplit][256][128] fp32 partials
-    int *counters;      // [n_nt*n_groups], zeroed before the launch
+    void *Vsave;
+    float *part;        // [(n_nt+n_vt)*n_groups][ksplit][256][128] fp32 partials
 };
 
 }  // namespace smlm

@@ -46,6 +46,11 @@ __device__ __forceinline__ void bf16x8_f32(const uint4 &u, float (&f)[8]) {
 // The decomposition depends only on `in`, so a row's V never depends on its batch position.
 // ------------------------------------------------------------------------------------------
 constexpr int kChunk = 512;
+constexpr int kRowsPerPass = 32;
+
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
+}
 
 template <int RP>
 __global__ void __launch_bounds__(256) shrink_partial_kernel(const __nv_bfloat16 *__restrict__ X,
@@ -53,88 +58,110 @@ __global__ void __launch_bounds__(256) shrink_partial_kernel(const __nv_bfloat16
                                                              const DevBlock *__restrict__ blocks,
                                                              const DevShortRow *__restrict__ srows, int in_f,
                                                              int r, float *__restrict__ part) {
+    // A_u[:, chunk] and the block's x rows [:, chunk] are staged in shared memory with coalesced
+    // 128-bit loads (every byte read once); then warp w computes outputs (i, j) = w, w+8, ...:
+    // lane l reduces columns [16 l, 16 l + 16) and a xor-shuffle tree finishes.
+    extern __shared__ __align__(16) uint8_t sm[];
+    __nv_bfloat16 *As = reinterpret_cast<__nv_bfloat16 *>(sm);                   // [RP][512]
+    __nv_bfloat16 *Xs = As + RP * kChunk;                                         // [32][512]
     const DevBlock blk = blocks[blockIdx.x];
     const int c = blockIdx.y, nch = gridDim.y;
     const __nv_bfloat16 *A = reinterpret_cast<const __nv_bfloat16 *>(slots[blk.slot].A);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int k = c * kChunk + 16 * lane;
+    const int k0 = c * kChunk;
+    for (int e = threadIdx.x; e < r * (kChunk / 8); e += 256) {
+        const int j = e / (kChunk / 8), v = e % (kChunk / 8);
+        cp_async16(reinterpret_cast<uint4 *>(As) + e, reinterpret_cast<const uint4 *>(A + (size_t)j * in_f + k0) + v);
+    }
     float *dst = part + ((size_t)blockIdx.x * nch + c) * 128 * RP;
-    for (int i = warp; i < blk.nrows; i += 8) {
-        const int row = srows[blk.row_begin + i].row;
-        float xf[16];
-        {
-            const uint4 *xp = reinterpret_cast<const uint4 *>(X + (size_t)row * in_f + k);
-            float t[8];
-            bf16x8_f32(__ldg(xp), t);
-#pragma unroll
-            for (int e = 0; e < 8; ++e) xf[e] = t[e];
-            bf16x8_f32(__ldg(xp + 1), t);
-#pragma unroll
-            for (int e = 0; e < 8; ++e) xf[8 + e] = t[e];
+    for (int rb = 0; rb < blk.nrows; rb += kRowsPerPass) {
+        const int nr = min(kRowsPerPass, blk.nrows - rb);
+        __syncthreads();
+        for (int e = threadIdx.x; e < nr * (kChunk / 8); e += 256) {
+            const int i = e / (kChunk / 8), v = e % (kChunk / 8);
+            const int row = srows[blk.row_begin + rb + i].row;
+            cp_async16(reinterpret_cast<uint4 *>(Xs) + e, reinterpret_cast<const uint4 *>(X + (size_t)row * in_f + k0) + v);
         }
-#pragma unroll 4
-        for (int j = 0; j < r; ++j) {
-            const uint4 *ap = reinterpret_cast<const uint4 *>(A + (size_t)j * in_f + k);
-            float a0[8], a1[8];
-            bf16x8_f32(__ldg(ap), a0);
-            bf16x8_f32(__ldg(ap + 1), a1);
+        asm volatile("cp.async.wait_all;" ::: "memory");
+        __syncthreads();
+        for (int o = warp; o < nr * r; o += 8) {
+            const int i = o / r, j = o % r;
+            const uint4 *ap = reinterpret_cast<const uint4 *>(As + j * kChunk + 16 * lane);
+            const uint4 *xp = reinterpret_cast<const uint4 *>(Xs + i * kChunk + 16 * lane);
+            float a0[8], a1[8], x0[8], x1[8];
+            bf16x8_f32(ap[0], a0);
+            bf16x8_f32(ap[1], a1);
+            bf16x8_f32(xp[0], x0);
+            bf16x8_f32(xp[1], x1);
             float acc = 0.f;
 #pragma unroll
-            for (int e = 0; e < 8; ++e) acc = fmaf(a0[e], xf[e], acc);
+            for (int e = 0; e < 8; ++e) acc = fmaf(a0[e], x0[e], acc);
 #pragma unroll
-            for (int e = 0; e < 8; ++e) acc = fmaf(a1[e], xf[8 + e], acc);
+            for (int e = 0; e < 8; ++e) acc = fmaf(a1[e], x1[e], acc);
             acc = warp_sum_d(acc);
-            if (lane == 0) dst[i * RP + j] = acc;
+            if (lane == 0) dst[(rb + i) * RP + j] = acc;
         }
     }
 }
 
 // combine partials in chunk order -> block-diagonal s*V (bf16 [128, RP]) and V_save
 template <int RP>
-__global__ void __launch_bounds__(128) shrink_combine_kernel(const DevBlock *__restrict__ blocks,
+__global__ void __launch_bounds__(256) shrink_combine_kernel(const DevBlock *__restrict__ blocks,
                                                              const DevShortRow *__restrict__ srows, int nch,
                                                              int r, const float *__restrict__ part,
                                                              __nv_bfloat16 *__restrict__ Vbd,
                                                              __nv_bfloat16 *__restrict__ Vsave) {
     const DevBlock blk = blocks[blockIdx.x];
     __shared__ int idx_of[128];
-    idx_of[threadIdx.x] = -1;
+    __shared__ float vals[128][RP];
+    for (int i = threadIdx.x; i < 128; i += blockDim.x) idx_of[i] = -1;
     __syncthreads();
     for (int i = threadIdx.x; i < blk.nrows; i += blockDim.x) idx_of[srows[blk.row_begin + i].pos] = i;
-    __syncthreads();
-    const int p = threadIdx.x;  // row position inside the short tile
-    const int i = idx_of[p];
-    __nv_bfloat16 *dst = Vbd + ((size_t)blockIdx.x * 128 + p) * RP;
-    if (i < 0) {
-#pragma unroll
-        for (int j = 0; j < RP; ++j) dst[j] = __float2bfloat16_rn(0.f);
-        return;
-    }
-    const DevShortRow sr = srows[blk.row_begin + i];
-    const float *src = part + (size_t)blockIdx.x * nch * 128 * RP + (size_t)i * RP;
-#pragma unroll
-    for (int j = 0; j < RP; ++j) {
+    const float *src = part + (size_t)blockIdx.x * nch * 128 * RP;
+    for (int e = threadIdx.x; e < blk.nrows * RP; e += blockDim.x) {
+        const int i = e / RP, j = e % RP;
         float v = 0.f;
-        if (j < r)
-            for (int c = 0; c < nch; ++c) v += src[(size_t)c * 128 * RP + j];
-        dst[j] = __float2bfloat16_rn(sr.scale * v);
-        if (Vsave && sr.ft && j < r) Vsave[(size_t)sr.row * r + j] = __float2bfloat16_rn(v);
+        if (j < r) {
+            float t[16];
+#pragma unroll
+            for (int c = 0; c < 16; ++c) t[c] = c < nch ? __ldcg(src + (size_t)c * 128 * RP + i * RP + j) : 0.f;
+            for (int c = 0; c < nch && c < 16; ++c) v += t[c];   // chunk order
+            for (int c = 16; c < nch; ++c) v += __ldcg(src + (size_t)c * 128 * RP + i * RP + j);
+        }
+        vals[i][j] = v;
+    }
+    __syncthreads();
+    __nv_bfloat16 *dst = Vbd + (size_t)blockIdx.x * 128 * RP;
+    for (int e = threadIdx.x; e < 128 * RP; e += blockDim.x) {
+        const int p = e / RP, j = e % RP;
+        const int i = idx_of[p];
+        dst[e] = __float2bfloat16_rn(i < 0 ? 0.f : srows[blk.row_begin + i].scale * vals[i][j]);
+    }
+    if (Vsave) {
+        for (int e = threadIdx.x; e < blk.nrows * r; e += blockDim.x) {
+            const int i = e / r, j = e % r;
+            const DevShortRow sr = srows[blk.row_begin + i];
+            if (sr.ft) Vsave[(size_t)sr.row * r + j] = __float2bfloat16_rn(vals[i][j]);
+        }
     }
 }
 
 // ------------------------------------------------------------------------------------------
-// transposed decode GEMM with split K
+// transposed decode GEMM with split K over the stacked rows [W ; A_stack]
+//   item = (row tile of 128 rows of W or of the stacked A_u of the batch's adapters,
+//           group of <= 256 decode rows, K split)
+//   D[n, m] = sum_{k in split} Rows[n0 + n, k] x_m[k]  -> fp32 partial tile [256 m][128 n]
 // ------------------------------------------------------------------------------------------
 constexpr int kDThreads = 256;
-constexpr uint32_t kDA = 128 * 128;   // W tile 128 rows x 64 k
-constexpr uint32_t kDB = 256 * 128;   // X tiles: up to 256 decode rows x 64 k
+constexpr uint32_t kDA = 128 * 128;   // 128 rows x 64 k
+constexpr uint32_t kDB = 256 * 128;   // up to 256 decode rows x 64 k
 constexpr uint32_t kDStage = kDA + kDB;
 
 __device__ __forceinline__ void dec_item(const DecArgs &a, int w, int &nt, int &grp, int &split) {
     split = w % a.ksplit;
     const int rest = w / a.ksplit;
     grp = rest % a.n_groups;
-    nt = rest / a.n_groups;
+    nt = rest / a.n_groups;   // < n_nt: W rows; >= n_nt: stacked adapter rows
 }
 
 template <int RP>
@@ -143,8 +170,6 @@ __global__ void __launch_bounds__(kDThreads, 1) smlm_dec_kernel(const __grid_con
     const uint32_t raw = smem_u32(smem_raw);
     const uint32_t base = (raw + 1023u) & ~1023u;
     uint8_t *base_ptr = smem_raw + (base - raw);
-    constexpr uint32_t RB = RP * 2;
-    constexpr uint32_t kSwR = RB >= 128 ? kSw128 : (RB == 64 ? kSw64 : kSw32);
     const int ST = args.stages;
     const uint32_t bar = base + ST * kDStage;
     auto full_bar = [&](int s) { return bar + 8u * s; };
@@ -166,15 +191,17 @@ __global__ void __launch_bounds__(kDThreads, 1) smlm_dec_kernel(const __grid_con
         fence_mbar_init();
         tma_prefetch_desc(&args.tmW);
         tma_prefetch_desc(&args.tmX);
-        tma_prefetch_desc(&args.tmV);
     }
     if (warp == 2) tmem_alloc(tmem_slot, 512);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *reinterpret_cast<volatile uint32_t *>(base_ptr + (tmem_slot - base));
-    const int total = args.n_nt * args.n_groups * args.ksplit;
+    // programmatic dependent launch: the reduce grid may start (and park) while this one streams
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    const int total = (args.n_nt + args.n_vt) * args.n_groups * args.ksplit;
     const int nkb = args.K / kBK;
+    constexpr int kAdPerTile = 128 / RP;   // adapters per stacked row tile
 
     auto kb_range = [&](int split, int &kb0, int &kb1) {
         const int q = nkb / args.ksplit, rm = nkb % args.ksplit;
@@ -188,39 +215,29 @@ __global__ void __launch_bounds__(kDThreads, 1) smlm_dec_kernel(const __grid_con
         for (int w = blockIdx.x; w < total; w += gridDim.x) {
             int nt, grp, split;
             dec_item(args, w, nt, grp, split);
-            const int n0 = nt * 128;
             const int t0 = 2 * grp, nt_in = min(2, args.n_tiles - t0);
+            const bool vt = nt >= args.n_nt;
+            const int a0 = (nt - args.n_nt) * kAdPerTile;
+            const int na = vt ? min(kAdPerTile, args.n_uniq - a0) : 0;
             int kb0, kb1;
             kb_range(split, kb0, kb1);
             for (int kb = kb0; kb < kb1; ++kb) {
                 mbar_wait(empty_bar(stage), phase ^ 1);
                 if (lane == 0) {
-                    mbar_expect_tx(full_bar(stage), kDA + 16384u * nt_in);
-                    tma_load_2d(a_addr(stage), &args.tmW, full_bar(stage), kb * kBK, n0);
+                    mbar_expect_tx(full_bar(stage), (vt ? (uint32_t)na * RP * 128u : kDA) + 16384u * nt_in);
+                    if (!vt) {
+                        tma_load_2d(a_addr(stage), &args.tmW, full_bar(stage), kb * kBK, nt * 128);
+                    } else {
+                        for (int i = 0; i < na; ++i)
+                            tma_load_2d(a_addr(stage) + (uint32_t)i * RP * 128u, &args.slots[args.vt_slots[a0 + i]].tmA,
+                                        full_bar(stage), kb * kBK, 0);
+                    }
                     for (int t = 0; t < nt_in; ++t)
                         tma_load_2d(b_addr(stage) + 16384u * t, &args.tmX, full_bar(stage), kb * kBK,
                                     args.tiles[t0 + t].row0);
                 }
                 __syncwarp();
                 if (++stage == ST) { stage = 0; phase ^= 1; }
-            }
-            if (split == 0) {
-                for (int t = 0; t < nt_in; ++t) {
-                    const DevTile tl = args.tiles[t0 + t];
-                    for (int bi = 0; bi < tl.nblk; ++bi) {
-                        const DevBlock blk = args.blocks[tl.blk0 + bi];
-                        const SlotDev *sd = args.slots + blk.slot;
-                        mbar_wait(empty_bar(stage), phase ^ 1);
-                        if (lane == 0) {
-                            mbar_expect_tx(full_bar(stage), 256u * RB);
-                            tma_load_2d(a_addr(stage), &sd->tmBk, full_bar(stage), 0, n0);
-                            tma_load_2d(a_addr(stage) + 64u * RB, &sd->tmBk, full_bar(stage), 0, n0 + 64);
-                            tma_load_2d(b_addr(stage), &args.tmV, full_bar(stage), 0, (tl.blk0 + bi) * 128);
-                        }
-                        __syncwarp();
-                        if (++stage == ST) { stage = 0; phase ^= 1; }
-                    }
-                }
             }
         }
     } else if (warp == 1) {
@@ -232,7 +249,7 @@ __global__ void __launch_bounds__(kDThreads, 1) smlm_dec_kernel(const __grid_con
         for (int w = blockIdx.x; w < total; w += gridDim.x) {
             int nt, grp, split;
             dec_item(args, w, nt, grp, split);
-            const int t0 = 2 * grp, nt_in = min(2, args.n_tiles - t0);
+            const int nt_in = min(2, args.n_tiles - 2 * grp);
             int kb0, kb1;
             kb_range(split, kb0, kb1);
             const uint32_t b = it & 1, u = it >> 1;
@@ -257,47 +274,25 @@ __global__ void __launch_bounds__(kDThreads, 1) smlm_dec_kernel(const __grid_con
                 __syncwarp();
                 if (++stage == ST) { stage = 0; phase ^= 1; }
             }
-            if (split == 0) {
-                for (int t = 0; t < nt_in; ++t) {
-                    const DevTile tl = args.tiles[t0 + t];
-                    for (int bi = 0; bi < tl.nblk; ++bi) {
-                        mbar_wait(full_bar(stage), phase);
-                        tc_fence_after();
-                        if (lane == 0) {
-                            const uint32_t ab = a_addr(stage), bb = b_addr(stage);
-#pragma unroll
-                            for (int kk = 0; kk < RP / 16; ++kk)
-                                mma_bf16(acc + 128u * t, smem_desc(ab + 32u * kk, 16, 8u * RB, kSwR),
-                                         smem_desc(bb + 32u * kk, 16, 8u * RB, kSwR), idesc128, 1);
-                            mma_commit(empty_bar(stage));
-                        }
-                        __syncwarp();
-                        if (++stage == ST) { stage = 0; phase ^= 1; }
-                    }
-                }
-            }
             if (lane == 0) mma_commit(accf0 + 8 * b);
             __syncwarp();
             ++it;
         }
     } else if (warp >= 4) {
         const int q = warp - 4;
-        const int n = q * 32 + lane;               // W row inside the n-tile (TMEM lane)
+        const int n = q * 32 + lane;               // row inside the row tile (TMEM lane)
         const uint32_t lane_base = (uint32_t)(q * 32) << 16;
-        __nv_bfloat16 *Y = reinterpret_cast<__nv_bfloat16 *>(args.Y);
         uint32_t it = 0;
         for (int w = blockIdx.x; w < total; w += gridDim.x) {
             int nt, grp, split;
             dec_item(args, w, nt, grp, split);
-            const int n0 = nt * 128;
-            const int t0 = 2 * grp, nt_in = min(2, args.n_tiles - t0);
+            const int nt_in = min(2, args.n_tiles - 2 * grp);
             const int pair = nt * args.n_groups + grp;
             const uint32_t b = it & 1, u = it >> 1;
             mbar_wait(accf0 + 8 * b, u & 1);
             tc_fence_after();
             float *mypart = args.part + ((size_t)pair * args.ksplit + split) * 256 * 128;
-            const int ncol = 128 * nt_in;
-            for (int c = 0; c < ncol; c += 32) {
+            for (int c = 0; c < 128 * nt_in; c += 32) {
                 uint32_t rr[32];
                 tmem_ld32(tmem_base + 256u * b + lane_base + c, rr);
                 tmem_wait_ld();
@@ -305,36 +300,7 @@ __global__ void __launch_bounds__(kDThreads, 1) smlm_dec_kernel(const __grid_con
                 for (int j = 0; j < 32; ++j) mypart[(size_t)(c + j) * 128 + n] = __uint_as_float(rr[j]);
             }
             tc_fence_before();
-            mbar_arrive(accf0 + 16 + 8 * b);   // TMEM buffer free for the next item
-            // Every split of an item has its own co-resident CTA (grid == items <= #SMs, 1 CTA/SM),
-            // so the splits can wait for each other: once all partials are written, split s sums
-            // rows [s*M/ks, (s+1)*M/ks) over the splits in split order (deterministic).
-            __threadfence();
-            asm volatile("bar.sync 1, 128;" ::: "memory");
-            if (q == 0 && lane == 0) {
-                atomicAdd(args.counters + pair, 1);
-                unsigned v;
-                do {
-                    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(args.counters + pair) : "memory");
-                    if ((int)v < args.ksplit) __nanosleep(32);
-                } while ((int)v < args.ksplit);
-            }
-            asm volatile("bar.sync 1, 128;" ::: "memory");
-            __threadfence();
-            {
-                const float *pp = args.part + (size_t)pair * args.ksplit * 256 * 128;
-                const bool col_ok = n0 + n < args.N;
-                const int mtot = ncol;
-                const int m_lo = split * mtot / args.ksplit, m_hi = (split + 1) * mtot / args.ksplit;
-                for (int m = m_lo; m < m_hi; ++m) {
-                    const int t = m >> 7, mm = m & 127;
-                    const DevTile tl = args.tiles[t0 + t];
-                    if (mm >= tl.rows) continue;
-                    float acc = 0.f;
-                    for (int s2 = 0; s2 < args.ksplit; ++s2) acc += __ldcg(pp + ((size_t)s2 * 256 + m) * 128 + n);
-                    if (col_ok) Y[(size_t)(tl.row0 + mm) * args.N + n0 + n] = __float2bfloat16_rn(acc);
-                }
-            }
+            mbar_arrive(accf0 + 16 + 8 * b);
             ++it;
         }
     }
@@ -343,6 +309,101 @@ __global__ void __launch_bounds__(kDThreads, 1) smlm_dec_kernel(const __grid_con
         tc_fence_after();
         tmem_dealloc(tmem_base, 512);
     }
+}
+
+// ------------------------------------------------------------------------------------------
+// reduce + expand: CTA (W row tile nt, decode-row group, 32-row chunk)
+//   V[m][j]      = sum_s part[stacked tile of (u(m), j)][s][m][.]       (fixed split order)
+//   Y[m][n0+n]   = sum_s part[nt][s][m][n] + s_m * sum_j B_u(m)[n0+n][j] V[m][j]
+// ------------------------------------------------------------------------------------------
+// CTA (W row tile nt, decode-row group, chunk of 8 decode rows); thread = (row, 4 columns)
+template <int RP>
+__global__ void __launch_bounds__(256) dec_reduce_kernel(const __grid_constant__ DecArgs args) {
+    const int nt = blockIdx.x;
+    const int grp = blockIdx.y >> 5, mc = blockIdx.y & 31;
+    __shared__ float Vs[8][RP + 1];
+    __shared__ DecRow rs[8];
+    __shared__ const __nv_bfloat16 *bptr[8];
+    const int ks = args.ksplit;
+    const size_t tile_elems = 256 * 128;
+    if (threadIdx.x < 8) {
+        const DecRow dr = args.rows[grp * 256 + mc * 8 + threadIdx.x];
+        rs[threadIdx.x] = dr;
+        bptr[threadIdx.x] = dr.uidx >= 0 ? reinterpret_cast<const __nv_bfloat16 *>(args.slots[args.vt_slots[dr.uidx]].B)
+                                         : nullptr;
+    }
+    __syncthreads();
+    if (rs[0].row < 0 && rs[7].row < 0 && rs[3].row < 0) {
+        // fully padded chunk (rows are packed from the start of each tile)
+        bool any = false;
+        for (int i = 0; i < 8; ++i) any |= rs[i].row >= 0;
+        if (!any) return;
+    }
+    // wait for the GEMM grid (programmatic dependent launch) before touching its partials
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    for (int e = threadIdx.x; e < 8 * RP; e += 256) {
+        const int ml = e / RP, j = e % RP;
+        const DecRow dr = rs[ml];
+        float v = 0.f;
+        if (dr.row >= 0 && dr.uidx >= 0 && j < args.r) {
+            const int vrow = dr.uidx * RP + j;
+            const int pair = (args.n_nt + vrow / 128) * args.n_groups + grp;
+            const float *pp = args.part + (size_t)pair * ks * tile_elems + (size_t)(mc * 8 + ml) * 128 + (vrow & 127);
+            for (int s0 = 0; s0 < ks; s0 += 8) {
+                float t[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) t[u] = s0 + u < ks ? __ldcg(pp + (size_t)(s0 + u) * tile_elems) : 0.f;
+#pragma unroll
+                for (int u = 0; u < 8; ++u) v += t[u];
+            }
+            if (nt == 0 && dr.ft && args.Vsave)
+                reinterpret_cast<__nv_bfloat16 *>(args.Vsave)[(size_t)dr.row * args.r + j] = __float2bfloat16_rn(v);
+        }
+        Vs[ml][j] = v;
+    }
+    __syncthreads();
+    const int ml = threadIdx.x >> 5;
+    const int nq = 4 * (threadIdx.x & 31);
+    const int n0 = nt * 128;
+    const DecRow dr = rs[ml];
+    if (dr.row < 0 || n0 + nq >= args.N) return;
+    const int pair = nt * args.n_groups + grp;
+    const float *pbase = args.part + (size_t)pair * ks * tile_elems + (size_t)(mc * 8 + ml) * 128 + nq;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int s0 = 0; s0 < ks; s0 += 8) {
+        float4 t[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+            t[u] = s0 + u < ks ? __ldcg(reinterpret_cast<const float4 *>(pbase + (size_t)(s0 + u) * tile_elems))
+                               : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) { acc.x += t[u].x; acc.y += t[u].y; acc.z += t[u].z; acc.w += t[u].w; }
+    }
+    float l[4] = {0.f, 0.f, 0.f, 0.f};
+    const __nv_bfloat16 *B = bptr[ml];
+    if (B) {
+#pragma unroll
+        for (int jg = 0; jg < RP; jg += 8) {
+            if (jg < args.r) {
+                uint4 bu[4];
+#pragma unroll
+                for (int q4 = 0; q4 < 4; ++q4)
+                    bu[q4] = __ldg(reinterpret_cast<const uint4 *>(B + (size_t)(n0 + nq + q4) * args.r + jg));
+#pragma unroll
+                for (int q4 = 0; q4 < 4; ++q4) {
+                    float bf[8];
+                    bf16x8_f32(bu[q4], bf);
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) l[q4] = fmaf(bf[e], Vs[ml][jg + e], l[q4]);
+                }
+            }
+        }
+    }
+    const float sc = B ? dr.scale : 0.f;
+    uint2 pk;
+    pk.x = pack_bf16x2(acc.x + sc * l[0], acc.y + sc * l[1]);
+    pk.y = pack_bf16x2(acc.z + sc * l[2], acc.w + sc * l[3]);
+    *reinterpret_cast<uint2 *>(reinterpret_cast<__nv_bfloat16 *>(args.Y) + (size_t)dr.row * args.N + n0 + nq) = pk;
 }
 
 template <int RP>
@@ -355,10 +416,22 @@ int launch_dec_impl(const DecArgs &a, int num_sms, cudaStream_t st) {
         if (e != cudaSuccess) return (int)e;
         attr_done = true;
     }
-    const int total = a.n_nt * a.n_groups * a.ksplit;
-    if (total > num_sms) return (int)cudaErrorInvalidValue;  // the split handshake needs co-residency
-    kern<<<total, kDThreads, smem, st>>>(a);
-    return (int)cudaGetLastError();
+    const int total = (a.n_nt + a.n_vt) * a.n_groups * a.ksplit;
+    kern<<<total < num_sms ? total : num_sms, kDThreads, smem, st>>>(a);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return (int)e;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(a.n_nt, a.n_groups * 32);
+    cfg.blockDim = dim3(256);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    e = cudaLaunchKernelEx(&cfg, dec_reduce_kernel<RP>, a);
+    return (int)e;
 }
 
 }  // namespace
@@ -375,16 +448,20 @@ int launch_shrink_split(const __nv_bfloat16 *X, const SlotDev *slots, const DevB
     dim3 g1(n_blocks, nch);
     switch (r_pad) {
         case 16:
-            shrink_partial_kernel<16><<<g1, 256, 0, st>>>(X, slots, blocks, srows, in_f, r, part);
-            shrink_combine_kernel<16><<<n_blocks, 128, 0, st>>>(blocks, srows, nch, r, part, Vbd, Vsave);
+            shrink_partial_kernel<16><<<g1, 256, (16 + kRowsPerPass) * kChunk * 2, st>>>(X, slots, blocks, srows, in_f, r, part);
+            shrink_combine_kernel<16><<<n_blocks, 256, 0, st>>>(blocks, srows, nch, r, part, Vbd, Vsave);
             break;
         case 32:
-            shrink_partial_kernel<32><<<g1, 256, 0, st>>>(X, slots, blocks, srows, in_f, r, part);
-            shrink_combine_kernel<32><<<n_blocks, 128, 0, st>>>(blocks, srows, nch, r, part, Vbd, Vsave);
+            cudaFuncSetAttribute(shrink_partial_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (32 + kRowsPerPass) * kChunk * 2);
+            shrink_partial_kernel<32><<<g1, 256, (32 + kRowsPerPass) * kChunk * 2, st>>>(X, slots, blocks, srows, in_f, r, part);
+            shrink_combine_kernel<32><<<n_blocks, 256, 0, st>>>(blocks, srows, nch, r, part, Vbd, Vsave);
             break;
         case 64:
-            shrink_partial_kernel<64><<<g1, 256, 0, st>>>(X, slots, blocks, srows, in_f, r, part);
-            shrink_combine_kernel<64><<<n_blocks, 128, 0, st>>>(blocks, srows, nch, r, part, Vbd, Vsave);
+            cudaFuncSetAttribute(shrink_partial_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (64 + kRowsPerPass) * kChunk * 2);
+            shrink_partial_kernel<64><<<g1, 256, (64 + kRowsPerPass) * kChunk * 2, st>>>(X, slots, blocks, srows, in_f, r, part);
+            shrink_combine_kernel<64><<<n_blocks, 256, 0, st>>>(blocks, srows, nch, r, part, Vbd, Vsave);
             break;
         default: return (int)cudaErrorInvalidValue;
     }

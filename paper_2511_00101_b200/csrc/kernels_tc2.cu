@@ -1,0 +1,354 @@
+// kernels_tc2.cu -- forward SMLM GEMM on CTA pairs (tcgen05 cta_group::2, M = 256).
+//
+// Same math as smlm_gemm_kernel<fwd> (shrink fused into the N=256 MMA by stacking A_a under the
+// W n-tile, expand folded in as an extra K-block, V never leaves the SM pair), but each work
+// item covers TWO 128-row tiles of the same segment (same adapter), one per CTA of a cluster
+// pair.  The pair issues one M=256 MMA per K-step: each CTA stages its own 128 X rows and HALF
+// of the 256-row B tile (W rows [n0, n0+128) in CTA 0; W rows [n0+128, n0+BNW) + A_a in CTA 1),
+// halving the per-SM operand traffic of the 1-CTA kernel; 6 pipeline stages of 32 KB.
+// Only the leader CTA (rank 0) issues MMAs; completions are multicast to both CTAs.
+#include <cuda_runtime.h>
+
+#include "device_types.h"
+#include "sm100.cuh"
+
+namespace smlm {
+using namespace sm100;
+
+namespace {
+
+constexpr int kThreads2 = 256;
+constexpr uint32_t kA2 = 128 * 128;   // own 128 X rows x 64 k
+constexpr uint32_t kB2 = 128 * 128;   // half of the 256 B rows x 64 k
+constexpr uint32_t kStage2 = kA2 + kB2;
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ uint32_t map_to_rank(uint32_t addr, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+__device__ __forceinline__ void cluster_sync() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tma_load_2d_pair(uint32_t dst, const void *map, uint32_t bar_leader, int c0, int c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar_leader)
+        : "memory");
+}
+__device__ __forceinline__ void mma2_bf16(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                          uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+__device__ __forceinline__ void mma2_commit_mc(uint32_t bar) {
+    asm volatile(
+        "{\n\t.reg .b16 m;\n\tmov.b16 m, 3;\n\t"
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], m;\n\t}" ::"r"(bar)
+        : "memory");
+}
+
+__device__ __forceinline__ void decode_pair(int w, int n_pairs, int n_nt, int group_m, int &pi, int &nt) {
+    const int gsz = group_m * n_nt;
+    const int g = w / gsz;
+    const int first = g * group_m;
+    const int gm = min(group_m, n_pairs - first);
+    const int local = w - g * gsz;
+    pi = first + local % gm;
+    nt = local / gm;
+}
+
+template <int RP>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
+    smlm_gemm2_kernel(const __grid_constant__ Gemm2Args args) {
+    extern __shared__ uint8_t smem_raw[];
+    const uint32_t raw = smem_u32(smem_raw);
+    const uint32_t base = (raw + 1023u) & ~1023u;
+    uint8_t *base_ptr = smem_raw + (base - raw);
+    constexpr uint32_t RB = RP * 2;
+    constexpr int BNW = 256 - RP;            // output columns per n-tile
+    constexpr int W1 = BNW - 128;            // W rows staged by CTA 1
+    constexpr uint32_t kSwR = RB >= 128 ? kSw128 : (RB == 64 ? kSw64 : kSw32);
+    const int stages = args.stages;
+    const uint32_t sv_addr = base + stages * kStage2;
+    const uint32_t bar = sv_addr + 128 * RB;
+    auto full_bar = [&](int s) { return bar + 8u * s; };
+    auto empty_bar = [&](int s) { return bar + 8u * (stages + s); };
+    const uint32_t acc_full0 = bar + 16u * stages;
+    const uint32_t acc_empty0 = acc_full0 + 16;
+    const uint32_t v_full = acc_full0 + 32;
+    const uint32_t sv_ready = acc_full0 + 40;
+    const uint32_t tmem_slot = acc_full0 + 48;
+    auto a_addr = [&](int s) { return base + s * kStage2; };
+    auto b_addr = [&](int s) { return base + s * kStage2 + kA2; };
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t rank = cluster_rank();
+    const bool leader = rank == 0;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < stages; ++s) {
+            mbar_init(full_bar(s), 1);
+            mbar_init(empty_bar(s), 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(acc_full0 + 8 * b, 1);
+            mbar_init(acc_empty0 + 8 * b, 256);   // both CTAs' epilogue threads (leader's copy is used)
+        }
+        mbar_init(v_full, 1);
+        mbar_init(sv_ready, 256);
+        fence_mbar_init();
+        tma_prefetch_desc(&args.tmX);
+        tma_prefetch_desc(&args.tmW0);
+        tma_prefetch_desc(&args.tmW1);
+    }
+    if (warp == 2) {
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(tmem_slot), "r"(512)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    }
+    tc_fence_before();
+    cluster_sync();
+    tc_fence_after();
+    const uint32_t tmem_base = *reinterpret_cast<volatile uint32_t *>(base_ptr + (tmem_slot - base));
+    auto acc_col = [&](uint32_t b) { return tmem_base + 256u * b; };
+
+    const int n_clusters = gridDim.x / 2;
+    const int cid = blockIdx.x / 2;
+    const int total = args.n_pairs * args.n_ntiles;
+    const int nkb = args.K / kBK;
+
+    if (warp == 0) {
+        // ========================= TMA producer (both CTAs) =========================
+        int stage = 0;
+        uint32_t phase = 0;
+        auto advance = [&]() {
+            if (++stage == stages) { stage = 0; phase ^= 1; }
+        };
+        for (int w = cid; w < total; w += n_clusters) {
+            int pi, nt;
+            decode_pair(w, args.n_pairs, args.n_ntiles, args.group_m, pi, nt);
+            const DevPair pr = args.pairs[pi];
+            const int n0 = nt * BNW;
+            const bool lora = pr.slot >= 0;
+            const SlotDev *sd = lora ? args.slots + pr.slot : nullptr;
+            const int my_row0 = leader ? pr.row0 : pr.row0 + 128;
+            const uint32_t bytes_pair = 2u * kA2 + 128u * 128u + (uint32_t)W1 * 128u + (lora ? RP * 128u : 0u);
+            for (int kb = 0; kb < nkb; ++kb) {
+                mbar_wait(empty_bar(stage), phase ^ 1);
+                if (lane == 0) {
+                    const uint32_t fb = map_to_rank(full_bar(stage), 0);   // the leader's barrier
+                    if (leader) mbar_expect_tx(full_bar(stage), bytes_pair);
+                    tma_load_2d_pair(a_addr(stage), &args.tmX, fb, kb * kBK, my_row0);
+                    if (leader) {
+                        tma_load_2d_pair(b_addr(stage), &args.tmW0, fb, kb * kBK, n0);
+                    } else {
+                        tma_load_2d_pair(b_addr(stage), &args.tmW1, fb, kb * kBK, n0 + 128);
+                        if (lora) tma_load_2d_pair(b_addr(stage) + W1 * 128u, &sd->tmA, fb, kb * kBK, 0);
+                    }
+                }
+                __syncwarp();
+                advance();
+            }
+            if (lora) {  // expand operand: B_a rows [n0 + 128 rank, +128) x r_pad (two 64-row boxes)
+                mbar_wait(empty_bar(stage), phase ^ 1);
+                if (lane == 0) {
+                    const uint32_t fb = map_to_rank(full_bar(stage), 0);
+                    if (leader) mbar_expect_tx(full_bar(stage), 2u * 128u * RB);
+                    const int rb0 = n0 + 128 * (int)rank;
+                    tma_load_2d_pair(b_addr(stage), &sd->tmBk, fb, 0, rb0);
+                    tma_load_2d_pair(b_addr(stage) + 64u * RB, &sd->tmBk, fb, 0, rb0 + 64);
+                }
+                __syncwarp();
+                advance();
+            }
+        }
+    } else if (warp == 1 && leader) {
+        // ========================= MMA issuer (leader CTA) =========================
+        int stage = 0;
+        uint32_t phase = 0;
+        auto advance = [&]() {
+            if (++stage == stages) { stage = 0; phase ^= 1; }
+        };
+        constexpr uint32_t idesc = idesc_bf16(256, 256, 0, 0);
+        uint32_t it = 0, lora_it = 0;
+        for (int w = cid; w < total; w += n_clusters) {
+            int pi, nt;
+            decode_pair(w, args.n_pairs, args.n_ntiles, args.group_m, pi, nt);
+            const DevPair pr = args.pairs[pi];
+            const bool lora = pr.slot >= 0;
+            const uint32_t b = it & 1, u = it >> 1;
+            const uint32_t acc = acc_col(b);
+            mbar_wait(acc_empty0 + 8 * b, (u & 1) ^ 1);
+            tc_fence_after();
+            for (int kb = 0; kb < nkb; ++kb) {
+                mbar_wait(full_bar(stage), phase);
+                tc_fence_after();
+                if (lane == 0) {
+                    const uint32_t ab = a_addr(stage), bb = b_addr(stage);
+#pragma unroll
+                    for (int k = 0; k < kBK / 16; ++k)
+                        mma2_bf16(acc, smem_desc(ab + 32u * k, 16, 1024, kSw128), smem_desc(bb + 32u * k, 16, 1024, kSw128),
+                                  idesc, (kb | k) != 0);
+                    mma2_commit_mc(empty_bar(stage));
+                }
+                __syncwarp();
+                advance();
+            }
+            if (lora) {
+                if (lane == 0) mma2_commit_mc(v_full);
+                __syncwarp();
+                mbar_wait(full_bar(stage), phase);
+                mbar_wait(sv_ready, lora_it & 1);
+                tc_fence_after();
+                if (lane == 0) {
+                    const uint32_t bb = b_addr(stage);
+#pragma unroll
+                    for (int kk = 0; kk < RP / 16; ++kk)
+                        mma2_bf16(acc, smem_desc(sv_addr + 32u * kk, 16, 8u * RB, kSwR),
+                                  smem_desc(bb + 32u * kk, 16, 8u * RB, kSwR), idesc, 1);
+                    mma2_commit_mc(empty_bar(stage));
+                }
+                __syncwarp();
+                advance();
+                ++lora_it;
+            }
+            if (lane == 0) mma2_commit_mc(acc_full0 + 8 * b);
+            __syncwarp();
+            ++it;
+        }
+    } else if (warp >= 4) {
+        // ========================= epilogue (both CTAs, own 128 rows) =========================
+        const int q = warp - 4;
+        const int m = q * 32 + lane;
+        const uint32_t lane_base = (uint32_t)(q * 32) << 16;
+        const uint32_t sv_ready_l = map_to_rank(sv_ready, 0);
+        const uint32_t acc_empty_l = map_to_rank(acc_empty0, 0);
+        uint32_t it = 0, lora_it = 0;
+        __nv_bfloat16 *Y = reinterpret_cast<__nv_bfloat16 *>(args.Y);
+        for (int w = cid; w < total; w += n_clusters) {
+            int pi, nt;
+            decode_pair(w, args.n_pairs, args.n_ntiles, args.group_m, pi, nt);
+            const DevPair pr = args.pairs[pi];
+            const int n0 = nt * BNW;
+            const bool lora = pr.slot >= 0;
+            const int my_rows = leader ? min(pr.rows, 128) : max(pr.rows - 128, 0);
+            const bool row_ok = m < my_rows;
+            const int row = pr.row0 + 128 * (int)rank + m;
+            const uint32_t b = it & 1, u = it >> 1;
+            if (lora) {
+                mbar_wait(v_full, lora_it & 1);
+                tc_fence_after();
+                uint32_t v[RP];
+#pragma unroll
+                for (int c = 0; c < RP; c += 16) {
+                    uint32_t tmp[16];
+                    tmem_ld16(acc_col(b) + BNW + lane_base + c, tmp);
+                    tmem_wait_ld();
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) v[c + j] = tmp[j];
+                }
+                if (nt == 0 && row_ok && pr.ft && args.Vsave) {
+                    __nv_bfloat16 *vs = reinterpret_cast<__nv_bfloat16 *>(args.Vsave) + (size_t)row * args.r;
+#pragma unroll
+                    for (int j = 0; j < RP; ++j)
+                        if (j < args.r) vs[j] = __float2bfloat16_rn(__uint_as_float(v[j]));
+                }
+                const float s = pr.scale;
+                uint8_t *sv = base_ptr + (sv_addr - base);
+#pragma unroll
+                for (int c = 0; c < RP / 8; ++c) {
+                    uint4 pk;
+                    pk.x = pack_bf16x2(s * __uint_as_float(v[8 * c + 0]), s * __uint_as_float(v[8 * c + 1]));
+                    pk.y = pack_bf16x2(s * __uint_as_float(v[8 * c + 2]), s * __uint_as_float(v[8 * c + 3]));
+                    pk.z = pack_bf16x2(s * __uint_as_float(v[8 * c + 4]), s * __uint_as_float(v[8 * c + 5]));
+                    pk.w = pack_bf16x2(s * __uint_as_float(v[8 * c + 6]), s * __uint_as_float(v[8 * c + 7]));
+                    *reinterpret_cast<uint4 *>(sv + swz((uint32_t)m * RB + 16u * c, RB)) = pk;
+                }
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                tc_fence_before();
+                mbar_arrive_cluster(sv_ready_l);
+                ++lora_it;
+            }
+            mbar_wait(acc_full0 + 8 * b, u & 1);
+            tc_fence_after();
+#pragma unroll 1
+            for (int c = 0; c < BNW / 16; ++c) {
+                uint32_t r[16];
+                tmem_ld16(acc_col(b) + lane_base + 16u * c, r);
+                tmem_wait_ld();
+                const int col = n0 + 16 * c;
+                if (row_ok && col < args.N) {
+                    uint4 *dst = reinterpret_cast<uint4 *>(Y + (size_t)row * args.N + col);
+#pragma unroll
+                    for (int q4 = 0; q4 < 2; ++q4) {
+                        uint4 pk;
+                        pk.x = pack_bf16x2(__uint_as_float(r[8 * q4 + 0]), __uint_as_float(r[8 * q4 + 1]));
+                        pk.y = pack_bf16x2(__uint_as_float(r[8 * q4 + 2]), __uint_as_float(r[8 * q4 + 3]));
+                        pk.z = pack_bf16x2(__uint_as_float(r[8 * q4 + 4]), __uint_as_float(r[8 * q4 + 5]));
+                        pk.w = pack_bf16x2(__uint_as_float(r[8 * q4 + 6]), __uint_as_float(r[8 * q4 + 7]));
+                        dst[q4] = pk;
+                    }
+                }
+            }
+            tc_fence_before();
+            mbar_arrive_cluster(acc_empty_l + 8 * b);
+            ++it;
+        }
+    }
+    tc_fence_before();
+    cluster_sync();
+    if (warp == 2) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(512) : "memory");
+    }
+}
+
+template <int RP>
+int launch2_impl(const Gemm2Args &a, int num_sms, cudaStream_t st) {
+    auto kern = smlm_gemm2_kernel<RP>;
+    const size_t smem = 1024 + (size_t)a.stages * kStage2 + 128 * RP * 2 + 256;
+    static bool attr_done = false;
+    if (!attr_done) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return (int)e;
+        attr_done = true;
+    }
+    const int total = a.n_pairs * a.n_ntiles;
+    int clusters = num_sms / 2;
+    if (total < clusters) clusters = total;
+    kern<<<2 * clusters, kThreads2, smem, st>>>(a);
+    return (int)cudaGetLastError();
+}
+
+}  // namespace
+
+int gemm2_stages(int r_pad) {
+    const size_t fixed = 1024 + (size_t)128 * r_pad * 2 + 256;
+    int s = (int)((232448 - fixed) / kStage2);
+    return s > 8 ? 8 : s;
+}
+
+int launch_gemm2(const Gemm2Args &a, int num_sms, cudaStream_t st) {
+    if (a.n_pairs == 0 || a.n_ntiles == 0) return 0;
+    switch (a.r_pad) {
+        case 16: return launch2_impl<16>(a, num_sms, st);
+        case 32: return launch2_impl<32>(a, num_sms, st);
+        case 64: return launch2_impl<64>(a, num_sms, st);
+    }
+    return (int)cudaErrorInvalidValue;
+}
+
+}  // namespace smlm

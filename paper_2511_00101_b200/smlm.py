@@ -19,7 +19,7 @@ SMLM_OK, SMLM_E_INVALID, SMLM_E_SHAPE, SMLM_E_SLOT, SMLM_E_CAPACITY, SMLM_E_CUDA
     SMLM_E_WORKSPACE = range(8)
 SMLM_FINETUNE, SMLM_EVAL, SMLM_PREFILL, SMLM_DECODE = range(4)
 SMLM_BF16, SMLM_FP32 = 0, 1
-SMLM_OPT_L_LONG = 0
+SMLM_OPT_L_LONG, SMLM_OPT_CTA_PAIR = 0, 1
 PROF_FWD_GEMM, PROF_BWD_GEMM, PROF_SHRINK, PROF_DADB = range(4)
 
 EXPORTED = [

@@ -67,7 +67,19 @@ def run_config(k, iters=30, graphs=False):
             e1.record(st)
             e1.synchronize()
             times.append(e0.elapsed_time(e1))
-        ms = statistics.median(times)
+        ms_sync = statistics.median(times)
+        # back-to-back: GPU time per call when the host stays ahead (events around the loop)
+        import time as _t
+        torch.cuda.synchronize()
+        h0 = _t.perf_counter()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        for i in range(iters):
+            call(i)
+        e1.record(st)
+        host_us = (_t.perf_counter() - h0) / iters * 1e6
+        e1.synchronize()
+        ms = e0.elapsed_time(e1) / iters
         total_ms += ms
         Sx = batch.S
         nbytes = in_f * out_f * 2 + len(uniq) * r * (in_f + out_f) * 2 + Sx * (in_f + out_f) * 2
@@ -76,7 +88,8 @@ def run_config(k, iters=30, graphs=False):
         flops = 2.0 * Sx * in_f * out_f + 2.0 * rows_lora * r * (in_f + out_f)
         t_hbm = nbytes / (PEAKS["hbm_gbs"] * 1e9) * 1e3
         t_tc = flops / (PEAKS["bf16_tflops"] * 1e12) * 1e3
-        out.append({"config": spec.name, "proj": p, "S": Sx, "ms": ms, "p10": sorted(times)[len(times) // 10],
+        out.append({"config": spec.name, "proj": p, "S": Sx, "ms": ms, "ms_isolated_call": ms_sync,
+                    "host_us_per_call": host_us,
                     "alg_MiB": nbytes / 2**20, "alg_GFLOP": flops / 1e9,
                     "hbm_GBs": nbytes / ms / 1e6, "hbm_frac": nbytes / ms / 1e6 / PEAKS["hbm_gbs"],
                     "tflops": flops / ms / 1e9, "tensor_frac": flops / ms / 1e9 / PEAKS["bf16_tflops"],
