@@ -26,7 +26,8 @@ namespace smlm {
 int gemm_stages(int r_pad, size_t *smem_bytes);
 int launch_gemm(const GemmArgs &a, bool bwd, int num_sms, cudaStream_t st);
 int gemm2_stages(int r_pad);
-int launch_gemm2(const Gemm2Args &a, int num_sms, cudaStream_t st);
+int launch_gemm2(const Gemm2Args &a, bool bwd, int num_sms, cudaStream_t st);
+int launch_u(const UArgs &a, int num_sms, cudaStream_t st);
 int launch_shrink_short(const __nv_bfloat16 *X, const SlotDev *slots, const DevBlock *blocks,
                         const DevShortRow *srows, int n_blocks, int in_f, int r, int r_pad, __nv_bfloat16 *Vbd,
                         __nv_bfloat16 *Vsave, cudaStream_t st);
@@ -264,6 +265,8 @@ struct WsLayout {
     size_t vbd_off = 0, vbd_bytes = 0;     // bf16 fwd: block-diagonal s*V of short tiles
     size_t u_off = 0, u_bytes = 0;         // bwd fp32 mode: U fp32 [S,r]
     size_t sut_off = 0, svt_off = 0, st_bytes = 0;  // bwd bf16: tile-compact s*U, s*V [tiles*128, r_pad]
+    size_t upart_off = 0, upart_bytes = 0; // bwd bf16: split-K partials of U = dY B_a
+    int u_items = 0, u_ksplit = 0;
     size_t vf_off = 0, vf_bytes = 0;       // fp32 V [S,r] (fp32 mode, or bwd recompute)
     size_t spart_off = 0, spart_bytes = 0; // bf16 fwd: K-split shrink partials
     size_t dpart_off = 0, dpart_bytes = 0; // bf16 fwd decode GEMM: split-K partials
@@ -291,7 +294,8 @@ WsLayout layout_for(smlm_pool p, const smlm_batch *b, const Plan &plan, bool bwd
                        (size_t)p->cap * 4 + 4 * 128 * sizeof(DecRow) + 64 +
                        plan.long_tiles.size() * sizeof(DevPair) + 16;
     } else {
-        L.plan_bytes = plan.bwd_tiles.size() * sizeof(DevTile) + plan.groups.size() * grad_group_bytes();
+        L.plan_bytes = plan.bwd_tiles.size() * (sizeof(DevTile) + 4 + sizeof(DevPair)) +
+                       plan.groups.size() * grad_group_bytes() + 64;
     }
     L.plan_off = off;
     off = align256(off + L.plan_bytes + 16);
@@ -341,6 +345,18 @@ WsLayout layout_for(smlm_pool p, const smlm_batch *b, const Plan &plan, bool bwd
         off = align256(off + L.st_bytes);
         L.svt_off = off;
         off = align256(off + L.st_bytes);
+        for (auto &t : plan.bwd_tiles)
+            if (t.slot >= 0) ++L.u_items;
+        if (L.u_items) {
+            int ks = p->num_sms / L.u_items;
+            const int nkb = p->out / 64;
+            if (ks > nkb / 4) ks = nkb / 4;
+            if (ks < 1) ks = 1;
+            L.u_ksplit = ks;
+            L.upart_off = off;
+            L.upart_bytes = (size_t)L.u_items * ks * 128 * p->r_pad * 4;
+            off = align256(off + L.upart_bytes);
+        }
     }
     if (need_vf) {
         L.vf_off = off;
@@ -764,7 +780,7 @@ int smlm_forward(smlm_pool p, const smlm_batch *b, const void *X, const void *W,
         g2.Y = Y;
         g2.Vsave = V_save;
         ProfScope ps(0, st);
-        CKL(launch_gemm2(g2, p->num_sms, st), 1);
+        CKL(launch_gemm2(g2, false, p->num_sms, st), 1);
         first_1cta = n_long_kept;
     }
     if ((int)tiles.size() == first_1cta) return SMLM_OK;
@@ -824,13 +840,43 @@ int smlm_backward(smlm_pool p, const smlm_batch *b, const void *X, const void *W
         ++n_grad;
     }
     gbytes.resize(n_grad * grad_group_bytes());
+    std::vector<int> uitems;
+    for (size_t i = 0; i < plan.bwd_tiles.size(); ++i)
+        if (plan.bwd_tiles[i].slot >= 0) uitems.push_back((int)i);
+    // CTA pairs of consecutive fine-tune tiles of one segment (the dX GEMM on cta_group::2)
+    std::vector<DevPair> bpairs;
+    for (size_t i = 0; i < plan.bwd_tiles.size();) {
+        const DevTile &t0 = plan.bwd_tiles[i];
+        DevPair pr{};
+        pr.row0 = t0.row0;
+        pr.slot = t0.slot;
+        pr.ft = 1;
+        pr.scale = t0.scale;
+        pr.tile = (int)i;
+        if (i + 1 < plan.bwd_tiles.size() && plan.bwd_tiles[i + 1].seg == t0.seg) {
+            pr.rows = 128 + plan.bwd_tiles[i + 1].rows;
+            i += 2;
+        } else {
+            pr.rows = t0.rows;
+            i += 1;
+        }
+        bpairs.push_back(pr);
+    }
     std::vector<uint8_t> bytes;
     append(bytes, plan.bwd_tiles);
     const size_t grp_off = bytes.size();
     bytes.insert(bytes.end(), gbytes.begin(), gbytes.end());
+    const size_t uit_off = bytes.size();
+    append(bytes, uitems);
+    while (bytes.size() % 16) bytes.push_back(0);
+    const size_t bpair_off = bytes.size();
+    append(bytes, bpairs);
     if ((rc = stage_upload(p, bytes, wsb + L.plan_off, st))) return rc;
     const DevTile *d_tiles = reinterpret_cast<const DevTile *>(wsb + L.plan_off);
     const void *d_groups = wsb + L.plan_off + grp_off;
+    const int *d_uitems = reinterpret_cast<const int *>(wsb + L.plan_off + uit_off);
+    const DevPair *d_pairs = reinterpret_cast<const DevPair *>(wsb + L.plan_off + bpair_off);
+    const int n_pairs = (int)bpairs.size();
     const int nt = (int)plan.bwd_tiles.size();
     float *Uf = reinterpret_cast<float *>(wsb + L.u_off);
     float *Vf = reinterpret_cast<float *>(wsb + L.vf_off);
@@ -857,32 +903,71 @@ int smlm_backward(smlm_pool p, const smlm_batch *b, const void *X, const void *W
     // ---------------- bf16 path ----------------
     __nv_bfloat16 *sUt = reinterpret_cast<__nv_bfloat16 *>(wsb + L.sut_off);
     __nv_bfloat16 *sVt = reinterpret_cast<__nv_bfloat16 *>(wsb + L.svt_off);
+    // U = dY B_a per fine-tune tile (split-K tensor-core pass) -> tile-compact s*U
+    if (L.u_items && (dX || n_grad)) {
+        UArgs u;
+        memset(&u, 0, sizeof(u));
+        if ((rc = make_map(&u.tmDY, dY, p->out, b->S, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B))) return rc;
+        u.slots = p->d_slots;
+        u.tiles = d_tiles;
+        u.items = d_uitems;
+        u.n_items = L.u_items;
+        u.ksplit = L.u_ksplit;
+        u.K = p->out;
+        u.r_pad = p->r_pad;
+        u.part = reinterpret_cast<float *>(wsb + L.upart_off);
+        u.sUt = sUt;
+        CKL(launch_u(u, p->num_sms, st), 2);
+    }
     if (dX) {
-        GemmArgs a;
-        memset(&a, 0, sizeof(a));
-        if ((rc = make_map(&a.tmA, dY, p->out, b->S, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B))) return rc;
-        if ((rc = make_map(&a.tmB, W, p->in, p->out, 64, 64, CU_TENSOR_MAP_SWIZZLE_128B))) return rc;
-        a.slots = p->d_slots;
-        a.tiles = d_tiles;
-        a.blocks = nullptr;
-        a.n_tiles = nt;
-        a.K = p->out;
-        a.N = p->in;
-        a.n_ntiles = (p->in + kBN - 1) / kBN;
-        a.r = p->r;
-        a.r_pad = p->r_pad;
-        a.stages = gemm_stages(p->r_pad, nullptr);
-        a.group_m = raster_group(p->out);
-        a.has_w = 1;
-        a.Y = dX;
-        a.Vsave = nullptr;
-        a.sUt = n_grad ? sUt : nullptr;
-        a.S = b->S;
         ProfScope ps(1, st);
-        CKL(launch_gemm(a, true, p->num_sms, st), 1);
-    } else if (n_grad) {
-        CKL(launch_rows_u<__nv_bfloat16>(d_tiles, nt, p->d_slots, (const __nv_bfloat16 *)dY, p->out, p->r, nullptr,
-                                         sUt, p->r_pad, st), 1);
+        if (p->cta_pair) {
+            Gemm2Args g2;
+            memset(&g2, 0, sizeof(g2));
+            if ((rc = make_map(&g2.tmX, dY, p->out, b->S, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B))) return rc;
+            if ((rc = make_map(&g2.tmW0, W, p->in, p->out, 64, 64, CU_TENSOR_MAP_SWIZZLE_128B))) return rc;
+            if (L.u_items &&
+                (rc = make_map(&g2.tmU, sUt, p->r_pad, (uint64_t)nt * 128, p->r_pad, 128, swizzle_for(p->r_pad * 2))))
+                return rc;
+            g2.slots = p->d_slots;
+            g2.pairs = d_pairs;
+            g2.n_pairs = n_pairs;
+            g2.n_ntiles = (p->in + kBN - 1) / kBN;
+            g2.group_m = (raster_group(p->out) + 1) / 2;
+            g2.K = p->out;
+            g2.N = p->in;
+            g2.r = p->r;
+            g2.r_pad = p->r_pad;
+            g2.stages = gemm2_stages(p->r_pad);
+            g2.Y = dX;
+            g2.Vsave = nullptr;
+            CKL(launch_gemm2(g2, true, p->num_sms, st), 1);
+        } else {
+            GemmArgs a;
+            memset(&a, 0, sizeof(a));
+            if ((rc = make_map(&a.tmA, dY, p->out, b->S, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B))) return rc;
+            if ((rc = make_map(&a.tmB, W, p->in, p->out, 64, 64, CU_TENSOR_MAP_SWIZZLE_128B))) return rc;
+            if (L.u_items &&
+                (rc = make_map(&a.tmV, sUt, p->r_pad, (uint64_t)nt * 128, p->r_pad, 128, swizzle_for(p->r_pad * 2))))
+                return rc;
+            a.slots = p->d_slots;
+            a.tiles = d_tiles;
+            a.blocks = nullptr;
+            a.n_tiles = nt;
+            a.K = p->out;
+            a.N = p->in;
+            a.n_ntiles = (p->in + kBN - 1) / kBN;
+            a.r = p->r;
+            a.r_pad = p->r_pad;
+            a.stages = gemm_stages(p->r_pad, nullptr);
+            a.group_m = raster_group(p->out);
+            a.has_w = 1;
+            a.Y = dX;
+            a.Vsave = nullptr;
+            a.sUt = nullptr;
+            a.S = b->S;
+            CKL(launch_gemm(a, true, p->num_sms, st), 1);
+        }
     }
     if (n_grad) {
         ProfScope ps(3, st);

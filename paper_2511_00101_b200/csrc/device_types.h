@@ -30,7 +30,7 @@ static_assert(sizeof(SlotDev) % 64 == 0, "SlotDev must keep 64-byte alignment of
 struct GemmArgs {
     CUtensorMap tmA;   // X [S,in] (fwd) or dY [S,out] (bwd): box {64,128} SW128
     CUtensorMap tmB;   // W [out,in]: fwd box {64,256} (K-major); bwd box {64,64} (MN-major)
-    CUtensorMap tmV;   // fwd short tiles: block-diagonal s*V [nblk*128, r_pad], box {r_pad,128}
+    CUtensorMap tmV;   // fwd short tiles: block-diagonal s*V [nblk*128, r_pad]; bwd: tile-compact s*U; box {r_pad,128}
     const SlotDev *slots;
     const DevTile *tiles;
     const DevBlock *blocks;
@@ -56,13 +56,15 @@ struct alignas(16) DevPair {
     int slot;     // adapter or -1
     int ft;       // FINETUNE segment (V_save)
     float scale;
-    int pad[3];
+    int tile;     // backward: index of the pair's first tile in the backward tile list (s*U rows)
+    int pad[2];
 };
 
 struct Gemm2Args {
-    CUtensorMap tmX;    // X [S,in] box {64,128} SW128
-    CUtensorMap tmW0;   // W [out,in] box {64,128}           (CTA 0's half of the B tile)
-    CUtensorMap tmW1;   // W [out,in] box {64,256-r_pad-128} (CTA 1's W rows; A_a stacked below)
+    CUtensorMap tmX;    // fwd: X [S,in] / bwd: dY [S,out]; box {64,128} SW128
+    CUtensorMap tmW0;   // fwd: W box {64,128} (CTA 0's half of B); bwd: W box {64,64} (MN-major)
+    CUtensorMap tmW1;   // fwd: W box {64,256-r_pad-128} (CTA 1's W rows; A_a stacked below)
+    CUtensorMap tmU;    // bwd: tile-compact s*U [n_tiles*128, r_pad] box {r_pad,128}
     const SlotDev *slots;
     const DevPair *pairs;
     int n_pairs;
@@ -85,6 +87,20 @@ struct GradGroup {
     int pad;
     float *dA;       // [r,in] fp32 or NULL
     float *dB;       // [out,r] fp32 or NULL
+};
+
+// U = dY B_a over the fine-tune tiles (backward), split K over out
+struct UArgs {
+    CUtensorMap tmDY;      // dY [S,out] box {64,128} SW128
+    const SlotDev *slots;
+    const DevTile *tiles;  // backward tile list
+    const int *items;      // indices of tiles with an adapter
+    int n_items;
+    int ksplit;
+    int K;                 // out
+    int r_pad;
+    float *part;           // [n_items][ksplit][128][r_pad] fp32
+    void *sUt;             // bf16 [n_tiles*128][r_pad]
 };
 
 // token-contraction GEMM (a5): dA_a^T = X^T (sU) and dB_a = dY^T (sV) over a's fine-tune tiles

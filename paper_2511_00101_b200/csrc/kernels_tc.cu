@@ -53,12 +53,11 @@ __global__ void __launch_bounds__(kThreads, 1) smlm_gemm_kernel(const __grid_con
     // Forward: the shrink is fused into the main MMA.  The B operand of one N=256 MMA is the W
     // n-tile (BNW = 256 - RP rows) stacked on A_a (RP rows), so the accumulator columns
     // [BNW, 256) receive V = X_tile A_a^T while [0, BNW) receive X_tile W^T, and the X tile is
-    // read from shared memory once per K-step.  Backward: dY W needs W as an MN-major operand,
-    // which cannot be stacked with B_a in one swizzle row, so U = dY B_a is a separate N=RP MMA
-    // whose accumulator lives in the top RP columns of the other TMEM buffer.
+    // read from shared memory once per K-step.  Backward: U = dY B_a comes precomputed (tile-compact
+    // s*U from smlm_u_kernel, also needed by the dA contraction) and is TMA-loaded as the A operand
+    // of the expand K-block; the main loop is a plain dY W with W as the MN-major operand.
     constexpr int BNW = BWD ? kBN : kBN - RP;   // output columns per n-tile
-    constexpr uint32_t kAaBytes = BWD ? RP * 128 : 0;
-    constexpr uint32_t kStage = kABytes + kBBytes + kAaBytes;
+    constexpr uint32_t kStage = kABytes + kBBytes;
     constexpr uint32_t kSwR = RB >= 128 ? kSw128 : (RB == 64 ? kSw64 : kSw32);
     const int stages = args.stages;
     const uint32_t sv_addr = base + stages * kStage;
@@ -67,13 +66,11 @@ __global__ void __launch_bounds__(kThreads, 1) smlm_gemm_kernel(const __grid_con
     auto empty_bar = [&](int s) { return bar + 8u * (stages + s); };
     const uint32_t acc_full0 = bar + 16u * stages;   // acc_full[2]
     const uint32_t acc_empty0 = acc_full0 + 16;      // acc_empty[2]
-    const uint32_t vfree0 = acc_full0 + 32;          // vfree[2] (backward)
     const uint32_t v_full = acc_full0 + 48;
     const uint32_t sv_ready = acc_full0 + 56;
     const uint32_t tmem_slot = acc_full0 + 64;
     auto a_addr = [&](int s) { return base + s * kStage; };
     auto b_addr = [&](int s) { return base + s * kStage + kABytes; };
-    auto aa_addr = [&](int s) { return base + s * kStage + kABytes + kBBytes; };
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -86,7 +83,6 @@ __global__ void __launch_bounds__(kThreads, 1) smlm_gemm_kernel(const __grid_con
         for (int b = 0; b < 2; ++b) {
             mbar_init(acc_full0 + 8 * b, 1);
             mbar_init(acc_empty0 + 8 * b, 128);
-            mbar_init(vfree0 + 8 * b, 128);
         }
         mbar_init(v_full, 1);
         mbar_init(sv_ready, 128);
@@ -102,9 +98,7 @@ __global__ void __launch_bounds__(kThreads, 1) smlm_gemm_kernel(const __grid_con
     const uint32_t tmem_base = *reinterpret_cast<volatile uint32_t *>(base_ptr + (tmem_slot - base));
     // two accumulator buffers ACC_b = TMEM columns [256 b, 256 b + 256)
     auto acc_col = [&](uint32_t b) { return tmem_base + 256u * b; };
-    auto v_col = [&](uint32_t b) {
-        return BWD ? tmem_base + 256u * (1u - b) + 256u - RP : tmem_base + 256u * b + BNW;
-    };
+    auto v_col = [&](uint32_t b) { return tmem_base + 256u * b + BNW; };   // forward V columns
 
     const int total = args.n_tiles * args.n_ntiles;
     const int nkb = args.K / kBK;
@@ -138,7 +132,7 @@ __global__ void __launch_bounds__(kThreads, 1) smlm_gemm_kernel(const __grid_con
                                 bytes += BNW * 128u;
                             }
                         }
-                        if (lora) bytes += RP * 128u;
+                        if (lora && !BWD) bytes += RP * 128u;
                         mbar_expect_tx(full_bar(stage), bytes);
                         tma_load_2d(a_addr(stage), &args.tmA, full_bar(stage), kb * kBK, t.row0);
                         if (args.has_w) {
@@ -151,12 +145,8 @@ __global__ void __launch_bounds__(kThreads, 1) smlm_gemm_kernel(const __grid_con
                                 tma_load_2d(b_addr(stage), &args.tmB, full_bar(stage), kb * kBK, n0);
                             }
                         }
-                        if (lora) {
-                            if (BWD)  // B_a rows [kb*64, +64) x r_pad  (MN-major U operand)
-                                tma_load_2d(aa_addr(stage), &sd->tmBk, full_bar(stage), 0, kb * kBK);
-                            else      // A_a [r_pad rows] x 64 k, stacked under the W rows
-                                tma_load_2d(b_addr(stage) + BNW * 128u, &sd->tmA, full_bar(stage), kb * kBK, 0);
-                        }
+                        if (lora && !BWD)  // A_a [r_pad rows] x 64 k, stacked under the W rows
+                            tma_load_2d(b_addr(stage) + BNW * 128u, &sd->tmA, full_bar(stage), kb * kBK, 0);
                     }
                     __syncwarp();
                     advance();
@@ -165,8 +155,9 @@ __global__ void __launch_bounds__(kThreads, 1) smlm_gemm_kernel(const __grid_con
             if (lora) {
                 mbar_wait(empty_bar(stage), phase ^ 1);
                 if (lane == 0) {
-                    if (BWD) {  // A_a [r_pad rows, n0 + 64 i ...] MN-major expand operand
-                        mbar_expect_tx(full_bar(stage), 256u * RB);
+                    if (BWD) {  // s*U rows of the tile (K-major) + A_a [r_pad rows, n0 + 64 i ...] (MN-major)
+                        mbar_expect_tx(full_bar(stage), 256u * RB + 128u * RB);
+                        tma_load_2d(a_addr(stage), &args.tmV, full_bar(stage), 0, ti * 128);
                         for (int i = 0; i < 4; ++i)
                             tma_load_2d(b_addr(stage) + (uint32_t)RP * 128u * i, &sd->tmA, full_bar(stage),
                                         n0 + 64 * i, 0);
@@ -201,7 +192,6 @@ __global__ void __launch_bounds__(kThreads, 1) smlm_gemm_kernel(const __grid_con
         };
         constexpr uint32_t idesc_full = idesc_bf16(128, kBN, 0, BWD ? 1 : 0);   // W (+ stacked A_a)
         constexpr uint32_t idesc_out = idesc_bf16(128, BNW, 0, BWD ? 1 : 0);    // output columns only
-        constexpr uint32_t idesc_v = idesc_bf16(128, RP, 0, 1);                 // backward U
         uint32_t it = 0, lora_it = 0;
         for (int w = blockIdx.x; w < total; w += gridDim.x) {
             int ti, nt;
@@ -212,7 +202,6 @@ __global__ void __launch_bounds__(kThreads, 1) smlm_gemm_kernel(const __grid_con
             const uint32_t b = it & 1, u = it >> 1;
             const uint32_t acc_tmem = acc_col(b), v_tmem = v_col(b);
             mbar_wait(acc_empty0 + 8 * b, (u & 1) ^ 1);
-            if (BWD && lora && it >= 1) mbar_wait(vfree0 + 8 * (1 - b), ((it - 1) >> 1) & 1);
             tc_fence_after();
             uint32_t acc_on = 0;  // 1 once the accumulator holds data
             if (!is_short || args.has_w) {
@@ -220,17 +209,13 @@ __global__ void __launch_bounds__(kThreads, 1) smlm_gemm_kernel(const __grid_con
                     mbar_wait(full_bar(stage), phase);
                     tc_fence_after();
                     if (lane == 0) {
-                        const uint32_t ab = a_addr(stage), bb = b_addr(stage), vb = aa_addr(stage);
+                        const uint32_t ab = a_addr(stage), bb = b_addr(stage);
 #pragma unroll
                         for (int k = 0; k < kBK / 16; ++k) {
                             const uint64_t ad = smem_desc(ab + 32u * k, 16, 1024, kSw128);
                             if (BWD) {
                                 const uint64_t bd = smem_desc(bb + 2048u * k, 8192, 1024, kSw128);
                                 mma_bf16(acc_tmem, ad, bd, idesc_full, (kb | k) != 0);
-                                if (lora) {
-                                    const uint64_t vd = smem_desc(vb + 16u * RB * k, 64u * RB, 8u * RB, kSwR);
-                                    mma_bf16(v_tmem, ad, vd, idesc_v, (kb | k) != 0);
-                                }
                             } else if (args.has_w) {
                                 const uint64_t bd = smem_desc(bb + 32u * k, 16, 1024, kSw128);
                                 mma_bf16(acc_tmem, ad, bd, lora ? idesc_full : idesc_out, (kb | k) != 0);
@@ -248,16 +233,19 @@ __global__ void __launch_bounds__(kThreads, 1) smlm_gemm_kernel(const __grid_con
                 acc_on = args.has_w ? 1u : 0u;
             }
             if (lora) {
-                if (lane == 0) mma_commit(v_full);
-                __syncwarp();
+                if (!BWD) {
+                    if (lane == 0) mma_commit(v_full);
+                    __syncwarp();
+                }
                 mbar_wait(full_bar(stage), phase);
-                mbar_wait(sv_ready, lora_it & 1);
+                if (!BWD) mbar_wait(sv_ready, lora_it & 1);
                 tc_fence_after();
                 if (lane == 0) {
                     const uint32_t bb = b_addr(stage);
+                    const uint32_t aop = BWD ? a_addr(stage) : sv_addr;   // s*U via TMA / s*V from the epilogue
 #pragma unroll
                     for (int kk = 0; kk < RP / 16; ++kk) {
-                        const uint64_t ad = smem_desc(sv_addr + 32u * kk, 16, 8u * RB, kSwR);
+                        const uint64_t ad = smem_desc(aop + 32u * kk, 16, 8u * RB, kSwR);
                         const uint64_t bd = BWD ? smem_desc(bb + 2048u * kk, (uint32_t)RP * 128u, 1024, kSw128)
                                                 : smem_desc(bb + 32u * kk, 16, 8u * RB, kSwR);
                         mma_bf16(acc_tmem, ad, bd, idesc_out, acc_on | (kk != 0));
@@ -305,7 +293,7 @@ __global__ void __launch_bounds__(kThreads, 1) smlm_gemm_kernel(const __grid_con
             const bool row_ok = m < t.rows;
             const int row = t.row0 + m;
             const uint32_t b = it & 1, u = it >> 1;
-            if (lora) {
+            if (lora && !BWD) {
                 mbar_wait(v_full, lora_it & 1);
                 tc_fence_after();
                 uint32_t v[RP];
@@ -325,12 +313,6 @@ __global__ void __launch_bounds__(kThreads, 1) smlm_gemm_kernel(const __grid_con
                 }
                 const float s = t.scale;
                 uint8_t *sv = base_ptr + (sv_addr - base);
-                // backward: n-tile 0 also stores s*U (bf16, tile-compact, zero rows past the segment)
-                // for the token-contraction dA kernel
-                uint4 *su_g = (BWD && nt == 0 && args.sUt)
-                                  ? reinterpret_cast<uint4 *>(reinterpret_cast<__nv_bfloat16 *>(args.sUt) +
-                                                              ((size_t)ti * 128 + m) * RP)
-                                  : nullptr;
 #pragma unroll
                 for (int c = 0; c < RP / 8; ++c) {
                     uint4 pk;
@@ -339,7 +321,6 @@ __global__ void __launch_bounds__(kThreads, 1) smlm_gemm_kernel(const __grid_con
                     pk.z = pack_bf16x2(s * __uint_as_float(v[8 * c + 4]), s * __uint_as_float(v[8 * c + 5]));
                     pk.w = pack_bf16x2(s * __uint_as_float(v[8 * c + 6]), s * __uint_as_float(v[8 * c + 7]));
                     *reinterpret_cast<uint4 *>(sv + swz((uint32_t)m * RB + 16u * c, RB)) = pk;
-                    if (su_g) su_g[c] = row_ok ? pk : make_uint4(0, 0, 0, 0);
                 }
                 fence_proxy_async_smem();
                 tc_fence_before();
@@ -348,17 +329,12 @@ __global__ void __launch_bounds__(kThreads, 1) smlm_gemm_kernel(const __grid_con
             }
             mbar_wait(acc_full0 + 8 * b, u & 1);
             tc_fence_after();
-            // drain the accumulator top-down in 16-column chunks (the backward's next V lands in
-            // the top columns, released early through vfree)
+            // drain the accumulator in 16-column chunks
 #pragma unroll 1
             for (int c = BNW / 16 - 1; c >= 0; --c) {
                 uint32_t r[16];
                 tmem_ld16(acc_col(b) + lane_base + 16u * c, r);
                 tmem_wait_ld();
-                if (BWD && c == BNW / 16 - 4) {
-                    tc_fence_before();
-                    mbar_arrive(vfree0 + 8 * b);
-                }
                 const int col = n0 + 16 * c;
                 if (row_ok && col < args.N) {
                     uint4 *dst = reinterpret_cast<uint4 *>(Y + (size_t)row * args.N + col);
@@ -389,10 +365,6 @@ __global__ void __launch_bounds__(kThreads, 1) smlm_gemm_kernel(const __grid_con
                         }
                     }
                 }
-            }
-            if (!BWD) {  // keep vfree phases in step for symmetry (unused in the forward)
-                tc_fence_before();
-                mbar_arrive(vfree0 + 8 * b);
             }
             tc_fence_before();
             mbar_arrive(acc_empty0 + 8 * b);
@@ -635,16 +607,226 @@ int launch_tok_impl(const TokArgs &a, int num_sms, cudaStream_t st) {
     return (int)cudaGetLastError();
 }
 
+
+// ==========================================================================================
+// U = dY B_a for the fine-tune tiles (backward), split K over `out`:
+//   item = (fine-tune tile with an adapter, K split); D[128 rows x r_pad] on tcgen05 with the dY
+//   tile as the K-major A operand and B_a k-rows as the MN-major B operand; fp32 partials
+//   [tile][split][128][r_pad]; u_reduce sums them in split order and writes the tile-compact
+//   s*U (bf16, zero rows past the segment) consumed by the dX expand and the dA contraction.
+// ==========================================================================================
+constexpr int kUStages = 8;
+
+template <int RP>
+__global__ void __launch_bounds__(kThreads, 1) smlm_u_kernel(const __grid_constant__ UArgs args) {
+    extern __shared__ uint8_t smem_raw[];
+    const uint32_t raw = smem_u32(smem_raw);
+    const uint32_t base = (raw + 1023u) & ~1023u;
+    uint8_t *base_ptr = smem_raw + (base - raw);
+    constexpr uint32_t RB = RP * 2;
+    constexpr uint32_t kSwR = RB >= 128 ? kSw128 : (RB == 64 ? kSw64 : kSw32);
+    constexpr uint32_t kStg = kABytes + ((64 * RB + 1023u) & ~1023u);
+    constexpr int ST = kUStages;
+    const uint32_t bar = base + ST * kStg;
+    auto full_bar = [&](int s) { return bar + 8u * s; };
+    auto empty_bar = [&](int s) { return bar + 8u * (ST + s); };
+    const uint32_t accf0 = bar + 16u * ST;   // acc_full[2], acc_empty[2]
+    const uint32_t tmem_slot = accf0 + 32;
+    auto a_addr = [&](int s) { return base + s * kStg; };
+    auto b_addr = [&](int s) { return base + s * kStg + kABytes; };
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < ST; ++s) {
+            mbar_init(full_bar(s), 1);
+            mbar_init(empty_bar(s), 1);
+        }
+        mbar_init(accf0 + 0, 1);
+        mbar_init(accf0 + 8, 1);
+        mbar_init(accf0 + 16, 128);
+        mbar_init(accf0 + 24, 128);
+        fence_mbar_init();
+        tma_prefetch_desc(&args.tmDY);
+    }
+    if (warp == 2) tmem_alloc(tmem_slot, 128);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *reinterpret_cast<volatile uint32_t *>(base_ptr + (tmem_slot - base));
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    const int total = args.n_items * args.ksplit;
+    const int nkb = args.K / kBK;
+    auto kb_range = [&](int split, int &kb0, int &kb1) {
+        const int q = nkb / args.ksplit, rm = nkb % args.ksplit;
+        kb0 = split * q + min(split, rm);
+        kb1 = kb0 + q + (split < rm ? 1 : 0);
+    };
+    if (warp == 0) {
+        int stage = 0;
+        uint32_t phase = 0;
+        for (int w = blockIdx.x; w < total; w += gridDim.x) {
+            const int item = w / args.ksplit, split = w % args.ksplit;
+            const DevTile t = args.tiles[args.items[item]];
+            const SlotDev *sd = args.slots + t.slot;
+            int kb0, kb1;
+            kb_range(split, kb0, kb1);
+            for (int kb = kb0; kb < kb1; ++kb) {
+                mbar_wait(empty_bar(stage), phase ^ 1);
+                if (lane == 0) {
+                    mbar_expect_tx(full_bar(stage), kABytes + 64u * RB);
+                    tma_load_2d(a_addr(stage), &args.tmDY, full_bar(stage), kb * kBK, t.row0);
+                    tma_load_2d(b_addr(stage), &sd->tmBk, full_bar(stage), 0, kb * kBK);
+                }
+                __syncwarp();
+                if (++stage == ST) { stage = 0; phase ^= 1; }
+            }
+        }
+    } else if (warp == 1) {
+        int stage = 0;
+        uint32_t phase = 0, it = 0;
+        constexpr uint32_t idesc = idesc_bf16(128, RP, 0, 1);
+        for (int w = blockIdx.x; w < total; w += gridDim.x) {
+            const int split = w % args.ksplit;
+            int kb0, kb1;
+            kb_range(split, kb0, kb1);
+            const uint32_t b = it & 1, u = it >> 1;
+            const uint32_t acc = tmem_base + b * RP;
+            mbar_wait(accf0 + 16 + 8 * b, (u & 1) ^ 1);
+            tc_fence_after();
+            uint32_t acc_on = 0;
+            for (int kb = kb0; kb < kb1; ++kb) {
+                mbar_wait(full_bar(stage), phase);
+                tc_fence_after();
+                if (lane == 0) {
+                    const uint32_t ab = a_addr(stage), bb = b_addr(stage);
+#pragma unroll
+                    for (int k = 0; k < kBK / 16; ++k) {
+                        mma_bf16(acc, smem_desc(ab + 32u * k, 16, 1024, kSw128),
+                                 smem_desc(bb + 16u * RB * k, 64u * RB, 8u * RB, kSwR), idesc, acc_on);
+                        acc_on = 1;
+                    }
+                    mma_commit(empty_bar(stage));
+                }
+                __syncwarp();
+                if (++stage == ST) { stage = 0; phase ^= 1; }
+            }
+            if (lane == 0) mma_commit(accf0 + 8 * b);
+            __syncwarp();
+            ++it;
+        }
+    } else if (warp >= 4) {
+        const int q = warp - 4;
+        const int m = q * 32 + lane;
+        const uint32_t lane_base = (uint32_t)(q * 32) << 16;
+        uint32_t it = 0;
+        for (int w = blockIdx.x; w < total; w += gridDim.x) {
+            const int item = w / args.ksplit, split = w % args.ksplit;
+            const uint32_t b = it & 1, u = it >> 1;
+            mbar_wait(accf0 + 8 * b, u & 1);
+            tc_fence_after();
+            float *dst = args.part + (((size_t)item * args.ksplit + split) * 128 + m) * RP;
+#pragma unroll
+            for (int c = 0; c < RP; c += 16) {
+                uint32_t v[16];
+                tmem_ld16(tmem_base + b * RP + lane_base + c, v);
+                tmem_wait_ld();
+#pragma unroll
+                for (int j = 0; j < 16; j += 4)
+                    *reinterpret_cast<float4 *>(dst + c + j) =
+                        make_float4(__uint_as_float(v[j]), __uint_as_float(v[j + 1]), __uint_as_float(v[j + 2]),
+                                    __uint_as_float(v[j + 3]));
+            }
+            tc_fence_before();
+            mbar_arrive(accf0 + 16 + 8 * b);
+            ++it;
+        }
+    }
+    __syncthreads();
+    if (warp == 2) {
+        tc_fence_after();
+        tmem_dealloc(tmem_base, 128);
+    }
+}
+
+// sUt[tile*128 + m][j] = bf16(s * sum_split part) (zero rows past the segment), split order fixed
+template <int RP>
+__global__ void __launch_bounds__(128) u_reduce_kernel(const __grid_constant__ UArgs args) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    const int item = blockIdx.x;
+    const int ti = args.items[item];
+    const DevTile t = args.tiles[ti];
+    const int m = threadIdx.x;
+    uint4 *dst = reinterpret_cast<uint4 *>(reinterpret_cast<__nv_bfloat16 *>(args.sUt) + ((size_t)ti * 128 + m) * RP);
+    float acc[RP];
+#pragma unroll
+    for (int j = 0; j < RP; ++j) acc[j] = 0.f;
+    if (m < t.rows) {
+        for (int s = 0; s < args.ksplit; ++s) {
+            const float4 *src = reinterpret_cast<const float4 *>(args.part + (((size_t)item * args.ksplit + s) * 128 + m) * RP);
+#pragma unroll
+            for (int j4 = 0; j4 < RP / 4; ++j4) {
+                const float4 v = __ldcg(src + j4);
+                acc[4 * j4] += v.x; acc[4 * j4 + 1] += v.y; acc[4 * j4 + 2] += v.z; acc[4 * j4 + 3] += v.w;
+            }
+        }
+    }
+#pragma unroll
+    for (int c = 0; c < RP / 8; ++c) {
+        uint4 pk;
+        pk.x = pack_bf16x2(t.scale * acc[8 * c + 0], t.scale * acc[8 * c + 1]);
+        pk.y = pack_bf16x2(t.scale * acc[8 * c + 2], t.scale * acc[8 * c + 3]);
+        pk.z = pack_bf16x2(t.scale * acc[8 * c + 4], t.scale * acc[8 * c + 5]);
+        pk.w = pack_bf16x2(t.scale * acc[8 * c + 6], t.scale * acc[8 * c + 7]);
+        dst[c] = pk;
+    }
+}
+
+template <int RP>
+int launch_u_impl(const UArgs &a, int num_sms, cudaStream_t st) {
+    auto kern = smlm_u_kernel<RP>;
+    constexpr size_t kStg = 16384 + ((64 * RP * 2 + 1023) & ~1023);
+    const size_t smem = 1024 + kUStages * kStg + 256;
+    static bool attr_done = false;
+    if (!attr_done) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return (int)e;
+        attr_done = true;
+    }
+    const int total = a.n_items * a.ksplit;
+    kern<<<total < num_sms ? total : num_sms, kThreads, smem, st>>>(a);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return (int)e;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(a.n_items);
+    cfg.blockDim = dim3(128);
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return (int)cudaLaunchKernelEx(&cfg, u_reduce_kernel<RP>, a);
+}
+
 }  // namespace
 
 // Shared-memory bytes and pipeline depth for a given r_pad.
 int gemm_stages(int r_pad, size_t *smem_bytes) {
-    const size_t stage = kABytes + kBBytes + (size_t)r_pad * 128;  // backward layout (forward is smaller)
+    const size_t stage = kABytes + kBBytes;
     const size_t fixed = 1024 + (size_t)128 * r_pad * 2 + 256;
     int stages = (int)((232448 - fixed) / stage);
     if (stages > 6) stages = 6;
     if (smem_bytes) *smem_bytes = fixed + stage * stages;
     return stages;
+}
+
+int launch_u(const UArgs &a, int num_sms, cudaStream_t st) {
+    if (a.n_items == 0) return 0;
+    switch (a.r_pad) {
+        case 16: return launch_u_impl<16>(a, num_sms, st);
+        case 32: return launch_u_impl<32>(a, num_sms, st);
+        case 64: return launch_u_impl<64>(a, num_sms, st);
+    }
+    return (int)cudaErrorInvalidValue;
 }
 
 int launch_tok(const TokArgs &a, int num_sms, cudaStream_t st) {

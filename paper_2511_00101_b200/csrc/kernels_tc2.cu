@@ -71,7 +71,7 @@ __device__ __forceinline__ void decode_pair(int w, int n_pairs, int n_nt, int gr
     nt = local / gm;
 }
 
-template <int RP>
+template <bool BWD, int RP>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
     smlm_gemm2_kernel(const __grid_constant__ Gemm2Args args) {
     extern __shared__ uint8_t smem_raw[];
@@ -79,8 +79,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
     const uint32_t base = (raw + 1023u) & ~1023u;
     uint8_t *base_ptr = smem_raw + (base - raw);
     constexpr uint32_t RB = RP * 2;
-    constexpr int BNW = 256 - RP;            // output columns per n-tile
-    constexpr int W1 = BNW - 128;            // W rows staged by CTA 1
+    // forward: n-tile = 256 - RP output columns (A_a stacked under W in CTA 1's half of B);
+    // backward: n-tile = 256 columns of dX, W as the MN-major B operand (two 64-column boxes per CTA)
+    constexpr int BNW = BWD ? 256 : 256 - RP;
+    constexpr int W1 = BWD ? 128 : BNW - 128;
     constexpr uint32_t kSwR = RB >= 128 ? kSw128 : (RB == 64 ? kSw64 : kSw32);
     const int stages = args.stages;
     const uint32_t sv_addr = base + stages * kStage2;
@@ -112,7 +114,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
         fence_mbar_init();
         tma_prefetch_desc(&args.tmX);
         tma_prefetch_desc(&args.tmW0);
-        tma_prefetch_desc(&args.tmW1);
+        if (!BWD) tma_prefetch_desc(&args.tmW1);
     }
     if (warp == 2) {
         asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(tmem_slot), "r"(512)
@@ -145,14 +147,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
             const bool lora = pr.slot >= 0;
             const SlotDev *sd = lora ? args.slots + pr.slot : nullptr;
             const int my_row0 = leader ? pr.row0 : pr.row0 + 128;
-            const uint32_t bytes_pair = 2u * kA2 + 128u * 128u + (uint32_t)W1 * 128u + (lora ? RP * 128u : 0u);
+            // backward: W column boxes past N are skipped (in is a multiple of 64)
+            auto nbox = [&](int rk) {
+                int nb = 0;
+                for (int i = 0; i < 2; ++i) nb += (n0 + 128 * rk + 64 * i < args.N);
+                return nb;
+            };
+            const uint32_t bytes_pair =
+                BWD ? 2u * kA2 + 8192u * (nbox(0) + nbox(1))
+                    : 2u * kA2 + 128u * 128u + (uint32_t)W1 * 128u + (lora ? RP * 128u : 0u);
             for (int kb = 0; kb < nkb; ++kb) {
                 mbar_wait(empty_bar(stage), phase ^ 1);
                 if (lane == 0) {
                     const uint32_t fb = map_to_rank(full_bar(stage), 0);   // the leader's barrier
                     if (leader) mbar_expect_tx(full_bar(stage), bytes_pair);
                     tma_load_2d_pair(a_addr(stage), &args.tmX, fb, kb * kBK, my_row0);
-                    if (leader) {
+                    if (BWD) {
+                        for (int i = 0; i < 2; ++i) {
+                            const int c0 = n0 + 128 * (int)rank + 64 * i;
+                            if (c0 < args.N) tma_load_2d_pair(b_addr(stage) + 8192u * i, &args.tmW0, fb, c0, kb * kBK);
+                        }
+                    } else if (leader) {
                         tma_load_2d_pair(b_addr(stage), &args.tmW0, fb, kb * kBK, n0);
                     } else {
                         tma_load_2d_pair(b_addr(stage), &args.tmW1, fb, kb * kBK, n0 + 128);
@@ -162,14 +177,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
                 __syncwarp();
                 advance();
             }
-            if (lora) {  // expand operand: B_a rows [n0 + 128 rank, +128) x r_pad (two 64-row boxes)
+            if (lora) {
                 mbar_wait(empty_bar(stage), phase ^ 1);
                 if (lane == 0) {
                     const uint32_t fb = map_to_rank(full_bar(stage), 0);
-                    if (leader) mbar_expect_tx(full_bar(stage), 2u * 128u * RB);
-                    const int rb0 = n0 + 128 * (int)rank;
-                    tma_load_2d_pair(b_addr(stage), &sd->tmBk, fb, 0, rb0);
-                    tma_load_2d_pair(b_addr(stage) + 64u * RB, &sd->tmBk, fb, 0, rb0 + 64);
+                    if (BWD) {
+                        // s*U rows of this CTA's tile (K-major) + A_a columns [n0 + 128 rank, +128) (MN-major)
+                        if (leader) mbar_expect_tx(full_bar(stage), 2u * 256u * RB);
+                        tma_load_2d_pair(a_addr(stage), &args.tmU, fb, 0, (pr.tile + (int)rank) * 128);
+                        for (int i = 0; i < 2; ++i)
+                            tma_load_2d_pair(b_addr(stage) + (uint32_t)i * RP * 128u, &sd->tmA, fb,
+                                             n0 + 128 * (int)rank + 64 * i, 0);
+                    } else {
+                        // B_a rows [n0 + 128 rank, +128) x r_pad (two 64-row boxes)
+                        if (leader) mbar_expect_tx(full_bar(stage), 2u * 128u * RB);
+                        const int rb0 = n0 + 128 * (int)rank;
+                        tma_load_2d_pair(b_addr(stage), &sd->tmBk, fb, 0, rb0);
+                        tma_load_2d_pair(b_addr(stage) + 64u * RB, &sd->tmBk, fb, 0, rb0 + 64);
+                    }
                 }
                 __syncwarp();
                 advance();
@@ -182,7 +207,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
         auto advance = [&]() {
             if (++stage == stages) { stage = 0; phase ^= 1; }
         };
-        constexpr uint32_t idesc = idesc_bf16(256, 256, 0, 0);
+        constexpr uint32_t idesc = idesc_bf16(256, 256, 0, BWD ? 1 : 0);
         uint32_t it = 0, lora_it = 0;
         for (int w = cid; w < total; w += n_clusters) {
             int pi, nt;
@@ -200,7 +225,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
                     const uint32_t ab = a_addr(stage), bb = b_addr(stage);
 #pragma unroll
                     for (int k = 0; k < kBK / 16; ++k)
-                        mma2_bf16(acc, smem_desc(ab + 32u * k, 16, 1024, kSw128), smem_desc(bb + 32u * k, 16, 1024, kSw128),
+                        mma2_bf16(acc, smem_desc(ab + 32u * k, 16, 1024, kSw128),
+                                  BWD ? smem_desc(bb + 2048u * k, 8192, 1024, kSw128)
+                                      : smem_desc(bb + 32u * k, 16, 1024, kSw128),
                                   idesc, (kb | k) != 0);
                     mma2_commit_mc(empty_bar(stage));
                 }
@@ -208,17 +235,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
                 advance();
             }
             if (lora) {
-                if (lane == 0) mma2_commit_mc(v_full);
-                __syncwarp();
+                if (!BWD) {
+                    if (lane == 0) mma2_commit_mc(v_full);
+                    __syncwarp();
+                }
                 mbar_wait(full_bar(stage), phase);
-                mbar_wait(sv_ready, lora_it & 1);
+                if (!BWD) mbar_wait(sv_ready, lora_it & 1);
                 tc_fence_after();
                 if (lane == 0) {
                     const uint32_t bb = b_addr(stage);
+                    const uint32_t aop = BWD ? a_addr(stage) : sv_addr;
 #pragma unroll
                     for (int kk = 0; kk < RP / 16; ++kk)
-                        mma2_bf16(acc, smem_desc(sv_addr + 32u * kk, 16, 8u * RB, kSwR),
-                                  smem_desc(bb + 32u * kk, 16, 8u * RB, kSwR), idesc, 1);
+                        mma2_bf16(acc, smem_desc(aop + 32u * kk, 16, 8u * RB, kSwR),
+                                  BWD ? smem_desc(bb + 2048u * kk, (uint32_t)RP * 128u, 1024, kSw128)
+                                      : smem_desc(bb + 32u * kk, 16, 8u * RB, kSwR),
+                                  idesc, 1);
                     mma2_commit_mc(empty_bar(stage));
                 }
                 __syncwarp();
@@ -248,7 +280,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
             const bool row_ok = m < my_rows;
             const int row = pr.row0 + 128 * (int)rank + m;
             const uint32_t b = it & 1, u = it >> 1;
-            if (lora) {
+            if (lora && !BWD) {
                 mbar_wait(v_full, lora_it & 1);
                 tc_fence_after();
                 uint32_t v[RP];
@@ -316,9 +348,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
     }
 }
 
-template <int RP>
+template <bool BWD, int RP>
 int launch2_impl(const Gemm2Args &a, int num_sms, cudaStream_t st) {
-    auto kern = smlm_gemm2_kernel<RP>;
+    auto kern = smlm_gemm2_kernel<BWD, RP>;
     const size_t smem = 1024 + (size_t)a.stages * kStage2 + 128 * RP * 2 + 256;
     static bool attr_done = false;
     if (!attr_done) {
@@ -341,12 +373,15 @@ int gemm2_stages(int r_pad) {
     return s > 8 ? 8 : s;
 }
 
-int launch_gemm2(const Gemm2Args &a, int num_sms, cudaStream_t st) {
+int launch_gemm2(const Gemm2Args &a, bool bwd, int num_sms, cudaStream_t st) {
     if (a.n_pairs == 0 || a.n_ntiles == 0) return 0;
-    switch (a.r_pad) {
-        case 16: return launch2_impl<16>(a, num_sms, st);
-        case 32: return launch2_impl<32>(a, num_sms, st);
-        case 64: return launch2_impl<64>(a, num_sms, st);
+    switch (a.r_pad * (bwd ? -1 : 1)) {
+        case 16: return launch2_impl<false, 16>(a, num_sms, st);
+        case 32: return launch2_impl<false, 32>(a, num_sms, st);
+        case 64: return launch2_impl<false, 64>(a, num_sms, st);
+        case -16: return launch2_impl<true, 16>(a, num_sms, st);
+        case -32: return launch2_impl<true, 32>(a, num_sms, st);
+        case -64: return launch2_impl<true, 64>(a, num_sms, st);
     }
     return (int)cudaErrorInvalidValue;
 }
