@@ -292,7 +292,7 @@ WsLayout layout_for(smlm_pool p, const smlm_batch *b, const Plan &plan, bool bwd
                        plan.blocks.size() * sizeof(DevBlock) + plan.short_rows.size() * sizeof(DevShortRow) +
                        // decode-path extras: distinct slots + per-row records (<= 4 short tiles)
                        (size_t)p->cap * 4 + 4 * 128 * sizeof(DecRow) + 64 +
-                       plan.long_tiles.size() * sizeof(DevPair) + 16;
+                       (plan.long_tiles.size() + plan.short_tiles.size()) * sizeof(DevPair) + 16;
     } else {
         L.plan_bytes = plan.bwd_tiles.size() * (sizeof(DevTile) + 4 + sizeof(DevPair)) +
                        plan.groups.size() * grad_group_bytes() + 64;
@@ -665,7 +665,7 @@ int smlm_forward(smlm_pool p, const smlm_batch *b, const void *X, const void *W,
             DevPair pr{};
             pr.row0 = t0.row0;
             pr.slot = t0.slot;
-            pr.ft = (t0.flags & kTileFT) ? 1 : 0;
+            pr.flags = (t0.flags & kTileFT) ? kPairFT : 0;
             pr.scale = t0.scale;
             int rows = t0.rows;
             if (i + 1 < n_long_kept && tiles[i + 1].seg == t0.seg) {
@@ -675,6 +675,18 @@ int smlm_forward(smlm_pool p, const smlm_batch *b, const void *X, const void *W,
                 i += 1;
             }
             pr.rows = rows;
+            pairs.push_back(pr);
+        }
+        // short tiles ride in the same launch: one per pair, CTA 1 a masked dummy
+        for (size_t i = n_long_kept; i < tiles.size(); ++i) {
+            const DevTile &t = tiles[i];
+            DevPair pr{};
+            pr.row0 = t.row0;
+            pr.rows = t.rows;
+            pr.slot = -1;
+            pr.flags = kPairShort;
+            pr.blk0 = t.blk0;
+            pr.nblk = t.nblk;
             pairs.push_back(pr);
         }
     }
@@ -767,6 +779,13 @@ int smlm_forward(smlm_pool p, const smlm_batch *b, const void *X, const void *W,
         if ((rc = make_map(&g2.tmX, X, p->in, b->S, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B))) return rc;
         if ((rc = make_map(&g2.tmW0, W, p->in, p->out, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B))) return rc;
         if ((rc = make_map(&g2.tmW1, W, p->in, p->out, 64, bnw - 128, CU_TENSOR_MAP_SWIZZLE_128B))) return rc;
+        if (!plan.blocks.empty()) {
+            if ((rc = make_map(&g2.tmU, Vbd, p->r_pad, plan.blocks.size() * 128, p->r_pad, 128,
+                               swizzle_for(p->r_pad * 2))))
+                return rc;
+            g2.has_u = 1;
+        }
+        g2.blocks = d_blocks;
         g2.slots = p->d_slots;
         g2.pairs = reinterpret_cast<const DevPair *>(wsb + L.plan_off + pair_off);
         g2.n_pairs = (int)pairs.size();
@@ -781,7 +800,7 @@ int smlm_forward(smlm_pool p, const smlm_batch *b, const void *X, const void *W,
         g2.Vsave = V_save;
         ProfScope ps(0, st);
         CKL(launch_gemm2(g2, false, p->num_sms, st), 1);
-        first_1cta = n_long_kept;
+        first_1cta = (int)tiles.size();
     }
     if ((int)tiles.size() == first_1cta) return SMLM_OK;
     GemmArgs a;
@@ -850,7 +869,7 @@ int smlm_backward(smlm_pool p, const smlm_batch *b, const void *X, const void *W
         DevPair pr{};
         pr.row0 = t0.row0;
         pr.slot = t0.slot;
-        pr.ft = 1;
+        pr.flags = kPairFT;
         pr.scale = t0.scale;
         pr.tile = (int)i;
         if (i + 1 < plan.bwd_tiles.size() && plan.bwd_tiles[i + 1].seg == t0.seg) {
@@ -929,6 +948,7 @@ int smlm_backward(smlm_pool p, const smlm_batch *b, const void *X, const void *W
             if (L.u_items &&
                 (rc = make_map(&g2.tmU, sUt, p->r_pad, (uint64_t)nt * 128, p->r_pad, 128, swizzle_for(p->r_pad * 2))))
                 return rc;
+            g2.has_u = L.u_items > 0;
             g2.slots = p->d_slots;
             g2.pairs = d_pairs;
             g2.n_pairs = n_pairs;

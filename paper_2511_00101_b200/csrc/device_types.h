@@ -54,19 +54,23 @@ struct alignas(16) DevPair {
     int row0;     // first row of the pair (CTA 0: [row0, row0+128), CTA 1: [row0+128, row0+256))
     int rows;     // valid rows of the pair (<= 256; past a segment end rows are masked)
     int slot;     // adapter or -1
-    int ft;       // FINETUNE segment (V_save)
+    int flags;    // bit 0: FINETUNE segment (V_save); bit 1: short tile (CTA 0 only, per-adapter blocks)
     float scale;
     int tile;     // backward: index of the pair's first tile in the backward tile list (s*U rows)
-    int pad[2];
+    int blk0;     // short pair: first adapter block of the tile
+    int nblk;     // short pair: number of adapter blocks
 };
+constexpr int kPairFT = 1, kPairShort = 2;
 
 struct Gemm2Args {
     CUtensorMap tmX;    // fwd: X [S,in] / bwd: dY [S,out]; box {64,128} SW128
     CUtensorMap tmW0;   // fwd: W box {64,128} (CTA 0's half of B); bwd: W box {64,64} (MN-major)
     CUtensorMap tmW1;   // fwd: W box {64,256-r_pad-128} (CTA 1's W rows; A_a stacked below)
-    CUtensorMap tmU;    // bwd: tile-compact s*U [n_tiles*128, r_pad] box {r_pad,128}
+    CUtensorMap tmU;    // bwd: tile-compact s*U; fwd: block-diagonal s*V of short tiles; box {r_pad,128}
     const SlotDev *slots;
     const DevPair *pairs;
+    const DevBlock *blocks;   // fwd short pairs
+    int has_u;                // tmU is valid
     int n_pairs;
     int n_ntiles;
     int group_m;

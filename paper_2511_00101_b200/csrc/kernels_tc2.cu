@@ -114,6 +114,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
         fence_mbar_init();
         tma_prefetch_desc(&args.tmX);
         tma_prefetch_desc(&args.tmW0);
+        if (args.has_u) tma_prefetch_desc(&args.tmU);
         if (!BWD) tma_prefetch_desc(&args.tmW1);
     }
     if (warp == 2) {
@@ -176,6 +177,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
                 }
                 __syncwarp();
                 advance();
+            }
+            if (!BWD && (pr.flags & kPairShort)) {
+                // short tile (CTA 0; CTA 1 is a masked dummy): one K = r_pad block per adapter,
+                // A = block-diagonal s*V rows, B = B_u rows [n0 + 128 rank, +128)
+                for (int bi = 0; bi < pr.nblk; ++bi) {
+                    const SlotDev *bs = args.slots + args.blocks[pr.blk0 + bi].slot;
+                    mbar_wait(empty_bar(stage), phase ^ 1);
+                    if (lane == 0) {
+                        const uint32_t fb = map_to_rank(full_bar(stage), 0);
+                        if (leader) mbar_expect_tx(full_bar(stage), 2u * 256u * RB);
+                        tma_load_2d_pair(a_addr(stage), &args.tmU, fb, 0, (pr.blk0 + bi) * 128);
+                        const int rb0 = n0 + 128 * (int)rank;
+                        tma_load_2d_pair(b_addr(stage), &bs->tmBk, fb, 0, rb0);
+                        tma_load_2d_pair(b_addr(stage) + 64u * RB, &bs->tmBk, fb, 0, rb0 + 64);
+                    }
+                    __syncwarp();
+                    advance();
+                }
             }
             if (lora) {
                 mbar_wait(empty_bar(stage), phase ^ 1);
@@ -257,6 +276,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
                 advance();
                 ++lora_it;
             }
+            if (!BWD && (pr.flags & kPairShort)) {
+                for (int bi = 0; bi < pr.nblk; ++bi) {
+                    mbar_wait(full_bar(stage), phase);
+                    tc_fence_after();
+                    if (lane == 0) {
+                        const uint32_t ab = a_addr(stage), bb = b_addr(stage);
+#pragma unroll
+                        for (int kk = 0; kk < RP / 16; ++kk)
+                            mma2_bf16(acc, smem_desc(ab + 32u * kk, 16, 8u * RB, kSwR),
+                                      smem_desc(bb + 32u * kk, 16, 8u * RB, kSwR), idesc, 1);
+                        mma2_commit_mc(empty_bar(stage));
+                    }
+                    __syncwarp();
+                    advance();
+                }
+            }
             if (lane == 0) mma2_commit_mc(acc_full0 + 8 * b);
             __syncwarp();
             ++it;
@@ -292,7 +327,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
 #pragma unroll
                     for (int j = 0; j < 16; ++j) v[c + j] = tmp[j];
                 }
-                if (nt == 0 && row_ok && pr.ft && args.Vsave) {
+                if (nt == 0 && row_ok && (pr.flags & kPairFT) && args.Vsave) {
                     __nv_bfloat16 *vs = reinterpret_cast<__nv_bfloat16 *>(args.Vsave) + (size_t)row * args.r;
 #pragma unroll
                     for (int j = 0; j < RP; ++j)
