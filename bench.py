@@ -404,7 +404,7 @@ def main():
     # ---- end to end: host buffers through the public API ----
     e2e = None
     if not args.no_e2e:
-        e2e = run_e2e(wl, stream, max(2, min(args.steps, 5)), n, dist)
+        e2e = run_e2e(wl, stream, max(4, min(args.steps, 8)), n, dist)
 
     cpu = None
     if rank == 0 and n == 1 and not args.no_cpu_baseline:
@@ -436,9 +436,15 @@ def main():
 def run_e2e(wl, stream, steps, n, dist):
     """Same step through the public API with HOST buffers: every step copies the step's inputs
     (X per projection group; dY rows of the fine-tune segments) from pinned host memory and reads
-    back the results (Y of every projection, dX of fine-tune rows, the fine-tune dA/dB)."""
+    back the results (Y of every projection, dX of fine-tune rows, the fine-tune dA/dB).
+
+    Pipelined like a serving/training loop would be: device buffers are double-buffered, H2D of
+    step i+1 runs on its own stream while step i computes, and each projection's outputs are read
+    back on a D2H stream as soon as that projection finishes.  Timed from the first H2D to the
+    last D2H with CUDA events (all copies and kernels inside the timed region)."""
     S = wl.S
     ft = wl.ft_rows  # fine-tune segments come first (row order F, E, P, D)
+    dev = wl.dev
     hX = {g: torch.empty_like(x, device="cpu").pin_memory() for g, x in wl.X.items()}
     hdY = {p: torch.empty(ft, y.shape[1], dtype=y.dtype).pin_memory() for p, y in wl.dY.items()}
     hY = {p: torch.empty_like(y, device="cpu").pin_memory() for p, y in wl.Y.items()}
@@ -451,38 +457,87 @@ def run_e2e(wl, stream, steps, n, dist):
     h2d = sum(t.numel() * t.element_size() for t in hX.values()) + sum(t.numel() * t.element_size() for t in hdY.values())
     d2h = sum(t.numel() * t.element_size() for t in hY.values()) + \
         sum(t.numel() * t.element_size() for t in hdX.values()) + sum(t.numel() * t.element_size() for t in hG.values())
+    # double-buffered device tensors: [0] = the workload's own, [1] = a second set
+    Xb = [wl.X, {g: torch.empty_like(x) for g, x in wl.X.items()}]
+    dYb = [wl.dY, {p: torch.empty_like(y) for p, y in wl.dY.items()}]
+    Yb = [wl.Y, {p: torch.empty_like(y) for p, y in wl.Y.items()}]
+    dXb = [wl.dX, {p: torch.empty_like(x) for p, x in wl.dX.items()}]
+    Vb = [wl.V, {p: torch.zeros_like(v) for p, v in wl.V.items()}]
+    s_h2d = torch.cuda.Stream(dev)
+    s_d2h = torch.cuda.Stream(dev)
+    in_ready = [torch.cuda.Event(), torch.cuda.Event()]
+    in_free = [None, None]
+    out_done = [None, None]
 
-    def e2e_step(i):
-        L = i % N_LAYER_SETS
-        layer = wl.layers[L]
-        for g in hX:
-            wl.X[g].copy_(hX[g], non_blocking=True)
-        for p in hdY:
-            wl.dY[p][:ft].copy_(hdY[p], non_blocking=True)
+    def issue_inputs(i):
+        b = i % 2
+        with torch.cuda.stream(s_h2d):
+            if in_free[b] is not None:
+                s_h2d.wait_event(in_free[b])
+            for g in hX:
+                Xb[b][g].copy_(hX[g], non_blocking=True)
+            for p in hdY:
+                dYb[b][p][:ft].copy_(hdY[p], non_blocking=True)
+            in_ready[b].record(s_h2d)
+
+    def compute(i):
+        b = i % 2
+        layer = wl.layers[i % N_LAYER_SETS]
+        stream.wait_event(in_ready[b])
+        if out_done[b] is not None:
+            stream.wait_event(out_done[b])
         for p in synth.PROJECTIONS:
             e = layer[p]
-            S.smlm_forward(e["pool"].h, wl.b, wl.X[GROUP_OF[p]], e["W"], wl.Y[p], wl.V[p], e["wsf"], stream)
-            hY[p].copy_(wl.Y[p], non_blocking=True)
+            S.smlm_forward(e["pool"].h, wl.b, Xb[b][GROUP_OF[p]], e["W"], Yb[b][p], Vb[b][p], e["wsf"], stream)
+            ev = torch.cuda.Event()
+            ev.record(stream)
+            s_d2h.wait_event(ev)
+            with torch.cuda.stream(s_d2h):
+                hY[p].copy_(Yb[b][p], non_blocking=True)
         for p in reversed(synth.PROJECTIONS):
             e = layer[p]
-            S.smlm_backward(e["pool"].h, wl.b, wl.X[GROUP_OF[p]], e["W"], wl.dY[p], wl.V[p], wl.dX[p], 0,
+            S.smlm_backward(e["pool"].h, wl.b, Xb[b][GROUP_OF[p]], e["W"], dYb[b][p], Vb[b][p], dXb[b][p], 0,
                             e["wsb"], stream)
             if dist is not None:
                 dist.all_reduce(e["grad"].flat, op=dist.ReduceOp.SUM)
-            hdX[p].copy_(wl.dX[p][:ft], non_blocking=True)
-            hG[p].copy_(e["grad"].flat, non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(stream)
+            s_d2h.wait_event(ev)
+            with torch.cuda.stream(s_d2h):
+                hdX[p].copy_(dXb[b][p][:ft], non_blocking=True)
+                hG[p].copy_(e["grad"].flat, non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record(stream)
+        in_free[b] = ev
+        od = torch.cuda.Event()
+        od.record(s_d2h)
+        out_done[b] = od
 
-    e2e_step(0)
+    # warm-up one pipelined pass, then time `steps` steps end to end
+    issue_inputs(0)
+    compute(0)
     torch.cuda.synchronize()
     if dist is not None:
         dist.barrier()
-    ms = _device_timed(e2e_step, steps, stream) / steps
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record(s_h2d)
+    issue_inputs(0)
+    for i in range(steps):
+        if i + 1 < steps:
+            issue_inputs(i + 1)
+        compute(i)
+    s_d2h.wait_stream(stream)
+    t1.record(s_d2h)
+    t1.synchronize()
+    ms = t0.elapsed_time(t1) / steps
     if dist is not None:
         t = torch.tensor([ms], device=wl.dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
+    del Xb, dYb, Yb, dXb, Vb
     return {"value": n * wl.rows / (ms / 1000.0), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
-            "d2h_bytes_per_step": int(d2h), "ms_per_step": ms}
+            "d2h_bytes_per_step": int(d2h), "ms_per_step": ms,
+            "pipelining": "double-buffered; H2D of step i+1 and per-projection D2H overlap step i's kernels"}
 
 
 if __name__ == "__main__":
