@@ -10,6 +10,7 @@
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
 #include <math.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
@@ -321,6 +322,7 @@ WsLayout layout_for(smlm_pool p, const smlm_batch *b, const Plan &plan, bool bwd
             const int n_vt = ((int)uniq.size() * p->r_pad + 127) / 128;
             const int items = (n_nt + n_vt) * groups;
             int ks = p->num_sms / items;        // one wave
+            if (const char *e = getenv("SMLM_DEC_KSPLIT")) ks = atoi(e);   // measurement override
             const int nkb = p->in / 64;
             const int ks_bytes = p->in / 256;   // partials <= ~2x the W bytes
             if (ks > ks_bytes) ks = ks_bytes;
@@ -786,6 +788,7 @@ int smlm_forward(smlm_pool p, const smlm_batch *b, const void *X, const void *W,
             g2.has_u = 1;
         }
         g2.blocks = d_blocks;
+        g2.defer = getenv("SMLM_NO_DEFER") ? 0 : 1;
         g2.slots = p->d_slots;
         g2.pairs = reinterpret_cast<const DevPair *>(wsb + L.plan_off + pair_off);
         g2.n_pairs = (int)pairs.size();

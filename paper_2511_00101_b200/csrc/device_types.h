@@ -71,6 +71,7 @@ struct Gemm2Args {
     const DevPair *pairs;
     const DevBlock *blocks;   // fwd short pairs
     int has_u;                // tmU is valid
+    int defer;                // forward: defer each item's expand into the next item's main loop
     int n_pairs;
     int n_ntiles;
     int group_m;

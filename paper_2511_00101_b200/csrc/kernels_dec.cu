@@ -161,7 +161,9 @@ __device__ __forceinline__ void dec_item(const DecArgs &a, int w, int &nt, int &
     split = w % a.ksplit;
     const int rest = w / a.ksplit;
     grp = rest % a.n_groups;
-    nt = rest / a.n_groups;   // < n_nt: W rows; >= n_nt: stacked adapter rows
+    // the stacked-adapter row tiles (several TMA descriptors per stage, the slowest items) go first
+    const int o = rest / a.n_groups;
+    nt = o < a.n_vt ? a.n_nt + o : o - a.n_vt;   // < n_nt: W rows; >= n_nt: stacked adapter rows
 }
 
 template <int RP>
@@ -362,48 +364,58 @@ __global__ void __launch_bounds__(256) dec_reduce_kernel(const __grid_constant__
         Vs[ml][j] = v;
     }
     __syncthreads();
-    const int ml = threadIdx.x >> 5;
-    const int nq = 4 * (threadIdx.x & 31);
+    // phase 2: warp = decode row, lane = columns n0 + lane + 32 q (q = 0..3): coalesced partial
+    // loads, B_u rows read as consecutive 2*r-byte rows across the warp, coalesced bf16 stores
+    const int ml = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int n0 = nt * 128;
     const DecRow dr = rs[ml];
-    if (dr.row < 0 || n0 + nq >= args.N) return;
+    if (dr.row < 0) return;
     const int pair = nt * args.n_groups + grp;
-    const float *pbase = args.part + (size_t)pair * ks * tile_elems + (size_t)(mc * 8 + ml) * 128 + nq;
-    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int s0 = 0; s0 < ks; s0 += 8) {
-        float4 t[8];
+    const float *pbase = args.part + (size_t)pair * ks * tile_elems + (size_t)(mc * 8 + ml) * 128 + lane;
+    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+    for (int s0 = 0; s0 < ks; s0 += 4) {
+        float t[4][4];
 #pragma unroll
-        for (int u = 0; u < 8; ++u)
-            t[u] = s0 + u < ks ? __ldcg(reinterpret_cast<const float4 *>(pbase + (size_t)(s0 + u) * tile_elems))
-                               : make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int u = 0; u < 4; ++u)
 #pragma unroll
-        for (int u = 0; u < 8; ++u) { acc.x += t[u].x; acc.y += t[u].y; acc.z += t[u].z; acc.w += t[u].w; }
+            for (int q = 0; q < 4; ++q)
+                t[u][q] = s0 + u < ks ? __ldcg(pbase + (size_t)(s0 + u) * tile_elems + 32 * q) : 0.f;
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) acc[q] += t[u][q];
     }
-    float l[4] = {0.f, 0.f, 0.f, 0.f};
     const __nv_bfloat16 *B = bptr[ml];
     if (B) {
+        float l[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
         for (int jg = 0; jg < RP; jg += 8) {
             if (jg < args.r) {
                 uint4 bu[4];
 #pragma unroll
-                for (int q4 = 0; q4 < 4; ++q4)
-                    bu[q4] = __ldg(reinterpret_cast<const uint4 *>(B + (size_t)(n0 + nq + q4) * args.r + jg));
+                for (int q = 0; q < 4; ++q) {
+                    const int n = n0 + lane + 32 * q;
+                    bu[q] = n < args.N ? __ldg(reinterpret_cast<const uint4 *>(B + (size_t)n * args.r + jg))
+                                       : make_uint4(0, 0, 0, 0);
+                }
 #pragma unroll
-                for (int q4 = 0; q4 < 4; ++q4) {
+                for (int q = 0; q < 4; ++q) {
                     float bf[8];
-                    bf16x8_f32(bu[q4], bf);
+                    bf16x8_f32(bu[q], bf);
 #pragma unroll
-                    for (int e = 0; e < 8; ++e) l[q4] = fmaf(bf[e], Vs[ml][jg + e], l[q4]);
+                    for (int e = 0; e < 8; ++e) l[q] = fmaf(bf[e], Vs[ml][jg + e], l[q]);
                 }
             }
         }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) acc[q] += dr.scale * l[q];
     }
-    const float sc = B ? dr.scale : 0.f;
-    uint2 pk;
-    pk.x = pack_bf16x2(acc.x + sc * l[0], acc.y + sc * l[1]);
-    pk.y = pack_bf16x2(acc.z + sc * l[2], acc.w + sc * l[3]);
-    *reinterpret_cast<uint2 *>(reinterpret_cast<__nv_bfloat16 *>(args.Y) + (size_t)dr.row * args.N + n0 + nq) = pk;
+    __nv_bfloat16 *Y = reinterpret_cast<__nv_bfloat16 *>(args.Y) + (size_t)dr.row * args.N;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const int n = n0 + lane + 32 * q;
+        if (n < args.N) Y[n] = __float2bfloat16_rn(acc[q]);
+    }
 }
 
 template <int RP>

@@ -221,6 +221,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
         }
     } else if (warp == 1 && leader) {
         // ========================= MMA issuer (leader CTA) =========================
+        // Forward LoRA items: the expand K-block of item i waits for the epilogue's s*V (sv_ready),
+        // so it is DEFERRED into the main loop of item i+1 (other TMEM buffer) and issued as soon as
+        // sv_ready is observed, at the latest before the ring wraps onto its stage.
         int stage = 0;
         uint32_t phase = 0;
         auto advance = [&]() {
@@ -228,6 +231,37 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
         };
         constexpr uint32_t idesc = idesc_bf16(256, 256, 0, BWD ? 1 : 0);
         uint32_t it = 0, lora_it = 0;
+        int pend_stage = -1, since = 0;
+        uint32_t pend_phase = 0, pend_b = 0, pend_lit = 0;
+        auto issue_expand = [&](int st, uint32_t ph, uint32_t bb_, bool from_sv) {
+            mbar_wait(full_bar(st), ph);
+            tc_fence_after();
+            if (lane == 0) {
+                const uint32_t bb = b_addr(st);
+                const uint32_t aop = from_sv ? sv_addr : a_addr(st);
+#pragma unroll
+                for (int kk = 0; kk < RP / 16; ++kk)
+                    mma2_bf16(acc_col(bb_), smem_desc(aop + 32u * kk, 16, 8u * RB, kSwR),
+                              BWD ? smem_desc(bb + 2048u * kk, (uint32_t)RP * 128u, 1024, kSw128)
+                                  : smem_desc(bb + 32u * kk, 16, 8u * RB, kSwR),
+                              idesc, 1);
+                mma2_commit_mc(empty_bar(st));
+            }
+            __syncwarp();
+        };
+        auto flush = [&](bool block) {
+            if (pend_stage < 0) return;
+            if (!block && since < stages - 2) {
+                uint32_t ok = lane == 0 ? mbar_test(sv_ready, pend_lit & 1) : 0;
+                ok = __shfl_sync(0xffffffffu, ok, 0);
+                if (!ok) return;
+            }
+            mbar_wait(sv_ready, pend_lit & 1);
+            issue_expand(pend_stage, pend_phase, pend_b, true);
+            if (lane == 0) mma2_commit_mc(acc_full0 + 8 * pend_b);
+            __syncwarp();
+            pend_stage = -1;
+        };
         for (int w = cid; w < total; w += n_clusters) {
             int pi, nt;
             decode_pair(w, args.n_pairs, args.n_ntiles, args.group_m, pi, nt);
@@ -235,9 +269,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
             const bool lora = pr.slot >= 0;
             const uint32_t b = it & 1, u = it >> 1;
             const uint32_t acc = acc_col(b);
+            if (pend_stage >= 0 && pend_b == b) flush(true);
             mbar_wait(acc_empty0 + 8 * b, (u & 1) ^ 1);
             tc_fence_after();
             for (int kb = 0; kb < nkb; ++kb) {
+                if (!BWD) flush(false);
                 mbar_wait(full_bar(stage), phase);
                 tc_fence_after();
                 if (lane == 0) {
@@ -252,50 +288,52 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
                 }
                 __syncwarp();
                 advance();
+                if (pend_stage >= 0) ++since;
             }
             if (lora) {
-                if (!BWD) {
+                if (BWD) {  // s*U arrives by TMA: expand right away
+                    issue_expand(stage, phase, b, false);
+                    advance();
+                    if (lane == 0) mma2_commit_mc(acc_full0 + 8 * b);
+                    __syncwarp();
+                } else {
                     if (lane == 0) mma2_commit_mc(v_full);
                     __syncwarp();
-                }
-                mbar_wait(full_bar(stage), phase);
-                if (!BWD) mbar_wait(sv_ready, lora_it & 1);
-                tc_fence_after();
-                if (lane == 0) {
-                    const uint32_t bb = b_addr(stage);
-                    const uint32_t aop = BWD ? a_addr(stage) : sv_addr;
-#pragma unroll
-                    for (int kk = 0; kk < RP / 16; ++kk)
-                        mma2_bf16(acc, smem_desc(aop + 32u * kk, 16, 8u * RB, kSwR),
-                                  BWD ? smem_desc(bb + 2048u * kk, (uint32_t)RP * 128u, 1024, kSw128)
-                                      : smem_desc(bb + 32u * kk, 16, 8u * RB, kSwR),
-                                  idesc, 1);
-                    mma2_commit_mc(empty_bar(stage));
-                }
-                __syncwarp();
-                advance();
-                ++lora_it;
-            }
-            if (!BWD && (pr.flags & kPairShort)) {
-                for (int bi = 0; bi < pr.nblk; ++bi) {
-                    mbar_wait(full_bar(stage), phase);
-                    tc_fence_after();
-                    if (lane == 0) {
-                        const uint32_t ab = a_addr(stage), bb = b_addr(stage);
-#pragma unroll
-                        for (int kk = 0; kk < RP / 16; ++kk)
-                            mma2_bf16(acc, smem_desc(ab + 32u * kk, 16, 8u * RB, kSwR),
-                                      smem_desc(bb + 32u * kk, 16, 8u * RB, kSwR), idesc, 1);
-                        mma2_commit_mc(empty_bar(stage));
-                    }
-                    __syncwarp();
+                    flush(true);   // at most one deferred expand
+                    pend_stage = stage;
+                    pend_phase = phase;
+                    pend_b = b;
+                    pend_lit = lora_it;
+                    since = 0;
                     advance();
+                    if (!args.defer) flush(true);
                 }
+                ++lora_it;
+            } else {
+                if (!BWD && (pr.flags & kPairShort)) {
+                    for (int bi = 0; bi < pr.nblk; ++bi) {
+                        flush(false);
+                        mbar_wait(full_bar(stage), phase);
+                        tc_fence_after();
+                        if (lane == 0) {
+                            const uint32_t ab = a_addr(stage), bb = b_addr(stage);
+#pragma unroll
+                            for (int kk = 0; kk < RP / 16; ++kk)
+                                mma2_bf16(acc, smem_desc(ab + 32u * kk, 16, 8u * RB, kSwR),
+                                          smem_desc(bb + 32u * kk, 16, 8u * RB, kSwR), idesc, 1);
+                            mma2_commit_mc(empty_bar(stage));
+                        }
+                        __syncwarp();
+                        advance();
+                        if (pend_stage >= 0) ++since;
+                    }
+                }
+                if (lane == 0) mma2_commit_mc(acc_full0 + 8 * b);
+                __syncwarp();
             }
-            if (lane == 0) mma2_commit_mc(acc_full0 + 8 * b);
-            __syncwarp();
             ++it;
         }
+        flush(true);
     } else if (warp >= 4) {
         // ========================= epilogue (both CTAs, own 128 rows) =========================
         const int q = warp - 4;
