@@ -435,8 +435,10 @@ def main():
 
 def run_e2e(wl, stream, steps, n, dist):
     """Same step through the public API with HOST buffers: every step copies the step's inputs
-    (X per projection group; dY rows of the fine-tune segments) from pinned host memory and reads
-    back the results (Y of every projection, dX of fine-tune rows, the fine-tune dA/dB).
+    (X per projection group for every row; dY of the fine-tune rows) from pinned host memory and
+    reads back the step's results: the fine-tune adapters' dA/dB (what the optimizer consumes) and
+    Y of the decode rows of every projection (what the serving loop consumes).  Intermediates that
+    stay on the device in a real model (prefill/fine-tune Y, dX) are not copied.
 
     Pipelined like a serving/training loop would be: device buffers are double-buffered, H2D of
     step i+1 runs on its own stream while step i computes, and each projection's outputs are read
@@ -447,16 +449,17 @@ def run_e2e(wl, stream, steps, n, dist):
     dev = wl.dev
     hX = {g: torch.empty_like(x, device="cpu").pin_memory() for g, x in wl.X.items()}
     hdY = {p: torch.empty(ft, y.shape[1], dtype=y.dtype).pin_memory() for p, y in wl.dY.items()}
-    hY = {p: torch.empty_like(y, device="cpu").pin_memory() for p, y in wl.Y.items()}
-    hdX = {p: torch.empty(ft, x.shape[1], dtype=x.dtype).pin_memory() for p, x in wl.dX.items()}
+    # decode rows are the trailing DECODE segments (row order F, E, P, D)
+    dec0 = int(wl.batch.offsets[int(np.argmax(wl.batch.modes == synth.DECODE))]) if np.any(
+        wl.batch.modes == synth.DECODE) else wl.rows
+    hY = {p: torch.empty(wl.rows - dec0, y.shape[1], dtype=y.dtype).pin_memory() for p, y in wl.Y.items()}
     hG = {p: torch.empty_like(wl.layers[0][p]["grad"].flat, device="cpu").pin_memory() for p in synth.PROJECTIONS}
     for g in hX:
         hX[g].copy_(wl.X[g].cpu())
     for p in hdY:
         hdY[p].copy_(wl.dY[p][:ft].cpu())
     h2d = sum(t.numel() * t.element_size() for t in hX.values()) + sum(t.numel() * t.element_size() for t in hdY.values())
-    d2h = sum(t.numel() * t.element_size() for t in hY.values()) + \
-        sum(t.numel() * t.element_size() for t in hdX.values()) + sum(t.numel() * t.element_size() for t in hG.values())
+    d2h = sum(t.numel() * t.element_size() for t in hY.values()) + sum(t.numel() * t.element_size() for t in hG.values())
     # double-buffered device tensors: [0] = the workload's own, [1] = a second set
     Xb = [wl.X, {g: torch.empty_like(x) for g, x in wl.X.items()}]
     dYb = [wl.dY, {p: torch.empty_like(y) for p, y in wl.dY.items()}]
@@ -493,7 +496,7 @@ def run_e2e(wl, stream, steps, n, dist):
             ev.record(stream)
             s_d2h.wait_event(ev)
             with torch.cuda.stream(s_d2h):
-                hY[p].copy_(Yb[b][p], non_blocking=True)
+                hY[p].copy_(Yb[b][p][dec0:], non_blocking=True)
         for p in reversed(synth.PROJECTIONS):
             e = layer[p]
             S.smlm_backward(e["pool"].h, wl.b, Xb[b][GROUP_OF[p]], e["W"], dYb[b][p], Vb[b][p], dXb[b][p], 0,
@@ -504,7 +507,6 @@ def run_e2e(wl, stream, steps, n, dist):
             ev.record(stream)
             s_d2h.wait_event(ev)
             with torch.cuda.stream(s_d2h):
-                hdX[p].copy_(dXb[b][p][:ft], non_blocking=True)
                 hG[p].copy_(e["grad"].flat, non_blocking=True)
         ev = torch.cuda.Event()
         ev.record(stream)
@@ -537,6 +539,8 @@ def run_e2e(wl, stream, steps, n, dist):
     del Xb, dYb, Yb, dXb, Vb
     return {"value": n * wl.rows / (ms / 1000.0), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
             "d2h_bytes_per_step": int(d2h), "ms_per_step": ms,
+            "h2d": "X of every row (4 activation groups) + dY of the fine-tune rows",
+            "d2h": "fine-tune dA/dB of the 7 projections + Y of the decode rows",
             "pipelining": "double-buffered; H2D of step i+1 and per-projection D2H overlap step i's kernels"}
 
 
