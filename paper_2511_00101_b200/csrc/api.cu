@@ -48,6 +48,7 @@ int launch_shrink_split(const __nv_bfloat16 *X, const SlotDev *slots, const DevB
                         const DevShortRow *srows, int n_blocks, int in_f, int r, int r_pad, float *part,
                         __nv_bfloat16 *Vbd, __nv_bfloat16 *Vsave, cudaStream_t st);
 int launch_dec(const DecArgs &a, int num_sms, cudaStream_t st);
+int launch_decf(const DecFArgs &a, cudaStream_t st);
 size_t grad_group_bytes();
 void fill_grad_group(void *dst, int slot, int tile_begin, int n_tiles, float *dA, float *dB);
 template <typename T, typename TV>
@@ -236,6 +237,8 @@ struct smlm_pool_s {
     std::vector<uint8_t> ok;
     std::vector<float> scales;
     SlotDev *d_slots = nullptr;
+    unsigned long long *d_counter = nullptr;   // fused decode kernel: release counter
+    unsigned long long dec_epoch = 0;
     Ring ring;
 };
 
@@ -273,6 +276,9 @@ struct WsLayout {
     size_t dpart_off = 0, dpart_bytes = 0; // bf16 fwd decode GEMM: split-K partials
     int dec_items = 0, dec_ksplit = 0;     // > 0: pure-decode batch takes the transposed split-K kernel
     std::vector<int> dec_uniq;             // distinct adapter slots of the decode batch
+    bool decf = false;                     // fused single-launch decode kernel
+    int decf_ksplit = 0;
+    size_t vg_off = 0;
     size_t total = 0;
 };
 
@@ -331,9 +337,30 @@ WsLayout layout_for(smlm_pool p, const smlm_batch *b, const Plan &plan, bool bwd
             L.dec_items = items;
             L.dec_ksplit = ks;
             L.dec_uniq = uniq;
-            L.dpart_off = off;
-            L.dpart_bytes = (size_t)items * ks * 256 * 128 * 4;
-            off = align256(off + L.dpart_bytes);
+            // <= 256 decode rows: fused single-launch kernel (DSMEM split-K reduction, in-kernel expand)
+            // experimental (opt-in, SMLM_DECF=1): measured slower than the two-kernel path so far
+            if (nst <= 2 && getenv("SMLM_DECF")) {
+                const int tiles_f = n_nt + n_vt;
+                const int m_rows = 128 * nst;
+                // power-of-two cluster <= 8 (portable): every cluster of a GPC-sized group co-resides
+                int kf = 1;
+                while (kf * 2 <= 8 && tiles_f * kf * 2 <= p->num_sms) kf *= 2;
+                if (const char *e = getenv("SMLM_DECF_KSPLIT")) kf = atoi(e);
+                if (kf > nkb) kf = nkb;
+                if (kf * 64 < m_rows) kf = (m_rows + 63) / 64;   // <= 64 decode rows per CTA slice
+                if (kf <= 8 && kf <= nkb && tiles_f * kf <= p->num_sms) {
+                    L.decf = true;
+                    L.decf_ksplit = kf;
+                }
+            }
+            if (L.decf) {
+                L.vg_off = off;
+                off = align256(off + 256 * (size_t)p->r_pad * 4);
+            } else {
+                L.dpart_off = off;
+                L.dpart_bytes = (size_t)items * ks * 256 * 128 * 4;
+                off = align256(off + L.dpart_bytes);
+            }
         }
     }
     if (bwd && p->dtype == SMLM_FP32) {
@@ -481,7 +508,9 @@ int smlm_pool_create(int device, int in_features, int out_features, int rank, in
         delete p;
         return cuda_err(e, "cudaMalloc(slot table)");
     }
-    e = cudaMemset(p->d_slots, 0, sizeof(SlotDev) * capacity);
+    if (e == cudaSuccess) e = cudaMalloc(&p->d_counter, 64);
+    if (e == cudaSuccess) e = cudaMemset(p->d_counter, 0, 64);
+    if (e == cudaSuccess) e = cudaMemset(p->d_slots, 0, sizeof(SlotDev) * capacity);
     if (e != cudaSuccess) {
         cudaFree(p->d_slots);
         delete p;
@@ -497,6 +526,7 @@ int smlm_pool_destroy(smlm_pool p) {
         DeviceGuard dg(p->device);
         cudaDeviceSynchronize();
         if (p->d_slots) cudaFree(p->d_slots);
+        if (p->d_counter) cudaFree(p->d_counter);
     }
     delete p;
     return SMLM_OK;
@@ -732,6 +762,36 @@ int smlm_forward(smlm_pool p, const smlm_batch *b, const void *X, const void *W,
         append(extra, drows);
         bytes.insert(bytes.end(), extra.begin(), extra.end());
         if ((rc = stage_upload(p, bytes, wsb + L.plan_off, st))) return rc;
+        if (L.decf) {
+            DecFArgs f;
+            memset(&f, 0, sizeof(f));
+            if ((rc = make_map(&f.tmW, W, p->in, p->out, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B))) return rc;
+            if ((rc = make_map(&f.tmX, X, p->in, b->S, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B))) return rc;
+            f.slots = p->d_slots;
+            f.vt_slots = reinterpret_cast<const int *>(wsb + L.plan_off + vt_off);
+            f.rows = reinterpret_cast<const DecRow *>(wsb + L.plan_off + rows_off);
+            for (size_t t = 0; t < tiles.size() && t < 2; ++t) f.tile_row0[t] = tiles[t].row0;
+            f.n_uniq = (int)L.dec_uniq.size();
+            f.n_vt = (f.n_uniq * p->r_pad + 127) / 128;
+            f.n_nt = (p->out + 127) / 128;
+            f.ksplit = L.decf_ksplit;
+            f.m_rows = 128 * (int)tiles.size();
+            f.K = p->in;
+            f.N = p->out;
+            f.r = p->r;
+            f.r_pad = p->r_pad;
+            f.stages = dec_stages();
+            f.Y = Y;
+            f.Vsave = V_save;
+            f.Vg = reinterpret_cast<float *>(wsb + L.vg_off);
+            f.v_done = p->d_counter;
+            p->dec_epoch += 1;
+            f.v_target = p->dec_epoch * (unsigned long long)(f.n_vt * f.ksplit);
+            if (f.n_vt == 0) p->dec_epoch -= 1;
+            ProfScope ps(0, st);
+            CKL(launch_decf(f, st), 1);
+            return SMLM_OK;
+        }
         DecArgs d;
         memset(&d, 0, sizeof(d));
         if ((rc = make_map(&d.tmW, W, p->in, p->out, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B))) return rc;

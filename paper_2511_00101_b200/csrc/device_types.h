@@ -157,4 +157,29 @@ struct DecArgs {
     float *part;        // [(n_nt+n_vt)*n_groups][ksplit][256][128] fp32 partials
 };
 
+// fused decode kernel (<= 256 decode rows): DSMEM split-K reduction + in-kernel expand
+struct DecFArgs {
+    CUtensorMap tmW;    // W [out,in] box {64,128} SW128
+    CUtensorMap tmX;    // X [S,in]   box {64,128} SW128
+    const SlotDev *slots;
+    const int *vt_slots;     // distinct adapter slots of the batch, ascending
+    const DecRow *rows;      // [256] per decode row (m = tile*128 + pos)
+    int tile_row0[2];        // first batch row of the (<= 2) short tiles
+    int n_vt;                // stacked-adapter row tiles
+    int n_nt;                // W row tiles (ceil(out/128))
+    int n_uniq;
+    int ksplit;              // cluster size along K
+    int m_rows;              // 128 * number of short tiles
+    int K;
+    int N;
+    int r;
+    int r_pad;
+    int stages;
+    void *Y;
+    void *Vsave;
+    float *Vg;               // [256][r_pad] fp32 V of every decode row (workspace)
+    unsigned long long *v_done;     // pool-owned release counter
+    unsigned long long v_target;    // value of *v_done once this call's adapter tiles are published
+};
+
 }  // namespace smlm

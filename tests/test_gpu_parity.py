@@ -244,3 +244,17 @@ def test_bf16_decode_grouped_with_finetune_short_rows():
     batch, w, X, dY = synth.random_case(31, 1024, 384, 16, 4, lengths, modes, [0, 1, 2, 1, 3, 0, -1, 2])
     res = run_smlm(batch, w, X, dY)
     _check(res, batch, w, X, dY, BF16_TOL)
+
+
+def test_bf16_decode_fused_variant(monkeypatch):
+    """The experimental fused decode kernel (SMLM_DECF=1: DSMEM split-K reduction + in-kernel
+    expand) matches the oracle as well."""
+    monkeypatch.setenv("SMLM_DECF", "1")
+    g = torch.Generator().manual_seed(5)
+    rows = 200
+    slots = torch.randint(-1, 6, (rows,), generator=g).tolist()
+    modes = [DECODE] * (rows - 3) + [FINETUNE] * 3
+    batch, w, X, dY = synth.random_case(77, 1024, 640, 16, 6, [1] * rows, modes, slots)
+    res = run_smlm(batch, w, X, dY, backward=False)
+    Y, V = oracle.forward(batch, w.W, w.A, w.B, w.slot_scale, X)
+    assert parity_err(res.Y, Y) <= BF16_TOL
