@@ -173,10 +173,12 @@ SMLM_API const char *smlm_last_error(void);
 /* ---- instrumentation (used by bench.py; not needed for correctness) ---- */
 /* Number of kernels this library has launched in this process. */
 SMLM_API uint64_t smlm_launch_count(void);
-/* When enabled, the library records CUDA events around its main GEMM kernels on the launching
- * stream; smlm_profile_read synchronises those events and returns the summed milliseconds and
- * launch count for kernel class `kind` (0 = forward GEMM, 1 = backward dX GEMM, 2 = short-row
- * shrink, 3 = dA/dB) since the last reset, then resets that class. */
+/* smlm_profile_enable(mask): for every kernel class k with bit k set in `mask`, the library records
+ * CUDA events around its launches on the launching stream (0 disables; 1 = forward GEMM only;
+ * 0xF = all).  smlm_profile_read synchronises those events and returns the summed milliseconds and
+ * launch count for class `kind` (0 = forward GEMM, 1 = backward dX GEMM, 2 = short-row shrink,
+ * 3 = dA/dB) since the last read, then resets that class.  Events between launches serialise
+ * programmatic dependent launch, so enable only what is measured. */
 SMLM_API int smlm_profile_enable(int on);
 SMLM_API int smlm_profile_read(int kind, double *total_ms, int *count);
 

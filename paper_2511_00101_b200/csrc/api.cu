@@ -91,7 +91,7 @@ namespace {
 
 struct Profiler {
     std::mutex mu;
-    bool on = false;
+    int mask = 0;   // bit k: record kernel class k
     struct Rec { cudaEvent_t a, b; int kind; };
     std::vector<Rec> recs;
     std::vector<cudaEvent_t> pool;
@@ -108,7 +108,7 @@ struct ProfScope {
     int kind;
     cudaStream_t st;
     ProfScope(int k, cudaStream_t s) : kind(k), st(s) {
-        if (g_prof.on) {
+        if (g_prof.mask & (1 << k)) {
             std::lock_guard<std::mutex> lk(g_prof.mu);
             a = g_prof.get();
             cudaEventRecord(a, st);
@@ -441,7 +441,7 @@ uint64_t smlm_launch_count(void) { return g_launches.load(); }
 
 int smlm_profile_enable(int on) {
     std::lock_guard<std::mutex> lk(g_prof.mu);
-    g_prof.on = on != 0;
+    g_prof.mask = on;
     return SMLM_OK;
 }
 

@@ -16,6 +16,7 @@
 #include <cuda_runtime.h>
 
 #include "device_types.h"
+#include "pdl.cuh"
 #include "sm100.cuh"
 
 namespace smlm {
@@ -64,6 +65,8 @@ __global__ void __launch_bounds__(256) shrink_partial_kernel(const __nv_bfloat16
     extern __shared__ __align__(16) uint8_t sm[];
     __nv_bfloat16 *As = reinterpret_cast<__nv_bfloat16 *>(sm);                   // [RP][512]
     __nv_bfloat16 *Xs = As + RP * kChunk;                                         // [32][512]
+    pdl_wait();
+    pdl_trigger();
     const DevBlock blk = blocks[blockIdx.x];
     const int c = blockIdx.y, nch = gridDim.y;
     const __nv_bfloat16 *A = reinterpret_cast<const __nv_bfloat16 *>(slots[blk.slot].A);
@@ -111,6 +114,8 @@ __global__ void __launch_bounds__(256) shrink_combine_kernel(const DevBlock *__r
                                                              int r, const float *__restrict__ part,
                                                              __nv_bfloat16 *__restrict__ Vbd,
                                                              __nv_bfloat16 *__restrict__ Vsave) {
+    pdl_wait();
+    pdl_trigger();
     const DevBlock blk = blocks[blockIdx.x];
     __shared__ int idx_of[128];
     __shared__ float vals[128][RP];
@@ -458,26 +463,30 @@ int launch_shrink_split(const __nv_bfloat16 *X, const SlotDev *slots, const DevB
     if (n_blocks == 0) return 0;
     const int nch = dec_chunks(in_f);
     dim3 g1(n_blocks, nch);
+    cudaError_t e = cudaSuccess;
     switch (r_pad) {
         case 16:
-            shrink_partial_kernel<16><<<g1, 256, (16 + kRowsPerPass) * kChunk * 2, st>>>(X, slots, blocks, srows, in_f, r, part);
-            shrink_combine_kernel<16><<<n_blocks, 256, 0, st>>>(blocks, srows, nch, r, part, Vbd, Vsave);
+            e = launch_pdl(shrink_partial_kernel<16>, g1, dim3(256), (16 + kRowsPerPass) * kChunk * 2, st, X, slots, blocks, srows, in_f, r, part);
+            if (e != cudaSuccess) return (int)e;
+            e = launch_pdl(shrink_combine_kernel<16>, dim3(n_blocks), dim3(256), 0, st, blocks, srows, nch, r, part, Vbd, Vsave);
             break;
         case 32:
             cudaFuncSetAttribute(shrink_partial_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (32 + kRowsPerPass) * kChunk * 2);
-            shrink_partial_kernel<32><<<g1, 256, (32 + kRowsPerPass) * kChunk * 2, st>>>(X, slots, blocks, srows, in_f, r, part);
-            shrink_combine_kernel<32><<<n_blocks, 256, 0, st>>>(blocks, srows, nch, r, part, Vbd, Vsave);
+            e = launch_pdl(shrink_partial_kernel<32>, g1, dim3(256), (32 + kRowsPerPass) * kChunk * 2, st, X, slots, blocks, srows, in_f, r, part);
+            if (e != cudaSuccess) return (int)e;
+            e = launch_pdl(shrink_combine_kernel<32>, dim3(n_blocks), dim3(256), 0, st, blocks, srows, nch, r, part, Vbd, Vsave);
             break;
         case 64:
             cudaFuncSetAttribute(shrink_partial_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (64 + kRowsPerPass) * kChunk * 2);
-            shrink_partial_kernel<64><<<g1, 256, (64 + kRowsPerPass) * kChunk * 2, st>>>(X, slots, blocks, srows, in_f, r, part);
-            shrink_combine_kernel<64><<<n_blocks, 256, 0, st>>>(blocks, srows, nch, r, part, Vbd, Vsave);
+            e = launch_pdl(shrink_partial_kernel<64>, g1, dim3(256), (64 + kRowsPerPass) * kChunk * 2, st, X, slots, blocks, srows, in_f, r, part);
+            if (e != cudaSuccess) return (int)e;
+            e = launch_pdl(shrink_combine_kernel<64>, dim3(n_blocks), dim3(256), 0, st, blocks, srows, nch, r, part, Vbd, Vsave);
             break;
         default: return (int)cudaErrorInvalidValue;
     }
-    return (int)cudaGetLastError();
+    return e != cudaSuccess ? (int)e : (int)cudaGetLastError();
 }
 
 int launch_dec(const DecArgs &a, int num_sms, cudaStream_t st) {

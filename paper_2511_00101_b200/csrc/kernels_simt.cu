@@ -14,6 +14,7 @@
 #include <cuda_runtime.h>
 
 #include "device_types.h"
+#include "pdl.cuh"
 
 namespace smlm {
 
@@ -226,6 +227,8 @@ __global__ void __launch_bounds__(256) rows_u_kernel(const DevTile *__restrict__
 template <typename TV, int RP>
 __global__ void __launch_bounds__(128) prep_sv_kernel(const DevTile *__restrict__ tiles, const TV *__restrict__ V,
                                                       int r, __nv_bfloat16 *__restrict__ sVt) {
+    pdl_wait();
+    pdl_trigger();
     const DevTile t = tiles[blockIdx.x];
     const int m = threadIdx.x;
     __nv_bfloat16 *dst = sVt + ((size_t)blockIdx.x * 128 + m) * RP;
@@ -439,11 +442,10 @@ int launch_prep_sv(const DevTile *tiles, int n_tiles, const TV *V, int r, int r_
                    cudaStream_t st) {
     if (n_tiles == 0) return 0;
     switch (r_pad) {
-        case 16: prep_sv_kernel<TV, 16><<<n_tiles, 128, 0, st>>>(tiles, V, r, sVt); break;
-        case 32: prep_sv_kernel<TV, 32><<<n_tiles, 128, 0, st>>>(tiles, V, r, sVt); break;
-        default: prep_sv_kernel<TV, 64><<<n_tiles, 128, 0, st>>>(tiles, V, r, sVt); break;
+        case 16: return (int)launch_pdl(prep_sv_kernel<TV, 16>, dim3(n_tiles), dim3(128), 0, st, tiles, V, r, sVt);
+        case 32: return (int)launch_pdl(prep_sv_kernel<TV, 32>, dim3(n_tiles), dim3(128), 0, st, tiles, V, r, sVt);
+        default: return (int)launch_pdl(prep_sv_kernel<TV, 64>, dim3(n_tiles), dim3(128), 0, st, tiles, V, r, sVt);
     }
-    return (int)cudaGetLastError();
 }
 template int launch_prep_sv<float>(const DevTile *, int, const float *, int, int, __nv_bfloat16 *, cudaStream_t);
 template int launch_prep_sv<__nv_bfloat16>(const DevTile *, int, const __nv_bfloat16 *, int, int, __nv_bfloat16 *,

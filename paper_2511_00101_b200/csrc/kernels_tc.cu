@@ -20,6 +20,7 @@
 #include <cuda_runtime.h>
 
 #include "device_types.h"
+#include "pdl.cuh"
 #include "sm100.cuh"
 
 namespace smlm {
@@ -99,6 +100,8 @@ __global__ void __launch_bounds__(kThreads, 1) smlm_gemm_kernel(const __grid_con
     // two accumulator buffers ACC_b = TMEM columns [256 b, 256 b + 256)
     auto acc_col = [&](uint32_t b) { return tmem_base + 256u * b; };
     auto v_col = [&](uint32_t b) { return tmem_base + 256u * b + BNW; };   // forward V columns
+    pdl_wait();
+    pdl_trigger();
 
     const int total = args.n_tiles * args.n_ntiles;
     const int nkb = args.K / kBK;
@@ -389,8 +392,7 @@ int launch_impl(const GemmArgs &a, int num_sms, size_t smem, cudaStream_t st) {
     }
     const int total = a.n_tiles * a.n_ntiles;
     const int grid = total < num_sms ? total : num_sms;
-    kern<<<grid, kThreads, smem, st>>>(a);
-    return (int)cudaGetLastError();
+    return (int)launch_pdl(kern, dim3(grid), dim3(kThreads), smem, st, a);
 }
 
 
@@ -459,6 +461,8 @@ __global__ void __launch_bounds__(kThreads, 1) smlm_tok_kernel(const __grid_cons
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *reinterpret_cast<volatile uint32_t *>(base_ptr + (tmem_slot - base));
+    pdl_wait();
+    pdl_trigger();
     const int total = args.n_groups * (args.mt_a + args.mt_b);
 
     if (warp == 0) {
@@ -603,8 +607,7 @@ int launch_tok_impl(const TokArgs &a, int num_sms, cudaStream_t st) {
     }
     const int total = a.n_groups * (a.mt_a + a.mt_b);
     const int grid = total < num_sms ? total : num_sms;
-    kern<<<grid, kThreads, smem, st>>>(a);
-    return (int)cudaGetLastError();
+    return (int)launch_pdl(kern, dim3(grid), dim3(kThreads), smem, st, a);
 }
 
 
@@ -652,7 +655,8 @@ __global__ void __launch_bounds__(kThreads, 1) smlm_u_kernel(const __grid_consta
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *reinterpret_cast<volatile uint32_t *>(base_ptr + (tmem_slot - base));
-    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    pdl_wait();
+    pdl_trigger();
     const int total = args.n_items * args.ksplit;
     const int nkb = args.K / kBK;
     auto kb_range = [&](int split, int &kb0, int &kb1) {
@@ -792,8 +796,7 @@ int launch_u_impl(const UArgs &a, int num_sms, cudaStream_t st) {
         attr_done = true;
     }
     const int total = a.n_items * a.ksplit;
-    kern<<<total < num_sms ? total : num_sms, kThreads, smem, st>>>(a);
-    cudaError_t e = cudaGetLastError();
+    cudaError_t e = launch_pdl(kern, dim3(total < num_sms ? total : num_sms), dim3(kThreads), smem, st, a);
     if (e != cudaSuccess) return (int)e;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(a.n_items);

@@ -10,6 +10,7 @@
 #include <cuda_runtime.h>
 
 #include "device_types.h"
+#include "pdl.cuh"
 #include "sm100.cuh"
 
 namespace smlm {
@@ -127,6 +128,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
     tc_fence_after();
     const uint32_t tmem_base = *reinterpret_cast<volatile uint32_t *>(base_ptr + (tmem_slot - base));
     auto acc_col = [&](uint32_t b) { return tmem_base + 256u * b; };
+    pdl_wait();
+    pdl_trigger();
 
     const int n_clusters = gridDim.x / 2;
     const int cid = blockIdx.x / 2;
@@ -434,8 +437,7 @@ int launch2_impl(const Gemm2Args &a, int num_sms, cudaStream_t st) {
     const int total = a.n_pairs * a.n_ntiles;
     int clusters = num_sms / 2;
     if (total < clusters) clusters = total;
-    kern<<<2 * clusters, kThreads2, smem, st>>>(a);
-    return (int)cudaGetLastError();
+    return (int)launch_pdl(kern, dim3(2 * clusters), dim3(kThreads2), smem, st, a);
 }
 
 }  // namespace

@@ -196,8 +196,11 @@ def smlm_launch_count() -> int:
     return int(_lib.smlm_launch_count())
 
 
-def smlm_profile_enable(on: bool):
-    _lib.smlm_profile_enable(int(bool(on)))
+def smlm_profile_enable(mask):
+    """Bitmask of kernel classes to time (bool True = all classes)."""
+    if isinstance(mask, bool):
+        mask = 0xF if mask else 0
+    _lib.smlm_profile_enable(int(mask))
 
 
 def smlm_profile_read(kind: int):
