@@ -275,6 +275,7 @@ struct WsLayout {
     size_t spart_off = 0, spart_bytes = 0; // bf16 fwd: K-split shrink partials
     size_t dpart_off = 0, dpart_bytes = 0; // bf16 fwd decode GEMM: split-K partials
     int dec_items = 0, dec_ksplit = 0;     // > 0: pure-decode batch takes the transposed split-K kernel
+    int dec_cmc = 1;
     std::vector<int> dec_uniq;             // distinct adapter slots of the decode batch
     bool decf = false;                     // fused single-launch decode kernel
     int decf_ksplit = 0;
@@ -326,7 +327,11 @@ WsLayout layout_for(smlm_pool p, const smlm_batch *b, const Plan &plan, bool bwd
             const int groups = (nst + 1) / 2;
             const int n_nt = (p->out + 127) / 128;
             const int n_vt = ((int)uniq.size() * p->r_pad + 127) / 128;
-            const int items = (n_nt + n_vt) * groups;
+            // opt-in (SMLM_DEC_MC=1): clusters of 4 row tiles share the X tile by TMA multicast;
+            // measured slower (the 4 CTAs must all release a stage before it is refilled)
+            const int cmc = getenv("SMLM_DEC_MC") ? 4 : 1;
+            L.dec_cmc = cmc;
+            const int items = ((n_nt + n_vt + cmc - 1) / cmc) * cmc * groups;
             int ks = p->num_sms / items;        // one wave
             if (const char *e = getenv("SMLM_DEC_KSPLIT")) ks = atoi(e);   // measurement override
             const int nkb = p->in / 64;
@@ -806,6 +811,8 @@ int smlm_forward(smlm_pool p, const smlm_batch *b, const void *X, const void *W,
         d.n_uniq = (int)L.dec_uniq.size();
         d.n_vt = (d.n_uniq * p->r_pad + 127) / 128;
         d.ksplit = L.dec_ksplit;
+        d.cmc = L.dec_cmc;
+        if (d.cmc > 1 && (rc = make_map(&d.tmX64, X, p->in, b->S, 64, 64, CU_TENSOR_MAP_SWIZZLE_128B))) return rc;
         d.K = p->in;
         d.N = p->out;
         d.r = p->r;

@@ -137,6 +137,7 @@ struct DecRow {        // one decode row, indexed by group*256 + m (m = position
 struct DecArgs {
     CUtensorMap tmW;    // W [out,in] box {64,128} SW128 (A operand: 128 W rows)
     CUtensorMap tmX;    // X [S,in]   box {64,128} SW128 (B operand: decode rows)
+    CUtensorMap tmX64;  // X [S,in]   box {64,64}  SW128 (multicast quarters of the decode rows)
     const SlotDev *slots;
     const DevTile *tiles;    // the short tiles (<= 4)
     const int *vt_slots;     // distinct adapter slots of the batch, ascending
@@ -147,6 +148,7 @@ struct DecArgs {
     int n_vt;           // ceil(n_uniq * r_pad / 128) stacked-adapter row tiles
     int n_uniq;
     int ksplit;
+    int cmc;            // cluster size sharing the X tile by TMA multicast (1 or 4)
     int K;
     int N;
     int r;

@@ -162,13 +162,36 @@ constexpr uint32_t kDA = 128 * 128;   // 128 rows x 64 k
 constexpr uint32_t kDB = 256 * 128;   // up to 256 decode rows x 64 k
 constexpr uint32_t kDStage = kDA + kDB;
 
+// item w -> (row tile, decode-row group, K split).  With clusters of C CTAs the C consecutive
+// items of a cluster share (split, group) and take C consecutive row tiles, so they can share the
+// decode rows' X tile through TMA multicast.  Stacked-adapter tiles come first; tiles past
+// n_vt + n_nt (cluster padding) are dummies (nt = -1).
 __device__ __forceinline__ void dec_item(const DecArgs &a, int w, int &nt, int &grp, int &split) {
-    split = w % a.ksplit;
-    const int rest = w / a.ksplit;
+    const int C = a.cmc;
+    const int n_all = a.n_vt + a.n_nt;
+    const int n_tg = (n_all + C - 1) / C;
+    const int rank = w % C;
+    int rest = w / C;
+    const int tg = rest % n_tg;
+    rest /= n_tg;
     grp = rest % a.n_groups;
-    // the stacked-adapter row tiles (several TMA descriptors per stage, the slowest items) go first
-    const int o = rest / a.n_groups;
-    nt = o < a.n_vt ? a.n_nt + o : o - a.n_vt;   // < n_nt: W rows; >= n_nt: stacked adapter rows
+    split = rest / a.n_groups;
+    const int o = tg * C + rank;
+    nt = o >= n_all ? -1 : (o < a.n_vt ? a.n_nt + o : o - a.n_vt);   // >= n_nt: stacked adapter rows
+}
+
+__device__ __forceinline__ void tma_load_2d_mc(uint32_t dst, const void *map, uint32_t bar, int c0, int c1,
+                                               uint16_t mask) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+        " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar), "h"(mask)
+        : "memory");
+}
+__device__ __forceinline__ void mma_commit_mc1(uint32_t bar, uint16_t mask) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
+                 ::"r"(bar), "h"(mask)
+                 : "memory");
 }
 
 template <int RP>
@@ -189,7 +212,7 @@ __global__ void __launch_bounds__(kDThreads, 1) smlm_dec_kernel(const __grid_con
     if (threadIdx.x == 0) {
         for (int s = 0; s < ST; ++s) {
             mbar_init(full_bar(s), 1);
-            mbar_init(empty_bar(s), 1);
+            mbar_init(empty_bar(s), args.cmc);   // released by the MMAs of every CTA of the cluster
         }
         mbar_init(accf0 + 0, 1);
         mbar_init(accf0 + 8, 1);
@@ -198,15 +221,25 @@ __global__ void __launch_bounds__(kDThreads, 1) smlm_dec_kernel(const __grid_con
         fence_mbar_init();
         tma_prefetch_desc(&args.tmW);
         tma_prefetch_desc(&args.tmX);
+        if (args.cmc > 1) tma_prefetch_desc(&args.tmX64);
     }
     if (warp == 2) tmem_alloc(tmem_slot, 512);
     tc_fence_before();
-    __syncthreads();
+    if (args.cmc > 1)
+        asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    else
+        __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *reinterpret_cast<volatile uint32_t *>(base_ptr + (tmem_slot - base));
+    pdl_wait();
     // programmatic dependent launch: the reduce grid may start (and park) while this one streams
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-    const int total = (args.n_nt + args.n_vt) * args.n_groups * args.ksplit;
+    const int C = args.cmc;
+    const int n_tg = (args.n_vt + args.n_nt + C - 1) / C;
+    const int total = n_tg * C * args.n_groups * args.ksplit;
+    uint32_t crank = 0;
+    if (C > 1) asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(crank));
+    const uint16_t mc_mask = (uint16_t)((1u << C) - 1u);
     const int nkb = args.K / kBK;
     constexpr int kAdPerTile = 128 / RP;   // adapters per stacked row tile
 
@@ -223,6 +256,7 @@ __global__ void __launch_bounds__(kDThreads, 1) smlm_dec_kernel(const __grid_con
             int nt, grp, split;
             dec_item(args, w, nt, grp, split);
             const int t0 = 2 * grp, nt_in = min(2, args.n_tiles - t0);
+            const bool dummy = nt < 0;
             const bool vt = nt >= args.n_nt;
             const int a0 = (nt - args.n_nt) * kAdPerTile;
             const int na = vt ? min(kAdPerTile, args.n_uniq - a0) : 0;
@@ -231,17 +265,26 @@ __global__ void __launch_bounds__(kDThreads, 1) smlm_dec_kernel(const __grid_con
             for (int kb = kb0; kb < kb1; ++kb) {
                 mbar_wait(empty_bar(stage), phase ^ 1);
                 if (lane == 0) {
-                    mbar_expect_tx(full_bar(stage), (vt ? (uint32_t)na * RP * 128u : kDA) + 16384u * nt_in);
-                    if (!vt) {
+                    const uint32_t abytes = dummy ? 0u : (vt ? (uint32_t)na * RP * 128u : kDA);
+                    mbar_expect_tx(full_bar(stage), abytes + 16384u * nt_in);
+                    if (dummy) {
+                    } else if (!vt) {
                         tma_load_2d(a_addr(stage), &args.tmW, full_bar(stage), kb * kBK, nt * 128);
                     } else {
                         for (int i = 0; i < na; ++i)
                             tma_load_2d(a_addr(stage) + (uint32_t)i * RP * 128u, &args.slots[args.vt_slots[a0 + i]].tmA,
                                         full_bar(stage), kb * kBK, 0);
                     }
-                    for (int t = 0; t < nt_in; ++t)
-                        tma_load_2d(b_addr(stage) + 16384u * t, &args.tmX, full_bar(stage), kb * kBK,
-                                    args.tiles[t0 + t].row0);
+                    if (C == 1) {
+                        for (int t = 0; t < nt_in; ++t)
+                            tma_load_2d(b_addr(stage) + 16384u * t, &args.tmX, full_bar(stage), kb * kBK,
+                                        args.tiles[t0 + t].row0);
+                    } else {
+                        // quarter crank of the (<= 256)-row X tile, multicast to the whole cluster
+                        for (int qq = (int)crank; qq < 2 * nt_in; qq += C)
+                            tma_load_2d_mc(b_addr(stage) + 8192u * qq, &args.tmX64, full_bar(stage), kb * kBK,
+                                           args.tiles[t0 + qq / 2].row0 + 64 * (qq & 1), mc_mask);
+                    }
                 }
                 __syncwarp();
                 if (++stage == ST) { stage = 0; phase ^= 1; }
@@ -276,7 +319,10 @@ __global__ void __launch_bounds__(kDThreads, 1) smlm_dec_kernel(const __grid_con
                                  acc_on);
                         acc_on = 1;
                     }
-                    mma_commit(empty_bar(stage));
+                    if (C == 1)
+                        mma_commit(empty_bar(stage));
+                    else
+                        mma_commit_mc1(empty_bar(stage), mc_mask);
                 }
                 __syncwarp();
                 if (++stage == ST) { stage = 0; phase ^= 1; }
@@ -299,7 +345,7 @@ __global__ void __launch_bounds__(kDThreads, 1) smlm_dec_kernel(const __grid_con
             mbar_wait(accf0 + 8 * b, u & 1);
             tc_fence_after();
             float *mypart = args.part + ((size_t)pair * args.ksplit + split) * 256 * 128;
-            for (int c = 0; c < 128 * nt_in; c += 32) {
+            for (int c = 0; c < (nt < 0 ? 0 : 128 * nt_in); c += 32) {
                 uint32_t rr[32];
                 tmem_ld32(tmem_base + 256u * b + lane_base + c, rr);
                 tmem_wait_ld();
@@ -311,7 +357,10 @@ __global__ void __launch_bounds__(kDThreads, 1) smlm_dec_kernel(const __grid_con
             ++it;
         }
     }
-    __syncthreads();
+    if (C > 1)
+        asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    else
+        __syncthreads();
     if (warp == 2) {
         tc_fence_after();
         tmem_dealloc(tmem_base, 512);
@@ -433,9 +482,25 @@ int launch_dec_impl(const DecArgs &a, int num_sms, cudaStream_t st) {
         if (e != cudaSuccess) return (int)e;
         attr_done = true;
     }
-    const int total = (a.n_nt + a.n_vt) * a.n_groups * a.ksplit;
-    kern<<<total < num_sms ? total : num_sms, kDThreads, smem, st>>>(a);
-    cudaError_t e = cudaGetLastError();
+    const int n_tg = (a.n_nt + a.n_vt + a.cmc - 1) / a.cmc;
+    const int total = n_tg * a.cmc * a.n_groups * a.ksplit;
+    int grid = total < num_sms ? total : num_sms;
+    grid -= grid % a.cmc;
+    cudaLaunchConfig_t c1 = {};
+    c1.gridDim = dim3(grid);
+    c1.blockDim = dim3(kDThreads);
+    c1.dynamicSmemBytes = smem;
+    c1.stream = st;
+    cudaLaunchAttribute at1[2];
+    at1[0].id = cudaLaunchAttributeClusterDimension;
+    at1[0].val.clusterDim.x = a.cmc;
+    at1[0].val.clusterDim.y = 1;
+    at1[0].val.clusterDim.z = 1;
+    at1[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at1[1].val.programmaticStreamSerializationAllowed = 1;
+    c1.attrs = at1;
+    c1.numAttrs = 2;
+    cudaError_t e = cudaLaunchKernelEx(&c1, kern, a);
     if (e != cudaSuccess) return (int)e;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(a.n_nt, a.n_groups * 32);

@@ -1,0 +1,160 @@
+"""GPU checks of the C-ABI contract (include/smlm.h): slot lifecycle, capacity, errors reported
+before any device work, workspace sizing, option handling, plan export on a live pool."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+from oracle import plan as plan_oracle
+from synth import DECODE, FINETUNE, PREFILL
+from tests.util import BF16_TOL, parity_err
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def S():
+    from paper_2511_00101_b200 import smlm
+    return smlm
+
+
+def _adapters(in_f, out_f, r, n, seed=0):
+    g = torch.Generator().manual_seed(seed)
+    w = synth.draw_weights(g, in_f, out_f, r, n)
+    return w, [a.cuda() for a in w.A], [b.cuda() for b in w.B]
+
+
+def test_pool_errors(S):
+    with pytest.raises(S.SmlmError) as e:
+        S.smlm_pool_create(0, 64, 64, 12, 4, S.SMLM_BF16)      # rank not in {8,16,32,64}
+    assert e.value.code == S.SMLM_E_UNSUPPORTED
+    with pytest.raises(S.SmlmError) as e:
+        S.smlm_pool_create(0, 100, 64, 16, 4, S.SMLM_BF16)     # in not a multiple of 64
+    assert e.value.code == S.SMLM_E_UNSUPPORTED
+    with pytest.raises(S.SmlmError) as e:
+        S.smlm_pool_create(0, 64, 64, 16, 0, S.SMLM_BF16)
+    assert e.value.code == S.SMLM_E_INVALID
+    with pytest.raises(S.SmlmError) as e:
+        S.smlm_pool_create(99, 64, 64, 16, 4, S.SMLM_BF16)
+    assert e.value.code == S.SMLM_E_UNSUPPORTED
+
+
+def test_slot_lifecycle_and_capacity(S):
+    w, A, B = _adapters(128, 128, 16, 3)
+    pool = S.Pool(128, 128, 16, 2, S.SMLM_BF16, 0)
+    assert pool.register(A[0], B[0], 2.0) == 0
+    assert pool.register(A[1], B[1], 2.0) == 1
+    with pytest.raises(S.SmlmError) as e:
+        pool.register(A[2], B[2], 2.0)
+    assert e.value.code == S.SMLM_E_CAPACITY
+    with pytest.raises(S.SmlmError) as e:
+        pool.register(A[2], B[2], 0.0)                            # scale must be > 0
+    assert e.value.code == S.SMLM_E_INVALID
+    pool.unregister(0)
+    with pytest.raises(S.SmlmError) as e:
+        pool.unregister(0)
+    assert e.value.code == S.SMLM_E_SLOT
+    # a batch referencing the freed slot is rejected before any device work
+    b = S.Batch([0, 3], [0], [PREFILL])
+    X = torch.randn(3, 128, device="cuda").to(torch.bfloat16)
+    Y = torch.full((3, 128), 7.0, device="cuda", dtype=torch.bfloat16)
+    ws = torch.empty(1 << 20, dtype=torch.uint8, device="cuda")
+    with pytest.raises(S.SmlmError) as e:
+        S.smlm_forward(pool.h, b, X, w.W.cuda(), Y, None, ws)
+    assert e.value.code == S.SMLM_E_SLOT
+    assert torch.all(Y == 7.0)                                    # outputs untouched on error
+    # slot reuse: registering again takes the freed slot and computes with the NEW adapter
+    assert pool.register(A[2], B[2], 2.0) == 0
+    b = S.Batch([0, 3], [0], [PREFILL])
+    pool.forward(b, X, w.W.cuda(), Y)
+    torch.cuda.synchronize()
+    batch = synth.batch_from_lengths([3], [0], [PREFILL])
+    Yr, _ = oracle.forward(batch, w.W, [w.A[2]], [w.B[2]], [2.0], X.cpu())
+    assert parity_err(Y.cpu(), Yr) <= BF16_TOL
+    pool.close()
+
+
+def test_workspace_and_batch_validation(S):
+    w, A, B = _adapters(128, 192, 16, 2)
+    pool = S.Pool(128, 192, 16, 2, S.SMLM_BF16, 0)
+    for i in range(2):
+        pool.register(A[i], B[i], 2.0)
+    b = S.Batch([0, 70, 75], [0, 1], [FINETUNE, DECODE])
+    need = S.smlm_workspace_size(pool.h, b, False)
+    assert need > 0
+    X = torch.randn(75, 128, device="cuda").to(torch.bfloat16)
+    Y = torch.zeros(75, 192, device="cuda", dtype=torch.bfloat16)
+    small = torch.empty(max(need - 256, 16), dtype=torch.uint8, device="cuda")
+    with pytest.raises(S.SmlmError) as e:
+        S.smlm_forward(pool.h, b, X, w.W.cuda(), Y, None, small)
+    assert e.value.code == S.SMLM_E_WORKSPACE
+    bad = S.Batch([0, 80, 75], [0, 1], [FINETUNE, DECODE])          # decreasing offsets
+    with pytest.raises(S.SmlmError) as e:
+        S.smlm_forward(pool.h, bad, X, w.W.cuda(), Y, None, pool.workspace(b))
+    assert e.value.code == S.SMLM_E_INVALID
+    badm = S.Batch([0, 70, 75], [0, 1], [FINETUNE, 7])               # mode out of range
+    with pytest.raises(S.SmlmError) as e:
+        S.smlm_forward(pool.h, badm, X, w.W.cuda(), Y, None, pool.workspace(b))
+    assert e.value.code == S.SMLM_E_INVALID
+    # live-pool plan export equals the oracle plan; L_long option changes it consistently
+    assert pool.plan(b) == plan_oracle.forward_plan(b.offsets, b.slots, b.modes)
+    pool.set_option(S.SMLM_OPT_L_LONG, 1)
+    assert pool.plan(b) == plan_oracle.forward_plan(b.offsets, b.slots, b.modes, l_long=1)
+    with pytest.raises(S.SmlmError):
+        pool.set_option(S.SMLM_OPT_L_LONG, 0)
+    pool.close()
+
+
+@pytest.mark.parametrize("cta_pair", [0, 1])
+def test_cta_pair_option_same_result(S, cta_pair):
+    """The 1-CTA and CTA-pair tensor-core kernels both match the oracle on the same batch."""
+    lengths = [300, 3, 1, 130, 200]
+    modes = [FINETUNE, DECODE, DECODE, PREFILL, FINETUNE]
+    batch, w, X, dY = synth.random_case(3, 256, 320, 16, 3, lengths, modes, [0, 1, 2, 1, -1])
+    pool = S.Pool(256, 320, 16, 3, S.SMLM_BF16, 0)
+    pool.set_option(S.SMLM_OPT_CTA_PAIR, cta_pair)
+    A = [a.cuda() for a in w.A]
+    B = [b.cuda() for b in w.B]
+    for i in range(3):
+        pool.register(A[i], B[i], w.slot_scale[i])
+    dA = torch.zeros(3, 16, 256, device="cuda")
+    dB = torch.zeros(3, 320, 16, device="cuda")
+    for i in range(3):
+        pool.set_grad(i, dA[i], dB[i])
+    b = S.Batch.from_synth(batch)
+    Xd, Wd, dYd = X.cuda(), w.W.cuda(), dY.cuda()
+    Y = pool.forward(b, Xd, Wd)
+    dX = torch.zeros_like(Xd)
+    pool.backward(b, Xd, Wd, dYd, None, dX)
+    torch.cuda.synchronize()
+    Yr, _ = oracle.forward(batch, w.W, w.A, w.B, w.slot_scale, X)
+    dXr, dAr, dBr = oracle.backward(batch, w.W, w.A, w.B, w.slot_scale, X, dY)
+    ft = batch.ft_rows()
+    assert parity_err(Y.cpu(), Yr) <= BF16_TOL
+    assert parity_err(dX.cpu()[ft], dXr[ft]) <= BF16_TOL
+    for a in (0,):
+        assert parity_err(dA[a].cpu(), dAr[a]) <= BF16_TOL and parity_err(dB[a].cpu(), dBr[a]) <= BF16_TOL
+    pool.close()
+
+
+def test_launch_count_and_no_host_sync(S):
+    """Calls are asynchronous (no host sync) and every call launches library kernels."""
+    w, A, B = _adapters(256, 256, 16, 2)
+    pool = S.Pool(256, 256, 16, 2, S.SMLM_BF16, 0)
+    for i in range(2):
+        pool.register(A[i], B[i], 2.0)
+    b = S.Batch([0, 200, 203], [0, 1], [PREFILL, DECODE])
+    X = torch.randn(203, 256, device="cuda").to(torch.bfloat16)
+    Wd = w.W.cuda()
+    n0 = S.smlm_launch_count()
+    side = torch.cuda.Stream()
+    with torch.cuda.stream(side):
+        torch.cuda._sleep(20_000_000)                 # keep the GPU busy ~10 ms on this stream
+        Y = pool.forward(b, X, Wd, stream=side)
+        done = torch.cuda.Event()
+        done.record(side)
+    assert not done.query()                           # the call returned before the GPU finished
+    torch.cuda.synchronize()
+    assert S.smlm_launch_count() - n0 >= 2
+    pool.close()
