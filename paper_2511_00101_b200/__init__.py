@@ -7,7 +7,13 @@ so that `python -m paper_2511_00101_b200.build` works before the library exists.
 """
 import importlib
 
+_SUBMODULES = ("build", "smlm", "dp")
+
 
 def __getattr__(name):
+    if name in _SUBMODULES:
+        return importlib.import_module("." + name, __name__)
+    if name.startswith("__"):
+        raise AttributeError(name)
     mod = importlib.import_module(".smlm", __name__)
     return getattr(mod, name)
