@@ -38,7 +38,9 @@
  *
  * Threading: all work is stream-ordered on the given stream with no host synchronisation
  * (the plan is staged through a pinned ring buffer).  A pool must be used by one host thread
- * at a time.
+ * at a time, and its forward calls must be ordered on one stream (or otherwise serialised):
+ * the decode kernel keeps self-resetting cross-CTA counters in pool-owned device memory.
+ * Each launch of that kernel needs its CTAs co-resident (one wave of <= 148 CTAs).
  */
 #ifndef SMLM_H_
 #define SMLM_H_
@@ -141,6 +143,24 @@ SMLM_API size_t smlm_workspace_size(smlm_pool pool, const smlm_batch *batch, int
  */
 SMLM_API int smlm_forward(smlm_pool pool, const smlm_batch *batch, const void *X, const void *W, void *Y,
                  void *V_save, void *ws, size_t ws_bytes, void *stream);
+
+/*
+ * Multi-projection forward (Alg. 1 P:331 computes q, k, v of a layer from
+ * the same hidden states): for i in [0, n_proj), exactly the result of
+ *     smlm_forward(pools[i], batch, X, W[i], Y[i], V_save ? V_save[i] : NULL, ...)
+ * up to the fp32 summation order (within the bf16 tolerance), but a pure short/decode batch
+ * (<= 512 rows, no segment >= L_long) runs as ONE launch that streams every W[i] once and reads X
+ * once.  Other batches run the per-pool calls in sequence.
+ *   n_proj in [1, 4]; pools share device, in_features, rank and dtype; every slot of the batch
+ *   must be registered in every pool with the same slot scale (else SMLM_E_SLOT);
+ *   W[i] != NULL; Y[i] [S, out_i]; V_save NULL or an array of n_proj pointers (each may be NULL).
+ *   ws: ws_bytes >= smlm_workspace_size_multi(n_proj, pools, batch).
+ * The decode kernel uses pools[0]'s counters: calls that share pools[0] must be stream-ordered.
+ */
+SMLM_API size_t smlm_workspace_size_multi(int n_proj, const smlm_pool *pools, const smlm_batch *batch);
+SMLM_API int smlm_forward_multi(int n_proj, const smlm_pool *pools, const smlm_batch *batch, const void *X,
+                                const void *const *W, void *const *Y, void *const *V_save, void *ws,
+                                size_t ws_bytes, void *stream);
 
 /*
  * Backward over FINETUNE rows.

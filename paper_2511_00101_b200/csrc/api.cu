@@ -42,13 +42,12 @@ template <typename TV>
 int launch_prep_sv(const DevTile *tiles, int n_tiles, const TV *V, int r, int r_pad, __nv_bfloat16 *sVt,
                    cudaStream_t st);
 int launch_tok(const TokArgs &a, int num_sms, cudaStream_t st);
-int dec_stages();
 int dec_chunks(int in_f);
+int dec3_stages();
+int launch_dec3(const Dec3Args &a, int clusters, cudaStream_t st);
 int launch_shrink_split(const __nv_bfloat16 *X, const SlotDev *slots, const DevBlock *blocks,
                         const DevShortRow *srows, int n_blocks, int in_f, int r, int r_pad, float *part,
                         __nv_bfloat16 *Vbd, __nv_bfloat16 *Vsave, cudaStream_t st);
-int launch_dec(const DecArgs &a, int num_sms, cudaStream_t st);
-int launch_decf(const DecFArgs &a, cudaStream_t st);
 size_t grad_group_bytes();
 void fill_grad_group(void *dst, int slot, int tile_begin, int n_tiles, float *dA, float *dB);
 template <typename T, typename TV>
@@ -237,8 +236,7 @@ struct smlm_pool_s {
     std::vector<uint8_t> ok;
     std::vector<float> scales;
     SlotDev *d_slots = nullptr;
-    unsigned long long *d_counter = nullptr;   // fused decode kernel: release counter
-    unsigned long long dec_epoch = 0;
+    int *d_ctr = nullptr;   // decode kernel: self-resetting cross-CTA counters (dec3_counter_ints())
     Ring ring;
 };
 
@@ -273,13 +271,6 @@ struct WsLayout {
     int u_items = 0, u_ksplit = 0;
     size_t vf_off = 0, vf_bytes = 0;       // fp32 V [S,r] (fp32 mode, or bwd recompute)
     size_t spart_off = 0, spart_bytes = 0; // bf16 fwd: K-split shrink partials
-    size_t dpart_off = 0, dpart_bytes = 0; // bf16 fwd decode GEMM: split-K partials
-    int dec_items = 0, dec_ksplit = 0;     // > 0: pure-decode batch takes the transposed split-K kernel
-    int dec_cmc = 1;
-    std::vector<int> dec_uniq;             // distinct adapter slots of the decode batch
-    bool decf = false;                     // fused single-launch decode kernel
-    int decf_ksplit = 0;
-    size_t vg_off = 0;
     size_t total = 0;
 };
 
@@ -292,14 +283,107 @@ int plan_for(smlm_pool p, const smlm_batch *b, bool bwd, Plan &plan) {
     return SMLM_OK;
 }
 
+// ------------------------------------------------------------------------------------------
+// decode path v3 (kernels_dec3.cu): pure short batches of <= 512 rows, one or several
+// projections that share X in one launch.
+// ------------------------------------------------------------------------------------------
+struct Dec3Plan {
+    bool ok = false;
+    std::vector<int> uslot, uoff, row_uidx;
+    std::vector<Dec3Row> urows;
+    std::vector<Dec3SItem> sitems;
+    int n_groups = 0, nw = 0, ks = 1, n_wpairs = 0, clusters = 0;
+    size_t plan_off = 0, sv_off[kDec3MaxProj] = {}, kpart_off = 0, total = 0;
+};
+
+// pools[0..n) share in, r and dtype (validated by the caller); every batch slot is registered in
+// all of them.  ok = false if the batch cannot take the single-launch kernel.
+Dec3Plan dec3_plan(int n_proj, const smlm_pool *pools, const smlm_batch *b, const Plan &plan) {
+    Dec3Plan D;
+    smlm_pool p0 = pools[0];
+    if (p0->dtype != SMLM_BF16 || !plan.long_tiles.empty() || plan.short_tiles.empty() || b->S > 512 ||
+        getenv("SMLM_NO_DEC3"))
+        return D;
+    // adapters of the batch (ascending), their rows (ascending), per-row adapter index
+    std::vector<std::vector<Dec3Row>> by_slot(p0->cap);
+    for (auto &bk : plan.blocks)
+        for (int i = 0; i < bk.nrows; ++i) {
+            const DevShortRow &sr = plan.short_rows[bk.row_begin + i];
+            by_slot[bk.slot].push_back(Dec3Row{sr.row, sr.scale, sr.ft, 0});
+        }
+    D.row_uidx.assign(b->S, -1);
+    D.uoff.push_back(0);
+    for (int sl = 0; sl < p0->cap; ++sl) {
+        if (by_slot[sl].empty()) continue;
+        std::sort(by_slot[sl].begin(), by_slot[sl].end(),
+                  [](const Dec3Row &x, const Dec3Row &y) { return x.row < y.row; });
+        const int u = (int)D.uslot.size();
+        D.uslot.push_back(sl);
+        for (auto &r : by_slot[sl]) D.row_uidx[r.row] = u;
+        D.urows.insert(D.urows.end(), by_slot[sl].begin(), by_slot[sl].end());
+        D.uoff.push_back((int)D.urows.size());
+    }
+    const int n_uniq = (int)D.uslot.size();
+    for (int p = 0; p < n_proj; ++p)
+        for (int u = 0; u < n_uniq; ++u) {
+            uint32_t mask[16] = {0};
+            for (int i = D.uoff[u]; i < D.uoff[u + 1]; ++i) mask[D.urows[i].row >> 5] |= 1u << (D.urows[i].row & 31);
+            for (int rb = D.uoff[u]; rb < D.uoff[u + 1]; rb += 8) {
+                Dec3SItem it;
+                memset(&it, 0, sizeof(it));
+                it.A = pools[p]->slots[D.uslot[u]].A;
+                it.p = p;
+                it.uidx = u;
+                it.n = std::min(8, D.uoff[u + 1] - rb);
+                it.zero_fill = rb == D.uoff[u];
+                for (int i = 0; i < it.n; ++i) {
+                    it.rows[i] = D.urows[rb + i].row;
+                    it.scale[i] = D.urows[rb + i].scale;
+                    if (D.urows[rb + i].ft) it.ft_mask |= 1 << i;
+                }
+                memcpy(it.mask, mask, sizeof(mask));
+                D.sitems.push_back(it);
+            }
+        }
+    const int n_si = (int)D.sitems.size();
+    D.n_groups = (b->S + 255) / 256;
+    for (int i = 0; i < n_proj; ++i) D.nw += (pools[i]->out + 255) / 256;
+    const int pairs = std::min(p0->num_sms / 2, kDec3MaxPairs);
+    const int NW = D.n_groups * D.nw;
+    const int nkb = p0->in / kBK;
+    // the shrink pairs take the rest of the wave: at least ~a third of the items' worth
+    const int sp_min = n_si ? std::max(1, std::min(pairs / 3, (n_si + 2) / 3)) : 0;
+    if (NW > pairs - sp_min) return D;   // more W tiles than one wave: not this kernel
+    int ks = (pairs - sp_min) / NW;
+    if (const char *e = getenv("SMLM_DEC_KSPLIT")) ks = atoi(e);   // measurement override
+    ks = std::max(1, std::min({ks, 8, std::max(1, nkb / 2)}));
+    while (ks > 1 && NW * ks > pairs - sp_min) --ks;
+    D.ks = ks;
+    D.n_wpairs = NW * ks;
+    D.clusters = n_si ? pairs : D.n_wpairs;
+    if (NW > 256) return D;   // tile arrival counters
+    if (n_si && (n_si + (D.clusters - D.n_wpairs) - 1) / (D.clusters - D.n_wpairs) > kDec3MaxShrinkItems) return D;
+    size_t off = 0;
+    D.plan_off = off;
+    off = align256(off + (size_t)n_uniq * 4 + 64 + D.sitems.size() * sizeof(Dec3SItem));
+    for (int i = 0; i < n_proj; ++i) {
+        D.sv_off[i] = off;
+        off = align256(off + (size_t)D.n_groups * std::max(n_uniq, 1) * 256 * p0->r_pad * 2);
+    }
+    D.kpart_off = off;
+    if (ks > 1) off = align256(off + (size_t)D.n_wpairs * 2 * 8 * kDec3ChunkBytes);
+    if (getenv("SMLM_DEC3_DEBUG")) off += 2 * kDec3MaxPairs * 16 * 8;   // phase timestamps at the tail
+    D.total = off;
+    D.ok = true;
+    return D;
+}
+
 WsLayout layout_for(smlm_pool p, const smlm_batch *b, const Plan &plan, bool bwd, bool need_vf) {
     WsLayout L;
     size_t off = 0;
     if (!bwd) {
         L.plan_bytes = (plan.long_tiles.size() + plan.short_tiles.size()) * sizeof(DevTile) +
-                       plan.blocks.size() * sizeof(DevBlock) + plan.short_rows.size() * sizeof(DevShortRow) +
-                       // decode-path extras: distinct slots + per-row records (<= 4 short tiles)
-                       (size_t)p->cap * 4 + 4 * 128 * sizeof(DecRow) + 64 +
+                       plan.blocks.size() * sizeof(DevBlock) + plan.short_rows.size() * sizeof(DevShortRow) + 16 +
                        (plan.long_tiles.size() + plan.short_tiles.size()) * sizeof(DevPair) + 16;
     } else {
         L.plan_bytes = plan.bwd_tiles.size() * (sizeof(DevTile) + 4 + sizeof(DevPair)) +
@@ -317,56 +401,10 @@ WsLayout layout_for(smlm_pool p, const smlm_batch *b, const Plan &plan, bool bwd
             L.spart_bytes = plan.blocks.size() * (size_t)nch * 128 * p->r_pad * 4;
             off = align256(off + L.spart_bytes);
         }
-        // pure decode / short batches (<= 512 rows in <= 4 short tiles): transposed split-K GEMM
-        const int nst = (int)plan.short_tiles.size();
-        if (plan.long_tiles.empty() && nst > 0 && nst <= 4) {
-            std::vector<int> uniq;
-            for (auto &bk : plan.blocks) uniq.push_back(bk.slot);
-            std::sort(uniq.begin(), uniq.end());
-            uniq.erase(std::unique(uniq.begin(), uniq.end()), uniq.end());
-            const int groups = (nst + 1) / 2;
-            const int n_nt = (p->out + 127) / 128;
-            const int n_vt = ((int)uniq.size() * p->r_pad + 127) / 128;
-            // opt-in (SMLM_DEC_MC=1): clusters of 4 row tiles share the X tile by TMA multicast;
-            // measured slower (the 4 CTAs must all release a stage before it is refilled)
-            const int cmc = getenv("SMLM_DEC_MC") ? 4 : 1;
-            L.dec_cmc = cmc;
-            const int items = ((n_nt + n_vt + cmc - 1) / cmc) * cmc * groups;
-            int ks = p->num_sms / items;        // one wave
-            if (const char *e = getenv("SMLM_DEC_KSPLIT")) ks = atoi(e);   // measurement override
-            const int nkb = p->in / 64;
-            const int ks_bytes = p->in / 256;   // partials <= ~2x the W bytes
-            if (ks > ks_bytes) ks = ks_bytes;
-            if (ks > nkb / 2) ks = nkb / 2;
-            if (ks < 1) ks = 1;
-            L.dec_items = items;
-            L.dec_ksplit = ks;
-            L.dec_uniq = uniq;
-            // <= 256 decode rows: fused single-launch kernel (DSMEM split-K reduction, in-kernel expand)
-            // experimental (opt-in, SMLM_DECF=1): measured slower than the two-kernel path so far
-            if (nst <= 2 && getenv("SMLM_DECF")) {
-                const int tiles_f = n_nt + n_vt;
-                const int m_rows = 128 * nst;
-                // power-of-two cluster <= 8 (portable): every cluster of a GPC-sized group co-resides
-                int kf = 1;
-                while (kf * 2 <= 8 && tiles_f * kf * 2 <= p->num_sms) kf *= 2;
-                if (const char *e = getenv("SMLM_DECF_KSPLIT")) kf = atoi(e);
-                if (kf > nkb) kf = nkb;
-                if (kf * 64 < m_rows) kf = (m_rows + 63) / 64;   // <= 64 decode rows per CTA slice
-                if (kf <= 8 && kf <= nkb && tiles_f * kf <= p->num_sms) {
-                    L.decf = true;
-                    L.decf_ksplit = kf;
-                }
-            }
-            if (L.decf) {
-                L.vg_off = off;
-                off = align256(off + 256 * (size_t)p->r_pad * 4);
-            } else {
-                L.dpart_off = off;
-                L.dpart_bytes = (size_t)items * ks * 256 * 128 * 4;
-                off = align256(off + L.dpart_bytes);
-            }
-        }
+    }
+    if (!bwd) {
+        const Dec3Plan D = dec3_plan(1, &p, b, plan);
+        if (D.ok) off = std::max(off, D.total);   // the decode path uses its own layout from offset 0
     }
     if (bwd && p->dtype == SMLM_FP32) {
         L.u_off = off;
@@ -417,6 +455,61 @@ int stage_upload(smlm_pool p, const std::vector<uint8_t> &bytes, void *dst, cuda
 template <typename T> void append(std::vector<uint8_t> &v, const std::vector<T> &x) {
     const uint8_t *s = reinterpret_cast<const uint8_t *>(x.data());
     v.insert(v.end(), s, s + x.size() * sizeof(T));
+}
+
+int run_dec3(int n_proj, const smlm_pool *pools, const smlm_batch *b, const Dec3Plan &D, const void *X,
+             const void *const *W, void *const *Y, void *const *Vsave, uint8_t *wsb, cudaStream_t st) {
+    smlm_pool p0 = pools[0];
+    const int n_uniq = (int)D.uslot.size();
+    std::vector<uint8_t> bytes;
+    append(bytes, D.uslot);
+    while (bytes.size() % 16) bytes.push_back(0);
+    const size_t si_off = bytes.size();
+    append(bytes, D.sitems);
+    int rc;
+    if ((rc = stage_upload(p0, bytes, wsb + D.plan_off, st))) return rc;
+    Dec3Args a;
+    memset(&a, 0, sizeof(a));
+    if ((rc = make_map(&a.tmX, X, p0->in, b->S, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B))) return rc;
+    int nt0 = 0;
+    for (int i = 0; i < n_proj; ++i) {
+        Dec3Proj &P = a.proj[i];
+        if ((rc = make_map(&P.tmW, W[i], p0->in, pools[i]->out, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B))) return rc;
+        if ((rc = make_map(&P.tmY, Y[i], pools[i]->out, b->S, 32, 128, CU_TENSOR_MAP_SWIZZLE_NONE))) return rc;
+        P.sv = wsb + D.sv_off[i];
+        if (n_uniq > 0 && (rc = make_map(&P.tmSV, P.sv, p0->r_pad, (uint64_t)D.n_groups * n_uniq * 256, p0->r_pad,
+                                         128, swizzle_for(p0->r_pad * 2))))
+            return rc;
+        P.slots = pools[i]->d_slots;
+        P.Vsave = Vsave ? Vsave[i] : nullptr;
+        P.out = pools[i]->out;
+        P.nt0 = nt0;
+        P.n_wt = (pools[i]->out + 255) / 256;
+        nt0 += P.n_wt;
+    }
+    a.X = X;
+    a.uslot = reinterpret_cast<const int *>(wsb + D.plan_off);
+    a.sitems = reinterpret_cast<const Dec3SItem *>(wsb + D.plan_off + si_off);
+    a.kpart = reinterpret_cast<float *>(wsb + D.kpart_off);
+    a.ctr = p0->d_ctr;
+    a.n_proj = n_proj;
+    a.n_uniq = n_uniq;
+    a.n_sitems = (int)D.sitems.size();
+    a.n_groups = D.n_groups;
+    a.n_wt = D.nw;
+    a.ks = D.ks;
+    a.n_wpairs = D.n_wpairs;
+    a.S = b->S;
+    a.K = p0->in;
+    a.r = p0->r;
+    a.r_pad = p0->r_pad;
+    a.stages = dec3_stages();
+    if (const char *e = getenv("SMLM_DEC3_EXPT")) a.flags = atoi(e);
+    if (getenv("SMLM_DEC3_DEBUG"))
+        a.dbg = reinterpret_cast<unsigned long long *>(wsb + D.total - 2 * kDec3MaxPairs * 16 * 8);
+    ProfScope ps(0, st);
+    CKL(launch_dec3(a, D.clusters, st), 1);
+    return SMLM_OK;
 }
 
 }  // namespace
@@ -513,8 +606,8 @@ int smlm_pool_create(int device, int in_features, int out_features, int rank, in
         delete p;
         return cuda_err(e, "cudaMalloc(slot table)");
     }
-    if (e == cudaSuccess) e = cudaMalloc(&p->d_counter, 64);
-    if (e == cudaSuccess) e = cudaMemset(p->d_counter, 0, 64);
+    if (e == cudaSuccess) e = cudaMalloc(&p->d_ctr, sizeof(int) * dec3_counter_ints());
+    if (e == cudaSuccess) e = cudaMemset(p->d_ctr, 0, sizeof(int) * dec3_counter_ints());
     if (e == cudaSuccess) e = cudaMemset(p->d_slots, 0, sizeof(SlotDev) * capacity);
     if (e != cudaSuccess) {
         cudaFree(p->d_slots);
@@ -531,7 +624,7 @@ int smlm_pool_destroy(smlm_pool p) {
         DeviceGuard dg(p->device);
         cudaDeviceSynchronize();
         if (p->d_slots) cudaFree(p->d_slots);
-        if (p->d_counter) cudaFree(p->d_counter);
+        if (p->d_ctr) cudaFree(p->d_ctr);
     }
     delete p;
     return SMLM_OK;
@@ -685,6 +778,11 @@ int smlm_forward(smlm_pool p, const smlm_batch *b, const void *X, const void *W,
 
     // ---------------- bf16 tensor-core path ----------------
     const bool has_w = W != nullptr;
+    if (has_w) {
+        // pure short / decode batch: one launch (kernels_dec3.cu)
+        const Dec3Plan D = dec3_plan(1, &p, b, plan);
+        if (D.ok) return run_dec3(1, &p, b, D, X, &W, &Y, &V_save, wsb, st);
+    }
     std::vector<DevTile> tiles;
     tiles.reserve(plan.long_tiles.size() + plan.short_tiles.size());
     for (auto &t : plan.long_tiles)
@@ -741,90 +839,6 @@ int smlm_forward(smlm_pool p, const smlm_batch *b, const void *X, const void *W,
     const DevShortRow *d_srows = reinterpret_cast<const DevShortRow *>(wsb + L.plan_off + srow_off);
     __nv_bfloat16 *Vbd = reinterpret_cast<__nv_bfloat16 *>(wsb + L.vbd_off);
 
-    if (has_w && L.dec_items > 0) {
-        // pure decode batch: one streaming pass over [W ; A_u] (base rows + rank-r rows of every
-        // adapter in the batch) with split K, then a wide reduce + expand pass
-        const int groups = ((int)tiles.size() + 1) / 2;
-        std::vector<DecRow> drows((size_t)groups * 256, DecRow{-1, -1, 0.f, 0});
-        std::vector<int> uidx_of(p->cap, -1);
-        for (size_t i = 0; i < L.dec_uniq.size(); ++i) uidx_of[L.dec_uniq[i]] = (int)i;
-        for (size_t t = 0; t < tiles.size(); ++t) {
-            const DevTile &tl = tiles[t];
-            for (int m = 0; m < tl.rows; ++m) drows[t * 128 + m] = DecRow{tl.row0 + m, -1, 0.f, 0};
-            for (int bi = 0; bi < tl.nblk; ++bi) {
-                const DevBlock &bk = plan.blocks[tl.blk0 + bi];
-                for (int i = 0; i < bk.nrows; ++i) {
-                    const DevShortRow &sr = plan.short_rows[bk.row_begin + i];
-                    drows[t * 128 + sr.pos] = DecRow{sr.row, uidx_of[bk.slot], sr.scale, sr.ft};
-                }
-            }
-        }
-        std::vector<uint8_t> extra;
-        const size_t vt_off = bytes.size();
-        append(extra, L.dec_uniq);
-        while (extra.size() % 16) extra.push_back(0);
-        const size_t rows_off = vt_off + extra.size();
-        append(extra, drows);
-        bytes.insert(bytes.end(), extra.begin(), extra.end());
-        if ((rc = stage_upload(p, bytes, wsb + L.plan_off, st))) return rc;
-        if (L.decf) {
-            DecFArgs f;
-            memset(&f, 0, sizeof(f));
-            if ((rc = make_map(&f.tmW, W, p->in, p->out, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B))) return rc;
-            if ((rc = make_map(&f.tmX, X, p->in, b->S, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B))) return rc;
-            f.slots = p->d_slots;
-            f.vt_slots = reinterpret_cast<const int *>(wsb + L.plan_off + vt_off);
-            f.rows = reinterpret_cast<const DecRow *>(wsb + L.plan_off + rows_off);
-            for (size_t t = 0; t < tiles.size() && t < 2; ++t) f.tile_row0[t] = tiles[t].row0;
-            f.n_uniq = (int)L.dec_uniq.size();
-            f.n_vt = (f.n_uniq * p->r_pad + 127) / 128;
-            f.n_nt = (p->out + 127) / 128;
-            f.ksplit = L.decf_ksplit;
-            f.m_rows = 128 * (int)tiles.size();
-            f.K = p->in;
-            f.N = p->out;
-            f.r = p->r;
-            f.r_pad = p->r_pad;
-            f.stages = dec_stages();
-            f.Y = Y;
-            f.Vsave = V_save;
-            f.Vg = reinterpret_cast<float *>(wsb + L.vg_off);
-            f.v_done = p->d_counter;
-            p->dec_epoch += 1;
-            f.v_target = p->dec_epoch * (unsigned long long)(f.n_vt * f.ksplit);
-            if (f.n_vt == 0) p->dec_epoch -= 1;
-            ProfScope ps(0, st);
-            CKL(launch_decf(f, st), 1);
-            return SMLM_OK;
-        }
-        DecArgs d;
-        memset(&d, 0, sizeof(d));
-        if ((rc = make_map(&d.tmW, W, p->in, p->out, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B))) return rc;
-        if ((rc = make_map(&d.tmX, X, p->in, b->S, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B))) return rc;
-        d.slots = p->d_slots;
-        d.tiles = d_tiles;  // only short tiles (no long tiles in a pure decode batch)
-        d.vt_slots = reinterpret_cast<const int *>(wsb + L.plan_off + vt_off);
-        d.rows = reinterpret_cast<const DecRow *>(wsb + L.plan_off + rows_off);
-        d.n_tiles = (int)tiles.size();
-        d.n_groups = groups;
-        d.n_nt = (p->out + 127) / 128;
-        d.n_uniq = (int)L.dec_uniq.size();
-        d.n_vt = (d.n_uniq * p->r_pad + 127) / 128;
-        d.ksplit = L.dec_ksplit;
-        d.cmc = L.dec_cmc;
-        if (d.cmc > 1 && (rc = make_map(&d.tmX64, X, p->in, b->S, 64, 64, CU_TENSOR_MAP_SWIZZLE_128B))) return rc;
-        d.K = p->in;
-        d.N = p->out;
-        d.r = p->r;
-        d.r_pad = p->r_pad;
-        d.stages = dec_stages();
-        d.Y = Y;
-        d.Vsave = V_save;
-        d.part = reinterpret_cast<float *>(wsb + L.dpart_off);
-        ProfScope ps(0, st);
-        CKL(launch_dec(d, p->num_sms, st), 2);
-        return SMLM_OK;
-    }
     if ((rc = stage_upload(p, bytes, wsb + L.plan_off, st))) return rc;
     if (!plan.blocks.empty()) {
         ProfScope ps(2, st);
@@ -900,6 +914,67 @@ int smlm_forward(smlm_pool p, const smlm_batch *b, const void *X, const void *W,
         ProfScope ps(0, st);
         CKL(launch_gemm(a, false, p->num_sms, st), 1);
     }
+    return SMLM_OK;
+}
+
+// validate a multi-projection call; returns SMLM_OK and the plan of pools[0]
+static int multi_check(int n_proj, const smlm_pool *pools, const smlm_batch *b, Plan &plan, bool &same_scales) {
+    if (n_proj < 1 || n_proj > kDec3MaxProj) return set_err(SMLM_E_INVALID, "n_proj must be in [1, 4]");
+    if (!pools || !b) return set_err(SMLM_E_INVALID, "NULL pools/batch");
+    for (int i = 0; i < n_proj; ++i) {
+        if (!pools[i]) return set_err(SMLM_E_INVALID, "NULL pool");
+        if (pools[i]->device != pools[0]->device || pools[i]->in != pools[0]->in || pools[i]->r != pools[0]->r ||
+            pools[i]->dtype != pools[0]->dtype)
+            return set_err(SMLM_E_SHAPE, "pools must share device, in_features, rank and dtype");
+    }
+    int rc = plan_for(pools[0], b, false, plan);
+    if (rc) return rc;
+    same_scales = true;
+    for (int g = 0; g < b->G; ++g) {
+        const int sl = b->seg_slot[g];
+        if (sl < 0) continue;
+        for (int i = 1; i < n_proj; ++i) {
+            if (sl >= pools[i]->cap || !pools[i]->ok[sl])
+                return set_err(SMLM_E_SLOT, "slot " + std::to_string(sl) + " not registered in pool " + std::to_string(i));
+            if (pools[i]->scales[sl] != pools[0]->scales[sl]) same_scales = false;
+        }
+    }
+    return SMLM_OK;
+}
+
+size_t smlm_workspace_size_multi(int n_proj, const smlm_pool *pools, const smlm_batch *b) {
+    Plan plan;
+    bool same = true;
+    if (multi_check(n_proj, pools, b, plan, same) != SMLM_OK) return 0;
+    size_t ws = 0;
+    for (int i = 0; i < n_proj; ++i) ws = std::max(ws, smlm_workspace_size(pools[i], b, 0));
+    if (same) {
+        const Dec3Plan D = dec3_plan(n_proj, pools, b, plan);
+        if (D.ok) ws = std::max(ws, D.total);
+    }
+    return ws;
+}
+
+int smlm_forward_multi(int n_proj, const smlm_pool *pools, const smlm_batch *b, const void *X, const void *const *W,
+                       void *const *Y, void *const *V_save, void *ws, size_t ws_bytes, void *stream) {
+    Plan plan;
+    bool same = true;
+    int rc = multi_check(n_proj, pools, b, plan, same);
+    if (rc) return rc;
+    if (b->S == 0 || b->G == 0) return SMLM_OK;
+    if (!X || !W || !Y) return set_err(SMLM_E_INVALID, "X, W and Y must be non-NULL");
+    for (int i = 0; i < n_proj; ++i)
+        if (!W[i] || !Y[i]) return set_err(SMLM_E_INVALID, "W[i] and Y[i] must be non-NULL");
+    const Dec3Plan D = same ? dec3_plan(n_proj, pools, b, plan) : Dec3Plan();
+    if (D.ok) {
+        if (!ws || ws_bytes < D.total) return set_err(SMLM_E_WORKSPACE, "workspace too small");
+        DeviceGuard dg(pools[0]->device);
+        if ((rc = check_sticky())) return rc;
+        return run_dec3(n_proj, pools, b, D, X, W, Y, V_save, reinterpret_cast<uint8_t *>(ws), (cudaStream_t)stream);
+    }
+    for (int i = 0; i < n_proj; ++i)
+        if ((rc = smlm_forward(pools[i], b, X, W[i], Y[i], V_save ? V_save[i] : nullptr, ws, ws_bytes, stream)))
+            return rc;
     return SMLM_OK;
 }
 

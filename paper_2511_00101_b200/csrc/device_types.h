@@ -127,61 +127,74 @@ struct TokArgs {
     int stages;
 };
 
-// decode / short-row GEMM (transposed, split K over the stacked rows [W ; A_u of the batch])
-struct DecRow {        // one decode row, indexed by group*256 + m (m = position in the group)
-    int row;           // batch row, -1 for padding
-    int uidx;          // index of its adapter in vt_slots, -1 = base only
-    float scale;       // effective s
-    int ft;            // FINETUNE row (V_save)
-};
-struct DecArgs {
-    CUtensorMap tmW;    // W [out,in] box {64,128} SW128 (A operand: 128 W rows)
-    CUtensorMap tmX;    // X [S,in]   box {64,128} SW128 (B operand: decode rows)
-    CUtensorMap tmX64;  // X [S,in]   box {64,64}  SW128 (multicast quarters of the decode rows)
-    const SlotDev *slots;
-    const DevTile *tiles;    // the short tiles (<= 4)
-    const int *vt_slots;     // distinct adapter slots of the batch, ascending
-    const DecRow *rows;      // [n_groups*256]
-    int n_tiles;
-    int n_groups;       // ceil(n_tiles / 2): <= 256 decode rows per MMA
-    int n_nt;           // ceil(out / 128) W row tiles
-    int n_vt;           // ceil(n_uniq * r_pad / 128) stacked-adapter row tiles
-    int n_uniq;
-    int ksplit;
-    int cmc;            // cluster size sharing the X tile by TMA multicast (1 or 4)
-    int K;
-    int N;
-    int r;
-    int r_pad;
-    int stages;
-    void *Y;
-    void *Vsave;
-    float *part;        // [(n_nt+n_vt)*n_groups][ksplit][256][128] fp32 partials
+// ------------------------------------------------------------------------------------------
+// decode path v3 (kernels_dec3.cu): pure short/decode batches (<= 512 rows), one or several
+// projections sharing X (q/k/v, gate/up) in ONE launch.  CTA pairs: M = 256 decode rows (128 per
+// CTA), N = 256 W rows, split K with an in-kernel reduce-scatter of the fp32 partials; the shrink
+// runs on the otherwise idle epilogue warps during the main loop; the expand is one extra
+// K = r_pad block per adapter (block-diagonal s*V slab x B_u rows).
+// ------------------------------------------------------------------------------------------
+constexpr int kDec3MaxProj = 4;
+constexpr int kDec3MaxPairs = 74;
+constexpr int kDec3MaxShrinkItems = 64;   // per shrink pair (staged in shared memory)    // one wave of CTA pairs (148 SMs); spin-waits need co-residency
+
+struct alignas(64) Dec3Proj {
+    CUtensorMap tmW;        // W_p [out_p, in] box {64,128} SW128 (B operand: 128 W rows per CTA)
+    CUtensorMap tmY;        // Y_p [S, out_p] box {32,128} (TMA store of a 32-column chunk)
+    CUtensorMap tmSV;       // s*V slabs [n_groups*n_uniq*256, r_pad] bf16 box {r_pad,128} (expand A operand)
+    const SlotDev *slots;   // pool p's slot table (A_u for the shrink, tmBk for the expand)
+    void *sv;               // slab base (generic pointer; written by the shrink CTAs)
+    void *Vsave;            // [S, r] bf16 or NULL (FINETUNE rows)
+    int out;
+    int nt0;                // first W tile of this projection (within a row group)
+    int n_wt;               // ceil(out_p / 256)
+    int pad[7];
 };
 
-// fused decode kernel (<= 256 decode rows): DSMEM split-K reduction + in-kernel expand
-struct DecFArgs {
-    CUtensorMap tmW;    // W [out,in] box {64,128} SW128
-    CUtensorMap tmX;    // X [S,in]   box {64,128} SW128
-    const SlotDev *slots;
-    const int *vt_slots;     // distinct adapter slots of the batch, ascending
-    const DecRow *rows;      // [256] per decode row (m = tile*128 + pos)
-    int tile_row0[2];        // first batch row of the (<= 2) short tiles
-    int n_vt;                // stacked-adapter row tiles
-    int n_nt;                // W row tiles (ceil(out/128))
+struct alignas(16) Dec3Row {   // a row with an adapter (grouped by adapter, ascending row)
+    int row;
+    float scale;            // effective s = slot_scale * seg_scale
+    int ft;                 // FINETUNE row (V_save)
+    int pad;
+};
+struct alignas(16) Dec3SItem {  // shrink work item: <= 8 rows of one adapter of one projection (self-contained)
+    const void *A;          // A_u [r, in] of projection p
+    int p;
+    int uidx;
+    int n;                  // rows (1..8)
+    int zero_fill;          // 1: also zero the slab rows of every other row (first item of the adapter)
+    int rows[8];
+    float scale[8];         // effective s of each row
+    int ft_mask;            // bit i: row i is a FINETUNE row (V_save)
+    int pad;
+    uint32_t mask[16];      // rows of this adapter (bit e of word e/32 = batch row e), for the zero fill
+};
+static_assert(sizeof(Dec3SItem) % 16 == 0, "Dec3SItem must be a multiple of 16 bytes");
+
+struct Dec3Args {
+    CUtensorMap tmX;        // X [S, in] box {64,128} SW128 (A operand: 128 decode rows per CTA)
+    Dec3Proj proj[kDec3MaxProj];
+    const void *X;          // X [S, in] bf16 (generic pointer for the SIMT shrink)
+    const int *uslot;       // [n_uniq] distinct adapter slots of the batch, ascending
+    const Dec3SItem *sitems;
+    float *kpart;           // split-K partials [W items][2 ranks][8 chunks][8 q][128 m] float4
+    int *ctr;               // pool-owned self-resetting counters (kernels_dec3.cu)
+    unsigned long long *dbg;  // optional per-CTA phase timestamps [grid][16] (SMLM_DEC3_DEBUG)
+    int n_proj;
     int n_uniq;
-    int ksplit;              // cluster size along K
-    int m_rows;              // 128 * number of short tiles
-    int K;
-    int N;
+    int n_sitems;
+    int n_groups;           // ceil(S / 256)
+    int n_wt;               // W tiles per row group (all projections)
+    int ks;                 // split-K factor of the W tiles
+    int n_wpairs;           // CTA pairs on W items (= n_groups * n_wt * ks); the rest run the shrink
+    int S;
+    int K;                  // in
     int r;
     int r_pad;
     int stages;
-    void *Y;
-    void *Vsave;
-    float *Vg;               // [256][r_pad] fp32 V of every decode row (workspace)
-    unsigned long long *v_done;     // pool-owned release counter
-    unsigned long long v_target;    // value of *v_done once this call's adapter tiles are published
+    int flags;
 };
+constexpr int kDec3ChunkBytes = 128 * 32 * 4;   // one 32-column fp32 chunk of a CTA accumulator
+constexpr int dec3_counter_ints() { return 2 + 2 * 128 + 62; }
 
 }  // namespace smlm

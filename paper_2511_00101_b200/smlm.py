@@ -26,7 +26,8 @@ EXPORTED = [
     "smlm_pool_create", "smlm_pool_destroy", "smlm_pool_set_option", "smlm_adapter_register",
     "smlm_adapter_set_grad", "smlm_adapter_unregister", "smlm_workspace_size", "smlm_forward",
     "smlm_backward", "smlm_plan", "smlm_plan_export", "smlm_status_string", "smlm_last_error",
-    "smlm_launch_count", "smlm_profile_enable", "smlm_profile_read",
+    "smlm_launch_count", "smlm_profile_enable", "smlm_profile_read", "smlm_workspace_size_multi",
+    "smlm_forward_multi",
 ]
 
 
@@ -57,6 +58,8 @@ def _load():
         "smlm_adapter_unregister": ([P, I, P], I),
         "smlm_workspace_size": ([P, BP, I], Z),
         "smlm_forward": ([P, BP, P, P, P, P, P, Z, P], I),
+        "smlm_workspace_size_multi": ([I, P, BP], Z),
+        "smlm_forward_multi": ([I, P, BP, P, P, P, P, P, Z, P], I),
         "smlm_backward": ([P, BP, P, P, P, P, P, I, P, Z, P], I),
         "smlm_plan": ([BP, I, P, I, I, P, I, ctypes.POINTER(I)], I),
         "smlm_plan_export": ([P, BP, I, P, I, ctypes.POINTER(I)], I),
@@ -159,6 +162,29 @@ def smlm_forward(pool: int, batch: Batch, X, W, Y, V_save=None, ws=None, stream=
     _check(_lib.smlm_forward(pool, ctypes.byref(batch.c), _ptr(X), _ptr(W), _ptr(Y), _ptr(V_save), _ptr(ws),
                              0 if ws is None else ws.numel() * ws.element_size(), _stream(stream, X.device)),
            "smlm_forward")
+
+
+def _ptr_array(xs):
+    arr = (ctypes.c_void_p * len(xs))(*[None if x is None else (x if isinstance(x, int) else x.data_ptr())
+                                        for x in xs])
+    return arr
+
+
+def smlm_workspace_size_multi(pools, batch: Batch) -> int:
+    hs = _ptr_array(list(pools))
+    return int(_lib.smlm_workspace_size_multi(len(pools), ctypes.cast(hs, ctypes.c_void_p), ctypes.byref(batch.c)))
+
+
+def smlm_forward_multi(pools, batch: Batch, X, Ws, Ys, V_saves=None, ws=None, stream=None):
+    """One call for several projections sharing X (q/k/v, gate/up): include/smlm.h smlm_forward_multi."""
+    n = len(pools)
+    hs, wp, yp = _ptr_array(list(pools)), _ptr_array(Ws), _ptr_array(Ys)
+    vp = None if V_saves is None else _ptr_array(V_saves)
+    _check(_lib.smlm_forward_multi(n, ctypes.cast(hs, ctypes.c_void_p), ctypes.byref(batch.c), _ptr(X),
+                                   ctypes.cast(wp, ctypes.c_void_p), ctypes.cast(yp, ctypes.c_void_p),
+                                   None if vp is None else ctypes.cast(vp, ctypes.c_void_p), _ptr(ws),
+                                   0 if ws is None else ws.numel() * ws.element_size(), _stream(stream, X.device)),
+           "smlm_forward_multi")
 
 
 def smlm_backward(pool: int, batch: Batch, X, W, dY, V_save=None, dX=None, accumulate=False, ws=None,

@@ -1,0 +1,104 @@
+// Microbenchmark: HBM read bandwidth of W-streaming patterns used by the decode kernel.
+//   mode 0: TMA 2D boxes {64 k, 128 rows} (SW128), CTA = (128-row block, K split), 6-stage ring
+//   mode 1: 1D bulk copies of 16 KB contiguous chunks (pre-packed layout), same bytes per CTA
+//   mode 2: TMA 2D boxes {64, 128}, CTA = (32-row block... ) full K (rows split instead of K)
+// nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tma_bw tma_bw.cu -lcuda
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+#include <stdio.h>
+#include <stdint.h>
+#include <vector>
+#include <stdlib.h>
+
+__device__ __forceinline__ uint32_t su32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint32_t b, uint32_t c) { asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(b), "r"(c)); }
+__device__ __forceinline__ void expect_tx(uint32_t b, uint32_t n) { asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(n) : "memory"); }
+__device__ __forceinline__ void mwait(uint32_t b, uint32_t ph) {
+    uint32_t d;
+    do { asm volatile("{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0,1,0,p;\n}" : "=r"(d) : "r"(b), "r"(ph) : "memory"); } while (!d);
+}
+__device__ __forceinline__ void tma2d(uint32_t dst, const void *map, uint32_t bar, int c0, int c1) {
+    asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(dst), "l"(map), "r"(c0), "r"(c1), "r"(bar) : "memory");
+}
+__device__ __forceinline__ void bulk1d(uint32_t dst, const void *src, uint32_t n, uint32_t bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst), "l"(src), "r"(n), "r"(bar) : "memory");
+}
+
+constexpr int STMAX = 13;
+__global__ void __launch_bounds__(32) kstream(const __grid_constant__ CUtensorMap map, const char *W, int mode, int rows, int K, int ks, int ST) {
+    extern __shared__ __align__(1024) uint8_t sm[];
+    __shared__ uint64_t bars[STMAX];
+    uint32_t base = (su32(sm) + 1023) & ~1023u;
+    if (threadIdx.x == 0) { for (int s = 0; s < ST; ++s) mbar_init(su32(&bars[s]), 1); asm volatile("fence.mbarrier_init.release.cluster;"); }
+    __syncthreads();
+    if (threadIdx.x != 0) return;
+    int nkb = K / 64;
+    int rb, kb0, kb1;
+    if (mode == 2) { rb = blockIdx.x; kb0 = 0; kb1 = nkb; }
+    else { rb = blockIdx.x / ks; int s = blockIdx.x % ks; int q = nkb / ks, rm = nkb % ks; kb0 = s * q + min(s, rm); kb1 = kb0 + q + (s < rm); }
+    int boxr = mode == 2 ? 128 : 128;
+    uint32_t bytes = 64 * 2 * boxr;
+    for (int i = kb0, n = 0; i < kb1; ++i, ++n) {
+        int s = n % ST;
+        uint32_t ph = (n / ST) & 1;
+        uint32_t bar = su32(&bars[s]);
+        if (n >= ST) mwait(bar, ph ^ 1);
+        expect_tx(bar, bytes);
+        if (mode == 1) bulk1d(base + s * 16384, W + ((size_t)rb * nkb + i) * 16384, 16384, bar);
+        else tma2d(base + s * 16384, &map, bar, i * 64, rb * boxr);
+    }
+    for (int n = max(0, (kb1 - kb0) - ST); n < kb1 - kb0; ++n) mwait(su32(&bars[n % ST]), (n / ST) & 1);
+}
+
+int main() {
+    int rows = 4096, K = 4096;
+    if (getenv("BIG")) rows = 32768;
+    size_t bytes = (size_t)rows * K * 2;
+    int nset = 8;
+    std::vector<char *> W(nset);
+    for (auto &w : W) { cudaMalloc(&w, bytes); cudaMemset(w, 1, bytes); }
+    void *fn; cudaDriverEntryPointQueryResult q;
+    cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
+    auto enc = (PFN_cuTensorMapEncodeTiled_v12000)fn;
+    std::vector<CUtensorMap> maps(nset);
+    for (int i = 0; i < nset; ++i) {
+        cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)rows}, str[1] = {(cuuint64_t)K * 2};
+        cuuint32_t box[2] = {64, 128}, es[2] = {1, 1};
+        enc(&maps[i], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, W[i], dims, str, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    }
+    cudaFuncSetAttribute(kstream, cudaFuncAttributeMaxDynamicSharedMemorySize, 13 * 16384 + 1024);
+    cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
+    struct Cfg { int mode, ks, st; const char *name; };
+    Cfg cfgs[] = {{0, 4, 6, "tma2d ks=4 st=6"}, {0, 4, 12, "tma2d ks=4 st=12"}, {1, 4, 12, "bulk1d ks=4 st=12"},
+                  {0, 2, 12, "tma2d ks=2 st=12"}, {0, 8, 12, "tma2d ks=8 st=12"}, {1, 8, 6, "bulk1d ks=8 st=6"}};
+    for (auto &c : cfgs) {
+        int grid = rows / 128 * c.ks;
+        size_t smem = c.st * 16384 + 1024;
+        for (int it = 0; it < 3; ++it) kstream<<<grid, 32, smem>>>(maps[it % nset], W[it % nset], c.mode, rows, K, c.ks, c.st);
+        cudaDeviceSynchronize();
+        float best = 1e9, tot = 0;
+        for (int it = 0; it < 16; ++it) {
+            cudaEventRecord(a);
+            kstream<<<grid, 32, smem>>>(maps[it % nset], W[it % nset], c.mode, rows, K, c.ks, c.st);
+            cudaEventRecord(b);
+            cudaEventSynchronize(b);
+            float ms; cudaEventElapsedTime(&ms, a, b);
+            best = ms < best ? ms : best; tot += ms;
+        }
+        printf("{\"rows\": %d, \"pattern\": \"%s\", \"grid\": %d, \"best_us\": %.2f, \"avg_us\": %.2f, \"GBs_best\": %.0f}\n", rows, c.name, grid, best * 1e3, tot / 16 * 1e3, bytes / (best * 1e-3) / 1e9);
+    }
+    // empty-ish kernel launch cost
+    {
+        for (int it = 0; it < 3; ++it) kstream<<<148, 32, 1024>>>(maps[0], W[0], 0, rows, 0, 1, 1);
+        cudaDeviceSynchronize();
+        cudaEventRecord(a);
+        for (int it = 0; it < 20; ++it) kstream<<<148, 32, 1024>>>(maps[0], W[0], 0, rows, 0, 1, 1);
+        cudaEventRecord(b);
+        cudaEventSynchronize(b);
+        float ms; cudaEventElapsedTime(&ms, a, b);
+        printf("{\"empty_kernel_us\": %.2f}\n", ms / 20 * 1e3);
+    }
+    printf("err=%s\n", cudaGetErrorString(cudaGetLastError()));
+    return 0;
+}

@@ -246,10 +246,11 @@ def test_bf16_decode_grouped_with_finetune_short_rows():
     _check(res, batch, w, X, dY, BF16_TOL)
 
 
-def test_bf16_decode_fused_variant(monkeypatch):
-    """The experimental fused decode kernel (SMLM_DECF=1: DSMEM split-K reduction + in-kernel
-    expand) matches the oracle as well."""
-    monkeypatch.setenv("SMLM_DECF", "1")
+@pytest.mark.parametrize("ks", ["1", "2", "3", "8"])
+def test_bf16_decode_ksplit_variants(monkeypatch, ks):
+    """The single-launch decode kernel (kernels_dec3.cu) at forced split-K factors: every split
+    count matches the oracle (in-kernel reduce-scatter of the fp32 partials)."""
+    monkeypatch.setenv("SMLM_DEC_KSPLIT", ks)
     g = torch.Generator().manual_seed(5)
     rows = 200
     slots = torch.randint(-1, 6, (rows,), generator=g).tolist()
@@ -258,3 +259,113 @@ def test_bf16_decode_fused_variant(monkeypatch):
     res = run_smlm(batch, w, X, dY, backward=False)
     Y, V = oracle.forward(batch, w.W, w.A, w.B, w.slot_scale, X)
     assert parity_err(res.Y, Y) <= BF16_TOL
+    ft = batch.ft_rows()
+    ft = ft[batch.row_slot()[ft] >= 0]
+    assert parity_err(res.V.double().numpy()[ft], V[ft]) <= BF16_TOL
+
+
+def test_bf16_decode_b_zero_and_permutation():
+    """Pure decode batch: B = 0 is value-identical to all slots -1 (the split-K ranges do not
+    depend on the adapters; the expand adds exact zeros), and permuting the one-row segments
+    permutes Y bit-exactly (per-row arithmetic is position independent)."""
+    rows = 240
+    g = torch.Generator().manual_seed(11)
+    slots = torch.randint(-1, 7, (rows,), generator=g).tolist()
+    batch, w, X, dY = synth.random_case(12, 1024, 768, 16, 7, [1] * rows, [DECODE] * rows, slots)
+    wz = synth.Weights(w.W, w.A, [torch.zeros_like(b) for b in w.B], w.slot_scale)
+    r1 = run_smlm(batch, wz, X, dY, backward=False)
+    nb = synth.Batch(batch.offsets, np.full_like(batch.slots, -1), batch.modes, None)
+    r2 = run_smlm(nb, wz, X, dY, backward=False)
+    assert torch.equal(r1.Y.float(), r2.Y.float())
+    r3 = run_smlm(batch, w, X, dY, backward=False)
+    perm = torch.randperm(rows, generator=g).numpy()
+    pb = synth.batch_from_lengths([1] * rows, [slots[i] for i in perm], [DECODE] * rows)
+    r4 = run_smlm(pb, w, X[perm], dY[perm], backward=False)
+    assert torch.equal(r4.Y.float(), r3.Y[perm].float())
+
+
+def _multi_case(seed, in_f, outs, r, U, rows, ft_rows=3):
+    g = torch.Generator().manual_seed(seed)
+    slots = torch.randint(-1, U, (rows,), generator=g).tolist()
+    modes = [DECODE] * (rows - ft_rows) + [FINETUNE] * ft_rows
+    cases = [synth.random_case(seed * 10 + i, in_f, o, r, U, [1] * rows, modes, slots) for i, o in enumerate(outs)]
+    return cases[0][0], [c[1] for c in cases], cases[0][2]
+
+
+def _run_multi(batch, ws_, X, slot_scales=None):
+    from paper_2511_00101_b200 import smlm as S
+    dev = torch.device("cuda", 0)
+    in_f, r, U = X.shape[1], ws_[0].A[0].shape[0], len(ws_[0].A)
+    pools, keep = [], []
+    for i, w in enumerate(ws_):
+        pool = S.Pool(in_f, w.W.shape[0], r, U)
+        for a in range(U):
+            A, B = w.A[a].to(dev).contiguous(), w.B[a].to(dev).contiguous()
+            sc = w.slot_scale[a] if slot_scales is None else slot_scales[i][a]
+            assert pool.register(A, B, sc) == a
+        pools.append(pool)
+    b = S.Batch.from_synth(batch)
+    Xd = X.to(dev).contiguous()
+    Ws = [w.W.to(dev).contiguous() for w in ws_]
+    Ys = [torch.full((batch.S, w.W.shape[0]), float("nan"), dtype=torch.bfloat16, device=dev) for w in ws_]
+    Vs = [torch.zeros(batch.S, r, dtype=torch.bfloat16, device=dev) for _ in ws_]
+    n = S.smlm_workspace_size_multi([p.h for p in pools], b)
+    wsb = torch.empty(max(n, 256), dtype=torch.uint8, device=dev)
+    n0 = S.smlm_launch_count()
+    S.smlm_forward_multi([p.h for p in pools], b, Xd, Ws, Ys, Vs, wsb)
+    torch.cuda.synchronize()
+    launches = S.smlm_launch_count() - n0
+    for p in pools:
+        p.close()
+    return [y.cpu() for y in Ys], [v.cpu() for v in Vs], launches
+
+
+@pytest.mark.parametrize("rows,in_f,outs,r", [(256, 1024, (1024, 256, 256), 16), (200, 512, (320, 192), 8),
+                                              (450, 512, (256, 128, 384, 64), 32), (64, 192, (128,), 64)])
+def test_bf16_decode_multi_projection(rows, in_f, outs, r):
+    """smlm_forward_multi: several projections sharing X in ONE launch, each Y and V_save against
+    the oracle of its own projection."""
+    batch, ws_, X = _multi_case(rows + in_f, in_f, outs, r, 5, rows)
+    Ys, Vs, launches = _run_multi(batch, ws_, X)
+    assert launches == 1
+    ft = batch.ft_rows()
+    ft = ft[batch.row_slot()[ft] >= 0]
+    for i, w in enumerate(ws_):
+        Yr, Vr = oracle.forward(batch, w.W, w.A, w.B, w.slot_scale, X)
+        assert parity_err(Ys[i], Yr) <= BF16_TOL, i
+        if len(ft):
+            assert parity_err(Vs[i].double().numpy()[ft], Vr[ft]) <= BF16_TOL, i
+
+
+def test_bf16_multi_fallbacks_and_errors():
+    """Different slot scales across pools -> per-pool calls (still correct); a mixed batch with
+    long segments -> per-pool calls; a slot missing from one pool -> SMLM_E_SLOT."""
+    from paper_2511_00101_b200 import smlm as S
+    batch, ws_, X = _multi_case(3, 512, (256, 192), 16, 4, 100)
+    scales = [[2.0] * 4, [1.0, 2.0, 3.0, 0.5]]
+    Ys, _, launches = _run_multi(batch, ws_, X, slot_scales=scales)
+    assert launches >= 2
+    for i, w in enumerate(ws_):
+        Yr, _ = oracle.forward(batch, w.W, w.A, w.B, scales[i], X)
+        assert parity_err(Ys[i], Yr) <= BF16_TOL
+    lengths = [130, 1, 1, 70, 2]
+    modes = [PREFILL, DECODE, DECODE, EVAL, DECODE]
+    cases = [synth.random_case(40 + i, 256, o, 16, 3, lengths, modes, [0, 1, 2, -1, 1]) for i, o in enumerate((256, 128))]
+    Ys, _, _ = _run_multi(cases[0][0], [c[1] for c in cases], cases[0][2])
+    for i, c in enumerate(cases):
+        Yr, _ = oracle.forward(c[0], c[1].W, c[1].A, c[1].B, c[1].slot_scale, cases[0][2])
+        assert parity_err(Ys[i], Yr) <= BF16_TOL
+    p0, p1 = S.Pool(256, 256, 16, 4), S.Pool(256, 128, 16, 4)
+    A, B0, B1 = (torch.zeros(16, 256, dtype=torch.bfloat16, device="cuda"),
+                 torch.zeros(256, 16, dtype=torch.bfloat16, device="cuda"),
+                 torch.zeros(128, 16, dtype=torch.bfloat16, device="cuda"))
+    p0.register(A, B0, 2.0)
+    p0.register(A, B0, 2.0)
+    p1.register(A, B1, 2.0)
+    b = S.Batch([0, 1, 2], [0, 1], [DECODE, DECODE])
+    with pytest.raises(S.SmlmError) as ei:
+        S.smlm_workspace_size_multi([p0.h, p1.h], b) or S.smlm_forward_multi(
+            [p0.h, p1.h], b, torch.zeros(2, 256, dtype=torch.bfloat16, device="cuda"), [None, None], [None, None])
+    assert ei.value.code in (S.SMLM_E_SLOT, S.SMLM_E_INVALID)
+    p0.close()
+    p1.close()
