@@ -13,6 +13,8 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <stdio.h>
+
 #include <algorithm>
 #include <atomic>
 #include <mutex>
@@ -44,7 +46,7 @@ int launch_prep_sv(const DevTile *tiles, int n_tiles, const TV *V, int r, int r_
 int launch_tok(const TokArgs &a, int num_sms, cudaStream_t st);
 int dec_chunks(int in_f);
 int dec3_stages();
-int launch_dec3(const Dec3Args &a, int clusters, cudaStream_t st);
+int launch_dec3(const Dec3Args &a, const Dec3Inline &in, int clusters, cudaStream_t st);
 int launch_shrink_split(const __nv_bfloat16 *X, const SlotDev *slots, const DevBlock *blocks,
                         const DevShortRow *srows, int n_blocks, int in_f, int r, int r_pad, float *part,
                         __nv_bfloat16 *Vbd, __nv_bfloat16 *Vsave, cudaStream_t st);
@@ -66,6 +68,22 @@ using namespace smlm;
 // ------------------------------------------------------------------------------------------
 static thread_local std::string g_last_error;
 static std::atomic<uint64_t> g_launches{0};
+
+// optional host-side phase timing (SMLM_HOST_PROF=1): microseconds per phase, printed at exit
+#include <chrono>
+struct HostProf {
+    bool on = getenv("SMLM_HOST_PROF") != nullptr;
+    double t[8] = {0};
+    long n = 0;
+    ~HostProf() {
+        if (on && n)
+            fprintf(stderr, "[smlm host] calls=%ld plan=%.2f dec3plan=%.2f upload=%.2f maps=%.2f launch=%.2f us/call\n", n,
+                    t[0] / n, t[1] / n, t[2] / n, t[3] / n, t[4] / n);
+    }
+} g_hprof;
+static inline double now_us() {
+    return std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
 
 static int set_err(int code, const std::string &msg) {
     g_last_error = msg;
@@ -237,6 +255,16 @@ struct smlm_pool_s {
     std::vector<float> scales;
     SlotDev *d_slots = nullptr;
     int *d_ctr = nullptr;   // decode kernel: self-resetting cross-CTA counters (dec3_counter_ints())
+    // encoded TMA descriptors of recently used (pointer, shape, box) keys: steady-state calls reuse them
+    struct MapEnt {
+        const void *ptr;
+        uint64_t inner, outer;
+        uint32_t b0, b1;
+        int swz;
+        CUtensorMap map;
+    };
+    std::vector<MapEnt> map_cache;
+    size_t map_next = 0;
     Ring ring;
 };
 
@@ -280,6 +308,26 @@ int plan_for(smlm_pool p, const smlm_batch *b, bool bwd, Plan &plan) {
     int l_long = p->dtype == SMLM_FP32 ? 1 : p->l_long;
     int rc = build_plan(b, p->cap, p->ok.data(), p->scales.data(), l_long, bwd, plan, msg);
     if (rc != SMLM_OK) return set_err(rc, msg);
+    return SMLM_OK;
+}
+
+// make_map through the pool's small descriptor cache (round-robin replacement, 64 entries)
+int make_map_cached(smlm_pool p, CUtensorMap *m, const void *ptr, uint64_t inner, uint64_t outer, uint32_t b0,
+                    uint32_t b1, CUtensorMapSwizzle swz) {
+    for (auto &e : p->map_cache)
+        if (e.ptr == ptr && e.inner == inner && e.outer == outer && e.b0 == b0 && e.b1 == b1 && e.swz == (int)swz) {
+            *m = e.map;
+            return SMLM_OK;
+        }
+    int rc = make_map(m, ptr, inner, outer, b0, b1, swz);
+    if (rc) return rc;
+    smlm_pool_s::MapEnt e{ptr, inner, outer, b0, b1, (int)swz, *m};
+    if (p->map_cache.size() < 64) {
+        p->map_cache.push_back(e);
+    } else {
+        p->map_cache[p->map_next] = e;
+        p->map_next = (p->map_next + 1) % 64;
+    }
     return SMLM_OK;
 }
 
@@ -467,18 +515,30 @@ int run_dec3(int n_proj, const smlm_pool *pools, const smlm_batch *b, const Dec3
     const size_t si_off = bytes.size();
     append(bytes, D.sitems);
     int rc;
-    if ((rc = stage_upload(p0, bytes, wsb + D.plan_off, st))) return rc;
+    double t0 = g_hprof.on ? now_us() : 0;
+    static thread_local Dec3Inline inl;   // kernel parameter block (copied at launch)
+    const bool inline_plan = n_uniq <= kDec3InlineSlots && (int)D.sitems.size() <= kDec3InlineItems;
+    if (inline_plan) {
+        if (n_uniq) memcpy(inl.uslot, D.uslot.data(), n_uniq * sizeof(int));
+        if (!D.sitems.empty()) memcpy(inl.items, D.sitems.data(), D.sitems.size() * sizeof(Dec3SItem));
+    } else if ((rc = stage_upload(p0, bytes, wsb + D.plan_off, st))) {
+        return rc;
+    }
+    double t1 = g_hprof.on ? now_us() : 0;
     Dec3Args a;
     memset(&a, 0, sizeof(a));
-    if ((rc = make_map(&a.tmX, X, p0->in, b->S, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B))) return rc;
+    a.inl = inline_plan ? 1 : 0;
+    if ((rc = make_map_cached(p0, &a.tmX, X, p0->in, b->S, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B))) return rc;
     int nt0 = 0;
     for (int i = 0; i < n_proj; ++i) {
         Dec3Proj &P = a.proj[i];
-        if ((rc = make_map(&P.tmW, W[i], p0->in, pools[i]->out, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B))) return rc;
-        if ((rc = make_map(&P.tmY, Y[i], pools[i]->out, b->S, 32, 128, CU_TENSOR_MAP_SWIZZLE_NONE))) return rc;
+        if ((rc = make_map_cached(p0, &P.tmW, W[i], p0->in, pools[i]->out, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B)))
+            return rc;
+        if ((rc = make_map_cached(p0, &P.tmY, Y[i], pools[i]->out, b->S, 32, 128, CU_TENSOR_MAP_SWIZZLE_NONE)))
+            return rc;
         P.sv = wsb + D.sv_off[i];
-        if (n_uniq > 0 && (rc = make_map(&P.tmSV, P.sv, p0->r_pad, (uint64_t)D.n_groups * n_uniq * 256, p0->r_pad,
-                                         128, swizzle_for(p0->r_pad * 2))))
+        if (n_uniq > 0 && (rc = make_map_cached(p0, &P.tmSV, P.sv, p0->r_pad, (uint64_t)D.n_groups * n_uniq * 256,
+                                                p0->r_pad, 128, swizzle_for(p0->r_pad * 2))))
             return rc;
         P.slots = pools[i]->d_slots;
         P.Vsave = Vsave ? Vsave[i] : nullptr;
@@ -507,8 +567,16 @@ int run_dec3(int n_proj, const smlm_pool *pools, const smlm_batch *b, const Dec3
     if (const char *e = getenv("SMLM_DEC3_EXPT")) a.flags = atoi(e);
     if (getenv("SMLM_DEC3_DEBUG"))
         a.dbg = reinterpret_cast<unsigned long long *>(wsb + D.total - 2 * kDec3MaxPairs * 16 * 8);
-    ProfScope ps(0, st);
-    CKL(launch_dec3(a, D.clusters, st), 1);
+    double t2 = g_hprof.on ? now_us() : 0;
+    {
+        ProfScope ps(0, st);
+        CKL(launch_dec3(a, inl, D.clusters, st), 1);
+    }
+    if (g_hprof.on) {
+        g_hprof.t[2] += t1 - t0;
+        g_hprof.t[3] += t2 - t1;
+        g_hprof.t[4] += now_us() - t2;
+    }
     return SMLM_OK;
 }
 
@@ -750,10 +818,27 @@ int smlm_forward(smlm_pool p, const smlm_batch *b, const void *X, const void *W,
                  size_t ws_bytes, void *stream) {
     if (!p || !b) return set_err(SMLM_E_INVALID, "NULL pool/batch");
     Plan plan;
+    const double h0 = g_hprof.on ? now_us() : 0;
     int rc = plan_for(p, b, false, plan);
     if (rc) return rc;
     if (b->S == 0 || b->G == 0) return SMLM_OK;
     if (!X || !Y) return set_err(SMLM_E_INVALID, "X and Y must be non-NULL");
+    if (p->dtype == SMLM_BF16 && W) {
+        // pure short / decode batch: one launch (kernels_dec3.cu)
+        const double h1 = g_hprof.on ? now_us() : 0;
+        const Dec3Plan D = dec3_plan(1, &p, b, plan);
+        if (g_hprof.on) {
+            g_hprof.t[0] += h1 - h0;
+            g_hprof.t[1] += now_us() - h1;
+            g_hprof.n++;
+        }
+        if (D.ok) {
+            if (!ws || ws_bytes < D.total) return set_err(SMLM_E_WORKSPACE, "workspace too small");
+            DeviceGuard dg(p->device);
+            if ((rc = check_sticky())) return rc;
+            return run_dec3(1, &p, b, D, X, &W, &Y, &V_save, reinterpret_cast<uint8_t *>(ws), (cudaStream_t)stream);
+        }
+    }
     const bool need_vf = p->dtype == SMLM_FP32;
     WsLayout L = layout_for(p, b, plan, false, need_vf);
     if (!ws || ws_bytes < L.total) return set_err(SMLM_E_WORKSPACE, "workspace too small");
@@ -778,11 +863,6 @@ int smlm_forward(smlm_pool p, const smlm_batch *b, const void *X, const void *W,
 
     // ---------------- bf16 tensor-core path ----------------
     const bool has_w = W != nullptr;
-    if (has_w) {
-        // pure short / decode batch: one launch (kernels_dec3.cu)
-        const Dec3Plan D = dec3_plan(1, &p, b, plan);
-        if (D.ok) return run_dec3(1, &p, b, D, X, &W, &Y, &V_save, wsb, st);
-    }
     std::vector<DevTile> tiles;
     tiles.reserve(plan.long_tiles.size() + plan.short_tiles.size());
     for (auto &t : plan.long_tiles)

@@ -193,6 +193,14 @@ struct Dec3Args {
     int r_pad;
     int stages;
     int flags;
+    int inl;                // 1: uslot / sitems are passed inline (Dec3Inline kernel parameter)
+};
+// small plans ride in the kernel parameters (no H2D copy in the stream)
+constexpr int kDec3InlineItems = 96;
+constexpr int kDec3InlineSlots = 256;
+struct Dec3Inline {
+    Dec3SItem items[kDec3InlineItems];
+    int uslot[kDec3InlineSlots];
 };
 constexpr int kDec3ChunkBytes = 128 * 32 * 4;   // one 32-column fp32 chunk of a CTA accumulator
 constexpr int dec3_counter_ints() { return 2 + 2 * 128 + 62; }

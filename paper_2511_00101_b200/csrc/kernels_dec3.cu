@@ -118,8 +118,8 @@ __device__ __forceinline__ Item3 dec3_item(const Dec3Args &a, int w) {
 // of K.  The pair's items are staged in shared memory first (no dependent global loads later).
 // ------------------------------------------------------------------------------------------
 template <int RP>
-__device__ __forceinline__ void dec3_shrink_pair(const Dec3Args &a, uint8_t *smem, uint32_t smem_s, uint32_t rank,
-                                                 int sp, int n_sp) {
+__device__ __forceinline__ void dec3_shrink_pair(const Dec3Args &a, const Dec3SItem *sitems, uint8_t *smem,
+                                                 uint32_t smem_s, uint32_t rank, int sp, int n_sp) {
     constexpr int JG = RP >= 32 ? 8 : 16;   // A rows per pass
     constexpr int kMaxItems = kDec3MaxShrinkItems;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -132,10 +132,10 @@ __device__ __forceinline__ void dec3_shrink_pair(const Dec3Args &a, uint8_t *sme
     const int n_mine = sp < a.n_sitems ? (a.n_sitems - sp + n_sp - 1) / n_sp : 0;
     {
         constexpr int W4 = sizeof(Dec3SItem) / 16;
-        const uint4 *src = reinterpret_cast<const uint4 *>(a.sitems);
+        const uint4 *src = reinterpret_cast<const uint4 *>(sitems);
         uint4 *dst = reinterpret_cast<uint4 *>(its);
         for (int e = threadIdx.x; e < min(n_mine, kMaxItems) * W4; e += kT3)
-            dst[e] = __ldg(src + (size_t)(sp + (e / W4) * n_sp) * W4 + e % W4);
+            dst[e] = src[(size_t)(sp + (e / W4) * n_sp) * W4 + e % W4];
     }
     __syncthreads();
     const int ngr = a.K / 8;                                   // 128-bit granules of a row
@@ -235,7 +235,10 @@ __device__ __forceinline__ void dec3_shrink_pair(const Dec3Args &a, uint8_t *sme
 }
 
 template <int RP>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT3, 1) smlm_dec3_kernel(const __grid_constant__ Dec3Args a) {
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT3, 1) smlm_dec3_kernel(const __grid_constant__ Dec3Args a,
+                                                                                        const __grid_constant__ Dec3Inline inl) {
+    const int *uslot = a.inl ? inl.uslot : a.uslot;
+    const Dec3SItem *sitems = a.inl ? inl.items : a.sitems;
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw = smem_u32(smem_raw);
     const uint32_t base = (raw + 1023u) & ~1023u;
@@ -289,7 +292,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT3, 1) smlm_dec3_ke
 
     if (!wpair) {
         // ========================= shrink pair =========================
-        dec3_shrink_pair<RP>(a, base_ptr, base, rank, cid - a.n_wpairs, n_clusters - a.n_wpairs);
+        dec3_shrink_pair<RP>(a, sitems, base_ptr, base, rank, cid - a.n_wpairs, n_clusters - a.n_wpairs);
         if (threadIdx.x == 0) dbg_stamp(a, 1);
     } else {
         const int ks = a.ks;
@@ -340,7 +343,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT3, 1) smlm_dec3_ke
                 }
                 __syncwarp();
                 for (int u = 0; u < a.n_uniq; ++u) {
-                    const int sl = a.uslot[u];
+                    const int sl = uslot[u];
                     if (sl % ks != it.s || (a.flags & 4)) continue;
                     mbar_wait(empty_bar(stage), phase ^ 1);
                     if (lane == 0) {
@@ -381,7 +384,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT3, 1) smlm_dec3_ke
                 if (++stage == ST) { stage = 0; phase ^= 1; }
             }
             for (int u = 0; u < a.n_uniq; ++u) {
-                if (a.uslot[u] % ks != it.s || (a.flags & 4)) continue;
+                if (uslot[u] % ks != it.s || (a.flags & 4)) continue;
                 mbar_wait(full_bar(stage), phase);
                 tc_fence_after();
                 if (lane == 0) {
@@ -400,7 +403,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT3, 1) smlm_dec3_ke
         } else if (warp == 3 && a.n_uniq > 0) {
             // expand operands of this split: descriptors and B_u rows of the tile -> caches / L2
             for (int u = lane; u < a.n_uniq; u += 32) {
-                const int sl = a.uslot[u];
+                const int sl = uslot[u];
                 if (sl % ks != it.s) continue;
                 const SlotDev *sd = P.slots + sl;
                 tma_prefetch_desc(&sd->tmBk);
@@ -542,7 +545,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT3, 1) smlm_dec3_ke
 }
 
 template <int RP>
-int launch_dec3_impl(const Dec3Args &a, int clusters, cudaStream_t st) {
+int launch_dec3_impl(const Dec3Args &a, const Dec3Inline &in, int clusters, cudaStream_t st) {
     auto kern = smlm_dec3_kernel<RP>;
     const size_t smem = 1024 + (size_t)a.stages * kStage3 + 2 * kYStage + 256;
     static bool attr_done = false;
@@ -551,18 +554,18 @@ int launch_dec3_impl(const Dec3Args &a, int clusters, cudaStream_t st) {
         if (e != cudaSuccess) return (int)e;
         attr_done = true;
     }
-    return (int)launch_pdl(kern, dim3(2 * clusters), dim3(kT3), smem, st, a);
+    return (int)launch_pdl(kern, dim3(2 * clusters), dim3(kT3), smem, st, a, in);
 }
 
 }  // namespace
 
 int dec3_stages() { return 6; }
 
-int launch_dec3(const Dec3Args &a, int clusters, cudaStream_t st) {
+int launch_dec3(const Dec3Args &a, const Dec3Inline &in, int clusters, cudaStream_t st) {
     switch (a.r_pad) {
-        case 16: return launch_dec3_impl<16>(a, clusters, st);
-        case 32: return launch_dec3_impl<32>(a, clusters, st);
-        case 64: return launch_dec3_impl<64>(a, clusters, st);
+        case 16: return launch_dec3_impl<16>(a, in, clusters, st);
+        case 32: return launch_dec3_impl<32>(a, in, clusters, st);
+        case 64: return launch_dec3_impl<64>(a, in, clusters, st);
     }
     return (int)cudaErrorInvalidValue;
 }

@@ -154,7 +154,9 @@ def test_launch_count_and_no_host_sync(S):
     n0 = S.smlm_launch_count()
     side = torch.cuda.Stream()
     with torch.cuda.stream(side):
-        torch.cuda._sleep(20_000_000)                 # keep the GPU busy ~10 ms on this stream
+        big = torch.randn(8192, 8192, device="cuda", dtype=torch.bfloat16)
+        for _ in range(16):                           # keep the GPU busy ~10 ms on this stream
+            big = big @ big.T * 1e-2
         Y = pool.forward(b, X, Wd, stream=side)
         done = torch.cuda.Event()
         done.record(side)
