@@ -400,7 +400,8 @@ Dec3Plan dec3_plan(int n_proj, const smlm_pool *pools, const smlm_batch *b, cons
     const int NW = D.n_groups * D.nw;
     const int nkb = p0->in / kBK;
     // the shrink pairs take the rest of the wave: at least ~a third of the items' worth
-    const int sp_min = n_si ? std::max(1, std::min(pairs / 3, (n_si + 2) / 3)) : 0;
+    int sp_min = n_si ? std::max(1, std::min(pairs / 3, (n_si + 2) / 3)) : 0;
+    if (const char *e = getenv("SMLM_DEC_SP")) sp_min = n_si ? std::max(1, atoi(e)) : 0;   // measurement override
     if (NW > pairs - sp_min) return D;   // more W tiles than one wave: not this kernel
     int ks = (pairs - sp_min) / NW;
     if (const char *e = getenv("SMLM_DEC_KSPLIT")) ks = atoi(e);   // measurement override
@@ -410,6 +411,7 @@ Dec3Plan dec3_plan(int n_proj, const smlm_pool *pools, const smlm_batch *b, cons
     D.n_wpairs = NW * ks;
     D.clusters = n_si ? pairs : D.n_wpairs;
     if (NW > 256) return D;   // tile arrival counters
+    if (n_uniq > kDec3InlineSlots) return D;   // per-split adapter list in shared memory
     if (n_si && (n_si + (D.clusters - D.n_wpairs) - 1) / (D.clusters - D.n_wpairs) > kDec3MaxShrinkItems) return D;
     size_t off = 0;
     D.plan_off = off;

@@ -117,115 +117,183 @@ __device__ __forceinline__ Item3 dec3_item(const Dec3Args &a, int w) {
 // shrink pair: items (projection, adapter, <= 8 rows); CTA `rank` takes every other 128-bit granule
 // of K.  The pair's items are staged in shared memory first (no dependent global loads later).
 // ------------------------------------------------------------------------------------------
+// shared-memory layout of a shrink CTA (inside the pipeline ring, which shrink pairs do not use)
 template <int RP>
-__device__ __forceinline__ void dec3_shrink_pair(const Dec3Args &a, const Dec3SItem *sitems, uint8_t *smem,
+struct ShrinkSmem {
+    static constexpr uint32_t red = 0;                                  // [8 warps][8 rows][RP] fp32
+    static constexpr uint32_t own = red + 8 * 8 * RP * 4;              // [8 rows][RP] this CTA's K half
+    static constexpr uint32_t items = own + 8 * RP * 4;                // [kDec3MaxShrinkItems] Dec3SItem
+    static constexpr uint32_t rx = items + kDec3MaxShrinkItems * sizeof(Dec3SItem);   // [items][8][RP] peer halves
+    static constexpr uint32_t bars = rx + kDec3MaxShrinkItems * 8 * RP * 4;           // [items] mbarriers
+    static constexpr uint32_t end = bars + kDec3MaxShrinkItems * 8;
+};
+
+__device__ __forceinline__ void mbar_arrive_remote_release(uint32_t cluster_addr) {
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_acq_cluster(uint32_t bar, uint32_t parity) {
+    uint32_t done;
+    do {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done)
+            : "r"(bar), "r"(parity)
+            : "memory");
+    } while (!done);
+}
+
+// ------------------------------------------------------------------------------------------
+// shrink pair: items (projection, adapter, <= 8 rows); CTA `rank` takes every other 128-bit
+// granule of K.  Items are staged in shared memory first; CTA 1 pushes its K half of every item
+// into CTA 0's shared memory (one slot and one mbarrier per item, no cluster-wide barrier).
+// ------------------------------------------------------------------------------------------
+template <int RP>
+__device__ __forceinline__ void dec3_shrink_pair(const Dec3Args &a, const Dec3Inline &inl, uint8_t *smem,
                                                  uint32_t smem_s, uint32_t rank, int sp, int n_sp) {
-    constexpr int JG = RP >= 32 ? 8 : 16;   // A rows per pass
-    constexpr int kMaxItems = kDec3MaxShrinkItems;
+    using L = ShrinkSmem<RP>;
+    constexpr int JG = 8;   // A rows per pass (acc 8x8 + x 8x8 + A 8 granules in registers)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const __nv_bfloat16 *X = reinterpret_cast<const __nv_bfloat16 *>(a.X);
-    float *red = reinterpret_cast<float *>(smem);              // [8 warps][8 rows][RP]
-    float *own = red + 8 * 8 * RP;                              // [8 rows][RP] this CTA's K half
-    float *rx = own + 8 * RP;                                   // [8 rows][RP] peer half (CTA 0)
-    const uint32_t rx_peer = map_to_rank(smem_s + 9 * 8 * RP * 4, 0);
-    Dec3SItem *its = reinterpret_cast<Dec3SItem *>(smem + 10 * 8 * RP * 4);
-    const int n_mine = sp < a.n_sitems ? (a.n_sitems - sp + n_sp - 1) / n_sp : 0;
+    const int K = a.K, r = a.r, n_groups = a.n_groups, n_uniq = a.n_uniq, n_si = a.n_sitems;
+    float *red = reinterpret_cast<float *>(smem + L::red);
+    float *own = reinterpret_cast<float *>(smem + L::own);
+    Dec3SItem *its = reinterpret_cast<Dec3SItem *>(smem + L::items);
+    const int n_mine = (a.flags & 8) ? 0 : (sp < n_si ? min((n_si - sp + n_sp - 1) / n_sp, kDec3MaxShrinkItems) : 0);
     {
         constexpr int W4 = sizeof(Dec3SItem) / 16;
-        const uint4 *src = reinterpret_cast<const uint4 *>(sitems);
         uint4 *dst = reinterpret_cast<uint4 *>(its);
-        for (int e = threadIdx.x; e < min(n_mine, kMaxItems) * W4; e += kT3)
-            dst[e] = src[(size_t)(sp + (e / W4) * n_sp) * W4 + e % W4];
+        for (int e = threadIdx.x; e < n_mine * W4; e += kT3) {
+            const int item = sp + (e / W4) * n_sp, w4 = e % W4;
+            dst[e] = a.inl ? reinterpret_cast<const uint4 *>(&inl.items[item])[w4]
+                           : __ldg(reinterpret_cast<const uint4 *>(a.sitems + item) + w4);
+        }
     }
     __syncthreads();
-    const int ngr = a.K / 8;                                   // 128-bit granules of a row
+    if (threadIdx.x == 0) dbg_stamp(a, 10);
+    const int ngr = K / 8;                                     // 128-bit granules of a row
     const int gl = (int)rank * kT3 + threadIdx.x;              // this lane's first granule
-    int done = 0;
-    for (int ii0 = 0; ii0 < ((a.flags & 8) ? 0 : n_mine); ++ii0) {
-        const Dec3SItem &si = its[ii0];   // the host keeps <= kDec3MaxShrinkItems items per pair
-        const Dec3Proj &P = a.proj[si.p];
+    for (int ii0 = 0; ii0 < n_mine; ++ii0) {
+        const Dec3SItem &si = its[ii0];
         const __nv_bfloat16 *A = reinterpret_cast<const __nv_bfloat16 *>(si.A);
-#pragma unroll 1
-        for (int j0 = 0; j0 < RP && j0 < a.r; j0 += JG) {
-            float acc[8][JG];
+        const int n = si.n;
+        int rows[8];
 #pragma unroll
-            for (int i = 0; i < 8; ++i)
-#pragma unroll
-                for (int j = 0; j < JG; ++j) acc[i][j] = 0.f;
+        for (int i = 0; i < 8; ++i) rows[i] = si.rows[i];
+        // one granule per lane per 512-lane sweep of K; A rows in groups of 8, the next group's
+        // loads in flight while the current group is multiplied (one HBM round trip for r <= 16)
 #pragma unroll 1
-            for (int gr = gl; gr < ngr; gr += 2 * kT3) {
-                uint4 xa[8], aa[JG];
+        for (int sw = 0; sw < ngr; sw += 2 * kT3) {   // every lane takes part (shuffles), idle lanes load zeros
+            const int gr = sw + gl;
+            const bool gok = gr < ngr;
+            float xf[8][8];
+            {
+                uint4 xa[8];
 #pragma unroll
                 for (int i = 0; i < 8; ++i)
-                    xa[i] = i < si.n ? __ldg(reinterpret_cast<const uint4 *>(X + (size_t)si.rows[i] * a.K) + gr)
-                                     : make_uint4(0, 0, 0, 0);
+                    xa[i] = (i < n && gok) ? __ldg(reinterpret_cast<const uint4 *>(X + (size_t)rows[i] * K) + gr)
+                                           : make_uint4(0, 0, 0, 0);
+#pragma unroll
+                for (int i = 0; i < 8; ++i) bf16x8_to_f32(xa[i], xf[i]);
+            }
+            auto load_group = [&](int j0, uint4 (&aa)[JG]) {
 #pragma unroll
                 for (int j = 0; j < JG; ++j)
-                    aa[j] = j0 + j < a.r ? __ldg(reinterpret_cast<const uint4 *>(A + (size_t)(j0 + j) * a.K) + gr)
-                                         : make_uint4(0, 0, 0, 0);
+                    aa[j] = (j0 + j < r && gok) ? __ldg(reinterpret_cast<const uint4 *>(A + (size_t)(j0 + j) * K) + gr)
+                                                : make_uint4(0, 0, 0, 0);
+            };
+            uint4 aa[JG], an[JG];
+            load_group(0, aa);
+            if (JG < r) load_group(JG, an);
+#pragma unroll 1
+            for (int j0 = 0; j0 < RP && j0 < r; j0 += JG) {
+                float acc[8][JG];
+#pragma unroll
+                for (int i = 0; i < 8; ++i)
+#pragma unroll
+                    for (int j = 0; j < JG; ++j) acc[i][j] = 0.f;
 #pragma unroll
                 for (int j = 0; j < JG; ++j) {
                     float af[8];
                     bf16x8_to_f32(aa[j], af);
 #pragma unroll
-                    for (int i = 0; i < 8; ++i) {
-                        float xf[8];
-                        bf16x8_to_f32(xa[i], xf);
+                    for (int i = 0; i < 8; ++i)
 #pragma unroll
-                        for (int e = 0; e < 8; ++e) acc[i][j] = fmaf(af[e], xf[e], acc[i][j]);
-                    }
+                        for (int e = 0; e < 8; ++e) acc[i][j] = fmaf(af[e], xf[i][e], acc[i][j]);
+                }
+#pragma unroll
+                for (int j = 0; j < JG; ++j) aa[j] = an[j];
+                if (j0 + 2 * JG < r) load_group(j0 + 2 * JG, an);
+                // lanes -> one value each (transpose-reduce); the sweep's partials accumulate in red
+#pragma unroll
+                for (int h = 0; h < JG / 4; ++h) {
+                    float v[32];
+#pragma unroll
+                    for (int jj = 0; jj < 4; ++jj)
+#pragma unroll
+                        for (int i = 0; i < 8; ++i) v[jj * 8 + i] = acc[i][4 * h + jj];
+                    const float s = warp_transpose_reduce32(v, lane);
+                    float *dst = &red[(warp * 8 + (lane & 7)) * RP + j0 + 4 * h + (lane >> 3)];
+                    *dst = sw == 0 ? s : *dst + s;
                 }
             }
-            // lanes -> one value each (transpose-reduce), then per warp into shared memory
-#pragma unroll
-            for (int h = 0; h < JG / 4; ++h) {
-                float v[32];
-#pragma unroll
-                for (int jj = 0; jj < 4; ++jj)
-#pragma unroll
-                    for (int i = 0; i < 8; ++i) v[jj * 8 + i] = acc[i][4 * h + jj];
-                const float s = warp_transpose_reduce32(v, lane);
-                red[(warp * 8 + (lane & 7)) * RP + j0 + 4 * h + (lane >> 3)] = s;
-            }
         }
+        if (threadIdx.x == 0 && ii0 == 0) dbg_stamp(a, 11);
         __syncthreads();
-        // warps in fixed order -> this CTA's K half; the peer's half goes to CTA 0 through DSMEM
-        for (int e = threadIdx.x; e < 8 * RP; e += kT3) {
-            const int ii = e / RP, jj = e % RP;
-            float t = 0.f;
-            if (jj < a.r)
-                for (int w = 0; w < 8; ++w) t += red[(w * 8 + ii) * RP + jj];
-            if (rank == 1) st_cluster_f32(rx_peer + (uint32_t)e * 4u, t);
-            else own[e] = t;
-        }
-        cluster_sync();
-        if (rank == 0) {
+        // warps in fixed order -> this CTA's K half; CTA 1 pushes it into CTA 0's slot of this item
+        const uint32_t rx_s = smem_s + L::rx + (uint32_t)ii0 * 8 * RP * 4;
+        const uint32_t bar_s = smem_s + L::bars + (uint32_t)ii0 * 8;
+        if (rank == 1) {
+            const uint32_t rx_peer = map_to_rank(rx_s, 0);
+            for (int e = threadIdx.x; e < 8 * RP; e += kT3) {
+                const int ii = e / RP, jj = e % RP;
+                float t = 0.f;
+                if (jj < r)
+                    for (int w = 0; w < 8; ++w) t += red[(w * 8 + ii) * RP + jj];
+                st_cluster_f32(rx_peer + (uint32_t)e * 4u, t);
+            }
+            mbar_arrive_remote_release(map_to_rank(bar_s, 0));   // every thread: its stores are released
+        } else {
+            for (int e = threadIdx.x; e < 8 * RP; e += kT3) {
+                const int ii = e / RP, jj = e % RP;
+                float t = 0.f;
+                if (jj < r)
+                    for (int w = 0; w < 8; ++w) t += red[(w * 8 + ii) * RP + jj];
+                own[e] = t;
+            }
+            mbar_wait_acq_cluster(bar_s, 0);
+            __syncthreads();
+            if (threadIdx.x == 0 && ii0 == 0) dbg_stamp(a, 13);
+            const Dec3Proj &P = a.proj[si.p];
             __nv_bfloat16 *sv = reinterpret_cast<__nv_bfloat16 *>(P.sv);
+            __nv_bfloat16 *vsave = reinterpret_cast<__nv_bfloat16 *>(P.Vsave);
+            const float *rx = reinterpret_cast<const float *>(smem + L::rx + (size_t)ii0 * 8 * RP * 4);
             if (si.zero_fill) {
                 // the adapter's slab rows of every other batch row (and past S) are zero
-                for (int e = threadIdx.x; e < a.n_groups * 256; e += kT3) {
+                for (int e = threadIdx.x; e < n_groups * 256; e += kT3) {
                     if ((si.mask[e >> 5] >> (e & 31)) & 1u) continue;
-                    uint4 *z = reinterpret_cast<uint4 *>(sv + ((size_t)((e >> 8) * a.n_uniq + si.uidx) * 256 + (e & 255)) * RP);
+                    uint4 *z = reinterpret_cast<uint4 *>(sv + ((size_t)((e >> 8) * n_uniq + si.uidx) * 256 + (e & 255)) * RP);
 #pragma unroll
                     for (int q = 0; q < RP / 8; ++q) z[q] = make_uint4(0, 0, 0, 0);
                 }
             }
             for (int e = threadIdx.x; e < 8 * RP; e += kT3) {
                 const int ii = e / RP, jj = e % RP;
-                if (ii >= si.n) continue;
+                if (ii >= n) continue;
                 const float v = own[e] + rx[e];   // K half 0 + K half 1 (fixed order)
                 const int row = si.rows[ii];
-                sv[((size_t)((row >> 8) * a.n_uniq + si.uidx) * 256 + (row & 255)) * RP + jj] =
+                sv[((size_t)((row >> 8) * n_uniq + si.uidx) * 256 + (row & 255)) * RP + jj] =
                     __float2bfloat16_rn(si.scale[ii] * v);
-                if (((si.ft_mask >> ii) & 1) && P.Vsave && jj < a.r)
-                    reinterpret_cast<__nv_bfloat16 *>(P.Vsave)[(size_t)row * a.r + jj] = __float2bfloat16_rn(v);
+                if (((si.ft_mask >> ii) & 1) && vsave && jj < r)
+                    vsave[(size_t)row * r + jj] = __float2bfloat16_rn(v);
             }
         }
-        ++done;
-        cluster_sync();   // rx / red reusable
+        if (threadIdx.x == 0 && ii0 == 0) dbg_stamp(a, 14);
+        __syncthreads();   // red / own reusable
     }
     // publish (slabs are read by TMA in other CTAs: generic -> async proxy)
-    if (a.flags & 8) done = n_mine;
+    const int done = (a.flags & 8) ? (sp < n_si ? (n_si - sp + n_sp - 1) / n_sp : 0) : n_mine;
     if (rank == 0 && done) {
         fence_proxy_async_global();
         __threadfence();
@@ -237,8 +305,7 @@ __device__ __forceinline__ void dec3_shrink_pair(const Dec3Args &a, const Dec3SI
 template <int RP>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT3, 1) smlm_dec3_kernel(const __grid_constant__ Dec3Args a,
                                                                                         const __grid_constant__ Dec3Inline inl) {
-    const int *uslot = a.inl ? inl.uslot : a.uslot;
-    const Dec3SItem *sitems = a.inl ? inl.items : a.sitems;
+
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw = smem_u32(smem_raw);
     const uint32_t base = (raw + 1023u) & ~1023u;
@@ -277,6 +344,36 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT3, 1) smlm_dec3_ke
             if (a.n_uniq) tma_prefetch_desc(&a.proj[p].tmSV);
         }
     }
+    // this split's expand adapters (uslot index), in ascending order, staged once in shared memory:
+    // the producer / MMA loops then never touch parameter or global memory per adapter
+    __shared__ int s_ulist[kDec3InlineSlots];
+    __shared__ int s_uslot[kDec3InlineSlots];
+    __shared__ int s_wcnt[kT3 / 32];
+    __shared__ int s_ucount;
+    if (wpair) {
+        // parallel: every thread one adapter (param / global reads in a serial loop cost ~0.1 us each)
+        const int nu = a.n_uniq, ksp = a.ks, s0 = cid % ksp;
+        const bool expand = !(a.flags & 4);
+        const int u = threadIdx.x;
+        int sl = -1;
+        if (u < nu && u < kDec3InlineSlots) sl = (a.flags & 64) ? u : (a.inl ? inl.uslot[u] : a.uslot[u]);
+        if (u < kDec3InlineSlots) s_uslot[u] = sl;
+        const bool mine = sl >= 0 && expand && sl % ksp == s0;
+        const uint32_t bal = __ballot_sync(0xffffffffu, mine);
+        if (lane == 0) s_wcnt[warp] = __popc(bal);
+        __syncthreads();
+        int off = 0, tot = 0;
+        for (int w = 0; w < kT3 / 32; ++w) {
+            off += w < warp ? s_wcnt[w] : 0;
+            tot += s_wcnt[w];
+        }
+        if (mine) s_ulist[off + __popc(bal & ((1u << lane) - 1u))] = u;
+        if (threadIdx.x == 0) s_ucount = tot;
+    }
+    if (!wpair && rank == 0 && threadIdx.x == 0) {
+        for (int i = 0; i < kDec3MaxShrinkItems; ++i) mbar_init(base + ShrinkSmem<RP>::bars + 8u * i, kT3);
+        fence_mbar_init();
+    }
     if (wpair && warp == 2) {
         asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(tmem_slot), "r"(256)
                      : "memory");
@@ -292,7 +389,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT3, 1) smlm_dec3_ke
 
     if (!wpair) {
         // ========================= shrink pair =========================
-        dec3_shrink_pair<RP>(a, sitems, base_ptr, base, rank, cid - a.n_wpairs, n_clusters - a.n_wpairs);
+        dec3_shrink_pair<RP>(a, inl, base_ptr, base, rank, cid - a.n_wpairs, n_clusters - a.n_wpairs);
         if (threadIdx.x == 0) dbg_stamp(a, 1);
     } else {
         const int ks = a.ks;
@@ -342,9 +439,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT3, 1) smlm_dec3_ke
                     dbg_stamp(a, 2);
                 }
                 __syncwarp();
-                for (int u = 0; u < a.n_uniq; ++u) {
-                    const int sl = uslot[u];
-                    if (sl % ks != it.s || (a.flags & 4)) continue;
+                for (int iu = 0; iu < s_ucount; ++iu) {
+                    const int u = s_ulist[iu];
+                    const int sl = s_uslot[u];
                     mbar_wait(empty_bar(stage), phase ^ 1);
                     if (lane == 0) {
                         const uint32_t fb = map_to_rank(full_bar(stage), 0);
@@ -359,6 +456,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT3, 1) smlm_dec3_ke
                     __syncwarp();
                     if (++stage == ST) { stage = 0; phase ^= 1; }
                 }
+                if (lane == 0) dbg_stamp(a, 8);
             }
         } else if (warp == 1 && leader) {
             // ========================= MMA issuer (leader CTA) =========================
@@ -370,6 +468,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT3, 1) smlm_dec3_ke
             for (int kb = kb0; kb < kb1; ++kb) {
                 mbar_wait(full_bar(stage), phase);
                 tc_fence_after();
+                if (lane == 0 && ((kb - kb0) & 3) == 0 && (kb - kb0) < 24) dbg_stamp(a, 10 + (kb - kb0) / 4);
                 if (lane == 0) {
                     const uint32_t ab = a_addr(stage), bb = b_addr(stage);
                     if (!(a.flags & 32) || kb == kb0) {
@@ -383,8 +482,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT3, 1) smlm_dec3_ke
                 __syncwarp();
                 if (++stage == ST) { stage = 0; phase ^= 1; }
             }
-            for (int u = 0; u < a.n_uniq; ++u) {
-                if (uslot[u] % ks != it.s || (a.flags & 4)) continue;
+            for (int iu = 0; iu < s_ucount; ++iu) {
                 mbar_wait(full_bar(stage), phase);
                 tc_fence_after();
                 if (lane == 0) {
@@ -398,13 +496,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT3, 1) smlm_dec3_ke
                 __syncwarp();
                 if (++stage == ST) { stage = 0; phase ^= 1; }
             }
-            if (lane == 0) mma2_commit_mc(acc_full);
+            if (lane == 0) {
+                dbg_stamp(a, 9);
+                mma2_commit_mc(acc_full);
+            }
             __syncwarp();
         } else if (warp == 3 && a.n_uniq > 0) {
             // expand operands of this split: descriptors and B_u rows of the tile -> caches / L2
-            for (int u = lane; u < a.n_uniq; u += 32) {
-                const int sl = uslot[u];
-                if (sl % ks != it.s) continue;
+            for (int iu = lane; iu < s_ucount; iu += 32) {
+                const int sl = s_uslot[s_ulist[iu]];
                 const SlotDev *sd = P.slots + sl;
                 tma_prefetch_desc(&sd->tmBk);
                 const int wrow = it.n0 + 128 * (int)rank;

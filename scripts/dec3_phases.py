@@ -41,13 +41,14 @@ for proj in (os.environ.get("PROJ", "q,k").split(",")):
     rel = (t - t0) / 1e3
     wm = t[:, 4] > 0
     out = {"proj": proj, "w_ctas": int(wm.sum()), "shrink_ctas": int((~wm).sum())}
-    names = ["start", "loads_issued", "v_seen", "parts_stored", "acc_ready", "arrived", "stored"]
+    names = ["start", "loads_issued", "v_seen", "parts_stored", "acc_ready", "arrived", "stored", "xbar", "exp_issued", "mma_done", "kb0", "kb4", "kb8", "kb12", "kb16", "kb20"]
     for k, name in enumerate(names):
         col = rel[wm, k][t[wm, k] > 0]
         if len(col):
             out[name] = [round(float(np.min(col)), 2), round(float(np.median(col)), 2), round(float(np.max(col)), 2)]
-    col = rel[~wm, 1][t[~wm, 1] > 0]
-    if len(col):
-        out["shrink_done"] = [round(float(np.min(col)), 2), round(float(np.median(col)), 2), round(float(np.max(col)), 2)]
+    for k, name in [(10, "s_staged"), (11, "s_item0_fma"), (12, "s_item0_red"), (13, "s_item0_csync"), (14, "s_item0_written"), (15, "s_item0_end"), (1, "shrink_done")]:
+        col = rel[~wm, k][t[~wm, k] > 0]
+        if len(col):
+            out[name] = [round(float(np.min(col)), 2), round(float(np.median(col)), 2), round(float(np.max(col)), 2)]
     print(json.dumps(out))
     pool.close()

@@ -26,6 +26,7 @@ __device__ __forceinline__ void bulk1d(uint32_t dst, const void *src, uint32_t n
 }
 
 constexpr int STMAX = 13;
+__device__ CUtensorMap xmap_g;
 __global__ void __launch_bounds__(32) kstream(const __grid_constant__ CUtensorMap map, const char *W, int mode, int rows, int K, int ks, int ST) {
     extern __shared__ __align__(1024) uint8_t sm[];
     __shared__ uint64_t bars[STMAX];
@@ -38,7 +39,7 @@ __global__ void __launch_bounds__(32) kstream(const __grid_constant__ CUtensorMa
     if (mode == 2) { rb = blockIdx.x; kb0 = 0; kb1 = nkb; }
     else { rb = blockIdx.x / ks; int s = blockIdx.x % ks; int q = nkb / ks, rm = nkb % ks; kb0 = s * q + min(s, rm); kb1 = kb0 + q + (s < rm); }
     int boxr = mode == 2 ? 128 : 128;
-    uint32_t bytes = 64 * 2 * boxr;
+    uint32_t bytes = 64 * 2 * boxr * (mode == 4 ? 2 : 1);
     for (int i = kb0, n = 0; i < kb1; ++i, ++n) {
         int s = n % ST;
         uint32_t ph = (n / ST) & 1;
@@ -46,7 +47,15 @@ __global__ void __launch_bounds__(32) kstream(const __grid_constant__ CUtensorMa
         if (n >= ST) mwait(bar, ph ^ 1);
         expect_tx(bar, bytes);
         if (mode == 1) bulk1d(base + s * 16384, W + ((size_t)rb * nkb + i) * 16384, 16384, bar);
-        else tma2d(base + s * 16384, &map, bar, i * 64, rb * boxr);
+        else if (mode == 4) {
+            // W box + an X box (2 MiB L2-resident matrix, 256 rows) per stage: 32 KB per stage
+            tma2d(base + s * 32768, &map, bar, i * 64, rb * boxr);
+            tma2d(base + s * 32768 + 16384, &xmap_g, bar, i * 64, (blockIdx.x & 1) * 128);
+        } else if (mode == 3) {
+            // 4 narrow boxes {16 cols (32 B), 128 rows} per 16 KB stage, from the [rows*K/16][16] view
+            for (int j = 0; j < 4; ++j)
+                tma2d(base + s * 16384 + j * 4096, &map, bar, 0, ((rb * nkb + i) * 4 + j) * 128);
+        } else tma2d(base + s * 16384, &map, bar, i * 64, rb * boxr);
     }
     for (int n = max(0, (kb1 - kb0) - ST); n < kb1 - kb0; ++n) mwait(su32(&bars[n % ST]), (n / ST) & 1);
 }
@@ -61,7 +70,20 @@ int main() {
     void *fn; cudaDriverEntryPointQueryResult q;
     cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
     auto enc = (PFN_cuTensorMapEncodeTiled_v12000)fn;
-    std::vector<CUtensorMap> maps(nset);
+    std::vector<CUtensorMap> maps(nset), nmaps(nset);
+    {
+        char *Xb; cudaMalloc(&Xb, (size_t)256 * K * 2); cudaMemset(Xb, 1, (size_t)256 * K * 2);
+        CUtensorMap xm;
+        cuuint64_t dims[2] = {(cuuint64_t)K, 256}, str[1] = {(cuuint64_t)K * 2};
+        cuuint32_t box[2] = {64, 128}, es[2] = {1, 1};
+        enc(&xm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, Xb, dims, str, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        cudaMemcpyToSymbol(xmap_g, &xm, sizeof(xm));
+    }
+    for (int i = 0; i < nset; ++i) {
+        cuuint64_t dims[2] = {16, (cuuint64_t)rows * K / 16}, str[1] = {32};
+        cuuint32_t box[2] = {16, 128}, es[2] = {1, 1};
+        enc(&nmaps[i], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, W[i], dims, str, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    }
     for (int i = 0; i < nset; ++i) {
         cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)rows}, str[1] = {(cuuint64_t)K * 2};
         cuuint32_t box[2] = {64, 128}, es[2] = {1, 1};
@@ -70,17 +92,17 @@ int main() {
     cudaFuncSetAttribute(kstream, cudaFuncAttributeMaxDynamicSharedMemorySize, 13 * 16384 + 1024);
     cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
     struct Cfg { int mode, ks, st; const char *name; };
-    Cfg cfgs[] = {{0, 4, 6, "tma2d ks=4 st=6"}, {0, 4, 12, "tma2d ks=4 st=12"}, {1, 4, 12, "bulk1d ks=4 st=12"},
-                  {0, 2, 12, "tma2d ks=2 st=12"}, {0, 8, 12, "tma2d ks=8 st=12"}, {1, 8, 6, "bulk1d ks=8 st=6"}};
+    Cfg cfgs[] = {{0, 3, 6, "W only ks=3 st=6 (16KB stages)"}, {4, 3, 6, "W + X(L2) ks=3 st=6 (32KB stages)"},
+                  {0, 4, 12, "W only ks=4 st=12"}, {4, 4, 6, "W + X ks=4 st=6"}};
     for (auto &c : cfgs) {
         int grid = rows / 128 * c.ks;
-        size_t smem = c.st * 16384 + 1024;
-        for (int it = 0; it < 3; ++it) kstream<<<grid, 32, smem>>>(maps[it % nset], W[it % nset], c.mode, rows, K, c.ks, c.st);
+        size_t smem = c.st * (c.mode == 4 ? 32768 : 16384) + 1024;
+        for (int it = 0; it < 3; ++it) kstream<<<grid, 32, smem>>>(c.mode == 3 ? nmaps[it % nset] : maps[it % nset], W[it % nset], c.mode, rows, K, c.ks, c.st);
         cudaDeviceSynchronize();
         float best = 1e9, tot = 0;
         for (int it = 0; it < 16; ++it) {
             cudaEventRecord(a);
-            kstream<<<grid, 32, smem>>>(maps[it % nset], W[it % nset], c.mode, rows, K, c.ks, c.st);
+            kstream<<<grid, 32, smem>>>(c.mode == 3 ? nmaps[it % nset] : maps[it % nset], W[it % nset], c.mode, rows, K, c.ks, c.st);
             cudaEventRecord(b);
             cudaEventSynchronize(b);
             float ms; cudaEventElapsedTime(&ms, a, b);
