@@ -266,6 +266,11 @@ struct smlm_pool_s {
     std::vector<MapEnt> map_cache;
     size_t map_next = 0;
     Ring ring;
+    // pinned arena for plan uploads recorded into a CUDA graph (stream capture): a captured memcpy
+    // node re-reads its host source at every replay, so captured plans get their own bytes that live
+    // until the pool is destroyed (bump allocation; no event synchronisation during capture)
+    uint8_t *cap_arena = nullptr;
+    size_t cap_used = 0, cap_size = 0;
 };
 
 namespace {
@@ -492,6 +497,27 @@ WsLayout layout_for(smlm_pool p, const smlm_batch *b, const Plan &plan, bool bwd
 // Copy a host byte vector into the workspace through the pinned ring (stream ordered).
 int stage_upload(smlm_pool p, const std::vector<uint8_t> &bytes, void *dst, cudaStream_t st) {
     if (bytes.empty()) return SMLM_OK;
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(st, &cs);
+    if (cs != cudaStreamCaptureStatusNone) {
+        const size_t need = (bytes.size() + 255) & ~size_t(255);
+        if (!p->cap_arena || p->cap_used + need > p->cap_size)
+            return set_err(SMLM_E_UNSUPPORTED, "graph capture: plan arena exhausted (call once outside capture to size it, "
+                                               "or capture fewer calls per pool)");
+        uint8_t *h = p->cap_arena + p->cap_used;
+        p->cap_used += need;
+        memcpy(h, bytes.data(), bytes.size());
+        cudaError_t e = cudaMemcpyAsync(dst, h, bytes.size(), cudaMemcpyHostToDevice, st);
+        if (e != cudaSuccess) return cuda_err(e, "plan upload (capture)");
+        return SMLM_OK;
+    }
+    if (!p->cap_arena) {   // sized once, outside capture: room for many captured calls of this size
+        p->cap_size = std::max<size_t>(1 << 20, 64 * ((bytes.size() + 255) & ~size_t(255)));
+        if (cudaMallocHost((void **)&p->cap_arena, p->cap_size) != cudaSuccess) {
+            p->cap_arena = nullptr;
+            p->cap_size = 0;
+        }
+    }
     void *h = nullptr;
     int idx = p->ring.acquire(bytes.size(), &h);
     if (idx < 0) return set_err(SMLM_E_CUDA, "cudaMallocHost failed");
@@ -519,7 +545,8 @@ int run_dec3(int n_proj, const smlm_pool *pools, const smlm_batch *b, const Dec3
     int rc;
     double t0 = g_hprof.on ? now_us() : 0;
     static thread_local Dec3Inline inl;   // kernel parameter block (copied at launch)
-    const bool inline_plan = n_uniq <= kDec3InlineSlots && (int)D.sitems.size() <= kDec3InlineItems;
+    static const bool no_inline = getenv("SMLM_DEC3_NOINLINE") != nullptr;   // measurement override
+    const bool inline_plan = !no_inline && n_uniq <= kDec3InlineSlots && (int)D.sitems.size() <= kDec3InlineItems;
     if (inline_plan) {
         if (n_uniq) memcpy(inl.uslot, D.uslot.data(), n_uniq * sizeof(int));
         if (!D.sitems.empty()) memcpy(inl.items, D.sitems.data(), D.sitems.size() * sizeof(Dec3SItem));
@@ -695,6 +722,7 @@ int smlm_pool_destroy(smlm_pool p) {
         cudaDeviceSynchronize();
         if (p->d_slots) cudaFree(p->d_slots);
         if (p->d_ctr) cudaFree(p->d_ctr);
+        if (p->cap_arena) cudaFreeHost(p->cap_arena);
     }
     delete p;
     return SMLM_OK;

@@ -196,7 +196,7 @@ struct Dec3Args {
     int inl;                // 1: uslot / sitems are passed inline (Dec3Inline kernel parameter)
 };
 // small plans ride in the kernel parameters (no H2D copy in the stream)
-constexpr int kDec3InlineItems = 96;
+constexpr int kDec3InlineItems = 176;   // Dec3Args + Dec3Inline stay under the 32 KB parameter limit
 constexpr int kDec3InlineSlots = 256;
 struct Dec3Inline {
     Dec3SItem items[kDec3InlineItems];

@@ -644,6 +644,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT3, 1) smlm_dec3_ke
     }
 }
 
+static_assert(sizeof(Dec3Args) + sizeof(Dec3Inline) <= 32764, "kernel parameters exceed 32 KB");
+
 template <int RP>
 int launch_dec3_impl(const Dec3Args &a, const Dec3Inline &in, int clusters, cudaStream_t st) {
     auto kern = smlm_dec3_kernel<RP>;

@@ -99,7 +99,90 @@ def run_config(k, iters=30, graphs=False):
     return out, total_ms
 
 
+def c2_layer_step(iters=40, graphs=True):
+    """C2 as a layer would issue it: q/k/v in ONE smlm_forward_multi call (they share X), then o
+    (its input is the attention output) -- back to back over 8 rotated weight sets, and as a CUDA
+    graph replay of 8 layer-steps.  Roofline units per SURVEY.md §8(d): the 4 projections' bytes."""
+    k = 2
+    spec = synth.CONFIGS[k]
+    dev = torch.device("cuda", 0)
+    batch = synth.config_batch(k)
+    b = S.Batch.from_synth(batch)
+    r, U = spec.rank, spec.n_adapters
+    uniq = sorted(set(int(x) for x in batch.slots if x >= 0))
+    g = torch.Generator(device=dev)
+    g.manual_seed(17)
+    in_f = 4096
+    Xqkv = torch.randn(batch.S, in_f, generator=g, device=dev).to(torch.bfloat16)
+    Xo = torch.randn(batch.S, in_f, generator=g, device=dev).to(torch.bfloat16)
+    sets = []
+    for _ in range(NSETS):
+        layer = {}
+        for p in ("q", "k", "v", "o"):
+            _, out_f = synth.PROJ_SHAPES[p]
+            W = (torch.randn(out_f, in_f, generator=g, device=dev) / math.sqrt(in_f)).to(torch.bfloat16)
+            A = (torch.randn(U, r, in_f, generator=g, device=dev) / math.sqrt(in_f)).to(torch.bfloat16)
+            B = (torch.randn(U, out_f, r, generator=g, device=dev) / (4 * math.sqrt(r))).to(torch.bfloat16)
+            pool = S.Pool(in_f, out_f, r, U, S.SMLM_BF16, 0)
+            for a in range(U):
+                pool.register(A[a], B[a], 2.0)
+            Y = torch.empty(batch.S, out_f, dtype=torch.bfloat16, device=dev)
+            layer[p] = (W, A, B, pool, Y)
+        sets.append(layer)
+    qkv = [sets[0][p][3].h for p in ("q", "k", "v")]
+    nws = max(S.smlm_workspace_size_multi(qkv, b), S.smlm_workspace_size(sets[0]["o"][3].h, b, False))
+    ws = torch.empty(nws + 256, dtype=torch.uint8, device=dev)
+    st = torch.cuda.current_stream()
+
+    def step(i):   # on the current stream (the capture stream inside the graph context)
+        L = sets[i % NSETS]
+        S.smlm_forward_multi([L[p][3].h for p in ("q", "k", "v")], b, Xqkv, [L[p][0] for p in ("q", "k", "v")],
+                             [L[p][4] for p in ("q", "k", "v")], None, ws)
+        S.smlm_forward(L["o"][3].h, b, Xo, L["o"][0], L["o"][4], None, ws)
+    for i in range(2 * NSETS):
+        step(i)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    for i in range(iters):
+        step(i)
+    e1.record(st)
+    e1.synchronize()
+    ms_b2b = e0.elapsed_time(e1) / iters
+    ms_graph = None
+    if graphs:
+        gr = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(gr, stream=torch.cuda.Stream()):
+            for i in range(NSETS):
+                step(i)
+        for _ in range(3):
+            gr.replay()
+        torch.cuda.synchronize()
+        e0.record()
+        reps = 10
+        for _ in range(reps):
+            gr.replay()
+        e1.record()
+        e1.synchronize()
+        ms_graph = e0.elapsed_time(e1) / (reps * NSETS)
+    roof_ms = 0.0
+    for p in ("q", "k", "v", "o"):
+        _, out_f = synth.PROJ_SHAPES[p]
+        nbytes = in_f * out_f * 2 + len(uniq) * r * (in_f + out_f) * 2 + batch.S * (in_f + out_f) * 2
+        flops = 2.0 * batch.S * in_f * out_f + 2.0 * batch.S * r * (in_f + out_f)
+        roof_ms += max(nbytes / (PEAKS["hbm_gbs"] * 1e9), flops / (PEAKS["bf16_tflops"] * 1e12)) * 1e3
+    for L in sets:
+        for p in L:
+            L[p][3].close()
+    best = min(ms_b2b, ms_graph or 1e9)
+    return {"config": "C2-decode layer-step (qkv fused + o)", "S": batch.S, "ms_back_to_back": ms_b2b,
+            "ms_graph_replay": ms_graph, "roofline_ms": roof_ms, "rows_per_s": batch.S / (best / 1e3),
+            "hbm_roofline_frac_b2b": roof_ms / ms_b2b,
+            "hbm_roofline_frac_graph": None if ms_graph is None else roof_ms / ms_graph}
+
+
 def main():
+    print(json.dumps(c2_layer_step()), flush=True)
     for k in (2, 3):
         rows, tot = run_config(k)
         for r in rows:
