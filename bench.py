@@ -277,6 +277,7 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-side", action="store_true", help="skip the C2 / C3 side measurements")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--dist-backend", default="nccl", help="nccl (production); gloo only to exercise the N>1 "
                     "path on a single-GPU box")
@@ -409,6 +410,26 @@ def main():
     if not args.no_e2e:
         e2e = run_e2e(wl, stream, max(4, min(args.steps, 8)), n, dist)
 
+    # ---- the other BASELINE.json configs as side measurements (rank 0, N=1): C2 decode layer-step
+    # (q/k/v in one smlm_forward_multi launch + o; CUDA-graph replay) and C3 prefill ----
+    side = None
+    if rank == 0 and n == 1 and not args.no_side:
+        try:
+            sys.path.insert(0, os.path.join(ROOT, "scripts"))
+            import bench_configs as bc
+            c2 = bc.c2_layer_step()
+            rows3, tot3 = bc.run_config(3, iters=10)
+            side = {"C2_decode": {"workload": c2["config"], "rows": c2["S"], "ms_graph_replay": c2["ms_graph_replay"],
+                                  "ms_back_to_back": c2["ms_back_to_back"], "rows_per_s": c2["rows_per_s"],
+                                  "hbm_roofline_frac": c2["hbm_roofline_frac_graph"],
+                                  "roofline_ms": c2["roofline_ms"], "bound": "hbm"},
+                    "C3_prefill": {"workload": synth.CONFIGS[3].name + ": gate, up, down", "ms": tot3,
+                                   "rows_per_s": synth.config_batch(3).S / (tot3 / 1e3),
+                                   "tensor_roofline_frac": sum(r["roofline_ms"] for r in rows3) / tot3,
+                                   "bound": "tensor"}}
+        except Exception as ex:   # side measurements never break the headline line
+            side = {"error": repr(ex)[:200]}
+
     cpu = None
     if rank == 0 and n == 1 and not args.no_cpu_baseline:
         v, dt, sub, threads = time_oracle(k, args.oracle_rows, 1)
@@ -429,7 +450,7 @@ def main():
                           "step": "1 layer-step = forward 7 projections + fine-tune backward 7 projections"
                                   + (" + NCCL all-reduce of fine-tune dA/dB" if n > 1 else "")},
                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
-               "clocks": clk}
+               "clocks": clk, "configs": side}
         print(json.dumps(out))
     if dist is not None:
         dist.barrier()

@@ -369,3 +369,41 @@ def test_bf16_multi_fallbacks_and_errors():
     assert ei.value.code in (S.SMLM_E_SLOT, S.SMLM_E_INVALID)
     p0.close()
     p1.close()
+
+
+def test_bf16_decode_graph_capture_replays_eager():
+    """A decode call recorded into a CUDA graph (inline plan in the kernel parameters) replays to
+    the same Y as the eager call, bit for bit, including after the inputs change in place."""
+    from paper_2511_00101_b200 import smlm as S
+    batch, ws_, X = _multi_case(21, 512, (256, 128), 16, 4, 96)
+    dev = torch.device("cuda", 0)
+    pools = []
+    for w in ws_:
+        pool = S.Pool(512, w.W.shape[0], 16, 4)
+        for a in range(4):
+            pool.register(w.A[a].to(dev).contiguous(), w.B[a].to(dev).contiguous(), w.slot_scale[a])
+        pools.append(pool)
+    b = S.Batch.from_synth(batch)
+    Xd = X.to(dev).contiguous()
+    Ws = [w.W.to(dev).contiguous() for w in ws_]
+    Ys = [torch.empty(batch.S, w.W.shape[0], dtype=torch.bfloat16, device=dev) for w in ws_]
+    wsb = torch.empty(S.smlm_workspace_size_multi([p.h for p in pools], b) + 256, dtype=torch.uint8, device=dev)
+    S.smlm_forward_multi([p.h for p in pools], b, Xd, Ws, Ys, None, wsb)
+    torch.cuda.synchronize()
+    eager = [y.clone() for y in Ys]
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        S.smlm_forward_multi([p.h for p in pools], b, Xd, Ws, Ys, None, wsb)
+    for y in Ys:
+        y.fill_(0)
+    g.replay()
+    torch.cuda.synchronize()
+    for y, e in zip(Ys, eager):
+        assert torch.equal(y, e)
+    Xd.mul_(-1)                                   # new inputs, same buffers: Y flips sign exactly
+    g.replay()
+    torch.cuda.synchronize()
+    for y, e in zip(Ys, eager):
+        assert torch.equal(y.float(), -e.float())
+    for p in pools:
+        p.close()
