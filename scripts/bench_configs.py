@@ -182,7 +182,9 @@ def c2_layer_step(iters=40, graphs=True):
 
 
 def main():
-    print(json.dumps(c2_layer_step()), flush=True)
+    print(json.dumps(c2_layer_step(graphs="--c2-only" not in sys.argv)), flush=True)
+    if "--c2-only" in sys.argv:
+        return
     for k in (2, 3):
         rows, tot = run_config(k)
         for r in rows:

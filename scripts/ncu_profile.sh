@@ -20,3 +20,7 @@ $NCU --set full --clock-control none --import-source on -k regex:smlm_gemm2_kern
 $NCU --set full --clock-control none --import-source on -k regex:smlm_tok_kernel -s 9 -c 1 -o $OUT/prof_tok -f $CMD > /dev/null 2>&1
 $NCU --set full --clock-control none --import-source on -k regex:smlm_u_kernel -s 9 -c 1 -o $OUT/prof_u -f $CMD > /dev/null 2>&1
 ls -la $OUT
+# decode path (kernels_dec3.cu): one q projection call and one fused q/k/v call at C2 shapes
+$NCU --set full --clock-control none --import-source on -k regex:smlm_dec3 -s 2 -c 1 -o $OUT/prof_dec3_q -f env PROJ=q N=3 python scripts/run_c2_once.py > /dev/null 2>&1
+$NCU --set full --clock-control none --import-source on -k regex:smlm_dec3 -s 2 -c 1 -o $OUT/prof_dec3_qkv -f python scripts/dec_layer_phases.py > /dev/null 2>&1
+$NCU --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file $OUT/dec_launches.csv python scripts/bench_configs.py --c2-only > /dev/null 2>&1
