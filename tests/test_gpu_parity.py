@@ -224,7 +224,7 @@ def test_full_config_sampled(k, proj):
 
 
 @pytest.mark.parametrize("rows,in_f,out_f,r", [(200, 512, 320, 16), (64, 1024, 256, 8), (450, 512, 192, 32),
-                                               (300, 192, 256, 16), (512, 1024, 128, 64)])
+                                               (300, 192, 256, 16), (512, 1024, 128, 64), (384, 14336, 256, 16)])
 def test_bf16_decode_batches(rows, in_f, out_f, r):
     """Pure decode batches (the transposed split-K kernel path): one-row DECODE segments, random
     slots including base-only rows, unsorted."""
@@ -235,6 +235,22 @@ def test_bf16_decode_batches(rows, in_f, out_f, r):
     assert res.plan_fwd == plan_oracle.forward_plan(batch.offsets, batch.slots, batch.modes)
     Y, _ = oracle.forward(batch, w.W, w.A, w.B, w.slot_scale, X)
     assert parity_err(res.Y, Y) <= BF16_TOL
+
+
+def test_bf16_decode_many_adapters_unsorted():
+    """512 unsorted one-row requests over 64 adapters (two 256-row groups, up to 8 adapters per
+    32-column expand split, several shrink items per adapter)."""
+    g = torch.Generator().manual_seed(64)
+    rows = 512
+    slots = torch.randint(-1, 64, (rows,), generator=g).tolist()
+    modes = [DECODE if i % 17 else FINETUNE for i in range(rows)]
+    batch, w, X, dY = synth.random_case(640, 1024, 512, 16, 64, [1] * rows, modes, slots)
+    res = run_smlm(batch, w, X, dY, backward=False)
+    Y, V = oracle.forward(batch, w.W, w.A, w.B, w.slot_scale, X)
+    assert parity_err(res.Y, Y) <= BF16_TOL
+    ft = batch.ft_rows()
+    ft = ft[batch.row_slot()[ft] >= 0]
+    assert parity_err(res.V.double().numpy()[ft], V[ft]) <= BF16_TOL
 
 
 def test_bf16_decode_grouped_with_finetune_short_rows():
