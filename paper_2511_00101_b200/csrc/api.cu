@@ -417,7 +417,7 @@ Dec3Plan dec3_plan(int n_proj, const smlm_pool *pools, const smlm_batch *b, cons
     D.clusters = n_si ? pairs : D.n_wpairs;
     if (NW > 256) return D;   // tile arrival counters
     if (n_uniq > kDec3InlineSlots) return D;   // per-split adapter list in shared memory
-    if (n_si && (n_si + (D.clusters - D.n_wpairs) - 1) / (D.clusters - D.n_wpairs) > kDec3MaxShrinkItems) return D;
+    if (n_si && (n_si + 2 * (D.clusters - D.n_wpairs) - 1) / (2 * (D.clusters - D.n_wpairs)) > 32) return D;   // kShrMI
     size_t off = 0;
     D.plan_off = off;
     off = align256(off + (size_t)n_uniq * 4 + 64 + D.sitems.size() * sizeof(Dec3SItem));

@@ -118,15 +118,18 @@ __device__ __forceinline__ Item3 dec3_item(const Dec3Args &a, int w) {
 // of K.  The pair's items are staged in shared memory first (no dependent global loads later).
 // ------------------------------------------------------------------------------------------
 // shared-memory layout of a shrink CTA (inside the pipeline ring, which shrink pairs do not use)
-template <int RP>
+template <int RP, int NW, int MI>
 struct ShrinkSmem {
-    static constexpr uint32_t red = 0;                                  // [8 warps][8 rows][RP] fp32
-    static constexpr uint32_t own = red + 8 * 8 * RP * 4;              // [8 rows][RP] this CTA's K half
-    static constexpr uint32_t items = own + 8 * RP * 4;                // [kDec3MaxShrinkItems] Dec3SItem
-    static constexpr uint32_t rx = items + kDec3MaxShrinkItems * sizeof(Dec3SItem);   // [items][8][RP] peer halves
-    static constexpr uint32_t bars = rx + kDec3MaxShrinkItems * 8 * RP * 4;           // [items] mbarriers
-    static constexpr uint32_t end = bars + kDec3MaxShrinkItems * 8;
+    static constexpr uint32_t red = 0;                                  // [NW warps][8 rows][RP] fp32
+    static constexpr uint32_t own = red + NW * 8 * RP * 4;             // [8 rows][RP] this CTA's K half
+    static constexpr uint32_t items = own + 8 * RP * 4;                // [MI] Dec3SItem
+    static constexpr uint32_t rx = items + MI * sizeof(Dec3SItem);     // [MI][8][RP] peer halves
+    static constexpr uint32_t bars = rx + MI * 8 * RP * 4;             // [MI] mbarriers
+    static constexpr uint32_t end = (bars + MI * 8 + 1023u) & ~1023u;
 };
+// a shrink CTA runs two independent 4-warp workers (warps 0-3, 4-7) so that one worker's loads
+// overlap the other's FMAs; each worker stages at most kShrMI items
+constexpr int kShrMI = 32;
 
 __device__ __forceinline__ void mbar_arrive_remote_release(uint32_t cluster_addr) {
     asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
@@ -149,31 +152,34 @@ __device__ __forceinline__ void mbar_wait_acq_cluster(uint32_t bar, uint32_t par
 // granule of K.  Items are staged in shared memory first; CTA 1 pushes its K half of every item
 // into CTA 0's shared memory (one slot and one mbarrier per item, no cluster-wide barrier).
 // ------------------------------------------------------------------------------------------
-template <int RP>
-__device__ __forceinline__ void dec3_shrink_pair(const Dec3Args &a, const Dec3Inline &inl, uint8_t *smem,
-                                                 uint32_t smem_s, uint32_t rank, int sp, int n_sp) {
-    using L = ShrinkSmem<RP>;
+template <int RP, int NW, int MI>
+__device__ __forceinline__ void dec3_shrink_worker(const Dec3Args &a, const Dec3Inline &inl, uint8_t *smem,
+                                                   uint32_t smem_s, uint32_t rank, int sp, int n_sp, int tid,
+                                                   int bar_id) {
+    using L = ShrinkSmem<RP, NW, MI>;
+    constexpr int NT = NW * 32;
     constexpr int JG = 8;   // A rows per pass (acc 8x8 + x 8x8 + A 8 granules in registers)
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int warp = tid >> 5, lane = tid & 31;
+    auto bar = [&]() { named_bar_sync(bar_id, NT); };
     const __nv_bfloat16 *X = reinterpret_cast<const __nv_bfloat16 *>(a.X);
     const int K = a.K, r = a.r, n_groups = a.n_groups, n_uniq = a.n_uniq, n_si = a.n_sitems;
     float *red = reinterpret_cast<float *>(smem + L::red);
     float *own = reinterpret_cast<float *>(smem + L::own);
     Dec3SItem *its = reinterpret_cast<Dec3SItem *>(smem + L::items);
-    const int n_mine = (a.flags & 8) ? 0 : (sp < n_si ? min((n_si - sp + n_sp - 1) / n_sp, kDec3MaxShrinkItems) : 0);
+    const int n_mine = (a.flags & 8) ? 0 : (sp < n_si ? min((n_si - sp + n_sp - 1) / n_sp, MI) : 0);
     {
         constexpr int W4 = sizeof(Dec3SItem) / 16;
         uint4 *dst = reinterpret_cast<uint4 *>(its);
-        for (int e = threadIdx.x; e < n_mine * W4; e += kT3) {
+        for (int e = tid; e < n_mine * W4; e += NT) {
             const int item = sp + (e / W4) * n_sp, w4 = e % W4;
             dst[e] = a.inl ? reinterpret_cast<const uint4 *>(&inl.items[item])[w4]
                            : __ldg(reinterpret_cast<const uint4 *>(a.sitems + item) + w4);
         }
     }
-    __syncthreads();
-    if (threadIdx.x == 0) dbg_stamp(a, 10);
+    bar();
+    if (tid == 0 && sp == 0) dbg_stamp(a, 10);
     const int ngr = K / 8;                                     // 128-bit granules of a row
-    const int gl = (int)rank * kT3 + threadIdx.x;              // this lane's first granule
+    const int gl = (int)rank * NT + tid;              // this lane's first granule
     for (int ii0 = 0; ii0 < n_mine; ++ii0) {
         const Dec3SItem &si = its[ii0];
         const __nv_bfloat16 *A = reinterpret_cast<const __nv_bfloat16 *>(si.A);
@@ -184,7 +190,7 @@ __device__ __forceinline__ void dec3_shrink_pair(const Dec3Args &a, const Dec3In
         // one granule per lane per 512-lane sweep of K; A rows in groups of 8, the next group's
         // loads in flight while the current group is multiplied (one HBM round trip for r <= 16)
 #pragma unroll 1
-        for (int sw = 0; sw < ngr; sw += 2 * kT3) {   // every lane takes part (shuffles), idle lanes load zeros
+        for (int sw = 0; sw < ngr; sw += 2 * NT) {   // every lane takes part (shuffles), idle lanes load zeros
             const int gr = sw + gl;
             const bool gok = gr < ngr;
             float xf[8][8];
@@ -239,46 +245,46 @@ __device__ __forceinline__ void dec3_shrink_pair(const Dec3Args &a, const Dec3In
                 }
             }
         }
-        if (threadIdx.x == 0 && ii0 == 0) dbg_stamp(a, 11);
-        __syncthreads();
+        if (tid == 0 && ii0 == 0) dbg_stamp(a, 11);
+        bar();
         // warps in fixed order -> this CTA's K half; CTA 1 pushes it into CTA 0's slot of this item
         const uint32_t rx_s = smem_s + L::rx + (uint32_t)ii0 * 8 * RP * 4;
         const uint32_t bar_s = smem_s + L::bars + (uint32_t)ii0 * 8;
         if (rank == 1) {
             const uint32_t rx_peer = map_to_rank(rx_s, 0);
-            for (int e = threadIdx.x; e < 8 * RP; e += kT3) {
+            for (int e = tid; e < 8 * RP; e += NT) {
                 const int ii = e / RP, jj = e % RP;
                 float t = 0.f;
                 if (jj < r)
-                    for (int w = 0; w < 8; ++w) t += red[(w * 8 + ii) * RP + jj];
+                    for (int w = 0; w < NW; ++w) t += red[(w * 8 + ii) * RP + jj];
                 st_cluster_f32(rx_peer + (uint32_t)e * 4u, t);
             }
             mbar_arrive_remote_release(map_to_rank(bar_s, 0));   // every thread: its stores are released
         } else {
-            for (int e = threadIdx.x; e < 8 * RP; e += kT3) {
+            for (int e = tid; e < 8 * RP; e += NT) {
                 const int ii = e / RP, jj = e % RP;
                 float t = 0.f;
                 if (jj < r)
-                    for (int w = 0; w < 8; ++w) t += red[(w * 8 + ii) * RP + jj];
+                    for (int w = 0; w < NW; ++w) t += red[(w * 8 + ii) * RP + jj];
                 own[e] = t;
             }
             mbar_wait_acq_cluster(bar_s, 0);
-            __syncthreads();
-            if (threadIdx.x == 0 && ii0 == 0) dbg_stamp(a, 13);
+            bar();
+            if (tid == 0 && ii0 == 0) dbg_stamp(a, 13);
             const Dec3Proj &P = a.proj[si.p];
             __nv_bfloat16 *sv = reinterpret_cast<__nv_bfloat16 *>(P.sv);
             __nv_bfloat16 *vsave = reinterpret_cast<__nv_bfloat16 *>(P.Vsave);
             const float *rx = reinterpret_cast<const float *>(smem + L::rx + (size_t)ii0 * 8 * RP * 4);
             if (si.zero_fill) {
                 // the adapter's slab rows of every other batch row (and past S) are zero
-                for (int e = threadIdx.x; e < n_groups * 256; e += kT3) {
+                for (int e = tid; e < n_groups * 256; e += NT) {
                     if ((si.mask[e >> 5] >> (e & 31)) & 1u) continue;
                     uint4 *z = reinterpret_cast<uint4 *>(sv + ((size_t)((e >> 8) * n_uniq + si.uidx) * 256 + (e & 255)) * RP);
 #pragma unroll
                     for (int q = 0; q < RP / 8; ++q) z[q] = make_uint4(0, 0, 0, 0);
                 }
             }
-            for (int e = threadIdx.x; e < 8 * RP; e += kT3) {
+            for (int e = tid; e < 8 * RP; e += NT) {
                 const int ii = e / RP, jj = e % RP;
                 if (ii >= n) continue;
                 const float v = own[e] + rx[e];   // K half 0 + K half 1 (fixed order)
@@ -289,16 +295,16 @@ __device__ __forceinline__ void dec3_shrink_pair(const Dec3Args &a, const Dec3In
                     vsave[(size_t)row * r + jj] = __float2bfloat16_rn(v);
             }
         }
-        if (threadIdx.x == 0 && ii0 == 0) dbg_stamp(a, 14);
-        __syncthreads();   // red / own reusable
+        if (tid == 0 && ii0 == 0) dbg_stamp(a, 14);
+        bar();   // red / own reusable
     }
     // publish (slabs are read by TMA in other CTAs: generic -> async proxy)
     const int done = (a.flags & 8) ? (sp < n_si ? (n_si - sp + n_sp - 1) / n_sp : 0) : n_mine;
     if (rank == 0 && done) {
         fence_proxy_async_global();
         __threadfence();
-        __syncthreads();
-        if (threadIdx.x == 0) atom_add_release_gpu(a.ctr, done);
+        bar();
+        if (tid == 0) atom_add_release_gpu(a.ctr, done);
     }
 }
 
@@ -370,8 +376,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT3, 1) smlm_dec3_ke
         if (mine) s_ulist[off + __popc(bal & ((1u << lane) - 1u))] = u;
         if (threadIdx.x == 0) s_ucount = tot;
     }
+    using SL = ShrinkSmem<RP, 4, kShrMI>;
     if (!wpair && rank == 0 && threadIdx.x == 0) {
-        for (int i = 0; i < kDec3MaxShrinkItems; ++i) mbar_init(base + ShrinkSmem<RP>::bars + 8u * i, kT3);
+        // per-item hand-off barriers of both workers (CTA 1's 128 worker threads arrive remotely)
+        for (int wk = 0; wk < 2; ++wk)
+            for (int i = 0; i < kShrMI; ++i) mbar_init(base + wk * SL::end + SL::bars + 8u * i, 128);
         fence_mbar_init();
     }
     if (wpair && warp == 2) {
@@ -389,7 +398,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT3, 1) smlm_dec3_ke
 
     if (!wpair) {
         // ========================= shrink pair =========================
-        dec3_shrink_pair<RP>(a, inl, base_ptr, base, rank, cid - a.n_wpairs, n_clusters - a.n_wpairs);
+        const int wk = warp >> 2;   // worker 0: warps 0-3, worker 1: warps 4-7
+        dec3_shrink_worker<RP, 4, kShrMI>(a, inl, base_ptr + wk * SL::end, base + wk * SL::end, rank,
+                                          2 * (cid - a.n_wpairs) + wk, 2 * (n_clusters - a.n_wpairs),
+                                          threadIdx.x & 127, 2 + wk);
         if (threadIdx.x == 0) dbg_stamp(a, 1);
     } else {
         const int ks = a.ks;
@@ -418,6 +430,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT3, 1) smlm_dec3_ke
             const int wrow = it.n0 + 128 * (int)rank;
             int kb0, kb1;
             kb_range(it.s, kb0, kb1);
+            // flag 256 (measurement): the W stream starts once the shrink has published, so the shrink's
+            // A_u / x reads do not queue behind ~20 MB of W requests in HBM
+            if ((a.flags & 256) && a.n_uniq > 0) {
+                if (lane == 0)
+                    while (ld_acquire_gpu(a.ctr) < a.n_sitems) __nanosleep(64);
+                __syncwarp();
+            }
             for (int kb = kb0; kb < kb1; ++kb) {
                 mbar_wait(empty_bar(stage), phase ^ 1);
                 if (lane == 0) {
@@ -645,6 +664,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT3, 1) smlm_dec3_ke
 }
 
 static_assert(sizeof(Dec3Args) + sizeof(Dec3Inline) <= 32764, "kernel parameters exceed 32 KB");
+static_assert(2 * ShrinkSmem<64, 4, kShrMI>::end <= 6 * kStage3, "shrink workers exceed the ring");
 
 template <int RP>
 int launch_dec3_impl(const Dec3Args &a, const Dec3Inline &in, int clusters, cudaStream_t st) {
