@@ -342,10 +342,9 @@ int make_map_cached(smlm_pool p, CUtensorMap *m, const void *ptr, uint64_t inner
 // ------------------------------------------------------------------------------------------
 struct Dec3Plan {
     bool ok = false;
-    std::vector<int> uslot, uoff, row_uidx;
-    std::vector<Dec3Row> urows;
-    std::vector<Dec3SItem> sitems;
-    int n_groups = 0, nw = 0, ks = 1, n_wpairs = 0, clusters = 0;
+    std::vector<int> uslot;
+    std::vector<Dec3RowInfo> rows;
+    int n_groups = 0, nw = 0, n_vt = 0, ks = 1, ks_v = 1, n_vpairs = 0, n_wpairs = 0, clusters = 0;
     size_t plan_off = 0, sv_off[kDec3MaxProj] = {}, kpart_off = 0, total = 0;
 };
 
@@ -354,79 +353,64 @@ struct Dec3Plan {
 Dec3Plan dec3_plan(int n_proj, const smlm_pool *pools, const smlm_batch *b, const Plan &plan) {
     Dec3Plan D;
     smlm_pool p0 = pools[0];
-    if (p0->dtype != SMLM_BF16 || !plan.long_tiles.empty() || plan.short_tiles.empty() || b->S > 512 ||
+    if (p0->dtype != SMLM_BF16 || !plan.long_tiles.empty() || plan.short_tiles.empty() || b->S > kDec3InlineRows ||
         getenv("SMLM_NO_DEC3"))
         return D;
-    // adapters of the batch (ascending), their rows (ascending), per-row adapter index
-    std::vector<std::vector<Dec3Row>> by_slot(p0->cap);
-    for (auto &bk : plan.blocks)
+    // adapters of the batch (ascending) and per-row records
+    D.rows.assign(b->S, Dec3RowInfo{-1, 0.f, 0, 0});
+    std::vector<int> row_slot(b->S, -1);
+    std::vector<uint8_t> present(p0->cap, 0);
+    for (auto &bk : plan.blocks) {
+        present[bk.slot] = 1;
         for (int i = 0; i < bk.nrows; ++i) {
             const DevShortRow &sr = plan.short_rows[bk.row_begin + i];
-            by_slot[bk.slot].push_back(Dec3Row{sr.row, sr.scale, sr.ft, 0});
+            row_slot[sr.row] = bk.slot;
+            D.rows[sr.row].scale = sr.scale;
+            D.rows[sr.row].ft = sr.ft;
         }
-    D.row_uidx.assign(b->S, -1);
-    D.uoff.push_back(0);
-    for (int sl = 0; sl < p0->cap; ++sl) {
-        if (by_slot[sl].empty()) continue;
-        std::sort(by_slot[sl].begin(), by_slot[sl].end(),
-                  [](const Dec3Row &x, const Dec3Row &y) { return x.row < y.row; });
-        const int u = (int)D.uslot.size();
-        D.uslot.push_back(sl);
-        for (auto &r : by_slot[sl]) D.row_uidx[r.row] = u;
-        D.urows.insert(D.urows.end(), by_slot[sl].begin(), by_slot[sl].end());
-        D.uoff.push_back((int)D.urows.size());
     }
-    const int n_uniq = (int)D.uslot.size();
-    for (int p = 0; p < n_proj; ++p)
-        for (int u = 0; u < n_uniq; ++u) {
-            uint32_t mask[16] = {0};
-            for (int i = D.uoff[u]; i < D.uoff[u + 1]; ++i) mask[D.urows[i].row >> 5] |= 1u << (D.urows[i].row & 31);
-            for (int rb = D.uoff[u]; rb < D.uoff[u + 1]; rb += 8) {
-                Dec3SItem it;
-                memset(&it, 0, sizeof(it));
-                it.A = pools[p]->slots[D.uslot[u]].A;
-                it.p = p;
-                it.uidx = u;
-                it.n = std::min(8, D.uoff[u + 1] - rb);
-                it.zero_fill = rb == D.uoff[u];
-                for (int i = 0; i < it.n; ++i) {
-                    it.rows[i] = D.urows[rb + i].row;
-                    it.scale[i] = D.urows[rb + i].scale;
-                    if (D.urows[rb + i].ft) it.ft_mask |= 1 << i;
-                }
-                memcpy(it.mask, mask, sizeof(mask));
-                D.sitems.push_back(it);
-            }
+    std::vector<int> uidx(p0->cap, -1);
+    for (int sl = 0; sl < p0->cap; ++sl)
+        if (present[sl]) {
+            uidx[sl] = (int)D.uslot.size();
+            D.uslot.push_back(sl);
         }
-    const int n_si = (int)D.sitems.size();
+    for (int r = 0; r < b->S; ++r)
+        if (row_slot[r] >= 0) D.rows[r].uidx = uidx[row_slot[r]];
+    const int n_uniq = (int)D.uslot.size();
+    if (n_uniq > kDec3InlineSlots) return D;
     D.n_groups = (b->S + 255) / 256;
     for (int i = 0; i < n_proj; ++i) D.nw += (pools[i]->out + 255) / 256;
+    D.n_vt = (n_uniq * p0->r_pad + 255) / 256;
     const int pairs = std::min(p0->num_sms / 2, kDec3MaxPairs);
-    const int NW = D.n_groups * D.nw;
+    const int NW = D.n_groups * D.nw, NV = D.n_groups * n_proj * D.n_vt;
     const int nkb = p0->in / kBK;
-    // the shrink pairs take the rest of the wave: at least ~a third of the items' worth
-    int sp_min = n_si ? std::max(1, std::min(pairs / 3, (n_si + 2) / 3)) : 0;
-    if (const char *e = getenv("SMLM_DEC_SP")) sp_min = n_si ? std::max(1, atoi(e)) : 0;   // measurement override
-    if (NW > pairs - sp_min) return D;   // more W tiles than one wave: not this kernel
-    int ks = (pairs - sp_min) / NW;
-    if (const char *e = getenv("SMLM_DEC_KSPLIT")) ks = atoi(e);   // measurement override
-    ks = std::max(1, std::min({ks, 8, std::max(1, nkb / 2)}));
-    while (ks > 1 && NW * ks > pairs - sp_min) --ks;
-    D.ks = ks;
-    D.n_wpairs = NW * ks;
-    D.clusters = n_si ? pairs : D.n_wpairs;
-    if (NW > 256) return D;   // tile arrival counters
-    if (n_uniq > kDec3InlineSlots) return D;   // per-split adapter list in shared memory
-    if (n_si && (n_si + 2 * (D.clusters - D.n_wpairs) - 1) / (2 * (D.clusters - D.n_wpairs)) > 32) return D;   // kShrMI
+    const int kmax = std::max(1, std::min(8, nkb / 2));
+    // split factors.  The W split depends only on the W tiles (so that B = 0 reproduces the
+    // base-only call bit for bit: same K ranges, same summation order), taking ~3/4 of the wave;
+    // the V tiles (shrink) get the rest, as many splits as fit (they must publish before the W
+    // tiles finish their main loop)
+    int best_ks = std::max(1, std::min(kmax, (pairs * 3 / 4) / std::max(NW, 1)));
+    if (const char *e = getenv("SMLM_DEC_KSPLIT")) best_ks = std::max(1, std::min(atoi(e), kmax));   // measurement
+    while (best_ks > 1 && NW * best_ks + NV > pairs) --best_ks;   // (only with very many adapters)
+    int best_ksv = NV ? std::max(1, std::min(kmax, (pairs - NW * best_ks) / NV)) : 1;
+    if (NW * best_ks + NV * best_ksv > pairs) best_ks = 0;
+    if (best_ks == 0) return D;   // more tiles than one wave: not this kernel
+    D.ks = best_ks;
+    D.ks_v = NV ? best_ksv : 1;
+    D.n_vpairs = NV * D.ks_v;
+    D.n_wpairs = NW * D.ks;
+    D.clusters = D.n_vpairs + D.n_wpairs;
+    if (NV + NW > 256) return D;   // tile arrival counters
     size_t off = 0;
     D.plan_off = off;
-    off = align256(off + (size_t)n_uniq * 4 + 64 + D.sitems.size() * sizeof(Dec3SItem));
+    off = align256(off + (size_t)n_uniq * 4 + 64 + D.rows.size() * sizeof(Dec3RowInfo));
     for (int i = 0; i < n_proj; ++i) {
         D.sv_off[i] = off;
         off = align256(off + (size_t)D.n_groups * std::max(n_uniq, 1) * 256 * p0->r_pad * 2);
     }
     D.kpart_off = off;
-    if (ks > 1) off = align256(off + (size_t)D.n_wpairs * 2 * 8 * kDec3ChunkBytes);
+    off = align256(off + (size_t)D.clusters * 2 * 8 * kDec3ChunkBytes);
     if (getenv("SMLM_DEC3_DEBUG")) off += 2 * kDec3MaxPairs * 16 * 8;   // phase timestamps at the tail
     D.total = off;
     D.ok = true;
@@ -537,21 +521,22 @@ int run_dec3(int n_proj, const smlm_pool *pools, const smlm_batch *b, const Dec3
              const void *const *W, void *const *Y, void *const *Vsave, uint8_t *wsb, cudaStream_t st) {
     smlm_pool p0 = pools[0];
     const int n_uniq = (int)D.uslot.size();
-    std::vector<uint8_t> bytes;
-    append(bytes, D.uslot);
-    while (bytes.size() % 16) bytes.push_back(0);
-    const size_t si_off = bytes.size();
-    append(bytes, D.sitems);
     int rc;
     double t0 = g_hprof.on ? now_us() : 0;
     static thread_local Dec3Inline inl;   // kernel parameter block (copied at launch)
     static const bool no_inline = getenv("SMLM_DEC3_NOINLINE") != nullptr;   // measurement override
-    const bool inline_plan = !no_inline && n_uniq <= kDec3InlineSlots && (int)D.sitems.size() <= kDec3InlineItems;
+    const bool inline_plan = !no_inline;   // sizes are bounded by dec3_plan (<= 256 adapters, <= 512 rows)
+    size_t rows_off = 0;
     if (inline_plan) {
         if (n_uniq) memcpy(inl.uslot, D.uslot.data(), n_uniq * sizeof(int));
-        if (!D.sitems.empty()) memcpy(inl.items, D.sitems.data(), D.sitems.size() * sizeof(Dec3SItem));
-    } else if ((rc = stage_upload(p0, bytes, wsb + D.plan_off, st))) {
-        return rc;
+        if (!D.rows.empty()) memcpy(inl.rows, D.rows.data(), D.rows.size() * sizeof(Dec3RowInfo));
+    } else {
+        std::vector<uint8_t> bytes;
+        append(bytes, D.uslot);
+        while (bytes.size() % 16) bytes.push_back(0);
+        rows_off = bytes.size();
+        append(bytes, D.rows);
+        if ((rc = stage_upload(p0, bytes, wsb + D.plan_off, st))) return rc;
     }
     double t1 = g_hprof.on ? now_us() : 0;
     Dec3Args a;
@@ -576,17 +561,18 @@ int run_dec3(int n_proj, const smlm_pool *pools, const smlm_batch *b, const Dec3
         P.n_wt = (pools[i]->out + 255) / 256;
         nt0 += P.n_wt;
     }
-    a.X = X;
     a.uslot = reinterpret_cast<const int *>(wsb + D.plan_off);
-    a.sitems = reinterpret_cast<const Dec3SItem *>(wsb + D.plan_off + si_off);
+    a.rows = reinterpret_cast<const Dec3RowInfo *>(wsb + D.plan_off + rows_off);
     a.kpart = reinterpret_cast<float *>(wsb + D.kpart_off);
     a.ctr = p0->d_ctr;
     a.n_proj = n_proj;
     a.n_uniq = n_uniq;
-    a.n_sitems = (int)D.sitems.size();
     a.n_groups = D.n_groups;
     a.n_wt = D.nw;
+    a.n_vt = D.n_vt;
     a.ks = D.ks;
+    a.ks_v = D.ks_v;
+    a.n_vpairs = D.n_vpairs;
     a.n_wpairs = D.n_wpairs;
     a.S = b->S;
     a.K = p0->in;

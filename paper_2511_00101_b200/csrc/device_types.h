@@ -142,8 +142,8 @@ struct alignas(64) Dec3Proj {
     CUtensorMap tmW;        // W_p [out_p, in] box {64,128} SW128 (B operand: 128 W rows per CTA)
     CUtensorMap tmY;        // Y_p [S, out_p] box {32,128} (TMA store of a 32-column chunk)
     CUtensorMap tmSV;       // s*V slabs [n_groups*n_uniq*256, r_pad] bf16 box {r_pad,128} (expand A operand)
-    const SlotDev *slots;   // pool p's slot table (A_u for the shrink, tmBk for the expand)
-    void *sv;               // slab base (generic pointer; written by the shrink CTAs)
+    const SlotDev *slots;   // pool p's slot table (tmA: stacked-A tiles; tmBk: expand)
+    void *sv;               // slab base (generic pointer; written by the V tiles' epilogues)
     void *Vsave;            // [S, r] bf16 or NULL (FINETUNE rows)
     int out;
     int nt0;                // first W tile of this projection (within a row group)
@@ -151,56 +151,44 @@ struct alignas(64) Dec3Proj {
     int pad[7];
 };
 
-struct alignas(16) Dec3Row {   // a row with an adapter (grouped by adapter, ascending row)
-    int row;
+struct alignas(16) Dec3RowInfo {   // per batch row
+    int uidx;               // index of its adapter among the batch's adapters, -1 = none
     float scale;            // effective s = slot_scale * seg_scale
     int ft;                 // FINETUNE row (V_save)
     int pad;
 };
-struct alignas(16) Dec3SItem {  // shrink work item: <= 8 rows of one adapter of one projection (self-contained)
-    const void *A;          // A_u [r, in] of projection p
-    int p;
-    int uidx;
-    int n;                  // rows (1..8)
-    int zero_fill;          // 1: also zero the slab rows of every other row (first item of the adapter)
-    int rows[8];
-    float scale[8];         // effective s of each row
-    int ft_mask;            // bit i: row i is a FINETUNE row (V_save)
-    int pad;
-    uint32_t mask[16];      // rows of this adapter (bit e of word e/32 = batch row e), for the zero fill
-};
-static_assert(sizeof(Dec3SItem) % 16 == 0, "Dec3SItem must be a multiple of 16 bytes");
 
 struct Dec3Args {
     CUtensorMap tmX;        // X [S, in] box {64,128} SW128 (A operand: 128 decode rows per CTA)
     Dec3Proj proj[kDec3MaxProj];
-    const void *X;          // X [S, in] bf16 (generic pointer for the SIMT shrink)
-    const int *uslot;       // [n_uniq] distinct adapter slots of the batch, ascending
-    const Dec3SItem *sitems;
-    float *kpart;           // split-K partials [W items][2 ranks][8 chunks][8 q][128 m] float4
+    const int *uslot;       // [n_uniq] distinct adapter slots of the batch, ascending (if !inl)
+    const Dec3RowInfo *rows;  // [S] (if !inl)
+    float *kpart;           // split-K partials [items][2 ranks][8 chunks][8 q][128 m] float4
     int *ctr;               // pool-owned self-resetting counters (kernels_dec3.cu)
     unsigned long long *dbg;  // optional per-CTA phase timestamps [grid][16] (SMLM_DEC3_DEBUG)
     int n_proj;
     int n_uniq;
-    int n_sitems;
     int n_groups;           // ceil(S / 256)
     int n_wt;               // W tiles per row group (all projections)
+    int n_vt;               // V tiles per (row group, projection): ceil(n_uniq * r_pad / 256)
     int ks;                 // split-K factor of the W tiles
-    int n_wpairs;           // CTA pairs on W items (= n_groups * n_wt * ks); the rest run the shrink
+    int ks_v;               // split-K factor of the V (stacked-A shrink) tiles
+    int n_vpairs;           // CTA pairs on V items (= n_groups * n_proj * n_vt * ks_v), first in the grid
+    int n_wpairs;           // CTA pairs on W items (= n_groups * n_wt * ks), after the V items
     int S;
     int K;                  // in
     int r;
     int r_pad;
     int stages;
     int flags;
-    int inl;                // 1: uslot / sitems are passed inline (Dec3Inline kernel parameter)
+    int inl;                // 1: uslot / rows are passed inline (Dec3Inline kernel parameter)
 };
 // small plans ride in the kernel parameters (no H2D copy in the stream)
-constexpr int kDec3InlineItems = 176;   // Dec3Args + Dec3Inline stay under the 32 KB parameter limit
 constexpr int kDec3InlineSlots = 256;
+constexpr int kDec3InlineRows = 512;
 struct Dec3Inline {
-    Dec3SItem items[kDec3InlineItems];
     int uslot[kDec3InlineSlots];
+    Dec3RowInfo rows[kDec3InlineRows];
 };
 constexpr int kDec3ChunkBytes = 128 * 32 * 4;   // one 32-column fp32 chunk of a CTA accumulator
 constexpr int dec3_counter_ints() { return 2 + 2 * 128 + 62; }

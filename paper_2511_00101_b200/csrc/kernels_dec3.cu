@@ -4,28 +4,26 @@
 // bottleneck has been hit".  A pure decode batch (<= 512 rows) is a skinny product: the cost is
 // streaming W and the batch's A_u / B_u from HBM once.  One launch per call; several projections
 // that share X (q/k/v, gate/up) ride in the same launch.  The grid is one wave of
-// CTA pairs (clusters of 2) with two roles:
+// CTA pairs (clusters of 2, tcgen05 cta_group::2: M = 256 decode rows, 128 per CTA; N = 256 rows of
+// the B operand, 128 staged per CTA; 6-stage TMA ring) working on two kinds of tiles:
 //
-//   * W pairs (tcgen05 cta_group::2): item = (row group of 256 decode rows, W tile of 256 output
-//     columns, K split).  M = 256 decode rows (128 per CTA), N = 256 W rows (128 staged per CTA):
-//     per SM 16 KB of X and 16 KB of W per 64-K block, 6-stage TMA ring.  After its base K range,
-//     split s folds in the expand of every adapter u with slot(u) % ksplit == s as one more
-//     K = r_pad block: A operand = the adapter's block-diagonal s*V slab (rows of other adapters
-//     are zero), B operand = B_u rows of the tile -- the LoRA term lands in the same fp32
-//     accumulator as the base product.  Split-K reduction in-kernel: each CTA stores the 32-column
-//     chunks it does not own (coalesced float4 rows, L2-resident), and once all 2*ksplit CTAs of
-//     the tile have arrived, sums its own chunks in split order (deterministic, independent of the
-//     row position) and stores bf16 Y with TMA.
-//   * Shrink pairs (the rest of the wave, all 8 warps, SIMT): V = A_u x for <= 8 rows of one
-//     adapter per item; the two CTAs of the pair take the two halves of K (128-bit granules of
-//     A_u and x per lane, lane partials, a 31-shuffle transpose-reduce, warps combined in fixed
-//     order, the peer half added through distributed shared memory), then write the adapter's
-//     block-diagonal bf16 slab (s*V rows, zeros elsewhere) and V_save.  W pairs wait for the slabs
-//     only before their expand blocks, i.e. after their own main loop.
+//   * V tiles (the shrink, first in the grid): B = the stacked A_u of 256/r_pad adapters of the
+//     batch (each by its own TMA descriptor, issued lane-parallel) -> X A_u^T for every (row,
+//     adapter) pair; split K (ks_v).  After the split-K reduction the owner of each 32-column
+//     chunk writes the block-diagonal bf16 slab of its adapters (s*V for the rows of the adapter,
+//     zero for every other row) and V_save, then publishes on a counter.
+//   * W tiles: B = 256 rows of W_p -> the base product; split K (ks).  After its base K range,
+//     split s folds in the expand of every adapter u with slot(u) % ks == s as one more
+//     K = r_pad block (A operand: the adapter's slab rows of this CTA; B operand: B_u rows of the
+//     tile), after waiting for the slabs -- the LoRA term lands in the base accumulator.
+//   * Split-K reduction in-kernel (both kinds): each CTA stores the 32-column chunks it does not
+//     own as coalesced float4 rows (L2-resident), counts itself in on the tile's counter, bulk-loads
+//     the peers' partials of its own chunks into the idle ring and sums them in split order
+//     (deterministic, independent of the row position); W tiles store bf16 Y with TMA.
 //
 // Counters (pool-owned int[dec3_counter_ints()], zero at pool creation, self-resetting):
-//   [0] shrink items published, [1] CTAs departed (the last one resets everything),
-//   [2 + tile] split arrivals of a W tile.
+//   [0] V-tile CTAs that published their slabs, [1] CTAs departed (the last one resets
+//   everything), [2 + tile] split arrivals of a tile (V tiles first, then W tiles).
 // All CTAs of a launch are co-resident (grid <= one wave of pairs) -- required by the spin-waits.
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -97,227 +95,51 @@ __device__ __forceinline__ void bf16x8_to_f32(const uint4 &u, float *f) {
 }
 
 struct Item3 {
-    int g, s, p, tile, n0;
+    bool vtile;
+    int g, s, p, ks, tile, item0;
+    int n0;   // W tile: first output column; V tile: first adapter index (uidx)
 };
-// W item w -> (tile = w / ks, split = w % ks); tile -> (row group, projection, n-tile)
+// pair w -> item: V items (row group, projection, V tile, split) first, then W items (row group,
+// W tile, split); the splits of a tile are consecutive pairs (item0 = the tile's first)
 __device__ __forceinline__ Item3 dec3_item(const Dec3Args &a, int w) {
     Item3 it;
-    it.s = w % a.ks;
-    it.tile = w / a.ks;
-    it.g = it.tile / a.n_wt;
-    const int t = it.tile % a.n_wt;
-    it.p = 0;
-    for (int p = 1; p < a.n_proj; ++p)
-        if (t >= a.proj[p].nt0) it.p = p;
-    it.n0 = (t - a.proj[it.p].nt0) * 256;
+    if (w < a.n_vpairs) {
+        it.vtile = true;
+        it.ks = a.ks_v;
+        it.s = w % a.ks_v;
+        it.tile = w / a.ks_v;                      // V tile id
+        const int vt = it.tile % a.n_vt, gp = it.tile / a.n_vt;
+        it.p = gp % a.n_proj;
+        it.g = gp / a.n_proj;
+        it.n0 = vt * (256 / a.r_pad);
+    } else {
+        it.vtile = false;
+        it.ks = a.ks;
+        const int w2 = w - a.n_vpairs;
+        it.s = w2 % a.ks;
+        const int tw = w2 / a.ks;
+        it.tile = a.n_vpairs / a.ks_v + tw;      // tile ids: V tiles, then W tiles
+        it.g = tw / a.n_wt;
+        const int t = tw % a.n_wt;
+        it.p = 0;
+        for (int p = 1; p < a.n_proj; ++p)
+            if (t >= a.proj[p].nt0) it.p = p;
+        it.n0 = (t - a.proj[it.p].nt0) * 256;
+    }
+    it.item0 = w - it.s;
     return it;
-}
-
-// ------------------------------------------------------------------------------------------
-// shrink pair: items (projection, adapter, <= 8 rows); CTA `rank` takes every other 128-bit granule
-// of K.  The pair's items are staged in shared memory first (no dependent global loads later).
-// ------------------------------------------------------------------------------------------
-// shared-memory layout of a shrink CTA (inside the pipeline ring, which shrink pairs do not use)
-template <int RP, int NW, int MI>
-struct ShrinkSmem {
-    static constexpr uint32_t red = 0;                                  // [NW warps][8 rows][RP] fp32
-    static constexpr uint32_t own = red + NW * 8 * RP * 4;             // [8 rows][RP] this CTA's K half
-    static constexpr uint32_t items = own + 8 * RP * 4;                // [MI] Dec3SItem
-    static constexpr uint32_t rx = items + MI * sizeof(Dec3SItem);     // [MI][8][RP] peer halves
-    static constexpr uint32_t bars = rx + MI * 8 * RP * 4;             // [MI] mbarriers
-    static constexpr uint32_t end = (bars + MI * 8 + 1023u) & ~1023u;
-};
-// a shrink CTA runs two independent 4-warp workers (warps 0-3, 4-7) so that one worker's loads
-// overlap the other's FMAs; each worker stages at most kShrMI items
-constexpr int kShrMI = 32;
-
-__device__ __forceinline__ void mbar_arrive_remote_release(uint32_t cluster_addr) {
-    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
-}
-__device__ __forceinline__ void mbar_wait_acq_cluster(uint32_t bar, uint32_t parity) {
-    uint32_t done;
-    do {
-        asm volatile(
-            "{\n\t.reg .pred p;\n\t"
-            "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
-            "selp.u32 %0, 1, 0, p;\n\t}"
-            : "=r"(done)
-            : "r"(bar), "r"(parity)
-            : "memory");
-    } while (!done);
-}
-
-// ------------------------------------------------------------------------------------------
-// shrink pair: items (projection, adapter, <= 8 rows); CTA `rank` takes every other 128-bit
-// granule of K.  Items are staged in shared memory first; CTA 1 pushes its K half of every item
-// into CTA 0's shared memory (one slot and one mbarrier per item, no cluster-wide barrier).
-// ------------------------------------------------------------------------------------------
-template <int RP, int NW, int MI>
-__device__ __forceinline__ void dec3_shrink_worker(const Dec3Args &a, const Dec3Inline &inl, uint8_t *smem,
-                                                   uint32_t smem_s, uint32_t rank, int sp, int n_sp, int tid,
-                                                   int bar_id) {
-    using L = ShrinkSmem<RP, NW, MI>;
-    constexpr int NT = NW * 32;
-    constexpr int JG = 8;   // A rows per pass (acc 8x8 + x 8x8 + A 8 granules in registers)
-    const int warp = tid >> 5, lane = tid & 31;
-    auto bar = [&]() { named_bar_sync(bar_id, NT); };
-    const __nv_bfloat16 *X = reinterpret_cast<const __nv_bfloat16 *>(a.X);
-    const int K = a.K, r = a.r, n_groups = a.n_groups, n_uniq = a.n_uniq, n_si = a.n_sitems;
-    float *red = reinterpret_cast<float *>(smem + L::red);
-    float *own = reinterpret_cast<float *>(smem + L::own);
-    Dec3SItem *its = reinterpret_cast<Dec3SItem *>(smem + L::items);
-    const int n_mine = (a.flags & 8) ? 0 : (sp < n_si ? min((n_si - sp + n_sp - 1) / n_sp, MI) : 0);
-    {
-        constexpr int W4 = sizeof(Dec3SItem) / 16;
-        uint4 *dst = reinterpret_cast<uint4 *>(its);
-        for (int e = tid; e < n_mine * W4; e += NT) {
-            const int item = sp + (e / W4) * n_sp, w4 = e % W4;
-            dst[e] = a.inl ? reinterpret_cast<const uint4 *>(&inl.items[item])[w4]
-                           : __ldg(reinterpret_cast<const uint4 *>(a.sitems + item) + w4);
-        }
-    }
-    bar();
-    if (tid == 0 && sp == 0) dbg_stamp(a, 10);
-    const int ngr = K / 8;                                     // 128-bit granules of a row
-    const int gl = (int)rank * NT + tid;              // this lane's first granule
-    for (int ii0 = 0; ii0 < n_mine; ++ii0) {
-        const Dec3SItem &si = its[ii0];
-        const __nv_bfloat16 *A = reinterpret_cast<const __nv_bfloat16 *>(si.A);
-        const int n = si.n;
-        int rows[8];
-#pragma unroll
-        for (int i = 0; i < 8; ++i) rows[i] = si.rows[i];
-        // one granule per lane per 512-lane sweep of K; A rows in groups of 8, the next group's
-        // loads in flight while the current group is multiplied (one HBM round trip for r <= 16)
-#pragma unroll 1
-        for (int sw = 0; sw < ngr; sw += 2 * NT) {   // every lane takes part (shuffles), idle lanes load zeros
-            const int gr = sw + gl;
-            const bool gok = gr < ngr;
-            float xf[8][8];
-            {
-                uint4 xa[8];
-#pragma unroll
-                for (int i = 0; i < 8; ++i)
-                    xa[i] = (i < n && gok) ? __ldg(reinterpret_cast<const uint4 *>(X + (size_t)rows[i] * K) + gr)
-                                           : make_uint4(0, 0, 0, 0);
-#pragma unroll
-                for (int i = 0; i < 8; ++i) bf16x8_to_f32(xa[i], xf[i]);
-            }
-            auto load_group = [&](int j0, uint4 (&aa)[JG]) {
-#pragma unroll
-                for (int j = 0; j < JG; ++j)
-                    aa[j] = (j0 + j < r && gok) ? __ldg(reinterpret_cast<const uint4 *>(A + (size_t)(j0 + j) * K) + gr)
-                                                : make_uint4(0, 0, 0, 0);
-            };
-            uint4 aa[JG], an[JG];
-            load_group(0, aa);
-            if (JG < r) load_group(JG, an);
-#pragma unroll 1
-            for (int j0 = 0; j0 < RP && j0 < r; j0 += JG) {
-                float acc[8][JG];
-#pragma unroll
-                for (int i = 0; i < 8; ++i)
-#pragma unroll
-                    for (int j = 0; j < JG; ++j) acc[i][j] = 0.f;
-#pragma unroll
-                for (int j = 0; j < JG; ++j) {
-                    float af[8];
-                    bf16x8_to_f32(aa[j], af);
-#pragma unroll
-                    for (int i = 0; i < 8; ++i)
-#pragma unroll
-                        for (int e = 0; e < 8; ++e) acc[i][j] = fmaf(af[e], xf[i][e], acc[i][j]);
-                }
-#pragma unroll
-                for (int j = 0; j < JG; ++j) aa[j] = an[j];
-                if (j0 + 2 * JG < r) load_group(j0 + 2 * JG, an);
-                // lanes -> one value each (transpose-reduce); the sweep's partials accumulate in red
-#pragma unroll
-                for (int h = 0; h < JG / 4; ++h) {
-                    float v[32];
-#pragma unroll
-                    for (int jj = 0; jj < 4; ++jj)
-#pragma unroll
-                        for (int i = 0; i < 8; ++i) v[jj * 8 + i] = acc[i][4 * h + jj];
-                    const float s = warp_transpose_reduce32(v, lane);
-                    float *dst = &red[(warp * 8 + (lane & 7)) * RP + j0 + 4 * h + (lane >> 3)];
-                    *dst = sw == 0 ? s : *dst + s;
-                }
-            }
-        }
-        if (tid == 0 && ii0 == 0) dbg_stamp(a, 11);
-        bar();
-        // warps in fixed order -> this CTA's K half; CTA 1 pushes it into CTA 0's slot of this item
-        const uint32_t rx_s = smem_s + L::rx + (uint32_t)ii0 * 8 * RP * 4;
-        const uint32_t bar_s = smem_s + L::bars + (uint32_t)ii0 * 8;
-        if (rank == 1) {
-            const uint32_t rx_peer = map_to_rank(rx_s, 0);
-            for (int e = tid; e < 8 * RP; e += NT) {
-                const int ii = e / RP, jj = e % RP;
-                float t = 0.f;
-                if (jj < r)
-                    for (int w = 0; w < NW; ++w) t += red[(w * 8 + ii) * RP + jj];
-                st_cluster_f32(rx_peer + (uint32_t)e * 4u, t);
-            }
-            mbar_arrive_remote_release(map_to_rank(bar_s, 0));   // every thread: its stores are released
-        } else {
-            for (int e = tid; e < 8 * RP; e += NT) {
-                const int ii = e / RP, jj = e % RP;
-                float t = 0.f;
-                if (jj < r)
-                    for (int w = 0; w < NW; ++w) t += red[(w * 8 + ii) * RP + jj];
-                own[e] = t;
-            }
-            mbar_wait_acq_cluster(bar_s, 0);
-            bar();
-            if (tid == 0 && ii0 == 0) dbg_stamp(a, 13);
-            const Dec3Proj &P = a.proj[si.p];
-            __nv_bfloat16 *sv = reinterpret_cast<__nv_bfloat16 *>(P.sv);
-            __nv_bfloat16 *vsave = reinterpret_cast<__nv_bfloat16 *>(P.Vsave);
-            const float *rx = reinterpret_cast<const float *>(smem + L::rx + (size_t)ii0 * 8 * RP * 4);
-            if (si.zero_fill) {
-                // the adapter's slab rows of every other batch row (and past S) are zero
-                for (int e = tid; e < n_groups * 256; e += NT) {
-                    if ((si.mask[e >> 5] >> (e & 31)) & 1u) continue;
-                    uint4 *z = reinterpret_cast<uint4 *>(sv + ((size_t)((e >> 8) * n_uniq + si.uidx) * 256 + (e & 255)) * RP);
-#pragma unroll
-                    for (int q = 0; q < RP / 8; ++q) z[q] = make_uint4(0, 0, 0, 0);
-                }
-            }
-            for (int e = tid; e < 8 * RP; e += NT) {
-                const int ii = e / RP, jj = e % RP;
-                if (ii >= n) continue;
-                const float v = own[e] + rx[e];   // K half 0 + K half 1 (fixed order)
-                const int row = si.rows[ii];
-                sv[((size_t)((row >> 8) * n_uniq + si.uidx) * 256 + (row & 255)) * RP + jj] =
-                    __float2bfloat16_rn(si.scale[ii] * v);
-                if (((si.ft_mask >> ii) & 1) && vsave && jj < r)
-                    vsave[(size_t)row * r + jj] = __float2bfloat16_rn(v);
-            }
-        }
-        if (tid == 0 && ii0 == 0) dbg_stamp(a, 14);
-        bar();   // red / own reusable
-    }
-    // publish (slabs are read by TMA in other CTAs: generic -> async proxy)
-    const int done = (a.flags & 8) ? (sp < n_si ? (n_si - sp + n_sp - 1) / n_sp : 0) : n_mine;
-    if (rank == 0 && done) {
-        fence_proxy_async_global();
-        __threadfence();
-        bar();
-        if (tid == 0) atom_add_release_gpu(a.ctr, done);
-    }
 }
 
 template <int RP>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT3, 1) smlm_dec3_kernel(const __grid_constant__ Dec3Args a,
                                                                                         const __grid_constant__ Dec3Inline inl) {
-
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw = smem_u32(smem_raw);
     const uint32_t base = (raw + 1023u) & ~1023u;
     uint8_t *base_ptr = smem_raw + (base - raw);
     constexpr uint32_t RB = RP * 2;
     constexpr uint32_t kSwR = RB >= 128 ? kSw128 : (RB == 64 ? kSw64 : kSw32);
+    constexpr int APC = 128 / RP;   // stacked adapters per CTA of a V tile
     const int ST = a.stages;
     const uint32_t ystage = base + ST * kStage3;   // 2 x 8 KB bf16 Y staging (TMA store)
     const uint32_t bar = ystage + 2 * kYStage;
@@ -333,9 +155,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT3, 1) smlm_dec3_ke
     const uint32_t rank = cluster_rank();
     const bool leader = rank == 0;
     const int cid = blockIdx.x >> 1;
-    const int n_clusters = gridDim.x >> 1;
-    const bool wpair = cid < a.n_wpairs;
-    if (wpair && threadIdx.x == 0) {
+    const bool active = cid < a.n_vpairs + a.n_wpairs;
+    const Item3 it = dec3_item(a, active ? cid : 0);
+    const Dec3Proj &P = a.proj[it.p];
+    if (active && threadIdx.x == 0) {
         for (int s = 0; s < ST; ++s) {
             mbar_init(full_bar(s), 1);
             mbar_init(empty_bar(s), 1);
@@ -344,25 +167,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT3, 1) smlm_dec3_ke
         mbar_init(xbar, 1);
         fence_mbar_init();
         tma_prefetch_desc(&a.tmX);
-        for (int p = 0; p < a.n_proj; ++p) {
-            tma_prefetch_desc(&a.proj[p].tmW);
-            tma_prefetch_desc(&a.proj[p].tmY);
-            if (a.n_uniq) tma_prefetch_desc(&a.proj[p].tmSV);
-        }
+        tma_prefetch_desc(&P.tmW);
+        tma_prefetch_desc(&P.tmY);
+        if (a.n_uniq) tma_prefetch_desc(&P.tmSV);
     }
-    // this split's expand adapters (uslot index), in ascending order, staged once in shared memory:
-    // the producer / MMA loops then never touch parameter or global memory per adapter
+    // the batch's adapter slots and (W tiles) this split's expand adapters, staged once in shared
+    // memory in parallel (parameter / global reads in serial loops cost ~0.1 us each)
     __shared__ int s_ulist[kDec3InlineSlots];
     __shared__ int s_uslot[kDec3InlineSlots];
     __shared__ int s_wcnt[kT3 / 32];
     __shared__ int s_ucount;
-    if (wpair) {
-        // parallel: every thread one adapter (param / global reads in a serial loop cost ~0.1 us each)
-        const int nu = a.n_uniq, ksp = a.ks, s0 = cid % ksp;
-        const bool expand = !(a.flags & 4);
+    if (active) {
+        const int nu = a.n_uniq, ksp = it.ks, s0 = it.s;
+        const bool expand = !(a.flags & 4) && !it.vtile;
         const int u = threadIdx.x;
         int sl = -1;
-        if (u < nu && u < kDec3InlineSlots) sl = (a.flags & 64) ? u : (a.inl ? inl.uslot[u] : a.uslot[u]);
+        if (u < nu && u < kDec3InlineSlots) sl = a.inl ? inl.uslot[u] : a.uslot[u];
         if (u < kDec3InlineSlots) s_uslot[u] = sl;
         const bool mine = sl >= 0 && expand && sl % ksp == s0;
         const uint32_t bal = __ballot_sync(0xffffffffu, mine);
@@ -376,14 +196,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT3, 1) smlm_dec3_ke
         if (mine) s_ulist[off + __popc(bal & ((1u << lane) - 1u))] = u;
         if (threadIdx.x == 0) s_ucount = tot;
     }
-    using SL = ShrinkSmem<RP, 4, kShrMI>;
-    if (!wpair && rank == 0 && threadIdx.x == 0) {
-        // per-item hand-off barriers of both workers (CTA 1's 128 worker threads arrive remotely)
-        for (int wk = 0; wk < 2; ++wk)
-            for (int i = 0; i < kShrMI; ++i) mbar_init(base + wk * SL::end + SL::bars + 8u * i, 128);
-        fence_mbar_init();
-    }
-    if (wpair && warp == 2) {
+    if (active && warp == 2) {
         asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(tmem_slot), "r"(256)
                      : "memory");
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
@@ -391,234 +204,259 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT3, 1) smlm_dec3_ke
     tc_fence_before();
     cluster_sync();
     tc_fence_after();
-    const uint32_t tmem_base = wpair ? *reinterpret_cast<volatile uint32_t *>(base_ptr + (tmem_slot - base)) : 0u;
+    const uint32_t tmem_base = active ? *reinterpret_cast<volatile uint32_t *>(base_ptr + (tmem_slot - base)) : 0u;
     pdl_wait();
     pdl_trigger();
     if (threadIdx.x == 0) dbg_stamp(a, 0);
 
-    if (!wpair) {
-        // ========================= shrink pair =========================
-        const int wk = warp >> 2;   // worker 0: warps 0-3, worker 1: warps 4-7
-        dec3_shrink_worker<RP, 4, kShrMI>(a, inl, base_ptr + wk * SL::end, base + wk * SL::end, rank,
-                                          2 * (cid - a.n_wpairs) + wk, 2 * (n_clusters - a.n_wpairs),
-                                          threadIdx.x & 127, 2 + wk);
-        if (threadIdx.x == 0) dbg_stamp(a, 1);
-    } else {
-        const int ks = a.ks;
-        const int nkb = a.K / kBK;
-        // split s owns k-blocks kb_of(i), i in [0, cnt): a contiguous range, or (flag 16, measurement)
-        // interleaved s, s + ks, ... so the splits of a tile read neighbouring 128-byte pieces of W rows
-        const bool kil = (a.flags & 16) != 0;
-        auto kb_range = [&](int s, int &kb0, int &kb1) {
-            if (kil) {
-                kb0 = 0;
-                kb1 = (nkb - s + ks - 1) / ks;
-                return;
+    const int ks = it.ks;
+    const int nkb = a.K / kBK;
+    auto kb_range = [&](int s, int &kb0, int &kb1) {
+        const int q = nkb / ks, rm = nkb % ks;
+        kb0 = s * q + min(s, rm);
+        kb1 = kb0 + q + (s < rm ? 1 : 0);
+    };
+    const int v_target = 2 * a.n_vpairs;   // V-tile CTAs that publish their slabs
+
+    if (!active) {
+        // idle pair (the wave is larger than the work)
+    } else if (warp == 0) {
+        // ========================= TMA producer (both CTAs) =========================
+        int stage = 0;
+        uint32_t phase = 0;
+        const int xrow = it.g * 256 + 128 * (int)rank;
+        const int wrow = it.n0 + 128 * (int)rank;
+        int kb0, kb1;
+        kb_range(it.s, kb0, kb1);
+        // V tile: this CTA stacks adapters [u0, u0 + nad) of the batch; the peer holds the next APC
+        const int u0 = it.n0 + APC * (int)rank;
+        const int nad = it.vtile ? max(0, min(APC, a.n_uniq - u0)) : 0;
+        const int nad1 = it.vtile ? max(0, min(APC, a.n_uniq - (it.n0 + APC))) : 0;
+        const uint32_t bytes_pair = it.vtile ? 2u * kA3 + (uint32_t)(max(0, min(APC, a.n_uniq - it.n0)) + nad1) * RP * 128u
+                                             : 2u * kStage3;
+        if (it.vtile && lane < nad) tma_prefetch_desc(&P.slots[s_uslot[u0 + lane]].tmA);
+        for (int kb = kb0; kb < kb1; ++kb) {
+            mbar_wait(empty_bar(stage), phase ^ 1);
+            const uint32_t fb = map_to_rank(full_bar(stage), 0);
+            if (lane == 0 && leader) mbar_expect_tx(full_bar(stage), bytes_pair);
+            __syncwarp();
+            // one TMA per lane: lane 31 the X rows, lanes 0.. the B operand (W rows, or the stacked
+            // A_u of a V tile -- several boxes, issued in parallel)
+            if (lane == 31) tma_load_2d_pair(a_addr(stage), &a.tmX, fb, kb * kBK, xrow);
+            if (!it.vtile) {
+                if (lane == 0) tma_load_2d_pair(b_addr(stage), &P.tmW, fb, kb * kBK, wrow);
+            } else if (lane < nad) {
+                tma_load_2d_pair(b_addr(stage) + (uint32_t)lane * RP * 128u, &P.slots[s_uslot[u0 + lane]].tmA, fb,
+                                 kb * kBK, 0);
             }
-            const int q = nkb / ks, rm = nkb % ks;
-            kb0 = s * q + min(s, rm);
-            kb1 = kb0 + q + (s < rm ? 1 : 0);
-        };
-        auto kb_of = [&](int s, int i) { return kil ? s + i * ks : i; };
-        const Item3 it = dec3_item(a, cid);   // one W item per pair
-        const Dec3Proj &P = a.proj[it.p];
-        if (warp == 0) {
-            // ========================= TMA producer (both CTAs) =========================
-            int stage = 0;
-            uint32_t phase = 0;
-            const int xrow = it.g * 256 + 128 * (int)rank;
-            const int wrow = it.n0 + 128 * (int)rank;
-            int kb0, kb1;
-            kb_range(it.s, kb0, kb1);
-            // flag 256 (measurement): the W stream starts once the shrink has published, so the shrink's
-            // A_u / x reads do not queue behind ~20 MB of W requests in HBM
-            if ((a.flags & 256) && a.n_uniq > 0) {
-                if (lane == 0)
-                    while (ld_acquire_gpu(a.ctr) < a.n_sitems) __nanosleep(64);
-                __syncwarp();
+            __syncwarp();
+            if (++stage == ST) { stage = 0; phase ^= 1; }
+        }
+        if (lane == 0) dbg_stamp(a, 1);
+        if (!it.vtile && s_ucount > 0) {
+            // the s*V slabs are published by the V tiles
+            if (lane == 0) {
+                while (ld_acquire_gpu(a.ctr) < v_target) __nanosleep(64);
+                fence_proxy_async_global();
+                dbg_stamp(a, 2);
             }
-            for (int kb = kb0; kb < kb1; ++kb) {
+            __syncwarp();
+            for (int iu = 0; iu < s_ucount; ++iu) {
+                const int u = s_ulist[iu];
+                const int sl = s_uslot[u];
                 mbar_wait(empty_bar(stage), phase ^ 1);
                 if (lane == 0) {
                     const uint32_t fb = map_to_rank(full_bar(stage), 0);
-                    if (leader) mbar_expect_tx(full_bar(stage), 2u * kStage3);
-                    const int kc = kb_of(it.s, kb) * kBK;
-                    tma_load_2d_pair(a_addr(stage), &a.tmX, fb, kc, xrow);
-                    tma_load_2d_pair(b_addr(stage), &P.tmW, fb, kc, wrow);
+                    if (leader) mbar_expect_tx(full_bar(stage), 2u * 256u * RB);
+                    tma_load_2d_pair(a_addr(stage), &P.tmSV, fb, 0, (it.g * a.n_uniq + u) * 256 + 128 * (int)rank);
+                    const SlotDev *sd = P.slots + sl;
+                    tma_load_2d_pair(b_addr(stage), &sd->tmBk, fb, 0, wrow);
+                    tma_load_2d_pair(b_addr(stage) + 64u * RB, &sd->tmBk, fb, 0, wrow + 64);
                 }
                 __syncwarp();
                 if (++stage == ST) { stage = 0; phase ^= 1; }
             }
-            if (lane == 0) dbg_stamp(a, 1);
-            if (a.n_uniq > 0) {
-                // the s*V slabs are published by the shrink pairs
-                if (lane == 0) {
-                    while (ld_acquire_gpu(a.ctr) < a.n_sitems) __nanosleep(64);
-                    fence_proxy_async_global();
-                    dbg_stamp(a, 2);
-                }
-                __syncwarp();
-                for (int iu = 0; iu < s_ucount; ++iu) {
-                    const int u = s_ulist[iu];
-                    const int sl = s_uslot[u];
-                    mbar_wait(empty_bar(stage), phase ^ 1);
-                    if (lane == 0) {
-                        const uint32_t fb = map_to_rank(full_bar(stage), 0);
-                        if (leader) mbar_expect_tx(full_bar(stage), (a.flags & 2) ? 256u * RB : 2u * 256u * RB);
-                        tma_load_2d_pair(a_addr(stage), &P.tmSV, fb, 0, (it.g * a.n_uniq + u) * 256 + 128 * (int)rank);
-                        const SlotDev *sd = P.slots + sl;
-                        if (!(a.flags & 2)) {
-                            tma_load_2d_pair(b_addr(stage), &sd->tmBk, fb, 0, wrow);
-                            tma_load_2d_pair(b_addr(stage) + 64u * RB, &sd->tmBk, fb, 0, wrow + 64);
-                        }
-                    }
-                    __syncwarp();
-                    if (++stage == ST) { stage = 0; phase ^= 1; }
-                }
-                if (lane == 0) dbg_stamp(a, 8);
-            }
-        } else if (warp == 1 && leader) {
-            // ========================= MMA issuer (leader CTA) =========================
-            int stage = 0;
-            uint32_t phase = 0;
-            constexpr uint32_t idesc = idesc_bf16(256, 256, 0, 0);
-            int kb0, kb1;
-            kb_range(it.s, kb0, kb1);
-            for (int kb = kb0; kb < kb1; ++kb) {
-                mbar_wait(full_bar(stage), phase);
-                tc_fence_after();
-                if (lane == 0 && ((kb - kb0) & 3) == 0 && (kb - kb0) < 24) dbg_stamp(a, 10 + (kb - kb0) / 4);
-                if (lane == 0) {
-                    const uint32_t ab = a_addr(stage), bb = b_addr(stage);
-                    if (!(a.flags & 32) || kb == kb0) {
-#pragma unroll
-                        for (int k = 0; k < kBK / 16; ++k)
-                            mma2_bf16(tmem_base, smem_desc(ab + 32u * k, 16, 1024, kSw128),
-                                      smem_desc(bb + 32u * k, 16, 1024, kSw128), idesc, (kb > kb0 || k > 0) ? 1u : 0u);
-                    }
-                    mma2_commit_mc(empty_bar(stage));
-                }
-                __syncwarp();
-                if (++stage == ST) { stage = 0; phase ^= 1; }
-            }
-            for (int iu = 0; iu < s_ucount; ++iu) {
-                mbar_wait(full_bar(stage), phase);
-                tc_fence_after();
-                if (lane == 0) {
-                    const uint32_t ab = a_addr(stage), bb = b_addr(stage);
-#pragma unroll
-                    for (int kk = 0; kk < RP / 16; ++kk)
-                        mma2_bf16(tmem_base, smem_desc(ab + 32u * kk, 16, 8u * RB, kSwR),
-                                  smem_desc(bb + 32u * kk, 16, 8u * RB, kSwR), idesc, 1u);
-                    mma2_commit_mc(empty_bar(stage));
-                }
-                __syncwarp();
-                if (++stage == ST) { stage = 0; phase ^= 1; }
-            }
+            if (lane == 0) dbg_stamp(a, 8);
+        }
+    } else if (warp == 1 && leader) {
+        // ========================= MMA issuer (leader CTA) =========================
+        int stage = 0;
+        uint32_t phase = 0;
+        constexpr uint32_t idesc = idesc_bf16(256, 256, 0, 0);
+        int kb0, kb1;
+        kb_range(it.s, kb0, kb1);
+        for (int kb = kb0; kb < kb1; ++kb) {
+            mbar_wait(full_bar(stage), phase);
+            tc_fence_after();
+            if (lane == 0 && ((kb - kb0) & 3) == 0 && (kb - kb0) < 24) dbg_stamp(a, 10 + (kb - kb0) / 4);
             if (lane == 0) {
-                dbg_stamp(a, 9);
-                mma2_commit_mc(acc_full);
+                const uint32_t ab = a_addr(stage), bb = b_addr(stage);
+#pragma unroll
+                for (int k = 0; k < kBK / 16; ++k)
+                    mma2_bf16(tmem_base, smem_desc(ab + 32u * k, 16, 1024, kSw128),
+                              smem_desc(bb + 32u * k, 16, 1024, kSw128), idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+                mma2_commit_mc(empty_bar(stage));
             }
             __syncwarp();
-        } else if (warp == 3 && a.n_uniq > 0) {
-            // expand operands of this split: descriptors and B_u rows of the tile -> caches / L2
-            for (int iu = lane; iu < s_ucount; iu += 32) {
-                const int sl = s_uslot[s_ulist[iu]];
-                const SlotDev *sd = P.slots + sl;
-                tma_prefetch_desc(&sd->tmBk);
-                const int wrow = it.n0 + 128 * (int)rank;
-                if (wrow < P.out) {
-                    const char *bp = reinterpret_cast<const char *>(sd->B) + (size_t)wrow * a.r * 2;
-                    const uint32_t bytes = (uint32_t)(min(128, P.out - wrow) * a.r * 2);
-                    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(bp), "r"(bytes) : "memory");
-                }
-            }
-        } else if (warp >= 4) {
-            // ========================= epilogue warps (both CTAs) =========================
-            const int ew = warp - 4;
-            const int tid_e = threadIdx.x - 128;
-            const int m = ew * 32 + lane;   // TMEM lane = decode row inside this CTA's 128
-            const uint32_t lane_base = (uint32_t)(ew * 32) << 16;
-            const int row0 = it.g * 256 + 128 * (int)rank;
-            mbar_wait(acc_full, 0);
+            if (++stage == ST) { stage = 0; phase ^= 1; }
+        }
+        const int n_exp = it.vtile ? 0 : s_ucount;
+        for (int iu = 0; iu < n_exp; ++iu) {
+            mbar_wait(full_bar(stage), phase);
             tc_fence_after();
-            if (tid_e == 0) dbg_stamp(a, 4);
-            // partial of (split s2, chunk c) of this CTA's rows: [8 q][128 m] float4 (coalesced)
-            auto part = [&](int s2, int c) {
-                return reinterpret_cast<float4 *>(a.kpart) +
-                       ((((size_t)(it.tile * ks + s2) * 2 + rank) * 8 + c) * 8) * 128 + m;
-            };
-            if (ks > 1) {
-#pragma unroll 1
-                for (int c = 0; c < 8; ++c) {
-                    if (c % ks == it.s) continue;
-                    uint32_t rr[32];
-                    tmem_ld32(tmem_base + lane_base + 32u * c, rr);
-                    tmem_wait_ld();
-                    float4 *dst = part(it.s, c);
+            if (lane == 0) {
+                const uint32_t ab = a_addr(stage), bb = b_addr(stage);
 #pragma unroll
-                    for (int q = 0; q < 8; ++q)
-                        __stcg(dst + q * 128, make_float4(__uint_as_float(rr[4 * q]), __uint_as_float(rr[4 * q + 1]),
-                                                          __uint_as_float(rr[4 * q + 2]), __uint_as_float(rr[4 * q + 3])));
-                }
-                __threadfence();
-                named_bar_sync(1, 128);
-                if (tid_e == 0) {
-                    dbg_stamp(a, 3);
-                    int *arrive = a.ctr + 2 + it.tile;
-                    atom_add_release_gpu(arrive, 1);
-                    while (ld_acquire_gpu(arrive) < 2 * ks) __nanosleep(32);
-                    dbg_stamp(a, 5);
-                }
-                named_bar_sync(1, 128);
+                for (int kk = 0; kk < RP / 16; ++kk)
+                    mma2_bf16(tmem_base, smem_desc(ab + 32u * kk, 16, 8u * RB, kSwR),
+                              smem_desc(bb + 32u * kk, 16, 8u * RB, kSwR), idesc, 1u);
+                mma2_commit_mc(empty_bar(stage));
             }
+            __syncwarp();
+            if (++stage == ST) { stage = 0; phase ^= 1; }
+        }
+        if (lane == 0) {
+            dbg_stamp(a, 9);
+            mma2_commit_mc(acc_full);
+        }
+        __syncwarp();
+    } else if (warp == 3 && !it.vtile && s_ucount > 0) {
+        // expand operands of this split: descriptors and B_u rows of the tile -> caches / L2
+        for (int iu = lane; iu < s_ucount; iu += 32) {
+            const int sl = s_uslot[s_ulist[iu]];
+            const SlotDev *sd = P.slots + sl;
+            tma_prefetch_desc(&sd->tmBk);
+            const int wrow = it.n0 + 128 * (int)rank;
+            if (wrow < P.out) {
+                const char *bp = reinterpret_cast<const char *>(sd->B) + (size_t)wrow * a.r * 2;
+                const uint32_t bytes = (uint32_t)(min(128, P.out - wrow) * a.r * 2);
+                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(bp), "r"(bytes) : "memory");
+            }
+        }
+    } else if (warp >= 4) {
+        // ========================= epilogue warps (both CTAs) =========================
+        const int ew = warp - 4;
+        const int tid_e = threadIdx.x - 128;
+        const int m = ew * 32 + lane;   // TMEM lane = decode row inside this CTA's 128
+        const uint32_t lane_base = (uint32_t)(ew * 32) << 16;
+        const int row0 = it.g * 256 + 128 * (int)rank;
+        const int row = row0 + m;
+        Dec3RowInfo ri{-1, 0.f, 0, 0};
+        if (it.vtile && row < a.S) ri = a.inl ? inl.rows[row] : a.rows[row];
+        mbar_wait(acc_full, 0);
+        tc_fence_after();
+        if (tid_e == 0) dbg_stamp(a, 4);
+        // partial of (split s2, chunk c) of this CTA's rows: [8 q][128 m] float4 (coalesced)
+        auto part = [&](int s2, int c) {
+            return reinterpret_cast<float4 *>(a.kpart) +
+                   ((((size_t)(it.item0 + s2) * 2 + rank) * 8 + c) * 8) * 128 + m;
+        };
+        if (ks > 1) {
+#pragma unroll 1
+            for (int c = 0; c < 8; ++c) {
+                if (c % ks == it.s) continue;
+                uint32_t rr[32];
+                tmem_ld32(tmem_base + lane_base + 32u * c, rr);
+                tmem_wait_ld();
+                float4 *dst = part(it.s, c);
+#pragma unroll
+                for (int q = 0; q < 8; ++q)
+                    __stcg(dst + q * 128, make_float4(__uint_as_float(rr[4 * q]), __uint_as_float(rr[4 * q + 1]),
+                                                      __uint_as_float(rr[4 * q + 2]), __uint_as_float(rr[4 * q + 3])));
+            }
+            __threadfence();
+            named_bar_sync(1, 128);
+            if (tid_e == 0) {
+                dbg_stamp(a, 3);
+                int *arrive = a.ctr + 2 + it.tile;
+                atom_add_release_gpu(arrive, 1);
+                while (ld_acquire_gpu(arrive) < 2 * ks) __nanosleep(32);
+                dbg_stamp(a, 5);
+            }
+            named_bar_sync(1, 128);
             // peers' partials of the owned chunks -> the (now idle) ring with one mbarrier
-            const int n_own = (8 - it.s + ks - 1) / ks;
-            if (ks > 1) {
-                if (tid_e == 0) {
-                    fence_proxy_async_global();
-                    mbar_expect_tx(xbar, (uint32_t)(n_own * (ks - 1)) * 16384u);
-                    int slot = 0;
-                    for (int c = it.s; c < 8; c += ks)
-                        for (int s2 = 0; s2 < ks; ++s2) {
-                            if (s2 == it.s) continue;
-                            bulk_load(base + (uint32_t)slot * 16384u, part(s2, c) - m, 16384u, xbar);
-                            ++slot;
-                        }
-                }
-                mbar_wait(xbar, 0);
-                if (tid_e == 0) dbg_stamp(a, 7);
+            if (tid_e == 0) {
+                fence_proxy_async_global();
+                const int n_own = (8 - it.s + ks - 1) / ks;
+                mbar_expect_tx(xbar, (uint32_t)(n_own * (ks - 1)) * 16384u);
+                int slot = 0;
+                for (int c = it.s; c < 8; c += ks)
+                    for (int s2 = 0; s2 < ks; ++s2) {
+                        if (s2 == it.s) continue;
+                        bulk_load(base + (uint32_t)slot * 16384u, part(s2, c) - m, 16384u, xbar);
+                        ++slot;
+                    }
             }
-            int ybuf = 0;
+            mbar_wait(xbar, 0);
+            if (tid_e == 0) dbg_stamp(a, 7);
+        }
+        int ybuf = 0;
 #pragma unroll 1
-            for (int c = it.s, oi = 0; c < 8; c += ks, ++oi) {
-                float v[32];
-                {
-                    uint32_t rr[32];
-                    tmem_ld32(tmem_base + lane_base + 32u * c, rr);
-                    tmem_wait_ld();
+        for (int c = it.s, oi = 0; c < 8; c += ks, ++oi) {
+            float v[32];
+            {
+                uint32_t rr[32];
+                tmem_ld32(tmem_base + lane_base + 32u * c, rr);
+                tmem_wait_ld();
 #pragma unroll 1
-                    for (int s2 = 0, j = 0; s2 < ks; ++s2) {
-                        float t[32];
-                        if (s2 == it.s) {
+                for (int s2 = 0, j = 0; s2 < ks; ++s2) {
+                    float t[32];
+                    if (s2 == it.s) {
 #pragma unroll
-                            for (int e = 0; e < 32; ++e) t[e] = __uint_as_float(rr[e]);
-                        } else {
-                            const float4 *src = reinterpret_cast<const float4 *>(base_ptr + (size_t)(oi * (ks - 1) + j) * 16384u) + m;
+                        for (int e = 0; e < 32; ++e) t[e] = __uint_as_float(rr[e]);
+                    } else {
+                        const float4 *src = reinterpret_cast<const float4 *>(base_ptr + (size_t)(oi * (ks - 1) + j) * 16384u) + m;
 #pragma unroll
-                            for (int q = 0; q < 8; ++q) {
-                                const float4 f = src[q * 128];
-                                t[4 * q] = f.x;
-                                t[4 * q + 1] = f.y;
-                                t[4 * q + 2] = f.z;
-                                t[4 * q + 3] = f.w;
-                            }
-                            ++j;
+                        for (int q = 0; q < 8; ++q) {
+                            const float4 f = src[q * 128];
+                            t[4 * q] = f.x;
+                            t[4 * q + 1] = f.y;
+                            t[4 * q + 2] = f.z;
+                            t[4 * q + 3] = f.w;
                         }
+                        ++j;
+                    }
 #pragma unroll
-                        for (int e = 0; e < 32; ++e) v[e] = s2 == 0 ? t[e] : v[e] + t[e];
+                    for (int e = 0; e < 32; ++e) v[e] = s2 == 0 ? t[e] : v[e] + t[e];
+                }
+            }
+            if (it.vtile) {
+                // columns [32c, 32c + 32) = adapters n0 + (32c + 32 rank... ) of the stacked tile: write the
+                // block-diagonal slab of those adapters for this CTA's rows (s*V of the row's own adapter,
+                // zero elsewhere) and V_save
+                if (row < a.S) {
+                    __nv_bfloat16 *sv = reinterpret_cast<__nv_bfloat16 *>(P.sv);
+                    __nv_bfloat16 *vsave = reinterpret_cast<__nv_bfloat16 *>(P.Vsave);
+#pragma unroll
+                    for (int h = 0; h < 32 / (RP < 32 ? RP : 32); ++h) {
+                        constexpr int W = RP < 32 ? RP : 32;   // columns of one adapter inside this chunk
+                        const int col = 32 * c + h * W;        // tile column of this piece
+                        const int ua = it.n0 + col / RP;       // its adapter
+                        const int j0 = col % RP;               // first rank index of the piece
+                        if (ua >= a.n_uniq) continue;
+                        const bool own_adapter = ri.uidx == ua;
+                        uint4 *dst = reinterpret_cast<uint4 *>(
+                            sv + ((size_t)(it.g * a.n_uniq + ua) * 256 + (row & 255)) * RP + j0);
+#pragma unroll
+                        for (int q = 0; q < W / 8; ++q) {
+                            uint4 pk = make_uint4(0, 0, 0, 0);
+                            if (own_adapter) {
+                                const float s = ri.scale;
+                                pk.x = pack_bf16x2(s * v[h * W + 8 * q + 0], s * v[h * W + 8 * q + 1]);
+                                pk.y = pack_bf16x2(s * v[h * W + 8 * q + 2], s * v[h * W + 8 * q + 3]);
+                                pk.z = pack_bf16x2(s * v[h * W + 8 * q + 4], s * v[h * W + 8 * q + 5]);
+                                pk.w = pack_bf16x2(s * v[h * W + 8 * q + 6], s * v[h * W + 8 * q + 7]);
+                            }
+                            dst[q] = pk;
+                        }
+                        if (own_adapter && ri.ft && vsave) {
+#pragma unroll
+                            for (int e = 0; e < W; ++e)
+                                if (j0 + e < a.r) vsave[(size_t)row * a.r + j0 + e] = __float2bfloat16_rn(v[h * W + e]);
+                        }
                     }
                 }
+            } else {
                 // bf16 chunk -> staging -> TMA store (rows >= S and columns >= out are clipped)
                 if (tid_e == 0) bulk_wait_read1();   // the store issued from this buffer two chunks ago has read it
                 named_bar_sync(1, 128);
@@ -640,15 +478,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT3, 1) smlm_dec3_ke
                 }
                 ybuf ^= 1;
             }
+        }
+        if (it.vtile) {
+            // publish: the slabs are read by TMA (async proxy) in other CTAs
+            fence_proxy_async_global();
+            __threadfence();
+            named_bar_sync(1, 128);
             if (tid_e == 0) {
-                bulk_wait_all();
+                atom_add_release_gpu(a.ctr, 1);
                 dbg_stamp(a, 6);
+                dbg_stamp(a, 15);   // marks a V-tile CTA for the timeline scripts
             }
+        } else if (tid_e == 0) {
+            bulk_wait_all();
+            dbg_stamp(a, 6);
         }
     }
     tc_fence_before();
     cluster_sync();
-    if (wpair && warp == 2) {
+    if (active && warp == 2) {
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(256) : "memory");
     }
@@ -658,13 +506,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT3, 1) smlm_dec3_ke
         if (atom_add_acq_rel_gpu(a.ctr + 1, 1) == (int)gridDim.x - 1) {
             a.ctr[0] = 0;
             a.ctr[1] = 0;
-            for (int t = 0; t < a.n_groups * a.n_wt; ++t) a.ctr[2 + t] = 0;
+            const int tiles = a.n_vpairs / a.ks_v + a.n_groups * a.n_wt;
+            for (int t = 0; t < tiles; ++t) a.ctr[2 + t] = 0;
         }
     }
 }
 
 static_assert(sizeof(Dec3Args) + sizeof(Dec3Inline) <= 32764, "kernel parameters exceed 32 KB");
-static_assert(2 * ShrinkSmem<64, 4, kShrMI>::end <= 6 * kStage3, "shrink workers exceed the ring");
 
 template <int RP>
 int launch_dec3_impl(const Dec3Args &a, const Dec3Inline &in, int clusters, cudaStream_t st) {

@@ -39,14 +39,14 @@ for proj in (os.environ.get("PROJ", "q,k").split(",")):
     t = t[used].astype(np.float64)
     t0 = t[:, 0].min()
     rel = (t - t0) / 1e3
-    wm = t[:, 4] > 0
-    out = {"proj": proj, "w_ctas": int(wm.sum()), "shrink_ctas": int((~wm).sum())}
+    wm = (t[:, 4] > 0) & (t[:, 15] == 0)
+    out = {"proj": proj, "w_ctas": int(wm.sum()), "v_ctas": int((~wm).sum())}
     names = ["start", "loads_issued", "v_seen", "parts_stored", "acc_ready", "arrived", "stored", "xbar", "exp_issued", "mma_done", "kb0", "kb4", "kb8", "kb12", "kb16", "kb20"]
     for k, name in enumerate(names):
         col = rel[wm, k][t[wm, k] > 0]
         if len(col):
             out[name] = [round(float(np.min(col)), 2), round(float(np.median(col)), 2), round(float(np.max(col)), 2)]
-    for k, name in [(10, "s_staged"), (11, "s_item0_fma"), (12, "s_item0_red"), (13, "s_item0_csync"), (14, "s_item0_written"), (15, "s_item0_end"), (1, "shrink_done")]:
+    for k, name in [(1, "v_loads_issued"), (4, "v_acc_ready"), (5, "v_arrived"), (6, "v_published")]:
         col = rel[~wm, k][t[~wm, k] > 0]
         if len(col):
             out[name] = [round(float(np.min(col)), 2), round(float(np.median(col)), 2), round(float(np.max(col)), 2)]

@@ -40,14 +40,15 @@ t = ws[n - 148 * 128:n].view(torch.int64).view(148, 16).cpu().numpy()
 used = t[:, 0] > 0
 t = t[used].astype(np.float64)
 rel = (t - t[:, 0].min()) / 1e3
-wm = t[:, 4] > 0
+wm = (t[:, 4] > 0) & (t[:, 15] == 0)
 names = ["start", "loads_issued", "v_seen", "parts_stored", "acc_ready", "arrived", "stored"]
-out = {"w_ctas": int(wm.sum()), "shrink_ctas": int((~wm).sum())}
+out = {"w_ctas": int(wm.sum()), "v_ctas": int((~wm).sum())}
 for k, name in enumerate(names):
     col = rel[wm, k][t[wm, k] > 0]
     if len(col):
         out[name] = [round(float(np.min(col)), 2), round(float(np.median(col)), 2), round(float(np.max(col)), 2)]
-col = rel[~wm, 1][t[~wm, 1] > 0]
-if len(col):
-    out["shrink_done"] = [round(float(np.min(col)), 2), round(float(np.median(col)), 2), round(float(np.max(col)), 2)]
+for k, name in [(1, "v_loads_issued"), (4, "v_acc_ready"), (5, "v_arrived"), (6, "v_published")]:
+    col = rel[~wm, k][t[~wm, k] > 0]
+    if len(col):
+        out[name] = [round(float(np.min(col)), 2), round(float(np.median(col)), 2), round(float(np.max(col)), 2)]
 print(json.dumps(out))
