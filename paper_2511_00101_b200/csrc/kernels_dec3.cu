@@ -288,7 +288,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT3, 1) smlm_dec3_ke
         for (int kb = kb0; kb < kb1; ++kb) {
             mbar_wait(full_bar(stage), phase);
             tc_fence_after();
-            if (lane == 0 && ((kb - kb0) & 3) == 0 && (kb - kb0) < 24) dbg_stamp(a, 10 + (kb - kb0) / 4);
             if (lane == 0) {
                 const uint32_t ab = a_addr(stage), bb = b_addr(stage);
 #pragma unroll
@@ -351,135 +350,110 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT3, 1) smlm_dec3_ke
             return reinterpret_cast<float4 *>(a.kpart) +
                    ((((size_t)(it.item0 + s2) * 2 + rank) * 8 + c) * 8) * 128 + m;
         };
-        if (ks > 1) {
+        if (it.vtile) {
+            // ---- V tile: only each row's own-adapter columns matter, so the split-K reduction moves
+            // r_pad floats per row (not the whole 256-column accumulator) ----
+            const int APT = 256 / RP;
+            const int ua = ri.uidx;
+            const bool in_tile = ua >= it.n0 && ua < it.n0 + APT;
+            const int col0 = (ua - it.n0) * RP;   // the row's adapter columns [col0, col0 + RP)
+            float vp[RP];
+#pragma unroll
+            for (int j = 0; j < RP; ++j) vp[j] = 0.f;
+            constexpr int W = RP < 32 ? RP : 32;  // columns of one adapter inside a 32-column chunk
 #pragma unroll 1
             for (int c = 0; c < 8; ++c) {
-                if (c % ks == it.s) continue;
                 uint32_t rr[32];
                 tmem_ld32(tmem_base + lane_base + 32u * c, rr);
                 tmem_wait_ld();
-                float4 *dst = part(it.s, c);
+                if (!__any_sync(0xffffffffu, in_tile && col0 < 32 * c + 32 && col0 + RP > 32 * c)) continue;
 #pragma unroll
-                for (int q = 0; q < 8; ++q)
-                    __stcg(dst + q * 128, make_float4(__uint_as_float(rr[4 * q]), __uint_as_float(rr[4 * q + 1]),
-                                                      __uint_as_float(rr[4 * q + 2]), __uint_as_float(rr[4 * q + 3])));
-            }
-            __threadfence();
-            named_bar_sync(1, 128);
-            if (tid_e == 0) {
-                dbg_stamp(a, 3);
-                int *arrive = a.ctr + 2 + it.tile;
-                atom_add_release_gpu(arrive, 1);
-                while (ld_acquire_gpu(arrive) < 2 * ks) __nanosleep(32);
-                dbg_stamp(a, 5);
-            }
-            named_bar_sync(1, 128);
-            // peers' partials of the owned chunks -> the (now idle) ring with one mbarrier
-            if (tid_e == 0) {
-                fence_proxy_async_global();
-                const int n_own = (8 - it.s + ks - 1) / ks;
-                mbar_expect_tx(xbar, (uint32_t)(n_own * (ks - 1)) * 16384u);
-                int slot = 0;
-                for (int c = it.s; c < 8; c += ks)
-                    for (int s2 = 0; s2 < ks; ++s2) {
-                        if (s2 == it.s) continue;
-                        bulk_load(base + (uint32_t)slot * 16384u, part(s2, c) - m, 16384u, xbar);
-                        ++slot;
-                    }
-            }
-            mbar_wait(xbar, 0);
-            if (tid_e == 0) dbg_stamp(a, 7);
-        }
-        int ybuf = 0;
-#pragma unroll 1
-        for (int c = it.s, oi = 0; c < 8; c += ks, ++oi) {
-            float v[32];
-            {
-                uint32_t rr[32];
-                tmem_ld32(tmem_base + lane_base + 32u * c, rr);
-                tmem_wait_ld();
-#pragma unroll 1
-                for (int s2 = 0, j = 0; s2 < ks; ++s2) {
-                    float t[32];
-                    if (s2 == it.s) {
+                for (int h = 0; h < 32 / W; ++h) {
+                    const int col = 32 * c + h * W;
+                    if (in_tile && col >= col0 && col < col0 + RP) {
+                        const int j0 = col - col0;   // 0, or 32 for r_pad = 64
 #pragma unroll
-                        for (int e = 0; e < 32; ++e) t[e] = __uint_as_float(rr[e]);
-                    } else {
-                        const float4 *src = reinterpret_cast<const float4 *>(base_ptr + (size_t)(oi * (ks - 1) + j) * 16384u) + m;
-#pragma unroll
-                        for (int q = 0; q < 8; ++q) {
-                            const float4 f = src[q * 128];
-                            t[4 * q] = f.x;
-                            t[4 * q + 1] = f.y;
-                            t[4 * q + 2] = f.z;
-                            t[4 * q + 3] = f.w;
-                        }
-                        ++j;
-                    }
-#pragma unroll
-                    for (int e = 0; e < 32; ++e) v[e] = s2 == 0 ? t[e] : v[e] + t[e];
-                }
-            }
-            if (it.vtile) {
-                // columns [32c, 32c + 32) = adapters n0 + (32c + 32 rank... ) of the stacked tile: write the
-                // block-diagonal slab of those adapters for this CTA's rows (s*V of the row's own adapter,
-                // zero elsewhere) and V_save
-                if (row < a.S) {
-                    __nv_bfloat16 *sv = reinterpret_cast<__nv_bfloat16 *>(P.sv);
-                    __nv_bfloat16 *vsave = reinterpret_cast<__nv_bfloat16 *>(P.Vsave);
-#pragma unroll
-                    for (int h = 0; h < 32 / (RP < 32 ? RP : 32); ++h) {
-                        constexpr int W = RP < 32 ? RP : 32;   // columns of one adapter inside this chunk
-                        const int col = 32 * c + h * W;        // tile column of this piece
-                        const int ua = it.n0 + col / RP;       // its adapter
-                        const int j0 = col % RP;               // first rank index of the piece
-                        if (ua >= a.n_uniq) continue;
-                        const bool own_adapter = ri.uidx == ua;
-                        uint4 *dst = reinterpret_cast<uint4 *>(
-                            sv + ((size_t)(it.g * a.n_uniq + ua) * 256 + (row & 255)) * RP + j0);
-#pragma unroll
-                        for (int q = 0; q < W / 8; ++q) {
-                            uint4 pk = make_uint4(0, 0, 0, 0);
-                            if (own_adapter) {
-                                const float s = ri.scale;
-                                pk.x = pack_bf16x2(s * v[h * W + 8 * q + 0], s * v[h * W + 8 * q + 1]);
-                                pk.y = pack_bf16x2(s * v[h * W + 8 * q + 2], s * v[h * W + 8 * q + 3]);
-                                pk.z = pack_bf16x2(s * v[h * W + 8 * q + 4], s * v[h * W + 8 * q + 5]);
-                                pk.w = pack_bf16x2(s * v[h * W + 8 * q + 6], s * v[h * W + 8 * q + 7]);
-                            }
-                            dst[q] = pk;
-                        }
-                        if (own_adapter && ri.ft && vsave) {
-#pragma unroll
-                            for (int e = 0; e < W; ++e)
-                                if (j0 + e < a.r) vsave[(size_t)row * a.r + j0 + e] = __float2bfloat16_rn(v[h * W + e]);
+                        for (int e = 0; e < W; ++e) {
+                            if (j0 == 0) vp[e] = __uint_as_float(rr[h * W + e]);
+                            else vp[(RP > 32 ? 32 : 0) + e] = __uint_as_float(rr[h * W + e]);
                         }
                     }
                 }
-            } else {
-                // bf16 chunk -> staging -> TMA store (rows >= S and columns >= out are clipped)
-                if (tid_e == 0) bulk_wait_read1();   // the store issued from this buffer two chunks ago has read it
-                named_bar_sync(1, 128);
-                uint4 *ys = reinterpret_cast<uint4 *>(base_ptr + (ystage - base) + ybuf * kYStage);
+            }
+            // compact partial of this split: [item][rank][128 rows][RP] fp32
+            float *vpart = a.kpart + ((size_t)it.item0 * 2 + rank) * 128 * RP;   // split s2 at + s2 * 2 * 128 * RP
+            if (ks > 1) {
+                if (in_tile) {
+                    float4 *dst = reinterpret_cast<float4 *>(vpart + ((size_t)it.s * 2 * 128 + m) * RP);
 #pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    uint4 pk;
-                    pk.x = pack_bf16x2(v[8 * q + 0], v[8 * q + 1]);
-                    pk.y = pack_bf16x2(v[8 * q + 2], v[8 * q + 3]);
-                    pk.z = pack_bf16x2(v[8 * q + 4], v[8 * q + 5]);
-                    pk.w = pack_bf16x2(v[8 * q + 6], v[8 * q + 7]);
-                    ys[m * 4 + q] = pk;
+                    for (int q = 0; q < RP / 4; ++q) __stcg(dst + q, make_float4(vp[4 * q], vp[4 * q + 1], vp[4 * q + 2], vp[4 * q + 3]));
                 }
-                fence_proxy_async_smem();
+                __threadfence();
                 named_bar_sync(1, 128);
                 if (tid_e == 0) {
-                    tma_store_2d(&P.tmY, ystage + ybuf * kYStage, it.n0 + 32 * c, row0);
-                    bulk_commit();
+                    dbg_stamp(a, 3);
+                    int *arrive = a.ctr + 2 + it.tile;
+                    atom_add_release_gpu(arrive, 1);
+                    while (ld_acquire_gpu(arrive) < 2 * ks) __nanosleep(32);
+                    dbg_stamp(a, 5);
                 }
-                ybuf ^= 1;
+                named_bar_sync(1, 128);
             }
-        }
-        if (it.vtile) {
+            // rows m with m % ks == s: sum the splits in order, write the row's slab entries for every
+            // adapter of the tile (s*V for its own adapter, zero otherwise) and V_save
+            if (m % ks == it.s && row < a.S) {
+                if (in_tile && ks > 1) {
+                    // all splits' partials of a 16-column slice in flight at once, summed in split order
+#pragma unroll
+                    for (int j0 = 0; j0 < RP; j0 += 16) {
+                        float t[8][16];
+#pragma unroll
+                        for (int s2 = 0; s2 < 8; ++s2) {
+                            if (s2 < ks) {
+                                const float4 *src = reinterpret_cast<const float4 *>(vpart + ((size_t)s2 * 2 * 128 + m) * RP + j0);
+#pragma unroll
+                                for (int q = 0; q < 4; ++q) {
+                                    const float4 f = __ldcg(src + q);
+                                    t[s2][4 * q] = f.x;
+                                    t[s2][4 * q + 1] = f.y;
+                                    t[s2][4 * q + 2] = f.z;
+                                    t[s2][4 * q + 3] = f.w;
+                                }
+                            }
+                        }
+#pragma unroll
+                        for (int s2 = 0; s2 < 8; ++s2)
+                            if (s2 < ks)
+#pragma unroll
+                                for (int j = 0; j < 16; ++j) vp[j0 + j] = s2 == 0 ? t[0][j] : vp[j0 + j] + t[s2][j];
+                    }
+                }
+                __nv_bfloat16 *sv = reinterpret_cast<__nv_bfloat16 *>(P.sv);
+                for (int ad = 0; ad < APT; ++ad) {
+                    const int uu = it.n0 + ad;
+                    if (uu >= a.n_uniq) break;
+                    uint4 *dst = reinterpret_cast<uint4 *>(sv + ((size_t)(it.g * a.n_uniq + uu) * 256 + (row & 255)) * RP);
+                    const bool own = in_tile && uu == ua;
+#pragma unroll
+                    for (int q = 0; q < RP / 8; ++q) {
+                        uint4 pk = make_uint4(0, 0, 0, 0);
+                        if (own) {
+                            const float s = ri.scale;
+                            pk.x = pack_bf16x2(s * vp[8 * q + 0], s * vp[8 * q + 1]);
+                            pk.y = pack_bf16x2(s * vp[8 * q + 2], s * vp[8 * q + 3]);
+                            pk.z = pack_bf16x2(s * vp[8 * q + 4], s * vp[8 * q + 5]);
+                            pk.w = pack_bf16x2(s * vp[8 * q + 6], s * vp[8 * q + 7]);
+                        }
+                        dst[q] = pk;
+                    }
+                }
+                __nv_bfloat16 *vsave = reinterpret_cast<__nv_bfloat16 *>(P.Vsave);
+                if (in_tile && ri.ft && vsave) {
+#pragma unroll
+                    for (int j = 0; j < RP; ++j)
+                        if (j < a.r) vsave[(size_t)row * a.r + j] = __float2bfloat16_rn(vp[j]);
+                }
+            }
             // publish: the slabs are read by TMA (async proxy) in other CTAs
             fence_proxy_async_global();
             __threadfence();
@@ -489,9 +463,139 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT3, 1) smlm_dec3_ke
                 dbg_stamp(a, 6);
                 dbg_stamp(a, 15);   // marks a V-tile CTA for the timeline scripts
             }
-        } else if (tid_e == 0) {
-            bulk_wait_all();
-            dbg_stamp(a, 6);
+        } else {
+            if (ks > 1) {
+    #pragma unroll 1
+                for (int c = 0; c < 8; ++c) {
+                    if (c % ks == it.s) continue;
+                    uint32_t rr[32];
+                    tmem_ld32(tmem_base + lane_base + 32u * c, rr);
+                    tmem_wait_ld();
+                    float4 *dst = part(it.s, c);
+    #pragma unroll
+                    for (int q = 0; q < 8; ++q)
+                        __stcg(dst + q * 128, make_float4(__uint_as_float(rr[4 * q]), __uint_as_float(rr[4 * q + 1]),
+                                                          __uint_as_float(rr[4 * q + 2]), __uint_as_float(rr[4 * q + 3])));
+                }
+                __threadfence();
+                named_bar_sync(1, 128);
+                if (tid_e == 0) {
+                    dbg_stamp(a, 3);
+                    int *arrive = a.ctr + 2 + it.tile;
+                    atom_add_release_gpu(arrive, 1);
+                    while (ld_acquire_gpu(arrive) < 2 * ks) __nanosleep(32);
+                    dbg_stamp(a, 5);
+                }
+                named_bar_sync(1, 128);
+                // peers' partials of the owned chunks -> the (now idle) ring with one mbarrier
+                if (tid_e == 0) {
+                    fence_proxy_async_global();
+                    const int n_own = (8 - it.s + ks - 1) / ks;
+                    mbar_expect_tx(xbar, (uint32_t)(n_own * (ks - 1)) * 16384u);
+                    int slot = 0;
+                    for (int c = it.s; c < 8; c += ks)
+                        for (int s2 = 0; s2 < ks; ++s2) {
+                            if (s2 == it.s) continue;
+                            bulk_load(base + (uint32_t)slot * 16384u, part(s2, c) - m, 16384u, xbar);
+                            ++slot;
+                        }
+                }
+                mbar_wait(xbar, 0);
+                if (tid_e == 0) dbg_stamp(a, 7);
+            }
+            int ybuf = 0;
+    #pragma unroll 1
+            for (int c = it.s, oi = 0; c < 8; c += ks, ++oi) {
+                float v[32];
+                {
+                    uint32_t rr[32];
+                    tmem_ld32(tmem_base + lane_base + 32u * c, rr);
+                    tmem_wait_ld();
+    #pragma unroll 1
+                    for (int s2 = 0, j = 0; s2 < ks; ++s2) {
+                        float t[32];
+                        if (s2 == it.s) {
+    #pragma unroll
+                            for (int e = 0; e < 32; ++e) t[e] = __uint_as_float(rr[e]);
+                        } else {
+                            const float4 *src = reinterpret_cast<const float4 *>(base_ptr + (size_t)(oi * (ks - 1) + j) * 16384u) + m;
+    #pragma unroll
+                            for (int q = 0; q < 8; ++q) {
+                                const float4 f = src[q * 128];
+                                t[4 * q] = f.x;
+                                t[4 * q + 1] = f.y;
+                                t[4 * q + 2] = f.z;
+                                t[4 * q + 3] = f.w;
+                            }
+                            ++j;
+                        }
+    #pragma unroll
+                        for (int e = 0; e < 32; ++e) v[e] = s2 == 0 ? t[e] : v[e] + t[e];
+                    }
+                }
+                if (it.vtile) {
+                    // columns [32c, 32c + 32) = adapters n0 + (32c + 32 rank... ) of the stacked tile: write the
+                    // block-diagonal slab of those adapters for this CTA's rows (s*V of the row's own adapter,
+                    // zero elsewhere) and V_save
+                    if (row < a.S) {
+                        __nv_bfloat16 *sv = reinterpret_cast<__nv_bfloat16 *>(P.sv);
+                        __nv_bfloat16 *vsave = reinterpret_cast<__nv_bfloat16 *>(P.Vsave);
+    #pragma unroll
+                        for (int h = 0; h < 32 / (RP < 32 ? RP : 32); ++h) {
+                            constexpr int W = RP < 32 ? RP : 32;   // columns of one adapter inside this chunk
+                            const int col = 32 * c + h * W;        // tile column of this piece
+                            const int ua = it.n0 + col / RP;       // its adapter
+                            const int j0 = col % RP;               // first rank index of the piece
+                            if (ua >= a.n_uniq) continue;
+                            const bool own_adapter = ri.uidx == ua;
+                            uint4 *dst = reinterpret_cast<uint4 *>(
+                                sv + ((size_t)(it.g * a.n_uniq + ua) * 256 + (row & 255)) * RP + j0);
+    #pragma unroll
+                            for (int q = 0; q < W / 8; ++q) {
+                                uint4 pk = make_uint4(0, 0, 0, 0);
+                                if (own_adapter) {
+                                    const float s = ri.scale;
+                                    pk.x = pack_bf16x2(s * v[h * W + 8 * q + 0], s * v[h * W + 8 * q + 1]);
+                                    pk.y = pack_bf16x2(s * v[h * W + 8 * q + 2], s * v[h * W + 8 * q + 3]);
+                                    pk.z = pack_bf16x2(s * v[h * W + 8 * q + 4], s * v[h * W + 8 * q + 5]);
+                                    pk.w = pack_bf16x2(s * v[h * W + 8 * q + 6], s * v[h * W + 8 * q + 7]);
+                                }
+                                dst[q] = pk;
+                            }
+                            if (own_adapter && ri.ft && vsave) {
+    #pragma unroll
+                                for (int e = 0; e < W; ++e)
+                                    if (j0 + e < a.r) vsave[(size_t)row * a.r + j0 + e] = __float2bfloat16_rn(v[h * W + e]);
+                            }
+                        }
+                    }
+                } else {
+                    // bf16 chunk -> staging -> TMA store (rows >= S and columns >= out are clipped)
+                    if (tid_e == 0) bulk_wait_read1();   // the store issued from this buffer two chunks ago has read it
+                    named_bar_sync(1, 128);
+                    uint4 *ys = reinterpret_cast<uint4 *>(base_ptr + (ystage - base) + ybuf * kYStage);
+    #pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        uint4 pk;
+                        pk.x = pack_bf16x2(v[8 * q + 0], v[8 * q + 1]);
+                        pk.y = pack_bf16x2(v[8 * q + 2], v[8 * q + 3]);
+                        pk.z = pack_bf16x2(v[8 * q + 4], v[8 * q + 5]);
+                        pk.w = pack_bf16x2(v[8 * q + 6], v[8 * q + 7]);
+                        ys[m * 4 + q] = pk;
+                    }
+                    fence_proxy_async_smem();
+                    named_bar_sync(1, 128);
+                    if (tid_e == 0) {
+                        tma_store_2d(&P.tmY, ystage + ybuf * kYStage, it.n0 + 32 * c, row0);
+                        bulk_commit();
+                    }
+                    ybuf ^= 1;
+                }
+            }
+            if (tid_e == 0) {
+                bulk_wait_all();
+                dbg_stamp(a, 6);
+            }
         }
     }
     tc_fence_before();

@@ -41,7 +41,7 @@ for proj in (os.environ.get("PROJ", "q,k").split(",")):
     rel = (t - t0) / 1e3
     wm = (t[:, 4] > 0) & (t[:, 15] == 0)
     out = {"proj": proj, "w_ctas": int(wm.sum()), "v_ctas": int((~wm).sum())}
-    names = ["start", "loads_issued", "v_seen", "parts_stored", "acc_ready", "arrived", "stored", "xbar", "exp_issued", "mma_done", "kb0", "kb4", "kb8", "kb12", "kb16", "kb20"]
+    names = ["start", "loads_issued", "v_seen", "parts_stored", "acc_ready", "arrived", "stored", "xbar", "exp_issued", "mma_done"]
     for k, name in enumerate(names):
         col = rel[wm, k][t[wm, k] > 0]
         if len(col):
