@@ -503,23 +503,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT3, 1) smlm_dec3_ke
                 mbar_wait(xbar, 0);
                 if (tid_e == 0) dbg_stamp(a, 7);
             }
-            int ybuf = 0;
-    #pragma unroll 1
+            // own chunks: sum the splits in order, bf16 into the idle ring above the loaded partials
+            // (<= 7 x 16 KB), then one TMA store per chunk (rows >= S / columns >= out clipped)
+            const uint32_t ybase = base + 7u * 16384u;
+#pragma unroll 1
             for (int c = it.s, oi = 0; c < 8; c += ks, ++oi) {
                 float v[32];
                 {
                     uint32_t rr[32];
                     tmem_ld32(tmem_base + lane_base + 32u * c, rr);
                     tmem_wait_ld();
-    #pragma unroll 1
+#pragma unroll 1
                     for (int s2 = 0, j = 0; s2 < ks; ++s2) {
                         float t[32];
                         if (s2 == it.s) {
-    #pragma unroll
+#pragma unroll
                             for (int e = 0; e < 32; ++e) t[e] = __uint_as_float(rr[e]);
                         } else {
                             const float4 *src = reinterpret_cast<const float4 *>(base_ptr + (size_t)(oi * (ks - 1) + j) * 16384u) + m;
-    #pragma unroll
+#pragma unroll
                             for (int q = 0; q < 8; ++q) {
                                 const float4 f = src[q * 128];
                                 t[4 * q] = f.x;
@@ -529,68 +531,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT3, 1) smlm_dec3_ke
                             }
                             ++j;
                         }
-    #pragma unroll
+#pragma unroll
                         for (int e = 0; e < 32; ++e) v[e] = s2 == 0 ? t[e] : v[e] + t[e];
                     }
                 }
-                if (it.vtile) {
-                    // columns [32c, 32c + 32) = adapters n0 + (32c + 32 rank... ) of the stacked tile: write the
-                    // block-diagonal slab of those adapters for this CTA's rows (s*V of the row's own adapter,
-                    // zero elsewhere) and V_save
-                    if (row < a.S) {
-                        __nv_bfloat16 *sv = reinterpret_cast<__nv_bfloat16 *>(P.sv);
-                        __nv_bfloat16 *vsave = reinterpret_cast<__nv_bfloat16 *>(P.Vsave);
-    #pragma unroll
-                        for (int h = 0; h < 32 / (RP < 32 ? RP : 32); ++h) {
-                            constexpr int W = RP < 32 ? RP : 32;   // columns of one adapter inside this chunk
-                            const int col = 32 * c + h * W;        // tile column of this piece
-                            const int ua = it.n0 + col / RP;       // its adapter
-                            const int j0 = col % RP;               // first rank index of the piece
-                            if (ua >= a.n_uniq) continue;
-                            const bool own_adapter = ri.uidx == ua;
-                            uint4 *dst = reinterpret_cast<uint4 *>(
-                                sv + ((size_t)(it.g * a.n_uniq + ua) * 256 + (row & 255)) * RP + j0);
-    #pragma unroll
-                            for (int q = 0; q < W / 8; ++q) {
-                                uint4 pk = make_uint4(0, 0, 0, 0);
-                                if (own_adapter) {
-                                    const float s = ri.scale;
-                                    pk.x = pack_bf16x2(s * v[h * W + 8 * q + 0], s * v[h * W + 8 * q + 1]);
-                                    pk.y = pack_bf16x2(s * v[h * W + 8 * q + 2], s * v[h * W + 8 * q + 3]);
-                                    pk.z = pack_bf16x2(s * v[h * W + 8 * q + 4], s * v[h * W + 8 * q + 5]);
-                                    pk.w = pack_bf16x2(s * v[h * W + 8 * q + 6], s * v[h * W + 8 * q + 7]);
-                                }
-                                dst[q] = pk;
-                            }
-                            if (own_adapter && ri.ft && vsave) {
-    #pragma unroll
-                                for (int e = 0; e < W; ++e)
-                                    if (j0 + e < a.r) vsave[(size_t)row * a.r + j0 + e] = __float2bfloat16_rn(v[h * W + e]);
-                            }
-                        }
-                    }
-                } else {
-                    // bf16 chunk -> staging -> TMA store (rows >= S and columns >= out are clipped)
-                    if (tid_e == 0) bulk_wait_read1();   // the store issued from this buffer two chunks ago has read it
-                    named_bar_sync(1, 128);
-                    uint4 *ys = reinterpret_cast<uint4 *>(base_ptr + (ystage - base) + ybuf * kYStage);
-    #pragma unroll
-                    for (int q = 0; q < 4; ++q) {
-                        uint4 pk;
-                        pk.x = pack_bf16x2(v[8 * q + 0], v[8 * q + 1]);
-                        pk.y = pack_bf16x2(v[8 * q + 2], v[8 * q + 3]);
-                        pk.z = pack_bf16x2(v[8 * q + 4], v[8 * q + 5]);
-                        pk.w = pack_bf16x2(v[8 * q + 6], v[8 * q + 7]);
-                        ys[m * 4 + q] = pk;
-                    }
-                    fence_proxy_async_smem();
-                    named_bar_sync(1, 128);
-                    if (tid_e == 0) {
-                        tma_store_2d(&P.tmY, ystage + ybuf * kYStage, it.n0 + 32 * c, row0);
-                        bulk_commit();
-                    }
-                    ybuf ^= 1;
+                uint4 *ys = reinterpret_cast<uint4 *>(base_ptr + (ybase - base) + (size_t)oi * kYStage);
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    uint4 pk;
+                    pk.x = pack_bf16x2(v[8 * q + 0], v[8 * q + 1]);
+                    pk.y = pack_bf16x2(v[8 * q + 2], v[8 * q + 3]);
+                    pk.z = pack_bf16x2(v[8 * q + 4], v[8 * q + 5]);
+                    pk.w = pack_bf16x2(v[8 * q + 6], v[8 * q + 7]);
+                    ys[m * 4 + q] = pk;
                 }
+            }
+            fence_proxy_async_smem();
+            named_bar_sync(1, 128);
+            if (tid_e == 0) {
+                for (int c = it.s, oi = 0; c < 8; c += ks, ++oi)
+                    tma_store_2d(&P.tmY, ybase + (uint32_t)oi * kYStage, it.n0 + 32 * c, row0);
+                bulk_commit();
             }
             if (tid_e == 0) {
                 bulk_wait_all();
