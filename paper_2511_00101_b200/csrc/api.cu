@@ -81,6 +81,19 @@ struct HostProf {
                     t[0] / n, t[1] / n, t[2] / n, t[3] / n, t[4] / n);
     }
 } g_hprof;
+// measurement overrides read once per process (getenv scans the environment on every call)
+static int env_int(const char *name) {
+    static std::mutex mu;
+    static std::vector<std::pair<std::string, int>> cache;
+    std::lock_guard<std::mutex> lk(mu);
+    for (auto &kv : cache)
+        if (kv.first == name) return kv.second;
+    const char *e = getenv(name);
+    const int v = e ? (atoi(e) ? atoi(e) : 1) : 0;
+    cache.emplace_back(name, v);
+    return v;
+}
+static bool env_flag(const char *name) { return env_int(name) != 0; }
 static inline double now_us() {
     return std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now().time_since_epoch()).count();
 }
@@ -354,7 +367,7 @@ Dec3Plan dec3_plan(int n_proj, const smlm_pool *pools, const smlm_batch *b, cons
     Dec3Plan D;
     smlm_pool p0 = pools[0];
     if (p0->dtype != SMLM_BF16 || !plan.long_tiles.empty() || plan.short_tiles.empty() || b->S > kDec3InlineRows ||
-        getenv("SMLM_NO_DEC3"))
+        env_flag("SMLM_NO_DEC3"))
         return D;
     // adapters of the batch (ascending) and per-row records
     D.rows.assign(b->S, Dec3RowInfo{-1, 0.f, 0, 0});
@@ -391,7 +404,8 @@ Dec3Plan dec3_plan(int n_proj, const smlm_pool *pools, const smlm_batch *b, cons
     // the V tiles (shrink) get the rest, as many splits as fit (they must publish before the W
     // tiles finish their main loop)
     int best_ks = std::max(1, std::min(kmax, (pairs * 3 / 4) / std::max(NW, 1)));
-    if (const char *e = getenv("SMLM_DEC_KSPLIT")) best_ks = std::max(1, std::min(atoi(e), kmax));   // measurement
+    if (const char *e = getenv("SMLM_DEC_KSPLIT"))   // measurement / test override (read per call)
+        best_ks = std::max(1, std::min(atoi(e), kmax));
     while (best_ks > 1 && NW * best_ks + NV > pairs) --best_ks;   // (only with very many adapters)
     int best_ksv = NV ? std::max(1, std::min(kmax, (pairs - NW * best_ks) / NV)) : 1;
     if (NW * best_ks + NV * best_ksv > pairs) best_ks = 0;
@@ -411,7 +425,7 @@ Dec3Plan dec3_plan(int n_proj, const smlm_pool *pools, const smlm_batch *b, cons
     }
     D.kpart_off = off;
     off = align256(off + (size_t)D.clusters * 2 * 8 * kDec3ChunkBytes);
-    if (getenv("SMLM_DEC3_DEBUG")) off += 2 * kDec3MaxPairs * 16 * 8;   // phase timestamps at the tail
+    if (env_flag("SMLM_DEC3_DEBUG")) off += 2 * kDec3MaxPairs * 16 * 8;   // phase timestamps at the tail
     D.total = off;
     D.ok = true;
     return D;
@@ -524,7 +538,7 @@ int run_dec3(int n_proj, const smlm_pool *pools, const smlm_batch *b, const Dec3
     int rc;
     double t0 = g_hprof.on ? now_us() : 0;
     static thread_local Dec3Inline inl;   // kernel parameter block (copied at launch)
-    static const bool no_inline = getenv("SMLM_DEC3_NOINLINE") != nullptr;   // measurement override
+    const bool no_inline = env_flag("SMLM_DEC3_NOINLINE");   // measurement override
     const bool inline_plan = !no_inline;   // sizes are bounded by dec3_plan (<= 256 adapters, <= 512 rows)
     size_t rows_off = 0;
     if (inline_plan) {
@@ -579,8 +593,8 @@ int run_dec3(int n_proj, const smlm_pool *pools, const smlm_batch *b, const Dec3
     a.r = p0->r;
     a.r_pad = p0->r_pad;
     a.stages = dec3_stages();
-    if (const char *e = getenv("SMLM_DEC3_EXPT")) a.flags = atoi(e);
-    if (getenv("SMLM_DEC3_DEBUG"))
+    a.flags = env_int("SMLM_DEC3_EXPT");
+    if (env_flag("SMLM_DEC3_DEBUG"))
         a.dbg = reinterpret_cast<unsigned long long *>(wsb + D.total - 2 * kDec3MaxPairs * 16 * 8);
     double t2 = g_hprof.on ? now_us() : 0;
     {
@@ -965,7 +979,7 @@ int smlm_forward(smlm_pool p, const smlm_batch *b, const void *X, const void *W,
             g2.has_u = 1;
         }
         g2.blocks = d_blocks;
-        g2.defer = getenv("SMLM_NO_DEFER") ? 0 : 1;
+        g2.defer = env_flag("SMLM_NO_DEFER") ? 0 : 1;
         g2.slots = p->d_slots;
         g2.pairs = reinterpret_cast<const DevPair *>(wsb + L.plan_off + pair_off);
         g2.n_pairs = (int)pairs.size();
