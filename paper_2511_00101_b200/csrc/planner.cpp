@@ -7,7 +7,6 @@
 #include <math.h>
 
 #include <algorithm>
-#include <map>
 
 #include "plan.h"
 
@@ -88,6 +87,8 @@ int build_plan(const smlm_batch *b, int capacity, const uint8_t *slot_ok, const 
             for (int t = off[g]; t < off[g + 1]; ++t) cur.push_back({t, b->seg_slot[g], g});
         }
         if (!cur.empty()) runs.push_back(cur);
+        std::vector<int> idx;
+        idx.reserve(kTileM);
         for (auto &run : runs) {
             for (size_t i = 0; i < run.size(); i += kTileM) {
                 size_t n = std::min<size_t>(kTileM, run.size() - i);
@@ -98,17 +99,22 @@ int build_plan(const smlm_batch *b, int capacity, const uint8_t *slot_ok, const 
                 t.flags = kTileShort;
                 t.seg = -1;
                 t.blk0 = (int)p.blocks.size();
-                std::map<int, std::vector<const R *>> by_slot;  // ascending slot order
+                // adapter blocks: the tile's rows with a slot, stably sorted by slot (ascending slot,
+                // rows in run order inside a block) -- no per-slot containers
+                idx.clear();
                 for (size_t j = i; j < i + n; ++j)
-                    if (run[j].slot >= 0) by_slot[run[j].slot].push_back(&run[j]);
+                    if (run[j].slot >= 0) idx.push_back((int)j);
+                std::stable_sort(idx.begin(), idx.end(), [&](int x, int y) { return run[x].slot < run[y].slot; });
                 int tile_index = (int)p.short_tiles.size();
-                for (auto &kv : by_slot) {
+                for (size_t q = 0; q < idx.size();) {
+                    const int slot = run[idx[q]].slot;
                     DevBlock blk{};
-                    blk.slot = kv.first;
+                    blk.slot = slot;
                     blk.tile = tile_index;
                     blk.row_begin = (int)p.short_rows.size();
-                    blk.nrows = (int)kv.second.size();
-                    for (const R *r : kv.second) {
+                    size_t q2 = q;
+                    for (; q2 < idx.size() && run[idx[q2]].slot == slot; ++q2) {
+                        const R *r = &run[idx[q2]];
                         DevShortRow sr{};
                         sr.row = r->row;
                         sr.scale = eff(r->g);
@@ -116,7 +122,9 @@ int build_plan(const smlm_batch *b, int capacity, const uint8_t *slot_ok, const 
                         sr.pos = r->row - t.row0;
                         p.short_rows.push_back(sr);
                     }
+                    blk.nrows = (int)(q2 - q);
                     p.blocks.push_back(blk);
+                    q = q2;
                 }
                 t.nblk = (int)p.blocks.size() - t.blk0;
                 p.short_tiles.push_back(t);
