@@ -7,7 +7,7 @@ import torch
 import oracle
 import synth
 from oracle import plan as plan_oracle
-from synth import DECODE, FINETUNE, PREFILL
+from synth import DECODE, EVAL, FINETUNE, PREFILL
 from tests.util import BF16_TOL, parity_err
 
 pytestmark = pytest.mark.gpu
@@ -163,4 +163,47 @@ def test_launch_count_and_no_host_sync(S):
     assert not done.query()                           # the call returned before the GPU finished
     torch.cuda.synchronize()
     assert S.smlm_launch_count() - n0 >= 2
+    pool.close()
+
+
+def test_graph_capture_mixed_batch_forward_backward(S):
+    """A mixed batch (long tiles: plan uploaded through the pinned ring) recorded into a CUDA graph:
+    the captured plan upload reads its own pinned bytes, so replays reproduce the eager results
+    (forward Y and backward dX / dA / dB) bit for bit."""
+    lengths = [150, 3, 1, 70, 2]
+    modes = [FINETUNE, DECODE, DECODE, PREFILL, EVAL]
+    batch, w, X, dY = synth.random_case(5, 256, 192, 16, 3, lengths, modes, [0, 1, 2, 1, 0])
+    pool = S.Pool(256, 192, 16, 3, S.SMLM_BF16, 0)
+    A = [a.cuda() for a in w.A]
+    B = [b.cuda() for b in w.B]
+    for i in range(3):
+        pool.register(A[i], B[i], w.slot_scale[i])
+    dA = torch.zeros(3, 16, 256, device="cuda")
+    dB = torch.zeros(3, 192, 16, device="cuda")
+    for i in range(3):
+        pool.set_grad(i, dA[i], dB[i])
+    b = S.Batch.from_synth(batch)
+    Xd, Wd, dYd = X.cuda(), w.W.cuda(), dY.cuda()
+    Y = torch.empty(batch.S, 192, dtype=torch.bfloat16, device="cuda")
+    V = torch.zeros(batch.S, 16, dtype=torch.bfloat16, device="cuda")
+    dX = torch.zeros_like(Xd)
+    wsf = torch.empty(S.smlm_workspace_size(pool.h, b, False) + 256, dtype=torch.uint8, device="cuda")
+    wsb = torch.empty(S.smlm_workspace_size(pool.h, b, True) + 256, dtype=torch.uint8, device="cuda")
+
+    def step():
+        S.smlm_forward(pool.h, b, Xd, Wd, Y, V, wsf)
+        S.smlm_backward(pool.h, b, Xd, Wd, dYd, V, dX, 0, wsb)
+    step()
+    torch.cuda.synchronize()
+    ref = [t.clone() for t in (Y, dX, dA, dB)]
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        step()
+    for t in (Y, dX, dA, dB):
+        t.zero_()
+    g.replay()
+    g.replay()
+    torch.cuda.synchronize()
+    for t, r in zip((Y, dX, dA, dB), ref):
+        assert torch.equal(t, r)
     pool.close()
