@@ -423,3 +423,19 @@ def test_bf16_decode_graph_capture_replays_eager():
         assert torch.equal(y.float(), -e.float())
     for p in pools:
         p.close()
+
+
+@pytest.mark.parametrize("rows,n_ad,outs", [(256, 160, (512,)), (1, 4, (256, 128)), (512, 64, (512, 256, 256))])
+def test_bf16_decode_edge_shapes(rows, n_ad, outs):
+    """Decode edge cases: many adapters (13 stacked-A tiles), a single row, and 512 rows x 3
+    projections x 64 adapters (split factors drop to 1)."""
+    batch, ws_, X = _multi_case(rows * 3 + n_ad, 512, outs, 16, n_ad, rows, ft_rows=min(3, rows))
+    Ys, Vs, launches = _run_multi(batch, ws_, X)
+    assert launches == 1
+    ft = batch.ft_rows()
+    ft = ft[batch.row_slot()[ft] >= 0]
+    for i, w in enumerate(ws_):
+        Yr, Vr = oracle.forward(batch, w.W, w.A, w.B, w.slot_scale, X)
+        assert parity_err(Ys[i], Yr) <= BF16_TOL, i
+        if len(ft):
+            assert parity_err(Vs[i].double().numpy()[ft], Vr[ft]) <= BF16_TOL, i
