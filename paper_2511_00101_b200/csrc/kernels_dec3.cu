@@ -196,6 +196,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT3, 1) smlm_dec3_ke
         if (mine) s_ulist[off + __popc(bal & ((1u << lane) - 1u))] = u;
         if (threadIdx.x == 0) s_ucount = tot;
     }
+    if (active && it.vtile && warp == 3) {
+        // this CTA's stacked-adapter descriptors: fetch them while the prologue runs
+        const int u0 = it.n0 + (128 / RP) * (int)rank;
+        if (lane < 128 / RP && u0 + lane < a.n_uniq) tma_prefetch_desc(&P.slots[s_uslot[u0 + lane]].tmA);
+    }
     if (active && warp == 2) {
         asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(tmem_slot), "r"(256)
                      : "memory");

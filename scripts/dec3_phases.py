@@ -46,7 +46,7 @@ for proj in (os.environ.get("PROJ", "q,k").split(",")):
         col = rel[wm, k][t[wm, k] > 0]
         if len(col):
             out[name] = [round(float(np.min(col)), 2), round(float(np.median(col)), 2), round(float(np.max(col)), 2)]
-    for k, name in [(1, "v_loads_issued"), (4, "v_acc_ready"), (5, "v_arrived"), (6, "v_published")]:
+    for k, name in [(1, "v_loads_issued"), (4, "v_acc_ready"), (3, "v_parts_stored"), (5, "v_arrived"), (6, "v_published")]:
         col = rel[~wm, k][t[~wm, k] > 0]
         if len(col):
             out[name] = [round(float(np.min(col)), 2), round(float(np.median(col)), 2), round(float(np.max(col)), 2)]
