@@ -187,6 +187,32 @@ SMLM_API int smlm_plan(const smlm_batch *batch, int capacity, const uint8_t *slo
 SMLM_API int smlm_plan_export(smlm_pool pool, const smlm_batch *batch, int backward, int32_t *items,
                      int max_items, int *n_items);
 
+/*
+ * AdamW step over the fine-tune adapters' parameters (Table 5, P:1067:
+ * HF Trainer, learning_rate 2e-5; optimizer defaults = DESIGN.md R9; masking P:422 = the caller
+ * puts only the trained adapters' parameters in the buffer).  All buffers are DEVICE memory of n
+ * elements with the same flat layout (e.g. every trained adapter's A then B, concatenated):
+ *   param [n] fp32 master weights, exp_avg [n], exp_avg_sq [n] fp32 optimizer state -- updated;
+ *   grad [n] fp32 -- the (all-reduced) gradient sum; read, and zeroed if zero_grad != 0;
+ *   param_bf16 [n] bf16 or NULL -- receives bf16(param) after the update (the tensors the pools
+ *   borrow can be views of it, so the next forward sees the new weights).
+ * With t = step (>= 1) and g = grad * grad_scale:
+ *   if max_grad_norm > 0: g *= min(1, max_grad_norm / (||g||_2 + 1e-6))  (norm over the buffer)
+ *   param *= 1 - lr * weight_decay;  m = beta1 m + (1 - beta1) g;  v = beta2 v + (1 - beta2) g^2
+ *   param -= lr / (1 - beta1^t) * m / (sqrt(v) / sqrt(1 - beta2^t) + eps)
+ * fp32 arithmetic; the clip norm is reduced in a fixed order (bitwise reproducible).  Clipping
+ * needs ws of smlm_adamw_workspace_size() bytes (ws may be NULL otherwise).  Stream-ordered, no
+ * host synchronisation; 1 launch (2 with clipping).
+ * Errors: SMLM_E_INVALID (null/misaligned buffer: fp32 16-byte, bf16 8-byte; step < 1;
+ * hyper-parameter out of range), SMLM_E_WORKSPACE, SMLM_E_UNSUPPORTED (current device not
+ * sm_100), SMLM_E_CUDA.
+ */
+SMLM_API size_t smlm_adamw_workspace_size(void);
+SMLM_API int smlm_adamw_step(float *param, float *exp_avg, float *exp_avg_sq, float *grad, void *param_bf16,
+                             size_t n, int step, float lr, float beta1, float beta2, float eps,
+                             float weight_decay, float grad_scale, float max_grad_norm, int zero_grad,
+                             void *ws, size_t ws_bytes, void *stream);
+
 SMLM_API const char *smlm_status_string(int status);
 SMLM_API const char *smlm_last_error(void);
 
@@ -197,7 +223,7 @@ SMLM_API uint64_t smlm_launch_count(void);
  * CUDA events around its launches on the launching stream (0 disables; 1 = forward GEMM only;
  * 0xF = all).  smlm_profile_read synchronises those events and returns the summed milliseconds and
  * launch count for class `kind` (0 = forward GEMM, 1 = backward dX GEMM, 2 = short-row shrink,
- * 3 = dA/dB) since the last read, then resets that class.  Events between launches serialise
+ * 3 = dA/dB, 4 = AdamW step) since the last read, then resets that class.  Events between launches serialise
  * programmatic dependent launch, so enable only what is measured. */
 SMLM_API int smlm_profile_enable(int on);
 SMLM_API int smlm_profile_read(int kind, double *total_ms, int *count);

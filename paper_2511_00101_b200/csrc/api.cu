@@ -47,6 +47,9 @@ int launch_tok(const TokArgs &a, int num_sms, cudaStream_t st);
 int dec_chunks(int in_f);
 int dec3_stages();
 int launch_dec3(const Dec3Args &a, const Dec3Inline &in, int clusters, cudaStream_t st);
+int adamw_grid(int num_sms, size_t n);
+int launch_adamw_sumsq(const float *g, size_t n, float gscale, float *partial, int grid, cudaStream_t st);
+int launch_adamw_step(const AdamwArgs &a, int grid, cudaStream_t st);
 int launch_shrink_split(const __nv_bfloat16 *X, const SlotDev *slots, const DevBlock *blocks,
                         const DevShortRow *srows, int n_blocks, int in_f, int r, int r_pad, float *part,
                         __nv_bfloat16 *Vbd, __nv_bfloat16 *Vsave, cudaStream_t st);
@@ -71,6 +74,7 @@ static std::atomic<uint64_t> g_launches{0};
 
 // optional host-side phase timing (SMLM_HOST_PROF=1): microseconds per phase, printed at exit
 #include <chrono>
+#include <cmath>
 struct HostProf {
     bool on = getenv("SMLM_HOST_PROF") != nullptr;
     double t[8] = {0};
@@ -658,6 +662,79 @@ int smlm_profile_read(int kind, double *total_ms, int *count) {
     g_prof.recs.swap(keep);
     if (total_ms) *total_ms = tot;
     if (count) *count = n;
+    return SMLM_OK;
+}
+
+// ---- AdamW step over the fine-tune adapters' flat parameters ----
+static int current_sm100_sms(int *num_sms) {
+    static thread_local int cached_dev = -1, cached_sms = 0;
+    int dev = -1;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return set_err(SMLM_E_UNSUPPORTED, "no CUDA device (there is no CPU fallback)");
+    if (dev != cached_dev) {
+        cudaDeviceProp prop;
+        CK(cudaGetDeviceProperties(&prop, dev));
+        if (prop.major != 10 || prop.minor != 0)
+            return set_err(SMLM_E_UNSUPPORTED, "device is not sm_100 (B200); this library is sm_100a-only");
+        cached_dev = dev;
+        cached_sms = prop.multiProcessorCount;
+    }
+    *num_sms = cached_sms;
+    return SMLM_OK;
+}
+
+size_t smlm_adamw_workspace_size(void) {
+    int sms = 0;
+    if (current_sm100_sms(&sms) != SMLM_OK) return 0;
+    return (size_t)sms * 8 * sizeof(float);
+}
+
+int smlm_adamw_step(float *param, float *exp_avg, float *exp_avg_sq, float *grad, void *param_bf16, size_t n,
+                    int step, float lr, float beta1, float beta2, float eps, float weight_decay, float grad_scale,
+                    float max_grad_norm, int zero_grad, void *ws, size_t ws_bytes, void *stream) {
+    if (n == 0) return SMLM_OK;
+    if (!param || !exp_avg || !exp_avg_sq || !grad) return set_err(SMLM_E_INVALID, "adamw: null buffer");
+    if (step < 1) return set_err(SMLM_E_INVALID, "adamw: step must be >= 1");
+    if (!(lr >= 0.f) || !(beta1 >= 0.f && beta1 < 1.f) || !(beta2 >= 0.f && beta2 < 1.f) || !(eps > 0.f) ||
+        !(weight_decay >= 0.f) || !std::isfinite(grad_scale) || !std::isfinite(max_grad_norm))
+        return set_err(SMLM_E_INVALID, "adamw: hyper-parameter out of range");
+    auto al = [](const void *q, size_t b) { return (reinterpret_cast<uintptr_t>(q) % b) == 0; };
+    if (!al(param, 16) || !al(exp_avg, 16) || !al(exp_avg_sq, 16) || !al(grad, 16) || (param_bf16 && !al(param_bf16, 8)))
+        return set_err(SMLM_E_INVALID, "adamw: fp32 buffers must be 16-byte and the bf16 copy 8-byte aligned");
+    int sms = 0, rc;
+    if ((rc = current_sm100_sms(&sms))) return rc;
+    cudaStream_t st = (cudaStream_t)stream;
+    const int grid = adamw_grid(sms, n);
+    AdamwArgs a;
+    a.p = param;
+    a.m = exp_avg;
+    a.v = exp_avg_sq;
+    a.g = grad;
+    a.pb = reinterpret_cast<uint16_t *>(param_bf16);
+    a.n = n;
+    a.decay = (float)(1.0 - (double)lr * weight_decay);
+    a.step_size = (float)((double)lr / (1.0 - std::pow((double)beta1, step)));
+    a.inv_bc2_sqrt = (float)(1.0 / std::sqrt(1.0 - std::pow((double)beta2, step)));
+    a.beta1 = beta1;
+    a.beta2 = beta2;
+    a.eps = eps;
+    a.gscale = grad_scale;
+    a.max_norm = max_grad_norm;
+    a.zero_grad = zero_grad ? 1 : 0;
+    a.partial = nullptr;
+    a.n_partial = 0;
+    if (max_grad_norm > 0.f) {
+        if (!ws || !al(ws, 4) || ws_bytes < (size_t)grid * sizeof(float))
+            return set_err(SMLM_E_WORKSPACE, "adamw: clipping needs smlm_adamw_workspace_size() bytes of workspace");
+        ProfScope ps(4, st);
+        CKL(launch_adamw_sumsq(grad, n, grad_scale, reinterpret_cast<float *>(ws), grid, st), 1);
+        a.partial = reinterpret_cast<const float *>(ws);
+        a.n_partial = grid;
+    }
+    {
+        ProfScope ps(4, st);
+        CKL(launch_adamw_step(a, grid, st), 1);
+    }
     return SMLM_OK;
 }
 

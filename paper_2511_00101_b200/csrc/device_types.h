@@ -190,6 +190,20 @@ struct Dec3Inline {
     int uslot[kDec3InlineSlots];
     Dec3RowInfo rows[kDec3InlineRows];
 };
+// AdamW step over a flat fp32 parameter buffer (kernels_opt.cu)
+struct AdamwArgs {
+    float *p, *m, *v, *g;
+    uint16_t *pb;        // optional bf16 copy of the updated parameters
+    size_t n;
+    float decay;         // 1 - lr * weight_decay
+    float step_size;     // lr / (1 - beta1^t)
+    float inv_bc2_sqrt;  // 1 / sqrt(1 - beta2^t)
+    float beta1, beta2, eps, gscale, max_norm;
+    int zero_grad;
+    const float *partial;   // per-CTA sum(g^2) of the clip pass, or nullptr
+    int n_partial;
+};
+
 constexpr int kDec3ChunkBytes = 128 * 32 * 4;   // one 32-column fp32 chunk of a CTA accumulator
 constexpr int dec3_counter_ints() { return 2 + 2 * 128 + 62; }
 

@@ -20,14 +20,14 @@ SMLM_OK, SMLM_E_INVALID, SMLM_E_SHAPE, SMLM_E_SLOT, SMLM_E_CAPACITY, SMLM_E_CUDA
 SMLM_FINETUNE, SMLM_EVAL, SMLM_PREFILL, SMLM_DECODE = range(4)
 SMLM_BF16, SMLM_FP32 = 0, 1
 SMLM_OPT_L_LONG, SMLM_OPT_CTA_PAIR = 0, 1
-PROF_FWD_GEMM, PROF_BWD_GEMM, PROF_SHRINK, PROF_DADB = range(4)
+PROF_FWD_GEMM, PROF_BWD_GEMM, PROF_SHRINK, PROF_DADB, PROF_ADAMW = range(5)
 
 EXPORTED = [
     "smlm_pool_create", "smlm_pool_destroy", "smlm_pool_set_option", "smlm_adapter_register",
     "smlm_adapter_set_grad", "smlm_adapter_unregister", "smlm_workspace_size", "smlm_forward",
     "smlm_backward", "smlm_plan", "smlm_plan_export", "smlm_status_string", "smlm_last_error",
     "smlm_launch_count", "smlm_profile_enable", "smlm_profile_read", "smlm_workspace_size_multi",
-    "smlm_forward_multi",
+    "smlm_forward_multi", "smlm_adamw_workspace_size", "smlm_adamw_step",
 ]
 
 
@@ -68,6 +68,8 @@ def _load():
         "smlm_launch_count": ([], ctypes.c_uint64),
         "smlm_profile_enable": ([I], I),
         "smlm_profile_read": ([I, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(I)], I),
+        "smlm_adamw_workspace_size": ([], Z),
+        "smlm_adamw_step": ([P, P, P, P, P, Z, I] + [ctypes.c_float] * 7 + [I, P, Z, P], I),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)
@@ -218,6 +220,24 @@ def smlm_plan_export(pool: int, batch: Batch, backward: bool = False):
     return buf[:n.value].tolist()
 
 
+def smlm_adamw_workspace_size() -> int:
+    return int(_lib.smlm_adamw_workspace_size())
+
+
+def smlm_adamw_step(param, exp_avg, exp_avg_sq, grad, param_bf16, step: int, lr: float, beta1: float = 0.9,
+                    beta2: float = 0.999, eps: float = 1e-8, weight_decay: float = 0.0, grad_scale: float = 1.0,
+                    max_grad_norm: float = 0.0, zero_grad: bool = False, ws=None, stream=None):
+    """AdamW over flat fp32 buffers of n elements (include/smlm.h smlm_adamw_step)."""
+    n = param.numel()
+    for t in (exp_avg, exp_avg_sq, grad) + (() if param_bf16 is None else (param_bf16,)):
+        if t.numel() != n:
+            raise ValueError("smlm_adamw_step: every buffer must have param.numel() elements")
+    _check(_lib.smlm_adamw_step(_ptr(param), _ptr(exp_avg), _ptr(exp_avg_sq), _ptr(grad), _ptr(param_bf16), n,
+                                int(step), lr, beta1, beta2, eps, weight_decay, grad_scale, max_grad_norm,
+                                int(bool(zero_grad)), _ptr(ws), 0 if ws is None else ws.numel() * ws.element_size(),
+                                _stream(stream, param.device)), "smlm_adamw_step")
+
+
 def smlm_launch_count() -> int:
     return int(_lib.smlm_launch_count())
 
@@ -225,7 +245,7 @@ def smlm_launch_count() -> int:
 def smlm_profile_enable(mask):
     """Bitmask of kernel classes to time (bool True = all classes)."""
     if isinstance(mask, bool):
-        mask = 0xF if mask else 0
+        mask = 0x1F if mask else 0
     _lib.smlm_profile_enable(int(mask))
 
 

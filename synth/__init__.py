@@ -236,3 +236,25 @@ def sample_rows(batch: Batch, every: int = 37) -> np.ndarray:
             rows.add(a)
             rows.add(b - 1)
     return np.array(sorted(rows), np.int64)
+
+
+def lora_param_count(rank: int, projections: Sequence[str] = tuple(PROJECTIONS)) -> int:
+    """Elements of one adapter's A and B over the given Llama-3-8B projections (no arithmetic of the
+    method: shapes only)."""
+    return sum(rank * PROJ_SHAPES[p][0] + PROJ_SHAPES[p][1] * rank for p in projections)
+
+
+def draw_adamw_state(seed: int, n: int, step: int = 1):
+    """Seeded fp32 AdamW inputs of n elements (CPU tensors): parameters ~ N(0, 0.02) (the
+    gaussian LoRA init scale), a gradient sum ~ N(0, 1e-3), and, for step > 1, moments of a run
+    in progress (exp_avg ~ N(0, 1e-4), exp_avg_sq ~ |N(0, 1e-6)|)."""
+    g = torch.Generator().manual_seed(seed)
+    p = torch.randn(n, generator=g) * 0.02
+    grad = torch.randn(n, generator=g) * 1e-3
+    if step > 1:
+        m = torch.randn(n, generator=g) * 1e-4
+        v = (torch.randn(n, generator=g) * 1e-6).abs()
+    else:
+        m = torch.zeros(n)
+        v = torch.zeros(n)
+    return p, m, v, grad

@@ -1,0 +1,160 @@
+"""GPU parity of the AdamW step (kernels_opt.cu) against the fp64 oracle
+(oracle/adamw.py), through the C ABI (smlm_adamw_step).
+
+Tolerance (R9): the kernel computes in fp32, so parameters and moments must agree with
+the fp64 oracle to rtol 2e-5 (a few fp32 ulps through ~10 dependent operations, plus the fp32
+sum of squares of the clip pass); the bf16 working copy must equal bf16(fp32 parameter) exactly
+and the oracle to within one bf16 ulp.  The clip coefficient and everything else is bitwise
+reproducible run to run."""
+import numpy as np
+import pytest
+import torch
+
+import synth
+from oracle import adamw as OA
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def S():
+    from paper_2511_00101_b200 import smlm
+    return smlm
+
+
+def _run(S, p, m, v, g, t, with_bf16=True, ws=True, **hp):
+    dev = torch.device("cuda", 0)
+    P, M, V, G = (x.clone().to(dev) for x in (p, m, v, g))
+    PB = torch.empty(p.numel(), dtype=torch.bfloat16, device=dev) if with_bf16 else None
+    W = torch.empty(max(S.smlm_adamw_workspace_size() // 4, 1), dtype=torch.float32, device=dev) if ws else None
+    S.smlm_adamw_step(P, M, V, G, PB, t, ws=W, **hp)
+    torch.cuda.synchronize()
+    return P.cpu(), M.cpu(), V.cpu(), G.cpu(), None if PB is None else PB.cpu()
+
+
+def _check(out, ref, inp, gscale=1.0, lr=0.0, wd=0.0, beta1=0.9, tol=2e-5):
+    """Elementwise |got - oracle| <= tol * (magnitude of the terms that form the result): the
+    parameter update can cancel the decayed parameter, so the bound uses |p decay| + |update|."""
+    P, M, V = (x.double().numpy() for x in out[:3])
+    p, m, v = ref
+    p0, m0, _, g = (np.asarray(x, np.float64) for x in inp)
+    decayed = p0 * (1.0 - lr * wd)
+    sp = np.abs(decayed) + np.abs(p - decayed)
+    sm = beta1 * np.abs(m0) + (1.0 - beta1) * np.abs(g) * gscale
+    for got, exp, sc in ((P, p, sp), (M, m, sm), (V, v, np.abs(v))):
+        bad = np.abs(got - exp) > tol * sc + 1e-30
+        assert not bad.any(), (np.flatnonzero(bad)[:5], got[bad][:5], exp[bad][:5])
+
+
+@pytest.mark.parametrize("n", [1, 3, 4, 1001, 65536 + 5, 3 * 2**20 + 3])
+@pytest.mark.parametrize("t", [1, 7])
+def test_adamw_parity(S, n, t):
+    p, m, v, g = synth.draw_adamw_state(n + 17 * t, n, step=t)
+    hp = dict(lr=2e-5, beta1=0.9, beta2=0.999, eps=1e-8, weight_decay=0.01, grad_scale=0.25, max_grad_norm=0.0)
+    out = _run(S, p, m, v, g, t, **hp)
+    ref = OA.adamw_step(p.numpy(), m.numpy(), v.numpy(), g.numpy(), t, 2e-5, 0.9, 0.999, 1e-8, 0.01, 0.25, 0.0)
+    _check(out, ref, (p, m, v, g), gscale=0.25, lr=2e-5, wd=0.01)
+    # bf16 copy: exactly the conversion of the kernel's own fp32, within 1 ulp of the oracle's
+    assert torch.equal(out[4], out[0].to(torch.bfloat16))
+    ref_b = torch.from_numpy(ref[0]).to(torch.float32).to(torch.bfloat16).float()
+    ulp = torch.from_numpy(np.abs(ref[0])).float().clamp_min(1e-30) * 2.0 ** -7
+    assert bool(((out[4].float() - ref_b).abs() <= ulp).all())
+    assert torch.equal(out[3], g)   # zero_grad off: gradient untouched
+
+
+@pytest.mark.parametrize("max_norm", [1.0, 1e-3, 1e6])
+def test_adamw_clip(S, max_norm):
+    n = 2**20 + 9
+    p, m, v, g = synth.draw_adamw_state(3, n, step=3)
+    g = g * 10.0   # ||g|| ~ 10 so max_norm 1 and 1e-3 clip, 1e6 does not
+    hp = dict(lr=1e-3, beta1=0.9, beta2=0.999, eps=1e-8, weight_decay=0.0, grad_scale=0.5, max_grad_norm=max_norm,
+              zero_grad=True)
+    out = _run(S, p, m, v, g, 3, **hp)
+    ref = OA.adamw_step(p.numpy(), m.numpy(), v.numpy(), g.numpy(), 3, 1e-3, 0.9, 0.999, 1e-8, 0.0, 0.5, max_norm)
+    _check(out, ref, (p, m, v, g), gscale=0.5, lr=1e-3)
+    assert bool((out[3] == 0).all())   # zero_grad
+    # bitwise reproducible (fixed reduction order)
+    out2 = _run(S, p, m, v, g, 3, **hp)
+    for a, b in zip(out[:3], out2[:3]):
+        assert torch.equal(a, b)
+
+
+def test_adamw_multistep_matches_oracle(S):
+    """Five steps with the moments carried on the device (state never leaves the GPU)."""
+    n = 40000 + 3
+    p, m, v, _ = synth.draw_adamw_state(11, n, step=1)
+    dev = torch.device("cuda", 0)
+    P, M, V = p.to(dev), m.to(dev), v.to(dev)
+    G = torch.empty(n, device=dev)
+    W = torch.empty(S.smlm_adamw_workspace_size() // 4, device=dev)
+    rp, rm, rv = p.numpy(), m.numpy(), v.numpy()
+    for t in range(1, 6):
+        g = synth.draw_adamw_state(100 + t, n)[3]
+        G.copy_(g)
+        S.smlm_adamw_step(P, M, V, G, None, t, 2e-5, weight_decay=0.1, max_grad_norm=1.0, ws=W)
+        inp = (rp, rm, rv, g.numpy())
+        rp, rm, rv = OA.adamw_step(rp, rm, rv, g.numpy(), t, 2e-5, weight_decay=0.1, max_norm=1.0)
+        torch.cuda.synchronize()
+        # compare every step (the device state carries the kernel's own rounding forward)
+        _check((P.cpu(), M.cpu(), V.cpu()), (rp, rm, rv), inp, lr=2e-5, wd=0.1, tol=5e-5)
+        rp, rm, rv = (x.cpu().double().numpy() for x in (P, M, V))
+
+
+def test_adamw_errors(S):
+    dev = torch.device("cuda", 0)
+    x = torch.zeros(64, device=dev)
+    with pytest.raises(S.SmlmError) as e:
+        S.smlm_adamw_step(x, x.clone(), x.clone(), x.clone(), None, 0, 1e-3)           # step 0
+    assert e.value.code == S.SMLM_E_INVALID
+    with pytest.raises(S.SmlmError) as e:
+        S.smlm_adamw_step(x, x.clone(), x.clone(), x.clone(), None, 1, 1e-3, beta1=1.0)
+    assert e.value.code == S.SMLM_E_INVALID
+    with pytest.raises(S.SmlmError) as e:
+        S.smlm_adamw_step(x[1:], x.clone()[1:], x.clone()[1:], x.clone()[1:], None, 1, 1e-3)   # misaligned
+    assert e.value.code == S.SMLM_E_INVALID
+    with pytest.raises(S.SmlmError) as e:
+        S.smlm_adamw_step(x, x.clone(), x.clone(), x.clone(), None, 1, 1e-3, max_grad_norm=1.0)   # no workspace
+    assert e.value.code == S.SMLM_E_WORKSPACE
+    # n = 0 is a no-op
+    e0 = torch.zeros(0, device=dev)
+    S.smlm_adamw_step(e0, e0, e0, e0, None, 1, 1e-3)
+
+
+def test_adapter_params_train_step(S):
+    """optim.AdapterParams + AdamW: the SMLM backward writes dA/dB into the flat gradient, one
+    AdamW launch updates the master weights, and the pool sees the new bf16 values."""
+    from paper_2511_00101_b200.optim import AdapterParams, AdamW
+    in_f, out_f, r = 256, 192, 16
+    gen = torch.Generator().manual_seed(5)
+    w = synth.draw_weights(gen, in_f, out_f, r, 2)
+    dev = torch.device("cuda", 0)
+    store = AdapterParams([(r, in_f, out_f)] * 2, device=dev)
+    for k in range(2):
+        store.load(k, w.A[k].float(), w.B[k].float())
+    pool = S.Pool(in_f, out_f, r, 4, S.SMLM_BF16, 0)
+    slots = [pool.register(store.A(k), store.B(k), 2.0) for k in range(2)]
+    for k, sl in enumerate(slots):
+        pool.set_grad(sl, store.dA(k), store.dB(k))
+    batch = synth.batch_from_lengths([40, 24], slots, [synth.FINETUNE] * 2)
+    b = S.Batch.from_synth(batch)
+    X = torch.randn(64, in_f, generator=gen).to(torch.bfloat16).to(dev)
+    W = (torch.randn(out_f, in_f, generator=gen) / 16).to(torch.bfloat16).to(dev)
+    dY = torch.randn(64, out_f, generator=gen).to(torch.bfloat16).to(dev)
+    V = torch.empty(64, r, dtype=torch.bfloat16, device=dev)
+    Y = pool.forward(b, X, W, V_save=V)
+    pool.backward(b, X, W, dY, V, None)
+    g_host = store.grad.cpu().clone()
+    p_host = store.master.cpu().clone()
+    opt = AdamW(store, lr=1e-3, max_grad_norm=1.0)
+    opt.step()
+    torch.cuda.synchronize()
+    ref_p, _, _ = OA.adamw_step(p_host.numpy(), np.zeros(store.n), np.zeros(store.n), g_host.numpy(), 1, 1e-3,
+                                max_norm=1.0)
+    _check((store.master.cpu(), torch.zeros(store.n), torch.zeros(store.n)), (ref_p, np.zeros(store.n), np.zeros(store.n)),
+           (p_host.numpy(), np.zeros(store.n), None, g_host.numpy()), lr=1e-3)
+    assert bool((store.grad == 0).all())
+    assert torch.equal(store.bf16, store.master.to(torch.bfloat16))
+    # the next forward uses the updated adapter (borrowed bf16 views)
+    Y2 = pool.forward(b, X, W)
+    assert not torch.equal(Y, Y2)
+    pool.close()
