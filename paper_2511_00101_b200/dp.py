@@ -44,18 +44,22 @@ class AllReduce:
         self.cuda = torch.device(device).type == "cuda"
         self.stream = torch.cuda.Stream(device) if self.cuda else None
 
-    def __call__(self, bucket: GradBucket, main_stream=None):
+    def __call__(self, bucket, main_stream=None):
+        """bucket: a GradBucket, an optim.AdapterParams (its flat gradient) or a flat tensor."""
+        flat = bucket if isinstance(bucket, torch.Tensor) else getattr(bucket, "flat", None)
+        if flat is None:
+            flat = bucket.grad
         if self.dist is None:
             return
         if not self.cuda:
-            self.dist.all_reduce(bucket.flat, op=self.dist.ReduceOp.SUM)
+            self.dist.all_reduce(flat, op=self.dist.ReduceOp.SUM)
             return
-        main = main_stream or torch.cuda.current_stream(bucket.flat.device)
+        main = main_stream or torch.cuda.current_stream(flat.device)
         ev = torch.cuda.Event()
         ev.record(main)
         self.stream.wait_event(ev)
         with torch.cuda.stream(self.stream):
-            self.dist.all_reduce(bucket.flat, op=self.dist.ReduceOp.SUM)
+            self.dist.all_reduce(flat, op=self.dist.ReduceOp.SUM)
 
     def join(self, main_stream=None):
         """Make the main stream wait for every issued all-reduce."""

@@ -87,3 +87,66 @@ def test_dp_allreduce_equals_union_oracle():
         ref.dB(i).copy_(torch.from_numpy(dB[s]))
     assert torch.allclose(flats[0].double(), ref.flat.double(), rtol=1e-6, atol=1e-6)
     assert flats[0].abs().sum() > 0
+
+
+def _worker_opt(rank, world, port, out_dir):
+    """Masked DP training step: each rank's fine-tune gradient goes into the flat AdapterParams
+    gradient (the layout the GPU optimizer uses), one all-reduce, then the AdamW update of the
+    mean gradient -- applied here with the oracle (the CUDA step is covered by test_gpu_adamw)."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import oracle
+    from oracle import adamw as OA
+    from paper_2511_00101_b200.dp import AllReduce
+    from paper_2511_00101_b200.optim import AdapterParams
+    w = _weights()
+    b, X, dY = _rank_batch(rank)
+    _, dA, dB = oracle.backward(b, w.W, w.A, w.B, w.slot_scale, X, dY)
+    store = AdapterParams([(R, IN, OUT)] * len(FT_SLOTS), device="cpu")
+    for i, s in enumerate(FT_SLOTS):
+        store.load(i, w.A[s].float(), w.B[s].float())
+        store.dA(i).copy_(torch.from_numpy(dA[s]))
+        store.dB(i).copy_(torch.from_numpy(dB[s]))
+    AllReduce(dist, "cpu")(store)
+    p, _, _ = OA.adamw_step(store.master.numpy(), np.zeros(store.n), np.zeros(store.n), store.grad.numpy(), 1, 1e-3,
+                            grad_scale=1.0 / world, max_norm=1.0)
+    torch.save({"grad": store.grad, "p": torch.from_numpy(p)}, os.path.join(out_dir, f"opt{rank}.pt"))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_dp_flat_adapter_params_step():
+    import oracle
+    from paper_2511_00101_b200.optim import AdapterParams
+    oracle.build()
+    world = 2
+    # layout: 8-element (16-byte) aligned pieces, disjoint views covering the buffer's data
+    store = AdapterParams([(R, IN, OUT), (8, 64, 24)], device="cpu")
+    assert all(a % 8 == 0 and b % 8 == 0 for a, b in store.offsets)
+    assert store.dA(0).shape == (R, IN) and store.dB(1).shape == (24, 8) and store.A(1).dtype == torch.bfloat16
+    store.grad.fill_(0)
+    for k in range(2):
+        store.dA(k).fill_(1.0)
+        store.dB(k).fill_(1.0)
+    assert int(store.grad.sum()) == R * IN + OUT * R + 8 * 64 + 24 * 8
+    with tempfile.TemporaryDirectory() as d:
+        mp.spawn(_worker_opt, args=(world, _free_port(), d), nprocs=world, join=True)
+        res = [torch.load(os.path.join(d, f"opt{r}.pt")) for r in range(world)]
+    assert torch.equal(res[0]["grad"], res[1]["grad"]) and torch.equal(res[0]["p"], res[1]["p"])
+    # the reduced flat gradient is the union-of-rows oracle gradient in the AdapterParams layout
+    w = _weights()
+    parts = [_rank_batch(r) for r in range(world)]
+    lengths, slots, modes = [], [], []
+    for b, _, _ in parts:
+        lengths += np.diff(b.offsets).tolist()
+        slots += b.slots.tolist()
+        modes += b.modes.tolist()
+    ub = synth.batch_from_lengths(lengths, slots, modes)
+    _, dA, dB = oracle.backward(ub, w.W, w.A, w.B, w.slot_scale, torch.cat([p[1] for p in parts]),
+                                torch.cat([p[2] for p in parts]))
+    ref = AdapterParams([(R, IN, OUT)] * len(FT_SLOTS), device="cpu")
+    for i, s in enumerate(FT_SLOTS):
+        ref.dA(i).copy_(torch.from_numpy(dA[s]))
+        ref.dB(i).copy_(torch.from_numpy(dB[s]))
+    assert torch.allclose(res[0]["grad"].double(), ref.grad.double(), rtol=1e-6, atol=1e-6)
