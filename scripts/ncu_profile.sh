@@ -24,3 +24,5 @@ ls -la $OUT
 $NCU --set full --clock-control none --import-source on -k regex:smlm_dec3 -s 2 -c 1 -o $OUT/prof_dec3_q -f env PROJ=q N=3 python scripts/run_c2_once.py > /dev/null 2>&1
 $NCU --set full --clock-control none --import-source on -k regex:smlm_dec3 -s 2 -c 1 -o $OUT/prof_dec3_qkv -f python scripts/dec_layer_phases.py > /dev/null 2>&1
 $NCU --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file $OUT/dec_launches.csv python scripts/bench_configs.py --c2-only > /dev/null 2>&1
+# AdamW step (kernels_opt.cu): duration + DRAM bytes of both passes at the 32-layer size
+$NCU --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -k regex:adamw -c 8 --csv --log-file $OUT/adamw_launches.csv python scripts/adamw_bench.py > /dev/null 2>&1
