@@ -181,6 +181,37 @@ def c2_layer_step(iters=40, graphs=True):
             "hbm_roofline_frac_graph": None if ms_graph is None else roof_ms / ms_graph}
 
 
+def adamw_step(layers=32, clip=1.0, iters=20):
+    """AdamW over the C4 fine-tune adapters (4 adapters, r=16, 7 projections) of
+    `layers` layers (kernels_opt.cu).  34 algorithmic bytes/element (+4 with the clip pass);
+    L2 flushed before every launch."""
+    peaks = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                                        "MEASURED_PEAKS.json")))
+    hbm = float(peaks["hbm_gbs"])
+    dev = torch.device("cuda", 0)
+    n = 4 * synth.lora_param_count(16) * layers
+    P, M, V, G = (torch.randn(n, device=dev) * 1e-3 for _ in range(4))
+    V.abs_()
+    PB = torch.empty(n, dtype=torch.bfloat16, device=dev)
+    Wk = torch.empty(S.smlm_adamw_workspace_size() // 4, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    ts = []
+    for it in range(iters + 3):
+        flush.zero_()
+        a, b = torch.cuda.Event(True), torch.cuda.Event(True)
+        a.record()
+        S.smlm_adamw_step(P, M, V, G, PB, it + 1, 2e-5, max_grad_norm=clip, zero_grad=True, ws=Wk)
+        b.record()
+        b.synchronize()
+        if it >= 3:
+            ts.append(a.elapsed_time(b))
+    ms = statistics.median(ts)
+    byts = n * (34 + (4 if clip > 0 else 0))
+    del P, M, V, G, PB, flush
+    return {"kernel": "smlm_adamw_step", "layers": layers, "n": n, "clip": clip, "ms": ms, "alg_bytes": byts,
+            "GB/s": byts / ms / 1e6, "hbm_peak_GB/s": hbm, "frac": byts / ms / 1e6 / hbm}
+
+
 def main():
     print(json.dumps(c2_layer_step(graphs="--c2-only" not in sys.argv)), flush=True)
     if "--c2-only" in sys.argv:
