@@ -76,9 +76,17 @@ def _ptr(a: Optional[np.ndarray]):
 
 
 def _stack(mats, shape):
+    """[U, *shape] fp64.  Adapters of a smaller rank (heterogeneous ranks) are
+    zero-padded to the largest rank: A_a gets zero rows, B_a zero columns.  Exact: a padded rank
+    index j contributes B[:, j] (A[j] x) = 0 to y, U_j = B[:, j]^T dy = 0, so dA_a[j] = 0 and
+    dB_a[:, j] = s dy (A[j] x) = 0 -- the padded entries are exact zeros and the rest is unchanged."""
     if len(mats) == 0:
         return np.zeros((1,) + shape, np.float64)
-    return np.ascontiguousarray(np.stack([_f64(m) for m in mats]))
+    out = np.zeros((len(mats),) + shape, np.float64)
+    for i, m in enumerate(mats):
+        md = _f64(m)
+        out[i, :md.shape[0], :md.shape[1]] = md
+    return out
 
 
 def _batch_arrays(batch):
@@ -102,7 +110,7 @@ def forward(batch, W, A, B, slot_scale, X, rows=None, Y_in=None):
     S, in_f = Xd.shape
     Wd = None if W is None else _f64(W)
     out_f = Wd.shape[0] if Wd is not None else _f64(Y_in).shape[1]
-    r = _f64(A[0]).shape[0] if len(A) else 1
+    r = max(_f64(a).shape[0] for a in A) if len(A) else 1   # largest rank (heterogeneous ranks padded)
     assert r <= 256
     Ad = _stack(A, (r, in_f))
     Bd = _stack(B, (out_f, r))
@@ -121,14 +129,15 @@ def forward(batch, W, A, B, slot_scale, X, rows=None, Y_in=None):
 
 def backward(batch, W, A, B, slot_scale, X, dY, has_grad=None, rows=None, dA_in=None, dB_in=None,
              accumulate=False, want_dx=True):
-    """Fine-tune backward in fp64.  Returns (dX [S,in] (zeros on non-FT rows), dA [U,r,in], dB [U,out,r])."""
+    """Fine-tune backward in fp64.  Returns (dX [S,in] (zeros on non-FT rows), dA [U,r,in], dB [U,out,r]);
+    r is the largest adapter rank: adapter a's gradients are dA[a, :r_a] and dB[a, :, :r_a]."""
     lib = _load()
     Xd, dYd = _f64(X), _f64(dY)
     S, in_f = Xd.shape
     out_f = dYd.shape[1]
     Wd = None if W is None else _f64(W)
     U = len(A)
-    r = _f64(A[0]).shape[0] if U else 1
+    r = max(_f64(a).shape[0] for a in A) if U else 1
     Ad = _stack(A, (r, in_f))
     Bd = _stack(B, (out_f, r))
     sl = np.ascontiguousarray(np.asarray(slot_scale if U else [0.0], np.float64))

@@ -258,3 +258,45 @@ def test_row_sampling_matches_full():
     dXf, _, _ = oracle.backward(batch, w.W, w.A, w.B, w.slot_scale, X, dY)
     dXs, _, _ = oracle.backward(batch, w.W, w.A, w.B, w.slot_scale, X, dY, rows=rows)
     assert np.array_equal(dXs[rows], dXf[rows])
+
+
+def test_heterogeneous_ranks_brute_force():
+    """SURVEY §8 f2 (heterogeneous ranks in one layer): the zero-padded oracle equals a
+    per-row numpy evaluation with each adapter's own rank, and the padded gradient entries are 0."""
+    rng = np.random.default_rng(3)
+    in_f, out_f, ranks = 12, 10, [4, 8, 2]
+    W = rng.standard_normal((out_f, in_f))
+    A = [rng.standard_normal((r, in_f)) for r in ranks]
+    B = [rng.standard_normal((out_f, r)) for r in ranks]
+    ss = [0.5, 2.0, -1.5]
+    lengths, slots, modes = [3, 2, 4, 1, 2], [0, 1, 2, -1, 1], [FINETUNE, DECODE, FINETUNE, PREFILL, FINETUNE]
+    batch = synth.batch_from_lengths(lengths, slots, modes, [1.0, 1.0, 0.5, 1.0, 2.0])
+    X = rng.standard_normal((batch.S, in_f))
+    dY = rng.standard_normal((batch.S, out_f))
+    Y, _ = oracle.forward(batch, torch.tensor(W), [torch.tensor(a) for a in A], [torch.tensor(b) for b in B], ss,
+                          torch.tensor(X))
+    dX, dA, dB = oracle.backward(batch, torch.tensor(W), [torch.tensor(a) for a in A], [torch.tensor(b) for b in B],
+                                 ss, torch.tensor(X), torch.tensor(dY))
+    Yb = X @ W.T
+    dXb = np.zeros_like(X)
+    dAb = [np.zeros_like(a) for a in A]
+    dBb = [np.zeros_like(b) for b in B]
+    for g in range(batch.G):
+        a = slots[g]
+        for t in range(batch.offsets[g], batch.offsets[g + 1]):
+            if a >= 0:
+                s = ss[a] * batch.seg_scale[g]
+                Yb[t] += s * B[a] @ (A[a] @ X[t])
+            if modes[g] == FINETUNE:
+                dXb[t] = W.T @ dY[t]
+                if a >= 0:
+                    u = B[a].T @ dY[t]
+                    dXb[t] += s * A[a].T @ u
+                    dAb[a] += s * np.outer(u, X[t])
+                    dBb[a] += s * np.outer(dY[t], A[a] @ X[t])
+    np.testing.assert_allclose(Y, Yb, rtol=1e-12, atol=1e-12)
+    np.testing.assert_allclose(dX, dXb, rtol=1e-12, atol=1e-12)
+    for a, r in enumerate(ranks):
+        np.testing.assert_allclose(dA[a, :r], dAb[a], rtol=1e-12, atol=1e-12)
+        np.testing.assert_allclose(dB[a, :, :r], dBb[a], rtol=1e-12, atol=1e-12)
+        assert np.all(dA[a, r:] == 0) and np.all(dB[a, :, r:] == 0)
