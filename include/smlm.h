@@ -105,8 +105,18 @@ SMLM_API int smlm_pool_set_option(smlm_pool pool, int option, int value);
  */
 SMLM_API int smlm_adapter_register(smlm_pool pool, const void *A, const void *B, float scale, void *stream,
                           int *slot_out);
-/* Bind fp32 gradient buffers dA [rank,in], dB [out,rank] (device) to a slot; NULL = frozen
- * (masked).  Takes effect for calls issued after it.  Errors: SMLM_E_SLOT. */
+/*
+ * Same, for an adapter of its own rank r_a <= the pool rank (heterogeneous ranks in one layer,
+ * SURVEY.md §8 f2): A [r_a,in], B [out,r_a].  The result is exactly that of the
+ * adapter zero-padded to the pool rank (the kernels read rank indices >= r_a as zero), and its
+ * gradient buffers are dA [r_a,in], dB [out,r_a].  bf16 pools: r_a a multiple of 8 in
+ * [8, pool rank] (TMA row pitch); fp32 pools: r_a = pool rank.
+ * Errors: as smlm_adapter_register, plus SMLM_E_SHAPE for a rank outside that range.
+ */
+SMLM_API int smlm_adapter_register_rank(smlm_pool pool, const void *A, const void *B, int rank, float scale,
+                                        void *stream, int *slot_out);
+/* Bind fp32 gradient buffers dA [rank,in], dB [out,rank] (device; rank = the adapter's) to a slot;
+ * NULL = frozen (masked).  Takes effect for calls issued after it.  Errors: SMLM_E_SLOT. */
 SMLM_API int smlm_adapter_set_grad(smlm_pool pool, int slot, float *dA, float *dB);
 /* Unload an adapter; the slot may be reused by a later register.  Errors: SMLM_E_SLOT. */
 SMLM_API int smlm_adapter_unregister(smlm_pool pool, int slot, void *stream);

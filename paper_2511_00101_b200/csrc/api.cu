@@ -54,7 +54,7 @@ int launch_shrink_split(const __nv_bfloat16 *X, const SlotDev *slots, const DevB
                         const DevShortRow *srows, int n_blocks, int in_f, int r, int r_pad, float *part,
                         __nv_bfloat16 *Vbd, __nv_bfloat16 *Vsave, cudaStream_t st);
 size_t grad_group_bytes();
-void fill_grad_group(void *dst, int slot, int tile_begin, int n_tiles, float *dA, float *dB);
+void fill_grad_group(void *dst, int slot, int tile_begin, int n_tiles, int r, float *dA, float *dB);
 template <typename T, typename TV>
 int launch_dadb(const DevTile *tiles, const void *groups, int n_groups, const T *X, const T *dY, const float *Uf,
                 const TV *V, int in_f, int out_f, int r, int accumulate, cudaStream_t st);
@@ -245,6 +245,7 @@ struct SlotHost {
     float scale = 1.f;
     float *dA = nullptr;
     float *dB = nullptr;
+    int r = 0;   // the adapter's rank (<= pool rank)
 };
 
 size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
@@ -830,13 +831,16 @@ static int upload_slot(smlm_pool p, int slot, cudaStream_t st) {
         d.dB = h.dB;
         d.scale = h.scale;
         d.used = 1;
+        d.r = h.r;
         if (p->dtype == SMLM_BF16) {
+            // descriptors over the adapter's own rank: TMA zero-fills the rank indices past it, so
+            // a lower-rank adapter is exactly the pool-rank one padded with zeros (f2)
             const int rb = p->r_pad * 2;
             int rc;
-            if ((rc = make_map(&d.tmA, h.A, p->in, p->r, 64, p->r_pad, CU_TENSOR_MAP_SWIZZLE_128B))) return rc;
+            if ((rc = make_map(&d.tmA, h.A, p->in, h.r, 64, p->r_pad, CU_TENSOR_MAP_SWIZZLE_128B))) return rc;
             // forward n-tile = 256 - r_pad output columns (the shrink rides in the same N=256 MMA)
-            if ((rc = make_map(&d.tmBn, h.B, p->r, p->out, p->r_pad, 256 - p->r_pad, swizzle_for(rb)))) return rc;
-            if ((rc = make_map(&d.tmBk, h.B, p->r, p->out, p->r_pad, 64, swizzle_for(rb)))) return rc;
+            if ((rc = make_map(&d.tmBn, h.B, h.r, p->out, p->r_pad, 256 - p->r_pad, swizzle_for(rb)))) return rc;
+            if ((rc = make_map(&d.tmBk, h.B, h.r, p->out, p->r_pad, 64, swizzle_for(rb)))) return rc;
         }
     }
     std::vector<uint8_t> bytes(sizeof(SlotDev));
@@ -845,7 +849,17 @@ static int upload_slot(smlm_pool p, int slot, cudaStream_t st) {
 }
 
 int smlm_adapter_register(smlm_pool p, const void *A, const void *B, float scale, void *stream, int *slot_out) {
+    if (!p) return set_err(SMLM_E_INVALID, "NULL argument");
+    return smlm_adapter_register_rank(p, A, B, p->r, scale, stream, slot_out);
+}
+
+int smlm_adapter_register_rank(smlm_pool p, const void *A, const void *B, int rank, float scale, void *stream,
+                               int *slot_out) {
     if (!p || !A || !B || !slot_out) return set_err(SMLM_E_INVALID, "NULL argument");
+    if (p->dtype == SMLM_BF16 ? (rank < 8 || rank > p->r || rank % 8 != 0) : rank != p->r)
+        return set_err(SMLM_E_SHAPE, p->dtype == SMLM_BF16
+                                         ? "adapter rank must be a multiple of 8 in [8, pool rank]"
+                                         : "fp32 pools take adapters of the pool rank only");
     if (!(scale > 0.f) || !isfinite(scale)) return set_err(SMLM_E_INVALID, "scale must be finite and > 0");
     if (p->dtype == SMLM_BF16 && (((uintptr_t)A & 15) || ((uintptr_t)B & 15)))
         return set_err(SMLM_E_INVALID, "A/B must be 16-byte aligned");
@@ -861,6 +875,7 @@ int smlm_adapter_register(smlm_pool p, const void *A, const void *B, float scale
     h.A = A;
     h.B = B;
     h.scale = scale;
+    h.r = rank;
     h.dA = h.dB = nullptr;
     rc = upload_slot(p, slot, (cudaStream_t)stream);
     if (rc) {
@@ -1187,7 +1202,7 @@ int smlm_backward(smlm_pool p, const smlm_batch *b, const void *X, const void *W
     for (auto &g : plan.groups) {
         const SlotHost &h = p->slots[g.slot];
         if (!h.dA && !h.dB) continue;
-        fill_grad_group(gbytes.data() + n_grad * grad_group_bytes(), g.slot, g.tile_begin, g.n_tiles, h.dA, h.dB);
+        fill_grad_group(gbytes.data() + n_grad * grad_group_bytes(), g.slot, g.tile_begin, g.n_tiles, h.r, h.dA, h.dB);
         ++n_grad;
     }
     gbytes.resize(n_grad * grad_group_bytes());

@@ -23,7 +23,8 @@ struct alignas(64) SlotDev {
     float *dB;
     float scale;
     int used;
-    int pad[6];
+    int r;             // this adapter's rank (<= the pool's; heterogeneous ranks)
+    int pad[5];
 };
 static_assert(sizeof(SlotDev) % 64 == 0, "SlotDev must keep 64-byte alignment of tensor maps");
 
@@ -89,7 +90,7 @@ struct GradGroup {
     int slot;
     int tile_begin;  // into the backward tile list (canonical reduction order)
     int n_tiles;
-    int pad;
+    int r;           // the adapter's rank (row count of dA, row stride of dB)
     float *dA;       // [r,in] fp32 or NULL
     float *dB;       // [out,r] fp32 or NULL
 };

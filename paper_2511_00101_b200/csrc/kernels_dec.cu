@@ -63,11 +63,15 @@ __global__ void __launch_bounds__(256) shrink_partial_kernel(const __nv_bfloat16
     const DevBlock blk = blocks[blockIdx.x];
     const int c = blockIdx.y, nch = gridDim.y;
     const __nv_bfloat16 *A = reinterpret_cast<const __nv_bfloat16 *>(slots[blk.slot].A);
+    const int ra = slots[blk.slot].r;   // rows of A past the adapter's own rank are zero
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int k0 = c * kChunk;
     for (int e = threadIdx.x; e < r * (kChunk / 8); e += 256) {
         const int j = e / (kChunk / 8), v = e % (kChunk / 8);
-        cp_async16(reinterpret_cast<uint4 *>(As) + e, reinterpret_cast<const uint4 *>(A + (size_t)j * in_f + k0) + v);
+        if (j < ra)
+            cp_async16(reinterpret_cast<uint4 *>(As) + e, reinterpret_cast<const uint4 *>(A + (size_t)j * in_f + k0) + v);
+        else
+            reinterpret_cast<uint4 *>(As)[e] = make_uint4(0, 0, 0, 0);
     }
     float *dst = part + ((size_t)blockIdx.x * nch + c) * 128 * RP;
     for (int rb = 0; rb < blk.nrows; rb += kRowsPerPass) {

@@ -332,8 +332,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT3, 1) smlm_dec3_ke
             tma_prefetch_desc(&sd->tmBk);
             const int wrow = it.n0 + 128 * (int)rank;
             if (wrow < P.out) {
-                const char *bp = reinterpret_cast<const char *>(sd->B) + (size_t)wrow * a.r * 2;
-                const uint32_t bytes = (uint32_t)(min(128, P.out - wrow) * a.r * 2);
+                const char *bp = reinterpret_cast<const char *>(sd->B) + (size_t)wrow * sd->r * 2;
+                const uint32_t bytes = (uint32_t)(min(128, P.out - wrow) * sd->r * 2);
                 asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(bp), "r"(bytes) : "memory");
             }
         }

@@ -62,6 +62,7 @@ __global__ void __launch_bounds__(256) shrink_short_kernel(const __nv_bfloat16 *
                                                            __nv_bfloat16 *__restrict__ Vsave) {
     const DevBlock blk = blocks[blockIdx.x];
     const __nv_bfloat16 *A = reinterpret_cast<const __nv_bfloat16 *>(slots[blk.slot].A);
+    const int ra = slots[blk.slot].r;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     __shared__ float part[8][4][16];
     __shared__ float vbuf[128][RP + 1];
@@ -92,7 +93,7 @@ __global__ void __launch_bounds__(256) shrink_short_kernel(const __nv_bfloat16 *
                 }
 #pragma unroll
                 for (int j = 0; j < 16; ++j) {
-                    if (jg + j < r) {
+                    if (jg + j < ra) {   // rows past the adapter's own rank are zero
                         float af[8];
                         uint4 au = *reinterpret_cast<const uint4 *>(A + (size_t)(jg + j) * in_f + k);
                         bf16x8_to_f32(au, af);
@@ -160,6 +161,7 @@ __global__ void __launch_bounds__(256) rows_shrink_kernel(const DevTile *__restr
     const DevTile t = tiles[blockIdx.x];
     if (t.slot < 0) return;
     const T *A = reinterpret_cast<const T *>(slots[t.slot].A);
+    const int ra = slots[t.slot].r;   // rows of A past the adapter's own rank are zero
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     for (int m = blockIdx.y * 8 + warp; m < t.rows; m += gridDim.y * 8) {
         const int row = t.row0 + m;
@@ -171,7 +173,7 @@ __global__ void __launch_bounds__(256) rows_shrink_kernel(const DevTile *__restr
             const float xv = ld_f(x + k);
 #pragma unroll
             for (int j = 0; j < RP; ++j)
-                if (j < r) acc[j] = fmaf(ld_f(A + (size_t)j * in_f + k), xv, acc[j]);
+                if (j < ra) acc[j] = fmaf(ld_f(A + (size_t)j * in_f + k), xv, acc[j]);
         }
 #pragma unroll
         for (int j = 0; j < RP; ++j) {
@@ -452,8 +454,8 @@ template int launch_prep_sv<__nv_bfloat16>(const DevTile *, int, const __nv_bflo
                                            cudaStream_t);
 
 size_t grad_group_bytes() { return sizeof(GradGroup); }
-void fill_grad_group(void *dst, int slot, int tile_begin, int n_tiles, float *dA, float *dB) {
-    GradGroup g{slot, tile_begin, n_tiles, 0, dA, dB};
+void fill_grad_group(void *dst, int slot, int tile_begin, int n_tiles, int r, float *dA, float *dB) {
+    GradGroup g{slot, tile_begin, n_tiles, r, dA, dB};
     *reinterpret_cast<GradGroup *>(dst) = g;
 }
 

@@ -571,14 +571,14 @@ __global__ void __launch_bounds__(kThreads, 1) smlm_tok_kernel(const __grid_cons
             const int col = mt * 128 + m;
             if (col < M) {
                 if (is_b) {
-                    float *p = grp.dB + (size_t)col * args.r;
+                    float *p = grp.dB + (size_t)col * grp.r;   // the adapter's own rank
 #pragma unroll
                     for (int j = 0; j < RP; ++j)
-                        if (j < args.r) p[j] = args.accumulate ? p[j] + __uint_as_float(v[j]) : __uint_as_float(v[j]);
+                        if (j < grp.r) p[j] = args.accumulate ? p[j] + __uint_as_float(v[j]) : __uint_as_float(v[j]);
                 } else {
 #pragma unroll
                     for (int j = 0; j < RP; ++j)
-                        if (j < args.r) {
+                        if (j < grp.r) {
                             float *p = grp.dA + (size_t)j * args.in_f + col;
                             *p = args.accumulate ? *p + __uint_as_float(v[j]) : __uint_as_float(v[j]);
                         }

@@ -27,7 +27,7 @@ EXPORTED = [
     "smlm_adapter_set_grad", "smlm_adapter_unregister", "smlm_workspace_size", "smlm_forward",
     "smlm_backward", "smlm_plan", "smlm_plan_export", "smlm_status_string", "smlm_last_error",
     "smlm_launch_count", "smlm_profile_enable", "smlm_profile_read", "smlm_workspace_size_multi",
-    "smlm_forward_multi", "smlm_adamw_workspace_size", "smlm_adamw_step",
+    "smlm_forward_multi", "smlm_adamw_workspace_size", "smlm_adamw_step", "smlm_adapter_register_rank",
 ]
 
 
@@ -54,6 +54,7 @@ def _load():
         "smlm_pool_destroy": ([P], I),
         "smlm_pool_set_option": ([P, I, I], I),
         "smlm_adapter_register": ([P, P, P, ctypes.c_float, P, ctypes.POINTER(I)], I),
+        "smlm_adapter_register_rank": ([P, P, P, I, ctypes.c_float, P, ctypes.POINTER(I)], I),
         "smlm_adapter_set_grad": ([P, I, P, P], I),
         "smlm_adapter_unregister": ([P, I, P], I),
         "smlm_workspace_size": ([P, BP, I], Z),
@@ -145,6 +146,13 @@ def smlm_adapter_register(pool: int, A, B, scale: float, stream=None) -> int:
     s = ctypes.c_int(-1)
     _check(_lib.smlm_adapter_register(pool, _ptr(A), _ptr(B), float(scale), _stream(stream, A.device),
                                       ctypes.byref(s)), "smlm_adapter_register")
+    return s.value
+
+
+def smlm_adapter_register_rank(pool: int, A, B, rank: int, scale: float, stream=None) -> int:
+    s = ctypes.c_int(-1)
+    _check(_lib.smlm_adapter_register_rank(pool, _ptr(A), _ptr(B), int(rank), float(scale),
+                                           _stream(stream, A.device), ctypes.byref(s)), "smlm_adapter_register_rank")
     return s.value
 
 
@@ -283,7 +291,11 @@ class Pool:
             pass
 
     def register(self, A, B, scale: float, stream=None) -> int:
-        slot = smlm_adapter_register(self.h, A, B, scale, stream)
+        """A [r_a, in], B [out, r_a]; r_a below the pool rank registers a lower-rank adapter."""
+        if A.shape[0] != self.rank:
+            slot = smlm_adapter_register_rank(self.h, A, B, A.shape[0], scale, stream)
+        else:
+            slot = smlm_adapter_register(self.h, A, B, scale, stream)
         self._keep[slot] = [A, B, None, None]
         return slot
 

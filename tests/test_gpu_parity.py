@@ -439,3 +439,71 @@ def test_bf16_decode_edge_shapes(rows, n_ad, outs):
         assert parity_err(Ys[i], Yr) <= BF16_TOL, i
         if len(ft):
             assert parity_err(Vs[i].double().numpy()[ft], Vr[ft]) <= BF16_TOL, i
+
+
+# ------------------------------------------------------------------------------------------
+# heterogeneous ranks in one pool: adapters registered with their own rank
+# ------------------------------------------------------------------------------------------
+def _truncate_ranks(w, ranks):
+    w.A = [a[:ra].contiguous() for a, ra in zip(w.A, ranks)]
+    w.B = [b[:, :ra].contiguous() for b, ra in zip(w.B, ranks)]
+    return w
+
+
+@pytest.mark.parametrize("r,ranks", [(16, [16, 8, 16, 8, 8]), (64, [64, 8, 32, 24, 48]), (32, [8, 32, 16, 24, 32])])
+def test_bf16_mixed_heterogeneous_ranks(r, ranks):
+    """Mixed batch (long fine-tune/prefill/eval tiles + short decode rows), forward and backward:
+    parity with the oracle (which zero-pads to the pool rank, an exact identity pinned in
+    test_oracle_pins), and no gradient write past an adapter's own rank (guards in run_smlm)."""
+    slots = [0, 1, 2, 1, 3, -1, 2, 0, 3, 4, -1, 4, 0]
+    batch, w, X, dY = synth.random_case(3000 + r, 256, 320, r, 5, MIXED_LENGTHS, MIXED_MODES, slots)
+    w = _truncate_ranks(w, ranks)
+    res = run_smlm(batch, w, X, dY)
+    _check(res, batch, w, X, dY, BF16_TOL)
+
+
+@pytest.mark.parametrize("rows,r,ranks", [(256, 16, [8, 16, 8, 16, 8, 16]), (300, 64, [8, 16, 24, 32, 48, 64])])
+def test_bf16_decode_heterogeneous_ranks(rows, r, ranks):
+    """Pure decode batch (the single-launch decode kernel) with adapters of different ranks."""
+    g = torch.Generator().manual_seed(rows + r)
+    slots = torch.randint(-1, 6, (rows,), generator=g).tolist()
+    batch, w, X, dY = synth.random_case(rows * 3 + r, 1024, 512, r, 6, [1] * rows, [DECODE] * rows, slots)
+    w = _truncate_ranks(w, ranks)
+    res = run_smlm(batch, w, X, dY, backward=False)
+    Y, V = oracle.forward(batch, w.W, w.A, w.B, w.slot_scale, X)
+    assert parity_err(res.Y, Y) <= BF16_TOL
+
+
+def test_bf16_lower_rank_equals_zero_padded_bitwise():
+    """A rank-8 adapter in a rank-16 pool gives bit for bit the result of the same adapter
+    zero-padded to rank 16 and registered at the pool rank (forward, V_save, dX, dA, dB)."""
+    batch, w, X, dY = synth.random_case(91, 256, 192, 16, 3, MIXED_LENGTHS, MIXED_MODES,
+                                        [0, 1, 2, 1, 0, -1, 2, 0, 1, 2, -1, 0, 1])
+    low = _truncate_ranks(synth.random_case(91, 256, 192, 16, 3, [1], [DECODE], [0])[1], [8, 16, 8])
+    pad = synth.random_case(91, 256, 192, 16, 3, [1], [DECODE], [0])[1]
+    for a in (0, 2):
+        pad.A[a] = torch.cat([low.A[a], torch.zeros_like(low.A[a])])
+        pad.B[a] = torch.cat([low.B[a], torch.zeros_like(low.B[a])], dim=1)
+    low.W = pad.W = w.W
+    r_low = run_smlm(batch, low, X, dY)
+    r_pad = run_smlm(batch, pad, X, dY)
+    assert torch.equal(r_low.Y, r_pad.Y) and torch.equal(r_low.V, r_pad.V) and torch.equal(r_low.dX, r_pad.dX)
+    assert torch.equal(r_low.dA, r_pad.dA) and torch.equal(r_low.dB, r_pad.dB)
+
+
+def test_register_rank_errors():
+    from paper_2511_00101_b200 import smlm as S
+    dev = torch.device("cuda", 0)
+    pool = S.Pool(128, 128, 16, 4, S.SMLM_BF16, 0)
+    for ra in (12, 32, 4):   # not a multiple of 8 / above the pool rank / below 8
+        A = torch.zeros(ra, 128, dtype=torch.bfloat16, device=dev)
+        B = torch.zeros(128, ra, dtype=torch.bfloat16, device=dev)
+        with pytest.raises(S.SmlmError) as e:
+            S.smlm_adapter_register_rank(pool.h, A, B, ra, 1.0)
+        assert e.value.code == S.SMLM_E_SHAPE
+    pool.close()
+    pf = S.Pool(128, 128, 16, 4, S.SMLM_FP32, 0)
+    with pytest.raises(S.SmlmError) as e:
+        S.smlm_adapter_register_rank(pf.h, torch.zeros(8, 128, device=dev), torch.zeros(128, 8, device=dev), 8, 1.0)
+    assert e.value.code == S.SMLM_E_SHAPE
+    pf.close()
