@@ -399,7 +399,7 @@ def main():
     step_tflops = (f_alg + b_alg) / (ms / 1000.0) / 1e12
     roofline = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                 "frac": achieved / peak if peak else None, "traffic": traffic,
-                "kernel": "smlm_gemm2_kernel<fwd> (tcgen05 cta_group::2; fused base + on-chip shrink + expand)",
+                "kernel": "smlm_gemm2_kernel<fwd, pre-shrunk> (tcgen05 cta_group::2; full 256-column W tiles + s*V expand K-block)",
                 "peak_source": peaks["source"] + " bf16_tflops_sustained",
                 "launches": fwd_n, "avg_launch_ms": fwd_ms / max(fwd_n, 1),
                 "share_of_step": fwd_ms / ms_total if ms_total else None,

@@ -322,8 +322,17 @@ struct WsLayout {
     int u_items = 0, u_ksplit = 0;
     size_t vf_off = 0, vf_bytes = 0;       // fp32 V [S,r] (fp32 mode, or bwd recompute)
     size_t spart_off = 0, spart_bytes = 0; // bf16 fwd: K-split shrink partials
+    size_t pre_sv_off = 0, pre_sv_bytes = 0;     // bf16 fwd: pre-shrunk s*V of the long tiles
+    size_t pre_part_off = 0, pre_part_bytes = 0; // bf16 fwd: its split-K partials
+    int pre_items = 0, pre_ksplit = 0;
     size_t total = 0;
 };
+
+// forward pre-shrink (s*V once per long tile, then full 256-column W tiles; DESIGN K1) on the
+// CTA-pair path; SMLM_FUSED_SHRINK=1 restores the per-n-tile fused shrink (measurement)
+static bool use_preshrink(smlm_pool p) {
+    return p->dtype == SMLM_BF16 && p->cta_pair && !env_flag("SMLM_FUSED_SHRINK");
+}
 
 int plan_for(smlm_pool p, const smlm_batch *b, bool bwd, Plan &plan) {
     std::string msg;
@@ -442,7 +451,8 @@ WsLayout layout_for(smlm_pool p, const smlm_batch *b, const Plan &plan, bool bwd
     if (!bwd) {
         L.plan_bytes = (plan.long_tiles.size() + plan.short_tiles.size()) * sizeof(DevTile) +
                        plan.blocks.size() * sizeof(DevBlock) + plan.short_rows.size() * sizeof(DevShortRow) + 16 +
-                       (plan.long_tiles.size() + plan.short_tiles.size()) * sizeof(DevPair) + 16;
+                       (plan.long_tiles.size() + plan.short_tiles.size()) * sizeof(DevPair) + 16 +
+                       plan.long_tiles.size() * sizeof(int) + 16;
     } else {
         L.plan_bytes = plan.bwd_tiles.size() * (sizeof(DevTile) + 4 + sizeof(DevPair)) +
                        plan.groups.size() * grad_group_bytes() + 64;
@@ -458,6 +468,23 @@ WsLayout layout_for(smlm_pool p, const smlm_batch *b, const Plan &plan, bool bwd
             L.spart_off = off;
             L.spart_bytes = plan.blocks.size() * (size_t)nch * 128 * p->r_pad * 4;
             off = align256(off + L.spart_bytes);
+        }
+        if (use_preshrink(p)) {
+            for (auto &t : plan.long_tiles)
+                if (t.slot >= 0) ++L.pre_items;
+            if (L.pre_items) {
+                int ks = p->num_sms / L.pre_items;
+                const int nkb = p->in / 64;
+                if (ks > nkb / 4) ks = nkb / 4;
+                if (ks < 1) ks = 1;
+                L.pre_ksplit = ks;
+                L.pre_sv_off = off;
+                L.pre_sv_bytes = plan.long_tiles.size() * 128 * (size_t)p->r_pad * 2;
+                off = align256(off + L.pre_sv_bytes);
+                L.pre_part_off = off;
+                L.pre_part_bytes = (size_t)L.pre_items * ks * 128 * p->r_pad * 4;
+                off = align256(off + L.pre_part_bytes);
+            }
         }
     }
     if (!bwd) {
@@ -996,6 +1023,11 @@ int smlm_forward(smlm_pool p, const smlm_batch *b, const void *X, const void *W,
     for (auto &t : tiles)
         if (!(t.flags & kTileShort)) ++n_long_kept;
     std::vector<DevPair> pairs;
+    std::vector<int> pre_items;   // long tiles with an adapter (pre-shrink work items)
+    const bool pre = has_w && use_preshrink(p) && L.pre_items > 0;
+    if (pre)
+        for (int i = 0; i < n_long_kept; ++i)
+            if (tiles[i].slot >= 0) pre_items.push_back(i);
     if (has_w && p->cta_pair) {
         for (int i = 0; i < n_long_kept;) {
             const DevTile &t0 = tiles[i];
@@ -1004,6 +1036,7 @@ int smlm_forward(smlm_pool p, const smlm_batch *b, const void *X, const void *W,
             pr.slot = t0.slot;
             pr.flags = (t0.flags & kTileFT) ? kPairFT : 0;
             pr.scale = t0.scale;
+            pr.tile = i;
             int rows = t0.rows;
             if (i + 1 < n_long_kept && tiles[i + 1].seg == t0.seg) {
                 rows = 128 + tiles[i + 1].rows;
@@ -1036,6 +1069,8 @@ int smlm_forward(smlm_pool p, const smlm_batch *b, const void *X, const void *W,
     while (bytes.size() % 16) bytes.push_back(0);
     const size_t pair_off = bytes.size();
     append(bytes, pairs);
+    const size_t pre_off = bytes.size();
+    append(bytes, pre_items);
     const DevTile *d_tiles = reinterpret_cast<const DevTile *>(wsb + L.plan_off);
     const DevBlock *d_blocks = reinterpret_cast<const DevBlock *>(wsb + L.plan_off + blk_off);
     const DevShortRow *d_srows = reinterpret_cast<const DevShortRow *>(wsb + L.plan_off + srow_off);
@@ -1055,7 +1090,29 @@ int smlm_forward(smlm_pool p, const smlm_batch *b, const void *X, const void *W,
         }
     }
     if (tiles.empty()) return SMLM_OK;
-    const int bnw = kBN - p->r_pad;
+    __nv_bfloat16 *pre_sv = reinterpret_cast<__nv_bfloat16 *>(wsb + L.pre_sv_off);
+    if (pre && !pre_items.empty()) {
+        // s*V = s X A_a^T once per long tile (split-K tensor-core contraction) -> tile-compact
+        // bf16 + V_save; the CTA-pair GEMM then streams full 256-column W tiles
+        ProfScope ps(2, st);
+        UArgs u;
+        memset(&u, 0, sizeof(u));
+        if ((rc = make_map(&u.tmDY, X, p->in, b->S, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B))) return rc;
+        u.slots = p->d_slots;
+        u.tiles = d_tiles;
+        u.items = reinterpret_cast<const int *>(wsb + L.plan_off + pre_off);
+        u.n_items = (int)pre_items.size();
+        u.ksplit = L.pre_ksplit;
+        u.K = p->in;
+        u.r_pad = p->r_pad;
+        u.part = reinterpret_cast<float *>(wsb + L.pre_part_off);
+        u.sUt = pre_sv;
+        u.vf = 1;
+        u.r = p->r;
+        u.Vsave = V_save;
+        CKL(launch_u(u, p->num_sms, st), 2);
+    }
+    const int bnw = pre ? kBN : kBN - p->r_pad;
     // long tiles on CTA pairs: consecutive tiles of one segment (same adapter) share one M=256 MMA
     int first_1cta = 0;  // tiles[first_1cta ..] go to the 1-CTA kernel
     if (has_w && p->cta_pair && !pairs.empty()) {
@@ -1063,7 +1120,13 @@ int smlm_forward(smlm_pool p, const smlm_batch *b, const void *X, const void *W,
         memset(&g2, 0, sizeof(g2));
         if ((rc = make_map(&g2.tmX, X, p->in, b->S, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B))) return rc;
         if ((rc = make_map(&g2.tmW0, W, p->in, p->out, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B))) return rc;
-        if ((rc = make_map(&g2.tmW1, W, p->in, p->out, 64, bnw - 128, CU_TENSOR_MAP_SWIZZLE_128B))) return rc;
+        if (!pre && (rc = make_map(&g2.tmW1, W, p->in, p->out, 64, bnw - 128, CU_TENSOR_MAP_SWIZZLE_128B))) return rc;
+        if (pre) {
+            if ((rc = make_map(&g2.tmV, pre_sv, p->r_pad, (uint64_t)n_long_kept * 128, p->r_pad, 128,
+                               swizzle_for(p->r_pad * 2))))
+                return rc;
+            g2.pre = 1;
+        }
         if (!plan.blocks.empty()) {
             if ((rc = make_map(&g2.tmU, Vbd, p->r_pad, plan.blocks.size() * 128, p->r_pad, 128,
                                swizzle_for(p->r_pad * 2))))

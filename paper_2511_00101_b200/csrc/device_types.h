@@ -57,7 +57,7 @@ struct alignas(16) DevPair {
     int slot;     // adapter or -1
     int flags;    // bit 0: FINETUNE segment (V_save); bit 1: short tile (CTA 0 only, per-adapter blocks)
     float scale;
-    int tile;     // backward: index of the pair's first tile in the backward tile list (s*U rows)
+    int tile;     // index of the pair's first tile in the tile list (bwd s*U rows / fwd pre-shrunk s*V rows)
     int blk0;     // short pair: first adapter block of the tile
     int nblk;     // short pair: number of adapter blocks
 };
@@ -68,10 +68,12 @@ struct Gemm2Args {
     CUtensorMap tmW0;   // fwd: W box {64,128} (CTA 0's half of B); bwd: W box {64,64} (MN-major)
     CUtensorMap tmW1;   // fwd: W box {64,256-r_pad-128} (CTA 1's W rows; A_a stacked below)
     CUtensorMap tmU;    // bwd: tile-compact s*U; fwd: block-diagonal s*V of short tiles; box {r_pad,128}
+    CUtensorMap tmV;    // fwd pre-shrunk (pre = 1): tile-compact s*V of the long tiles; box {r_pad,128}
     const SlotDev *slots;
     const DevPair *pairs;
     const DevBlock *blocks;   // fwd short pairs
     int has_u;                // tmU is valid
+    int pre;                  // forward: s*V precomputed (smlm_u_kernel vf) -> full 256-column W tiles
     int defer;                // forward: defer each item's expand into the next item's main loop
     int n_pairs;
     int n_ntiles;
@@ -107,6 +109,11 @@ struct UArgs {
     int r_pad;
     float *part;           // [n_items][ksplit][128][r_pad] fp32
     void *sUt;             // bf16 [n_tiles*128][r_pad]
+    // forward pre-shrink (vf = 1): tmDY holds X [S,in], the adapter operand is A_a (K-major, tmA),
+    // the result is s*V tile-compact in sUt; V_save (unscaled, FINETUNE tiles) when non-NULL
+    int vf;
+    int r;
+    void *Vsave;
 };
 
 // token-contraction GEMM (a5): dA_a^T = X^T (sU) and dB_a = dY^T (sV) over a's fine-tune tiles

@@ -622,6 +622,8 @@ constexpr int kUStages = 8;
 
 template <int RP>
 __global__ void __launch_bounds__(kThreads, 1) smlm_u_kernel(const __grid_constant__ UArgs args) {
+    // VF (args.vf): the forward pre-shrink V = X A_a^T of long tiles -- same split-K contraction,
+    // the adapter operand A_a [r, in] K-major (tmA box {64, r_pad}) instead of B_a MN-major
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw = smem_u32(smem_raw);
     const uint32_t base = (raw + 1023u) & ~1023u;
@@ -678,7 +680,8 @@ __global__ void __launch_bounds__(kThreads, 1) smlm_u_kernel(const __grid_consta
                 if (lane == 0) {
                     mbar_expect_tx(full_bar(stage), kABytes + 64u * RB);
                     tma_load_2d(a_addr(stage), &args.tmDY, full_bar(stage), kb * kBK, t.row0);
-                    tma_load_2d(b_addr(stage), &sd->tmBk, full_bar(stage), 0, kb * kBK);
+                    if (args.vf) tma_load_2d(b_addr(stage), &sd->tmA, full_bar(stage), kb * kBK, 0);
+                    else tma_load_2d(b_addr(stage), &sd->tmBk, full_bar(stage), 0, kb * kBK);
                 }
                 __syncwarp();
                 if (++stage == ST) { stage = 0; phase ^= 1; }
@@ -687,7 +690,8 @@ __global__ void __launch_bounds__(kThreads, 1) smlm_u_kernel(const __grid_consta
     } else if (warp == 1) {
         int stage = 0;
         uint32_t phase = 0, it = 0;
-        constexpr uint32_t idesc = idesc_bf16(128, RP, 0, 1);
+        constexpr uint32_t idesc_u = idesc_bf16(128, RP, 0, 1), idesc_v = idesc_bf16(128, RP, 0, 0);
+        const bool vf = args.vf != 0;
         for (int w = blockIdx.x; w < total; w += gridDim.x) {
             const int split = w % args.ksplit;
             int kb0, kb1;
@@ -704,8 +708,12 @@ __global__ void __launch_bounds__(kThreads, 1) smlm_u_kernel(const __grid_consta
                     const uint32_t ab = a_addr(stage), bb = b_addr(stage);
 #pragma unroll
                     for (int k = 0; k < kBK / 16; ++k) {
-                        mma_bf16(acc, smem_desc(ab + 32u * k, 16, 1024, kSw128),
-                                 smem_desc(bb + 16u * RB * k, 64u * RB, 8u * RB, kSwR), idesc, acc_on);
+                        if (vf)
+                            mma_bf16(acc, smem_desc(ab + 32u * k, 16, 1024, kSw128),
+                                     smem_desc(bb + 32u * k, 16, 1024, kSw128), idesc_v, acc_on);
+                        else
+                            mma_bf16(acc, smem_desc(ab + 32u * k, 16, 1024, kSw128),
+                                     smem_desc(bb + 16u * RB * k, 64u * RB, 8u * RB, kSwR), idesc_u, acc_on);
                         acc_on = 1;
                     }
                     mma_commit(empty_bar(stage));
@@ -772,6 +780,12 @@ __global__ void __launch_bounds__(128) u_reduce_kernel(const __grid_constant__ U
                 acc[4 * j4] += v.x; acc[4 * j4 + 1] += v.y; acc[4 * j4 + 2] += v.z; acc[4 * j4 + 3] += v.w;
             }
         }
+    }
+    if (args.vf && args.Vsave && (t.flags & kTileFT) && m < t.rows) {
+        __nv_bfloat16 *vs = reinterpret_cast<__nv_bfloat16 *>(args.Vsave) + (size_t)(t.row0 + m) * args.r;
+#pragma unroll
+        for (int j = 0; j < RP; ++j)
+            if (j < args.r) vs[j] = __float2bfloat16_rn(acc[j]);
     }
 #pragma unroll
     for (int c = 0; c < RP / 8; ++c) {

@@ -33,7 +33,10 @@ __device__ __forceinline__ void decode_pair(int w, int n_pairs, int n_nt, int gr
     nt = local / gm;
 }
 
-template <bool BWD, int RP>
+// PRE (forward only): s*V was precomputed once per tile (smlm_u_kernel, vf) -- the n-tile is the
+// full 256 W rows (no A_a stacked under W, no per-n-tile re-shrink) and the expand K-block takes
+// its A operand from the tile-compact s*V by TMA, like the backward's s*U.
+template <bool BWD, int RP, bool PRE>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
     smlm_gemm2_kernel(const __grid_constant__ Gemm2Args args) {
     extern __shared__ uint8_t smem_raw[];
@@ -43,8 +46,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
     constexpr uint32_t RB = RP * 2;
     // forward: n-tile = 256 - RP output columns (A_a stacked under W in CTA 1's half of B);
     // backward: n-tile = 256 columns of dX, W as the MN-major B operand (two 64-column boxes per CTA)
-    constexpr int BNW = BWD ? 256 : 256 - RP;
-    constexpr int W1 = BWD ? 128 : BNW - 128;
+    constexpr int BNW = (BWD || PRE) ? 256 : 256 - RP;
+    constexpr int W1 = (BWD || PRE) ? 128 : BNW - 128;
     constexpr uint32_t kSwR = RB >= 128 ? kSw128 : (RB == 64 ? kSw64 : kSw32);
     const int stages = args.stages;
     const uint32_t sv_addr = base + stages * kStage2;
@@ -77,7 +80,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
         tma_prefetch_desc(&args.tmX);
         tma_prefetch_desc(&args.tmW0);
         if (args.has_u) tma_prefetch_desc(&args.tmU);
-        if (!BWD) tma_prefetch_desc(&args.tmW1);
+        if (!BWD && !PRE) tma_prefetch_desc(&args.tmW1);
+        if (PRE) tma_prefetch_desc(&args.tmV);
     }
     if (warp == 2) {
         asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(tmem_slot), "r"(512)
@@ -120,7 +124,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
             };
             const uint32_t bytes_pair =
                 BWD ? 2u * kA2 + 8192u * (nbox(0) + nbox(1))
-                    : 2u * kA2 + 128u * 128u + (uint32_t)W1 * 128u + (lora ? RP * 128u : 0u);
+                    : 2u * kA2 + 128u * 128u + (uint32_t)W1 * 128u + ((lora && !PRE) ? RP * 128u : 0u);
             for (int kb = 0; kb < nkb; ++kb) {
                 mbar_wait(empty_bar(stage), phase ^ 1);
                 if (lane == 0) {
@@ -134,6 +138,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
                         }
                     } else if (leader) {
                         tma_load_2d_pair(b_addr(stage), &args.tmW0, fb, kb * kBK, n0);
+                    } else if (PRE) {
+                        tma_load_2d_pair(b_addr(stage), &args.tmW0, fb, kb * kBK, n0 + 128);
                     } else {
                         tma_load_2d_pair(b_addr(stage), &args.tmW1, fb, kb * kBK, n0 + 128);
                         if (lora) tma_load_2d_pair(b_addr(stage) + W1 * 128u, &sd->tmA, fb, kb * kBK, 0);
@@ -164,7 +170,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
                 mbar_wait(empty_bar(stage), phase ^ 1);
                 if (lane == 0) {
                     const uint32_t fb = map_to_rank(full_bar(stage), 0);
-                    if (BWD) {
+                    if (PRE) {
+                        // s*V rows of this CTA's tile (precomputed) + B_a rows [n0 + 128 rank, +128)
+                        if (leader) mbar_expect_tx(full_bar(stage), 2u * 256u * RB);
+                        tma_load_2d_pair(a_addr(stage), &args.tmV, fb, 0, (pr.tile + (int)rank) * 128);
+                        const int rb0 = n0 + 128 * (int)rank;
+                        tma_load_2d_pair(b_addr(stage), &sd->tmBk, fb, 0, rb0);
+                        tma_load_2d_pair(b_addr(stage) + 64u * RB, &sd->tmBk, fb, 0, rb0 + 64);
+                    } else if (BWD) {
                         // s*U rows of this CTA's tile (K-major) + A_a columns [n0 + 128 rank, +128) (MN-major)
                         if (leader) mbar_expect_tx(full_bar(stage), 2u * 256u * RB);
                         tma_load_2d_pair(a_addr(stage), &args.tmU, fb, 0, (pr.tile + (int)rank) * 128);
@@ -255,7 +268,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
                 if (pend_stage >= 0) ++since;
             }
             if (lora) {
-                if (BWD) {  // s*U arrives by TMA: expand right away
+                if (BWD || PRE) {  // s*U / s*V arrives by TMA: expand right away
                     issue_expand(stage, phase, b, false);
                     advance();
                     if (lane == 0) mma2_commit_mc(acc_full0 + 8 * b);
@@ -317,7 +330,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
             const bool row_ok = m < my_rows;
             const int row = pr.row0 + 128 * (int)rank + m;
             const uint32_t b = it & 1, u = it >> 1;
-            if (lora && !BWD) {
+            if (lora && !BWD && !PRE) {
                 mbar_wait(v_full, lora_it & 1);
                 tc_fence_after();
                 uint32_t v[RP];
@@ -385,9 +398,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
     }
 }
 
-template <bool BWD, int RP>
+template <bool BWD, int RP, bool PRE = false>
 int launch2_impl(const Gemm2Args &a, int num_sms, cudaStream_t st) {
-    auto kern = smlm_gemm2_kernel<BWD, RP>;
+    auto kern = smlm_gemm2_kernel<BWD, RP, PRE>;
     const size_t smem = 1024 + (size_t)a.stages * kStage2 + 128 * RP * 2 + 256;
     static bool attr_done = false;
     if (!attr_done) {
@@ -411,6 +424,14 @@ int gemm2_stages(int r_pad) {
 
 int launch_gemm2(const Gemm2Args &a, bool bwd, int num_sms, cudaStream_t st) {
     if (a.n_pairs == 0 || a.n_ntiles == 0) return 0;
+    if (!bwd && a.pre) {
+        switch (a.r_pad) {
+            case 16: return launch2_impl<false, 16, true>(a, num_sms, st);
+            case 32: return launch2_impl<false, 32, true>(a, num_sms, st);
+            case 64: return launch2_impl<false, 64, true>(a, num_sms, st);
+        }
+        return (int)cudaErrorInvalidValue;
+    }
     switch (a.r_pad * (bwd ? -1 : 1)) {
         case 16: return launch2_impl<false, 16>(a, num_sms, st);
         case 32: return launch2_impl<false, 32>(a, num_sms, st);

@@ -4,7 +4,7 @@
 #      compare SHARES, not absolutes)
 #   2. DRAM bytes of every forward CTA-pair GEMM launch of one step (-> profiles/ncu_traffic.json)
 #   3. ncu --set full of the forward GEMM (gate), the backward dX GEMM (gate), the token
-#      contraction and the U pass
+#      contraction, the U pass and the forward pre-shrink
 set -x
 OUT=${1:-gpurun_out}
 mkdir -p $OUT
@@ -18,7 +18,10 @@ $NCU --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum
 $NCU --set full --clock-control none --import-source on -k regex:smlm_gemm2_kernel -s 18 -c 1 -o $OUT/prof_fwd_gate -f $CMD > /dev/null 2>&1
 $NCU --set full --clock-control none --import-source on -k regex:smlm_gemm2_kernel -s 23 -c 1 -o $OUT/prof_bwd_gate -f $CMD > /dev/null 2>&1
 $NCU --set full --clock-control none --import-source on -k regex:smlm_tok_kernel -s 9 -c 1 -o $OUT/prof_tok -f $CMD > /dev/null 2>&1
-$NCU --set full --clock-control none --import-source on -k regex:smlm_u_kernel -s 9 -c 1 -o $OUT/prof_u -f $CMD > /dev/null 2>&1
+# smlm_u_kernel per step: 7 forward pre-shrinks (q,k,v,o,gate,up,down) then 7 backward U passes
+# (down,up,gate,...); the timed step starts at launch 14 -> gate pre-shrink = 18, gate U = 23
+$NCU --set full --clock-control none --import-source on -k regex:smlm_u_kernel -s 23 -c 1 -o $OUT/prof_u -f $CMD > /dev/null 2>&1
+$NCU --set full --clock-control none --import-source on -k regex:smlm_u_kernel -s 18 -c 1 -o $OUT/prof_preshrink -f $CMD > /dev/null 2>&1
 ls -la $OUT
 # decode path (kernels_dec3.cu): one q projection call and one fused q/k/v call at C2 shapes
 $NCU --set full --clock-control none --import-source on -k regex:smlm_dec3 -s 2 -c 1 -o $OUT/prof_dec3_q -f env PROJ=q N=3 python scripts/run_c2_once.py > /dev/null 2>&1
