@@ -328,6 +328,20 @@ struct WsLayout {
     size_t total = 0;
 };
 
+// split-K factor of the U / pre-shrink pass: ~4 work units per SM (balance across the persistent
+// grid) while every unit keeps >= 8 K-blocks (pipeline fill)
+static int u_ksplit(int num_sms, int items, int nkb) {
+    if (env_flag("SMLM_U_KS_LEGACY")) {   // measurement A/B: one unit per SM, >= 4 K-blocks
+        int ks = num_sms / items;
+        if (ks > nkb / 4) ks = nkb / 4;
+        return ks < 1 ? 1 : ks;
+    }
+    int ks = (4 * num_sms + items - 1) / items;
+    const int cap = nkb / 8 > 1 ? nkb / 8 : 1;
+    if (ks > cap) ks = cap;
+    return ks < 1 ? 1 : ks;
+}
+
 // forward pre-shrink (s*V once per long tile, then full 256-column W tiles; DESIGN K1) on the
 // CTA-pair path; SMLM_FUSED_SHRINK=1 restores the per-n-tile fused shrink (measurement)
 static bool use_preshrink(smlm_pool p) {
@@ -473,10 +487,7 @@ WsLayout layout_for(smlm_pool p, const smlm_batch *b, const Plan &plan, bool bwd
             for (auto &t : plan.long_tiles)
                 if (t.slot >= 0) ++L.pre_items;
             if (L.pre_items) {
-                int ks = p->num_sms / L.pre_items;
-                const int nkb = p->in / 64;
-                if (ks > nkb / 4) ks = nkb / 4;
-                if (ks < 1) ks = 1;
+                const int ks = u_ksplit(p->num_sms, L.pre_items, p->in / 64);
                 L.pre_ksplit = ks;
                 L.pre_sv_off = off;
                 L.pre_sv_bytes = plan.long_tiles.size() * 128 * (size_t)p->r_pad * 2;
@@ -505,10 +516,7 @@ WsLayout layout_for(smlm_pool p, const smlm_batch *b, const Plan &plan, bool bwd
         for (auto &t : plan.bwd_tiles)
             if (t.slot >= 0) ++L.u_items;
         if (L.u_items) {
-            int ks = p->num_sms / L.u_items;
-            const int nkb = p->out / 64;
-            if (ks > nkb / 4) ks = nkb / 4;
-            if (ks < 1) ks = 1;
+            const int ks = u_ksplit(p->num_sms, L.u_items, p->out / 64);
             L.u_ksplit = ks;
             L.upart_off = off;
             L.upart_bytes = (size_t)L.u_items * ks * 128 * p->r_pad * 4;

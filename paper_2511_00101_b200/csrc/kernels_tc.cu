@@ -618,7 +618,14 @@ int launch_tok_impl(const TokArgs &a, int num_sms, cudaStream_t st) {
 //   [tile][split][128][r_pad]; u_reduce sums them in split order and writes the tile-compact
 //   s*U (bf16, zero rows past the segment) consumed by the dX expand and the dA contraction.
 // ==========================================================================================
-constexpr int kUStages = 8;
+// pipeline depth of the U / pre-shrink pass: as many 16 KB + r_pad-row stages as shared memory
+// holds (the pass is a latency-bound stream of small K-blocks: depth is what keeps HBM busy)
+template <int RP>
+constexpr int u_stages() {
+    return (int)((232448u - 1280u) / (kABytes + ((64u * RP * 2u + 1023u) & ~1023u))) > 12
+               ? 12
+               : (int)((232448u - 1280u) / (kABytes + ((64u * RP * 2u + 1023u) & ~1023u)));
+}
 
 template <int RP>
 __global__ void __launch_bounds__(kThreads, 1) smlm_u_kernel(const __grid_constant__ UArgs args) {
@@ -631,7 +638,7 @@ __global__ void __launch_bounds__(kThreads, 1) smlm_u_kernel(const __grid_consta
     constexpr uint32_t RB = RP * 2;
     constexpr uint32_t kSwR = RB >= 128 ? kSw128 : (RB == 64 ? kSw64 : kSw32);
     constexpr uint32_t kStg = kABytes + ((64 * RB + 1023u) & ~1023u);
-    constexpr int ST = kUStages;
+    constexpr int ST = u_stages<RP>();
     const uint32_t bar = base + ST * kStg;
     auto full_bar = [&](int s) { return bar + 8u * s; };
     auto empty_bar = [&](int s) { return bar + 8u * (ST + s); };
@@ -802,7 +809,7 @@ template <int RP>
 int launch_u_impl(const UArgs &a, int num_sms, cudaStream_t st) {
     auto kern = smlm_u_kernel<RP>;
     constexpr size_t kStg = 16384 + ((64 * RP * 2 + 1023) & ~1023);
-    const size_t smem = 1024 + kUStages * kStg + 256;
+    const size_t smem = 1024 + u_stages<RP>() * kStg + 256;
     static bool attr_done = false;
     if (!attr_done) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

@@ -9,7 +9,7 @@ set -x
 OUT=${1:-gpurun_out}
 mkdir -p $OUT
 NCU=/usr/local/cuda/bin/ncu
-CMD="python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline"
+CMD="python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline --no-side"
 $NCU --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches.csv $CMD > /dev/null 2>&1
 # smlm_gemm2_kernel launches per step: 7 forward (q,k,v,o,gate,up,down) then 7 backward
 # (down,up,gate,o,v,k,q); the first step is the warm-up, so the timed step's forward is 14..20

@@ -55,7 +55,8 @@ def main():
     os.makedirs(dst, exist_ok=True)
     for rep in sorted(os.listdir(src)):
         if rep.startswith("prof_") and rep.endswith(".ncu-rep") and rep in (
-                "prof_fwd_gate.ncu-rep", "prof_bwd_gate.ncu-rep", "prof_tok.ncu-rep", "prof_u.ncu-rep"):
+                "prof_fwd_gate.ncu-rep", "prof_bwd_gate.ncu-rep", "prof_tok.ncu-rep", "prof_u.ncu-rep",
+                "prof_preshrink.ncu-rep", "prof_dec3_q.ncu-rep", "prof_dec3_qkv.ncu-rep"):
             d = raw(os.path.join(src, rep))
             with open(os.path.join(dst, "ncu_" + rep[5:-8] + ".json"), "w") as f:
                 json.dump(d, f, indent=1)
