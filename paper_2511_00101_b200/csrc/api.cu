@@ -273,6 +273,7 @@ struct smlm_pool_s {
     std::vector<float> scales;
     SlotDev *d_slots = nullptr;
     int *d_ctr = nullptr;   // decode kernel: self-resetting cross-CTA counters (dec3_counter_ints())
+    int *d_uctr = nullptr;  // U / pre-shrink pass: self-resetting per-item split counters (kUCtrMax)
     // encoded TMA descriptors of recently used (pointer, shape, box) keys: steady-state calls reuse them
     struct MapEnt {
         const void *ptr;
@@ -818,6 +819,8 @@ int smlm_pool_create(int device, int in_features, int out_features, int rank, in
     }
     if (e == cudaSuccess) e = cudaMalloc(&p->d_ctr, sizeof(int) * dec3_counter_ints());
     if (e == cudaSuccess) e = cudaMemset(p->d_ctr, 0, sizeof(int) * dec3_counter_ints());
+    if (e == cudaSuccess) e = cudaMalloc(&p->d_uctr, sizeof(int) * kUCtrMax);
+    if (e == cudaSuccess) e = cudaMemset(p->d_uctr, 0, sizeof(int) * kUCtrMax);
     if (e == cudaSuccess) e = cudaMemset(p->d_slots, 0, sizeof(SlotDev) * capacity);
     if (e != cudaSuccess) {
         cudaFree(p->d_slots);
@@ -835,6 +838,7 @@ int smlm_pool_destroy(smlm_pool p) {
         cudaDeviceSynchronize();
         if (p->d_slots) cudaFree(p->d_slots);
         if (p->d_ctr) cudaFree(p->d_ctr);
+        if (p->d_uctr) cudaFree(p->d_uctr);
         if (p->cap_arena) cudaFreeHost(p->cap_arena);
     }
     delete p;
@@ -1118,7 +1122,8 @@ int smlm_forward(smlm_pool p, const smlm_batch *b, const void *X, const void *W,
         u.vf = 1;
         u.r = p->r;
         u.Vsave = V_save;
-        CKL(launch_u(u, p->num_sms, st), 2);
+        u.ctr = (u.n_items <= kUCtrMax && !env_flag("SMLM_U_SEPARATE_REDUCE")) ? p->d_uctr : nullptr;
+        CKL(launch_u(u, p->num_sms, st), u.ctr ? 1 : 2);
     }
     const int bnw = pre ? kBN : kBN - p->r_pad;
     // long tiles on CTA pairs: consecutive tiles of one segment (same adapter) share one M=256 MMA
@@ -1354,7 +1359,8 @@ int smlm_backward(smlm_pool p, const smlm_batch *b, const void *X, const void *W
         u.r_pad = p->r_pad;
         u.part = reinterpret_cast<float *>(wsb + L.upart_off);
         u.sUt = sUt;
-        CKL(launch_u(u, p->num_sms, st), 2);
+        u.ctr = (u.n_items <= kUCtrMax && !env_flag("SMLM_U_SEPARATE_REDUCE")) ? p->d_uctr : nullptr;
+        CKL(launch_u(u, p->num_sms, st), u.ctr ? 1 : 2);
     }
     if (dX) {
         ProfScope ps(1, st);

@@ -114,7 +114,9 @@ struct UArgs {
     int vf;
     int r;
     void *Vsave;
+    int *ctr;   // per-item split arrival counters (pool-owned, self-resetting) or NULL: separate reduce
 };
+constexpr int kUCtrMax = 4096;   // items per U / pre-shrink launch that use the in-kernel reduce
 
 // token-contraction GEMM (a5): dA_a^T = X^T (sU) and dB_a = dY^T (sV) over a's fine-tune tiles
 struct TokArgs {

@@ -627,6 +627,49 @@ constexpr int u_stages() {
                : (int)((232448u - 1280u) / (kABytes + ((64u * RP * 2u + 1023u) & ~1023u)));
 }
 
+// sUt[tile*128 + m][j] = bf16(s * sum_split part) (zero rows past the segment), split order fixed
+template <int RP>
+__device__ __forceinline__ void u_reduce_row(const UArgs &args, int item, int m) {
+    const int ti = args.items[item];
+    const DevTile t = args.tiles[ti];
+    uint4 *dst = reinterpret_cast<uint4 *>(reinterpret_cast<__nv_bfloat16 *>(args.sUt) + ((size_t)ti * 128 + m) * RP);
+    float acc[RP];
+#pragma unroll
+    for (int j = 0; j < RP; ++j) acc[j] = 0.f;
+    if (m < t.rows) {
+        for (int s = 0; s < args.ksplit; ++s) {
+            const float4 *src = reinterpret_cast<const float4 *>(args.part + (((size_t)item * args.ksplit + s) * 128 + m) * RP);
+#pragma unroll
+            for (int j4 = 0; j4 < RP / 4; ++j4) {
+                const float4 v = __ldcg(src + j4);
+                acc[4 * j4] += v.x; acc[4 * j4 + 1] += v.y; acc[4 * j4 + 2] += v.z; acc[4 * j4 + 3] += v.w;
+            }
+        }
+    }
+    if (args.vf && args.Vsave && (t.flags & kTileFT) && m < t.rows) {
+        __nv_bfloat16 *vs = reinterpret_cast<__nv_bfloat16 *>(args.Vsave) + (size_t)(t.row0 + m) * args.r;
+#pragma unroll
+        for (int j = 0; j < RP; ++j)
+            if (j < args.r) vs[j] = __float2bfloat16_rn(acc[j]);
+    }
+#pragma unroll
+    for (int c = 0; c < RP / 8; ++c) {
+        uint4 pk;
+        pk.x = pack_bf16x2(t.scale * acc[8 * c + 0], t.scale * acc[8 * c + 1]);
+        pk.y = pack_bf16x2(t.scale * acc[8 * c + 2], t.scale * acc[8 * c + 3]);
+        pk.z = pack_bf16x2(t.scale * acc[8 * c + 4], t.scale * acc[8 * c + 5]);
+        pk.w = pack_bf16x2(t.scale * acc[8 * c + 6], t.scale * acc[8 * c + 7]);
+        dst[c] = pk;
+    }
+}
+
+// stand-alone reduce (when the kernel has no arrival counters)
+template <int RP>
+__global__ void __launch_bounds__(128) u_reduce_kernel(const __grid_constant__ UArgs args) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    u_reduce_row<RP>(args, blockIdx.x, threadIdx.x);
+}
+
 template <int RP>
 __global__ void __launch_bounds__(kThreads, 1) smlm_u_kernel(const __grid_constant__ UArgs args) {
     // VF (args.vf): the forward pre-shrink V = X A_a^T of long tiles -- same split-K contraction,
@@ -756,6 +799,23 @@ __global__ void __launch_bounds__(kThreads, 1) smlm_u_kernel(const __grid_consta
             }
             tc_fence_before();
             mbar_arrive(accf0 + 16 + 8 * b);
+            if (args.ctr) {
+                // the last split of the item to arrive reduces it (split order, as u_reduce_kernel);
+                // the counter returns to 0 for the next launch
+                __shared__ int s_last;
+                __threadfence();
+                named_bar_sync(1, 128);
+                if (threadIdx.x == 128) {
+                    const int old = atomicAdd(args.ctr + item, 1);
+                    s_last = old == args.ksplit - 1;
+                    if (s_last) args.ctr[item] = 0;
+                }
+                named_bar_sync(1, 128);
+                if (s_last) {
+                    __threadfence();
+                    u_reduce_row<RP>(args, item, m);
+                }
+            }
             ++it;
         }
     }
@@ -763,45 +823,6 @@ __global__ void __launch_bounds__(kThreads, 1) smlm_u_kernel(const __grid_consta
     if (warp == 2) {
         tc_fence_after();
         tmem_dealloc(tmem_base, 128);
-    }
-}
-
-// sUt[tile*128 + m][j] = bf16(s * sum_split part) (zero rows past the segment), split order fixed
-template <int RP>
-__global__ void __launch_bounds__(128) u_reduce_kernel(const __grid_constant__ UArgs args) {
-    asm volatile("griddepcontrol.wait;" ::: "memory");
-    const int item = blockIdx.x;
-    const int ti = args.items[item];
-    const DevTile t = args.tiles[ti];
-    const int m = threadIdx.x;
-    uint4 *dst = reinterpret_cast<uint4 *>(reinterpret_cast<__nv_bfloat16 *>(args.sUt) + ((size_t)ti * 128 + m) * RP);
-    float acc[RP];
-#pragma unroll
-    for (int j = 0; j < RP; ++j) acc[j] = 0.f;
-    if (m < t.rows) {
-        for (int s = 0; s < args.ksplit; ++s) {
-            const float4 *src = reinterpret_cast<const float4 *>(args.part + (((size_t)item * args.ksplit + s) * 128 + m) * RP);
-#pragma unroll
-            for (int j4 = 0; j4 < RP / 4; ++j4) {
-                const float4 v = __ldcg(src + j4);
-                acc[4 * j4] += v.x; acc[4 * j4 + 1] += v.y; acc[4 * j4 + 2] += v.z; acc[4 * j4 + 3] += v.w;
-            }
-        }
-    }
-    if (args.vf && args.Vsave && (t.flags & kTileFT) && m < t.rows) {
-        __nv_bfloat16 *vs = reinterpret_cast<__nv_bfloat16 *>(args.Vsave) + (size_t)(t.row0 + m) * args.r;
-#pragma unroll
-        for (int j = 0; j < RP; ++j)
-            if (j < args.r) vs[j] = __float2bfloat16_rn(acc[j]);
-    }
-#pragma unroll
-    for (int c = 0; c < RP / 8; ++c) {
-        uint4 pk;
-        pk.x = pack_bf16x2(t.scale * acc[8 * c + 0], t.scale * acc[8 * c + 1]);
-        pk.y = pack_bf16x2(t.scale * acc[8 * c + 2], t.scale * acc[8 * c + 3]);
-        pk.z = pack_bf16x2(t.scale * acc[8 * c + 4], t.scale * acc[8 * c + 5]);
-        pk.w = pack_bf16x2(t.scale * acc[8 * c + 6], t.scale * acc[8 * c + 7]);
-        dst[c] = pk;
     }
 }
 
@@ -818,7 +839,7 @@ int launch_u_impl(const UArgs &a, int num_sms, cudaStream_t st) {
     }
     const int total = a.n_items * a.ksplit;
     cudaError_t e = launch_pdl(kern, dim3(total < num_sms ? total : num_sms), dim3(kThreads), smem, st, a);
-    if (e != cudaSuccess) return (int)e;
+    if (e != cudaSuccess || a.ctr) return (int)e;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(a.n_items);
     cfg.blockDim = dim3(128);
