@@ -499,6 +499,7 @@ def run_e2e(wl, stream, steps, n, dist):
     s_h2d2 = torch.cuda.Stream(dev)   # second copy engine for the input stream
     s_d2h = torch.cuda.Stream(dev)
     in_ready = [torch.cuda.Event(), torch.cuda.Event()]
+    diag = [] if os.environ.get("BENCH_E2E_DIAG") else None   # per-step copy/compute timeline (stderr)
     in_free = [None, None]
     out_done = [None, None]
 
@@ -513,6 +514,12 @@ def run_e2e(wl, stream, steps, n, dist):
         with torch.cuda.stream(s_h2d2):
             for p in hdY:
                 dYb[b][p][:ft].copy_(hdY[p], non_blocking=True)
+        if diag is not None:
+            e1, e2 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e1.record(s_h2d)
+            e2.record(s_h2d2)
+            diag.append(("h2d_x_end", i, e1))
+            diag.append(("h2d_dy_end", i, e2))
         s_h2d.wait_stream(s_h2d2)
         in_ready[b].record(s_h2d)
 
@@ -522,6 +529,10 @@ def run_e2e(wl, stream, steps, n, dist):
         stream.wait_event(in_ready[b])
         if out_done[b] is not None:
             stream.wait_event(out_done[b])
+        if diag is not None:
+            e = torch.cuda.Event(enable_timing=True)
+            e.record(stream)
+            diag.append(("compute_start", i, e))
         for p in synth.PROJECTIONS:
             e = layer[p]
             S.smlm_forward(e["pool"].h, wl.b, Xb[b][GROUP_OF[p]], e["W"], Yb[b][p], Vb[b][p], e["wsf"], stream)
@@ -541,9 +552,11 @@ def run_e2e(wl, stream, steps, n, dist):
             s_d2h.wait_event(ev)
             with torch.cuda.stream(s_d2h):
                 hG[p].copy_(e["grad"].flat, non_blocking=True)
-        ev = torch.cuda.Event()
+        ev = torch.cuda.Event(enable_timing=diag is not None)
         ev.record(stream)
         in_free[b] = ev
+        if diag is not None:
+            diag.append(("compute_end", i, ev))
         od = torch.cuda.Event()
         od.record(s_d2h)
         out_done[b] = od
@@ -565,6 +578,13 @@ def run_e2e(wl, stream, steps, n, dist):
     t1.record(s_d2h)
     t1.synchronize()
     ms = t0.elapsed_time(t1) / steps
+    if diag is not None:
+        for name, i, e in diag:
+            if e.query():
+                try:
+                    print(f"[e2e diag] step {i} {name} {t0.elapsed_time(e):.2f} ms", file=sys.stderr)
+                except RuntimeError:
+                    pass
     if dist is not None:
         t = torch.tensor([ms], device=wl.dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)

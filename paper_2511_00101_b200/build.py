@@ -18,7 +18,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 BUILD = os.path.join(HERE, "_build")
 LIB = os.path.join(HERE, "libsmlm.so")
-SOURCES = ["api.cu", "planner.cpp", "kernels_tc.cu", "kernels_simt.cu", "kernels_dec.cu", "kernels_tc2.cu", "kernels_dec3.cu", "kernels_opt.cu"]
+SOURCES = ["api.cu", "planner.cpp", "kernels_tc.cu", "kernels_simt.cu", "kernels_dec.cu", "kernels_tc2.cu", "kernels_dec3.cu", "kernels_opt.cu", "kernels_plan.cu"]
 HEADERS = ["plan.h", "device_types.h", "sm100.cuh", "pdl.cuh"]
 NVCC = os.environ.get("NVCC", "nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

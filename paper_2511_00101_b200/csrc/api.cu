@@ -47,6 +47,7 @@ int launch_tok(const TokArgs &a, int num_sms, cudaStream_t st);
 int dec_chunks(int in_f);
 int dec3_stages();
 int launch_dec3(const Dec3Args &a, const Dec3Inline &in, int clusters, cudaStream_t st);
+int launch_plan_copy(void *dst, const void *src, size_t n, cudaStream_t st);
 int adamw_grid(int num_sms, size_t n);
 int launch_adamw_sumsq(const float *g, size_t n, float gscale, float *partial, int grid, cudaStream_t st);
 int launch_adamw_step(const AdamwArgs &a, int grid, cudaStream_t st);
@@ -536,6 +537,15 @@ WsLayout layout_for(smlm_pool p, const smlm_batch *b, const Plan &plan, bool bwd
 // Copy a host byte vector into the workspace through the pinned ring (stream ordered).
 int stage_upload(smlm_pool p, const std::vector<uint8_t> &bytes, void *dst, cudaStream_t st) {
     if (bytes.empty()) return SMLM_OK;
+    if (!env_flag("SMLM_PLAN_MEMCPY")) {
+        // small plans ride in kernel parameters (kernels_plan.cu): never queued behind bulk DMA
+        const int rc = launch_plan_copy(dst, bytes.data(), bytes.size(), st);
+        if (rc == 0) {
+            ++g_launches;
+            return SMLM_OK;
+        }
+        if (rc > 0) return cuda_err((cudaError_t)rc, "plan upload (parameter copy)");
+    }
     cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
     cudaStreamIsCapturing(st, &cs);
     if (cs != cudaStreamCaptureStatusNone) {
