@@ -507,3 +507,18 @@ def test_register_rank_errors():
         S.smlm_adapter_register_rank(pf.h, torch.zeros(8, 128, device=dev), torch.zeros(128, 8, device=dev), 8, 1.0)
     assert e.value.code == S.SMLM_E_SHAPE
     pf.close()
+
+
+def test_bf16_large_plan_memcpy_fallback():
+    """A batch whose plan exceeds one kernel-parameter block (3000 one-row decode segments of 40
+    adapters plus a fine-tune segment: > 32 KB of plan records) takes the pinned-ring memcpy
+    upload instead of the parameter copy kernel; parity as usual."""
+    rows = 3000
+    g = torch.Generator().manual_seed(17)
+    slots = torch.randint(-1, 40, (rows,), generator=g).tolist() + [3]
+    lengths = [1] * rows + [200]
+    modes = [DECODE] * rows + [FINETUNE]
+    batch, w, X, dY = synth.random_case(4321, 256, 192, 16, 40, lengths, modes, slots)
+    res = run_smlm(batch, w, X, dY)
+    rows_chk = np.concatenate([np.arange(0, rows, 7), np.arange(rows, rows + 200)])
+    _check(res, batch, w, X, dY, BF16_TOL, rows=rows_chk)
