@@ -437,7 +437,11 @@ Dec3Plan dec3_plan(int n_proj, const smlm_pool *pools, const smlm_batch *b, cons
     if (const char *e = getenv("SMLM_DEC_KSPLIT"))   // measurement / test override (read per call)
         best_ks = std::max(1, std::min(atoi(e), kmax));
     while (best_ks > 1 && NW * best_ks + NV > pairs) --best_ks;   // (only with very many adapters)
-    int best_ksv = NV ? std::max(1, std::min(kmax, (pairs - NW * best_ks) / NV)) : 1;
+    // V splits (up to 16): fewer K-blocks per split keep all of a split's loads in
+    // flight in the 6-stage ring (the V chain is load-latency bound, not bandwidth bound)
+    const int kmax_v = std::max(1, std::min(env_int("SMLM_DEC3_KSV_MAX") > 0 ? env_int("SMLM_DEC3_KSV_MAX") : 16,
+                                            nkb / 2));
+    int best_ksv = NV ? std::max(1, std::min(kmax_v, (pairs - NW * best_ks) / NV)) : 1;
     if (NW * best_ks + NV * best_ksv > pairs) best_ks = 0;
     if (best_ks == 0) return D;   // more tiles than one wave: not this kernel
     D.ks = best_ks;

@@ -23,7 +23,8 @@
 //
 // Counters (pool-owned int[dec3_counter_ints()], zero at pool creation, self-resetting):
 //   [0] V-tile CTAs that published their slabs, [1] CTAs departed (the last one resets
-//   everything), [2 + tile] split arrivals of a tile (V tiles first, then W tiles).
+//   everything), [2 + tile] split arrivals of a tile (V tiles first, then W tiles),
+//   [258] V-tile CTAs that issued their first ring of loads (the W tiles start streaming after).
 // All CTAs of a launch are co-resident (grid <= one wave of pairs) -- required by the spin-waits.
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -42,6 +43,7 @@ constexpr uint32_t kA3 = 128 * 128;   // own 128 decode rows x 64 k
 constexpr uint32_t kB3 = 128 * 128;   // own 128 W rows x 64 k
 constexpr uint32_t kStage3 = kA3 + kB3;
 constexpr uint32_t kYStage = 128 * 32 * 2;   // bf16 Y chunk staged for the TMA store
+constexpr int kVIssuedCtr = 2 + 256;          // counter: V-tile CTAs that issued their first ring of loads
 
 __device__ __forceinline__ void dbg_stamp(const Dec3Args &a, int k) {
     if (a.dbg) {
@@ -240,6 +242,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT3, 1) smlm_dec3_ke
         const uint32_t bytes_pair = it.vtile ? 2u * kA3 + (uint32_t)(max(0, min(APC, a.n_uniq - it.n0)) + nad1) * RP * 128u
                                              : 2u * kStage3;
         if (it.vtile && lane < nad) tma_prefetch_desc(&P.slots[s_uslot[u0 + lane]].tmA);
+        if (!it.vtile && a.n_vpairs > 0 && !(a.flags & 16)) {
+            // the V tiles' first ring of loads goes to the memory system before the W stream: the
+            // V chain (shrink -> split-K reduction -> publish) is what the W tiles' expand waits for
+            if (lane == 0)
+                while (ld_acquire_gpu(a.ctr + kVIssuedCtr) < 2 * a.n_vpairs) __nanosleep(64);
+            __syncwarp();
+        }
         for (int kb = kb0; kb < kb1; ++kb) {
             mbar_wait(empty_bar(stage), phase ^ 1);
             const uint32_t fb = map_to_rank(full_bar(stage), 0);
@@ -255,6 +264,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT3, 1) smlm_dec3_ke
                                  kb * kBK, 0);
             }
             __syncwarp();
+            if (it.vtile && lane == 0 && kb - kb0 + 1 == min(ST, kb1 - kb0)) atom_add_release_gpu(a.ctr + kVIssuedCtr, 1);
             if (++stage == ST) { stage = 0; phase ^= 1; }
         }
         if (lane == 0) dbg_stamp(a, 1);
@@ -410,12 +420,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT3, 1) smlm_dec3_ke
                 if (in_tile && ks > 1) {
                     // all splits' partials of a 16-column slice in flight at once, summed in split order
 #pragma unroll
-                    for (int j0 = 0; j0 < RP; j0 += 16) {
+                    for (int j0 = 0; j0 < RP; j0 += 16)
+#pragma unroll 1
+                    for (int sb = 0; sb < ks; sb += 8) {   // 8 splits in flight, then the next 8
                         float t[8][16];
 #pragma unroll
                         for (int s2 = 0; s2 < 8; ++s2) {
-                            if (s2 < ks) {
-                                const float4 *src = reinterpret_cast<const float4 *>(vpart + ((size_t)s2 * 2 * 128 + m) * RP + j0);
+                            if (sb + s2 < ks) {
+                                const float4 *src = reinterpret_cast<const float4 *>(vpart + ((size_t)(sb + s2) * 2 * 128 + m) * RP + j0);
 #pragma unroll
                                 for (int q = 0; q < 4; ++q) {
                                     const float4 f = __ldcg(src + q);
@@ -428,9 +440,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT3, 1) smlm_dec3_ke
                         }
 #pragma unroll
                         for (int s2 = 0; s2 < 8; ++s2)
-                            if (s2 < ks)
+                            if (sb + s2 < ks)
 #pragma unroll
-                                for (int j = 0; j < 16; ++j) vp[j0 + j] = s2 == 0 ? t[0][j] : vp[j0 + j] + t[s2][j];
+                                for (int j = 0; j < 16; ++j) vp[j0 + j] = sb + s2 == 0 ? t[0][j] : vp[j0 + j] + t[s2][j];
                     }
                 }
                 __nv_bfloat16 *sv = reinterpret_cast<__nv_bfloat16 *>(P.sv);
@@ -576,6 +588,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT3, 1) smlm_dec3_ke
         if (atom_add_acq_rel_gpu(a.ctr + 1, 1) == (int)gridDim.x - 1) {
             a.ctr[0] = 0;
             a.ctr[1] = 0;
+            a.ctr[kVIssuedCtr] = 0;
             const int tiles = a.n_vpairs / a.ks_v + a.n_groups * a.n_wt;
             for (int t = 0; t < tiles; ++t) a.ctr[2 + t] = 0;
         }
