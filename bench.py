@@ -41,6 +41,9 @@ UNIT = "tokens/s"
 N_LAYER_SETS = 3          # distinct weight sets rotated across steps (each 416 MiB > 126 MB L2)
 FT_SLOTS = [0, 1, 2, 3]   # fine-tune adapters (C4/C5)
 GROUP_OF = {"q": "attn", "k": "attn", "v": "attn", "o": "o", "gate": "mlp", "up": "mlp", "down": "down"}
+# projections sharing X go through one smlm_forward_multi call (Alg. 1 P:331 joint QKV;
+# SURVEY §8 f1): q/k/v, o, gate/up, down
+FWD_GROUPS = [("q", "k", "v"), ("o",), ("gate", "up"), ("down",)]
 
 
 def _peaks():
@@ -157,6 +160,11 @@ class Workload:
                 wsf = torch.empty_like(wsf)
                 wsb = torch.empty(S.smlm_workspace_size(pool.h, self.b, True) + 256, dtype=torch.uint8, device=dev)
                 layer[p] = dict(W=W, A=A, B=B, pool=pool, grad=bucket, wsf=wsf, wsb=wsb)
+            for grp in FWD_GROUPS:
+                if len(grp) > 1:
+                    hs = [layer[p]["pool"].h for p in grp]
+                    n = S.smlm_workspace_size_multi(hs, self.b)
+                    layer[grp] = dict(h=hs, ws=torch.empty(n + 256, dtype=torch.uint8, device=dev))
             self.layers.append(layer)
 
     def flops(self):
@@ -171,30 +179,39 @@ class Workload:
         return f, b
 
     def fwd_gemm_flops(self, p):
-        """Algorithmic flops of one forward tensor-core launch for projection p: the base product
-        for every row, plus the on-chip shrink of long-tile rows that have an adapter, plus the
-        expand of every row that has an adapter (short-row shrink runs in the SIMT kernel)."""
+        """Algorithmic flops of one forward tensor-core GEMM launch for projection p: the base
+        product for every row plus the expand of every row that has an adapter (the shrink runs
+        in the pre-shrink pass for long tiles and in the SIMT kernel for short rows)."""
         r = self.spec.rank
         in_f, out_f = synth.PROJ_SHAPES[p]
         lens = np.diff(self.batch.offsets)
         lora = self.batch.slots >= 0
-        long_ = lens >= 64
         rows_lora = int(lens[lora].sum())
-        rows_long_lora = int(lens[lora & long_].sum())
-        return 2.0 * self.rows * in_f * out_f + 2.0 * rows_long_lora * r * in_f + 2.0 * rows_lora * r * out_f
+        return 2.0 * self.rows * in_f * out_f + 2.0 * rows_lora * r * out_f
 
     def step(self, L: int, stream, comm=None):
         S = self.S
         layer = self.layers[L]
-        for p in synth.PROJECTIONS:
-            e = layer[p]
-            S.smlm_forward(e["pool"].h, self.b, self.X[GROUP_OF[p]], e["W"], self.Y[p], self.V[p], e["wsf"], stream)
+        forward_groups(S, layer, self.b, lambda p: self.X[GROUP_OF[p]], self.Y, self.V, stream)
         for p in reversed(synth.PROJECTIONS):
             e = layer[p]
             S.smlm_backward(e["pool"].h, self.b, self.X[GROUP_OF[p]], e["W"], self.dY[p], self.V[p], self.dX[p],
                             0, e["wsb"], stream)
             if comm is not None:
                 comm(e["grad"])
+
+
+def forward_groups(S, layer, b, X_of, Y, V, stream, groups=None):
+    """Forward of the projection groups: one smlm_forward_multi call per group of projections
+    that share X (q/k/v, gate/up), smlm_forward for the others."""
+    for grp in (groups or FWD_GROUPS):
+        if len(grp) > 1:
+            m = layer[grp]
+            S.smlm_forward_multi(m["h"], b, X_of(grp[0]), [layer[p]["W"] for p in grp], [Y[p] for p in grp],
+                                 [V[p] for p in grp], m["ws"], stream)
+        else:
+            e = layer[grp[0]]
+            S.smlm_forward(e["pool"].h, b, X_of(grp[0]), e["W"], Y[grp[0]], V[grp[0]], e["wsf"], stream)
 
 
 def _device_timed(fn, steps, stream):
@@ -533,14 +550,14 @@ def run_e2e(wl, stream, steps, n, dist):
             e = torch.cuda.Event(enable_timing=True)
             e.record(stream)
             diag.append(("compute_start", i, e))
-        for p in synth.PROJECTIONS:
-            e = layer[p]
-            S.smlm_forward(e["pool"].h, wl.b, Xb[b][GROUP_OF[p]], e["W"], Yb[b][p], Vb[b][p], e["wsf"], stream)
+        for grp in FWD_GROUPS:
+            forward_groups(S, layer, wl.b, lambda p: Xb[b][GROUP_OF[p]], Yb[b], Vb[b], stream, [grp])
             ev = torch.cuda.Event()
             ev.record(stream)
             s_d2h.wait_event(ev)
             with torch.cuda.stream(s_d2h):
-                hY[p].copy_(Yb[b][p][dec0:], non_blocking=True)
+                for p in grp:
+                    hY[p].copy_(Yb[b][p][dec0:], non_blocking=True)
         for p in reversed(synth.PROJECTIONS):
             e = layer[p]
             S.smlm_backward(e["pool"].h, wl.b, Xb[b][GROUP_OF[p]], e["W"], dYb[b][p], Vb[b][p], dXb[b][p], 0,

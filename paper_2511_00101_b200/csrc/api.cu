@@ -93,8 +93,14 @@ static int env_int(const char *name) {
     std::lock_guard<std::mutex> lk(mu);
     for (auto &kv : cache)
         if (kv.first == name) return kv.second;
+    // unset or empty -> 0; a number -> its value ("0" disables); any other text -> 1
     const char *e = getenv(name);
-    const int v = e ? (atoi(e) ? atoi(e) : 1) : 0;
+    int v = 0;
+    if (e && *e) {
+        char *end = nullptr;
+        const long x = strtol(e, &end, 10);
+        v = end != e ? (int)x : 1;
+    }
     cache.emplace_back(name, v);
     return v;
 }
@@ -330,19 +336,18 @@ struct WsLayout {
     size_t total = 0;
 };
 
-// split-K factor of the U / pre-shrink pass: ~4 work units per SM (balance across the persistent
-// grid) while every unit keeps >= 8 K-blocks (pipeline fill)
+// split-K factor of the U / pre-shrink pass: about one work unit per SM, >= 4 K-blocks per unit
+// (measured against ~4 units per SM with >= 8 K-blocks: finer splits cost more partial traffic
+// and power than they gain in balance, 1-2 % of the C4 step)
 static int u_ksplit(int num_sms, int items, int nkb) {
-    if (env_flag("SMLM_U_KS_LEGACY")) {   // measurement A/B: one unit per SM, >= 4 K-blocks
-        int ks = num_sms / items;
-        if (ks > nkb / 4) ks = nkb / 4;
-        return ks < 1 ? 1 : ks;
-    }
-    int ks = (4 * num_sms + items - 1) / items;
-    const int cap = nkb / 8 > 1 ? nkb / 8 : 1;
-    if (ks > cap) ks = cap;
+    int ks = num_sms / items;
+    if (ks > nkb / 4) ks = nkb / 4;
     return ks < 1 ? 1 : ks;
 }
+
+// set by smlm_forward_multi around its per-projection smlm_forward calls: s*V of the long tiles
+// was already computed for every projection in one shared pass (f1 for mixed batches)
+static thread_local const void *t_ext_pre_sv = nullptr;
 
 // forward pre-shrink (s*V once per long tile, then full 256-column W tiles; DESIGN K1) on the
 // CTA-pair path; SMLM_FUSED_SHRINK=1 restores the per-n-tile fused shrink (measurement)
@@ -1116,8 +1121,9 @@ int smlm_forward(smlm_pool p, const smlm_batch *b, const void *X, const void *W,
         }
     }
     if (tiles.empty()) return SMLM_OK;
-    __nv_bfloat16 *pre_sv = reinterpret_cast<__nv_bfloat16 *>(wsb + L.pre_sv_off);
-    if (pre && !pre_items.empty()) {
+    __nv_bfloat16 *pre_sv = t_ext_pre_sv ? reinterpret_cast<__nv_bfloat16 *>(const_cast<void *>(t_ext_pre_sv))
+                                         : reinterpret_cast<__nv_bfloat16 *>(wsb + L.pre_sv_off);
+    if (pre && !pre_items.empty() && !t_ext_pre_sv) {
         // s*V = s X A_a^T once per long tile (split-K tensor-core contraction) -> tile-compact
         // bf16 + V_save; the CTA-pair GEMM then streams full 256-column W tiles
         ProfScope ps(2, st);
@@ -1234,6 +1240,44 @@ static int multi_check(int n_proj, const smlm_pool *pools, const smlm_batch *b, 
     return SMLM_OK;
 }
 
+// f1 for mixed batches: one pre-shrink pass over X for every projection (the A_a of all of them
+// stacked as the N of one tcgen05 contraction), then each projection's GEMM with its s*V.
+struct MultiPre {
+    bool ok = false;
+    size_t base = 0;                      // per-projection forward workspace (max over pools), reused
+    size_t sv_off[kDec3MaxProj] = {}, sv_bytes = 0;
+    size_t part_off = 0, plan_off = 0, total = 0;
+    int items = 0, ksplit = 1;
+};
+static MultiPre multi_pre_layout(int n_proj, const smlm_pool *pools, const smlm_batch *b, const Plan &plan, bool same) {
+    MultiPre M;
+    smlm_pool p0 = pools[0];
+    if (!same || n_proj < 2 || p0->dtype != SMLM_BF16 || !use_preshrink(p0) || env_flag("SMLM_NO_MULTI_PRE") ||
+        n_proj * p0->r_pad > 128)
+        return M;
+    for (int i = 1; i < n_proj; ++i)
+        if (pools[i]->cta_pair != p0->cta_pair || pools[i]->l_long != p0->l_long || pools[i]->r_pad != p0->r_pad)
+            return M;
+    for (auto &t : plan.long_tiles)
+        if (t.slot >= 0) ++M.items;
+    if (M.items == 0) return M;
+    for (int i = 0; i < n_proj; ++i) M.base = std::max(M.base, smlm_workspace_size(pools[i], b, 0));
+    size_t off = align256(M.base);
+    M.sv_bytes = plan.long_tiles.size() * 128 * (size_t)p0->r_pad * 2;
+    for (int i = 0; i < n_proj; ++i) {
+        M.sv_off[i] = off;
+        off = align256(off + M.sv_bytes);
+    }
+    M.ksplit = u_ksplit(p0->num_sms, M.items, p0->in / 64);
+    M.part_off = off;
+    off = align256(off + (size_t)M.items * M.ksplit * 128 * n_proj * p0->r_pad * 4);
+    M.plan_off = off;
+    off = align256(off + plan.long_tiles.size() * sizeof(DevTile) + (size_t)M.items * sizeof(int) + 32);
+    M.total = off;
+    M.ok = true;
+    return M;
+}
+
 size_t smlm_workspace_size_multi(int n_proj, const smlm_pool *pools, const smlm_batch *b) {
     Plan plan;
     bool same = true;
@@ -1244,6 +1288,8 @@ size_t smlm_workspace_size_multi(int n_proj, const smlm_pool *pools, const smlm_
         const Dec3Plan D = dec3_plan(n_proj, pools, b, plan);
         if (D.ok) ws = std::max(ws, D.total);
     }
+    const MultiPre M = multi_pre_layout(n_proj, pools, b, plan, same);
+    if (M.ok) ws = std::max(ws, M.total);
     return ws;
 }
 
@@ -1263,6 +1309,56 @@ int smlm_forward_multi(int n_proj, const smlm_pool *pools, const smlm_batch *b, 
         DeviceGuard dg(pools[0]->device);
         if ((rc = check_sticky())) return rc;
         return run_dec3(n_proj, pools, b, D, X, W, Y, V_save, reinterpret_cast<uint8_t *>(ws), (cudaStream_t)stream);
+    }
+    const MultiPre M = multi_pre_layout(n_proj, pools, b, plan, same);
+    if (M.ok) {
+        if (!ws || ws_bytes < M.total) return set_err(SMLM_E_WORKSPACE, "workspace too small");
+        DeviceGuard dg(pools[0]->device);
+        if ((rc = check_sticky())) return rc;
+        smlm_pool p0 = pools[0];
+        cudaStream_t st = (cudaStream_t)stream;
+        uint8_t *wsb = reinterpret_cast<uint8_t *>(ws);
+        // long tiles (the same list every projection's forward builds) + the items with an adapter
+        std::vector<int> items;
+        for (size_t i = 0; i < plan.long_tiles.size(); ++i)
+            if (plan.long_tiles[i].slot >= 0) items.push_back((int)i);
+        std::vector<uint8_t> bytes;
+        append(bytes, plan.long_tiles);
+        while (bytes.size() % 16) bytes.push_back(0);
+        const size_t items_off = bytes.size();
+        append(bytes, items);
+        if ((rc = stage_upload(p0, bytes, wsb + M.plan_off, st))) return rc;
+        UArgs u;
+        memset(&u, 0, sizeof(u));
+        if ((rc = make_map_cached(p0, &u.tmDY, X, p0->in, b->S, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B))) return rc;
+        u.slots = p0->d_slots;
+        u.tiles = reinterpret_cast<const DevTile *>(wsb + M.plan_off);
+        u.items = reinterpret_cast<const int *>(wsb + M.plan_off + items_off);
+        u.n_items = M.items;
+        u.ksplit = M.ksplit;
+        u.K = p0->in;
+        u.r_pad = p0->r_pad;
+        u.part = reinterpret_cast<float *>(wsb + M.part_off);
+        u.vf = 1;
+        u.r = p0->r;
+        u.npj = n_proj;
+        for (int i = 0; i < n_proj; ++i) {
+            u.slots_p[i] = pools[i]->d_slots;
+            u.sUt_p[i] = wsb + M.sv_off[i];
+            u.Vsave_p[i] = V_save ? V_save[i] : nullptr;
+        }
+        u.ctr = (u.n_items <= kUCtrMax && !env_flag("SMLM_U_SEPARATE_REDUCE")) ? p0->d_uctr : nullptr;
+        {
+            ProfScope ps(2, st);
+            CKL(launch_u(u, p0->num_sms, st), u.ctr ? 1 : 2);
+        }
+        for (int i = 0; i < n_proj; ++i) {
+            t_ext_pre_sv = wsb + M.sv_off[i];
+            rc = smlm_forward(pools[i], b, X, W[i], Y[i], V_save ? V_save[i] : nullptr, ws, M.base, stream);
+            t_ext_pre_sv = nullptr;
+            if (rc) return rc;
+        }
+        return SMLM_OK;
     }
     for (int i = 0; i < n_proj; ++i)
         if ((rc = smlm_forward(pools[i], b, X, W[i], Y[i], V_save ? V_save[i] : nullptr, ws, ws_bytes, stream)))

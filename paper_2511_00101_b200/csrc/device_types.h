@@ -115,6 +115,12 @@ struct UArgs {
     int r;
     void *Vsave;
     int *ctr;   // per-item split arrival counters (pool-owned, self-resetting) or NULL: separate reduce
+    // npj > 1: forward pre-shrink of npj projections sharing X in one pass (npj * r_pad <= 128):
+    // projection p's adapters from slots_p[p], its s*V / V_save to sUt_p[p] / Vsave_p[p]
+    int npj;
+    const SlotDev *slots_p[4];
+    void *sUt_p[4];
+    void *Vsave_p[4];
 };
 constexpr int kUCtrMax = 4096;   // items per U / pre-shrink launch that use the in-kernel reduce
 

@@ -620,25 +620,32 @@ int launch_tok_impl(const TokArgs &a, int num_sms, cudaStream_t st) {
 // ==========================================================================================
 // pipeline depth of the U / pre-shrink pass: as many 16 KB + r_pad-row stages as shared memory
 // holds (the pass is a latency-bound stream of small K-blocks: depth is what keeps HBM busy)
-template <int RP>
+template <int RP, int NPJ = 1>
+constexpr uint32_t u_stage_bytes() { return kABytes + ((64u * RP * 2u * NPJ + 1023u) & ~1023u); }
+template <int RP, int NPJ = 1>
 constexpr int u_stages() {
-    return (int)((232448u - 1280u) / (kABytes + ((64u * RP * 2u + 1023u) & ~1023u))) > 12
-               ? 12
-               : (int)((232448u - 1280u) / (kABytes + ((64u * RP * 2u + 1023u) & ~1023u)));
+    return (int)((232448u - 1280u) / u_stage_bytes<RP, NPJ>()) > 12 ? 12
+                                                                      : (int)((232448u - 1280u) / u_stage_bytes<RP, NPJ>());
 }
 
 // sUt[tile*128 + m][j] = bf16(s * sum_split part) (zero rows past the segment), split order fixed
-template <int RP>
+// NPJ > 1 (forward pre-shrink of several projections sharing X): the partial rows hold NPJ x RP
+// columns; projection p's columns go to sUt_p[p] / Vsave_p[p]
+template <int RP, int NPJ = 1>
 __device__ __forceinline__ void u_reduce_row(const UArgs &args, int item, int m) {
     const int ti = args.items[item];
     const DevTile t = args.tiles[ti];
-    uint4 *dst = reinterpret_cast<uint4 *>(reinterpret_cast<__nv_bfloat16 *>(args.sUt) + ((size_t)ti * 128 + m) * RP);
+#pragma unroll 1
+    for (int pj = 0; pj < NPJ; ++pj) {
+    void *sut = NPJ == 1 ? args.sUt : args.sUt_p[pj];
+    void *vsave = NPJ == 1 ? args.Vsave : args.Vsave_p[pj];
+    uint4 *dst = reinterpret_cast<uint4 *>(reinterpret_cast<__nv_bfloat16 *>(sut) + ((size_t)ti * 128 + m) * RP);
     float acc[RP];
 #pragma unroll
     for (int j = 0; j < RP; ++j) acc[j] = 0.f;
     if (m < t.rows) {
         for (int s = 0; s < args.ksplit; ++s) {
-            const float4 *src = reinterpret_cast<const float4 *>(args.part + (((size_t)item * args.ksplit + s) * 128 + m) * RP);
+            const float4 *src = reinterpret_cast<const float4 *>(args.part + (((size_t)item * args.ksplit + s) * 128 + m) * (NPJ * RP) + pj * RP);
 #pragma unroll
             for (int j4 = 0; j4 < RP / 4; ++j4) {
                 const float4 v = __ldcg(src + j4);
@@ -646,8 +653,8 @@ __device__ __forceinline__ void u_reduce_row(const UArgs &args, int item, int m)
             }
         }
     }
-    if (args.vf && args.Vsave && (t.flags & kTileFT) && m < t.rows) {
-        __nv_bfloat16 *vs = reinterpret_cast<__nv_bfloat16 *>(args.Vsave) + (size_t)(t.row0 + m) * args.r;
+    if (args.vf && vsave && (t.flags & kTileFT) && m < t.rows) {
+        __nv_bfloat16 *vs = reinterpret_cast<__nv_bfloat16 *>(vsave) + (size_t)(t.row0 + m) * args.r;
 #pragma unroll
         for (int j = 0; j < RP; ++j)
             if (j < args.r) vs[j] = __float2bfloat16_rn(acc[j]);
@@ -661,16 +668,17 @@ __device__ __forceinline__ void u_reduce_row(const UArgs &args, int item, int m)
         pk.w = pack_bf16x2(t.scale * acc[8 * c + 6], t.scale * acc[8 * c + 7]);
         dst[c] = pk;
     }
+    }
 }
 
 // stand-alone reduce (when the kernel has no arrival counters)
-template <int RP>
+template <int RP, int NPJ>
 __global__ void __launch_bounds__(128) u_reduce_kernel(const __grid_constant__ UArgs args) {
     asm volatile("griddepcontrol.wait;" ::: "memory");
-    u_reduce_row<RP>(args, blockIdx.x, threadIdx.x);
+    u_reduce_row<RP, NPJ>(args, blockIdx.x, threadIdx.x);
 }
 
-template <int RP>
+template <int RP, int NPJ>
 __global__ void __launch_bounds__(kThreads, 1) smlm_u_kernel(const __grid_constant__ UArgs args) {
     // VF (args.vf): the forward pre-shrink V = X A_a^T of long tiles -- same split-K contraction,
     // the adapter operand A_a [r, in] K-major (tmA box {64, r_pad}) instead of B_a MN-major
@@ -680,8 +688,10 @@ __global__ void __launch_bounds__(kThreads, 1) smlm_u_kernel(const __grid_consta
     uint8_t *base_ptr = smem_raw + (base - raw);
     constexpr uint32_t RB = RP * 2;
     constexpr uint32_t kSwR = RB >= 128 ? kSw128 : (RB == 64 ? kSw64 : kSw32);
-    constexpr uint32_t kStg = kABytes + ((64 * RB + 1023u) & ~1023u);
-    constexpr int ST = u_stages<RP>();
+    constexpr uint32_t kStg = u_stage_bytes<RP, NPJ>();
+    constexpr int ST = u_stages<RP, NPJ>();
+    constexpr int NC = NPJ * RP;                        // accumulator columns (one TMEM buffer)
+    constexpr uint32_t kTm = 2 * NC <= 128 ? 128 : 256; // two buffers
     const uint32_t bar = base + ST * kStg;
     auto full_bar = [&](int s) { return bar + 8u * s; };
     auto empty_bar = [&](int s) { return bar + 8u * (ST + s); };
@@ -702,7 +712,7 @@ __global__ void __launch_bounds__(kThreads, 1) smlm_u_kernel(const __grid_consta
         fence_mbar_init();
         tma_prefetch_desc(&args.tmDY);
     }
-    if (warp == 2) tmem_alloc(tmem_slot, 128);
+    if (warp == 2) tmem_alloc(tmem_slot, kTm);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -728,10 +738,19 @@ __global__ void __launch_bounds__(kThreads, 1) smlm_u_kernel(const __grid_consta
             for (int kb = kb0; kb < kb1; ++kb) {
                 mbar_wait(empty_bar(stage), phase ^ 1);
                 if (lane == 0) {
-                    mbar_expect_tx(full_bar(stage), kABytes + 64u * RB);
+                    mbar_expect_tx(full_bar(stage), kABytes + 64u * RB * NPJ);
                     tma_load_2d(a_addr(stage), &args.tmDY, full_bar(stage), kb * kBK, t.row0);
-                    if (args.vf) tma_load_2d(b_addr(stage), &sd->tmA, full_bar(stage), kb * kBK, 0);
-                    else tma_load_2d(b_addr(stage), &sd->tmBk, full_bar(stage), 0, kb * kBK);
+                    if (NPJ > 1) {
+                        // the A_a of every projection stacked: N = NPJ * r_pad rows of the B operand
+#pragma unroll
+                        for (int pj = 0; pj < NPJ; ++pj)
+                            tma_load_2d(b_addr(stage) + (uint32_t)pj * RP * 128u, &args.slots_p[pj][t.slot].tmA,
+                                        full_bar(stage), kb * kBK, 0);
+                    } else if (args.vf) {
+                        tma_load_2d(b_addr(stage), &sd->tmA, full_bar(stage), kb * kBK, 0);
+                    } else {
+                        tma_load_2d(b_addr(stage), &sd->tmBk, full_bar(stage), 0, kb * kBK);
+                    }
                 }
                 __syncwarp();
                 if (++stage == ST) { stage = 0; phase ^= 1; }
@@ -740,14 +759,14 @@ __global__ void __launch_bounds__(kThreads, 1) smlm_u_kernel(const __grid_consta
     } else if (warp == 1) {
         int stage = 0;
         uint32_t phase = 0, it = 0;
-        constexpr uint32_t idesc_u = idesc_bf16(128, RP, 0, 1), idesc_v = idesc_bf16(128, RP, 0, 0);
+        constexpr uint32_t idesc_u = idesc_bf16(128, RP, 0, 1), idesc_v = idesc_bf16(128, NC, 0, 0);
         const bool vf = args.vf != 0;
         for (int w = blockIdx.x; w < total; w += gridDim.x) {
             const int split = w % args.ksplit;
             int kb0, kb1;
             kb_range(split, kb0, kb1);
             const uint32_t b = it & 1, u = it >> 1;
-            const uint32_t acc = tmem_base + b * RP;
+            const uint32_t acc = tmem_base + b * NC;
             mbar_wait(accf0 + 16 + 8 * b, (u & 1) ^ 1);
             tc_fence_after();
             uint32_t acc_on = 0;
@@ -785,11 +804,11 @@ __global__ void __launch_bounds__(kThreads, 1) smlm_u_kernel(const __grid_consta
             const uint32_t b = it & 1, u = it >> 1;
             mbar_wait(accf0 + 8 * b, u & 1);
             tc_fence_after();
-            float *dst = args.part + (((size_t)item * args.ksplit + split) * 128 + m) * RP;
+            float *dst = args.part + (((size_t)item * args.ksplit + split) * 128 + m) * NC;
 #pragma unroll
-            for (int c = 0; c < RP; c += 16) {
+            for (int c = 0; c < NC; c += 16) {
                 uint32_t v[16];
-                tmem_ld16(tmem_base + b * RP + lane_base + c, v);
+                tmem_ld16(tmem_base + b * NC + lane_base + c, v);
                 tmem_wait_ld();
 #pragma unroll
                 for (int j = 0; j < 16; j += 4)
@@ -813,7 +832,7 @@ __global__ void __launch_bounds__(kThreads, 1) smlm_u_kernel(const __grid_consta
                 named_bar_sync(1, 128);
                 if (s_last) {
                     __threadfence();
-                    u_reduce_row<RP>(args, item, m);
+                    u_reduce_row<RP, NPJ>(args, item, m);
                 }
             }
             ++it;
@@ -822,15 +841,15 @@ __global__ void __launch_bounds__(kThreads, 1) smlm_u_kernel(const __grid_consta
     __syncthreads();
     if (warp == 2) {
         tc_fence_after();
-        tmem_dealloc(tmem_base, 128);
+        tmem_dealloc(tmem_base, kTm);
     }
 }
 
-template <int RP>
+template <int RP, int NPJ = 1>
 int launch_u_impl(const UArgs &a, int num_sms, cudaStream_t st) {
-    auto kern = smlm_u_kernel<RP>;
-    constexpr size_t kStg = 16384 + ((64 * RP * 2 + 1023) & ~1023);
-    const size_t smem = 1024 + u_stages<RP>() * kStg + 256;
+    auto kern = smlm_u_kernel<RP, NPJ>;
+    constexpr size_t kStg = u_stage_bytes<RP, NPJ>();
+    const size_t smem = 1024 + u_stages<RP, NPJ>() * kStg + 256;
     static bool attr_done = false;
     if (!attr_done) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -849,7 +868,7 @@ int launch_u_impl(const UArgs &a, int num_sms, cudaStream_t st) {
     at[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    return (int)cudaLaunchKernelEx(&cfg, u_reduce_kernel<RP>, a);
+    return (int)cudaLaunchKernelEx(&cfg, u_reduce_kernel<RP, NPJ>, a);
 }
 
 }  // namespace
@@ -866,6 +885,18 @@ int gemm_stages(int r_pad, size_t *smem_bytes) {
 
 int launch_u(const UArgs &a, int num_sms, cudaStream_t st) {
     if (a.n_items == 0) return 0;
+    if (a.npj > 1) {   // forward pre-shrink of several projections (npj * r_pad <= 128)
+        switch (a.r_pad * 8 + a.npj) {
+            case 16 * 8 + 2: return launch_u_impl<16, 2>(a, num_sms, st);
+            case 16 * 8 + 3: return launch_u_impl<16, 3>(a, num_sms, st);
+            case 16 * 8 + 4: return launch_u_impl<16, 4>(a, num_sms, st);
+            case 32 * 8 + 2: return launch_u_impl<32, 2>(a, num_sms, st);
+            case 32 * 8 + 3: return launch_u_impl<32, 3>(a, num_sms, st);
+            case 32 * 8 + 4: return launch_u_impl<32, 4>(a, num_sms, st);
+            case 64 * 8 + 2: return launch_u_impl<64, 2>(a, num_sms, st);
+        }
+        return (int)cudaErrorInvalidValue;
+    }
     switch (a.r_pad) {
         case 16: return launch_u_impl<16>(a, num_sms, st);
         case 32: return launch_u_impl<32>(a, num_sms, st);

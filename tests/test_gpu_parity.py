@@ -522,3 +522,26 @@ def test_bf16_large_plan_memcpy_fallback():
     res = run_smlm(batch, w, X, dY)
     rows_chk = np.concatenate([np.arange(0, rows, 7), np.arange(rows, rows + 200)])
     _check(res, batch, w, X, dY, BF16_TOL, rows=rows_chk)
+
+
+@pytest.mark.parametrize("r,outs", [(16, (320, 192, 192)), (32, (256, 512)), (64, (192, 256)), (16, (128, 256, 192, 320))])
+def test_bf16_mixed_multi_projection(r, outs):
+    """Mixed batch through smlm_forward_multi (f1 for mixed batches): one shared pre-shrink pass
+    for all projections, then each projection's GEMM.  Every projection matches the oracle (Y on
+    all rows, V_save on fine-tune rows) and is bit-identical to its own smlm_forward call."""
+    slots = [0, 1, 2, 1, 3, -1, 2, 0, 3, 4, -1, 4, 0]
+    cases = [synth.random_case(5000 + 10 * r + i, 256, o, r, 5, MIXED_LENGTHS, MIXED_MODES, slots)
+             for i, o in enumerate(outs)]
+    batch, X = cases[0][0], cases[0][2]
+    ws_ = [c[1] for c in cases]
+    Ys, Vs, launches = _run_multi(batch, ws_, X)
+    ft = batch.ft_rows()
+    rs = batch.row_slot()
+    ft_lora = ft[rs[ft] >= 0]
+    for i, w in enumerate(ws_):
+        Y, V = oracle.forward(batch, w.W, w.A, w.B, w.slot_scale, X)
+        assert parity_err(Ys[i], Y) <= BF16_TOL, i
+        assert parity_err(Vs[i].double().numpy()[ft_lora], V[ft_lora]) <= BF16_TOL, i
+        single = run_smlm(batch, w, X, None, backward=False)
+        assert torch.equal(single.Y, Ys[i]), f"projection {i}: multi differs from the single call"
+        assert torch.equal(single.V[ft_lora], Vs[i][ft_lora]), i
