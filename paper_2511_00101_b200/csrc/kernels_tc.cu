@@ -407,7 +407,14 @@ int launch_impl(const GemmArgs &a, int num_sms, size_t smem, cudaStream_t st) {
 // memory before the MMA (isolation from other requests' rows).  Two TMEM accumulators of r_pad
 // columns let the epilogue of one item overlap the main loop of the next.
 // ==========================================================================================
-constexpr int kTokStages = 6;
+// pipeline depth: as many stages as shared memory holds (HBM-bound stream of 64-token K-blocks;
+// bytes in flight per SM are what keep the memory system busy), at most 12
+template <int RP>
+constexpr int tok_stages() {
+    return (int)((232448u - 1280u) / (16384u + ((64u * RP * 2u + 1023u) & ~1023u))) > 12
+               ? 12
+               : (int)((232448u - 1280u) / (16384u + ((64u * RP * 2u + 1023u) & ~1023u)));
+}
 
 __device__ __forceinline__ bool tok_item(const TokArgs &a, int w, int &g, int &mt, bool &is_b) {
     const int na = a.n_groups * a.mt_a;
@@ -435,7 +442,7 @@ __global__ void __launch_bounds__(kThreads, 1) smlm_tok_kernel(const __grid_cons
     constexpr uint32_t kB = 64 * RB;            // 64 tokens x r_pad
     constexpr uint32_t kStage = kA + ((kB + 1023u) & ~1023u);
     constexpr uint32_t kSwR = RB >= 128 ? kSw128 : (RB == 64 ? kSw64 : kSw32);
-    constexpr int ST = kTokStages;
+    constexpr int ST = tok_stages<RP>();
     const uint32_t bar = base + ST * kStage;
     auto full_bar = [&](int s) { return bar + 8u * s; };
     auto empty_bar = [&](int s) { return bar + 8u * (ST + s); };
@@ -598,7 +605,7 @@ template <int RP>
 int launch_tok_impl(const TokArgs &a, int num_sms, cudaStream_t st) {
     auto kern = smlm_tok_kernel<RP>;
     constexpr size_t kStage = 16384 + ((64 * RP * 2 + 1023) & ~1023);
-    const size_t smem = 1024 + kTokStages * kStage + 256;
+    const size_t smem = 1024 + tok_stages<RP>() * kStage + 256;
     static bool attr_done = false;
     if (!attr_done) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

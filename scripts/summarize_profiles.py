@@ -4,7 +4,7 @@
   profiles/<round>/launch_shares.md    per-kernel share of one bench step (launch list)
   profiles/ncu_traffic.json            DRAM bytes per forward-GEMM launch (read by bench.py)
 
-Usage: python scripts/summarize_profiles.py gpurun_out profiles/r01
+Usage: python scripts/summarize_profiles.py gpurun_out profiles/r01 [launches_per_step]
 """
 import collections
 import csv
@@ -60,11 +60,14 @@ def main():
             d = raw(os.path.join(src, rep))
             with open(os.path.join(dst, "ncu_" + rep[5:-8] + ".json"), "w") as f:
                 json.dump(d, f, indent=1)
+    # the library's launches (kernels in namespace smlm, incl. the plan-copy kernel); the timed
+    # step is the last `per_step` of them (bench.py --steps 1 --warmup 1; gpu_launches / steps)
+    per_step = int(sys.argv[3]) if len(sys.argv) > 3 else 69
     data = [d for d in launches(os.path.join(src, "launches.csv")) if "smlm" in d["Kernel Name"]]
-    step = data[len(data) // 2:]
+    step = data[-per_step:]
     agg = collections.OrderedDict()
     for d in step:
-        k = d["Kernel Name"].split("(")[0].replace("void smlm::<unnamed>::", "")
+        k = d["Kernel Name"].split("(")[0].replace("void smlm::<unnamed>::", "").replace("smlm::<unnamed>::", "")
         agg[k] = agg.get(k, 0.0) + float(d["Metric Value"]) / 1000.0
     tot = sum(agg.values())
     with open(os.path.join(dst, "launch_shares.md"), "w") as f:
