@@ -160,9 +160,12 @@ SMLM_API int smlm_forward(smlm_pool pool, const smlm_batch *batch, const void *X
  *     smlm_forward(pools[i], batch, X, W[i], Y[i], V_save ? V_save[i] : NULL, ...)
  * up to the fp32 summation order (within the bf16 tolerance), but a pure short/decode batch
  * (<= 512 rows, no segment >= L_long) runs as ONE launch that streams every W[i] once and reads X
- * once.  Other batches run the per-pool calls in sequence.
+ * once, and a mixed bf16 batch computes s*V of its long tiles for every projection in ONE
+ * pre-shrink pass over X (n_proj * r_pad <= 128; bit-identical to the per-pool calls) before each
+ * projection's GEMM.  Otherwise (e.g. different slot scales across pools) the per-pool calls run
+ * in sequence.
  *   n_proj in [1, 4]; pools share device, in_features, rank and dtype; every slot of the batch
- *   must be registered in every pool with the same slot scale (else SMLM_E_SLOT);
+ *   must be registered in every pool (else SMLM_E_SLOT);
  *   W[i] != NULL; Y[i] [S, out_i]; V_save NULL or an array of n_proj pointers (each may be NULL).
  *   ws: ws_bytes >= smlm_workspace_size_multi(n_proj, pools, batch).
  * The decode kernel uses pools[0]'s counters: calls that share pools[0] must be stream-ordered.
