@@ -524,7 +524,8 @@ def test_bf16_large_plan_memcpy_fallback():
     _check(res, batch, w, X, dY, BF16_TOL, rows=rows_chk)
 
 
-@pytest.mark.parametrize("r,outs", [(16, (320, 192, 192)), (32, (256, 512)), (64, (192, 256)), (16, (128, 256, 192, 320))])
+@pytest.mark.parametrize("r,outs", [(16, (320, 192, 192)), (32, (256, 512)), (64, (192, 256)), (16, (128, 256, 192, 320)),
+                                    (64, (192, 256, 128))])   # last: 3 x 64 > 128 columns -> per-pool calls
 def test_bf16_mixed_multi_projection(r, outs):
     """Mixed batch through smlm_forward_multi (f1 for mixed batches): one shared pre-shrink pass
     for all projections, then each projection's GEMM.  Every projection matches the oracle (Y on
