@@ -340,6 +340,12 @@ struct WsLayout {
 // (measured against ~4 units per SM with >= 8 K-blocks: finer splits cost more partial traffic
 // and power than they gain in balance, 1-2 % of the C4 step)
 static int u_ksplit(int num_sms, int items, int nkb) {
+    if (env_flag("SMLM_U_KS_FINE")) {   // measurement A/B: ~4 units per SM, >= 8 K-blocks each
+        int ks = (4 * num_sms + items - 1) / items;
+        const int cap = nkb / 8 > 1 ? nkb / 8 : 1;
+        if (ks > cap) ks = cap;
+        return ks < 1 ? 1 : ks;
+    }
     int ks = num_sms / items;
     if (ks > nkb / 4) ks = nkb / 4;
     return ks < 1 ? 1 : ks;
