@@ -622,8 +622,12 @@ int launch_tok_impl(const TokArgs &a, int num_sms, cudaStream_t st) {
 // U = dY B_a for the fine-tune tiles (backward), split K over `out`:
 //   item = (fine-tune tile with an adapter, K split); D[128 rows x r_pad] on tcgen05 with the dY
 //   tile as the K-major A operand and B_a k-rows as the MN-major B operand; fp32 partials
-//   [tile][split][128][r_pad]; u_reduce sums them in split order and writes the tile-compact
-//   s*U (bf16, zero rows past the segment) consumed by the dX expand and the dA contraction.
+//   [tile][split][128][r_pad]; the last split of a tile to arrive (per-item counter) sums them in
+//   split order and writes the tile-compact s*U (bf16, zero rows past the segment) consumed by the
+//   dX expand and the dA contraction.
+// The same kernel is the forward PRE-SHRINK (vf = 1, DESIGN K1a): V = X A_a^T of every long tile
+//   with an adapter, A_a as the K-major B operand, -> tile-compact s*V + V_save; with NPJ > 1 the
+//   A_a of several projections that share X are stacked (N = NPJ * r_pad) so X is read once.
 // ==========================================================================================
 // pipeline depth of the U / pre-shrink pass: as many 16 KB + r_pad-row stages as shared memory
 // holds (the pass is a latency-bound stream of small K-blocks: depth is what keeps HBM busy)

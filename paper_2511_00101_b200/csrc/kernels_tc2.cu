@@ -1,9 +1,11 @@
 // kernels_tc2.cu -- forward SMLM GEMM on CTA pairs (tcgen05 cta_group::2, M = 256).
 //
-// Same math as smlm_gemm_kernel<fwd> (shrink fused into the N=256 MMA by stacking A_a under the
-// W n-tile, expand folded in as an extra K-block, V never leaves the SM pair), but each work
-// item covers TWO 128-row tiles of the same segment (same adapter), one per CTA of a cluster
-// pair.  The pair issues one M=256 MMA per K-step: each CTA stages its own 128 X rows and HALF
+// Default forward (PRE = true, DESIGN K1): s*V was computed once per tile by the pre-shrink pass
+// (kernels_tc.cu smlm_u_kernel, vf), so the n-tile is the full 256 W rows and the expand is one
+// extra K-block whose A operand is the tile-compact s*V loaded by TMA.  PRE = false keeps the
+// fused variant (SMLM_FUSED_SHRINK=1): A_a stacked under the W n-tile so the shrink rides in the
+// N=256 MMA and V never leaves the SM pair (n-tile 256 - r_pad).  Each work item covers TWO
+// 128-row tiles of the same segment (same adapter), one per CTA of a cluster pair.  The pair issues one M=256 MMA per K-step: each CTA stages its own 128 X rows and HALF
 // of the 256-row B tile (W rows [n0, n0+128) in CTA 0; W rows [n0+128, n0+BNW) + A_a in CTA 1),
 // halving the per-SM operand traffic of the 1-CTA kernel; 6 pipeline stages of 32 KB.
 // Only the leader CTA (rank 0) issues MMAs; completions are multicast to both CTAs.
