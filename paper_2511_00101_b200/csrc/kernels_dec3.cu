@@ -142,6 +142,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT3, 1) smlm_dec3_ke
     constexpr uint32_t RB = RP * 2;
     constexpr uint32_t kSwR = RB >= 128 ? kSw128 : (RB == 64 ? kSw64 : kSw32);
     constexpr int APC = 128 / RP;   // stacked adapters per CTA of a V tile
+    // expand adapters per ring stage (16 KB A + 16 KB B per CTA); flags & 128: one (A/B measurement)
+    const int EPS = (a.flags & 128) ? 1 : 64 / RP;
     const int ST = a.stages;
     const uint32_t ystage = base + ST * kStage3;   // 2 x 8 KB bf16 Y staging (TMA store)
     const uint32_t bar = ystage + 2 * kYStage;
@@ -276,17 +278,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT3, 1) smlm_dec3_ke
                 dbg_stamp(a, 2);
             }
             __syncwarp();
-            for (int iu = 0; iu < s_ucount; ++iu) {
-                const int u = s_ulist[iu];
-                const int sl = s_uslot[u];
+            // EPS adapters per ring stage (each: 128 slab rows + 128 B_u rows per CTA), issued
+            // lane-parallel: a split's expand is one or two ring rounds instead of one per adapter
+            for (int iu0 = 0; iu0 < s_ucount; iu0 += EPS) {
+                const int na = min(EPS, s_ucount - iu0);
                 mbar_wait(empty_bar(stage), phase ^ 1);
-                if (lane == 0) {
-                    const uint32_t fb = map_to_rank(full_bar(stage), 0);
-                    if (leader) mbar_expect_tx(full_bar(stage), 2u * 256u * RB);
-                    tma_load_2d_pair(a_addr(stage), &P.tmSV, fb, 0, (it.g * a.n_uniq + u) * 256 + 128 * (int)rank);
-                    const SlotDev *sd = P.slots + sl;
-                    tma_load_2d_pair(b_addr(stage), &sd->tmBk, fb, 0, wrow);
-                    tma_load_2d_pair(b_addr(stage) + 64u * RB, &sd->tmBk, fb, 0, wrow + 64);
+                const uint32_t fb = map_to_rank(full_bar(stage), 0);
+                if (lane == 0 && leader) mbar_expect_tx(full_bar(stage), (uint32_t)na * 2u * 256u * RB);
+                __syncwarp();
+                if (lane < na) {
+                    const int u = s_ulist[iu0 + lane];
+                    const SlotDev *sd = P.slots + s_uslot[u];
+                    const uint32_t off = (uint32_t)lane * 128u * RB;
+                    tma_load_2d_pair(a_addr(stage) + off, &P.tmSV, fb, 0, (it.g * a.n_uniq + u) * 256 + 128 * (int)rank);
+                    tma_load_2d_pair(b_addr(stage) + off, &sd->tmBk, fb, 0, wrow);
+                    tma_load_2d_pair(b_addr(stage) + off + 64u * RB, &sd->tmBk, fb, 0, wrow + 64);
                 }
                 __syncwarp();
                 if (++stage == ST) { stage = 0; phase ^= 1; }
@@ -315,15 +321,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT3, 1) smlm_dec3_ke
             if (++stage == ST) { stage = 0; phase ^= 1; }
         }
         const int n_exp = it.vtile ? 0 : s_ucount;
-        for (int iu = 0; iu < n_exp; ++iu) {
+        for (int iu0 = 0; iu0 < n_exp; iu0 += EPS) {
+            const int na = min(EPS, n_exp - iu0);
             mbar_wait(full_bar(stage), phase);
             tc_fence_after();
             if (lane == 0) {
-                const uint32_t ab = a_addr(stage), bb = b_addr(stage);
+                for (int jj = 0; jj < na; ++jj) {
+                    const uint32_t ab = a_addr(stage) + (uint32_t)jj * 128u * RB, bb = b_addr(stage) + (uint32_t)jj * 128u * RB;
 #pragma unroll
-                for (int kk = 0; kk < RP / 16; ++kk)
-                    mma2_bf16(tmem_base, smem_desc(ab + 32u * kk, 16, 8u * RB, kSwR),
-                              smem_desc(bb + 32u * kk, 16, 8u * RB, kSwR), idesc, 1u);
+                    for (int kk = 0; kk < RP / 16; ++kk)
+                        mma2_bf16(tmem_base, smem_desc(ab + 32u * kk, 16, 8u * RB, kSwR),
+                                  smem_desc(bb + 32u * kk, 16, 8u * RB, kSwR), idesc, 1u);
+                }
                 mma2_commit_mc(empty_bar(stage));
             }
             __syncwarp();
