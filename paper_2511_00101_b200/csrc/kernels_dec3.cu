@@ -412,7 +412,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT3, 1) smlm_dec3_ke
 #pragma unroll
                     for (int q = 0; q < RP / 4; ++q) __stcg(dst + q, make_float4(vp[4 * q], vp[4 * q + 1], vp[4 * q + 2], vp[4 * q + 3]));
                 }
-                __threadfence();
+                // the CTA barrier orders every thread's partial stores before thread 0's gpu-scope
+                // release (cumulative), as in a split-K semaphore: no per-thread fence
+                if (a.flags & 256) __threadfence();
                 named_bar_sync(1, 128);
                 if (tid_e == 0) {
                     dbg_stamp(a, 3);
@@ -482,7 +484,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT3, 1) smlm_dec3_ke
             }
             // publish: the slabs are read by TMA (async proxy) in other CTAs
             fence_proxy_async_global();
-            __threadfence();
+            if (a.flags & 256) __threadfence();
             named_bar_sync(1, 128);
             if (tid_e == 0) {
                 atom_add_release_gpu(a.ctr, 1);
@@ -503,7 +505,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT3, 1) smlm_dec3_ke
                         __stcg(dst + q * 128, make_float4(__uint_as_float(rr[4 * q]), __uint_as_float(rr[4 * q + 1]),
                                                           __uint_as_float(rr[4 * q + 2]), __uint_as_float(rr[4 * q + 3])));
                 }
-                __threadfence();
+                if (a.flags & 256) __threadfence();   // (see the V tiles: barrier + release by thread 0)
                 named_bar_sync(1, 128);
                 if (tid_e == 0) {
                     dbg_stamp(a, 3);
