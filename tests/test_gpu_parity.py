@@ -546,3 +546,16 @@ def test_bf16_mixed_multi_projection(r, outs):
         single = run_smlm(batch, w, X, None, backward=False)
         assert torch.equal(single.Y, Ys[i]), f"projection {i}: multi differs from the single call"
         assert torch.equal(single.V[ft_lora], Vs[i][ft_lora]), i
+
+
+def test_full_c4_qkv_multi_sampled():
+    """C4 (unified batch, full size) q/k/v through smlm_forward_multi: the shared pre-shrink at
+    13 448 rows and 64 adapters, checked on sampled rows of every projection."""
+    batch = synth.config_batch(4)
+    ws_ = [synth.config_weights(4, p) for p in ("q", "k", "v")]
+    X, _ = synth.config_activations(4, "q", batch.S)
+    Ys, Vs, launches = _run_multi(batch, ws_, X)
+    rows = synth.sample_rows(batch, every=97)
+    for i, w in enumerate(ws_):
+        Y, _ = oracle.forward(batch, w.W, w.A, w.B, w.slot_scale, X, rows=rows)
+        assert parity_err(Ys[i].double().numpy()[rows], Y[rows]) <= BF16_TOL, i
