@@ -150,14 +150,20 @@ def test_launch_count_and_no_host_sync(S):
     # warm-up: the first launch of each kernel loads its module (CUDA lazy loading), which may
     # synchronize; the property under test is steady-state asynchrony
     pool.forward(b, X, Wd)
+    # every device buffer exists before the asynchrony probe (a caching-allocator cudaMalloc inside
+    # the probe may synchronize the device and is not the library's doing)
+    Ypre = torch.empty(203, 256, dtype=torch.bfloat16, device="cuda")
+    wspre = pool.workspace(b, False)
     torch.cuda.synchronize()
     n0 = S.smlm_launch_count()
     side = torch.cuda.Stream()
+    big = torch.randn(8192, 8192, device="cuda", dtype=torch.bfloat16)
+    tmp = torch.empty_like(big)
+    torch.cuda.synchronize()
     with torch.cuda.stream(side):
-        big = torch.randn(8192, 8192, device="cuda", dtype=torch.bfloat16)
         for _ in range(16):                           # keep the GPU busy ~10 ms on this stream
-            big = big @ big.T * 1e-2
-        Y = pool.forward(b, X, Wd, stream=side)
+            torch.matmul(big, big.T, out=tmp)
+        Y = pool.forward(b, X, Wd, Y=Ypre, ws=wspre, stream=side)
         done = torch.cuda.Event()
         done.record(side)
     assert not done.query()                           # the call returned before the GPU finished
