@@ -1552,8 +1552,9 @@ int smlm_backward(smlm_pool p, const smlm_batch *b, const void *X, const void *W
         ta.out_f = p->out;
         ta.r = p->r;
         ta.r_pad = p->r_pad;
-        ta.mt_a = (p->in + 127) / 128;
-        ta.mt_b = (p->out + 127) / 128;
+        ta.nh = env_flag("SMLM_TOK_NARROW") ? 1 : 2;   // 256-column items (measurement override)
+        ta.mt_a = (p->in + 128 * ta.nh - 1) / (128 * ta.nh);
+        ta.mt_b = (p->out + 128 * ta.nh - 1) / (128 * ta.nh);
         ta.accumulate = accumulate ? 1 : 0;
         CKL(launch_tok(ta, p->num_sms, st), 1);
     }

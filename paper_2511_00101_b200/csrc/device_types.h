@@ -137,8 +137,9 @@ struct TokArgs {
     int out_f;
     int r;
     int r_pad;
-    int mt_a;           // ceil(in/128)
-    int mt_b;           // ceil(out/128)
+    int mt_a;           // ceil(in / (128 nh)): column items of dA^T
+    int mt_b;           // ceil(out / (128 nh)): column items of dB
+    int nh;             // 128-column halves per item (1 or 2)
     int accumulate;
     int stages;
 };

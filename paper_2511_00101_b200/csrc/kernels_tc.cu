@@ -409,11 +409,11 @@ int launch_impl(const GemmArgs &a, int num_sms, size_t smem, cudaStream_t st) {
 // ==========================================================================================
 // pipeline depth: as many stages as shared memory holds (HBM-bound stream of 64-token K-blocks;
 // bytes in flight per SM are what keep the memory system busy), at most 12
-template <int RP>
+template <int RP, int NH = 1>
 constexpr int tok_stages() {
-    return (int)((232448u - 1280u) / (16384u + ((64u * RP * 2u + 1023u) & ~1023u))) > 12
+    return (int)((232448u - 1280u) / (16384u * NH + ((64u * RP * 2u + 1023u) & ~1023u))) > 12
                ? 12
-               : (int)((232448u - 1280u) / (16384u + ((64u * RP * 2u + 1023u) & ~1023u)));
+               : (int)((232448u - 1280u) / (16384u * NH + ((64u * RP * 2u + 1023u) & ~1023u)));
 }
 
 __device__ __forceinline__ bool tok_item(const TokArgs &a, int w, int &g, int &mt, bool &is_b) {
@@ -431,18 +431,21 @@ __device__ __forceinline__ bool tok_item(const TokArgs &a, int w, int &g, int &m
     return a.groups[g].dB != nullptr;
 }
 
-template <int RP>
+// NH = 2: an item covers 256 columns (two 128-column halves, two accumulators sharing the s*U /
+// s*V operand): each token row is read as 512 contiguous bytes per K-block instead of 256
+template <int RP, int NH>
 __global__ void __launch_bounds__(kThreads, 1) smlm_tok_kernel(const __grid_constant__ TokArgs args) {
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw = smem_u32(smem_raw);
     const uint32_t base = (raw + 1023u) & ~1023u;
     uint8_t *base_ptr = smem_raw + (base - raw);
     constexpr uint32_t RB = RP * 2;
-    constexpr uint32_t kA = 16384;              // 64 tokens x 128 columns bf16 (2 boxes of 8 KB)
+    constexpr uint32_t kA = 16384 * NH;         // 64 tokens x 128*NH columns bf16 (2*NH boxes of 8 KB)
     constexpr uint32_t kB = 64 * RB;            // 64 tokens x r_pad
     constexpr uint32_t kStage = kA + ((kB + 1023u) & ~1023u);
     constexpr uint32_t kSwR = RB >= 128 ? kSw128 : (RB == 64 ? kSw64 : kSw32);
-    constexpr int ST = tok_stages<RP>();
+    constexpr int ST = tok_stages<RP, NH>();
+    constexpr uint32_t kTm = 2 * NH * RP <= 128 ? 128 : 256;
     const uint32_t bar = base + ST * kStage;
     auto full_bar = [&](int s) { return bar + 8u * s; };
     auto empty_bar = [&](int s) { return bar + 8u * (ST + s); };
@@ -463,7 +466,7 @@ __global__ void __launch_bounds__(kThreads, 1) smlm_tok_kernel(const __grid_cons
         mbar_init(accf0 + 24, 128);
         fence_mbar_init();
     }
-    if (warp == 2) tmem_alloc(tmem_slot, 128);
+    if (warp == 2) tmem_alloc(tmem_slot, kTm);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -481,8 +484,10 @@ __global__ void __launch_bounds__(kThreads, 1) smlm_tok_kernel(const __grid_cons
             if (!tok_item(args, w, g, mt, is_b)) continue;
             const GradGroup grp = args.groups[g];
             const int M = is_b ? args.out_f : args.in_f;
-            const int m0 = mt * 128;
-            const bool two = m0 + 64 < M;
+            const int m0 = mt * 128 * NH;
+            int nbox = 0;   // 64-column boxes of this item inside M (in/out are multiples of 64)
+#pragma unroll
+            for (int bx = 0; bx < 2 * NH; ++bx) nbox += (m0 + 64 * bx < M);
             const CUtensorMap *ma = is_b ? &args.tmDY : &args.tmX;
             const CUtensorMap *mb = is_b ? &args.tmSV : &args.tmSU;
             for (int ti = 0; ti < grp.n_tiles; ++ti) {
@@ -491,9 +496,9 @@ __global__ void __launch_bounds__(kThreads, 1) smlm_tok_kernel(const __grid_cons
                 for (int kb = 0; kb * 64 < t.rows; ++kb) {
                     mbar_wait(empty_bar(stage), phase ^ 1);
                     if (lane == 0) {
-                        mbar_expect_tx(full_bar(stage), (two ? kA : kA / 2) + kB);
-                        tma_load_2d(a_addr(stage), ma, full_bar(stage), m0, t.row0 + 64 * kb);
-                        if (two) tma_load_2d(a_addr(stage) + 8192, ma, full_bar(stage), m0 + 64, t.row0 + 64 * kb);
+                        mbar_expect_tx(full_bar(stage), (uint32_t)nbox * 8192u + kB);
+                        for (int bx = 0; bx < nbox; ++bx)
+                            tma_load_2d(a_addr(stage) + 8192u * bx, ma, full_bar(stage), m0 + 64 * bx, t.row0 + 64 * kb);
                         tma_load_2d(b_addr(stage), mb, full_bar(stage), 0, tix * 128 + 64 * kb);
                     }
                     __syncwarp();
@@ -514,7 +519,8 @@ __global__ void __launch_bounds__(kThreads, 1) smlm_tok_kernel(const __grid_cons
             const uint32_t buf = it & 1;
             mbar_wait(accf0 + 16 + 8 * buf, ((it >> 1) & 1) ^ 1);
             tc_fence_after();
-            const uint32_t acc = tmem_base + buf * RP;
+            const uint32_t acc = tmem_base + buf * NH * RP;
+            const int nh = (NH == 2 && mt * 256 + 128 < (is_b ? args.out_f : args.in_f)) ? 2 : 1;
             uint32_t acc_on = 0;
             for (int ti = 0; ti < grp.n_tiles; ++ti) {
                 const DevTile t = args.tiles[grp.tile_begin + ti];
@@ -524,8 +530,8 @@ __global__ void __launch_bounds__(kThreads, 1) smlm_tok_kernel(const __grid_cons
                     if (valid < 64) {
                         // zero token rows past the segment end in both 64-column boxes
                         uint8_t *ap = base_ptr + (a_addr(stage) - base);
-                        for (int e = lane; e < (64 - valid) * 16; e += 32) {
-                            const int row = valid + (e >> 4), box = (e >> 3) & 1, ch = e & 7;
+                        for (int e = lane; e < (64 - valid) * 8 * 2 * NH; e += 32) {
+                            const int row = valid + e / (16 * NH), box = (e >> 3) % (2 * NH), ch = e & 7;
                             *reinterpret_cast<uint4 *>(ap + box * 8192 + row * 128 + ch * 16) = make_uint4(0, 0, 0, 0);
                         }
                         fence_proxy_async_smem();
@@ -535,9 +541,11 @@ __global__ void __launch_bounds__(kThreads, 1) smlm_tok_kernel(const __grid_cons
                     if (lane == 0) {
                         const uint32_t ab = a_addr(stage), bb = b_addr(stage);
                         for (int k = 0; k * 16 < valid; ++k) {
-                            const uint64_t ad = smem_desc(ab + 2048u * k, 8192, 1024, kSw128);
                             const uint64_t bd = smem_desc(bb + 16u * RB * k, 64u * RB, 8u * RB, kSwR);
-                            mma_bf16(acc, ad, bd, idesc, acc_on);
+                            for (int h = 0; h < nh; ++h) {
+                                const uint64_t ad = smem_desc(ab + 16384u * h + 2048u * k, 8192, 1024, kSw128);
+                                mma_bf16(acc + (uint32_t)h * RP, ad, bd, idesc, acc_on);
+                            }
                             acc_on = 1;
                         }
                         mma_commit(empty_bar(stage));
@@ -563,19 +571,24 @@ __global__ void __launch_bounds__(kThreads, 1) smlm_tok_kernel(const __grid_cons
             const uint32_t buf = it & 1;
             mbar_wait(accf0 + 8 * buf, (it >> 1) & 1);
             tc_fence_after();
-            uint32_t v[RP];
+            uint32_t vv[NH][RP];
 #pragma unroll
-            for (int c = 0; c < RP; c += 16) {
-                uint32_t tmp[16];
-                tmem_ld16(tmem_base + buf * RP + lane_base + c, tmp);
-                tmem_wait_ld();
+            for (int h = 0; h < NH; ++h)
 #pragma unroll
-                for (int j = 0; j < 16; ++j) v[c + j] = tmp[j];
-            }
+                for (int c = 0; c < RP; c += 16) {
+                    uint32_t tmp[16];
+                    tmem_ld16(tmem_base + buf * NH * RP + h * RP + lane_base + c, tmp);
+                    tmem_wait_ld();
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) vv[h][c + j] = tmp[j];
+                }
             tc_fence_before();
             mbar_arrive(accf0 + 16 + 8 * buf);
             const int M = is_b ? args.out_f : args.in_f;
-            const int col = mt * 128 + m;
+#pragma unroll
+            for (int h = 0; h < NH; ++h) {
+            const uint32_t *v = vv[h];
+            const int col = mt * 128 * NH + 128 * h + m;
             if (col < M) {
                 if (is_b) {
                     float *p = grp.dB + (size_t)col * grp.r;   // the adapter's own rank
@@ -591,21 +604,22 @@ __global__ void __launch_bounds__(kThreads, 1) smlm_tok_kernel(const __grid_cons
                         }
                 }
             }
+            }
             ++it;
         }
     }
     __syncthreads();
     if (warp == 2) {
         tc_fence_after();
-        tmem_dealloc(tmem_base, 128);
+        tmem_dealloc(tmem_base, kTm);
     }
 }
 
-template <int RP>
+template <int RP, int NH>
 int launch_tok_impl(const TokArgs &a, int num_sms, cudaStream_t st) {
-    auto kern = smlm_tok_kernel<RP>;
-    constexpr size_t kStage = 16384 + ((64 * RP * 2 + 1023) & ~1023);
-    const size_t smem = 1024 + tok_stages<RP>() * kStage + 256;
+    auto kern = smlm_tok_kernel<RP, NH>;
+    constexpr size_t kStage = 16384 * NH + ((64 * RP * 2 + 1023) & ~1023);
+    const size_t smem = 1024 + tok_stages<RP, NH>() * kStage + 256;
     static bool attr_done = false;
     if (!attr_done) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -918,10 +932,13 @@ int launch_u(const UArgs &a, int num_sms, cudaStream_t st) {
 
 int launch_tok(const TokArgs &a, int num_sms, cudaStream_t st) {
     if (a.n_groups == 0) return 0;
-    switch (a.r_pad) {
-        case 16: return launch_tok_impl<16>(a, num_sms, st);
-        case 32: return launch_tok_impl<32>(a, num_sms, st);
-        case 64: return launch_tok_impl<64>(a, num_sms, st);
+    switch (a.r_pad * (a.nh == 2 ? -1 : 1)) {
+        case 16: return launch_tok_impl<16, 1>(a, num_sms, st);
+        case 32: return launch_tok_impl<32, 1>(a, num_sms, st);
+        case 64: return launch_tok_impl<64, 1>(a, num_sms, st);
+        case -16: return launch_tok_impl<16, 2>(a, num_sms, st);
+        case -32: return launch_tok_impl<32, 2>(a, num_sms, st);
+        case -64: return launch_tok_impl<64, 2>(a, num_sms, st);
     }
     return (int)cudaErrorInvalidValue;
 }
