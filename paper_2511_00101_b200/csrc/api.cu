@@ -53,7 +53,7 @@ int launch_adamw_sumsq(const float *g, size_t n, float gscale, float *partial, i
 int launch_adamw_step(const AdamwArgs &a, int grid, cudaStream_t st);
 int launch_shrink_split(const __nv_bfloat16 *X, const SlotDev *slots, const DevBlock *blocks,
                         const DevShortRow *srows, int n_blocks, int in_f, int r, int r_pad, float *part,
-                        __nv_bfloat16 *Vbd, __nv_bfloat16 *Vsave, cudaStream_t st);
+                        __nv_bfloat16 *Vbd, __nv_bfloat16 *Vsave, int *ctr, cudaStream_t st);
 size_t grad_group_bytes();
 void fill_grad_group(void *dst, int slot, int tile_begin, int n_tiles, int r, float *dA, float *dB);
 template <typename T, typename TV>
@@ -1117,9 +1117,12 @@ int smlm_forward(smlm_pool p, const smlm_batch *b, const void *X, const void *W,
     if (!plan.blocks.empty()) {
         ProfScope ps(2, st);
         if (L.spart_bytes) {
+            // the last chunk of each block combines it in-kernel (pool counters, self-resetting)
+            int *sctr = ((int)plan.blocks.size() <= kUCtrMax && !env_flag("SMLM_SHRINK_SEPARATE_COMBINE")) ? p->d_uctr
+                                                                                                          : nullptr;
             CKL(launch_shrink_split((const __nv_bfloat16 *)X, p->d_slots, d_blocks, d_srows, (int)plan.blocks.size(),
                                     p->in, p->r, p->r_pad, reinterpret_cast<float *>(wsb + L.spart_off), Vbd,
-                                    (__nv_bfloat16 *)V_save, st), 2);
+                                    (__nv_bfloat16 *)V_save, sctr, st), sctr ? 1 : 2);
         } else {
             CKL(launch_shrink_short((const __nv_bfloat16 *)X, p->d_slots, d_blocks, d_srows,
                                     (int)plan.blocks.size(), p->in, p->r, p->r_pad, Vbd, (__nv_bfloat16 *)V_save,

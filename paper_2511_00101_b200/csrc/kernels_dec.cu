@@ -46,12 +46,54 @@ __device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
 }
 
+// combine partials in chunk order -> block-diagonal s*V (bf16 [128, RP]) and V_save of block bi
+// (256 threads; idx_of[128] and vals[128 * RP] in shared memory)
+template <int RP>
+__device__ __forceinline__ void shrink_combine_block(int bi, const DevBlock *__restrict__ blocks,
+                                                     const DevShortRow *__restrict__ srows, int nch, int r,
+                                                     const float *__restrict__ part, __nv_bfloat16 *__restrict__ Vbd,
+                                                     __nv_bfloat16 *__restrict__ Vsave, int *idx_of, float *vals) {
+    const DevBlock blk = blocks[bi];
+    for (int i = threadIdx.x; i < 128; i += blockDim.x) idx_of[i] = -1;
+    __syncthreads();
+    for (int i = threadIdx.x; i < blk.nrows; i += blockDim.x) idx_of[srows[blk.row_begin + i].pos] = i;
+    const float *src = part + (size_t)bi * nch * 128 * RP;
+    for (int e = threadIdx.x; e < blk.nrows * RP; e += blockDim.x) {
+        const int i = e / RP, j = e % RP;
+        float v = 0.f;
+        if (j < r) {
+            float t[16];
+#pragma unroll
+            for (int c = 0; c < 16; ++c) t[c] = c < nch ? __ldcg(src + (size_t)c * 128 * RP + i * RP + j) : 0.f;
+            for (int c = 0; c < nch && c < 16; ++c) v += t[c];   // chunk order
+            for (int c = 16; c < nch; ++c) v += __ldcg(src + (size_t)c * 128 * RP + i * RP + j);
+        }
+        vals[i * RP + j] = v;
+    }
+    __syncthreads();
+    __nv_bfloat16 *dst = Vbd + (size_t)bi * 128 * RP;
+    for (int e = threadIdx.x; e < 128 * RP; e += blockDim.x) {
+        const int p = e / RP, j = e % RP;
+        const int i = idx_of[p];
+        dst[e] = __float2bfloat16_rn(i < 0 ? 0.f : srows[blk.row_begin + i].scale * vals[i * RP + j]);
+    }
+    if (Vsave) {
+        for (int e = threadIdx.x; e < blk.nrows * r; e += blockDim.x) {
+            const int i = e / r, j = e % r;
+            const DevShortRow sr = srows[blk.row_begin + i];
+            if (sr.ft) Vsave[(size_t)sr.row * r + j] = __float2bfloat16_rn(vals[i * RP + j]);
+        }
+    }
+}
+
 template <int RP>
 __global__ void __launch_bounds__(256) shrink_partial_kernel(const __nv_bfloat16 *__restrict__ X,
                                                              const SlotDev *__restrict__ slots,
                                                              const DevBlock *__restrict__ blocks,
                                                              const DevShortRow *__restrict__ srows, int in_f,
-                                                             int r, float *__restrict__ part) {
+                                                             int r, float *__restrict__ part, int *ctr,
+                                                             __nv_bfloat16 *__restrict__ Vbd,
+                                                             __nv_bfloat16 *__restrict__ Vsave) {
     // A_u[:, chunk] and the block's x rows [:, chunk] are staged in shared memory with coalesced
     // 128-bit loads (every byte read once); then warp w computes outputs (i, j) = w, w+8, ...:
     // lane l reduces columns [16 l, 16 l + 16) and a xor-shuffle tree finishes.
@@ -102,9 +144,30 @@ __global__ void __launch_bounds__(256) shrink_partial_kernel(const __nv_bfloat16
             if (lane == 0) dst[(rb + i) * RP + j] = acc;
         }
     }
+    if (ctr) {
+        // the last chunk of the block to finish combines it (no second launch): barrier, then one
+        // gpu-scope fence + counter by thread 0 (split-K semaphore); the counter returns to 0
+        __shared__ int s_last;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            __threadfence();
+            const int old = atomicAdd(ctr + blockIdx.x, 1);
+            s_last = old == nch - 1;
+            if (s_last) {
+                ctr[blockIdx.x] = 0;
+                __threadfence();
+            }
+        }
+        __syncthreads();
+        if (s_last) {
+            // the staged A / X tiles are no longer needed: reuse the dynamic shared memory
+            int *idx_of = reinterpret_cast<int *>(sm);
+            float *vals = reinterpret_cast<float *>(sm + 512);
+            shrink_combine_block<RP>(blockIdx.x, blocks, srows, nch, r, part, Vbd, Vsave, idx_of, vals);
+        }
+    }
 }
 
-// combine partials in chunk order -> block-diagonal s*V (bf16 [128, RP]) and V_save
 template <int RP>
 __global__ void __launch_bounds__(256) shrink_combine_kernel(const DevBlock *__restrict__ blocks,
                                                              const DevShortRow *__restrict__ srows, int nch,
@@ -113,39 +176,9 @@ __global__ void __launch_bounds__(256) shrink_combine_kernel(const DevBlock *__r
                                                              __nv_bfloat16 *__restrict__ Vsave) {
     pdl_wait();
     pdl_trigger();
-    const DevBlock blk = blocks[blockIdx.x];
     __shared__ int idx_of[128];
-    __shared__ float vals[128][RP];
-    for (int i = threadIdx.x; i < 128; i += blockDim.x) idx_of[i] = -1;
-    __syncthreads();
-    for (int i = threadIdx.x; i < blk.nrows; i += blockDim.x) idx_of[srows[blk.row_begin + i].pos] = i;
-    const float *src = part + (size_t)blockIdx.x * nch * 128 * RP;
-    for (int e = threadIdx.x; e < blk.nrows * RP; e += blockDim.x) {
-        const int i = e / RP, j = e % RP;
-        float v = 0.f;
-        if (j < r) {
-            float t[16];
-#pragma unroll
-            for (int c = 0; c < 16; ++c) t[c] = c < nch ? __ldcg(src + (size_t)c * 128 * RP + i * RP + j) : 0.f;
-            for (int c = 0; c < nch && c < 16; ++c) v += t[c];   // chunk order
-            for (int c = 16; c < nch; ++c) v += __ldcg(src + (size_t)c * 128 * RP + i * RP + j);
-        }
-        vals[i][j] = v;
-    }
-    __syncthreads();
-    __nv_bfloat16 *dst = Vbd + (size_t)blockIdx.x * 128 * RP;
-    for (int e = threadIdx.x; e < 128 * RP; e += blockDim.x) {
-        const int p = e / RP, j = e % RP;
-        const int i = idx_of[p];
-        dst[e] = __float2bfloat16_rn(i < 0 ? 0.f : srows[blk.row_begin + i].scale * vals[i][j]);
-    }
-    if (Vsave) {
-        for (int e = threadIdx.x; e < blk.nrows * r; e += blockDim.x) {
-            const int i = e / r, j = e % r;
-            const DevShortRow sr = srows[blk.row_begin + i];
-            if (sr.ft) Vsave[(size_t)sr.row * r + j] = __float2bfloat16_rn(vals[i][j]);
-        }
-    }
+    __shared__ float vals[128 * RP];
+    shrink_combine_block<RP>(blockIdx.x, blocks, srows, nch, r, part, Vbd, Vsave, idx_of, vals);
 }
 
 }  // namespace
@@ -154,29 +187,31 @@ int dec_chunks(int in_f) { return in_f / kChunk > 0 && in_f % kChunk == 0 ? in_f
 
 int launch_shrink_split(const __nv_bfloat16 *X, const SlotDev *slots, const DevBlock *blocks,
                         const DevShortRow *srows, int n_blocks, int in_f, int r, int r_pad, float *part,
-                        __nv_bfloat16 *Vbd, __nv_bfloat16 *Vsave, cudaStream_t st) {
+                        __nv_bfloat16 *Vbd, __nv_bfloat16 *Vsave, int *ctr, cudaStream_t st) {
     if (n_blocks == 0) return 0;
     const int nch = dec_chunks(in_f);
     dim3 g1(n_blocks, nch);
     cudaError_t e = cudaSuccess;
     switch (r_pad) {
         case 16:
-            e = launch_pdl(shrink_partial_kernel<16>, g1, dim3(256), (16 + kRowsPerPass) * kChunk * 2, st, X, slots, blocks, srows, in_f, r, part);
-            if (e != cudaSuccess) return (int)e;
+            cudaFuncSetAttribute(shrink_partial_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (16 + kRowsPerPass) * kChunk * 2);
+            e = launch_pdl(shrink_partial_kernel<16>, g1, dim3(256), (16 + kRowsPerPass) * kChunk * 2, st, X, slots, blocks, srows, in_f, r, part, ctr, Vbd, Vsave);
+            if (e != cudaSuccess || ctr) break;
             e = launch_pdl(shrink_combine_kernel<16>, dim3(n_blocks), dim3(256), 0, st, blocks, srows, nch, r, part, Vbd, Vsave);
             break;
         case 32:
             cudaFuncSetAttribute(shrink_partial_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (32 + kRowsPerPass) * kChunk * 2);
-            e = launch_pdl(shrink_partial_kernel<32>, g1, dim3(256), (32 + kRowsPerPass) * kChunk * 2, st, X, slots, blocks, srows, in_f, r, part);
-            if (e != cudaSuccess) return (int)e;
+            e = launch_pdl(shrink_partial_kernel<32>, g1, dim3(256), (32 + kRowsPerPass) * kChunk * 2, st, X, slots, blocks, srows, in_f, r, part, ctr, Vbd, Vsave);
+            if (e != cudaSuccess || ctr) break;
             e = launch_pdl(shrink_combine_kernel<32>, dim3(n_blocks), dim3(256), 0, st, blocks, srows, nch, r, part, Vbd, Vsave);
             break;
         case 64:
             cudaFuncSetAttribute(shrink_partial_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (64 + kRowsPerPass) * kChunk * 2);
-            e = launch_pdl(shrink_partial_kernel<64>, g1, dim3(256), (64 + kRowsPerPass) * kChunk * 2, st, X, slots, blocks, srows, in_f, r, part);
-            if (e != cudaSuccess) return (int)e;
+            e = launch_pdl(shrink_partial_kernel<64>, g1, dim3(256), (64 + kRowsPerPass) * kChunk * 2, st, X, slots, blocks, srows, in_f, r, part, ctr, Vbd, Vsave);
+            if (e != cudaSuccess || ctr) break;
             e = launch_pdl(shrink_combine_kernel<64>, dim3(n_blocks), dim3(256), 0, st, blocks, srows, nch, r, part, Vbd, Vsave);
             break;
         default: return (int)cudaErrorInvalidValue;
