@@ -1478,6 +1478,11 @@ int smlm_backward(smlm_pool p, const smlm_batch *b, const void *X, const void *W
         u.r_pad = p->r_pad;
         u.part = reinterpret_cast<float *>(wsb + L.upart_off);
         u.sUt = sUt;
+        if (V_save && n_grad && !env_flag("SMLM_SEPARATE_PREP_SV")) {   // s*V folded into the reduce
+            u.Vsave_in = V_save;
+            u.sVt = sVt;
+            u.r = p->r;
+        }
         u.ctr = (u.n_items <= kUCtrMax && !env_flag("SMLM_U_SEPARATE_REDUCE")) ? p->d_uctr : nullptr;
         CKL(launch_u(u, p->num_sms, st), u.ctr ? 1 : 2);
     }
@@ -1535,7 +1540,9 @@ int smlm_backward(smlm_pool p, const smlm_batch *b, const void *X, const void *W
     if (n_grad) {
         ProfScope ps(3, st);
         if (V_save) {
-            CKL(launch_prep_sv<__nv_bfloat16>(d_tiles, nt, (const __nv_bfloat16 *)V_save, p->r, p->r_pad, sVt, st), 1);
+            const bool folded = L.u_items && !env_flag("SMLM_SEPARATE_PREP_SV");   // done by the U pass
+            if (!folded)
+                CKL(launch_prep_sv<__nv_bfloat16>(d_tiles, nt, (const __nv_bfloat16 *)V_save, p->r, p->r_pad, sVt, st), 1);
         } else {
             CKL(launch_rows_shrink<__nv_bfloat16>(d_tiles, nt, p->d_slots, (const __nv_bfloat16 *)X, p->in, p->r, Vf,
                                                   nullptr, 0, st), 1);

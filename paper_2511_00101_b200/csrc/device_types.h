@@ -117,6 +117,10 @@ struct UArgs {
     int *ctr;   // per-item split arrival counters (pool-owned, self-resetting) or NULL: separate reduce
     // npj > 1: forward pre-shrink of npj projections sharing X in one pass (npj * r_pad <= 128):
     // projection p's adapters from slots_p[p], its s*V / V_save to sUt_p[p] / Vsave_p[p]
+    // backward (vf = 0): also write the tile-compact s*V of the same tiles from V_save (the dB
+    // operand of the token contraction), folded into the reduction
+    const void *Vsave_in;
+    void *sVt;
     int npj;
     const SlotDev *slots_p[4];
     void *sUt_p[4];

@@ -694,6 +694,16 @@ __device__ __forceinline__ void u_reduce_row(const UArgs &args, int item, int m)
         dst[c] = pk;
     }
     }
+    if (!args.vf && args.sVt) {
+        const __nv_bfloat16 *vin = reinterpret_cast<const __nv_bfloat16 *>(args.Vsave_in);
+        __nv_bfloat16 *dv = reinterpret_cast<__nv_bfloat16 *>(args.sVt) + ((size_t)ti * 128 + m) * RP;
+#pragma unroll
+        for (int j = 0; j < RP; ++j) {
+            float v = 0.f;
+            if (m < t.rows && j < args.r) v = t.scale * __bfloat162float(vin[(size_t)(t.row0 + m) * args.r + j]);
+            dv[j] = __float2bfloat16_rn(v);
+        }
+    }
 }
 
 // stand-alone reduce (when the kernel has no arrival counters)
