@@ -158,3 +158,30 @@ def test_adapter_params_train_step(S):
     Y2 = pool.forward(b, X, W)
     assert not torch.equal(Y, Y2)
     pool.close()
+
+
+def test_adamw_full_size_sampled(S):
+    """The bench's F3 workload size (4 fine-tune adapters x r=16 x 7 Llama-3-8B projections x 32
+    layers = 167.8 M parameters) in the launch configuration bench.py times (clip 1.0, zero_grad,
+    bf16 copy): sampled elements against the oracle, with the clip coefficient of the oracle
+    computed in fp64 over the whole gradient."""
+    n = 4 * synth.lora_param_count(16) * 32
+    dev = torch.device("cuda", 0)
+    g = torch.Generator(device=dev).manual_seed(123)
+    P = torch.randn(n, device=dev, generator=g) * 0.02
+    M = torch.randn(n, device=dev, generator=g) * 1e-4
+    V = (torch.randn(n, device=dev, generator=g) * 1e-6).abs()
+    G = torch.randn(n, device=dev, generator=g) * 1e-3
+    idx = torch.randint(0, n, (200000,), device=dev, generator=g)
+    p0, m0, v0, g0 = (x[idx].double().cpu().numpy() for x in (P, M, V, G))
+    gnorm = float(torch.linalg.vector_norm(G.double()).item())
+    PB = torch.empty(n, dtype=torch.bfloat16, device=dev)
+    W = torch.empty(S.smlm_adamw_workspace_size() // 4, device=dev)
+    S.smlm_adamw_step(P, M, V, G, PB, 5, 2e-5, weight_decay=0.01, max_grad_norm=1.0, zero_grad=True, ws=W)
+    torch.cuda.synchronize()
+    coef = min(1.0, 1.0 / (gnorm + 1e-6))
+    ref = OA.adamw_step(p0, m0, v0, g0 * coef, 5, 2e-5, weight_decay=0.01)   # clip applied with the full norm
+    got = (P[idx].cpu(), M[idx].cpu(), V[idx].cpu())
+    _check(got, ref, (p0, m0, v0, g0 * coef), lr=2e-5, wd=0.01)
+    assert bool((G[idx] == 0).all())
+    assert torch.equal(PB[idx], P[idx].to(torch.bfloat16))
