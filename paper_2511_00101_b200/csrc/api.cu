@@ -1138,6 +1138,7 @@ int smlm_forward(smlm_pool p, const smlm_batch *b, const void *X, const void *W,
         ProfScope ps(2, st);
         UArgs u;
         memset(&u, 0, sizeof(u));
+        u.kw1 = env_flag("SMLM_U_KW1") ? 1 : 0;
         if ((rc = make_map(&u.tmDY, X, p->in, b->S, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B))) return rc;
         u.slots = p->d_slots;
         u.tiles = d_tiles;
@@ -1339,6 +1340,7 @@ int smlm_forward_multi(int n_proj, const smlm_pool *pools, const smlm_batch *b, 
         if ((rc = stage_upload(p0, bytes, wsb + M.plan_off, st))) return rc;
         UArgs u;
         memset(&u, 0, sizeof(u));
+        u.kw1 = env_flag("SMLM_U_KW1") ? 1 : 0;
         if ((rc = make_map_cached(p0, &u.tmDY, X, p0->in, b->S, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B))) return rc;
         u.slots = p0->d_slots;
         u.tiles = reinterpret_cast<const DevTile *>(wsb + M.plan_off);
@@ -1468,6 +1470,7 @@ int smlm_backward(smlm_pool p, const smlm_batch *b, const void *X, const void *W
     if (L.u_items && (dX || n_grad)) {
         UArgs u;
         memset(&u, 0, sizeof(u));
+        u.kw1 = env_flag("SMLM_U_KW1") ? 1 : 0;
         if ((rc = make_map(&u.tmDY, dY, p->out, b->S, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B))) return rc;
         u.slots = p->d_slots;
         u.tiles = d_tiles;

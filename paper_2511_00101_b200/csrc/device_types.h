@@ -121,6 +121,7 @@ struct UArgs {
     // operand of the token contraction), folded into the reduction
     const void *Vsave_in;
     void *sVt;
+    int kw1;    // measurement override: one K-block per ring stage
     int npj;
     const SlotDev *slots_p[4];
     void *sUt_p[4];

@@ -647,10 +647,11 @@ int launch_tok_impl(const TokArgs &a, int num_sms, cudaStream_t st) {
 // holds (the pass is a latency-bound stream of small K-blocks: depth is what keeps HBM busy)
 template <int RP, int NPJ = 1>
 constexpr uint32_t u_stage_bytes() { return kABytes + ((64u * RP * 2u * NPJ + 1023u) & ~1023u); }
-template <int RP, int NPJ = 1>
+template <int RP, int NPJ = 1, int KW = 1>
 constexpr int u_stages() {
-    return (int)((232448u - 1280u) / u_stage_bytes<RP, NPJ>()) > 12 ? 12
-                                                                      : (int)((232448u - 1280u) / u_stage_bytes<RP, NPJ>());
+    return (int)((232448u - 1280u) / (KW * u_stage_bytes<RP, NPJ>())) > 12
+               ? 12
+               : (int)((232448u - 1280u) / (KW * u_stage_bytes<RP, NPJ>()));
 }
 
 // sUt[tile*128 + m][j] = bf16(s * sum_split part) (zero rows past the segment), split order fixed
@@ -713,7 +714,9 @@ __global__ void __launch_bounds__(128) u_reduce_kernel(const __grid_constant__ U
     u_reduce_row<RP, NPJ>(args, blockIdx.x, threadIdx.x);
 }
 
-template <int RP, int NPJ>
+// KW = 2: a ring stage holds two consecutive 64-wide K-blocks (sub-stages), so each token row is
+// requested as 256 contiguous bytes at a time
+template <int RP, int NPJ, int KW>
 __global__ void __launch_bounds__(kThreads, 1) smlm_u_kernel(const __grid_constant__ UArgs args) {
     // VF (args.vf): the forward pre-shrink V = X A_a^T of long tiles -- same split-K contraction,
     // the adapter operand A_a [r, in] K-major (tmA box {64, r_pad}) instead of B_a MN-major
@@ -723,8 +726,9 @@ __global__ void __launch_bounds__(kThreads, 1) smlm_u_kernel(const __grid_consta
     uint8_t *base_ptr = smem_raw + (base - raw);
     constexpr uint32_t RB = RP * 2;
     constexpr uint32_t kSwR = RB >= 128 ? kSw128 : (RB == 64 ? kSw64 : kSw32);
-    constexpr uint32_t kStg = u_stage_bytes<RP, NPJ>();
-    constexpr int ST = u_stages<RP, NPJ>();
+    constexpr uint32_t kStg1 = u_stage_bytes<RP, NPJ>();   // one 64-wide K-block (sub-stage)
+    constexpr uint32_t kStg = KW * kStg1;
+    constexpr int ST = u_stages<RP, NPJ, KW>();
     constexpr int NC = NPJ * RP;                        // accumulator columns (one TMEM buffer)
     constexpr uint32_t kTm = 2 * NC <= 128 ? 128 : 256; // two buffers
     const uint32_t bar = base + ST * kStg;
@@ -732,8 +736,8 @@ __global__ void __launch_bounds__(kThreads, 1) smlm_u_kernel(const __grid_consta
     auto empty_bar = [&](int s) { return bar + 8u * (ST + s); };
     const uint32_t accf0 = bar + 16u * ST;   // acc_full[2], acc_empty[2]
     const uint32_t tmem_slot = accf0 + 32;
-    auto a_addr = [&](int s) { return base + s * kStg; };
-    auto b_addr = [&](int s) { return base + s * kStg + kABytes; };
+    auto a_addr = [&](int s, int i = 0) { return base + s * kStg + i * kStg1; };
+    auto b_addr = [&](int s, int i = 0) { return base + s * kStg + i * kStg1 + kABytes; };
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
         for (int s = 0; s < ST; ++s) {
@@ -770,21 +774,25 @@ __global__ void __launch_bounds__(kThreads, 1) smlm_u_kernel(const __grid_consta
             const SlotDev *sd = args.slots + t.slot;
             int kb0, kb1;
             kb_range(split, kb0, kb1);
-            for (int kb = kb0; kb < kb1; ++kb) {
+            for (int kb = kb0; kb < kb1; kb += KW) {
+                const int nb = min(KW, kb1 - kb);
                 mbar_wait(empty_bar(stage), phase ^ 1);
                 if (lane == 0) {
-                    mbar_expect_tx(full_bar(stage), kABytes + 64u * RB * NPJ);
-                    tma_load_2d(a_addr(stage), &args.tmDY, full_bar(stage), kb * kBK, t.row0);
-                    if (NPJ > 1) {
-                        // the A_a of every projection stacked: N = NPJ * r_pad rows of the B operand
+                    mbar_expect_tx(full_bar(stage), (uint32_t)nb * (kABytes + 64u * RB * NPJ));
+                    for (int i = 0; i < nb; ++i)   // the X rows of both sub-stages back to back
+                        tma_load_2d(a_addr(stage, i), &args.tmDY, full_bar(stage), (kb + i) * kBK, t.row0);
+                    for (int i = 0; i < nb; ++i) {
+                        if (NPJ > 1) {
+                            // the A_a of every projection stacked: N = NPJ * r_pad rows of the B operand
 #pragma unroll
-                        for (int pj = 0; pj < NPJ; ++pj)
-                            tma_load_2d(b_addr(stage) + (uint32_t)pj * RP * 128u, &args.slots_p[pj][t.slot].tmA,
-                                        full_bar(stage), kb * kBK, 0);
-                    } else if (args.vf) {
-                        tma_load_2d(b_addr(stage), &sd->tmA, full_bar(stage), kb * kBK, 0);
-                    } else {
-                        tma_load_2d(b_addr(stage), &sd->tmBk, full_bar(stage), 0, kb * kBK);
+                            for (int pj = 0; pj < NPJ; ++pj)
+                                tma_load_2d(b_addr(stage, i) + (uint32_t)pj * RP * 128u, &args.slots_p[pj][t.slot].tmA,
+                                            full_bar(stage), (kb + i) * kBK, 0);
+                        } else if (args.vf) {
+                            tma_load_2d(b_addr(stage, i), &sd->tmA, full_bar(stage), (kb + i) * kBK, 0);
+                        } else {
+                            tma_load_2d(b_addr(stage, i), &sd->tmBk, full_bar(stage), 0, (kb + i) * kBK);
+                        }
                     }
                 }
                 __syncwarp();
@@ -805,20 +813,23 @@ __global__ void __launch_bounds__(kThreads, 1) smlm_u_kernel(const __grid_consta
             mbar_wait(accf0 + 16 + 8 * b, (u & 1) ^ 1);
             tc_fence_after();
             uint32_t acc_on = 0;
-            for (int kb = kb0; kb < kb1; ++kb) {
+            for (int kb = kb0; kb < kb1; kb += KW) {
+                const int nb = min(KW, kb1 - kb);
                 mbar_wait(full_bar(stage), phase);
                 tc_fence_after();
                 if (lane == 0) {
-                    const uint32_t ab = a_addr(stage), bb = b_addr(stage);
+                    for (int i = 0; i < nb; ++i) {
+                        const uint32_t ab = a_addr(stage, i), bb = b_addr(stage, i);
 #pragma unroll
-                    for (int k = 0; k < kBK / 16; ++k) {
-                        if (vf)
-                            mma_bf16(acc, smem_desc(ab + 32u * k, 16, 1024, kSw128),
-                                     smem_desc(bb + 32u * k, 16, 1024, kSw128), idesc_v, acc_on);
-                        else
-                            mma_bf16(acc, smem_desc(ab + 32u * k, 16, 1024, kSw128),
-                                     smem_desc(bb + 16u * RB * k, 64u * RB, 8u * RB, kSwR), idesc_u, acc_on);
-                        acc_on = 1;
+                        for (int k = 0; k < kBK / 16; ++k) {
+                            if (vf)
+                                mma_bf16(acc, smem_desc(ab + 32u * k, 16, 1024, kSw128),
+                                         smem_desc(bb + 32u * k, 16, 1024, kSw128), idesc_v, acc_on);
+                            else
+                                mma_bf16(acc, smem_desc(ab + 32u * k, 16, 1024, kSw128),
+                                         smem_desc(bb + 16u * RB * k, 64u * RB, 8u * RB, kSwR), idesc_u, acc_on);
+                            acc_on = 1;
+                        }
                     }
                     mma_commit(empty_bar(stage));
                 }
@@ -880,11 +891,11 @@ __global__ void __launch_bounds__(kThreads, 1) smlm_u_kernel(const __grid_consta
     }
 }
 
-template <int RP, int NPJ = 1>
+template <int RP, int NPJ = 1, int KW = 2>
 int launch_u_impl(const UArgs &a, int num_sms, cudaStream_t st) {
-    auto kern = smlm_u_kernel<RP, NPJ>;
-    constexpr size_t kStg = u_stage_bytes<RP, NPJ>();
-    const size_t smem = 1024 + u_stages<RP, NPJ>() * kStg + 256;
+    auto kern = smlm_u_kernel<RP, NPJ, KW>;
+    constexpr size_t kStg = KW * u_stage_bytes<RP, NPJ>();
+    const size_t smem = 1024 + u_stages<RP, NPJ, KW>() * kStg + 256;
     static bool attr_done = false;
     if (!attr_done) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -929,6 +940,14 @@ int launch_u(const UArgs &a, int num_sms, cudaStream_t st) {
             case 32 * 8 + 3: return launch_u_impl<32, 3>(a, num_sms, st);
             case 32 * 8 + 4: return launch_u_impl<32, 4>(a, num_sms, st);
             case 64 * 8 + 2: return launch_u_impl<64, 2>(a, num_sms, st);
+        }
+        return (int)cudaErrorInvalidValue;
+    }
+    if (a.kw1) {   // one 64-wide K-block per ring stage (measurement override)
+        switch (a.r_pad) {
+            case 16: return launch_u_impl<16, 1, 1>(a, num_sms, st);
+            case 32: return launch_u_impl<32, 1, 1>(a, num_sms, st);
+            case 64: return launch_u_impl<64, 1, 1>(a, num_sms, st);
         }
         return (int)cudaErrorInvalidValue;
     }
