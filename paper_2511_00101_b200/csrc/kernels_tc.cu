@@ -29,7 +29,6 @@ using namespace sm100;
 namespace {
 
 constexpr int kThreads = 256;
-constexpr int kGroupM = 8;  // m-tiles per raster group (L2 reuse of W n-tiles and X m-tiles)
 constexpr uint32_t kABytes = 128 * 128;   // X/dY tile: 128 rows x 64 bf16
 constexpr uint32_t kBBytes = 256 * 128;   // W tile: 256 x 64 bf16
 
