@@ -243,7 +243,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT3, 1) smlm_dec3_ke
         if (!it.vtile && s_ucount > 0) {
             // the s*V slabs are published by the V tiles
             if (lane == 0) {
-                while (ld_acquire_gpu(a.ctr) < v_target) __nanosleep(64);
+                while (ld_acquire_gpu(a.ctr) < v_target) {   // one thread per CTA: a tight spin is cheapest
+                }
                 fence_proxy_async_global();
                 dbg_stamp(a, 2);
             }
@@ -390,7 +391,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT3, 1) smlm_dec3_ke
                     dbg_stamp(a, 3);
                     int *arrive = a.ctr + 2 + it.tile;
                     atom_add_release_gpu(arrive, 1);
-                    while (ld_acquire_gpu(arrive) < 2 * ks) __nanosleep(32);
+                    while (ld_acquire_gpu(arrive) < 2 * ks) {
+                    }
                     dbg_stamp(a, 5);
                 }
                 named_bar_sync(1, 128);
@@ -481,7 +483,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT3, 1) smlm_dec3_ke
                     dbg_stamp(a, 3);
                     int *arrive = a.ctr + 2 + it.tile;
                     atom_add_release_gpu(arrive, 1);
-                    while (ld_acquire_gpu(arrive) < 2 * ks) __nanosleep(32);
+                    while (ld_acquire_gpu(arrive) < 2 * ks) {
+                    }
                     dbg_stamp(a, 5);
                 }
                 named_bar_sync(1, 128);
