@@ -25,7 +25,9 @@ PEAKS = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.ex
 NSETS = 8
 
 
-def run_config(k, iters=30, graphs=False):
+def run_config(k, iters=30, graphs=False, ranks=None):
+    """ranks: optional per-adapter ranks (<= the config's) -- heterogeneous ranks in one pool
+    (SURVEY f2): adapter a is registered with its first ranks[a] rank indices."""
     spec = synth.CONFIGS[k]
     dev = torch.device("cuda", 0)
     batch = synth.config_batch(k)
@@ -47,14 +49,20 @@ def run_config(k, iters=30, graphs=False):
             A = (torch.randn(U, r, in_f, generator=g, device=dev) / math.sqrt(in_f)).to(torch.bfloat16)
             B = (torch.randn(U, out_f, r, generator=g, device=dev) / (4 * math.sqrt(r))).to(torch.bfloat16)
             pool = S.Pool(in_f, out_f, r, U, S.SMLM_BF16, 0)
+            keep = []
             for a in range(U):
-                pool.register(A[a], B[a], 2.0)
+                if ranks is None or ranks[a] == r:
+                    pool.register(A[a], B[a], 2.0)
+                else:
+                    Aa, Ba = A[a][:ranks[a]].contiguous(), B[a][:, :ranks[a]].contiguous()
+                    keep += [Aa, Ba]
+                    pool.register(Aa, Ba, 2.0)
             ws = torch.empty(S.smlm_workspace_size(pool.h, b, False) + 256, dtype=torch.uint8, device=dev)
-            sets.append((W, A, B, pool, ws))
+            sets.append((W, A, B, pool, ws, keep))
         st = torch.cuda.current_stream()
 
         def call(i):
-            W, _, _, pool, ws = sets[i % NSETS]
+            W, _, _, pool, ws, _ = sets[i % NSETS]
             S.smlm_forward(pool.h, b, X, W, Y, None, ws, st)
         for i in range(2 * NSETS):
             call(i)
@@ -213,6 +221,13 @@ def adamw_step(layers=32, clip=1.0, iters=20):
 
 
 def main():
+    if "--hetero" in sys.argv:
+        # C3 (gate/up/down, 8 adapters at r=64) with uniform ranks vs mixed 64/32/16/8
+        _, t_u = run_config(3, iters=10)
+        _, t_h = run_config(3, iters=10, ranks=[64, 64, 32, 32, 16, 16, 8, 8])
+        print(json.dumps({"config": "C3-prefill", "uniform_r64_ms": t_u, "hetero_64_32_16_8_ms": t_h,
+                          "ratio": t_h / t_u}), flush=True)
+        return
     print(json.dumps(c2_layer_step(graphs="--c2-only" not in sys.argv)), flush=True)
     if "--c2-only" in sys.argv:
         return
