@@ -193,12 +193,26 @@ class Workload:
         S = self.S
         layer = self.layers[L]
         forward_groups(S, layer, self.b, lambda p: self.X[GROUP_OF[p]], self.Y, self.V, stream)
-        for p in reversed(synth.PROJECTIONS):
+        # the 7 backward calls are independent (own pool, workspace, dX, dA/dB): alternate them over
+        # two streams so one projection's GEMM tail / small kernels overlap the next one's
+        two = comm is None and os.environ.get("BENCH_BWD_STREAMS", "2") == "2"
+        if two:
+            if getattr(self, "_s2", None) is None:
+                self._s2 = torch.cuda.Stream(self.dev)
+            ev = torch.cuda.Event()
+            ev.record(stream)
+            self._s2.wait_event(ev)
+        for i, p in enumerate(reversed(synth.PROJECTIONS)):
             e = layer[p]
+            st = self._s2 if (two and i % 2 == 1) else stream
             S.smlm_backward(e["pool"].h, self.b, self.X[GROUP_OF[p]], e["W"], self.dY[p], self.V[p], self.dX[p],
-                            0, e["wsb"], stream)
+                            0, e["wsb"], st)
             if comm is not None:
                 comm(e["grad"])
+        if two:
+            ev2 = torch.cuda.Event()
+            ev2.record(self._s2)
+            stream.wait_event(ev2)
 
 
 def forward_groups(S, layer, b, X_of, Y, V, stream, groups=None):
