@@ -192,7 +192,21 @@ class Workload:
     def step(self, L: int, stream, comm=None):
         S = self.S
         layer = self.layers[L]
-        forward_groups(S, layer, self.b, lambda p: self.X[GROUP_OF[p]], self.Y, self.V, stream)
+        two_f = comm is None and os.environ.get("BENCH_FWD_STREAMS", "1") == "2"
+        if two_f:
+            if getattr(self, "_s2", None) is None:
+                self._s2 = torch.cuda.Stream(self.dev)
+            ev0 = torch.cuda.Event()
+            ev0.record(stream)
+            self._s2.wait_event(ev0)
+            for gi, grp in enumerate(FWD_GROUPS):
+                forward_groups(S, layer, self.b, lambda p: self.X[GROUP_OF[p]], self.Y, self.V,
+                               self._s2 if gi % 2 else stream, [grp])
+            ev1 = torch.cuda.Event()
+            ev1.record(self._s2)
+            stream.wait_event(ev1)
+        else:
+            forward_groups(S, layer, self.b, lambda p: self.X[GROUP_OF[p]], self.Y, self.V, stream)
         # the 7 backward calls are independent (own pool, workspace, dX, dA/dB): alternate them over
         # two streams so one projection's GEMM tail / small kernels overlap the next one's
         two = comm is None and os.environ.get("BENCH_BWD_STREAMS", "2") == "2"
