@@ -37,10 +37,16 @@
  * There is no CPU fallback: a device that is not sm_100 gives SMLM_E_UNSUPPORTED.
  *
  * Threading: all work is stream-ordered on the given stream with no host synchronisation
- * (the plan is staged through a pinned ring buffer).  A pool must be used by one host thread
- * at a time, and its forward calls must be ordered on one stream (or otherwise serialised):
- * the decode kernel keeps self-resetting cross-CTA counters in pool-owned device memory.
- * Each launch of that kernel needs its CTAs co-resident (one wave of <= 148 CTAs).
+ * (plans ride in kernel parameters or a pinned ring buffer).  A pool must be used by one host
+ * thread at a time.  Its calls may be issued on several streams (e.g. the next micro-batch's
+ * forward overlapping this one's backward): the self-resetting cross-CTA counters of the split-K
+ * passes and of the decode kernel are kept per launching stream, so only calls on the SAME
+ * stream share them, and those are ordered.  A CUDA graph keeps the counters of its capture
+ * stream: do not replay it concurrently with direct calls issued on that capture stream.
+ * The decode kernel spin-waits across CTAs: its grid is capped to one co-resident wave
+ * (cudaOccupancyMaxActiveClusters; a pure decode batch that does not fit takes the mixed-batch
+ * path), and decode calls that may run concurrently on several streams need the pool option
+ * SMLM_OPT_DEC_COOPERATIVE (cooperative launch).
  */
 #ifndef SMLM_H_
 #define SMLM_H_
@@ -81,7 +87,15 @@ enum smlm_dtype { SMLM_BF16 = 0, SMLM_FP32 = 1 };
 /* Options for smlm_pool_set_option */
 enum smlm_option {
     SMLM_OPT_L_LONG = 0,  /* segments with >= L_long rows take the long (per-segment tile) path; default 64 */
-    SMLM_OPT_CTA_PAIR = 1 /* 1 (default): forward long tiles on CTA pairs (tcgen05 cta_group::2); 0: one CTA */
+    SMLM_OPT_CTA_PAIR = 1, /* 1 (default): forward long tiles on CTA pairs (tcgen05 cta_group::2); 0: one CTA */
+    SMLM_OPT_DECODE_KERNEL = 2, /* 1 (default): pure short/decode batches of <= 512 rows take the
+                                 * single-launch decode kernel; 0: the mixed-batch path (same math) */
+    SMLM_OPT_DEC_KSPLIT = 3,    /* decode kernel W split-K factor in [1, 8]; 0 (default) = automatic.
+                                 * Changes only the fp32 summation order (results within tolerance) */
+    SMLM_OPT_DEC_COOPERATIVE = 4 /* 1: launch the decode kernel cooperatively (whole grid co-scheduled);
+                                  * needed when decode calls of several pools/streams can run at once
+                                  * (two partially resident spin-waiting grids could wait on each
+                                  * other).  0 (default): grid capped to one co-resident wave */
 };
 
 /*
@@ -202,9 +216,12 @@ SMLM_API int smlm_plan_export(smlm_pool pool, const smlm_batch *batch, int backw
 
 /*
  * AdamW step over the fine-tune adapters' parameters (Table 5, P:1067:
- * HF Trainer, learning_rate 2e-5; optimizer defaults = DESIGN.md R9; masking P:422 = the caller
- * puts only the trained adapters' parameters in the buffer).  All buffers are DEVICE memory of n
- * elements with the same flat layout (e.g. every trained adapter's A then B, concatenated):
+ * HF Trainer, learning_rate 2e-5; optimizer defaults = DESIGN.md R12; masking P:422 = the caller
+ * puts only the trained adapters' parameters in the buffer).  One call = one optimizer step of ONE
+ * fine-tune job (each job is its own trainer: its own clip norm over its own parameters and its
+ * own step count; optim.AdamW calls this once per job on the job's contiguous sub-range of a
+ * shared flat store).  All buffers are DEVICE memory of n elements with the same flat layout
+ * (e.g. the job's adapters' A then B, concatenated):
  *   param [n] fp32 master weights, exp_avg [n], exp_avg_sq [n] fp32 optimizer state -- updated;
  *   grad [n] fp32 -- the (all-reduced) gradient sum; read, and zeroed if zero_grad != 0;
  *   param_bf16 [n] bf16 or NULL -- receives bf16(param) after the update (the tensors the pools

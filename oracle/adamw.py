@@ -3,7 +3,7 @@
 SURVEY.md §8(f3): "a fused masked AdamW step on the LoRA params (lr 2e-5)" after the per-adapter
 gradient reduction.  PAPER.md Table 5 ("Training Args") fixes learning_rate 2e-5 and
 gradient_accumulation_steps 4 for the HF Trainer runs but is silent on the optimizer itself; the
-reading (R9) is the HF Trainer default, AdamW (decoupled weight decay, Loshchilov &
+reading (R12) is the HF Trainer default, AdamW (decoupled weight decay, Loshchilov &
 Hutter) with betas (0.9, 0.999), eps 1e-8, weight_decay 0.0 and global gradient-norm clipping at
 max_grad_norm 1.0.  Masking (MixedLoRAModelForTrainer: each trainer updates only its own
 adapter) is the caller's choice of which adapters' parameters form the flat buffer.

@@ -46,6 +46,7 @@ int launch_prep_sv(const DevTile *tiles, int n_tiles, const TV *V, int r, int r_
 int launch_tok(const TokArgs &a, int num_sms, cudaStream_t st);
 int dec_chunks(int in_f);
 int dec3_stages();
+int dec3_max_clusters(int r_pad);
 int launch_dec3(const Dec3Args &a, const Dec3Inline &in, int clusters, cudaStream_t st);
 int launch_plan_copy(void *dst, const void *src, size_t n, cudaStream_t st);
 int adamw_grid(int num_sms, size_t n);
@@ -73,11 +74,22 @@ using namespace smlm;
 static thread_local std::string g_last_error;
 static std::atomic<uint64_t> g_launches{0};
 
-// optional host-side phase timing (SMLM_HOST_PROF=1): microseconds per phase, printed at exit
+// Measurement-only switches exist only in a library built with -DSMLM_MEASURE (build.py --measure
+// -> libsmlm_measure.so); the release library reads no environment variable.  None of them
+// changes a result: SMLM_HOST_PROF prints host phase times, SMLM_DEC3_DEBUG records per-CTA
+// phase timestamps of the decode kernel in the workspace tail.
 #include <chrono>
 #include <cmath>
+#ifdef SMLM_MEASURE
+static bool measure_flag(const char *name) {
+    const char *e = getenv(name);
+    return e && *e && strcmp(e, "0") != 0;
+}
+#else
+static constexpr bool measure_flag(const char *) { return false; }
+#endif
 struct HostProf {
-    bool on = getenv("SMLM_HOST_PROF") != nullptr;
+    bool on = measure_flag("SMLM_HOST_PROF");
     double t[8] = {0};
     long n = 0;
     ~HostProf() {
@@ -86,25 +98,6 @@ struct HostProf {
                     t[0] / n, t[1] / n, t[2] / n, t[3] / n, t[4] / n);
     }
 } g_hprof;
-// measurement overrides read once per process (getenv scans the environment on every call)
-static int env_int(const char *name) {
-    static std::mutex mu;
-    static std::vector<std::pair<std::string, int>> cache;
-    std::lock_guard<std::mutex> lk(mu);
-    for (auto &kv : cache)
-        if (kv.first == name) return kv.second;
-    // unset or empty -> 0; a number -> its value ("0" disables); any other text -> 1
-    const char *e = getenv(name);
-    int v = 0;
-    if (e && *e) {
-        char *end = nullptr;
-        const long x = strtol(e, &end, 10);
-        v = end != e ? (int)x : 1;
-    }
-    cache.emplace_back(name, v);
-    return v;
-}
-static bool env_flag(const char *name) { return env_int(name) != 0; }
 static inline double now_us() {
     return std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now().time_since_epoch()).count();
 }
@@ -274,13 +267,20 @@ struct smlm_pool_s {
     int in = 0, out = 0, r = 0, r_pad = 16, cap = 0, dtype = 0;
     int l_long = 64;
     int cta_pair = 1;   // forward long tiles on CTA pairs (cta_group::2)
+    int dec_kernel = 1; // pure decode batches take the single-launch decode kernel (SMLM_OPT_DECODE_KERNEL)
+    int dec_ksplit = 0; // decode W split-K factor, 0 = automatic (SMLM_OPT_DEC_KSPLIT)
+    int dec_coop = 0;   // cooperative decode launches (SMLM_OPT_DEC_COOPERATIVE)
     int num_sms = 148;
     std::vector<SlotHost> slots;
     std::vector<uint8_t> ok;
     std::vector<float> scales;
     SlotDev *d_slots = nullptr;
-    int *d_ctr = nullptr;   // decode kernel: self-resetting cross-CTA counters (dec3_counter_ints())
-    int *d_uctr = nullptr;  // U / pre-shrink pass: self-resetting per-item split counters (kUCtrMax)
+    // self-resetting cross-CTA counters, one set per launching stream (calls on one stream are
+    // ordered; calls of one pool on different streams -- e.g. the next micro-batch's forward
+    // overlapping this one's backward -- must not share them): [0, dec3_counter_ints()) decode
+    // kernel, then kUCtrMax per-item split counters of the U / pre-shrink / short-shrink passes
+    struct CtrSet { cudaStream_t st; int *d; };
+    std::vector<CtrSet> ctrs;
     // encoded TMA descriptors of recently used (pointer, shape, box) keys: steady-state calls reuse them
     struct MapEnt {
         const void *ptr;
@@ -320,6 +320,42 @@ int check_sticky() {
     return SMLM_OK;
 }
 
+// The pool's counter set of stream `st`: pool_create pre-allocates kCtrSets zeroed sets that are
+// bound to streams on first use (no allocation or memset on the call path, so calls can be
+// captured into CUDA graphs); more streams allocate further sets outside graph capture.
+constexpr int kCtrSets = 4;
+size_t ctr_set_ints() { return (size_t)dec3_counter_ints() + kUCtrMax; }
+int stream_counters(smlm_pool p, cudaStream_t st, int **dec_ctr, int **u_ctr) {
+    int *d = nullptr;
+    for (auto &c : p->ctrs)
+        if (c.d && c.st == st) d = c.d;
+    if (!d)
+        for (auto &c : p->ctrs)
+            if (c.d && c.st == (cudaStream_t)-1) {   // a free pre-allocated set
+                c.st = st;
+                d = c.d;
+                break;
+            }
+    if (!d) {
+        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+        cudaStreamIsCapturing(st, &cs);
+        if (cs != cudaStreamCaptureStatusNone)
+            return set_err(SMLM_E_UNSUPPORTED, "graph capture on a new stream: this pool already serves its maximum of "
+                                               "streams; issue one call on the stream outside capture first");
+        cudaError_t e = cudaMalloc(&d, ctr_set_ints() * sizeof(int));
+        if (e != cudaSuccess) return cuda_err(e, "cudaMalloc(counters)");
+        e = cudaMemset(d, 0, ctr_set_ints() * sizeof(int));
+        if (e != cudaSuccess) {
+            cudaFree(d);
+            return cuda_err(e, "cudaMemset(counters)");
+        }
+        p->ctrs.push_back({st, d});
+    }
+    if (dec_ctr) *dec_ctr = d;
+    if (u_ctr) *u_ctr = d + dec3_counter_ints();
+    return SMLM_OK;
+}
+
 // Sizes of the workspace sections for a planned call.
 struct WsLayout {
     size_t plan_off = 0, plan_bytes = 0;
@@ -340,12 +376,6 @@ struct WsLayout {
 // (measured against ~4 units per SM with >= 8 K-blocks: finer splits cost more partial traffic
 // and power than they gain in balance, 1-2 % of the C4 step)
 static int u_ksplit(int num_sms, int items, int nkb) {
-    if (env_flag("SMLM_U_KS_FINE")) {   // measurement A/B: ~4 units per SM, >= 8 K-blocks each
-        int ks = (4 * num_sms + items - 1) / items;
-        const int cap = nkb / 8 > 1 ? nkb / 8 : 1;
-        if (ks > cap) ks = cap;
-        return ks < 1 ? 1 : ks;
-    }
     int ks = num_sms / items;
     if (ks > nkb / 4) ks = nkb / 4;
     return ks < 1 ? 1 : ks;
@@ -356,10 +386,8 @@ static int u_ksplit(int num_sms, int items, int nkb) {
 static thread_local const void *t_ext_pre_sv = nullptr;
 
 // forward pre-shrink (s*V once per long tile, then full 256-column W tiles; DESIGN K1) on the
-// CTA-pair path; SMLM_FUSED_SHRINK=1 restores the per-n-tile fused shrink (measurement)
-static bool use_preshrink(smlm_pool p) {
-    return p->dtype == SMLM_BF16 && p->cta_pair && !env_flag("SMLM_FUSED_SHRINK");
-}
+// CTA-pair path (the 1-CTA kernel keeps the shrink fused into its N=256 MMA)
+static bool use_preshrink(smlm_pool p) { return p->dtype == SMLM_BF16 && p->cta_pair; }
 
 int plan_for(smlm_pool p, const smlm_batch *b, bool bwd, Plan &plan) {
     std::string msg;
@@ -408,7 +436,7 @@ Dec3Plan dec3_plan(int n_proj, const smlm_pool *pools, const smlm_batch *b, cons
     Dec3Plan D;
     smlm_pool p0 = pools[0];
     if (p0->dtype != SMLM_BF16 || !plan.long_tiles.empty() || plan.short_tiles.empty() || b->S > kDec3InlineRows ||
-        env_flag("SMLM_NO_DEC3"))
+        !p0->dec_kernel)
         return D;
     // adapters of the batch (ascending) and per-row records
     D.rows.assign(b->S, Dec3RowInfo{-1, 0.f, 0, 0});
@@ -436,7 +464,9 @@ Dec3Plan dec3_plan(int n_proj, const smlm_pool *pools, const smlm_batch *b, cons
     D.n_groups = (b->S + 255) / 256;
     for (int i = 0; i < n_proj; ++i) D.nw += (pools[i]->out + 255) / 256;
     D.n_vt = (n_uniq * p0->r_pad + 255) / 256;
-    const int pairs = std::min(p0->num_sms / 2, kDec3MaxPairs);
+    // one co-resident wave (the kernel spin-waits across CTAs; launched cooperatively)
+    const int pairs = std::min(std::min(p0->num_sms / 2, kDec3MaxPairs), dec3_max_clusters(p0->r_pad));
+    if (pairs < 2) return D;
     const int NW = D.n_groups * D.nw, NV = D.n_groups * n_proj * D.n_vt;
     const int nkb = p0->in / kBK;
     const int kmax = std::max(1, std::min(8, nkb / 2));
@@ -445,13 +475,12 @@ Dec3Plan dec3_plan(int n_proj, const smlm_pool *pools, const smlm_batch *b, cons
     // the V tiles (shrink) get the rest, as many splits as fit (they must publish before the W
     // tiles finish their main loop)
     int best_ks = std::max(1, std::min(kmax, (pairs * 3 / 4) / std::max(NW, 1)));
-    if (const char *e = getenv("SMLM_DEC_KSPLIT"))   // measurement / test override (read per call)
-        best_ks = std::max(1, std::min(atoi(e), kmax));
+    if (p0->dec_ksplit > 0)   // pool option SMLM_OPT_DEC_KSPLIT (tests: every split count is parity-checked)
+        best_ks = std::max(1, std::min(p0->dec_ksplit, kmax));
     while (best_ks > 1 && NW * best_ks + NV > pairs) --best_ks;   // (only with very many adapters)
     // V splits (up to 16): fewer K-blocks per split keep all of a split's loads in
     // flight in the 6-stage ring (the V chain is load-latency bound, not bandwidth bound)
-    const int kmax_v = std::max(1, std::min(env_int("SMLM_DEC3_KSV_MAX") > 0 ? env_int("SMLM_DEC3_KSV_MAX") : 16,
-                                            nkb / 2));
+    const int kmax_v = std::max(1, std::min(16, nkb / 2));
     int best_ksv = NV ? std::max(1, std::min(kmax_v, (pairs - NW * best_ks) / NV)) : 1;
     if (NW * best_ks + NV * best_ksv > pairs) best_ks = 0;
     if (best_ks == 0) return D;   // more tiles than one wave: not this kernel
@@ -470,7 +499,7 @@ Dec3Plan dec3_plan(int n_proj, const smlm_pool *pools, const smlm_batch *b, cons
     }
     D.kpart_off = off;
     off = align256(off + (size_t)D.clusters * 2 * 8 * kDec3ChunkBytes);
-    if (env_flag("SMLM_DEC3_DEBUG")) off += 2 * kDec3MaxPairs * 16 * 8;   // phase timestamps at the tail
+    if (measure_flag("SMLM_DEC3_DEBUG")) off += 2 * kDec3MaxPairs * 16 * 8;   // phase timestamps at the tail
     D.total = off;
     D.ok = true;
     return D;
@@ -550,9 +579,11 @@ WsLayout layout_for(smlm_pool p, const smlm_batch *b, const Plan &plan, bool bwd
 }
 
 // Copy a host byte vector into the workspace through the pinned ring (stream ordered).
-int stage_upload(smlm_pool p, const std::vector<uint8_t> &bytes, void *dst, cudaStream_t st) {
+// via_memcpy: always a copy-engine transfer (slot-table updates: TMA descriptors must never be
+// written by a kernel that its PDL successors overlap)
+int stage_upload(smlm_pool p, const std::vector<uint8_t> &bytes, void *dst, cudaStream_t st, bool via_memcpy = false) {
     if (bytes.empty()) return SMLM_OK;
-    if (!env_flag("SMLM_PLAN_MEMCPY")) {
+    if (!via_memcpy) {
         // small plans ride in kernel parameters (kernels_plan.cu): never queued behind bulk DMA
         const int rc = launch_plan_copy(dst, bytes.data(), bytes.size(), st);
         if (rc == 0) {
@@ -603,25 +634,15 @@ int run_dec3(int n_proj, const smlm_pool *pools, const smlm_batch *b, const Dec3
     const int n_uniq = (int)D.uslot.size();
     int rc;
     double t0 = g_hprof.on ? now_us() : 0;
-    static thread_local Dec3Inline inl;   // kernel parameter block (copied at launch)
-    const bool no_inline = env_flag("SMLM_DEC3_NOINLINE");   // measurement override
-    const bool inline_plan = !no_inline;   // sizes are bounded by dec3_plan (<= 256 adapters, <= 512 rows)
-    size_t rows_off = 0;
-    if (inline_plan) {
-        if (n_uniq) memcpy(inl.uslot, D.uslot.data(), n_uniq * sizeof(int));
-        if (!D.rows.empty()) memcpy(inl.rows, D.rows.data(), D.rows.size() * sizeof(Dec3RowInfo));
-    } else {
-        std::vector<uint8_t> bytes;
-        append(bytes, D.uslot);
-        while (bytes.size() % 16) bytes.push_back(0);
-        rows_off = bytes.size();
-        append(bytes, D.rows);
-        if ((rc = stage_upload(p0, bytes, wsb + D.plan_off, st))) return rc;
-    }
+    // the plan rides in the kernel parameters (sizes bounded by dec3_plan: <= 256 adapters, <= 512 rows)
+    static thread_local Dec3Inline inl;
+    if (n_uniq) memcpy(inl.uslot, D.uslot.data(), n_uniq * sizeof(int));
+    if (!D.rows.empty()) memcpy(inl.rows, D.rows.data(), D.rows.size() * sizeof(Dec3RowInfo));
     double t1 = g_hprof.on ? now_us() : 0;
+    int *ctr = nullptr;
+    if ((rc = stream_counters(p0, st, &ctr, nullptr))) return rc;
     Dec3Args a;
     memset(&a, 0, sizeof(a));
-    a.inl = inline_plan ? 1 : 0;
     if ((rc = make_map_cached(p0, &a.tmX, X, p0->in, b->S, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B))) return rc;
     int nt0 = 0;
     for (int i = 0; i < n_proj; ++i) {
@@ -641,10 +662,8 @@ int run_dec3(int n_proj, const smlm_pool *pools, const smlm_batch *b, const Dec3
         P.n_wt = (pools[i]->out + 255) / 256;
         nt0 += P.n_wt;
     }
-    a.uslot = reinterpret_cast<const int *>(wsb + D.plan_off);
-    a.rows = reinterpret_cast<const Dec3RowInfo *>(wsb + D.plan_off + rows_off);
     a.kpart = reinterpret_cast<float *>(wsb + D.kpart_off);
-    a.ctr = p0->d_ctr;
+    a.ctr = ctr;
     a.n_proj = n_proj;
     a.n_uniq = n_uniq;
     a.n_groups = D.n_groups;
@@ -659,8 +678,8 @@ int run_dec3(int n_proj, const smlm_pool *pools, const smlm_batch *b, const Dec3
     a.r = p0->r;
     a.r_pad = p0->r_pad;
     a.stages = dec3_stages();
-    a.flags = env_int("SMLM_DEC3_EXPT");
-    if (env_flag("SMLM_DEC3_DEBUG"))
+    a.cooperative = p0->dec_coop;
+    if (measure_flag("SMLM_DEC3_DEBUG"))
         a.dbg = reinterpret_cast<unsigned long long *>(wsb + D.total - 2 * kDec3MaxPairs * 16 * 8);
     double t2 = g_hprof.on ? now_us() : 0;
     {
@@ -842,15 +861,20 @@ int smlm_pool_create(int device, int in_features, int out_features, int rank, in
         delete p;
         return cuda_err(e, "cudaMalloc(slot table)");
     }
-    if (e == cudaSuccess) e = cudaMalloc(&p->d_ctr, sizeof(int) * dec3_counter_ints());
-    if (e == cudaSuccess) e = cudaMemset(p->d_ctr, 0, sizeof(int) * dec3_counter_ints());
-    if (e == cudaSuccess) e = cudaMalloc(&p->d_uctr, sizeof(int) * kUCtrMax);
-    if (e == cudaSuccess) e = cudaMemset(p->d_uctr, 0, sizeof(int) * kUCtrMax);
     if (e == cudaSuccess) e = cudaMemset(p->d_slots, 0, sizeof(SlotDev) * capacity);
+    for (int i = 0; i < kCtrSets && e == cudaSuccess; ++i) {
+        int *d = nullptr;
+        e = cudaMalloc(&d, ctr_set_ints() * sizeof(int));
+        if (e == cudaSuccess) {
+            p->ctrs.push_back({(cudaStream_t)-1, d});
+            e = cudaMemset(d, 0, ctr_set_ints() * sizeof(int));
+        }
+    }
     if (e != cudaSuccess) {
         cudaFree(p->d_slots);
+        for (auto &c : p->ctrs) cudaFree(c.d);
         delete p;
-        return cuda_err(e, "cudaMemset(slot table)");
+        return cuda_err(e, "pool allocation");
     }
     *out = p;
     return SMLM_OK;
@@ -862,8 +886,7 @@ int smlm_pool_destroy(smlm_pool p) {
         DeviceGuard dg(p->device);
         cudaDeviceSynchronize();
         if (p->d_slots) cudaFree(p->d_slots);
-        if (p->d_ctr) cudaFree(p->d_ctr);
-        if (p->d_uctr) cudaFree(p->d_uctr);
+        for (auto &c : p->ctrs) cudaFree(c.d);
         if (p->cap_arena) cudaFreeHost(p->cap_arena);
     }
     delete p;
@@ -879,6 +902,19 @@ int smlm_pool_set_option(smlm_pool p, int option, int value) {
     }
     if (option == SMLM_OPT_CTA_PAIR) {
         p->cta_pair = value != 0;
+        return SMLM_OK;
+    }
+    if (option == SMLM_OPT_DECODE_KERNEL) {
+        p->dec_kernel = value != 0;
+        return SMLM_OK;
+    }
+    if (option == SMLM_OPT_DEC_COOPERATIVE) {
+        p->dec_coop = value != 0;
+        return SMLM_OK;
+    }
+    if (option == SMLM_OPT_DEC_KSPLIT) {
+        if (value < 0 || value > 8) return set_err(SMLM_E_INVALID, "decode split-K must be in [0, 8]");
+        p->dec_ksplit = value;
         return SMLM_OK;
     }
     return set_err(SMLM_E_INVALID, "unknown option");
@@ -909,7 +945,7 @@ static int upload_slot(smlm_pool p, int slot, cudaStream_t st) {
     }
     std::vector<uint8_t> bytes(sizeof(SlotDev));
     memcpy(bytes.data(), &d, sizeof(SlotDev));
-    return stage_upload(p, bytes, p->d_slots + slot, st);
+    return stage_upload(p, bytes, p->d_slots + slot, st, true);
 }
 
 int smlm_adapter_register(smlm_pool p, const void *A, const void *B, float scale, void *stream, int *slot_out) {
@@ -1032,6 +1068,8 @@ int smlm_forward(smlm_pool p, const smlm_batch *b, const void *X, const void *W,
     if ((rc = check_sticky())) return rc;
     cudaStream_t st = (cudaStream_t)stream;
     uint8_t *wsb = reinterpret_cast<uint8_t *>(ws);
+    int *uctr = nullptr;
+    if ((rc = stream_counters(p, st, nullptr, &uctr))) return rc;
 
     if (p->dtype == SMLM_FP32) {
         std::vector<uint8_t> bytes;
@@ -1118,8 +1156,7 @@ int smlm_forward(smlm_pool p, const smlm_batch *b, const void *X, const void *W,
         ProfScope ps(2, st);
         if (L.spart_bytes) {
             // the last chunk of each block combines it in-kernel (pool counters, self-resetting)
-            int *sctr = ((int)plan.blocks.size() <= kUCtrMax && !env_flag("SMLM_SHRINK_SEPARATE_COMBINE")) ? p->d_uctr
-                                                                                                          : nullptr;
+            int *sctr = (int)plan.blocks.size() <= kUCtrMax ? uctr : nullptr;
             CKL(launch_shrink_split((const __nv_bfloat16 *)X, p->d_slots, d_blocks, d_srows, (int)plan.blocks.size(),
                                     p->in, p->r, p->r_pad, reinterpret_cast<float *>(wsb + L.spart_off), Vbd,
                                     (__nv_bfloat16 *)V_save, sctr, st), sctr ? 1 : 2);
@@ -1138,7 +1175,6 @@ int smlm_forward(smlm_pool p, const smlm_batch *b, const void *X, const void *W,
         ProfScope ps(2, st);
         UArgs u;
         memset(&u, 0, sizeof(u));
-        u.kw1 = env_flag("SMLM_U_KW1") ? 1 : 0;
         if ((rc = make_map(&u.tmDY, X, p->in, b->S, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B))) return rc;
         u.slots = p->d_slots;
         u.tiles = d_tiles;
@@ -1152,7 +1188,7 @@ int smlm_forward(smlm_pool p, const smlm_batch *b, const void *X, const void *W,
         u.vf = 1;
         u.r = p->r;
         u.Vsave = V_save;
-        u.ctr = (u.n_items <= kUCtrMax && !env_flag("SMLM_U_SEPARATE_REDUCE")) ? p->d_uctr : nullptr;
+        u.ctr = u.n_items <= kUCtrMax ? uctr : nullptr;
         CKL(launch_u(u, p->num_sms, st), u.ctr ? 1 : 2);
     }
     const int bnw = pre ? kBN : kBN - p->r_pad;
@@ -1177,7 +1213,7 @@ int smlm_forward(smlm_pool p, const smlm_batch *b, const void *X, const void *W,
             g2.has_u = 1;
         }
         g2.blocks = d_blocks;
-        g2.defer = env_flag("SMLM_NO_DEFER") ? 0 : 1;
+        g2.defer = 1;
         g2.slots = p->d_slots;
         g2.pairs = reinterpret_cast<const DevPair *>(wsb + L.plan_off + pair_off);
         g2.n_pairs = (int)pairs.size();
@@ -1262,7 +1298,7 @@ struct MultiPre {
 static MultiPre multi_pre_layout(int n_proj, const smlm_pool *pools, const smlm_batch *b, const Plan &plan, bool same) {
     MultiPre M;
     smlm_pool p0 = pools[0];
-    if (!same || n_proj < 2 || p0->dtype != SMLM_BF16 || !use_preshrink(p0) || env_flag("SMLM_NO_MULTI_PRE") ||
+    if (!same || n_proj < 2 || p0->dtype != SMLM_BF16 || !use_preshrink(p0) ||
         n_proj * p0->r_pad > 128)
         return M;
     for (int i = 1; i < n_proj; ++i)
@@ -1328,6 +1364,8 @@ int smlm_forward_multi(int n_proj, const smlm_pool *pools, const smlm_batch *b, 
         smlm_pool p0 = pools[0];
         cudaStream_t st = (cudaStream_t)stream;
         uint8_t *wsb = reinterpret_cast<uint8_t *>(ws);
+        int *uctr = nullptr;
+        if ((rc = stream_counters(p0, st, nullptr, &uctr))) return rc;
         // long tiles (the same list every projection's forward builds) + the items with an adapter
         std::vector<int> items;
         for (size_t i = 0; i < plan.long_tiles.size(); ++i)
@@ -1340,7 +1378,6 @@ int smlm_forward_multi(int n_proj, const smlm_pool *pools, const smlm_batch *b, 
         if ((rc = stage_upload(p0, bytes, wsb + M.plan_off, st))) return rc;
         UArgs u;
         memset(&u, 0, sizeof(u));
-        u.kw1 = env_flag("SMLM_U_KW1") ? 1 : 0;
         if ((rc = make_map_cached(p0, &u.tmDY, X, p0->in, b->S, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B))) return rc;
         u.slots = p0->d_slots;
         u.tiles = reinterpret_cast<const DevTile *>(wsb + M.plan_off);
@@ -1358,7 +1395,7 @@ int smlm_forward_multi(int n_proj, const smlm_pool *pools, const smlm_batch *b, 
             u.sUt_p[i] = wsb + M.sv_off[i];
             u.Vsave_p[i] = V_save ? V_save[i] : nullptr;
         }
-        u.ctr = (u.n_items <= kUCtrMax && !env_flag("SMLM_U_SEPARATE_REDUCE")) ? p0->d_uctr : nullptr;
+        u.ctr = u.n_items <= kUCtrMax ? uctr : nullptr;
         {
             ProfScope ps(2, st);
             CKL(launch_u(u, p0->num_sms, st), u.ctr ? 1 : 2);
@@ -1392,6 +1429,8 @@ int smlm_backward(smlm_pool p, const smlm_batch *b, const void *X, const void *W
     if ((rc = check_sticky())) return rc;
     cudaStream_t st = (cudaStream_t)stream;
     uint8_t *wsb = reinterpret_cast<uint8_t *>(ws);
+    int *uctr = nullptr;
+    if ((rc = stream_counters(p, st, nullptr, &uctr))) return rc;
 
     // grad groups with the current grad bindings (masking: NULL => no dA/dB for that slot)
     std::vector<uint8_t> gbytes(plan.groups.size() * grad_group_bytes());
@@ -1470,7 +1509,6 @@ int smlm_backward(smlm_pool p, const smlm_batch *b, const void *X, const void *W
     if (L.u_items && (dX || n_grad)) {
         UArgs u;
         memset(&u, 0, sizeof(u));
-        u.kw1 = env_flag("SMLM_U_KW1") ? 1 : 0;
         if ((rc = make_map(&u.tmDY, dY, p->out, b->S, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B))) return rc;
         u.slots = p->d_slots;
         u.tiles = d_tiles;
@@ -1481,12 +1519,12 @@ int smlm_backward(smlm_pool p, const smlm_batch *b, const void *X, const void *W
         u.r_pad = p->r_pad;
         u.part = reinterpret_cast<float *>(wsb + L.upart_off);
         u.sUt = sUt;
-        if (V_save && n_grad && !env_flag("SMLM_SEPARATE_PREP_SV")) {   // s*V folded into the reduce
+        if (V_save && n_grad) {   // s*V folded into the reduce
             u.Vsave_in = V_save;
             u.sVt = sVt;
             u.r = p->r;
         }
-        u.ctr = (u.n_items <= kUCtrMax && !env_flag("SMLM_U_SEPARATE_REDUCE")) ? p->d_uctr : nullptr;
+        u.ctr = u.n_items <= kUCtrMax ? uctr : nullptr;
         CKL(launch_u(u, p->num_sms, st), u.ctr ? 1 : 2);
     }
     if (dX) {
@@ -1543,7 +1581,7 @@ int smlm_backward(smlm_pool p, const smlm_batch *b, const void *X, const void *W
     if (n_grad) {
         ProfScope ps(3, st);
         if (V_save) {
-            const bool folded = L.u_items && !env_flag("SMLM_SEPARATE_PREP_SV");   // done by the U pass
+            const bool folded = L.u_items > 0;   // done by the U pass
             if (!folded)
                 CKL(launch_prep_sv<__nv_bfloat16>(d_tiles, nt, (const __nv_bfloat16 *)V_save, p->r, p->r_pad, sVt, st), 1);
         } else {
@@ -1565,7 +1603,7 @@ int smlm_backward(smlm_pool p, const smlm_batch *b, const void *X, const void *W
         ta.out_f = p->out;
         ta.r = p->r;
         ta.r_pad = p->r_pad;
-        ta.nh = env_flag("SMLM_TOK_NARROW") ? 1 : 2;   // 256-column items (measurement override)
+        ta.nh = 2;   // 256-column items (two M=128 accumulators sharing the B operand)
         ta.mt_a = (p->in + 128 * ta.nh - 1) / (128 * ta.nh);
         ta.mt_b = (p->out + 128 * ta.nh - 1) / (128 * ta.nh);
         ta.accumulate = accumulate ? 1 : 0;

@@ -27,6 +27,12 @@ struct alignas(64) SlotDev {
     int pad[5];
 };
 static_assert(sizeof(SlotDev) % 64 == 0, "SlotDev must keep 64-byte alignment of tensor maps");
+// The slot table's descriptors are written in global memory only by copy-engine transfers
+// (register / unregister: cudaMemcpyAsync on the caller's stream, never a kernel that PDL
+// successors overlap), and every kernel reads them only after griddepcontrol.wait: the kernel
+// launch that follows the transfer in stream order starts with fresh descriptor caches, so a
+// descriptor cached for a slot's previous adapter is never used (no tensormap proxy fence needed;
+// that fence is required only for descriptors modified by device code).
 
 struct GemmArgs {
     CUtensorMap tmA;   // X [S,in] (fwd) or dY [S,out] (bwd): box {64,128} SW128
@@ -121,7 +127,6 @@ struct UArgs {
     // operand of the token contraction), folded into the reduction
     const void *Vsave_in;
     void *sVt;
-    int kw1;    // measurement override: one K-block per ring stage
     int npj;
     const SlotDev *slots_p[4];
     void *sUt_p[4];
@@ -183,8 +188,6 @@ struct alignas(16) Dec3RowInfo {   // per batch row
 struct Dec3Args {
     CUtensorMap tmX;        // X [S, in] box {64,128} SW128 (A operand: 128 decode rows per CTA)
     Dec3Proj proj[kDec3MaxProj];
-    const int *uslot;       // [n_uniq] distinct adapter slots of the batch, ascending (if !inl)
-    const Dec3RowInfo *rows;  // [S] (if !inl)
     float *kpart;           // split-K partials [items][2 ranks][8 chunks][8 q][128 m] float4
     int *ctr;               // pool-owned self-resetting counters (kernels_dec3.cu)
     unsigned long long *dbg;  // optional per-CTA phase timestamps [grid][16] (SMLM_DEC3_DEBUG)
@@ -202,8 +205,7 @@ struct Dec3Args {
     int r;
     int r_pad;
     int stages;
-    int flags;
-    int inl;                // 1: uslot / rows are passed inline (Dec3Inline kernel parameter)
+    int cooperative;        // launch attribute (pool option SMLM_OPT_DEC_COOPERATIVE), host side only
 };
 // small plans ride in the kernel parameters (no H2D copy in the stream)
 constexpr int kDec3InlineSlots = 256;

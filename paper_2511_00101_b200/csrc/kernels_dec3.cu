@@ -112,8 +112,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT3, 1) smlm_dec3_ke
     constexpr uint32_t RB = RP * 2;
     constexpr uint32_t kSwR = RB >= 128 ? kSw128 : (RB == 64 ? kSw64 : kSw32);
     constexpr int APC = 128 / RP;   // stacked adapters per CTA of a V tile
-    // expand adapters per ring stage (16 KB A + 16 KB B per CTA); flags & 128: one (A/B measurement)
-    const int EPS = (a.flags & 128) ? 1 : 64 / RP;
+    // expand adapters per ring stage (16 KB A + 16 KB B per CTA)
+    constexpr int EPS = 64 / RP;
     const int ST = a.stages;
     const uint32_t ystage = base + ST * kStage3;   // 2 x 8 KB bf16 Y staging (TMA store)
     const uint32_t bar = ystage + 2 * kYStage;
@@ -153,10 +153,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT3, 1) smlm_dec3_ke
     __shared__ int s_ucount;
     if (active) {
         const int nu = a.n_uniq, ksp = it.ks, s0 = it.s;
-        const bool expand = !(a.flags & 4) && !it.vtile;
+        const bool expand = !it.vtile;
         const int u = threadIdx.x;
         int sl = -1;
-        if (u < nu && u < kDec3InlineSlots) sl = a.inl ? inl.uslot[u] : a.uslot[u];
+        if (u < nu && u < kDec3InlineSlots) sl = inl.uslot[u];
         if (u < kDec3InlineSlots) s_uslot[u] = sl;
         const bool mine = sl >= 0 && expand && sl % ksp == s0;
         const uint32_t bal = __ballot_sync(0xffffffffu, mine);
@@ -170,11 +170,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT3, 1) smlm_dec3_ke
         if (mine) s_ulist[off + __popc(bal & ((1u << lane) - 1u))] = u;
         if (threadIdx.x == 0) s_ucount = tot;
     }
-    if (active && it.vtile && warp == 3) {
-        // this CTA's stacked-adapter descriptors: fetch them while the prologue runs
-        const int u0 = it.n0 + (128 / RP) * (int)rank;
-        if (lane < 128 / RP && u0 + lane < a.n_uniq) tma_prefetch_desc(&P.slots[s_uslot[u0 + lane]].tmA);
-    }
     if (active && warp == 2) {
         asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(tmem_slot), "r"(256)
                      : "memory");
@@ -184,6 +179,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT3, 1) smlm_dec3_ke
     cluster_sync();
     tc_fence_after();
     const uint32_t tmem_base = active ? *reinterpret_cast<volatile uint32_t *>(base_ptr + (tmem_slot - base)) : 0u;
+    // nothing in global memory is read before this point: the slot table (TMA descriptors of the
+    // adapters) may be written by the stream's preceding work
     pdl_wait();
     pdl_trigger();
     if (threadIdx.x == 0) dbg_stamp(a, 0);
@@ -213,8 +210,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT3, 1) smlm_dec3_ke
         const int nad1 = it.vtile ? max(0, min(APC, a.n_uniq - (it.n0 + APC))) : 0;
         const uint32_t bytes_pair = it.vtile ? 2u * kA3 + (uint32_t)(max(0, min(APC, a.n_uniq - it.n0)) + nad1) * RP * 128u
                                              : 2u * kStage3;
-        if (it.vtile && lane < nad) tma_prefetch_desc(&P.slots[s_uslot[u0 + lane]].tmA);
-        if (!it.vtile && a.n_vpairs > 0 && !(a.flags & 16)) {
+        if (it.vtile && lane < nad) {
+            const void *d = &P.slots[s_uslot[u0 + lane]].tmA;
+            tma_prefetch_desc(d);
+        }
+        if (!it.vtile && a.n_vpairs > 0) {
             // the V tiles' first ring of loads goes to the memory system before the W stream: the
             // V chain (shrink -> split-K reduction -> publish) is what the W tiles' expand waits for
             if (lane == 0)
@@ -336,7 +336,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT3, 1) smlm_dec3_ke
         const int row0 = it.g * 256 + 128 * (int)rank;
         const int row = row0 + m;
         Dec3RowInfo ri{-1, 0.f, 0, 0};
-        if (it.vtile && row < a.S) ri = a.inl ? inl.rows[row] : a.rows[row];
+        if (it.vtile && row < a.S) ri = inl.rows[row];
         mbar_wait(acc_full, 0);
         tc_fence_after();
         if (tid_e == 0) dbg_stamp(a, 4);
@@ -385,7 +385,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT3, 1) smlm_dec3_ke
                 }
                 // the CTA barrier orders every thread's partial stores before thread 0's gpu-scope
                 // release (cumulative), as in a split-K semaphore: no per-thread fence
-                if (a.flags & 256) __threadfence();
                 named_bar_sync(1, 128);
                 if (tid_e == 0) {
                     dbg_stamp(a, 3);
@@ -456,7 +455,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT3, 1) smlm_dec3_ke
             }
             // publish: the slabs are read by TMA (async proxy) in other CTAs
             fence_proxy_async_global();
-            if (a.flags & 256) __threadfence();
             named_bar_sync(1, 128);
             if (tid_e == 0) {
                 atom_add_release_gpu(a.ctr, 1);
@@ -477,7 +475,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT3, 1) smlm_dec3_ke
                         __stcg(dst + q * 128, make_float4(__uint_as_float(rr[4 * q]), __uint_as_float(rr[4 * q + 1]),
                                                           __uint_as_float(rr[4 * q + 2]), __uint_as_float(rr[4 * q + 3])));
                 }
-                if (a.flags & 256) __threadfence();   // (see the V tiles: barrier + release by thread 0)
                 named_bar_sync(1, 128);
                 if (tid_e == 0) {
                     dbg_stamp(a, 3);
@@ -581,22 +578,72 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT3, 1) smlm_dec3_ke
 
 static_assert(sizeof(Dec3Args) + sizeof(Dec3Inline) <= 32764, "kernel parameters exceed 32 KB");
 
+constexpr size_t dec3_smem() { return 1024 + (size_t)6 * kStage3 + 2 * kYStage + 256; }
+
+template <int RP>
+cudaError_t dec3_attr() {
+    static cudaError_t done = cudaErrorNotReady;
+    if (done != cudaSuccess)
+        done = cudaFuncSetAttribute(smlm_dec3_kernel<RP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dec3_smem());
+    return done;
+}
+
+// The CTAs of one launch spin-wait on each other (V publish, split-K arrival), so they must all be
+// resident at once: the grid is capped by the clusters that fit the device at one CTA per SM (on
+// an otherwise idle GPU every CTA is placed; a kernel of another stream only delays the late
+// ones).  Two spin-waiting grids that each hold part of the GPU could wait on each other: with
+// the pool option SMLM_OPT_DEC_COOPERATIVE the launch is cooperative (the whole grid is
+// co-scheduled), for callers that issue decode calls on several streams at once (~2 us per
+// launch, measured).
+template <int RP>
+int dec3_max_clusters_impl() {
+    static int cached = -1;
+    if (cached >= 0) return cached;
+    if (dec3_attr<RP>() != cudaSuccess) return 0;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(2 * kDec3MaxPairs);
+    cfg.blockDim = dim3(kT3);
+    cfg.dynamicSmemBytes = dec3_smem();
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, smlm_dec3_kernel<RP>, &cfg) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    cached = n;
+    return n;
+}
+
 template <int RP>
 int launch_dec3_impl(const Dec3Args &a, const Dec3Inline &in, int clusters, cudaStream_t st) {
-    auto kern = smlm_dec3_kernel<RP>;
-    const size_t smem = 1024 + (size_t)a.stages * kStage3 + 2 * kYStage + 256;
-    static bool attr_done = false;
-    if (!attr_done) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return (int)e;
-        attr_done = true;
-    }
-    return (int)launch_pdl(kern, dim3(2 * clusters), dim3(kT3), smem, st, a, in);
+    cudaError_t e = dec3_attr<RP>();
+    if (e != cudaSuccess) return (int)e;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(2 * clusters);
+    cfg.blockDim = dim3(kT3);
+    cfg.dynamicSmemBytes = dec3_smem();
+    cfg.stream = st;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    at[1].id = cudaLaunchAttributeCooperative;
+    at[1].val.cooperative = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = a.cooperative ? 2 : 1;
+    return (int)cudaLaunchKernelEx(&cfg, smlm_dec3_kernel<RP>, a, in);
 }
 
 }  // namespace
 
 int dec3_stages() { return 6; }
+
+int dec3_max_clusters(int r_pad) {
+    switch (r_pad) {
+        case 16: return dec3_max_clusters_impl<16>();
+        case 32: return dec3_max_clusters_impl<32>();
+        case 64: return dec3_max_clusters_impl<64>();
+    }
+    return 0;
+}
 
 int launch_dec3(const Dec3Args &a, const Dec3Inline &in, int clusters, cudaStream_t st) {
     switch (a.r_pad) {

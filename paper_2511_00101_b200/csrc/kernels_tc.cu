@@ -942,14 +942,6 @@ int launch_u(const UArgs &a, int num_sms, cudaStream_t st) {
         }
         return (int)cudaErrorInvalidValue;
     }
-    if (a.kw1) {   // one 64-wide K-block per ring stage (measurement override)
-        switch (a.r_pad) {
-            case 16: return launch_u_impl<16, 1, 1>(a, num_sms, st);
-            case 32: return launch_u_impl<32, 1, 1>(a, num_sms, st);
-            case 64: return launch_u_impl<64, 1, 1>(a, num_sms, st);
-        }
-        return (int)cudaErrorInvalidValue;
-    }
     switch (a.r_pad) {
         case 16: return launch_u_impl<16>(a, num_sms, st);
         case 32: return launch_u_impl<32>(a, num_sms, st);
@@ -960,13 +952,11 @@ int launch_u(const UArgs &a, int num_sms, cudaStream_t st) {
 
 int launch_tok(const TokArgs &a, int num_sms, cudaStream_t st) {
     if (a.n_groups == 0) return 0;
-    switch (a.r_pad * (a.nh == 2 ? -1 : 1)) {
-        case 16: return launch_tok_impl<16, 1>(a, num_sms, st);
-        case 32: return launch_tok_impl<32, 1>(a, num_sms, st);
-        case 64: return launch_tok_impl<64, 1>(a, num_sms, st);
-        case -16: return launch_tok_impl<16, 2>(a, num_sms, st);
-        case -32: return launch_tok_impl<32, 2>(a, num_sms, st);
-        case -64: return launch_tok_impl<64, 2>(a, num_sms, st);
+    if (a.nh != 2) return (int)cudaErrorInvalidValue;   // 256-column items only
+    switch (a.r_pad) {
+        case 16: return launch_tok_impl<16, 2>(a, num_sms, st);
+        case 32: return launch_tok_impl<32, 2>(a, num_sms, st);
+        case 64: return launch_tok_impl<64, 2>(a, num_sms, st);
     }
     return (int)cudaErrorInvalidValue;
 }

@@ -13,13 +13,15 @@ from typing import Optional
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libsmlm.so")
+# the release library; SMLM_MEASURE_LIB=1 loads the -DSMLM_MEASURE build (build.py --measure:
+# phase timestamps / host timing for the scripts under scripts/, same kernels and results)
+LIB_PATH = os.path.join(_HERE, "libsmlm_measure.so" if os.environ.get("SMLM_MEASURE_LIB") == "1" else "libsmlm.so")
 
 SMLM_OK, SMLM_E_INVALID, SMLM_E_SHAPE, SMLM_E_SLOT, SMLM_E_CAPACITY, SMLM_E_CUDA, SMLM_E_UNSUPPORTED, \
     SMLM_E_WORKSPACE = range(8)
 SMLM_FINETUNE, SMLM_EVAL, SMLM_PREFILL, SMLM_DECODE = range(4)
 SMLM_BF16, SMLM_FP32 = 0, 1
-SMLM_OPT_L_LONG, SMLM_OPT_CTA_PAIR = 0, 1
+SMLM_OPT_L_LONG, SMLM_OPT_CTA_PAIR, SMLM_OPT_DECODE_KERNEL, SMLM_OPT_DEC_KSPLIT, SMLM_OPT_DEC_COOPERATIVE = 0, 1, 2, 3, 4
 PROF_FWD_GEMM, PROF_BWD_GEMM, PROF_SHRINK, PROF_DADB, PROF_ADAMW = range(5)
 
 EXPORTED = [

@@ -189,10 +189,12 @@ def c2_layer_step(iters=40, graphs=True):
             "hbm_roofline_frac_graph": None if ms_graph is None else roof_ms / ms_graph}
 
 
-def adamw_step(layers=32, clip=1.0, iters=20):
+def adamw_step(layers=32, clip=1.0, iters=20, jobs=4):
     """AdamW over the C4 fine-tune adapters (4 adapters, r=16, 7 projections) of
-    `layers` layers (kernels_opt.cu).  34 algorithmic bytes/element (+4 with the clip pass);
-    L2 flushed before every launch."""
+    `layers` layers (kernels_opt.cu), one optimizer step PER fine-tune job (each job is its own
+    trainer: own clip norm and step count, optim.py): `jobs` contiguous sub-ranges of one flat
+    store, each a clip pass + a step launch.  34 algorithmic bytes/element (+4 with the clip
+    pass); L2 flushed before every step."""
     peaks = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
                                         "MEASURED_PEAKS.json")))
     hbm = float(peaks["hbm_gbs"])
@@ -208,7 +210,10 @@ def adamw_step(layers=32, clip=1.0, iters=20):
         flush.zero_()
         a, b = torch.cuda.Event(True), torch.cuda.Event(True)
         a.record()
-        S.smlm_adamw_step(P, M, V, G, PB, it + 1, 2e-5, max_grad_norm=clip, zero_grad=True, ws=Wk)
+        for j in range(jobs):
+            lo, hi = n * j // jobs // 8 * 8, (n * (j + 1) // jobs // 8 * 8 if j + 1 < jobs else n)
+            S.smlm_adamw_step(P[lo:hi], M[lo:hi], V[lo:hi], G[lo:hi], PB[lo:hi], it + 1, 2e-5, max_grad_norm=clip,
+                              zero_grad=True, ws=Wk)
         b.record()
         b.synchronize()
         if it >= 3:
@@ -216,7 +221,7 @@ def adamw_step(layers=32, clip=1.0, iters=20):
     ms = statistics.median(ts)
     byts = n * (34 + (4 if clip > 0 else 0))
     del P, M, V, G, PB, flush
-    return {"kernel": "smlm_adamw_step", "layers": layers, "n": n, "clip": clip, "ms": ms, "alg_bytes": byts,
+    return {"kernel": "smlm_adamw_step", "layers": layers, "n": n, "jobs": jobs, "clip": clip, "ms": ms, "alg_bytes": byts,
             "GB/s": byts / ms / 1e6, "hbm_peak_GB/s": hbm, "frac": byts / ms / 1e6 / hbm}
 
 

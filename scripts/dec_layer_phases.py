@@ -5,6 +5,7 @@ import os
 import sys
 
 os.environ["SMLM_DEC3_DEBUG"] = "1"
+os.environ["SMLM_MEASURE_LIB"] = "1"   # build.py --measure
 import numpy as np
 import torch
 

@@ -17,7 +17,8 @@ class GpuResult:
 
 
 def run_smlm(batch, w, X, dY, dtype=None, backward=True, w_null=False, vsave=True, want_dx=True,
-             grads=None, l_long=None, accumulate=False, dA0=None, dB0=None, base_in=None, device=0):
+             grads=None, l_long=None, accumulate=False, dA0=None, dB0=None, base_in=None, device=0,
+             options=None):
     from paper_2511_00101_b200 import smlm as S
     dev = torch.device("cuda", device)
     tdt = X.dtype
@@ -30,6 +31,8 @@ def run_smlm(batch, w, X, dY, dtype=None, backward=True, w_null=False, vsave=Tru
     pool = S.Pool(in_f, out_f, r, max(U, 1), dt, device)
     if l_long is not None:
         pool.set_option(S.SMLM_OPT_L_LONG, l_long)
+    for opt, val in (options or {}).items():
+        pool.set_option(opt, val)
     A = [a.to(dev).contiguous() for a in w.A]
     B = [b.to(dev).contiguous() for b in w.B]
     slots = [pool.register(A[i], B[i], w.slot_scale[i]) for i in range(U)]

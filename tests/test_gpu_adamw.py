@@ -1,7 +1,7 @@
 """GPU parity of the AdamW step (kernels_opt.cu) against the fp64 oracle
 (oracle/adamw.py), through the C ABI (smlm_adamw_step).
 
-Tolerance (R9): the kernel computes in fp32, so parameters and moments must agree with
+Tolerance (R12): the kernel computes in fp32, so parameters and moments must agree with
 the fp64 oracle to rtol 2e-5 (a few fp32 ulps through ~10 dependent operations, plus the fp32
 sum of squares of the clip pass); the bf16 working copy must equal bf16(fp32 parameter) exactly
 and the oracle to within one bf16 ulp.  The clip coefficient and everything else is bitwise
@@ -148,16 +148,55 @@ def test_adapter_params_train_step(S):
     opt = AdamW(store, lr=1e-3, max_grad_norm=1.0)
     opt.step()
     torch.cuda.synchronize()
-    ref_p, _, _ = OA.adamw_step(p_host.numpy(), np.zeros(store.n), np.zeros(store.n), g_host.numpy(), 1, 1e-3,
-                                max_norm=1.0)
-    _check((store.master.cpu(), torch.zeros(store.n), torch.zeros(store.n)), (ref_p, np.zeros(store.n), np.zeros(store.n)),
-           (p_host.numpy(), np.zeros(store.n), None, g_host.numpy()), lr=1e-3)
+    # one job per adapter (the default): each clips by its own norm (optim.py)
+    for j, (lo, hi) in store.job_range.items():
+        n = hi - lo
+        ref_p, _, _ = OA.adamw_step(p_host[lo:hi].numpy(), np.zeros(n), np.zeros(n), g_host[lo:hi].numpy(), 1, 1e-3,
+                                    max_norm=1.0)
+        _check((store.master[lo:hi].cpu(), torch.zeros(n), torch.zeros(n)), (ref_p, np.zeros(n), np.zeros(n)),
+               (p_host[lo:hi].numpy(), np.zeros(n), None, g_host[lo:hi].numpy()), lr=1e-3)
     assert bool((store.grad == 0).all())
     assert torch.equal(store.bf16, store.master.to(torch.bfloat16))
     # the next forward uses the updated adapter (borrowed bf16 views)
     Y2 = pool.forward(b, X, W)
     assert not torch.equal(Y, Y2)
     pool.close()
+
+
+def test_adamw_per_job_clip_and_steps(S):
+    """Per-job optimizer state (Loquetier runs one HF Trainer per fine-tune job): a job
+    with a huge gradient does not shrink another job's update, and a job that steps less often
+    keeps its own step count (bias correction) -- against the fp64 oracle per job."""
+    from paper_2511_00101_b200.optim import AdapterParams, AdamW
+    dev = torch.device("cuda", 0)
+    store = AdapterParams([(8, 64, 48), (8, 64, 48), (16, 128, 64)], device=dev, jobs=[0, 0, 1])
+    assert store.job_range[0][1] == store.job_range[1][0]
+    g = torch.Generator(device=dev).manual_seed(9)
+    store.master.copy_(torch.randn(store.n, device=dev, generator=g) * 0.02)
+    opt = AdamW(store, lr=1e-3, max_grad_norm=1.0)
+    host = {j: (store.master[lo:hi].double().cpu().numpy(), np.zeros(hi - lo), np.zeros(hi - lo))
+            for j, (lo, hi) in store.job_range.items()}
+    steps = {0: 0, 1: 0}
+    for it in range(3):
+        jobs = [0, 1] if it != 1 else [1]          # job 0 accumulates over two micro-batches once
+        for j in jobs:
+            lo, hi = store.job_range[j]
+            scale = 100.0 if j == 1 else 1e-3          # job 1: a huge gradient (clipped hard)
+            store.grad[lo:hi].copy_(torch.randn(hi - lo, device=dev, generator=g) * scale)
+        gh = store.grad.double().cpu().numpy().copy()
+        opt.step(jobs)
+        torch.cuda.synchronize()
+        for j in jobs:
+            lo, hi = store.job_range[j]
+            steps[j] += 1
+            p0, m0, v0 = host[j]
+            ref = OA.adamw_step(p0, m0, v0, gh[lo:hi], steps[j], 1e-3, max_norm=1.0)
+            _check((store.master[lo:hi].cpu(), store.exp_avg[lo:hi].cpu(), store.exp_avg_sq[lo:hi].cpu()), ref,
+                   (p0, m0, v0, gh[lo:hi]), lr=1e-3)
+            host[j] = tuple(np.asarray(x, np.float64) for x in (store.master[lo:hi].double().cpu().numpy(),
+                                                                store.exp_avg[lo:hi].double().cpu().numpy(),
+                                                                store.exp_avg_sq[lo:hi].double().cpu().numpy()))
+    assert opt.t == {0: 2, 1: 3}
 
 
 def test_adamw_full_size_sampled(S):

@@ -262,17 +262,22 @@ def test_bf16_decode_grouped_with_finetune_short_rows():
     _check(res, batch, w, X, dY, BF16_TOL)
 
 
-@pytest.mark.parametrize("ks", ["1", "2", "3", "8"])
-def test_bf16_decode_ksplit_variants(monkeypatch, ks):
-    """The single-launch decode kernel (kernels_dec3.cu) at forced split-K factors: every split
-    count matches the oracle (in-kernel reduce-scatter of the fp32 partials)."""
-    monkeypatch.setenv("SMLM_DEC_KSPLIT", ks)
+@pytest.mark.parametrize("ks", [1, 2, 3, 8, -1, 0])
+def test_bf16_decode_ksplit_variants(ks):
+    """The single-launch decode kernel (kernels_dec3.cu) at forced split-K factors (pool option
+    SMLM_OPT_DEC_KSPLIT): every split count matches the oracle (in-kernel reduce-scatter of the
+    fp32 partials); ks = -1 runs the same batch through the mixed-batch path instead
+    (SMLM_OPT_DECODE_KERNEL = 0); ks = 0 is the automatic split with a cooperative launch
+    (SMLM_OPT_DEC_COOPERATIVE)."""
+    from paper_2511_00101_b200 import smlm as S
+    opts = ({S.SMLM_OPT_DECODE_KERNEL: 0} if ks < 0 else
+            {S.SMLM_OPT_DEC_COOPERATIVE: 1} if ks == 0 else {S.SMLM_OPT_DEC_KSPLIT: ks})
     g = torch.Generator().manual_seed(5)
     rows = 200
     slots = torch.randint(-1, 6, (rows,), generator=g).tolist()
     modes = [DECODE] * (rows - 3) + [FINETUNE] * 3
     batch, w, X, dY = synth.random_case(77, 1024, 640, 16, 6, [1] * rows, modes, slots)
-    res = run_smlm(batch, w, X, dY, backward=False)
+    res = run_smlm(batch, w, X, dY, backward=False, options=opts)
     Y, V = oracle.forward(batch, w.W, w.A, w.B, w.slot_scale, X)
     assert parity_err(res.Y, Y) <= BF16_TOL
     ft = batch.ft_rows()
