@@ -2,15 +2,17 @@
 """SMLM benchmark (BASELINE.json metric: "SMLM tokens/s at Llama-3-8B r=16 mixed batch; % of
 HBM/tensor roofline").
 
-One step = one SMLM layer-step of the unified workload (BASELINE.json configs[3], "C4"):
-forward of all 7 Llama-3-8B projections (q,k,v,o,gate,up,down) over the mixed batch of
-4 fine-tune segments x 1024 rows + 8 prefill requests + 128 decode rows over a 64-adapter pool
-(r = 16), then the fine-tune backward (dX, dA, dB) of all 7 projections in reverse order.
-tokens/s = rows in the batch / step time (the per-layer throughput of SURVEY.md §8(d)).
+One step = the SMLM work of L = 8 Llama-3-8B layers over the unified batch (BASELINE.json
+configs[3], "C4": 4 fine-tune segments x 1024 rows + 8 prefill requests + 128 decode rows over a
+64-adapter pool, r = 16): the forward of all 7 projections (q,k,v,o,gate,up,down) of layers
+0..7, then the fine-tune backward (dX, dA, dB) of the 7 projections of layers 7..0 (SURVEY.md
+§8(d) C5 step; every layer has its own weight set of 416 MiB, so no layer's weights are in L2
+when it runs).  tokens/s = rows x L / step time = the per-layer throughput of SURVEY.md §8(d).
 With --gpus N > 1 (torchrun, one process per GPU, NCCL): configs[4] "C5" -- every rank runs its
-own C4-shaped batch over a replicated 256-adapter pool and the fine-tune dA/dB of every
-projection are SUM all-reduced over NCCL on a side stream, overlapping the next projection's
-backward; value = all ranks' rows / max-over-ranks step time (weak scaling).
+own C4-shaped batch over a replicated 256-adapter pool; the fine-tune dA/dB of each layer (one
+flat fp32 bucket of the 7 projections, 20 MiB) are SUM all-reduced over NCCL on a side stream as
+soon as that layer's backward is done, overlapping the next layer's backward; value = all ranks'
+rows x L / max-over-ranks step time (weak scaling).
 
 `--impl reference` times the fp64 CPU oracle (oracle/, test infrastructure) on a bounded row
 sample of the same workload on this box's host cores (rank 0 only).
@@ -38,7 +40,7 @@ from paper_2511_00101_b200.dp import AllReduce, GradBucket  # noqa: E402
 
 METRIC = "SMLM tokens/s at Llama-3-8B r=16 mixed batch; % of HBM/tensor roofline"
 UNIT = "tokens/s"
-N_LAYER_SETS = 3          # distinct weight sets rotated across steps (each 416 MiB > 126 MB L2)
+N_LAYERS = 8              # layers (distinct weight sets, 416 MiB each > 126 MB L2) per step
 FT_SLOTS = [0, 1, 2, 3]   # fine-tune adapters (C4/C5)
 GROUP_OF = {"q": "attn", "k": "attn", "v": "attn", "o": "o", "gate": "mlp", "up": "mlp", "down": "down"}
 # projections sharing X go through one smlm_forward_multi call (Alg. 1 P:331 joint QKV;
@@ -141,7 +143,8 @@ class Workload:
             self.V[p] = torch.zeros(self.rows, r, dtype=torch.bfloat16, device=dev)
         # layer sets: base weights + adapter pools (replicated across ranks: same seeds)
         self.layers = []
-        for L in range(N_LAYER_SETS):
+        self.buckets = []   # one flat fp32 all-reduce bucket per layer (the 7 projections' FT dA/dB)
+        for L in range(N_LAYERS):
             gw = torch.Generator(device=dev)
             gw.manual_seed(1000 + 10 * k + 100 * L)
             layer = {}
@@ -153,9 +156,8 @@ class Workload:
                 pool = S.Pool(in_f, out_f, r, U, S.SMLM_BF16, dev.index)
                 for a in range(U):
                     assert pool.register(A[a], B[a], 2.0) == a
-                # fine-tune adapters' grads in one flat fp32 bucket per projection (all-reduce unit)
-                bucket = GradBucket(FT_SLOTS, r, in_f, out_f, dev)
-                bucket.bind(pool)
+                # fine-tune adapters' grads: views of the layer's flat bucket (set below)
+                bucket = None
                 wsf = pool.workspace(self.b, False)
                 wsf = torch.empty_like(wsf)
                 wsb = torch.empty(S.smlm_workspace_size(pool.h, self.b, True) + 256, dtype=torch.uint8, device=dev)
@@ -165,6 +167,10 @@ class Workload:
                     hs = [layer[p]["pool"].h for p in grp]
                     n = S.smlm_workspace_size_multi(hs, self.b)
                     layer[grp] = dict(h=hs, ws=torch.empty(n + 256, dtype=torch.uint8, device=dev))
+            lb = LayerBucket(FT_SLOTS, r, dev)
+            for p in synth.PROJECTIONS:
+                layer[p]["grad"] = lb.bind(p, layer[p]["pool"])
+            self.buckets.append(lb)
             self.layers.append(layer)
 
     def flops(self):
@@ -189,44 +195,54 @@ class Workload:
         rows_lora = int(lens[lora].sum())
         return 2.0 * self.rows * in_f * out_f + 2.0 * rows_lora * r * out_f
 
-    def step(self, L: int, stream, comm=None):
+    def step(self, stream, comm=None, layers=None):
+        """One step: forward of every layer in order, then the fine-tune backward of every layer
+        in reverse; comm(bucket) after each layer's backward (its all-reduce overlaps the next
+        layer's backward).  The 7 backward calls of a layer are independent (own pool, workspace,
+        dX, dA/dB views): they alternate over two streams so one projection's GEMM tail and small
+        kernels overlap the next one's; both streams join before the layer's bucket is reduced."""
         S = self.S
-        layer = self.layers[L]
-        two_f = comm is None and os.environ.get("BENCH_FWD_STREAMS", "1") == "2"
-        if two_f:
-            if getattr(self, "_s2", None) is None:
-                self._s2 = torch.cuda.Stream(self.dev)
-            ev0 = torch.cuda.Event()
-            ev0.record(stream)
-            self._s2.wait_event(ev0)
-            for gi, grp in enumerate(FWD_GROUPS):
-                forward_groups(S, layer, self.b, lambda p: self.X[GROUP_OF[p]], self.Y, self.V,
-                               self._s2 if gi % 2 else stream, [grp])
-            ev1 = torch.cuda.Event()
-            ev1.record(self._s2)
-            stream.wait_event(ev1)
-        else:
-            forward_groups(S, layer, self.b, lambda p: self.X[GROUP_OF[p]], self.Y, self.V, stream)
-        # the 7 backward calls are independent (own pool, workspace, dX, dA/dB): alternate them over
-        # two streams so one projection's GEMM tail / small kernels overlap the next one's
-        two = comm is None and os.environ.get("BENCH_BWD_STREAMS", "2") == "2"
-        if two:
-            if getattr(self, "_s2", None) is None:
-                self._s2 = torch.cuda.Stream(self.dev)
+        order = list(range(N_LAYERS)) if layers is None else list(layers)
+        for L in order:
+            forward_groups(S, self.layers[L], self.b, lambda p: self.X[GROUP_OF[p]], self.Y, self.V, stream)
+        if getattr(self, "_s2", None) is None:
+            self._s2 = torch.cuda.Stream(self.dev)
+        for L in reversed(order):
+            layer = self.layers[L]
             ev = torch.cuda.Event()
             ev.record(stream)
             self._s2.wait_event(ev)
-        for i, p in enumerate(reversed(synth.PROJECTIONS)):
-            e = layer[p]
-            st = self._s2 if (two and i % 2 == 1) else stream
-            S.smlm_backward(e["pool"].h, self.b, self.X[GROUP_OF[p]], e["W"], self.dY[p], self.V[p], self.dX[p],
-                            0, e["wsb"], st)
-            if comm is not None:
-                comm(e["grad"])
-        if two:
+            for i, p in enumerate(reversed(synth.PROJECTIONS)):
+                e = layer[p]
+                st = self._s2 if i % 2 == 1 else stream
+                S.smlm_backward(e["pool"].h, self.b, self.X[GROUP_OF[p]], e["W"], self.dY[p], self.V[p],
+                                self.dX[p], 0, e["wsb"], st)
             ev2 = torch.cuda.Event()
             ev2.record(self._s2)
             stream.wait_event(ev2)
+            if comm is not None:
+                comm(self.buckets[L])
+
+
+class LayerBucket:
+    """One flat fp32 buffer per layer holding the fine-tune adapters' dA/dB of all 7 projections
+    (one all-reduce bucket per layer, 20 MiB at C4/C5); each projection's grads are
+    a dp.GradBucket-shaped view into it."""
+
+    def __init__(self, slots, r, dev):
+        self.slots = list(slots)
+        n = sum(len(self.slots) * r * (i + o) for i, o in (synth.PROJ_SHAPES[p] for p in synth.PROJECTIONS))
+        self.flat = torch.zeros(n, dtype=torch.float32, device=dev)
+        self.r, self.off, self.views = r, 0, {}
+
+    def bind(self, p, pool):
+        in_f, out_f = synth.PROJ_SHAPES[p]
+        n = len(self.slots) * self.r * (in_f + out_f)
+        gb = GradBucket(self.slots, self.r, in_f, out_f, flat=self.flat[self.off:self.off + n])
+        self.off += n
+        gb.bind(pool)
+        self.views[p] = gb
+        return gb
 
 
 def forward_groups(S, layer, b, X_of, Y, V, stream, groups=None):
@@ -303,8 +319,10 @@ def oracle_weights(k):
     return cache
 
 
-def time_oracle(k, n_sample, steps=1):
+def time_oracle(k, n_sample, steps=1, threads=0):
+    """Oracle rows/s on a row sample; threads: OpenMP threads (0 = all host cores)."""
     import oracle
+    oracle.set_num_threads(threads)
     sub, _ = oracle_sample(k, n_sample)
     wc = oracle_weights(k)
     run_oracle_step(synth.batch_from_lengths([1], [0], [0]), k, wc)  # build + warm
@@ -312,7 +330,9 @@ def time_oracle(k, n_sample, steps=1):
     for _ in range(steps):
         run_oracle_step(sub, k, wc)
     dt = time.perf_counter() - t0
-    return sub.S * steps / dt, dt, sub, oracle.num_threads()
+    used = oracle.num_threads()
+    oracle.set_num_threads(0)
+    return sub.S * steps / dt, dt, sub, used
 
 
 # ------------------------------------------------------------------------------------------
@@ -329,7 +349,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-kernel-timing", action="store_true",
                     help="skip the per-kernel CUDA events (A/B check of their overhead)")
-    ap.add_argument("--oracle-rows", type=int, default=24, help="cpu_baseline sample rows (~20 s)")
+    ap.add_argument("--oracle-rows", type=int, default=48, help="cpu_baseline sample rows, all host cores")
+    ap.add_argument("--oracle-rows-1t", type=int, default=6, help="cpu_baseline sample rows, 1 thread")
     ap.add_argument("--ref-rows", type=int, default=8, help="--impl reference sample rows per step")
     args = ap.parse_args()
 
@@ -390,7 +411,7 @@ def main():
             allreduce(bucket, stream)
 
     def one_step(i):
-        wl.step(i % N_LAYER_SETS, stream, comm)
+        wl.step(stream, comm)
         if comm is not None:
             allreduce.join(stream)
 
@@ -399,11 +420,9 @@ def main():
     torch.cuda.synchronize()
     if dist is not None:
         dist.barrier()
-    # time only the dominant kernel class (forward GEMM) inside the timed region: events between
-    # launches serialise programmatic dependent launch, so every extra class costs step time
-    S.smlm_profile_enable(0 if args.no_kernel_timing else 1)
-    for kind in range(4):
-        S.smlm_profile_read(kind)
+
+    # ---- the timed region: K steps, an event after each (all streams joined at a step's end);
+    # no per-launch events in here (they would serialise programmatic dependent launch) ----
     launches0 = S.smlm_launch_count()
     clocks = ClockSampler(dev.index if dev.index is not None else 0)
     clocks.start()
@@ -411,27 +430,51 @@ def main():
     torch.cuda.synchronize()
     if dist is not None:
         dist.barrier()
-    ms_total = _device_timed(one_step, args.steps, stream)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    ev[0].record(stream)
+    for i in range(args.steps):
+        one_step(i)
+        ev[i + 1].record(stream)
+    ev[-1].synchronize()
     torch.cuda.synchronize()
     launches = S.smlm_launch_count() - launches0
-    prof = {kind: S.smlm_profile_read(kind) for kind in range(4)}
-    S.smlm_profile_enable(False)
     clk = clocks.stop()
+    ms_total = ev[0].elapsed_time(ev[-1])
+    per_step = [ev[i].elapsed_time(ev[i + 1]) for i in range(args.steps)]
     if dist is not None:
-        t = torch.tensor([ms_total], device=dev)
+        t = torch.tensor([ms_total] + per_step, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms_total = float(t.item())
+        ms_total, per_step = float(t[0].item()), [float(x) for x in t[1:].tolist()]
         dist.barrier()
     ms = ms_total / args.steps
-    value = n * wl.rows / (ms / 1000.0)
+    value = n * wl.rows * N_LAYERS / (ms / 1000.0)
+    q = np.percentile(np.array(per_step), [10, 50, 90])
+    step_stats = {"p10_ms": float(q[0]), "p50_ms": float(q[1]), "p90_ms": float(q[2]),
+                  "mean_ms": ms, "note": "per-step CUDA events on the launching stream, max over ranks"}
 
-    # ---- roofline of the dominant kernel: the forward tensor-core GEMM ----
+    # ---- roofline of the dominant kernel (the forward tensor-core GEMM): a second pass of K
+    # steps with CUDA events around each of its launches on the launching stream ----
+    prof = {kind: (0.0, 0) for kind in range(4)}
+    ms_prof = None
+    if not args.no_kernel_timing:
+        S.smlm_profile_enable(1)
+        for kind in range(4):
+            S.smlm_profile_read(kind)
+        torch.cuda.synchronize()
+        ms_prof = _device_timed(one_step, args.steps, stream)
+        torch.cuda.synchronize()
+        prof = {kind: S.smlm_profile_read(kind) for kind in range(4)}
+        S.smlm_profile_enable(False)
     peaks = _peaks()
     fwd_ms, fwd_n = prof[0]
-    bwd_ms, bwd_n = prof[1]
-    fwd_flops = sum(wl.fwd_gemm_flops(p) for p in synth.PROJECTIONS) * args.steps
+    fwd_flops = sum(wl.fwd_gemm_flops(p) for p in synth.PROJECTIONS) * N_LAYERS * args.steps
     achieved = fwd_flops / (fwd_ms / 1000.0) / 1e12 if fwd_ms > 0 else 0.0
-    peak = peaks["bf16_sustained"] or peaks["bf16"]
+    # denominator: the burst cuBLAS peak when the timed region ran at max SM clock, else (power
+    # cap active, clocks below max) the sustained one measured under the same cap; both reported
+    peak_b = peaks["bf16"]
+    peak_s = peaks["bf16_sustained"] or peaks["bf16"]
+    at_max = bool(clk.get("sm_mhz") and clk.get("sm_max_mhz") and clk["sm_mhz"] >= 0.97 * clk["sm_max_mhz"])
+    peak = peak_b if at_max else peak_s
     traffic = None
     ncu_sum = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(ncu_sum):
@@ -441,14 +484,21 @@ def main():
         except Exception:
             traffic = None
     f_alg, b_alg = wl.flops()
-    step_tflops = (f_alg + b_alg) / (ms / 1000.0) / 1e12
+    step_tflops = (f_alg + b_alg) * N_LAYERS / (ms / 1000.0) / 1e12
     roofline = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                 "frac": achieved / peak if peak else None, "traffic": traffic,
                 "kernel": "smlm_gemm2_kernel<fwd, pre-shrunk> (tcgen05 cta_group::2; full 256-column W tiles + s*V expand K-block)",
-                "peak_source": peaks["source"] + " bf16_tflops_sustained",
+                "peak_source": peaks["source"] + (" bf16_tflops (burst: the timed region ran at max SM clock)" if at_max
+                                                  else " bf16_tflops_sustained (the timed region ran below max SM "
+                                                       "clock under the power cap)"),
+                "frac_burst": achieved / peak_b if peak_b else None, "peak_burst": peak_b,
+                "frac_sustained": achieved / peak_s if peak_s else None, "peak_sustained": peak_s,
                 "launches": fwd_n, "avg_launch_ms": fwd_ms / max(fwd_n, 1),
-                "share_of_step": fwd_ms / ms_total if ms_total else None,
-                "step_alg_tflops": step_tflops, "step_frac": step_tflops / peak}
+                "share_of_step": fwd_ms / ms_prof if ms_prof else None,
+                "timing": "per-launch CUDA events in a second pass of the same K steps (the graded timed "
+                          "region has none)",
+                "step_alg_tflops": step_tflops, "step_frac": step_tflops / peak,
+                "step_frac_burst": step_tflops / peak_b, "step_frac_sustained": step_tflops / peak_s}
 
     # ---- end to end: host buffers through the public API ----
     e2e = None
@@ -467,6 +517,7 @@ def main():
             side = {"C2_decode": {"workload": c2["config"], "rows": c2["S"], "ms_graph_replay": c2["ms_graph_replay"],
                                   "ms_back_to_back": c2["ms_back_to_back"], "rows_per_s": c2["rows_per_s"],
                                   "hbm_roofline_frac": c2["hbm_roofline_frac_graph"],
+                                  "hbm_roofline_frac_back_to_back": c2["hbm_roofline_frac_b2b"],
                                   "roofline_ms": c2["roofline_ms"], "bound": "hbm"},
                     "C3_prefill": {"workload": synth.CONFIGS[3].name + ": gate, up, down", "ms": tot3,
                                    "rows_per_s": synth.config_batch(3).S / (tot3 / 1e3),
@@ -484,9 +535,12 @@ def main():
     cpu = None
     if rank == 0 and n == 1 and not args.no_cpu_baseline:
         v, dt, sub, threads = time_oracle(k, args.oracle_rows, 1)
+        v1, dt1, sub1, _ = time_oracle(k, args.oracle_rows_1t, 1, threads=1)
         cpu = {"value": v, "unit": UNIT, "cores": threads, "kind": "oracle",
                "sample": f"{sub.S} rows evenly spread over the {spec.name} batch; fp64 forward of 7 projections "
-                         f"+ fine-tune backward (dX, dA, dB); {dt:.1f} s"}
+                         f"+ fine-tune backward (dX, dA, dB) = one layer-step of those rows; {dt:.1f} s",
+               "single_thread": {"value": v1, "unit": UNIT, "cores": 1,
+                                 "sample": f"{sub1.S} rows, same recipe; {dt1:.1f} s"}}
 
     if rank == 0:
         out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": n, "steps": args.steps,
@@ -495,11 +549,16 @@ def main():
                "config": {"workload": spec.name + ": Llama-3-8B projections q,k,v,o,gate,up,down; r=16; "
                           f"{spec.n_adapters} adapters; 4 fine-tune x 1024 rows (fwd+bwd) + 8 prefill "
                           "(512-2048) + 128 decode rows",
-                          "rows_per_step_per_gpu": wl.rows, "finetune_rows": wl.ft_rows, "rank": spec.rank,
-                          "adapters": spec.n_adapters, "parallelism": f"dp{n}",
-                          "l2": f"inputs larger than L2: {N_LAYER_SETS} rotated layer weight sets of 416 MiB",
-                          "step": "1 layer-step = forward 7 projections + fine-tune backward 7 projections"
-                                  + (" + NCCL all-reduce of fine-tune dA/dB" if n > 1 else "")},
+                          "rows_per_layer_per_gpu": wl.rows, "finetune_rows": wl.ft_rows, "rank": spec.rank,
+                          "adapters": spec.n_adapters, "parallelism": f"dp{n}", "layers_per_step": N_LAYERS,
+                          "l2": f"inputs larger than L2: every layer of the step has its own weight set "
+                                f"(416 MiB each, {N_LAYERS} per step)",
+                          "step": f"forward of the 7 projections of layers 0..{N_LAYERS - 1}, then the fine-tune "
+                                  f"backward of layers {N_LAYERS - 1}..0"
+                                  + (" with one NCCL all-reduce of the layer's fine-tune dA/dB (20 MiB fp32 bucket) "
+                                     "per layer, overlapping the next layer's backward" if n > 1 else ""),
+                          "tokens_per_s": "rows x layers / step time (per-layer throughput, SURVEY §8(d))"},
+               "step_stats": step_stats,
                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
                "clocks": clk, "configs": side}
         print(json.dumps(out))
@@ -511,9 +570,10 @@ def main():
 def run_e2e(wl, stream, steps, n, dist):
     """Same step through the public API with HOST buffers: every step copies the step's inputs
     (X per projection group for every row; dY of the fine-tune rows) from pinned host memory and
-    reads back the step's results: the fine-tune adapters' dA/dB (what the optimizer consumes) and
-    Y of the decode rows of every projection (what the serving loop consumes).  Intermediates that
-    stay on the device in a real model (prefill/fine-tune Y, dX) are not copied.
+    reads back the step's results: every layer's fine-tune dA/dB (what the optimizer consumes) and
+    Y of the decode rows of every projection of the last layer (what the serving loop consumes).
+    Intermediates that stay on the device in a real model (other layers' activations, prefill /
+    fine-tune Y, dX) are not copied.
 
     Pipelined like a serving/training loop would be: device buffers are double-buffered, H2D of
     step i+1 runs on its own stream while step i computes, and each projection's outputs are read
@@ -528,13 +588,13 @@ def run_e2e(wl, stream, steps, n, dist):
     dec0 = int(wl.batch.offsets[int(np.argmax(wl.batch.modes == synth.DECODE))]) if np.any(
         wl.batch.modes == synth.DECODE) else wl.rows
     hY = {p: torch.empty(wl.rows - dec0, y.shape[1], dtype=y.dtype).pin_memory() for p, y in wl.Y.items()}
-    hG = {p: torch.empty_like(wl.layers[0][p]["grad"].flat, device="cpu").pin_memory() for p in synth.PROJECTIONS}
+    hG = [torch.empty_like(b.flat, device="cpu").pin_memory() for b in wl.buckets]
     for g in hX:
         hX[g].copy_(wl.X[g].cpu())
     for p in hdY:
         hdY[p].copy_(wl.dY[p][:ft].cpu())
     h2d = sum(t.numel() * t.element_size() for t in hX.values()) + sum(t.numel() * t.element_size() for t in hdY.values())
-    d2h = sum(t.numel() * t.element_size() for t in hY.values()) + sum(t.numel() * t.element_size() for t in hG.values())
+    d2h = sum(t.numel() * t.element_size() for t in hY.values()) + sum(t.numel() * t.element_size() for t in hG)
     # double-buffered device tensors: [0] = the workload's own, [1] = a second set
     Xb = [wl.X, {g: torch.empty_like(x) for g, x in wl.X.items()}]
     dYb = [wl.dY, {p: torch.empty_like(y) for p, y in wl.dY.items()}]
@@ -569,9 +629,11 @@ def run_e2e(wl, stream, steps, n, dist):
         s_h2d.wait_stream(s_h2d2)
         in_ready[b].record(s_h2d)
 
+    if getattr(wl, "_s2", None) is None:
+        wl._s2 = torch.cuda.Stream(dev)
+
     def compute(i):
         b = i % 2
-        layer = wl.layers[i % N_LAYER_SETS]
         stream.wait_event(in_ready[b])
         if out_done[b] is not None:
             stream.wait_event(out_done[b])
@@ -579,25 +641,36 @@ def run_e2e(wl, stream, steps, n, dist):
             e = torch.cuda.Event(enable_timing=True)
             e.record(stream)
             diag.append(("compute_start", i, e))
-        for grp in FWD_GROUPS:
-            forward_groups(S, layer, wl.b, lambda p: Xb[b][GROUP_OF[p]], Yb[b], Vb[b], stream, [grp])
+        for L in range(N_LAYERS):
+            layer = wl.layers[L]
+            for grp in FWD_GROUPS:
+                forward_groups(S, layer, wl.b, lambda p: Xb[b][GROUP_OF[p]], Yb[b], Vb[b], stream, [grp])
+                if L == N_LAYERS - 1:
+                    ev = torch.cuda.Event()
+                    ev.record(stream)
+                    s_d2h.wait_event(ev)
+                    with torch.cuda.stream(s_d2h):
+                        for p in grp:
+                            hY[p].copy_(Yb[b][p][dec0:], non_blocking=True)
+        for L in reversed(range(N_LAYERS)):
+            layer = wl.layers[L]
             ev = torch.cuda.Event()
             ev.record(stream)
-            s_d2h.wait_event(ev)
-            with torch.cuda.stream(s_d2h):
-                for p in grp:
-                    hY[p].copy_(Yb[b][p][dec0:], non_blocking=True)
-        for p in reversed(synth.PROJECTIONS):
-            e = layer[p]
-            S.smlm_backward(e["pool"].h, wl.b, Xb[b][GROUP_OF[p]], e["W"], dYb[b][p], Vb[b][p], dXb[b][p], 0,
-                            e["wsb"], stream)
+            wl._s2.wait_event(ev)
+            for j, p in enumerate(reversed(synth.PROJECTIONS)):
+                e = layer[p]
+                S.smlm_backward(e["pool"].h, wl.b, Xb[b][GROUP_OF[p]], e["W"], dYb[b][p], Vb[b][p], dXb[b][p], 0,
+                                e["wsb"], wl._s2 if j % 2 else stream)
+            ev = torch.cuda.Event()
+            ev.record(wl._s2)
+            stream.wait_event(ev)
             if dist is not None:
-                dist.all_reduce(e["grad"].flat, op=dist.ReduceOp.SUM)
+                dist.all_reduce(wl.buckets[L].flat, op=dist.ReduceOp.SUM)
             ev = torch.cuda.Event()
             ev.record(stream)
             s_d2h.wait_event(ev)
             with torch.cuda.stream(s_d2h):
-                hG[p].copy_(e["grad"].flat, non_blocking=True)
+                hG[L].copy_(wl.buckets[L].flat, non_blocking=True)
         ev = torch.cuda.Event(enable_timing=diag is not None)
         ev.record(stream)
         in_free[b] = ev
@@ -636,11 +709,12 @@ def run_e2e(wl, stream, steps, n, dist):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     del Xb, dYb, Yb, dXb, Vb
-    return {"value": n * wl.rows / (ms / 1000.0), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+    return {"value": n * wl.rows * N_LAYERS / (ms / 1000.0), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
             "d2h_bytes_per_step": int(d2h), "ms_per_step": ms,
-            "h2d": "X of every row (4 activation groups) + dY of the fine-tune rows",
-            "d2h": "fine-tune dA/dB of the 7 projections + Y of the decode rows",
-            "pipelining": "double-buffered; H2D of step i+1 and per-projection D2H overlap step i's kernels"}
+            "h2d": "X of every row (4 activation groups) + dY of the fine-tune rows, once per step",
+            "d2h": f"fine-tune dA/dB of the 7 projections of all {N_LAYERS} layers + Y of the decode rows "
+                   "(last layer)",
+            "pipelining": "double-buffered; H2D of step i+1 and per-layer D2H overlap step i's kernels"}
 
 
 if __name__ == "__main__":

@@ -52,12 +52,19 @@ def _load():
                                             P, I, I, P]
             lib.oracle_backward.restype = I
             lib.oracle_num_threads.restype = I
+            lib.oracle_set_num_threads.argtypes = [I]
+            lib.oracle_set_num_threads.restype = None
             _lib = lib
     return _lib
 
 
 def num_threads() -> int:
     return _load().oracle_num_threads()
+
+
+def set_num_threads(n: int) -> None:
+    """Threads of the row-parallel loops (n <= 0: all host cores); results do not depend on it."""
+    _load().oracle_set_num_threads(int(n))
 
 
 def _f64(t) -> np.ndarray:

@@ -225,3 +225,17 @@ int oracle_num_threads(void)
     return 1;
 #endif
 }
+
+/* Thread count of the row-parallel loops (bench.py times the oracle at 1 thread and at all host
+ * cores); n <= 0 restores the OpenMP default.  No effect on results (rows are independent and
+ * every sum runs in a fixed order inside one thread). */
+void oracle_set_num_threads(int n)
+{
+#ifdef _OPENMP
+    extern void omp_set_num_threads(int);
+    extern int omp_get_num_procs(void);
+    omp_set_num_threads(n > 0 ? n : omp_get_num_procs());
+#else
+    (void)n;
+#endif
+}

@@ -2,10 +2,11 @@
 
 Request batches are independent per GPU; base weights and adapters are replicated; the only
 exchange is a SUM all-reduce of the fine-tune adapters' fp32 dA/dB (PAPER.md P:422 masking: only
-fine-tune adapters carry gradients).  One flat bucket per (layer, projection) holds the dA/dB of
-the fine-tune slots so that a single NCCL call reduces them; on CUDA the call is issued on a
-side stream that waits on an event recorded after the projection's backward, so it overlaps the
-next projection's backward.  Pure plumbing: no SMLM arithmetic lives here.
+fine-tune adapters carry gradients).  A flat bucket holds the dA/dB of the fine-tune slots so
+that a single NCCL call reduces them (bench.py: one bucket per layer whose per-projection
+GradBucket views share one buffer); on CUDA the call is issued on a side stream that waits on an
+event recorded after the layer's backward, so it overlaps the next layer's backward.  Pure
+plumbing: no SMLM arithmetic lives here.
 """
 from __future__ import annotations
 
@@ -17,11 +18,15 @@ import torch
 class GradBucket:
     """Flat fp32 buffer [ |slots| * r*in  |  |slots| * out*r ] with per-slot dA/dB views."""
 
-    def __init__(self, slots: Sequence[int], r: int, in_f: int, out_f: int, device="cpu"):
+    def __init__(self, slots: Sequence[int], r: int, in_f: int, out_f: int, device="cpu", flat=None):
+        """flat: an existing fp32 buffer of numel() elements to use (e.g. a slice of a per-layer bucket)."""
         self.slots = list(slots)
         self.r, self.in_f, self.out_f = r, in_f, out_f
         self.nA, self.nB = r * in_f, out_f * r
-        self.flat = torch.zeros(len(self.slots) * (self.nA + self.nB), dtype=torch.float32, device=device)
+        n = len(self.slots) * (self.nA + self.nB)
+        if flat is not None and (flat.numel() != n or flat.dtype != torch.float32):
+            raise ValueError("GradBucket: flat must be fp32 with len(slots) * r * (in + out) elements")
+        self.flat = torch.zeros(n, dtype=torch.float32, device=device) if flat is None else flat
 
     def dA(self, i: int) -> torch.Tensor:
         return self.flat[i * self.nA:(i + 1) * self.nA].view(self.r, self.in_f)

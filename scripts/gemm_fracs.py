@@ -15,14 +15,14 @@ dev = torch.device("cuda", 0)
 wl = bench.Workload(4, synth.CONFIGS[4].rank, dev)
 st = torch.cuda.current_stream()
 for i in range(4):
-    wl.step(i % bench.N_LAYER_SETS, st)
+    wl.step(st)
 torch.cuda.synchronize()
 peaks = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "MEASURED_PEAKS.json")))
 for kind, name in ((0, "fwd"), (1, "bwd")):
     S.smlm_profile_enable(1 << kind)
     S.smlm_profile_read(kind)
     for i in range(6):
-        wl.step(i % bench.N_LAYER_SETS, st)
+        wl.step(st)
     torch.cuda.synchronize()
     ms, n = S.smlm_profile_read(kind)
     S.smlm_profile_enable(0)

@@ -14,11 +14,11 @@ dev = torch.device("cuda", 0)
 wl = bench.Workload(4, 0, dev)
 st = torch.cuda.current_stream()
 for i in range(3):
-    wl.step(i % bench.N_LAYER_SETS, st)
+    wl.step(st)
 torch.cuda.synchronize()
 with profile(activities=[ProfilerActivity.CUDA]) as prof:
     for i in range(3):
-        wl.step(i % bench.N_LAYER_SETS, st)
+        wl.step(st)
     torch.cuda.synchronize()
 ev = [e for e in prof.events() if e.device_type.name == "CUDA"]
 ev.sort(key=lambda e: e.time_range.start)
