@@ -134,13 +134,16 @@ class Workload:
         self.X = {}
         for grp, in_f in (("attn", 4096), ("o", 4096), ("mlp", 4096), ("down", 14336)):
             self.X[grp] = torch.randn(self.rows, in_f, generator=g, device=dev).to(torch.bfloat16)
-        self.dY, self.Y, self.dX, self.V = {}, {}, {}, {}
+        # V_save of the fine-tune rows is per layer (layer L's backward consumes layer L's forward V)
+        self.dY, self.Y, self.dX = {}, {}, {}
+        self.V = [{} for _ in range(N_LAYERS)]
         for p in synth.PROJECTIONS:
             in_f, out_f = synth.PROJ_SHAPES[p]
             self.dY[p] = torch.randn(self.rows, out_f, generator=g, device=dev).to(torch.bfloat16)
             self.Y[p] = torch.empty(self.rows, out_f, dtype=torch.bfloat16, device=dev)
             self.dX[p] = torch.empty(self.rows, in_f, dtype=torch.bfloat16, device=dev)
-            self.V[p] = torch.zeros(self.rows, r, dtype=torch.bfloat16, device=dev)
+            for L in range(N_LAYERS):
+                self.V[L][p] = torch.zeros(self.rows, r, dtype=torch.bfloat16, device=dev)
         # layer sets: base weights + adapter pools (replicated across ranks: same seeds)
         self.layers = []
         self.buckets = []   # one flat fp32 all-reduce bucket per layer (the 7 projections' FT dA/dB)
@@ -204,7 +207,7 @@ class Workload:
         S = self.S
         order = list(range(N_LAYERS)) if layers is None else list(layers)
         for L in order:
-            forward_groups(S, self.layers[L], self.b, lambda p: self.X[GROUP_OF[p]], self.Y, self.V, stream)
+            forward_groups(S, self.layers[L], self.b, lambda p: self.X[GROUP_OF[p]], self.Y, self.V[L], stream)
         if getattr(self, "_s2", None) is None:
             self._s2 = torch.cuda.Stream(self.dev)
         for L in reversed(order):
@@ -215,7 +218,7 @@ class Workload:
             for i, p in enumerate(reversed(synth.PROJECTIONS)):
                 e = layer[p]
                 st = self._s2 if i % 2 == 1 else stream
-                S.smlm_backward(e["pool"].h, self.b, self.X[GROUP_OF[p]], e["W"], self.dY[p], self.V[p],
+                S.smlm_backward(e["pool"].h, self.b, self.X[GROUP_OF[p]], e["W"], self.dY[p], self.V[L][p],
                                 self.dX[p], 0, e["wsb"], st)
             ev2 = torch.cuda.Event()
             ev2.record(self._s2)
@@ -600,7 +603,7 @@ def run_e2e(wl, stream, steps, n, dist):
     dYb = [wl.dY, {p: torch.empty_like(y) for p, y in wl.dY.items()}]
     Yb = [wl.Y, {p: torch.empty_like(y) for p, y in wl.Y.items()}]
     dXb = [wl.dX, {p: torch.empty_like(x) for p, x in wl.dX.items()}]
-    Vb = [wl.V, {p: torch.zeros_like(v) for p, v in wl.V.items()}]
+    Vb = [wl.V, [{p: torch.zeros_like(v) for p, v in VL.items()} for VL in wl.V]]
     s_h2d = torch.cuda.Stream(dev)
     s_h2d2 = torch.cuda.Stream(dev)   # second copy engine for the input stream
     s_d2h = torch.cuda.Stream(dev)
@@ -644,7 +647,7 @@ def run_e2e(wl, stream, steps, n, dist):
         for L in range(N_LAYERS):
             layer = wl.layers[L]
             for grp in FWD_GROUPS:
-                forward_groups(S, layer, wl.b, lambda p: Xb[b][GROUP_OF[p]], Yb[b], Vb[b], stream, [grp])
+                forward_groups(S, layer, wl.b, lambda p: Xb[b][GROUP_OF[p]], Yb[b], Vb[b][L], stream, [grp])
                 if L == N_LAYERS - 1:
                     ev = torch.cuda.Event()
                     ev.record(stream)
@@ -659,7 +662,7 @@ def run_e2e(wl, stream, steps, n, dist):
             wl._s2.wait_event(ev)
             for j, p in enumerate(reversed(synth.PROJECTIONS)):
                 e = layer[p]
-                S.smlm_backward(e["pool"].h, wl.b, Xb[b][GROUP_OF[p]], e["W"], dYb[b][p], Vb[b][p], dXb[b][p], 0,
+                S.smlm_backward(e["pool"].h, wl.b, Xb[b][GROUP_OF[p]], e["W"], dYb[b][p], Vb[b][L][p], dXb[b][p], 0,
                                 e["wsb"], wl._s2 if j % 2 else stream)
             ev = torch.cuda.Event()
             ev.record(wl._s2)
