@@ -169,7 +169,9 @@ class Workload:
                 if len(grp) > 1:
                     hs = [layer[p]["pool"].h for p in grp]
                     n = S.smlm_workspace_size_multi(hs, self.b)
-                    layer[grp] = dict(h=hs, ws=torch.empty(n + 256, dtype=torch.uint8, device=dev))
+                    nb = S.smlm_workspace_size_backward_multi(hs, self.b)
+                    layer[grp] = dict(h=hs, ws=torch.empty(n + 256, dtype=torch.uint8, device=dev),
+                                      wsb=torch.empty(nb + 256, dtype=torch.uint8, device=dev))
             lb = LayerBucket(FT_SLOTS, r, dev)
             for p in synth.PROJECTIONS:
                 layer[p]["grad"] = lb.bind(p, layer[p]["pool"])
@@ -201,9 +203,10 @@ class Workload:
     def step(self, stream, comm=None, layers=None):
         """One step: forward of every layer in order, then the fine-tune backward of every layer
         in reverse; comm(bucket) after each layer's backward (its all-reduce overlaps the next
-        layer's backward).  The 7 backward calls of a layer are independent (own pool, workspace,
-        dX, dA/dB views): they alternate over two streams so one projection's GEMM tail and small
-        kernels overlap the next one's; both streams join before the layer's bucket is reduced."""
+        layer's backward).  The backward of a layer is 4 independent calls (down; gate+up and
+        q+k+v through smlm_backward_multi: one dX GEMM launch per group; o): they alternate over
+        two streams so one group's GEMM tail and small kernels overlap the next one's; both
+        streams join before the layer's bucket is reduced."""
         S = self.S
         order = list(range(N_LAYERS)) if layers is None else list(layers)
         for L in order:
@@ -215,11 +218,9 @@ class Workload:
             ev = torch.cuda.Event()
             ev.record(stream)
             self._s2.wait_event(ev)
-            for i, p in enumerate(reversed(synth.PROJECTIONS)):
-                e = layer[p]
-                st = self._s2 if i % 2 == 1 else stream
-                S.smlm_backward(e["pool"].h, self.b, self.X[GROUP_OF[p]], e["W"], self.dY[p], self.V[L][p],
-                                self.dX[p], 0, e["wsb"], st)
+            for i, grp in enumerate(reversed(FWD_GROUPS)):
+                backward_group(S, layer, self.b, self.X[GROUP_OF[grp[0]]], self.dY, self.V[L], self.dX, grp,
+                               self._s2 if i % 2 == 1 else stream)
             ev2 = torch.cuda.Event()
             ev2.record(self._s2)
             stream.wait_event(ev2)
@@ -246,6 +247,17 @@ class LayerBucket:
         gb.bind(pool)
         self.views[p] = gb
         return gb
+
+
+def backward_group(S, layer, b, X, dY, V, dX, grp, stream):
+    """Backward of one projection group: smlm_backward_multi for projections that share X (one dX
+    GEMM launch over all their n-tiles), smlm_backward for the others."""
+    if len(grp) > 1:
+        S.smlm_backward_multi(layer[grp]["h"], b, X, [layer[p]["W"] for p in grp], [dY[p] for p in grp],
+                              [V[p] for p in grp], [dX[p] for p in grp], False, layer[grp]["wsb"], stream)
+    else:
+        e = layer[grp[0]]
+        S.smlm_backward(e["pool"].h, b, X, e["W"], dY[grp[0]], V[grp[0]], dX[grp[0]], 0, e["wsb"], stream)
 
 
 def forward_groups(S, layer, b, X_of, Y, V, stream, groups=None):
@@ -660,10 +672,9 @@ def run_e2e(wl, stream, steps, n, dist):
             ev = torch.cuda.Event()
             ev.record(stream)
             wl._s2.wait_event(ev)
-            for j, p in enumerate(reversed(synth.PROJECTIONS)):
-                e = layer[p]
-                S.smlm_backward(e["pool"].h, wl.b, Xb[b][GROUP_OF[p]], e["W"], dYb[b][p], Vb[b][L][p], dXb[b][p], 0,
-                                e["wsb"], wl._s2 if j % 2 else stream)
+            for j, grp in enumerate(reversed(FWD_GROUPS)):
+                backward_group(S, layer, wl.b, Xb[b][GROUP_OF[grp[0]]], dYb[b], Vb[b][L], dXb[b], grp,
+                               wl._s2 if j % 2 else stream)
             ev = torch.cuda.Event()
             ev.record(wl._s2)
             stream.wait_event(ev)

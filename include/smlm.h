@@ -176,8 +176,9 @@ SMLM_API int smlm_forward(smlm_pool pool, const smlm_batch *batch, const void *X
  * (<= 512 rows, no segment >= L_long) runs as ONE launch that streams every W[i] once and reads X
  * once, and a mixed bf16 batch computes s*V of its long tiles for every projection in ONE
  * pre-shrink pass over X (n_proj * r_pad <= 128; bit-identical to the per-pool calls) before each
- * projection's GEMM.  Otherwise (e.g. different slot scales across pools) the per-pool calls run
- * in sequence.
+ * projection's short-row shrink, and (n_proj <= 3) all projections' GEMMs run as ONE persistent
+ * CTA-pair launch over the n-tiles of every projection.  Otherwise (e.g. different slot scales
+ * across pools) the per-pool calls run in sequence.
  *   n_proj in [1, 4]; pools share device, in_features, rank and dtype; every slot of the batch
  *   must be registered in every pool (else SMLM_E_SLOT);
  *   W[i] != NULL; Y[i] [S, out_i]; V_save NULL or an array of n_proj pointers (each may be NULL).
@@ -202,6 +203,24 @@ SMLM_API int smlm_forward_multi(int n_proj, const smlm_pool *pools, const smlm_b
 SMLM_API int smlm_backward(smlm_pool pool, const smlm_batch *batch, const void *X, const void *W,
                   const void *dY, const void *V_save, void *dX, int accumulate, void *ws,
                   size_t ws_bytes, void *stream);
+
+/*
+ * Multi-projection backward (SURVEY §8(f1) for the backward; "a shared backward
+ * pass"; Alg. 1: q, k, v -- or gate, up -- read the same X): for i in [0, n_proj), exactly
+ *     smlm_backward(pools[i], batch, X, W[i], dY[i], V_save ? V_save[i] : NULL, dX[i], accumulate, ...)
+ * (bit-identical), but the dX GEMMs of all projections run as ONE persistent CTA-pair launch over
+ * the n-tiles of every projection (no per-projection wave tail); each projection's U pass and
+ * dA/dB contraction are its own launches.
+ *   n_proj in [1, 3]; pools share device, in_features, rank, dtype and options; W[i], dY[i] [S,out_i]
+ *   and dX[i] [S,in] non-NULL; V_save NULL or an array of n_proj pointers (each may be NULL).
+ *   ws: ws_bytes >= smlm_workspace_size_backward_multi(n_proj, pools, batch).
+ * Errors as smlm_backward; SMLM_E_INVALID for n_proj outside [1, 3], SMLM_E_SHAPE for pools that
+ * differ in in_features / rank / dtype / options.
+ */
+SMLM_API size_t smlm_workspace_size_backward_multi(int n_proj, const smlm_pool *pools, const smlm_batch *batch);
+SMLM_API int smlm_backward_multi(int n_proj, const smlm_pool *pools, const smlm_batch *batch, const void *X,
+                                 const void *const *W, const void *const *dY, const void *const *V_save,
+                                 void *const *dX, int accumulate, void *ws, size_t ws_bytes, void *stream);
 
 /*
  * The canonical work plan (segment scheduler output), as int32

@@ -694,6 +694,164 @@ int run_dec3(int n_proj, const smlm_pool *pools, const smlm_batch *b, const Dec3
     return SMLM_OK;
 }
 
+// ------------------------------------------------------------------------------------------
+// bf16 forward: plan upload + short-row shrink (everything but the GEMM), and the CTA-pair GEMM
+// arguments for one or several projections that share X and the batch
+// ------------------------------------------------------------------------------------------
+struct FwdPrep {
+    int n_tiles = 0, n_long = 0, n_pairs = 0, n_pre_items = 0, n_blocks = 0;
+    const DevTile *tiles_dev = nullptr;
+    const DevBlock *blocks_dev = nullptr;
+    const DevPair *pairs_dev = nullptr;   // set when the CTA-pair GEMM runs (W != NULL, cta_pair)
+    const int *pre_items_dev = nullptr;
+    __nv_bfloat16 *vbd = nullptr;          // block-diagonal s*V of the short tiles
+    const SlotDev *slots = nullptr;
+};
+
+// A CTA pair takes two CONSECUTIVE tiles of the kept list (long tiles in segment order, then the
+// short tiles), whatever their segments: only the partial 128-row tile at each segment end is
+// padding (DESIGN K1).  An odd tile count leaves one half empty.
+static DevHalf half_of(const DevTile &t, int idx) {
+    DevHalf h{};
+    h.row0 = t.row0;
+    h.rows = t.rows;
+    if (t.flags & kTileShort) {
+        h.slot = -1;
+        h.flags = kPairShort;
+        h.blk0 = t.blk0;
+        h.nblk = t.nblk;
+    } else {
+        h.slot = t.slot;
+        h.flags = (t.flags & kTileFT) ? kPairFT : 0;
+        h.scale = t.scale;
+        h.tile = idx;
+    }
+    return h;
+}
+static void make_pairs(const std::vector<DevTile> &tiles, std::vector<DevPair> &pairs) {
+    pairs.clear();
+    for (size_t i = 0; i < tiles.size(); i += 2) {
+        DevPair pr{};
+        pr.h[0] = half_of(tiles[i], (int)i);
+        if (i + 1 < tiles.size()) {
+            pr.h[1] = half_of(tiles[i + 1], (int)i + 1);
+        } else {
+            pr.h[1] = pr.h[0];
+            pr.h[1].rows = 0;
+            pr.h[1].slot = -1;
+            pr.h[1].flags = 0;
+            pr.h[1].nblk = 0;
+        }
+        pairs.push_back(pr);
+    }
+}
+
+static int fwd_prepare(smlm_pool p, const smlm_batch *b, const Plan &plan, const WsLayout &L, const void *X,
+                       const void *W, void *V_save, uint8_t *wsb, int *uctr, cudaStream_t st, FwdPrep &F) {
+    int rc;
+    const bool has_w = W != nullptr;
+    std::vector<DevTile> tiles;
+    tiles.reserve(plan.long_tiles.size() + plan.short_tiles.size());
+    for (auto &t : plan.long_tiles)
+        if (has_w || (t.flags & kTileLora)) tiles.push_back(t);
+    F.n_long = (int)tiles.size();
+    for (auto &t : plan.short_tiles)
+        if (has_w || t.nblk > 0) tiles.push_back(t);
+    F.n_tiles = (int)tiles.size();
+    std::vector<DevPair> pairs;
+    const bool pair_gemm = has_w && p->cta_pair;
+    if (pair_gemm) make_pairs(tiles, pairs);
+    std::vector<int> pre_items;   // long tiles with an adapter (pre-shrink work items)
+    if (pair_gemm && use_preshrink(p))
+        for (int i = 0; i < F.n_long; ++i)
+            if (tiles[i].slot >= 0) pre_items.push_back(i);
+    std::vector<uint8_t> bytes;
+    append(bytes, tiles);
+    const size_t blk_off = bytes.size();
+    append(bytes, plan.blocks);
+    const size_t srow_off = bytes.size();
+    append(bytes, plan.short_rows);
+    while (bytes.size() % 16) bytes.push_back(0);
+    const size_t pair_off = bytes.size();
+    append(bytes, pairs);
+    const size_t pre_off = bytes.size();
+    append(bytes, pre_items);
+    F.tiles_dev = reinterpret_cast<const DevTile *>(wsb + L.plan_off);
+    F.blocks_dev = reinterpret_cast<const DevBlock *>(wsb + L.plan_off + blk_off);
+    const DevShortRow *d_srows = reinterpret_cast<const DevShortRow *>(wsb + L.plan_off + srow_off);
+    F.pairs_dev = pair_gemm ? reinterpret_cast<const DevPair *>(wsb + L.plan_off + pair_off) : nullptr;
+    F.pre_items_dev = reinterpret_cast<const int *>(wsb + L.plan_off + pre_off);
+    F.n_pairs = (int)pairs.size();
+    F.n_pre_items = (int)pre_items.size();
+    F.n_blocks = (int)plan.blocks.size();
+    F.vbd = reinterpret_cast<__nv_bfloat16 *>(wsb + L.vbd_off);
+    F.slots = p->d_slots;
+    if ((rc = stage_upload(p, bytes, wsb + L.plan_off, st))) return rc;
+    if (!plan.blocks.empty()) {
+        ProfScope ps(2, st);
+        if (L.spart_bytes) {
+            // the last chunk of each block combines it in-kernel (stream counters, self-resetting)
+            int *sctr = (int)plan.blocks.size() <= kUCtrMax ? uctr : nullptr;
+            CKL(launch_shrink_split((const __nv_bfloat16 *)X, p->d_slots, F.blocks_dev, d_srows,
+                                    (int)plan.blocks.size(), p->in, p->r, p->r_pad,
+                                    reinterpret_cast<float *>(wsb + L.spart_off), F.vbd, (__nv_bfloat16 *)V_save,
+                                    sctr, st), sctr ? 1 : 2);
+        } else {
+            CKL(launch_shrink_short((const __nv_bfloat16 *)X, p->d_slots, F.blocks_dev, d_srows,
+                                    (int)plan.blocks.size(), p->in, p->r, p->r_pad, F.vbd, (__nv_bfloat16 *)V_save,
+                                    st), 1);
+        }
+    }
+    return SMLM_OK;
+}
+
+// CTA-pair GEMM arguments for n_proj projections (pools share in / r / dtype and the batch plan):
+// F[i] from fwd_prepare of projection i (its own workspace: short-tile s*V), pre_sv[i] its
+// tile-compact s*V of the long tiles.  The pairs / tiles of F[0] serve every projection.
+static int gemm2_fwd_args(int n_proj, const smlm_pool *pools, const smlm_batch *b, const void *X,
+                          const void *const *W, void *const *Y, const FwdPrep *F, __nv_bfloat16 *const *pre_sv,
+                          Gemm2Args &g2) {
+    int rc;
+    smlm_pool p0 = pools[0];
+    memset(&g2, 0, sizeof(g2));
+    int nt0 = 0;
+    for (int i = 0; i < n_proj; ++i) {
+        smlm_pool pi = pools[i];
+        Gemm2Proj &P = g2.proj[i];
+        if ((rc = make_map_cached(p0, &P.tmA, X, p0->in, b->S, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B))) return rc;
+        P.K = p0->in;
+        if ((rc = make_map_cached(p0, &P.tmW, W[i], pi->in, pi->out, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B))) return rc;
+        const uint32_t rp = (uint32_t)pi->r_pad;
+        if (F[i].n_blocks) {
+            if ((rc = make_map(&P.tmU, F[i].vbd, rp, (uint64_t)F[i].n_blocks * 128, rp, 128, swizzle_for(rp * 2))))
+                return rc;
+            P.has_u = 1;
+            P.u_rows = F[i].n_blocks * 128;
+        }
+        if (F[i].n_pre_items) {
+            if ((rc = make_map(&P.tmV, pre_sv[i], rp, (uint64_t)F[i].n_long * 128, rp, 128, swizzle_for(rp * 2))))
+                return rc;
+            P.has_v = 1;
+            P.v_rows = F[i].n_long * 128;
+        }
+        P.slots = pi->d_slots;
+        P.Y = Y[i];
+        P.N = pi->out;
+        P.nt0 = nt0;
+        nt0 += (pi->out + kBN - 1) / kBN;
+    }
+    g2.pairs = F[0].pairs_dev;
+    g2.blocks = F[0].blocks_dev;
+    g2.n_proj = n_proj;
+    g2.n_pairs = F[0].n_pairs;
+    g2.n_nt = nt0;
+    g2.group_m = (raster_group(p0->in) + 1) / 2;
+    g2.r = p0->r;
+    g2.r_pad = p0->r_pad;
+    g2.stages = gemm2_stages(p0->r_pad);
+    return SMLM_OK;
+}
+
 }  // namespace
 
 // ==========================================================================================
@@ -1086,162 +1244,54 @@ int smlm_forward(smlm_pool p, const smlm_batch *b, const void *X, const void *W,
     }
 
     // ---------------- bf16 tensor-core path ----------------
-    const bool has_w = W != nullptr;
-    std::vector<DevTile> tiles;
-    tiles.reserve(plan.long_tiles.size() + plan.short_tiles.size());
-    for (auto &t : plan.long_tiles)
-        if (has_w || (t.flags & kTileLora)) tiles.push_back(t);
-    for (auto &t : plan.short_tiles)
-        if (has_w || t.nblk > 0) tiles.push_back(t);
-    // pairs of long tiles (same segment) for the CTA-pair kernel
-    int n_long_kept = 0;
-    for (auto &t : tiles)
-        if (!(t.flags & kTileShort)) ++n_long_kept;
-    std::vector<DevPair> pairs;
-    std::vector<int> pre_items;   // long tiles with an adapter (pre-shrink work items)
-    const bool pre = has_w && use_preshrink(p) && L.pre_items > 0;
-    if (pre)
-        for (int i = 0; i < n_long_kept; ++i)
-            if (tiles[i].slot >= 0) pre_items.push_back(i);
-    if (has_w && p->cta_pair) {
-        for (int i = 0; i < n_long_kept;) {
-            const DevTile &t0 = tiles[i];
-            DevPair pr{};
-            pr.row0 = t0.row0;
-            pr.slot = t0.slot;
-            pr.flags = (t0.flags & kTileFT) ? kPairFT : 0;
-            pr.scale = t0.scale;
-            pr.tile = i;
-            int rows = t0.rows;
-            if (i + 1 < n_long_kept && tiles[i + 1].seg == t0.seg) {
-                rows = 128 + tiles[i + 1].rows;
-                i += 2;
-            } else {
-                i += 1;
-            }
-            pr.rows = rows;
-            pairs.push_back(pr);
+    FwdPrep F;
+    if ((rc = fwd_prepare(p, b, plan, L, X, W, V_save, wsb, uctr, st, F))) return rc;
+    if (F.n_tiles == 0) return SMLM_OK;
+    if (F.pairs_dev) {
+        __nv_bfloat16 *pre_sv = t_ext_pre_sv ? reinterpret_cast<__nv_bfloat16 *>(const_cast<void *>(t_ext_pre_sv))
+                                             : reinterpret_cast<__nv_bfloat16 *>(wsb + L.pre_sv_off);
+        if (F.n_pre_items && !t_ext_pre_sv) {
+            // s*V = s X A_a^T once per long tile (split-K tensor-core contraction) -> tile-compact
+            // bf16 + V_save; the CTA-pair GEMM then streams full 256-column W tiles
+            ProfScope ps(2, st);
+            UArgs u;
+            memset(&u, 0, sizeof(u));
+            if ((rc = make_map(&u.tmDY, X, p->in, b->S, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B))) return rc;
+            u.slots = p->d_slots;
+            u.tiles = F.tiles_dev;
+            u.items = F.pre_items_dev;
+            u.n_items = F.n_pre_items;
+            u.ksplit = L.pre_ksplit;
+            u.K = p->in;
+            u.r_pad = p->r_pad;
+            u.part = reinterpret_cast<float *>(wsb + L.pre_part_off);
+            u.sUt = pre_sv;
+            u.vf = 1;
+            u.r = p->r;
+            u.Vsave = V_save;
+            u.ctr = u.n_items <= kUCtrMax ? uctr : nullptr;
+            CKL(launch_u(u, p->num_sms, st), u.ctr ? 1 : 2);
         }
-        // short tiles ride in the same launch: one per pair, CTA 1 a masked dummy
-        for (size_t i = n_long_kept; i < tiles.size(); ++i) {
-            const DevTile &t = tiles[i];
-            DevPair pr{};
-            pr.row0 = t.row0;
-            pr.rows = t.rows;
-            pr.slot = -1;
-            pr.flags = kPairShort;
-            pr.blk0 = t.blk0;
-            pr.nblk = t.nblk;
-            pairs.push_back(pr);
-        }
-    }
-    std::vector<uint8_t> bytes;
-    append(bytes, tiles);
-    const size_t blk_off = bytes.size();
-    append(bytes, plan.blocks);
-    const size_t srow_off = bytes.size();
-    append(bytes, plan.short_rows);
-    while (bytes.size() % 16) bytes.push_back(0);
-    const size_t pair_off = bytes.size();
-    append(bytes, pairs);
-    const size_t pre_off = bytes.size();
-    append(bytes, pre_items);
-    const DevTile *d_tiles = reinterpret_cast<const DevTile *>(wsb + L.plan_off);
-    const DevBlock *d_blocks = reinterpret_cast<const DevBlock *>(wsb + L.plan_off + blk_off);
-    const DevShortRow *d_srows = reinterpret_cast<const DevShortRow *>(wsb + L.plan_off + srow_off);
-    __nv_bfloat16 *Vbd = reinterpret_cast<__nv_bfloat16 *>(wsb + L.vbd_off);
-
-    if ((rc = stage_upload(p, bytes, wsb + L.plan_off, st))) return rc;
-    if (!plan.blocks.empty()) {
-        ProfScope ps(2, st);
-        if (L.spart_bytes) {
-            // the last chunk of each block combines it in-kernel (pool counters, self-resetting)
-            int *sctr = (int)plan.blocks.size() <= kUCtrMax ? uctr : nullptr;
-            CKL(launch_shrink_split((const __nv_bfloat16 *)X, p->d_slots, d_blocks, d_srows, (int)plan.blocks.size(),
-                                    p->in, p->r, p->r_pad, reinterpret_cast<float *>(wsb + L.spart_off), Vbd,
-                                    (__nv_bfloat16 *)V_save, sctr, st), sctr ? 1 : 2);
-        } else {
-            CKL(launch_shrink_short((const __nv_bfloat16 *)X, p->d_slots, d_blocks, d_srows,
-                                    (int)plan.blocks.size(), p->in, p->r, p->r_pad, Vbd, (__nv_bfloat16 *)V_save,
-                                    st), 1);
-        }
-    }
-    if (tiles.empty()) return SMLM_OK;
-    __nv_bfloat16 *pre_sv = t_ext_pre_sv ? reinterpret_cast<__nv_bfloat16 *>(const_cast<void *>(t_ext_pre_sv))
-                                         : reinterpret_cast<__nv_bfloat16 *>(wsb + L.pre_sv_off);
-    if (pre && !pre_items.empty() && !t_ext_pre_sv) {
-        // s*V = s X A_a^T once per long tile (split-K tensor-core contraction) -> tile-compact
-        // bf16 + V_save; the CTA-pair GEMM then streams full 256-column W tiles
-        ProfScope ps(2, st);
-        UArgs u;
-        memset(&u, 0, sizeof(u));
-        if ((rc = make_map(&u.tmDY, X, p->in, b->S, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B))) return rc;
-        u.slots = p->d_slots;
-        u.tiles = d_tiles;
-        u.items = reinterpret_cast<const int *>(wsb + L.plan_off + pre_off);
-        u.n_items = (int)pre_items.size();
-        u.ksplit = L.pre_ksplit;
-        u.K = p->in;
-        u.r_pad = p->r_pad;
-        u.part = reinterpret_cast<float *>(wsb + L.pre_part_off);
-        u.sUt = pre_sv;
-        u.vf = 1;
-        u.r = p->r;
-        u.Vsave = V_save;
-        u.ctr = u.n_items <= kUCtrMax ? uctr : nullptr;
-        CKL(launch_u(u, p->num_sms, st), u.ctr ? 1 : 2);
-    }
-    const int bnw = pre ? kBN : kBN - p->r_pad;
-    // long tiles on CTA pairs: consecutive tiles of one segment (same adapter) share one M=256 MMA
-    int first_1cta = 0;  // tiles[first_1cta ..] go to the 1-CTA kernel
-    if (has_w && p->cta_pair && !pairs.empty()) {
         Gemm2Args g2;
-        memset(&g2, 0, sizeof(g2));
-        if ((rc = make_map(&g2.tmX, X, p->in, b->S, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B))) return rc;
-        if ((rc = make_map(&g2.tmW0, W, p->in, p->out, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B))) return rc;
-        if (!pre && (rc = make_map(&g2.tmW1, W, p->in, p->out, 64, bnw - 128, CU_TENSOR_MAP_SWIZZLE_128B))) return rc;
-        if (pre) {
-            if ((rc = make_map(&g2.tmV, pre_sv, p->r_pad, (uint64_t)n_long_kept * 128, p->r_pad, 128,
-                               swizzle_for(p->r_pad * 2))))
-                return rc;
-            g2.pre = 1;
-        }
-        if (!plan.blocks.empty()) {
-            if ((rc = make_map(&g2.tmU, Vbd, p->r_pad, plan.blocks.size() * 128, p->r_pad, 128,
-                               swizzle_for(p->r_pad * 2))))
-                return rc;
-            g2.has_u = 1;
-        }
-        g2.blocks = d_blocks;
-        g2.defer = 1;
-        g2.slots = p->d_slots;
-        g2.pairs = reinterpret_cast<const DevPair *>(wsb + L.plan_off + pair_off);
-        g2.n_pairs = (int)pairs.size();
-        g2.n_ntiles = (p->out + bnw - 1) / bnw;
-        g2.group_m = (raster_group(p->in) + 1) / 2;
-        g2.K = p->in;
-        g2.N = p->out;
-        g2.r = p->r;
-        g2.r_pad = p->r_pad;
-        g2.stages = gemm2_stages(p->r_pad);
-        g2.Y = Y;
-        g2.Vsave = V_save;
+        if ((rc = gemm2_fwd_args(1, &p, b, X, &W, &Y, &F, &pre_sv, g2))) return rc;
         ProfScope ps(0, st);
         CKL(launch_gemm2(g2, false, p->num_sms, st), 1);
-        first_1cta = (int)tiles.size();
+        return SMLM_OK;
     }
-    if ((int)tiles.size() == first_1cta) return SMLM_OK;
+    // one CTA per tile (SMLM_OPT_CTA_PAIR = 0, or W == NULL: Y holds the base output, LoRA term added)
+    const bool has_w = W != nullptr;
+    const int bnw = kBN - p->r_pad;
     GemmArgs a;
     memset(&a, 0, sizeof(a));
     if ((rc = make_map(&a.tmA, X, p->in, b->S, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B))) return rc;
     if (has_w && (rc = make_map(&a.tmB, W, p->in, p->out, 64, bnw, CU_TENSOR_MAP_SWIZZLE_128B))) return rc;
     if (!plan.blocks.empty() &&
-        (rc = make_map(&a.tmV, Vbd, p->r_pad, plan.blocks.size() * 128, p->r_pad, 128, swizzle_for(p->r_pad * 2))))
+        (rc = make_map(&a.tmV, F.vbd, p->r_pad, plan.blocks.size() * 128, p->r_pad, 128, swizzle_for(p->r_pad * 2))))
         return rc;
     a.slots = p->d_slots;
-    a.tiles = d_tiles + first_1cta;
-    a.blocks = d_blocks;
-    a.n_tiles = (int)tiles.size() - first_1cta;
+    a.tiles = F.tiles_dev;
+    a.blocks = F.blocks_dev;
+    a.n_tiles = F.n_tiles;
     a.K = p->in;
     a.N = p->out;
     a.n_ntiles = (p->out + bnw - 1) / bnw;
@@ -1290,7 +1340,9 @@ static int multi_check(int n_proj, const smlm_pool *pools, const smlm_batch *b, 
 // stacked as the N of one tcgen05 contraction), then each projection's GEMM with its s*V.
 struct MultiPre {
     bool ok = false;
-    size_t base = 0;                      // per-projection forward workspace (max over pools), reused
+    bool merged = false;                  // all projections' GEMMs in ONE CTA-pair launch
+    size_t base = 0;                      // per-projection forward workspace (max over pools)
+    size_t base_off[kDec3MaxProj] = {};   // merged: one per projection (short-tile s*V live together)
     size_t sv_off[kDec3MaxProj] = {}, sv_bytes = 0;
     size_t part_off = 0, plan_off = 0, total = 0;
     int items = 0, ksplit = 1;
@@ -1308,7 +1360,12 @@ static MultiPre multi_pre_layout(int n_proj, const smlm_pool *pools, const smlm_
         if (t.slot >= 0) ++M.items;
     if (M.items == 0) return M;
     for (int i = 0; i < n_proj; ++i) M.base = std::max(M.base, smlm_workspace_size(pools[i], b, 0));
-    size_t off = align256(M.base);
+    M.merged = n_proj <= kGemm2MaxProj;
+    size_t off = 0;
+    for (int i = 0; i < (M.merged ? n_proj : 1); ++i) {
+        M.base_off[i] = off;
+        off = align256(off + M.base);
+    }
     M.sv_bytes = plan.long_tiles.size() * 128 * (size_t)p0->r_pad * 2;
     for (int i = 0; i < n_proj; ++i) {
         M.sv_off[i] = off;
@@ -1400,17 +1457,171 @@ int smlm_forward_multi(int n_proj, const smlm_pool *pools, const smlm_batch *b, 
             ProfScope ps(2, st);
             CKL(launch_u(u, p0->num_sms, st), u.ctr ? 1 : 2);
         }
-        for (int i = 0; i < n_proj; ++i) {
-            t_ext_pre_sv = wsb + M.sv_off[i];
-            rc = smlm_forward(pools[i], b, X, W[i], Y[i], V_save ? V_save[i] : nullptr, ws, M.base, stream);
-            t_ext_pre_sv = nullptr;
-            if (rc) return rc;
+        if (!M.merged) {
+            for (int i = 0; i < n_proj; ++i) {
+                t_ext_pre_sv = wsb + M.sv_off[i];
+                rc = smlm_forward(pools[i], b, X, W[i], Y[i], V_save ? V_save[i] : nullptr, ws, M.base, stream);
+                t_ext_pre_sv = nullptr;
+                if (rc) return rc;
+            }
+            return SMLM_OK;
         }
+        // every projection's plan upload + short-row shrink in its own sub-workspace, then ONE
+        // CTA-pair GEMM launch over the n-tiles of all projections (no per-projection wave tail)
+        FwdPrep F[kGemm2MaxProj];
+        __nv_bfloat16 *pre_sv[kGemm2MaxProj];
+        for (int i = 0; i < n_proj; ++i) {
+            const WsLayout Li = layout_for(pools[i], b, plan, false, false);
+            if ((rc = fwd_prepare(pools[i], b, plan, Li, X, W[i], V_save ? V_save[i] : nullptr, wsb + M.base_off[i],
+                                  uctr, st, F[i])))
+                return rc;
+            pre_sv[i] = reinterpret_cast<__nv_bfloat16 *>(wsb + M.sv_off[i]);
+        }
+        if (F[0].n_tiles == 0) return SMLM_OK;
+        Gemm2Args g2;
+        if ((rc = gemm2_fwd_args(n_proj, pools, b, X, W, Y, F, pre_sv, g2))) return rc;
+        ProfScope ps(0, st);
+        CKL(launch_gemm2(g2, false, p0->num_sms, st), 1);
         return SMLM_OK;
     }
     for (int i = 0; i < n_proj; ++i)
         if ((rc = smlm_forward(pools[i], b, X, W[i], Y[i], V_save ? V_save[i] : nullptr, ws, ws_bytes, stream)))
             return rc;
+    return SMLM_OK;
+}
+
+// ---- backward phases (bf16 path; also the plan upload of the fp32 path) ----
+struct BwdPrep {
+    int nt = 0, n_pairs = 0, n_grad = 0, u_items = 0;
+    const DevTile *tiles = nullptr;
+    const void *groups = nullptr;
+    const DevPair *pairs = nullptr;
+    __nv_bfloat16 *sUt = nullptr, *sVt = nullptr;
+    float *Uf = nullptr, *Vf = nullptr;
+};
+
+// grad groups + tiles + U items + CTA pairs -> workspace; bf16: the U pass (s*U, and s*V of the
+// tile-compact dA/dB operand from V_save)
+static int bwd_prepare(smlm_pool p, const smlm_batch *b, const Plan &plan, const WsLayout &L, const void *dY,
+                       const void *V_save, bool want_dx, uint8_t *wsb, int *uctr, cudaStream_t st, BwdPrep &B) {
+    int rc;
+    // grad groups with the current grad bindings (masking: NULL => no dA/dB for that slot)
+    std::vector<uint8_t> gbytes(plan.groups.size() * grad_group_bytes());
+    int n_grad = 0;
+    for (auto &g : plan.groups) {
+        const SlotHost &h = p->slots[g.slot];
+        if (!h.dA && !h.dB) continue;
+        fill_grad_group(gbytes.data() + n_grad * grad_group_bytes(), g.slot, g.tile_begin, g.n_tiles, h.r, h.dA, h.dB);
+        ++n_grad;
+    }
+    gbytes.resize(n_grad * grad_group_bytes());
+    std::vector<int> uitems;
+    for (size_t i = 0; i < plan.bwd_tiles.size(); ++i)
+        if (plan.bwd_tiles[i].slot >= 0) uitems.push_back((int)i);
+    // CTA pairs of consecutive fine-tune tiles (the dX GEMM on cta_group::2; any two tiles: a pair
+    // of different adapters takes one expand block per adapter)
+    std::vector<DevPair> bpairs;
+    make_pairs(plan.bwd_tiles, bpairs);
+    std::vector<uint8_t> bytes;
+    append(bytes, plan.bwd_tiles);
+    const size_t grp_off = bytes.size();
+    bytes.insert(bytes.end(), gbytes.begin(), gbytes.end());
+    const size_t uit_off = bytes.size();
+    append(bytes, uitems);
+    while (bytes.size() % 16) bytes.push_back(0);
+    const size_t bpair_off = bytes.size();
+    append(bytes, bpairs);
+    if ((rc = stage_upload(p, bytes, wsb + L.plan_off, st))) return rc;
+    B.tiles = reinterpret_cast<const DevTile *>(wsb + L.plan_off);
+    B.groups = wsb + L.plan_off + grp_off;
+    B.pairs = reinterpret_cast<const DevPair *>(wsb + L.plan_off + bpair_off);
+    B.n_pairs = (int)bpairs.size();
+    B.nt = (int)plan.bwd_tiles.size();
+    B.n_grad = n_grad;
+    B.u_items = L.u_items;
+    B.Uf = reinterpret_cast<float *>(wsb + L.u_off);
+    B.Vf = reinterpret_cast<float *>(wsb + L.vf_off);
+    B.sUt = reinterpret_cast<__nv_bfloat16 *>(wsb + L.sut_off);
+    B.sVt = reinterpret_cast<__nv_bfloat16 *>(wsb + L.svt_off);
+    if (p->dtype != SMLM_BF16) return SMLM_OK;
+    // U = dY B_a per fine-tune tile (split-K tensor-core pass) -> tile-compact s*U
+    if (L.u_items && (want_dx || n_grad)) {
+        UArgs u;
+        memset(&u, 0, sizeof(u));
+        if ((rc = make_map(&u.tmDY, dY, p->out, b->S, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B))) return rc;
+        u.slots = p->d_slots;
+        u.tiles = B.tiles;
+        u.items = reinterpret_cast<const int *>(wsb + L.plan_off + uit_off);
+        u.n_items = L.u_items;
+        u.ksplit = L.u_ksplit;
+        u.K = p->out;
+        u.r_pad = p->r_pad;
+        u.part = reinterpret_cast<float *>(wsb + L.upart_off);
+        u.sUt = B.sUt;
+        if (V_save && n_grad) {   // s*V folded into the reduce
+            u.Vsave_in = V_save;
+            u.sVt = B.sVt;
+            u.r = p->r;
+        }
+        u.ctr = u.n_items <= kUCtrMax ? uctr : nullptr;
+        CKL(launch_u(u, p->num_sms, st), u.ctr ? 1 : 2);
+    }
+    return SMLM_OK;
+}
+
+// the dX GEMM operands of one projection in a CTA-pair launch
+static int bwd_gemm2_proj(smlm_pool p, const smlm_batch *b, const void *W, const void *dY, void *dX, const BwdPrep &B,
+                          int nt0, Gemm2Proj &P) {
+    int rc;
+    if ((rc = make_map(&P.tmA, dY, p->out, b->S, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B))) return rc;
+    if ((rc = make_map(&P.tmW, W, p->in, p->out, 64, 64, CU_TENSOR_MAP_SWIZZLE_128B))) return rc;
+    if (B.u_items) {
+        if ((rc = make_map(&P.tmU, B.sUt, p->r_pad, (uint64_t)B.nt * 128, p->r_pad, 128, swizzle_for(p->r_pad * 2))))
+            return rc;
+        P.has_u = 1;
+        P.u_rows = B.nt * 128;
+    }
+    P.slots = p->d_slots;
+    P.Y = dX;
+    P.N = p->in;
+    P.K = p->out;
+    P.nt0 = nt0;
+    return SMLM_OK;
+}
+
+// dA/dB: the token contraction over the fine-tune tiles, per adapter in canonical order
+static int bwd_tok(smlm_pool p, const smlm_batch *b, const void *X, const void *dY, const void *V_save,
+                   int accumulate, const BwdPrep &B, cudaStream_t st) {
+    int rc;
+    if (!B.n_grad) return SMLM_OK;
+    ProfScope ps(3, st);
+    if (V_save) {
+        if (!B.u_items)   // otherwise folded into the U pass
+            CKL(launch_prep_sv<__nv_bfloat16>(B.tiles, B.nt, (const __nv_bfloat16 *)V_save, p->r, p->r_pad, B.sVt, st), 1);
+    } else {
+        CKL(launch_rows_shrink<__nv_bfloat16>(B.tiles, B.nt, p->d_slots, (const __nv_bfloat16 *)X, p->in, p->r, B.Vf,
+                                              nullptr, 0, st), 1);
+        CKL(launch_prep_sv<float>(B.tiles, B.nt, B.Vf, p->r, p->r_pad, B.sVt, st), 1);
+    }
+    TokArgs ta;
+    memset(&ta, 0, sizeof(ta));
+    const int rb = p->r_pad * 2;
+    if ((rc = make_map(&ta.tmX, X, p->in, b->S, 64, 64, CU_TENSOR_MAP_SWIZZLE_128B))) return rc;
+    if ((rc = make_map(&ta.tmDY, dY, p->out, b->S, 64, 64, CU_TENSOR_MAP_SWIZZLE_128B))) return rc;
+    if ((rc = make_map(&ta.tmSU, B.sUt, p->r_pad, (uint64_t)B.nt * 128, p->r_pad, 64, swizzle_for(rb)))) return rc;
+    if ((rc = make_map(&ta.tmSV, B.sVt, p->r_pad, (uint64_t)B.nt * 128, p->r_pad, 64, swizzle_for(rb)))) return rc;
+    ta.tiles = B.tiles;
+    ta.groups = reinterpret_cast<const GradGroup *>(B.groups);
+    ta.n_groups = B.n_grad;
+    ta.in_f = p->in;
+    ta.out_f = p->out;
+    ta.r = p->r;
+    ta.r_pad = p->r_pad;
+    ta.nh = 2;   // 256-column items (two M=128 accumulators sharing the B operand)
+    ta.mt_a = (p->in + 128 * ta.nh - 1) / (128 * ta.nh);
+    ta.mt_b = (p->out + 128 * ta.nh - 1) / (128 * ta.nh);
+    ta.accumulate = accumulate ? 1 : 0;
+    CKL(launch_tok(ta, p->num_sms, st), 1);
     return SMLM_OK;
 }
 
@@ -1431,138 +1642,56 @@ int smlm_backward(smlm_pool p, const smlm_batch *b, const void *X, const void *W
     uint8_t *wsb = reinterpret_cast<uint8_t *>(ws);
     int *uctr = nullptr;
     if ((rc = stream_counters(p, st, nullptr, &uctr))) return rc;
-
-    // grad groups with the current grad bindings (masking: NULL => no dA/dB for that slot)
-    std::vector<uint8_t> gbytes(plan.groups.size() * grad_group_bytes());
-    int n_grad = 0;
-    for (auto &g : plan.groups) {
-        const SlotHost &h = p->slots[g.slot];
-        if (!h.dA && !h.dB) continue;
-        fill_grad_group(gbytes.data() + n_grad * grad_group_bytes(), g.slot, g.tile_begin, g.n_tiles, h.r, h.dA, h.dB);
-        ++n_grad;
-    }
-    gbytes.resize(n_grad * grad_group_bytes());
-    std::vector<int> uitems;
-    for (size_t i = 0; i < plan.bwd_tiles.size(); ++i)
-        if (plan.bwd_tiles[i].slot >= 0) uitems.push_back((int)i);
-    // CTA pairs of consecutive fine-tune tiles of one segment (the dX GEMM on cta_group::2)
-    std::vector<DevPair> bpairs;
-    for (size_t i = 0; i < plan.bwd_tiles.size();) {
-        const DevTile &t0 = plan.bwd_tiles[i];
-        DevPair pr{};
-        pr.row0 = t0.row0;
-        pr.slot = t0.slot;
-        pr.flags = kPairFT;
-        pr.scale = t0.scale;
-        pr.tile = (int)i;
-        if (i + 1 < plan.bwd_tiles.size() && plan.bwd_tiles[i + 1].seg == t0.seg) {
-            pr.rows = 128 + plan.bwd_tiles[i + 1].rows;
-            i += 2;
-        } else {
-            pr.rows = t0.rows;
-            i += 1;
-        }
-        bpairs.push_back(pr);
-    }
-    std::vector<uint8_t> bytes;
-    append(bytes, plan.bwd_tiles);
-    const size_t grp_off = bytes.size();
-    bytes.insert(bytes.end(), gbytes.begin(), gbytes.end());
-    const size_t uit_off = bytes.size();
-    append(bytes, uitems);
-    while (bytes.size() % 16) bytes.push_back(0);
-    const size_t bpair_off = bytes.size();
-    append(bytes, bpairs);
-    if ((rc = stage_upload(p, bytes, wsb + L.plan_off, st))) return rc;
-    const DevTile *d_tiles = reinterpret_cast<const DevTile *>(wsb + L.plan_off);
-    const void *d_groups = wsb + L.plan_off + grp_off;
-    const int *d_uitems = reinterpret_cast<const int *>(wsb + L.plan_off + uit_off);
-    const DevPair *d_pairs = reinterpret_cast<const DevPair *>(wsb + L.plan_off + bpair_off);
-    const int n_pairs = (int)bpairs.size();
-    const int nt = (int)plan.bwd_tiles.size();
-    float *Uf = reinterpret_cast<float *>(wsb + L.u_off);
-    float *Vf = reinterpret_cast<float *>(wsb + L.vf_off);
+    BwdPrep B;
+    if ((rc = bwd_prepare(p, b, plan, L, dY, V_save, dX != nullptr, wsb, uctr, st, B))) return rc;
 
     if (p->dtype == SMLM_FP32) {
-        CKL(launch_rows_u<float>(d_tiles, nt, p->d_slots, (const float *)dY, p->out, p->r, Uf, nullptr, p->r_pad,
+        CKL(launch_rows_u<float>(B.tiles, B.nt, p->d_slots, (const float *)dY, p->out, p->r, B.Uf, nullptr, p->r_pad,
                                  st), 1);
         if (dX)
-            CKL(launch_f32_dx(d_tiles, nt, p->d_slots, (const float *)dY, (const float *)W, (float *)dX, Uf, p->in,
+            CKL(launch_f32_dx(B.tiles, B.nt, p->d_slots, (const float *)dY, (const float *)W, (float *)dX, B.Uf, p->in,
                               p->out, p->r, st), 1);
-        if (n_grad) {
+        if (B.n_grad) {
             const float *V = (const float *)V_save;
             if (!V) {
-                CKL(launch_rows_shrink<float>(d_tiles, nt, p->d_slots, (const float *)X, p->in, p->r, Vf, nullptr,
+                CKL(launch_rows_shrink<float>(B.tiles, B.nt, p->d_slots, (const float *)X, p->in, p->r, B.Vf, nullptr,
                                               0, st), 1);
-                V = Vf;
+                V = B.Vf;
             }
-            CKL((launch_dadb<float, float>(d_tiles, d_groups, n_grad, (const float *)X, (const float *)dY, Uf, V,
+            CKL((launch_dadb<float, float>(B.tiles, B.groups, B.n_grad, (const float *)X, (const float *)dY, B.Uf, V,
                                            p->in, p->out, p->r, accumulate, st)), 2);
         }
         return SMLM_OK;
     }
 
     // ---------------- bf16 path ----------------
-    __nv_bfloat16 *sUt = reinterpret_cast<__nv_bfloat16 *>(wsb + L.sut_off);
-    __nv_bfloat16 *sVt = reinterpret_cast<__nv_bfloat16 *>(wsb + L.svt_off);
-    // U = dY B_a per fine-tune tile (split-K tensor-core pass) -> tile-compact s*U
-    if (L.u_items && (dX || n_grad)) {
-        UArgs u;
-        memset(&u, 0, sizeof(u));
-        if ((rc = make_map(&u.tmDY, dY, p->out, b->S, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B))) return rc;
-        u.slots = p->d_slots;
-        u.tiles = d_tiles;
-        u.items = d_uitems;
-        u.n_items = L.u_items;
-        u.ksplit = L.u_ksplit;
-        u.K = p->out;
-        u.r_pad = p->r_pad;
-        u.part = reinterpret_cast<float *>(wsb + L.upart_off);
-        u.sUt = sUt;
-        if (V_save && n_grad) {   // s*V folded into the reduce
-            u.Vsave_in = V_save;
-            u.sVt = sVt;
-            u.r = p->r;
-        }
-        u.ctr = u.n_items <= kUCtrMax ? uctr : nullptr;
-        CKL(launch_u(u, p->num_sms, st), u.ctr ? 1 : 2);
-    }
     if (dX) {
         ProfScope ps(1, st);
         if (p->cta_pair) {
             Gemm2Args g2;
             memset(&g2, 0, sizeof(g2));
-            if ((rc = make_map(&g2.tmX, dY, p->out, b->S, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B))) return rc;
-            if ((rc = make_map(&g2.tmW0, W, p->in, p->out, 64, 64, CU_TENSOR_MAP_SWIZZLE_128B))) return rc;
-            if (L.u_items &&
-                (rc = make_map(&g2.tmU, sUt, p->r_pad, (uint64_t)nt * 128, p->r_pad, 128, swizzle_for(p->r_pad * 2))))
-                return rc;
-            g2.has_u = L.u_items > 0;
-            g2.slots = p->d_slots;
-            g2.pairs = d_pairs;
-            g2.n_pairs = n_pairs;
-            g2.n_ntiles = (p->in + kBN - 1) / kBN;
+            if ((rc = bwd_gemm2_proj(p, b, W, dY, dX, B, 0, g2.proj[0]))) return rc;
+            g2.pairs = B.pairs;
+            g2.n_proj = 1;
+            g2.n_pairs = B.n_pairs;
+            g2.n_nt = (p->in + kBN - 1) / kBN;
             g2.group_m = (raster_group(p->out) + 1) / 2;
-            g2.K = p->out;
-            g2.N = p->in;
             g2.r = p->r;
             g2.r_pad = p->r_pad;
             g2.stages = gemm2_stages(p->r_pad);
-            g2.Y = dX;
-            g2.Vsave = nullptr;
             CKL(launch_gemm2(g2, true, p->num_sms, st), 1);
         } else {
             GemmArgs a;
             memset(&a, 0, sizeof(a));
             if ((rc = make_map(&a.tmA, dY, p->out, b->S, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B))) return rc;
             if ((rc = make_map(&a.tmB, W, p->in, p->out, 64, 64, CU_TENSOR_MAP_SWIZZLE_128B))) return rc;
-            if (L.u_items &&
-                (rc = make_map(&a.tmV, sUt, p->r_pad, (uint64_t)nt * 128, p->r_pad, 128, swizzle_for(p->r_pad * 2))))
+            if (B.u_items && (rc = make_map(&a.tmV, B.sUt, p->r_pad, (uint64_t)B.nt * 128, p->r_pad, 128,
+                                            swizzle_for(p->r_pad * 2))))
                 return rc;
             a.slots = p->d_slots;
-            a.tiles = d_tiles;
+            a.tiles = B.tiles;
             a.blocks = nullptr;
-            a.n_tiles = nt;
+            a.n_tiles = B.nt;
             a.K = p->out;
             a.N = p->in;
             a.n_ntiles = (p->in + kBN - 1) / kBN;
@@ -1578,37 +1707,97 @@ int smlm_backward(smlm_pool p, const smlm_batch *b, const void *X, const void *W
             CKL(launch_gemm(a, true, p->num_sms, st), 1);
         }
     }
-    if (n_grad) {
-        ProfScope ps(3, st);
-        if (V_save) {
-            const bool folded = L.u_items > 0;   // done by the U pass
-            if (!folded)
-                CKL(launch_prep_sv<__nv_bfloat16>(d_tiles, nt, (const __nv_bfloat16 *)V_save, p->r, p->r_pad, sVt, st), 1);
-        } else {
-            CKL(launch_rows_shrink<__nv_bfloat16>(d_tiles, nt, p->d_slots, (const __nv_bfloat16 *)X, p->in, p->r, Vf,
-                                                  nullptr, 0, st), 1);
-            CKL(launch_prep_sv<float>(d_tiles, nt, Vf, p->r, p->r_pad, sVt, st), 1);
-        }
-        TokArgs ta;
-        memset(&ta, 0, sizeof(ta));
-        const int rb = p->r_pad * 2;
-        if ((rc = make_map(&ta.tmX, X, p->in, b->S, 64, 64, CU_TENSOR_MAP_SWIZZLE_128B))) return rc;
-        if ((rc = make_map(&ta.tmDY, dY, p->out, b->S, 64, 64, CU_TENSOR_MAP_SWIZZLE_128B))) return rc;
-        if ((rc = make_map(&ta.tmSU, sUt, p->r_pad, (uint64_t)nt * 128, p->r_pad, 64, swizzle_for(rb)))) return rc;
-        if ((rc = make_map(&ta.tmSV, sVt, p->r_pad, (uint64_t)nt * 128, p->r_pad, 64, swizzle_for(rb)))) return rc;
-        ta.tiles = d_tiles;
-        ta.groups = reinterpret_cast<const GradGroup *>(d_groups);
-        ta.n_groups = n_grad;
-        ta.in_f = p->in;
-        ta.out_f = p->out;
-        ta.r = p->r;
-        ta.r_pad = p->r_pad;
-        ta.nh = 2;   // 256-column items (two M=128 accumulators sharing the B operand)
-        ta.mt_a = (p->in + 128 * ta.nh - 1) / (128 * ta.nh);
-        ta.mt_b = (p->out + 128 * ta.nh - 1) / (128 * ta.nh);
-        ta.accumulate = accumulate ? 1 : 0;
-        CKL(launch_tok(ta, p->num_sms, st), 1);
+    return bwd_tok(p, b, X, dY, V_save, accumulate, B, st);
+}
+
+// ---- several projections that share X (q/k/v, gate/up): one dX GEMM launch ----
+static int multi_bwd_check(int n_proj, const smlm_pool *pools, const smlm_batch *b, Plan &plan) {
+    if (n_proj < 1 || n_proj > kGemm2MaxProj) return set_err(SMLM_E_INVALID, "n_proj must be in [1, 3]");
+    if (!pools || !b) return set_err(SMLM_E_INVALID, "NULL pools/batch");
+    for (int i = 0; i < n_proj; ++i) {
+        if (!pools[i]) return set_err(SMLM_E_INVALID, "NULL pool");
+        if (pools[i]->device != pools[0]->device || pools[i]->in != pools[0]->in || pools[i]->r != pools[0]->r ||
+            pools[i]->dtype != pools[0]->dtype || pools[i]->cta_pair != pools[0]->cta_pair ||
+            pools[i]->l_long != pools[0]->l_long)
+            return set_err(SMLM_E_SHAPE, "pools must share device, in_features, rank, dtype and options");
     }
+    for (int i = 0; i < n_proj; ++i) {
+        Plan pl;
+        int rc = plan_for(pools[i], b, true, i == 0 ? plan : pl);
+        if (rc) return rc;
+    }
+    return SMLM_OK;
+}
+
+static size_t bwd_ws_each(int n_proj, const smlm_pool *pools, const smlm_batch *b, const Plan &plan, bool need_vf) {
+    size_t m = 0;
+    for (int i = 0; i < n_proj; ++i)
+        m = std::max(m, layout_for(pools[i], b, plan, true, need_vf).total);
+    return align256(m);
+}
+
+size_t smlm_workspace_size_backward_multi(int n_proj, const smlm_pool *pools, const smlm_batch *b) {
+    Plan plan;
+    if (multi_bwd_check(n_proj, pools, b, plan) != SMLM_OK) return 0;
+    return (size_t)n_proj * bwd_ws_each(n_proj, pools, b, plan, true);
+}
+
+int smlm_backward_multi(int n_proj, const smlm_pool *pools, const smlm_batch *b, const void *X,
+                        const void *const *W, const void *const *dY, const void *const *V_save, void *const *dX,
+                        int accumulate, void *ws, size_t ws_bytes, void *stream) {
+    Plan plan;
+    int rc = multi_bwd_check(n_proj, pools, b, plan);
+    if (rc) return rc;
+    if (b->S == 0 || b->G == 0 || plan.bwd_tiles.empty()) return SMLM_OK;
+    if (!X || !dY || !W || !dX) return set_err(SMLM_E_INVALID, "X, W, dY and dX arrays must be non-NULL");
+    for (int i = 0; i < n_proj; ++i)
+        if (!dY[i] || !W[i] || !dX[i]) return set_err(SMLM_E_INVALID, "W[i], dY[i] and dX[i] must be non-NULL");
+    smlm_pool p0 = pools[0];
+    const size_t each = bwd_ws_each(n_proj, pools, b, plan, true);
+    if (!ws || ws_bytes < (size_t)n_proj * each) return set_err(SMLM_E_WORKSPACE, "workspace too small");
+    if (p0->dtype != SMLM_BF16 || !p0->cta_pair) {   // one call per projection (same math)
+        for (int i = 0; i < n_proj; ++i)
+            if ((rc = smlm_backward(pools[i], b, X, W[i], dY[i], V_save ? V_save[i] : nullptr, dX[i], accumulate,
+                                    reinterpret_cast<uint8_t *>(ws) + i * each, each, stream)))
+                return rc;
+        return SMLM_OK;
+    }
+    DeviceGuard dg(p0->device);
+    if ((rc = check_sticky())) return rc;
+    cudaStream_t st = (cudaStream_t)stream;
+    uint8_t *wsb = reinterpret_cast<uint8_t *>(ws);
+    int *uctr = nullptr;
+    if ((rc = stream_counters(p0, st, nullptr, &uctr))) return rc;
+    BwdPrep B[kGemm2MaxProj];
+    for (int i = 0; i < n_proj; ++i) {
+        const void *vs = V_save ? V_save[i] : nullptr;
+        Plan pl;
+        if ((rc = plan_for(pools[i], b, true, pl))) return rc;
+        const WsLayout L = layout_for(pools[i], b, pl, true, vs == nullptr);
+        if ((rc = bwd_prepare(pools[i], b, pl, L, dY[i], vs, true, wsb + i * each, uctr, st, B[i]))) return rc;
+    }
+    {
+        ProfScope ps(1, st);
+        Gemm2Args g2;
+        memset(&g2, 0, sizeof(g2));
+        int nt0 = 0, kmax = 0;
+        for (int i = 0; i < n_proj; ++i) {
+            if ((rc = bwd_gemm2_proj(pools[i], b, W[i], dY[i], dX[i], B[i], nt0, g2.proj[i]))) return rc;
+            nt0 += (pools[i]->in + kBN - 1) / kBN;
+            kmax = std::max(kmax, pools[i]->out);
+        }
+        g2.pairs = B[0].pairs;
+        g2.n_proj = n_proj;
+        g2.n_pairs = B[0].n_pairs;
+        g2.n_nt = nt0;
+        g2.group_m = (raster_group(kmax) + 1) / 2;
+        g2.r = p0->r;
+        g2.r_pad = p0->r_pad;
+        g2.stages = gemm2_stages(p0->r_pad);
+        CKL(launch_gemm2(g2, true, p0->num_sms, st), 1);
+    }
+    for (int i = 0; i < n_proj; ++i)
+        if ((rc = bwd_tok(pools[i], b, X, dY[i], V_save ? V_save[i] : nullptr, accumulate, B[i], st))) return rc;
     return SMLM_OK;
 }
 

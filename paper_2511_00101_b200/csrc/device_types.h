@@ -56,41 +56,52 @@ struct GemmArgs {
     int S;
 };
 
-// a pair of 128-row tiles of one segment processed by a CTA pair (cta_group::2)
-struct alignas(16) DevPair {
-    int row0;     // first row of the pair (CTA 0: [row0, row0+128), CTA 1: [row0+128, row0+256))
-    int rows;     // valid rows of the pair (<= 256; past a segment end rows are masked)
-    int slot;     // adapter or -1
-    int flags;    // bit 0: FINETUNE segment (V_save); bit 1: short tile (CTA 0 only, per-adapter blocks)
+// one 128-row tile of a CTA pair (cta_group::2): CTA `rank` stages rows [row0, row0 + 128)
+struct alignas(16) DevHalf {
+    int row0;     // first row (rows past `rows` are masked in the epilogue; TMA zero-fills past S)
+    int rows;     // valid rows (0: an empty half -- the pair has a single tile)
+    int slot;     // long tile: adapter or -1; short tile: -1 (adapters per block)
+    int flags;    // kPairFT: FINETUNE segment; kPairShort: short tile (adapter blocks blk0..blk0+nblk)
     float scale;
-    int tile;     // index of the pair's first tile in the tile list (bwd s*U rows / fwd pre-shrunk s*V rows)
-    int blk0;     // short pair: first adapter block of the tile
-    int nblk;     // short pair: number of adapter blocks
+    int tile;     // long: index in the tile list (row block of the tile-compact s*V / s*U operand)
+    int blk0;     // short: first adapter block (row block of the block-diagonal s*V operand)
+    int nblk;     // short: number of adapter blocks
+};
+// two consecutive tiles of the plan (same segment or not) on one CTA pair
+struct alignas(16) DevPair {
+    DevHalf h[2];
 };
 constexpr int kPairFT = 1, kPairShort = 2;
 
+// one projection of a CTA-pair GEMM launch (forward: up to kGemm2MaxProj projections sharing X)
+constexpr int kGemm2MaxProj = 3;
+struct alignas(64) Gemm2Proj {
+    CUtensorMap tmA;    // A operand rows: fwd X [S,in] (shared); bwd dY_p [S,out_p]; box {64,128} SW128
+    CUtensorMap tmW;    // fwd: W [out,in] box {64,128} (K-major, CTA rank's half of the n-tile);
+                        // bwd: W box {64,64} (MN-major)
+    CUtensorMap tmU;    // fwd: block-diagonal s*V of short tiles; bwd: tile-compact s*U; box {r_pad,128}
+    CUtensorMap tmV;    // fwd: tile-compact s*V of the long tiles (pre-shrink); box {r_pad,128}
+    const SlotDev *slots;   // this projection's pool slot table
+    void *Y;            // fwd: Y [S,N]; bwd: dX [S,N]
+    int N;              // output width (fwd out, bwd in)
+    int K;              // reduction length (fwd in, bwd out_p)
+    int nt0;            // first global n-tile of this projection
+    int u_rows, v_rows; // row extents of tmU / tmV (an A box at that row is all zeros)
+    int has_u, has_v;
+    int pad;
+};
+
 struct Gemm2Args {
-    CUtensorMap tmX;    // fwd: X [S,in] / bwd: dY [S,out]; box {64,128} SW128
-    CUtensorMap tmW0;   // fwd: W box {64,128} (CTA 0's half of B); bwd: W box {64,64} (MN-major)
-    CUtensorMap tmW1;   // fwd: W box {64,256-r_pad-128} (CTA 1's W rows; A_a stacked below)
-    CUtensorMap tmU;    // bwd: tile-compact s*U; fwd: block-diagonal s*V of short tiles; box {r_pad,128}
-    CUtensorMap tmV;    // fwd pre-shrunk (pre = 1): tile-compact s*V of the long tiles; box {r_pad,128}
-    const SlotDev *slots;
+    Gemm2Proj proj[kGemm2MaxProj];
     const DevPair *pairs;
-    const DevBlock *blocks;   // fwd short pairs
-    int has_u;                // tmU is valid
-    int pre;                  // forward: s*V precomputed (smlm_u_kernel vf) -> full 256-column W tiles
-    int defer;                // forward: defer each item's expand into the next item's main loop
+    const DevBlock *blocks;   // fwd short tiles' adapter blocks
+    int n_proj;
     int n_pairs;
-    int n_ntiles;
+    int n_nt;                 // n-tiles over all projections
     int group_m;
-    int K;
-    int N;
     int r;
     int r_pad;
     int stages;
-    void *Y;
-    void *Vsave;
 };
 
 // backward: one adapter with fine-tune rows and bound gradient buffers (PAPER.md P:422 masking)

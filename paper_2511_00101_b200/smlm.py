@@ -30,6 +30,7 @@ EXPORTED = [
     "smlm_backward", "smlm_plan", "smlm_plan_export", "smlm_status_string", "smlm_last_error",
     "smlm_launch_count", "smlm_profile_enable", "smlm_profile_read", "smlm_workspace_size_multi",
     "smlm_forward_multi", "smlm_adamw_workspace_size", "smlm_adamw_step", "smlm_adapter_register_rank",
+    "smlm_workspace_size_backward_multi", "smlm_backward_multi",
 ]
 
 
@@ -64,6 +65,8 @@ def _load():
         "smlm_workspace_size_multi": ([I, P, BP], Z),
         "smlm_forward_multi": ([I, P, BP, P, P, P, P, P, Z, P], I),
         "smlm_backward": ([P, BP, P, P, P, P, P, I, P, Z, P], I),
+        "smlm_workspace_size_backward_multi": ([I, P, BP], Z),
+        "smlm_backward_multi": ([I, P, BP, P, P, P, P, P, I, P, Z, P], I),
         "smlm_plan": ([BP, I, P, I, I, P, I, ctypes.POINTER(I)], I),
         "smlm_plan_export": ([P, BP, I, P, I, ctypes.POINTER(I)], I),
         "smlm_status_string": ([I], ctypes.c_char_p),
@@ -204,6 +207,24 @@ def smlm_backward(pool: int, batch: Batch, X, W, dY, V_save=None, dX=None, accum
     _check(_lib.smlm_backward(pool, ctypes.byref(batch.c), _ptr(X), _ptr(W), _ptr(dY), _ptr(V_save), _ptr(dX),
                               int(bool(accumulate)), _ptr(ws), 0 if ws is None else ws.numel() * ws.element_size(),
                               _stream(stream, X.device)), "smlm_backward")
+
+
+def smlm_workspace_size_backward_multi(pools, batch: Batch) -> int:
+    hs = _ptr_array(list(pools))
+    return int(_lib.smlm_workspace_size_backward_multi(len(pools), ctypes.cast(hs, ctypes.c_void_p),
+                                                       ctypes.byref(batch.c)))
+
+
+def smlm_backward_multi(pools, batch: Batch, X, Ws, dYs, V_saves, dXs, accumulate=False, ws=None, stream=None):
+    """Backward of several projections sharing X (include/smlm.h smlm_backward_multi)."""
+    n = len(pools)
+    hs, wp, yp, xp = _ptr_array(list(pools)), _ptr_array(Ws), _ptr_array(dYs), _ptr_array(dXs)
+    vp = None if V_saves is None else _ptr_array(V_saves)
+    c = lambda a: ctypes.cast(a, ctypes.c_void_p)  # noqa: E731
+    _check(_lib.smlm_backward_multi(n, c(hs), ctypes.byref(batch.c), _ptr(X), c(wp), c(yp),
+                                    None if vp is None else c(vp), c(xp), int(bool(accumulate)), _ptr(ws),
+                                    0 if ws is None else ws.numel() * ws.element_size(), _stream(stream, X.device)),
+           "smlm_backward_multi")
 
 
 def smlm_plan(batch: Batch, capacity: int, registered, l_long: int = 64, backward: bool = False):

@@ -27,6 +27,6 @@ for kind, name in ((0, "fwd"), (1, "bwd")):
     ms, n = S.smlm_profile_read(kind)
     S.smlm_profile_enable(0)
     f, b = wl.flops()
-    fl = (sum(wl.fwd_gemm_flops(p) for p in synth.PROJECTIONS) if kind == 0 else b) * 6
+    fl = (sum(wl.fwd_gemm_flops(p) for p in synth.PROJECTIONS) if kind == 0 else b) * 6 * bench.N_LAYERS
     print(json.dumps({"gemm": name, "launches": n, "ms_total": ms, "tflops": fl / ms / 1e9,
                       "frac_sustained": fl / ms / 1e9 / peaks["bf16_tflops_sustained"]}))

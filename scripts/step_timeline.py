@@ -33,6 +33,6 @@ for e in ev:
         gaps.append(e.time_range.start - prev_end)
     prev_end = max(prev_end or 0, e.time_range.end)
 span = t1 - t0
-out = {"span_us_per_step": span / 3, "busy_us_per_step": sum(busy.values()) / 3, "gap_us_per_step": sum(gaps) / 3,
+out = {"layers_per_step": bench.N_LAYERS, "span_us_per_step": span / 3, "busy_us_per_step": sum(busy.values()) / 3, "gap_us_per_step": sum(gaps) / 3,
        "n_gaps": len(gaps) // 3, "top": sorted(((k, round(v / 3, 1)) for k, v in busy.items()), key=lambda x: -x[1])[:14]}
 print(json.dumps(out, indent=1))

@@ -564,3 +564,72 @@ def test_full_c4_qkv_multi_sampled():
     for i, w in enumerate(ws_):
         Y, _ = oracle.forward(batch, w.W, w.A, w.B, w.slot_scale, X, rows=rows)
         assert parity_err(Ys[i].double().numpy()[rows], Y[rows]) <= BF16_TOL, i
+
+
+@pytest.mark.parametrize("r,outs,lengths", [
+    (16, (320, 192, 192), [300, 260, 3, 1, 140]),          # q/k/v-like: three projections
+    (32, (256, 512), [129, 127, 1, 2, 513]),               # gate/up-like, odd tile counts
+    (64, (192,), [200, 70]),
+])
+def test_bf16_backward_multi_equals_single(r, outs, lengths):
+    """smlm_backward_multi (one dX GEMM launch over every projection's n-tiles) is bit-identical to
+    the per-projection smlm_backward calls and matches the oracle."""
+    from paper_2511_00101_b200 import smlm as S
+    dev = torch.device("cuda", 0)
+    in_f, U = 256, 5
+    modes = [FINETUNE, FINETUNE, DECODE, DECODE, FINETUNE][:len(lengths)]
+    slots = [0, 3, 1, -1, 2][:len(lengths)]
+    batch = synth.batch_from_lengths(lengths, slots, modes)
+    g = torch.Generator().manual_seed(77)
+    ws_ = [synth.draw_weights(g, in_f, o, r, U) for o in outs]
+    X = torch.randn(batch.S, in_f, generator=g).to(torch.bfloat16)
+    dYs = [torch.randn(batch.S, o, generator=g).to(torch.bfloat16) for o in outs]
+    b = S.Batch.from_synth(batch)
+    Xd = X.to(dev)
+
+    def run(multi):
+        pools, keep, grads = [], [], []
+        for w in ws_:
+            pool = S.Pool(in_f, w.W.shape[0], r, U)
+            gA = torch.zeros(U, r, in_f, device=dev)
+            gB = torch.zeros(U, w.W.shape[0], r, device=dev)
+            for a in range(U):
+                A, B = w.A[a].to(dev).contiguous(), w.B[a].to(dev).contiguous()
+                keep += [A, B]
+                pool.register(A, B, w.slot_scale[a])
+                pool.set_grad(a, gA[a], gB[a])
+            pools.append(pool)
+            grads.append((gA, gB))
+        Wd = [w.W.to(dev) for w in ws_]
+        dYd = [y.to(dev) for y in dYs]
+        dXs = [torch.zeros(batch.S, in_f, dtype=torch.bfloat16, device=dev) for _ in ws_]
+        Vs = []
+        for i, pool in enumerate(pools):
+            V = torch.zeros(batch.S, r, dtype=torch.bfloat16, device=dev)
+            pool.forward(b, Xd, Wd[i], V_save=V)
+            Vs.append(V)
+        if multi:
+            n0 = S.smlm_launch_count()
+            ws = torch.empty(S.smlm_workspace_size_backward_multi([p.h for p in pools], b) + 256, dtype=torch.uint8,
+                             device=dev)
+            S.smlm_backward_multi([p.h for p in pools], b, Xd, Wd, dYd, Vs, dXs, ws=ws)
+        else:
+            for i, pool in enumerate(pools):
+                pool.backward(b, Xd, Wd[i], dYd[i], Vs[i], dXs[i])
+        torch.cuda.synchronize()
+        for p_ in pools:
+            p_.close()
+        return [x.cpu() for x in dXs], [(a.cpu(), bb.cpu()) for a, bb in grads]
+
+    dX1, g1 = run(False)
+    dXm, gm = run(True)
+    ft = batch.ft_rows()
+    rs = batch.row_slot()
+    for i, w in enumerate(ws_):
+        assert torch.equal(dX1[i][ft], dXm[i][ft]), i
+        assert torch.equal(g1[i][0], gm[i][0]) and torch.equal(g1[i][1], gm[i][1]), i
+        dXr, dAr, dBr = oracle.backward(batch, w.W, w.A, w.B, w.slot_scale, X, dYs[i])
+        assert parity_err(dXm[i].double().numpy()[ft], dXr[ft]) <= BF16_TOL, i
+        for a in sorted(set(rs[ft].tolist()) - {-1}):
+            assert parity_err(gm[i][0][a], dAr[a]) <= BF16_TOL, (i, a)
+            assert parity_err(gm[i][1][a], dBr[a]) <= BF16_TOL, (i, a)
