@@ -46,10 +46,11 @@ def _load():
             lib = ctypes.CDLL(_LIB_PATH)
             P = ctypes.c_void_p
             I = ctypes.c_int
-            lib.oracle_forward.argtypes = [I, I, I, I, I, P, P, P, P, P, P, P, P, P, P, P, I, P]
+            D = ctypes.c_double
+            lib.oracle_forward.argtypes = [I, I, I, I, I, P, P, P, P, P, P, P, P, P, P, P, I, P, P, D]
             lib.oracle_forward.restype = I
             lib.oracle_backward.argtypes = [I, I, I, I, I, P, P, P, P, I, P, P, P, P, P, P, P, P, P,
-                                            P, I, I, P]
+                                            P, I, I, P, P, D]
             lib.oracle_backward.restype = I
             lib.oracle_num_threads.restype = I
             lib.oracle_set_num_threads.argtypes = [I]
@@ -104,8 +105,20 @@ def _batch_arrays(batch):
     return off, slot, mode, ss
 
 
-def forward(batch, W, A, B, slot_scale, X, rows=None, Y_in=None):
+def _keep(keep, S, in_f):
+    """Dropout keep mask [S, in] (1 = kept) as uint8, or None (no dropout)."""
+    if keep is None:
+        return None
+    k = np.ascontiguousarray(np.asarray(keep).astype(np.uint8))
+    assert k.shape == (S, in_f), (k.shape, S, in_f)
+    return k
+
+
+def forward(batch, W, A, B, slot_scale, X, rows=None, Y_in=None, keep=None, p=0.0):
     """y_t = W x_t + s B_a (A_a x_t) in fp64.
+
+    keep / p: LoRA dropout of FINETUNE rows (keep [S,in] bool mask, p the drop probability:
+    x~ = keep * x / (1 - p) feeds A_a; smlm_oracle.c header).
 
     W: [out,in] or None (then Y_in [S,out] is the base output, updated in place semantics).
     A: list of [r,in]; B: list of [out,r]; slot_scale: list of floats (per slot).
@@ -126,16 +139,17 @@ def forward(batch, W, A, B, slot_scale, X, rows=None, Y_in=None):
     Y = np.zeros((S, out_f)) if Y_in is None else _f64(Y_in).copy()
     V = np.zeros((S, r))
     rr = None if rows is None else np.ascontiguousarray(rows, np.int64)
+    kp = _keep(keep, S, in_f)
     rc = lib.oracle_forward(S, in_f, out_f, r, batch.G, _ptr(off), _ptr(slot), _ptr(mode), _ptr(ss),
                             _ptr(sl), _ptr(Ad), _ptr(Bd), _ptr(Xd), _ptr(Wd), _ptr(Y), _ptr(V),
-                            0 if rr is None else len(rr), _ptr(rr))
+                            0 if rr is None else len(rr), _ptr(rr), _ptr(kp), 1.0 / (1.0 - p))
     if rc != 0:
         raise ValueError("oracle_forward: malformed batch")
     return Y, V
 
 
 def backward(batch, W, A, B, slot_scale, X, dY, has_grad=None, rows=None, dA_in=None, dB_in=None,
-             accumulate=False, want_dx=True):
+             accumulate=False, want_dx=True, keep=None, p=0.0):
     """Fine-tune backward in fp64.  Returns (dX [S,in] (zeros on non-FT rows), dA [U,r,in], dB [U,out,r]);
     r is the largest adapter rank: adapter a's gradients are dA[a, :r_a] and dB[a, :, :r_a]."""
     lib = _load()
@@ -157,7 +171,7 @@ def backward(batch, W, A, B, slot_scale, X, dY, has_grad=None, rows=None, dA_in=
     rc = lib.oracle_backward(S, in_f, out_f, r, batch.G, _ptr(off), _ptr(slot), _ptr(mode), _ptr(ss),
                              U, _ptr(sl), _ptr(Ad), _ptr(Bd), _ptr(Xd), _ptr(Wd), _ptr(dYd), _ptr(dX),
                              _ptr(dA), _ptr(dB), _ptr(hg), int(bool(accumulate)),
-                             0 if rr is None else len(rr), _ptr(rr))
+                             0 if rr is None else len(rr), _ptr(rr), _ptr(_keep(keep, S, in_f)), 1.0 / (1.0 - p))
     if rc != 0:
         raise ValueError("oracle_backward: malformed batch")
     return dX, dA[:U], dB[:U]

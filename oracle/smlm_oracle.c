@@ -23,6 +23,15 @@
  *     dx_t   = W^T dy_t + s A_a^T u
  *     dA_a  += s u x_t^T ,   dB_a += s dy_t v^T     (only for adapters that have grads)
  *
+ * LoRA dropout (f2; App. D Table 5 "lora_dropout 0.05"; reading R13):
+ * with the PEFT LoRA definition y = W x + s B A dropout(x), dropout acting in training mode only,
+ * i.e. on FINETUNE rows.  The mask is an INPUT here (keep [S,in], 1 = kept, NULL = no dropout):
+ *     x~_t   = keep_t * x_t * keep_scale            (keep_scale = 1/(1-p), inverted dropout)
+ *     v      = A_a x~_t ,   y_t = W x_t + s B_a v
+ *     dx_t   = W^T dy_t + s keep_t * keep_scale * (A_a^T u)
+ *     dA_a  += s u x~_t^T ,  dB_a += s dy_t v^T
+ * for fine-tune rows with an adapter; every other row is unchanged.
+ *
  * Every sum is a straight loop in ascending index order with an fp64 accumulator.
  * No blocking, no fusion, no reordering.  OpenMP only splits independent rows/entries.
  */
@@ -59,7 +68,7 @@ int oracle_forward(int S, int in_f, int out_f, int r, int G,
                    const double *seg_scale, const double *slot_scale,
                    const double *A, const double *B,
                    const double *X, const double *W, double *Y, double *Vsave,
-                   int n_rows, const long *rows)
+                   int n_rows, const long *rows, const unsigned char *keep, double keep_scale)
 {
     int *seg = (int *)malloc(sizeof(int) * (S > 0 ? S : 1));
     if (row_segments(S, G, off, seg)) { free(seg); return 1; }
@@ -71,12 +80,16 @@ int oracle_forward(int S, int in_f, int out_f, int r, int G,
         int a = slot[g];
         double s = eff_scale(g, a, slot_scale, seg_scale);
         const double *x = X + (size_t)t * in_f;
+        const unsigned char *kp = (keep && mode[g] == SMLM_FINETUNE) ? keep + (size_t)t * in_f : NULL;
         double v[256];
         if (a >= 0) {
             const double *Aa = A + (size_t)a * r * in_f;
             for (int j = 0; j < r; ++j) {
                 double acc = 0.0;
-                for (int k = 0; k < in_f; ++k) acc += Aa[(size_t)j * in_f + k] * x[k];
+                for (int k = 0; k < in_f; ++k) {
+                    double xk = kp ? (kp[k] ? x[k] * keep_scale : 0.0) : x[k];   /* dropout(x) */
+                    acc += Aa[(size_t)j * in_f + k] * xk;
+                }
                 v[j] = acc;
             }
         }
@@ -116,7 +129,8 @@ int oracle_backward(int S, int in_f, int out_f, int r, int G,
                     const double *seg_scale, int n_slots, const double *slot_scale,
                     const double *A, const double *B, const double *X, const double *W,
                     const double *dY, double *dX, double *dA, double *dB,
-                    const int *has_grad, int accumulate, int n_rows, const long *rows)
+                    const int *has_grad, int accumulate, int n_rows, const long *rows,
+                    const unsigned char *keep, double keep_scale)
 {
     int *seg = (int *)malloc(sizeof(int) * (S > 0 ? S : 1));
     if (row_segments(S, G, off, seg)) { free(seg); return 1; }
@@ -149,6 +163,7 @@ int oracle_backward(int S, int in_f, int out_f, int r, int G,
                 if (a >= 0) {
                     const double *Aa = A + (size_t)a * r * in_f;
                     for (int j = 0; j < r; ++j) lora += u[j] * Aa[(size_t)j * in_f + k];
+                    if (keep) lora *= keep[(size_t)t * in_f + k] ? keep_scale : 0.0;   /* d dropout(x) / dx */
                 }
                 dX[(size_t)t * in_f + k] = base + s * lora;
             }
@@ -179,10 +194,12 @@ int oracle_backward(int S, int in_f, int out_f, int r, int G,
             for (int i = 0; i < T; ++i) {
                 const double *x = X + (size_t)trows[i] * in_f;
                 const double *dy = dY + (size_t)trows[i] * out_f;
+                const unsigned char *kp = keep ? keep + (size_t)trows[i] * in_f : NULL;
                 for (int j = 0; j < r; ++j) {
                     double uv = 0.0, vv = 0.0;
                     for (int o = 0; o < out_f; ++o) uv += dy[o] * Ba[(size_t)o * r + j];
-                    for (int k = 0; k < in_f; ++k) vv += Aa[(size_t)j * in_f + k] * x[k];
+                    for (int k = 0; k < in_f; ++k)
+                        vv += Aa[(size_t)j * in_f + k] * (kp ? (kp[k] ? x[k] * keep_scale : 0.0) : x[k]);
                     U[(size_t)i * r + j] = uv;
                     V[(size_t)i * r + j] = vv;
                 }
@@ -193,8 +210,11 @@ int oracle_backward(int S, int in_f, int out_f, int r, int G,
                 for (long e = 0; e < (long)r * in_f; ++e) {
                     int j = (int)(e / in_f), k = (int)(e % in_f);
                     double acc = 0.0;
-                    for (int i = 0; i < T; ++i)
-                        acc += sc[i] * U[(size_t)i * r + j] * X[(size_t)trows[i] * in_f + k];
+                    for (int i = 0; i < T; ++i) {
+                        double xk = X[(size_t)trows[i] * in_f + k];
+                        if (keep) xk = keep[(size_t)trows[i] * in_f + k] ? xk * keep_scale : 0.0;   /* x~ */
+                        acc += sc[i] * U[(size_t)i * r + j] * xk;
+                    }
                     dAa[e] = accumulate ? dAa[e] + acc : acc;
                 }
             }

@@ -258,3 +258,49 @@ def draw_adamw_state(seed: int, n: int, step: int = 1):
         m = torch.zeros(n)
         v = torch.zeros(n)
     return p, m, v, grad
+
+
+# ----------------------------------------------------------------------------------------
+# LoRA dropout mask (Table 5 lora_dropout 0.05; R13):
+# a counter-based generator, so the oracle gets the mask as an explicit input while the CUDA
+# path draws the same bits from (seed, row, column) with its own implementation of this hash
+# (no shared code: csrc implements it in CUDA).  It is a random-number generator, not method
+# arithmetic.
+#   thr = round(p * 65536)  (drop probability quantised to 1/65536; keep scale 65536/(65536-thr))
+#   element (t, k) of X [S, in]:  c = t * ceil(in/2) + floor(k/2)   (uint32, wrapping)
+#     h = lowbias32(lowbias32(c ^ seed_lo) ^ seed_hi)
+#     u = (k odd) ? h >> 16 : h & 0xffff ;   kept  <=>  u >= thr
+# ----------------------------------------------------------------------------------------
+def dropout_threshold(p: float) -> int:
+    if not (0.0 <= p < 1.0):
+        raise ValueError("dropout p must be in [0, 1)")
+    return int(round(p * 65536.0))
+
+
+def dropout_effective_p(p: float) -> float:
+    """The drop probability the threshold realises (what the oracle's keep scale uses)."""
+    return dropout_threshold(p) / 65536.0
+
+
+def _lowbias32(x: np.ndarray) -> np.ndarray:
+    x = x.astype(np.uint32)
+    x ^= x >> np.uint32(16)
+    x = (x * np.uint32(0x7FEB352D)).astype(np.uint32)
+    x ^= x >> np.uint32(15)
+    x = (x * np.uint32(0x846CA68B)).astype(np.uint32)
+    x ^= x >> np.uint32(16)
+    return x
+
+
+def dropout_keep(seed: int, p: float, S: int, in_f: int) -> np.ndarray:
+    """bool [S, in_f]: True where the element is kept."""
+    thr = dropout_threshold(p)
+    seed_lo, seed_hi = np.uint32(seed & 0xFFFFFFFF), np.uint32((seed >> 32) & 0xFFFFFFFF)
+    half = (in_f + 1) // 2
+    t = np.arange(S, dtype=np.uint64)[:, None]
+    k = np.arange(in_f, dtype=np.uint64)[None, :]
+    c = ((t * np.uint64(half) + k // np.uint64(2)) & np.uint64(0xFFFFFFFF)).astype(np.uint32)
+    with np.errstate(over="ignore"):
+        h = _lowbias32(_lowbias32(c ^ seed_lo) ^ seed_hi)
+    u = np.where((k % 2).astype(bool), h >> np.uint32(16), h & np.uint32(0xFFFF))
+    return u >= np.uint32(thr)
