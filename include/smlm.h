@@ -143,6 +143,18 @@ SMLM_API int smlm_adapter_unregister(smlm_pool pool, int slot, void *stream);
  *   seg_mode    [G]  : SMLM_FINETUNE .. SMLM_DECODE
  *   seg_scale   [G]  : dynamic per-request scale (finite, > 0) or NULL (= 1); multiplies the
  *                      slot scale ("applied on a per-request basis during the forward pass")
+ *   dropout_p, dropout_seed: LoRA dropout of the FINETUNE rows (App. D
+ *                      Table 5 lora_dropout 0.05; PEFT y = W x + s B A dropout(x), training mode =
+ *                      fine-tune rows only; R13).  p in [0, 1), 0 = off (zero-initialise
+ *                      the struct); quantised to thr = round(p * 65536).  Element (t, k) of X is kept
+ *                      iff u >= thr, u the 16-bit half (k odd: high) of
+ *                      lowbias32(lowbias32((t * ceil(in/2) + k/2) ^ seed_lo) ^ seed_hi), and kept
+ *                      elements are scaled by 65536 / (65536 - thr).  The forward and the backward of
+ *                      one step must pass the same seed (the mask is recomputed, never stored).
+ *                      smlm_forward_multi / smlm_backward_multi use seed + i * 0x9E3779B97F4A7C15 for
+ *                      projection i (independent masks, as PEFT's per-module dropout).  bf16 pools
+ *                      need SMLM_OPT_CTA_PAIR = 1 and W != NULL for fine-tune rows with dropout
+ *                      (else SMLM_E_UNSUPPORTED).
  */
 typedef struct {
     int S;
@@ -151,6 +163,8 @@ typedef struct {
     const int32_t *seg_slot;
     const int8_t *seg_mode;
     const float *seg_scale;
+    float dropout_p;
+    uint64_t dropout_seed;
 } smlm_batch;
 
 /* Bytes of device workspace a forward (backward = 0) or backward (backward = 1) call needs. */

@@ -33,10 +33,10 @@ int launch_gemm2(const Gemm2Args &a, bool bwd, int num_sms, cudaStream_t st);
 int launch_u(const UArgs &a, int num_sms, cudaStream_t st);
 int launch_shrink_short(const __nv_bfloat16 *X, const SlotDev *slots, const DevBlock *blocks,
                         const DevShortRow *srows, int n_blocks, int in_f, int r, int r_pad, __nv_bfloat16 *Vbd,
-                        __nv_bfloat16 *Vsave, cudaStream_t st);
+                        __nv_bfloat16 *Vsave, const DropArgs &drop, cudaStream_t st);
 template <typename T>
 int launch_rows_shrink(const DevTile *tiles, int n_tiles, const SlotDev *slots, const T *X, int in_f, int r,
-                       float *Vf, T *Vsave, int ft_only, cudaStream_t st);
+                       float *Vf, T *Vsave, int ft_only, const DropArgs &drop, cudaStream_t st);
 template <typename T>
 int launch_rows_u(const DevTile *tiles, int n_tiles, const SlotDev *slots, const T *dY, int out_f, int r, float *Uf,
                   __nv_bfloat16 *sUt, int r_pad, cudaStream_t st);
@@ -54,16 +54,16 @@ int launch_adamw_sumsq(const float *g, size_t n, float gscale, float *partial, i
 int launch_adamw_step(const AdamwArgs &a, int grid, cudaStream_t st);
 int launch_shrink_split(const __nv_bfloat16 *X, const SlotDev *slots, const DevBlock *blocks,
                         const DevShortRow *srows, int n_blocks, int in_f, int r, int r_pad, float *part,
-                        __nv_bfloat16 *Vbd, __nv_bfloat16 *Vsave, int *ctr, cudaStream_t st);
+                        __nv_bfloat16 *Vbd, __nv_bfloat16 *Vsave, int *ctr, const DropArgs &drop, cudaStream_t st);
 size_t grad_group_bytes();
 void fill_grad_group(void *dst, int slot, int tile_begin, int n_tiles, int r, float *dA, float *dB);
 template <typename T, typename TV>
 int launch_dadb(const DevTile *tiles, const void *groups, int n_groups, const T *X, const T *dY, const float *Uf,
-                const TV *V, int in_f, int out_f, int r, int accumulate, cudaStream_t st);
+                const TV *V, int in_f, int out_f, int r, int accumulate, const DropArgs &drop, cudaStream_t st);
 int launch_f32_fwd(const DevTile *tiles, int n_tiles, const SlotDev *slots, const float *X, const float *W, float *Y,
                    const float *Vf, int in_f, int out_f, int r, cudaStream_t st);
 int launch_f32_dx(const DevTile *tiles, int n_tiles, const SlotDev *slots, const float *dY, const float *W, float *dX,
-                  const float *Uf, int in_f, int out_f, int r, cudaStream_t st);
+                  const float *Uf, int in_f, int out_f, int r, const DropArgs &drop, cudaStream_t st);
 }  // namespace smlm
 
 using namespace smlm;
@@ -398,6 +398,36 @@ int plan_for(smlm_pool p, const smlm_batch *b, bool bwd, Plan &plan) {
     return SMLM_OK;
 }
 
+// LoRA dropout of the batch's FINETUNE rows (smlm.h smlm_batch; R13)
+DropArgs make_drop(const smlm_batch *b, int in_f) {
+    DropArgs d;
+    memset(&d, 0, sizeof(d));
+    const double pq = std::floor((double)b->dropout_p * 65536.0 + 0.5);   // round(p * 65536), p in [0, 1)
+    d.thr = (uint32_t)std::min(pq, 65535.0);
+    d.on = d.thr > 0;
+    d.s0 = (uint32_t)(b->dropout_seed & 0xffffffffu);
+    d.s1 = (uint32_t)(b->dropout_seed >> 32);
+    d.half_in = (uint32_t)((in_f + 1) / 2);
+    d.scale = (float)(65536.0 / (65536.0 - (double)d.thr));
+    return d;
+}
+// does the plan have fine-tune rows with an adapter (the rows dropout acts on)?
+bool has_ft_lora(const Plan &plan) {
+    for (auto &t : plan.long_tiles)
+        if (t.flags & kTileFT) return true;
+    for (auto &r : plan.short_rows)
+        if (r.ft) return true;
+    for (auto &t : plan.bwd_tiles)
+        if (t.slot >= 0) return true;
+    return false;
+}
+// projection i of a multi-projection call draws an independent mask (PEFT: one dropout per module)
+smlm_batch batch_for_projection(const smlm_batch *b, int i) {
+    smlm_batch c = *b;
+    c.dropout_seed = b->dropout_seed + (uint64_t)i * 0x9E3779B97F4A7C15ull;
+    return c;
+}
+
 // make_map through the pool's small descriptor cache (round-robin replacement, 64 entries)
 int make_map_cached(smlm_pool p, CUtensorMap *m, const void *ptr, uint64_t inner, uint64_t outer, uint32_t b0,
                     uint32_t b1, CUtensorMapSwizzle swz) {
@@ -436,7 +466,7 @@ Dec3Plan dec3_plan(int n_proj, const smlm_pool *pools, const smlm_batch *b, cons
     Dec3Plan D;
     smlm_pool p0 = pools[0];
     if (p0->dtype != SMLM_BF16 || !plan.long_tiles.empty() || plan.short_tiles.empty() || b->S > kDec3InlineRows ||
-        !p0->dec_kernel)
+        !p0->dec_kernel || (b->dropout_p > 0.f && has_ft_lora(plan)))   // dropout rows: the mixed path
         return D;
     // adapters of the batch (ascending) and per-row records
     D.rows.assign(b->S, Dec3RowInfo{-1, 0.f, 0, 0});
@@ -795,11 +825,11 @@ static int fwd_prepare(smlm_pool p, const smlm_batch *b, const Plan &plan, const
             CKL(launch_shrink_split((const __nv_bfloat16 *)X, p->d_slots, F.blocks_dev, d_srows,
                                     (int)plan.blocks.size(), p->in, p->r, p->r_pad,
                                     reinterpret_cast<float *>(wsb + L.spart_off), F.vbd, (__nv_bfloat16 *)V_save,
-                                    sctr, st), sctr ? 1 : 2);
+                                    sctr, make_drop(b, p->in), st), sctr ? 1 : 2);
         } else {
             CKL(launch_shrink_short((const __nv_bfloat16 *)X, p->d_slots, F.blocks_dev, d_srows,
                                     (int)plan.blocks.size(), p->in, p->r, p->r_pad, F.vbd, (__nv_bfloat16 *)V_save,
-                                    st), 1);
+                                    make_drop(b, p->in), st), 1);
         }
     }
     return SMLM_OK;
@@ -1237,13 +1267,16 @@ int smlm_forward(smlm_pool p, const smlm_batch *b, const void *X, const void *W,
         const int nt = (int)plan.long_tiles.size();
         float *Vf = reinterpret_cast<float *>(wsb + L.vf_off);
         CKL(launch_rows_shrink<float>(tiles, nt, p->d_slots, (const float *)X, p->in, p->r, Vf, (float *)V_save, 1,
-                                      st), 1);
+                                      make_drop(b, p->in), st), 1);
         CKL(launch_f32_fwd(tiles, nt, p->d_slots, (const float *)X, (const float *)W, (float *)Y, Vf, p->in, p->out,
                            p->r, st), 1);
         return SMLM_OK;
     }
 
     // ---------------- bf16 tensor-core path ----------------
+    if (b->dropout_p > 0.f && (!W || !p->cta_pair) && has_ft_lora(plan))
+        return set_err(SMLM_E_UNSUPPORTED, "LoRA dropout on fine-tune rows needs W != NULL and SMLM_OPT_CTA_PAIR = 1 "
+                                           "(the pre-shrink pass masks x; the fused 1-CTA shrink cannot)");
     FwdPrep F;
     if ((rc = fwd_prepare(p, b, plan, L, X, W, V_save, wsb, uctr, st, F))) return rc;
     if (F.n_tiles == 0) return SMLM_OK;
@@ -1269,6 +1302,7 @@ int smlm_forward(smlm_pool p, const smlm_batch *b, const void *X, const void *W,
             u.vf = 1;
             u.r = p->r;
             u.Vsave = V_save;
+            u.drop = make_drop(b, p->in);
             u.ctr = u.n_items <= kUCtrMax ? uctr : nullptr;
             CKL(launch_u(u, p->num_sms, st), u.ctr ? 1 : 2);
         }
@@ -1406,6 +1440,16 @@ int smlm_forward_multi(int n_proj, const smlm_pool *pools, const smlm_batch *b, 
     if (!X || !W || !Y) return set_err(SMLM_E_INVALID, "X, W and Y must be non-NULL");
     for (int i = 0; i < n_proj; ++i)
         if (!W[i] || !Y[i]) return set_err(SMLM_E_INVALID, "W[i] and Y[i] must be non-NULL");
+    if (b->dropout_p > 0.f && has_ft_lora(plan)) {
+        // LoRA dropout: every projection draws its own mask (seed + i * golden), so the shared
+        // pre-shrink cannot serve them all -- the per-projection calls
+        for (int i = 0; i < n_proj; ++i) {
+            const smlm_batch bi = batch_for_projection(b, i);
+            if ((rc = smlm_forward(pools[i], &bi, X, W[i], Y[i], V_save ? V_save[i] : nullptr, ws, ws_bytes, stream)))
+                return rc;
+        }
+        return SMLM_OK;
+    }
     const Dec3Plan D = same ? dec3_plan(n_proj, pools, b, plan) : Dec3Plan();
     if (D.ok) {
         if (!ws || ws_bytes < D.total) return set_err(SMLM_E_WORKSPACE, "workspace too small");
@@ -1600,7 +1644,7 @@ static int bwd_tok(smlm_pool p, const smlm_batch *b, const void *X, const void *
             CKL(launch_prep_sv<__nv_bfloat16>(B.tiles, B.nt, (const __nv_bfloat16 *)V_save, p->r, p->r_pad, B.sVt, st), 1);
     } else {
         CKL(launch_rows_shrink<__nv_bfloat16>(B.tiles, B.nt, p->d_slots, (const __nv_bfloat16 *)X, p->in, p->r, B.Vf,
-                                              nullptr, 0, st), 1);
+                                              nullptr, 0, make_drop(b, p->in), st), 1);
         CKL(launch_prep_sv<float>(B.tiles, B.nt, B.Vf, p->r, p->r_pad, B.sVt, st), 1);
     }
     TokArgs ta;
@@ -1621,6 +1665,7 @@ static int bwd_tok(smlm_pool p, const smlm_batch *b, const void *X, const void *
     ta.mt_a = (p->in + 128 * ta.nh - 1) / (128 * ta.nh);
     ta.mt_b = (p->out + 128 * ta.nh - 1) / (128 * ta.nh);
     ta.accumulate = accumulate ? 1 : 0;
+    ta.drop = make_drop(b, p->in);
     CKL(launch_tok(ta, p->num_sms, st), 1);
     return SMLM_OK;
 }
@@ -1648,18 +1693,19 @@ int smlm_backward(smlm_pool p, const smlm_batch *b, const void *X, const void *W
     if (p->dtype == SMLM_FP32) {
         CKL(launch_rows_u<float>(B.tiles, B.nt, p->d_slots, (const float *)dY, p->out, p->r, B.Uf, nullptr, p->r_pad,
                                  st), 1);
+        const DropArgs drop = make_drop(b, p->in);
         if (dX)
             CKL(launch_f32_dx(B.tiles, B.nt, p->d_slots, (const float *)dY, (const float *)W, (float *)dX, B.Uf, p->in,
-                              p->out, p->r, st), 1);
+                              p->out, p->r, drop, st), 1);
         if (B.n_grad) {
             const float *V = (const float *)V_save;
             if (!V) {
                 CKL(launch_rows_shrink<float>(B.tiles, B.nt, p->d_slots, (const float *)X, p->in, p->r, B.Vf, nullptr,
-                                              0, st), 1);
+                                              0, drop, st), 1);
                 V = B.Vf;
             }
             CKL((launch_dadb<float, float>(B.tiles, B.groups, B.n_grad, (const float *)X, (const float *)dY, B.Uf, V,
-                                           p->in, p->out, p->r, accumulate, st)), 2);
+                                           p->in, p->out, p->r, accumulate, drop, st)), 2);
         }
         return SMLM_OK;
     }
@@ -1671,6 +1717,7 @@ int smlm_backward(smlm_pool p, const smlm_batch *b, const void *X, const void *W
             Gemm2Args g2;
             memset(&g2, 0, sizeof(g2));
             if ((rc = bwd_gemm2_proj(p, b, W, dY, dX, B, 0, g2.proj[0]))) return rc;
+            g2.drop = make_drop(b, p->in);
             g2.pairs = B.pairs;
             g2.n_proj = 1;
             g2.n_pairs = B.n_pairs;
@@ -1681,6 +1728,9 @@ int smlm_backward(smlm_pool p, const smlm_batch *b, const void *X, const void *W
             g2.stages = gemm2_stages(p->r_pad);
             CKL(launch_gemm2(g2, true, p->num_sms, st), 1);
         } else {
+            if (b->dropout_p > 0.f && B.u_items)
+                return set_err(SMLM_E_UNSUPPORTED, "LoRA dropout needs SMLM_OPT_CTA_PAIR = 1 for dX (the mask multiplies "
+                                                   "only the LoRA term: a separate accumulator)");
             GemmArgs a;
             memset(&a, 0, sizeof(a));
             if ((rc = make_map(&a.tmA, dY, p->out, b->S, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B))) return rc;
@@ -1755,11 +1805,16 @@ int smlm_backward_multi(int n_proj, const smlm_pool *pools, const smlm_batch *b,
     smlm_pool p0 = pools[0];
     const size_t each = bwd_ws_each(n_proj, pools, b, plan, true);
     if (!ws || ws_bytes < (size_t)n_proj * each) return set_err(SMLM_E_WORKSPACE, "workspace too small");
-    if (p0->dtype != SMLM_BF16 || !p0->cta_pair) {   // one call per projection (same math)
-        for (int i = 0; i < n_proj; ++i)
-            if ((rc = smlm_backward(pools[i], b, X, W[i], dY[i], V_save ? V_save[i] : nullptr, dX[i], accumulate,
+    const bool drop = b->dropout_p > 0.f && has_ft_lora(plan);
+    if (p0->dtype != SMLM_BF16 || !p0->cta_pair || drop) {
+        // one call per projection (same math; with LoRA dropout each projection has its own mask,
+        // seed + i * golden, as smlm_forward_multi)
+        for (int i = 0; i < n_proj; ++i) {
+            const smlm_batch bi = batch_for_projection(b, i);
+            if ((rc = smlm_backward(pools[i], &bi, X, W[i], dY[i], V_save ? V_save[i] : nullptr, dX[i], accumulate,
                                     reinterpret_cast<uint8_t *>(ws) + i * each, each, stream)))
                 return rc;
+        }
         return SMLM_OK;
     }
     DeviceGuard dg(p0->device);

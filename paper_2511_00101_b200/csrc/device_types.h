@@ -34,6 +34,19 @@ static_assert(sizeof(SlotDev) % 64 == 0, "SlotDev must keep 64-byte alignment of
 // descriptor cached for a slot's previous adapter is never used (no tensormap proxy fence needed;
 // that fence is required only for descriptors modified by device code).
 
+// LoRA dropout on FINETUNE rows (Table 5; R13): the keep
+// mask of element (t, k) of X [S, in] is drawn from a counter-based hash of (seed, t, k) -- the
+// definition synth.dropout_keep implements on the host for the oracle (no shared code):
+//   c = t * half_in + k / 2 (uint32), h = lowbias32(lowbias32(c ^ s0) ^ s1),
+//   u = k odd ? h >> 16 : h & 0xffff, kept <=> u >= thr;  x~ = kept * x * scale, scale = 1/(1 - p)
+struct DropArgs {
+    uint32_t thr;       // round(p * 65536); 0 = dropout off
+    uint32_t s0, s1;    // seed (low / high 32 bits)
+    uint32_t half_in;   // ceil(in / 2): hash counters per row
+    float scale;        // 65536 / (65536 - thr)
+    int on;
+};
+
 struct GemmArgs {
     CUtensorMap tmA;   // X [S,in] (fwd) or dY [S,out] (bwd): box {64,128} SW128
     CUtensorMap tmB;   // W [out,in]: fwd box {64,256} (K-major); bwd box {64,64} (MN-major)
@@ -93,6 +106,7 @@ struct alignas(64) Gemm2Proj {
 
 struct Gemm2Args {
     Gemm2Proj proj[kGemm2MaxProj];
+    DropArgs drop;            // backward: dX = W^T dy + keep * scale * (s A_a^T u) (separate LoRA accumulator)
     const DevPair *pairs;
     const DevBlock *blocks;   // fwd short tiles' adapter blocks
     int n_proj;
@@ -142,6 +156,7 @@ struct UArgs {
     const SlotDev *slots_p[4];
     void *sUt_p[4];
     void *Vsave_p[4];
+    DropArgs drop;   // forward pre-shrink (vf): LoRA dropout of the FINETUNE tiles' X
 };
 constexpr int kUCtrMax = 4096;   // items per U / pre-shrink launch that use the in-kernel reduce
 
@@ -163,6 +178,7 @@ struct TokArgs {
     int nh;             // 128-column halves per item (1 or 2)
     int accumulate;
     int stages;
+    DropArgs drop;      // dA items: LoRA dropout of X (the mask of the forward), dA scaled by drop.scale
 };
 
 // ------------------------------------------------------------------------------------------

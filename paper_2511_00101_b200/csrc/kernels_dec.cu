@@ -9,6 +9,7 @@
 #include <cuda_runtime.h>
 
 #include "device_types.h"
+#include "dropout.cuh"
 #include "pdl.cuh"
 #include "sm100.cuh"
 
@@ -52,7 +53,8 @@ template <int RP>
 __device__ __forceinline__ void shrink_combine_block(int bi, const DevBlock *__restrict__ blocks,
                                                      const DevShortRow *__restrict__ srows, int nch, int r,
                                                      const float *__restrict__ part, __nv_bfloat16 *__restrict__ Vbd,
-                                                     __nv_bfloat16 *__restrict__ Vsave, int *idx_of, float *vals) {
+                                                     __nv_bfloat16 *__restrict__ Vsave, int *idx_of, float *vals,
+                                                     const DropArgs &drop) {
     const DevBlock blk = blocks[bi];
     for (int i = threadIdx.x; i < 128; i += blockDim.x) idx_of[i] = -1;
     __syncthreads();
@@ -67,6 +69,7 @@ __device__ __forceinline__ void shrink_combine_block(int bi, const DevBlock *__r
             for (int c = 0; c < 16; ++c) t[c] = c < nch ? __ldcg(src + (size_t)c * 128 * RP + i * RP + j) : 0.f;
             for (int c = 0; c < nch && c < 16; ++c) v += t[c];   // chunk order
             for (int c = 16; c < nch; ++c) v += __ldcg(src + (size_t)c * 128 * RP + i * RP + j);
+            if (drop.on && srows[blk.row_begin + i].ft) v *= drop.scale;   // V~ of a dropout row
         }
         vals[i * RP + j] = v;
     }
@@ -93,7 +96,7 @@ __global__ void __launch_bounds__(256) shrink_partial_kernel(const __nv_bfloat16
                                                              const DevShortRow *__restrict__ srows, int in_f,
                                                              int r, float *__restrict__ part, int *ctr,
                                                              __nv_bfloat16 *__restrict__ Vbd,
-                                                             __nv_bfloat16 *__restrict__ Vsave) {
+                                                             __nv_bfloat16 *__restrict__ Vsave, const DropArgs drop) {
     // A_u[:, chunk] and the block's x rows [:, chunk] are staged in shared memory with coalesced
     // 128-bit loads (every byte read once); then warp w computes outputs (i, j) = w, w+8, ...:
     // lane l reduces columns [16 l, 16 l + 16) and a xor-shuffle tree finishes.
@@ -126,6 +129,17 @@ __global__ void __launch_bounds__(256) shrink_partial_kernel(const __nv_bfloat16
         }
         asm volatile("cp.async.wait_all;" ::: "memory");
         __syncthreads();
+        if (drop.on) {   // LoRA dropout of FINETUNE rows: zero the dropped elements of the staged x rows
+            for (int e = threadIdx.x; e < nr * (kChunk / 8); e += 256) {
+                const int i = e / (kChunk / 8), v = e % (kChunk / 8);
+                const DevShortRow sr = srows[blk.row_begin + rb + i];
+                if (sr.ft) {
+                    uint4 *p = reinterpret_cast<uint4 *>(Xs) + e;
+                    *p = drop_mask8(drop, (uint32_t)sr.row, (uint32_t)(k0 + 8 * v), *p);
+                }
+            }
+            __syncthreads();
+        }
         for (int o = warp; o < nr * r; o += 8) {
             const int i = o / r, j = o % r;
             const uint4 *ap = reinterpret_cast<const uint4 *>(As + j * kChunk + 16 * lane);
@@ -163,7 +177,7 @@ __global__ void __launch_bounds__(256) shrink_partial_kernel(const __nv_bfloat16
             // the staged A / X tiles are no longer needed: reuse the dynamic shared memory
             int *idx_of = reinterpret_cast<int *>(sm);
             float *vals = reinterpret_cast<float *>(sm + 512);
-            shrink_combine_block<RP>(blockIdx.x, blocks, srows, nch, r, part, Vbd, Vsave, idx_of, vals);
+            shrink_combine_block<RP>(blockIdx.x, blocks, srows, nch, r, part, Vbd, Vsave, idx_of, vals, drop);
         }
     }
 }
@@ -173,12 +187,12 @@ __global__ void __launch_bounds__(256) shrink_combine_kernel(const DevBlock *__r
                                                              const DevShortRow *__restrict__ srows, int nch,
                                                              int r, const float *__restrict__ part,
                                                              __nv_bfloat16 *__restrict__ Vbd,
-                                                             __nv_bfloat16 *__restrict__ Vsave) {
+                                                             __nv_bfloat16 *__restrict__ Vsave, const DropArgs drop) {
     pdl_wait();
     pdl_trigger();
     __shared__ int idx_of[128];
     __shared__ float vals[128 * RP];
-    shrink_combine_block<RP>(blockIdx.x, blocks, srows, nch, r, part, Vbd, Vsave, idx_of, vals);
+    shrink_combine_block<RP>(blockIdx.x, blocks, srows, nch, r, part, Vbd, Vsave, idx_of, vals, drop);
 }
 
 }  // namespace
@@ -187,7 +201,7 @@ int dec_chunks(int in_f) { return in_f / kChunk > 0 && in_f % kChunk == 0 ? in_f
 
 int launch_shrink_split(const __nv_bfloat16 *X, const SlotDev *slots, const DevBlock *blocks,
                         const DevShortRow *srows, int n_blocks, int in_f, int r, int r_pad, float *part,
-                        __nv_bfloat16 *Vbd, __nv_bfloat16 *Vsave, int *ctr, cudaStream_t st) {
+                        __nv_bfloat16 *Vbd, __nv_bfloat16 *Vsave, int *ctr, const DropArgs &drop, cudaStream_t st) {
     if (n_blocks == 0) return 0;
     const int nch = dec_chunks(in_f);
     dim3 g1(n_blocks, nch);
@@ -196,23 +210,23 @@ int launch_shrink_split(const __nv_bfloat16 *X, const SlotDev *slots, const DevB
         case 16:
             cudaFuncSetAttribute(shrink_partial_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (16 + kRowsPerPass) * kChunk * 2);
-            e = launch_pdl(shrink_partial_kernel<16>, g1, dim3(256), (16 + kRowsPerPass) * kChunk * 2, st, X, slots, blocks, srows, in_f, r, part, ctr, Vbd, Vsave);
+            e = launch_pdl(shrink_partial_kernel<16>, g1, dim3(256), (16 + kRowsPerPass) * kChunk * 2, st, X, slots, blocks, srows, in_f, r, part, ctr, Vbd, Vsave, drop);
             if (e != cudaSuccess || ctr) break;
-            e = launch_pdl(shrink_combine_kernel<16>, dim3(n_blocks), dim3(256), 0, st, blocks, srows, nch, r, part, Vbd, Vsave);
+            e = launch_pdl(shrink_combine_kernel<16>, dim3(n_blocks), dim3(256), 0, st, blocks, srows, nch, r, part, Vbd, Vsave, drop);
             break;
         case 32:
             cudaFuncSetAttribute(shrink_partial_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (32 + kRowsPerPass) * kChunk * 2);
-            e = launch_pdl(shrink_partial_kernel<32>, g1, dim3(256), (32 + kRowsPerPass) * kChunk * 2, st, X, slots, blocks, srows, in_f, r, part, ctr, Vbd, Vsave);
+            e = launch_pdl(shrink_partial_kernel<32>, g1, dim3(256), (32 + kRowsPerPass) * kChunk * 2, st, X, slots, blocks, srows, in_f, r, part, ctr, Vbd, Vsave, drop);
             if (e != cudaSuccess || ctr) break;
-            e = launch_pdl(shrink_combine_kernel<32>, dim3(n_blocks), dim3(256), 0, st, blocks, srows, nch, r, part, Vbd, Vsave);
+            e = launch_pdl(shrink_combine_kernel<32>, dim3(n_blocks), dim3(256), 0, st, blocks, srows, nch, r, part, Vbd, Vsave, drop);
             break;
         case 64:
             cudaFuncSetAttribute(shrink_partial_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (64 + kRowsPerPass) * kChunk * 2);
-            e = launch_pdl(shrink_partial_kernel<64>, g1, dim3(256), (64 + kRowsPerPass) * kChunk * 2, st, X, slots, blocks, srows, in_f, r, part, ctr, Vbd, Vsave);
+            e = launch_pdl(shrink_partial_kernel<64>, g1, dim3(256), (64 + kRowsPerPass) * kChunk * 2, st, X, slots, blocks, srows, in_f, r, part, ctr, Vbd, Vsave, drop);
             if (e != cudaSuccess || ctr) break;
-            e = launch_pdl(shrink_combine_kernel<64>, dim3(n_blocks), dim3(256), 0, st, blocks, srows, nch, r, part, Vbd, Vsave);
+            e = launch_pdl(shrink_combine_kernel<64>, dim3(n_blocks), dim3(256), 0, st, blocks, srows, nch, r, part, Vbd, Vsave, drop);
             break;
         default: return (int)cudaErrorInvalidValue;
     }

@@ -14,6 +14,7 @@
 #include <cuda_runtime.h>
 
 #include "device_types.h"
+#include "dropout.cuh"
 #include "pdl.cuh"
 
 namespace smlm {
@@ -59,7 +60,7 @@ __global__ void __launch_bounds__(256) shrink_short_kernel(const __nv_bfloat16 *
                                                            const DevBlock *__restrict__ blocks,
                                                            const DevShortRow *__restrict__ srows, int in_f, int r,
                                                            __nv_bfloat16 *__restrict__ Vbd,
-                                                           __nv_bfloat16 *__restrict__ Vsave) {
+                                                           __nv_bfloat16 *__restrict__ Vsave, const DropArgs drop) {
     const DevBlock blk = blocks[blockIdx.x];
     const __nv_bfloat16 *A = reinterpret_cast<const __nv_bfloat16 *>(slots[blk.slot].A);
     const int ra = slots[blk.slot].r;
@@ -75,8 +76,13 @@ __global__ void __launch_bounds__(256) shrink_short_kernel(const __nv_bfloat16 *
     for (int rb = 0; rb < blk.nrows; rb += 4) {
         const int nr = min(4, blk.nrows - rb);
         int rows[4];
+        bool dmask[4];   // LoRA dropout on this (FINETUNE) row
 #pragma unroll
-        for (int i = 0; i < 4; ++i) rows[i] = srows[blk.row_begin + rb + min(i, nr - 1)].row;
+        for (int i = 0; i < 4; ++i) {
+            const DevShortRow sr = srows[blk.row_begin + rb + min(i, nr - 1)];
+            rows[i] = sr.row;
+            dmask[i] = drop.on && sr.ft;
+        }
         for (int jg = 0; jg < r; jg += 16) {
             float acc[4][16];
 #pragma unroll
@@ -89,6 +95,7 @@ __global__ void __launch_bounds__(256) shrink_short_kernel(const __nv_bfloat16 *
 #pragma unroll
                 for (int i = 0; i < 4; ++i) {
                     uint4 xu = *reinterpret_cast<const uint4 *>(X + (size_t)rows[i] * in_f + k);
+                    if (dmask[i]) xu = drop_mask8(drop, (uint32_t)rows[i], (uint32_t)k, xu);
                     bf16x8_to_f32(xu, xf[i]);
                 }
 #pragma unroll
@@ -117,7 +124,8 @@ __global__ void __launch_bounds__(256) shrink_short_kernel(const __nv_bfloat16 *
                 float s = 0.f;
 #pragma unroll
                 for (int w = 0; w < 8; ++w) s += part[w][i][j];
-                if (i < nr && jg + j < RP) vbuf[rb + i][jg + j] = s;
+                if (i < nr && jg + j < RP)
+                    vbuf[rb + i][jg + j] = (drop.on && srows[blk.row_begin + rb + i].ft) ? s * drop.scale : s;
             }
             __syncthreads();
         }
@@ -157,9 +165,10 @@ __global__ void __launch_bounds__(256) rows_shrink_kernel(const DevTile *__restr
                                                           const SlotDev *__restrict__ slots,
                                                           const T *__restrict__ X, int in_f, int r,
                                                           float *__restrict__ Vf, T *__restrict__ Vsave,
-                                                          int ft_only_vsave) {
+                                                          int ft_only_vsave, const DropArgs drop) {
     const DevTile t = tiles[blockIdx.x];
     if (t.slot < 0) return;
+    const bool dm = drop.on && (t.flags & kTileFT);   // LoRA dropout: V~ = A (keep * x) / (1 - p)
     const T *A = reinterpret_cast<const T *>(slots[t.slot].A);
     const int ra = slots[t.slot].r;   // rows of A past the adapter's own rank are zero
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -170,7 +179,8 @@ __global__ void __launch_bounds__(256) rows_shrink_kernel(const DevTile *__restr
 #pragma unroll
         for (int j = 0; j < RP; ++j) acc[j] = 0.f;
         for (int k = lane; k < in_f; k += 32) {
-            const float xv = ld_f(x + k);
+            float xv = ld_f(x + k);
+            if (dm && !drop_keep(drop, (uint32_t)row, (uint32_t)k)) xv = 0.f;
 #pragma unroll
             for (int j = 0; j < RP; ++j)
                 if (j < ra) acc[j] = fmaf(ld_f(A + (size_t)j * in_f + k), xv, acc[j]);
@@ -178,6 +188,7 @@ __global__ void __launch_bounds__(256) rows_shrink_kernel(const DevTile *__restr
 #pragma unroll
         for (int j = 0; j < RP; ++j) {
             float s = warp_sum(acc[j]);
+            if (dm) s *= drop.scale;
             if (lane == 0 && j < r) {
                 if (Vf) Vf[(size_t)row * r + j] = s;
                 if (Vsave && (!ft_only_vsave || (t.flags & kTileFT))) st_f(Vsave + (size_t)row * r + j, s);
@@ -250,7 +261,7 @@ template <typename T, int RP>
 __global__ void __launch_bounds__(128) dA_kernel(const DevTile *__restrict__ tiles,
                                                  const GradGroup *__restrict__ groups,
                                                  const T *__restrict__ X, const float *__restrict__ Uf,
-                                                 int in_f, int r, int accumulate) {
+                                                 int in_f, int r, int accumulate, const DropArgs drop) {
     const GradGroup g = groups[blockIdx.y];
     if (!g.dA) return;
     const int k = blockIdx.x * 128 + threadIdx.x;
@@ -270,7 +281,8 @@ __global__ void __launch_bounds__(128) dA_kernel(const DevTile *__restrict__ til
             __syncthreads();
             if (k < in_f) {
                 for (int i = 0; i < nm; ++i) {
-                    const float xv = ld_f(X + (size_t)(t.row0 + m0 + i) * in_f + k);
+                    float xv = ld_f(X + (size_t)(t.row0 + m0 + i) * in_f + k);
+                    if (drop.on && !drop_keep(drop, (uint32_t)(t.row0 + m0 + i), (uint32_t)k)) xv = 0.f;
 #pragma unroll
                     for (int j = 0; j < RP; ++j) acc[j] = fmaf(su[i][j], xv, acc[j]);
                 }
@@ -282,7 +294,8 @@ __global__ void __launch_bounds__(128) dA_kernel(const DevTile *__restrict__ til
         for (int j = 0; j < RP; ++j) {
             if (j < r) {
                 float *p = g.dA + (size_t)j * in_f + k;
-                *p = accumulate ? *p + acc[j] : acc[j];
+                const float v = drop.on ? acc[j] * drop.scale : acc[j];   // x~ = keep * x / (1 - p)
+                *p = accumulate ? *p + v : v;
             }
         }
     }
@@ -367,7 +380,7 @@ __global__ void __launch_bounds__(256) f32_dx_kernel(const DevTile *__restrict__
                                                      const SlotDev *__restrict__ slots,
                                                      const float *__restrict__ dY, const float *__restrict__ W,
                                                      float *__restrict__ dX, const float *__restrict__ Uf,
-                                                     int in_f, int out_f, int r) {
+                                                     int in_f, int out_f, int r, const DropArgs drop) {
     const DevTile t = tiles[blockIdx.x >> 7];
     const int m = blockIdx.x & 127;
     if (m >= t.rows) return;
@@ -383,6 +396,7 @@ __global__ void __launch_bounds__(256) f32_dx_kernel(const DevTile *__restrict__
         if (t.slot >= 0) {
             const float *A = reinterpret_cast<const float *>(slots[t.slot].A);
             for (int j = 0; j < r; ++j) lora = fmaf(Uf[(size_t)row * r + j], A[(size_t)j * in_f + k], lora);
+            if (drop.on) lora *= drop_keep(drop, (uint32_t)row, (uint32_t)k) ? drop.scale : 0.f;   // d dropout(x)/dx
         }
         dX[(size_t)row * in_f + k] = base + t.scale * lora;
     }
@@ -394,12 +408,12 @@ inline int rp_of(int r) { return r <= 16 ? 16 : (r <= 32 ? 32 : 64); }
 
 int launch_shrink_short(const __nv_bfloat16 *X, const SlotDev *slots, const DevBlock *blocks,
                         const DevShortRow *srows, int n_blocks, int in_f, int r, int r_pad,
-                        __nv_bfloat16 *Vbd, __nv_bfloat16 *Vsave, cudaStream_t st) {
+                        __nv_bfloat16 *Vbd, __nv_bfloat16 *Vsave, const DropArgs &drop, cudaStream_t st) {
     if (n_blocks == 0) return 0;
     switch (r_pad) {
-        case 16: shrink_short_kernel<16><<<n_blocks, 256, 0, st>>>(X, slots, blocks, srows, in_f, r, Vbd, Vsave); break;
-        case 32: shrink_short_kernel<32><<<n_blocks, 256, 0, st>>>(X, slots, blocks, srows, in_f, r, Vbd, Vsave); break;
-        case 64: shrink_short_kernel<64><<<n_blocks, 256, 0, st>>>(X, slots, blocks, srows, in_f, r, Vbd, Vsave); break;
+        case 16: shrink_short_kernel<16><<<n_blocks, 256, 0, st>>>(X, slots, blocks, srows, in_f, r, Vbd, Vsave, drop); break;
+        case 32: shrink_short_kernel<32><<<n_blocks, 256, 0, st>>>(X, slots, blocks, srows, in_f, r, Vbd, Vsave, drop); break;
+        case 64: shrink_short_kernel<64><<<n_blocks, 256, 0, st>>>(X, slots, blocks, srows, in_f, r, Vbd, Vsave, drop); break;
         default: return (int)cudaErrorInvalidValue;
     }
     return (int)cudaGetLastError();
@@ -407,20 +421,20 @@ int launch_shrink_short(const __nv_bfloat16 *X, const SlotDev *slots, const DevB
 
 template <typename T>
 int launch_rows_shrink(const DevTile *tiles, int n_tiles, const SlotDev *slots, const T *X, int in_f, int r,
-                       float *Vf, T *Vsave, int ft_only, cudaStream_t st) {
+                       float *Vf, T *Vsave, int ft_only, const DropArgs &drop, cudaStream_t st) {
     if (n_tiles == 0) return 0;
     dim3 grid(n_tiles, 16);
     switch (rp_of(r)) {
-        case 16: rows_shrink_kernel<T, 16><<<grid, 256, 0, st>>>(tiles, slots, X, in_f, r, Vf, Vsave, ft_only); break;
-        case 32: rows_shrink_kernel<T, 32><<<grid, 256, 0, st>>>(tiles, slots, X, in_f, r, Vf, Vsave, ft_only); break;
-        default: rows_shrink_kernel<T, 64><<<grid, 256, 0, st>>>(tiles, slots, X, in_f, r, Vf, Vsave, ft_only); break;
+        case 16: rows_shrink_kernel<T, 16><<<grid, 256, 0, st>>>(tiles, slots, X, in_f, r, Vf, Vsave, ft_only, drop); break;
+        case 32: rows_shrink_kernel<T, 32><<<grid, 256, 0, st>>>(tiles, slots, X, in_f, r, Vf, Vsave, ft_only, drop); break;
+        default: rows_shrink_kernel<T, 64><<<grid, 256, 0, st>>>(tiles, slots, X, in_f, r, Vf, Vsave, ft_only, drop); break;
     }
     return (int)cudaGetLastError();
 }
 template int launch_rows_shrink<float>(const DevTile *, int, const SlotDev *, const float *, int, int, float *,
-                                       float *, int, cudaStream_t);
+                                       float *, int, const DropArgs &, cudaStream_t);
 template int launch_rows_shrink<__nv_bfloat16>(const DevTile *, int, const SlotDev *, const __nv_bfloat16 *, int,
-                                               int, float *, __nv_bfloat16 *, int, cudaStream_t);
+                                               int, float *, __nv_bfloat16 *, int, const DropArgs &, cudaStream_t);
 
 template <typename T>
 int launch_rows_u(const DevTile *tiles, int n_tiles, const SlotDev *slots, const T *dY, int out_f, int r, float *Uf,
@@ -461,34 +475,34 @@ void fill_grad_group(void *dst, int slot, int tile_begin, int n_tiles, int r, fl
 
 template <typename T, typename TV>
 int launch_dadb(const DevTile *tiles, const void *groups, int n_groups, const T *X, const T *dY, const float *Uf,
-                const TV *V, int in_f, int out_f, int r, int accumulate, cudaStream_t st) {
+                const TV *V, int in_f, int out_f, int r, int accumulate, const DropArgs &drop, cudaStream_t st) {
     if (n_groups == 0) return 0;
     const GradGroup *g = reinterpret_cast<const GradGroup *>(groups);
     dim3 ga((in_f + 127) / 128, n_groups), gb((out_f + 127) / 128, n_groups);
     switch (rp_of(r)) {
         case 16:
-            dA_kernel<T, 16><<<ga, 128, 0, st>>>(tiles, g, X, Uf, in_f, r, accumulate);
+            dA_kernel<T, 16><<<ga, 128, 0, st>>>(tiles, g, X, Uf, in_f, r, accumulate, drop);
             dB_kernel<T, TV, 16><<<gb, 128, 0, st>>>(tiles, g, dY, V, out_f, r, accumulate);
             break;
         case 32:
-            dA_kernel<T, 32><<<ga, 128, 0, st>>>(tiles, g, X, Uf, in_f, r, accumulate);
+            dA_kernel<T, 32><<<ga, 128, 0, st>>>(tiles, g, X, Uf, in_f, r, accumulate, drop);
             dB_kernel<T, TV, 32><<<gb, 128, 0, st>>>(tiles, g, dY, V, out_f, r, accumulate);
             break;
         default:
-            dA_kernel<T, 64><<<ga, 128, 0, st>>>(tiles, g, X, Uf, in_f, r, accumulate);
+            dA_kernel<T, 64><<<ga, 128, 0, st>>>(tiles, g, X, Uf, in_f, r, accumulate, drop);
             dB_kernel<T, TV, 64><<<gb, 128, 0, st>>>(tiles, g, dY, V, out_f, r, accumulate);
             break;
     }
     return (int)cudaGetLastError();
 }
 template int launch_dadb<float, float>(const DevTile *, const void *, int, const float *, const float *,
-                                       const float *, const float *, int, int, int, int, cudaStream_t);
+                                       const float *, const float *, int, int, int, int, const DropArgs &, cudaStream_t);
 template int launch_dadb<__nv_bfloat16, __nv_bfloat16>(const DevTile *, const void *, int, const __nv_bfloat16 *,
                                                        const __nv_bfloat16 *, const float *, const __nv_bfloat16 *,
-                                                       int, int, int, int, cudaStream_t);
+                                                       int, int, int, int, const DropArgs &, cudaStream_t);
 template int launch_dadb<__nv_bfloat16, float>(const DevTile *, const void *, int, const __nv_bfloat16 *,
                                                const __nv_bfloat16 *, const float *, const float *, int, int, int,
-                                               int, cudaStream_t);
+                                               int, const DropArgs &, cudaStream_t);
 
 int launch_f32_fwd(const DevTile *tiles, int n_tiles, const SlotDev *slots, const float *X, const float *W, float *Y,
                    const float *Vf, int in_f, int out_f, int r, cudaStream_t st) {
@@ -499,10 +513,10 @@ int launch_f32_fwd(const DevTile *tiles, int n_tiles, const SlotDev *slots, cons
 }
 
 int launch_f32_dx(const DevTile *tiles, int n_tiles, const SlotDev *slots, const float *dY, const float *W, float *dX,
-                  const float *Uf, int in_f, int out_f, int r, cudaStream_t st) {
+                  const float *Uf, int in_f, int out_f, int r, const DropArgs &drop, cudaStream_t st) {
     if (n_tiles == 0) return 0;
     dim3 grid(n_tiles * 128, (in_f + 7) / 8);
-    f32_dx_kernel<<<grid, 256, 0, st>>>(tiles, slots, dY, W, dX, Uf, in_f, out_f, r);
+    f32_dx_kernel<<<grid, 256, 0, st>>>(tiles, slots, dY, W, dX, Uf, in_f, out_f, r, drop);
     return (int)cudaGetLastError();
 }
 

@@ -22,6 +22,7 @@
 #include "device_types.h"
 #include "pdl.cuh"
 #include "sm100.cuh"
+#include "dropout.cuh"
 
 namespace smlm {
 using namespace sm100;
@@ -410,9 +411,9 @@ int launch_impl(const GemmArgs &a, int num_sms, size_t smem, cudaStream_t st) {
 // bytes in flight per SM are what keep the memory system busy), at most 12
 template <int RP, int NH = 1>
 constexpr int tok_stages() {
-    return (int)((232448u - 1280u) / (16384u * NH + ((64u * RP * 2u + 1023u) & ~1023u))) > 12
+    return (int)((232448u - 1536u) / (16384u * NH + ((64u * RP * 2u + 1023u) & ~1023u))) > 12
                ? 12
-               : (int)((232448u - 1280u) / (16384u * NH + ((64u * RP * 2u + 1023u) & ~1023u)));
+               : (int)((232448u - 1536u) / (16384u * NH + ((64u * RP * 2u + 1023u) & ~1023u)));
 }
 
 __device__ __forceinline__ bool tok_item(const TokArgs &a, int w, int &g, int &mt, bool &is_b) {
@@ -450,6 +451,7 @@ __global__ void __launch_bounds__(kThreads, 1) smlm_tok_kernel(const __grid_cons
     auto empty_bar = [&](int s) { return bar + 8u * (ST + s); };
     const uint32_t accf0 = bar + 16u * ST;      // acc_full[2], acc_empty[2]
     const uint32_t tmem_slot = accf0 + 32;
+    auto mask_bar = [&](int s) { return accf0 + 48u + 8u * s; };   // dropout: the X stage is masked
     auto a_addr = [&](int s) { return base + s * kStage; };
     auto b_addr = [&](int s) { return base + s * kStage + kA; };
 
@@ -463,6 +465,7 @@ __global__ void __launch_bounds__(kThreads, 1) smlm_tok_kernel(const __grid_cons
         mbar_init(accf0 + 8, 1);
         mbar_init(accf0 + 16, 128);
         mbar_init(accf0 + 24, 128);
+        for (int s = 0; s < ST; ++s) mbar_init(mask_bar(s), 64);
         fence_mbar_init();
     }
     if (warp == 2) tmem_alloc(tmem_slot, kTm);
@@ -474,7 +477,40 @@ __global__ void __launch_bounds__(kThreads, 1) smlm_tok_kernel(const __grid_cons
     pdl_trigger();
     const int total = args.n_groups * (args.mt_a + args.mt_b);
 
-    if (warp == 0) {
+    if (warp == 2 || warp == 3) {
+        // LoRA dropout (dA items): zero the dropped X elements of each staged token block -- the
+        // forward's mask (same counter-based hash of (seed, token, column)); dA is scaled by
+        // 1/(1-p) in the epilogue
+        if (args.drop.on) {
+            int stage = 0;
+            uint32_t phase = 0;
+            const int tid = threadIdx.x - 64;
+            for (int w = blockIdx.x; w < total; w += gridDim.x) {
+                int g, mt;
+                bool is_b;
+                if (!tok_item(args, w, g, mt, is_b)) continue;
+                const GradGroup grp = args.groups[g];
+                const int m0 = mt * 128 * NH;
+                int nbox = 0;
+#pragma unroll
+                for (int bx = 0; bx < 2 * NH; ++bx) nbox += (m0 + 64 * bx < args.in_f);
+                for (int ti = 0; ti < grp.n_tiles; ++ti) {
+                    const DevTile t = args.tiles[grp.tile_begin + ti];
+                    for (int kb = 0; kb * 64 < t.rows; ++kb) {
+                        if (!is_b) {
+                            mbar_wait(full_bar(stage), phase);
+                            for (int bx = 0; bx < nbox; ++bx)
+                                drop_mask_box_sw128(args.drop, base_ptr + (a_addr(stage) - base) + 8192 * bx, 64,
+                                                    (uint32_t)(t.row0 + 64 * kb), (uint32_t)(m0 + 64 * bx), tid, 64);
+                            fence_proxy_async_smem();
+                            mbar_arrive(mask_bar(stage));
+                        }
+                        if (++stage == ST) { stage = 0; phase ^= 1; }
+                    }
+                }
+            }
+        }
+    } else if (warp == 0) {
         int stage = 0;
         uint32_t phase = 0;
         for (int w = blockIdx.x; w < total; w += gridDim.x) {
@@ -507,7 +543,7 @@ __global__ void __launch_bounds__(kThreads, 1) smlm_tok_kernel(const __grid_cons
         }
     } else if (warp == 1) {
         int stage = 0;
-        uint32_t phase = 0;
+        uint32_t phase = 0, mph = 0;
         uint32_t it = 0;
         constexpr uint32_t idesc = idesc_bf16(128, RP, 1, 1);
         for (int w = blockIdx.x; w < total; w += gridDim.x) {
@@ -524,7 +560,12 @@ __global__ void __launch_bounds__(kThreads, 1) smlm_tok_kernel(const __grid_cons
             for (int ti = 0; ti < grp.n_tiles; ++ti) {
                 const DevTile t = args.tiles[grp.tile_begin + ti];
                 for (int kb = 0; kb * 64 < t.rows; ++kb) {
-                    mbar_wait(full_bar(stage), phase);
+                    if (args.drop.on && !is_b) {
+                        mbar_wait(mask_bar(stage), (mph >> stage) & 1u);
+                        mph ^= 1u << stage;
+                    } else {
+                        mbar_wait(full_bar(stage), phase);
+                    }
                     const int valid = min(64, t.rows - 64 * kb);
                     if (valid < 64) {
                         // zero token rows past the segment end in both 64-column boxes
@@ -595,11 +636,13 @@ __global__ void __launch_bounds__(kThreads, 1) smlm_tok_kernel(const __grid_cons
                     for (int j = 0; j < RP; ++j)
                         if (j < grp.r) p[j] = args.accumulate ? p[j] + __uint_as_float(v[j]) : __uint_as_float(v[j]);
                 } else {
+                    const float ds = args.drop.on ? args.drop.scale : 1.f;   // x~ = keep * x / (1 - p)
 #pragma unroll
                     for (int j = 0; j < RP; ++j)
                         if (j < grp.r) {
                             float *p = grp.dA + (size_t)j * args.in_f + col;
-                            *p = args.accumulate ? *p + __uint_as_float(v[j]) : __uint_as_float(v[j]);
+                            const float dv = ds * __uint_as_float(v[j]);
+                            *p = args.accumulate ? *p + dv : dv;
                         }
                 }
             }
@@ -618,7 +661,7 @@ template <int RP, int NH>
 int launch_tok_impl(const TokArgs &a, int num_sms, cudaStream_t st) {
     auto kern = smlm_tok_kernel<RP, NH>;
     constexpr size_t kStage = 16384 * NH + ((64 * RP * 2 + 1023) & ~1023);
-    const size_t smem = 1024 + tok_stages<RP, NH>() * kStage + 256;
+    const size_t smem = 1024 + tok_stages<RP, NH>() * kStage + 512;
     static bool attr_done = false;
     if (!attr_done) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -648,9 +691,9 @@ template <int RP, int NPJ = 1>
 constexpr uint32_t u_stage_bytes() { return kABytes + ((64u * RP * 2u * NPJ + 1023u) & ~1023u); }
 template <int RP, int NPJ = 1, int KW = 1>
 constexpr int u_stages() {
-    return (int)((232448u - 1280u) / (KW * u_stage_bytes<RP, NPJ>())) > 12
+    return (int)((232448u - 1536u) / (KW * u_stage_bytes<RP, NPJ>())) > 12
                ? 12
-               : (int)((232448u - 1280u) / (KW * u_stage_bytes<RP, NPJ>()));
+               : (int)((232448u - 1536u) / (KW * u_stage_bytes<RP, NPJ>()));
 }
 
 // sUt[tile*128 + m][j] = bf16(s * sum_split part) (zero rows past the segment), split order fixed
@@ -676,6 +719,10 @@ __device__ __forceinline__ void u_reduce_row(const UArgs &args, int item, int m)
                 const float4 v = __ldcg(src + j4);
                 acc[4 * j4] += v.x; acc[4 * j4 + 1] += v.y; acc[4 * j4 + 2] += v.z; acc[4 * j4 + 3] += v.w;
             }
+        }
+        if (args.vf && args.drop.on && (t.flags & kTileFT)) {   // V~ = A_a (keep * x) / (1 - p)
+#pragma unroll
+            for (int j = 0; j < RP; ++j) acc[j] *= args.drop.scale;
         }
     }
     if (args.vf && vsave && (t.flags & kTileFT) && m < t.rows) {
@@ -735,6 +782,7 @@ __global__ void __launch_bounds__(kThreads, 1) smlm_u_kernel(const __grid_consta
     auto empty_bar = [&](int s) { return bar + 8u * (ST + s); };
     const uint32_t accf0 = bar + 16u * ST;   // acc_full[2], acc_empty[2]
     const uint32_t tmem_slot = accf0 + 32;
+    auto mask_bar = [&](int s) { return accf0 + 48u + 8u * s; };   // dropout: the X stage is masked
     auto a_addr = [&](int s, int i = 0) { return base + s * kStg + i * kStg1; };
     auto b_addr = [&](int s, int i = 0) { return base + s * kStg + i * kStg1 + kABytes; };
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -747,6 +795,7 @@ __global__ void __launch_bounds__(kThreads, 1) smlm_u_kernel(const __grid_consta
         mbar_init(accf0 + 8, 1);
         mbar_init(accf0 + 16, 128);
         mbar_init(accf0 + 24, 128);
+        for (int s = 0; s < ST; ++s) mbar_init(mask_bar(s), 64);
         fence_mbar_init();
         tma_prefetch_desc(&args.tmDY);
     }
@@ -764,7 +813,38 @@ __global__ void __launch_bounds__(kThreads, 1) smlm_u_kernel(const __grid_consta
         kb0 = split * q + min(split, rm);
         kb1 = kb0 + q + (split < rm ? 1 : 0);
     };
-    if (warp == 0) {
+    // forward pre-shrink of a FINETUNE tile with LoRA dropout: warps 2-3 zero the dropped X
+    // elements of each staged K-block before the MMA reads it (the 1/(1-p) is applied in the reduce)
+    auto masked_item = [&](int w) {
+        return args.vf && args.drop.on && (args.tiles[args.items[w / args.ksplit]].flags & kTileFT);
+    };
+    if (warp == 2 || warp == 3) {
+        if (args.vf && args.drop.on) {
+            int stage = 0;
+            uint32_t phase = 0, mph = 0;
+            const int tid = threadIdx.x - 64;
+            for (int w = blockIdx.x; w < total; w += gridDim.x) {
+                const int split = w % args.ksplit;
+                int kb0, kb1;
+                kb_range(split, kb0, kb1);
+                const bool mk = masked_item(w);
+                const DevTile t = args.tiles[args.items[w / args.ksplit]];
+                for (int kb = kb0; kb < kb1; kb += KW) {
+                    if (mk) {
+                        const int nb = min(KW, kb1 - kb);
+                        mbar_wait(full_bar(stage), phase);
+                        for (int i = 0; i < nb; ++i)
+                            drop_mask_box_sw128(args.drop, base_ptr + (a_addr(stage, i) - base), 128, (uint32_t)t.row0,
+                                                (uint32_t)(kb + i) * kBK, tid, 64);
+                        fence_proxy_async_smem();
+                        mbar_arrive(mask_bar(stage));
+                        mph ^= 1u << stage;
+                    }
+                    if (++stage == ST) { stage = 0; phase ^= 1; }
+                }
+            }
+        }
+    } else if (warp == 0) {
         int stage = 0;
         uint32_t phase = 0;
         for (int w = blockIdx.x; w < total; w += gridDim.x) {
@@ -800,7 +880,7 @@ __global__ void __launch_bounds__(kThreads, 1) smlm_u_kernel(const __grid_consta
         }
     } else if (warp == 1) {
         int stage = 0;
-        uint32_t phase = 0, it = 0;
+        uint32_t phase = 0, it = 0, mph = 0;
         constexpr uint32_t idesc_u = idesc_bf16(128, RP, 0, 1), idesc_v = idesc_bf16(128, NC, 0, 0);
         const bool vf = args.vf != 0;
         for (int w = blockIdx.x; w < total; w += gridDim.x) {
@@ -812,9 +892,15 @@ __global__ void __launch_bounds__(kThreads, 1) smlm_u_kernel(const __grid_consta
             mbar_wait(accf0 + 16 + 8 * b, (u & 1) ^ 1);
             tc_fence_after();
             uint32_t acc_on = 0;
+            const bool mk = masked_item(w);
             for (int kb = kb0; kb < kb1; kb += KW) {
                 const int nb = min(KW, kb1 - kb);
-                mbar_wait(full_bar(stage), phase);
+                if (mk) {
+                    mbar_wait(mask_bar(stage), (mph >> stage) & 1u);
+                    mph ^= 1u << stage;
+                } else {
+                    mbar_wait(full_bar(stage), phase);
+                }
                 tc_fence_after();
                 if (lane == 0) {
                     for (int i = 0; i < nb; ++i) {
@@ -894,7 +980,7 @@ template <int RP, int NPJ = 1, int KW = 2>
 int launch_u_impl(const UArgs &a, int num_sms, cudaStream_t st) {
     auto kern = smlm_u_kernel<RP, NPJ, KW>;
     constexpr size_t kStg = KW * u_stage_bytes<RP, NPJ>();
-    const size_t smem = 1024 + u_stages<RP, NPJ, KW>() * kStg + 256;
+    const size_t smem = 1024 + u_stages<RP, NPJ, KW>() * kStg + 512;
     static bool attr_done = false;
     if (!attr_done) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

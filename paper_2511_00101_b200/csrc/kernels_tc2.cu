@@ -18,9 +18,13 @@
 // n-tiles of all projections form one persistent work list (no per-projection wave tail).
 // Only the leader CTA (rank 0) issues MMAs; completions are multicast to both CTAs; two 256-column
 // TMEM accumulators let the epilogue of item i overlap the main loop of item i+1.
+// Backward with LoRA dropout (DESIGN R13): dx = W^T dy + keep * scale * (s A_a^T u) -- the mask
+// multiplies only the LoRA term, so the expand blocks accumulate into the SECOND accumulator and
+// the epilogue combines the two with the keep mask (one item in flight: no epilogue overlap).
 #include <cuda_runtime.h>
 
 #include "device_types.h"
+#include "dropout.cuh"
 #include "pdl.cuh"
 #include "sm100.cuh"
 
@@ -123,6 +127,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
     const int n_clusters = gridDim.x / 2;
     const int cid = blockIdx.x / 2;
     const int total = args.n_pairs * args.n_nt;
+    const bool drop = BWD && args.drop.on;
 
     if (warp == 0) {
         // ========================= TMA producer (both CTAs) =========================
@@ -216,9 +221,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
             decode_pair(w, args.n_pairs, args.n_nt, args.group_m, pi, gnt);
             const DevPair pr = args.pairs[pi];
             const int nkb = args.proj[proj_of(args, gnt)].K / kBK;
-            const uint32_t b = it & 1, u = it >> 1;
+            const uint32_t b = drop ? 0u : (it & 1), u = drop ? it : (it >> 1);
             const uint32_t acc = acc_col(b);
             mbar_wait(acc_empty0 + 8 * b, (u & 1) ^ 1);
+            if (drop) mbar_wait(acc_empty0 + 8, (u & 1) ^ 1);   // the LoRA accumulator
             tc_fence_after();
             for (int kb = 0; kb < nkb; ++kb) {
                 mbar_wait(full_bar(stage), phase);
@@ -244,10 +250,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
                     const uint32_t ab = a_addr(stage), bb = b_addr(stage);
 #pragma unroll
                     for (int kk = 0; kk < RP / 16; ++kk)
-                        mma2_bf16(acc, smem_desc(ab + 32u * kk, 16, 8u * RB, kSwR),
+                        mma2_bf16(drop ? acc_col(1) : acc, smem_desc(ab + 32u * kk, 16, 8u * RB, kSwR),
                                   BWD ? smem_desc(bb + 2048u * kk, (uint32_t)RP * 128u, 1024, kSw128)
                                       : smem_desc(bb + 32u * kk, 16, 8u * RB, kSwR),
-                                  idesc, 1);
+                                  idesc, (!drop || j > 0 || kk > 0) ? 1u : 0u);
                     mma2_commit_mc(empty_bar(stage));
                 }
                 __syncwarp();
@@ -270,11 +276,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
             const int p = proj_of(args, gnt);
             const Gemm2Proj &P = args.proj[p];
             const DevHalf mine = args.pairs[pi].h[rank];
+            const bool dl = drop && n_expand(args.pairs[pi]) > 0;   // a LoRA accumulator to combine
             const int n0 = (gnt - P.nt0) * kBN;
             const bool row_ok = m < mine.rows;
             const int row = mine.row0 + m;
             __nv_bfloat16 *Y = reinterpret_cast<__nv_bfloat16 *>(P.Y);
-            const uint32_t b = it & 1, u = it >> 1;
+            const uint32_t b = drop ? 0u : (it & 1), u = drop ? it : (it >> 1);
             mbar_wait(acc_full0 + 8 * b, u & 1);
             tc_fence_after();
 #pragma unroll 1
@@ -283,6 +290,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
                 tmem_ld16(acc_col(b) + lane_base + 16u * c, r);
                 tmem_wait_ld();
                 const int col = n0 + 16 * c;
+                if (dl) {
+                    uint32_t l[16];
+                    tmem_ld16(acc_col(1) + lane_base + 16u * c, l);
+                    tmem_wait_ld();
+                    if (row_ok) {
+#pragma unroll
+                        for (int e = 0; e < 16; e += 2) {
+                            const uint32_t kp = drop_keep2(args.drop, (uint32_t)row, (uint32_t)(col + e));
+                            r[e] = __float_as_uint(__uint_as_float(r[e]) +
+                                                   ((kp & 1u) ? args.drop.scale * __uint_as_float(l[e]) : 0.f));
+                            r[e + 1] = __float_as_uint(__uint_as_float(r[e + 1]) +
+                                                       ((kp & 2u) ? args.drop.scale * __uint_as_float(l[e + 1]) : 0.f));
+                        }
+                    }
+                }
                 if (row_ok && col < P.N) {
                     uint4 *dst = reinterpret_cast<uint4 *>(Y + (size_t)row * P.N + col);
 #pragma unroll
@@ -298,6 +320,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
             }
             tc_fence_before();
             mbar_arrive_cluster(acc_empty_l + 8 * b);
+            if (drop) mbar_arrive_cluster(acc_empty_l + 8);
             ++it;
         }
     }

@@ -28,6 +28,8 @@ int build_plan(const smlm_batch *b, int capacity, const uint8_t *slot_ok, const 
     }
     if (!b->seg_offsets || !b->seg_slot || !b->seg_mode)
         return fail(msg, SMLM_E_INVALID, "segment arrays must be non-NULL");
+    if (!(b->dropout_p >= 0.0f && b->dropout_p < 1.0f))
+        return fail(msg, SMLM_E_INVALID, "dropout_p must be in [0, 1)");
     const int32_t *off = b->seg_offsets;
     if (off[0] != 0) return fail(msg, SMLM_E_INVALID, "seg_offsets[0] must be 0");
     if (off[b->G] != b->S) return fail(msg, SMLM_E_INVALID, "seg_offsets[G] must equal S");

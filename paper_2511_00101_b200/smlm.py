@@ -14,8 +14,10 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 # the release library; SMLM_MEASURE_LIB=1 loads the -DSMLM_MEASURE build (build.py --measure:
-# phase timestamps / host timing for the scripts under scripts/, same kernels and results)
-LIB_PATH = os.path.join(_HERE, "libsmlm_measure.so" if os.environ.get("SMLM_MEASURE_LIB") == "1" else "libsmlm.so")
+# phase timestamps / host timing for the scripts under scripts/, same kernels and results);
+# SMLM_LIB_PATH loads another build of the same C ABI (same-box A/B of two library versions)
+LIB_PATH = os.environ.get("SMLM_LIB_PATH") or os.path.join(
+    _HERE, "libsmlm_measure.so" if os.environ.get("SMLM_MEASURE_LIB") == "1" else "libsmlm.so")
 
 SMLM_OK, SMLM_E_INVALID, SMLM_E_SHAPE, SMLM_E_SLOT, SMLM_E_CAPACITY, SMLM_E_CUDA, SMLM_E_UNSUPPORTED, \
     SMLM_E_WORKSPACE = range(8)
@@ -42,7 +44,8 @@ class SmlmError(RuntimeError):
 
 class smlm_batch(ctypes.Structure):
     _fields_ = [("S", ctypes.c_int), ("G", ctypes.c_int), ("seg_offsets", ctypes.c_void_p),
-                ("seg_slot", ctypes.c_void_p), ("seg_mode", ctypes.c_void_p), ("seg_scale", ctypes.c_void_p)]
+                ("seg_slot", ctypes.c_void_p), ("seg_mode", ctypes.c_void_p), ("seg_scale", ctypes.c_void_p),
+                ("dropout_p", ctypes.c_float), ("dropout_seed", ctypes.c_uint64)]
 
 
 def _load():
@@ -112,18 +115,23 @@ def _stream(stream, device) -> int:
 class Batch:
     """Host-side segment arrays kept alive for the duration of the calls."""
 
-    def __init__(self, offsets, slots, modes, seg_scale=None):
+    def __init__(self, offsets, slots, modes, seg_scale=None, dropout_p=0.0, dropout_seed=0):
         self.offsets = np.ascontiguousarray(offsets, np.int32)
         self.slots = np.ascontiguousarray(slots, np.int32)
         self.modes = np.ascontiguousarray(modes, np.int8)
         self.seg_scale = None if seg_scale is None else np.ascontiguousarray(seg_scale, np.float32)
         self.c = smlm_batch(int(self.offsets[-1]) if len(self.offsets) else 0, len(self.slots),
                             self.offsets.ctypes.data, self.slots.ctypes.data, self.modes.ctypes.data,
-                            None if self.seg_scale is None else self.seg_scale.ctypes.data)
+                            None if self.seg_scale is None else self.seg_scale.ctypes.data,
+                            float(dropout_p), int(dropout_seed) & 0xFFFFFFFFFFFFFFFF)
+
+    def with_dropout(self, p: float, seed: int) -> "Batch":
+        """The same segments with LoRA dropout p on the fine-tune rows and mask seed `seed`."""
+        return Batch(self.offsets, self.slots, self.modes, self.seg_scale, p, seed)
 
     @classmethod
-    def from_synth(cls, b):
-        return cls(b.offsets, b.slots, b.modes, b.seg_scale)
+    def from_synth(cls, b, dropout_p=0.0, dropout_seed=0):
+        return cls(b.offsets, b.slots, b.modes, b.seg_scale, dropout_p, dropout_seed)
 
     @property
     def S(self):

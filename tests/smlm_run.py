@@ -18,7 +18,8 @@ class GpuResult:
 
 def run_smlm(batch, w, X, dY, dtype=None, backward=True, w_null=False, vsave=True, want_dx=True,
              grads=None, l_long=None, accumulate=False, dA0=None, dB0=None, base_in=None, device=0,
-             options=None):
+             options=None, dropout=None):
+    """dropout: (p, seed) -- LoRA dropout of the fine-tune rows (smlm_batch.dropout_p / _seed)."""
     from paper_2511_00101_b200 import smlm as S
     dev = torch.device("cuda", device)
     tdt = X.dtype
@@ -60,7 +61,7 @@ def run_smlm(batch, w, X, dY, dtype=None, backward=True, w_null=False, vsave=Tru
                 pool.set_grad(i, guards[0][i][:ra * in_f].view(ra, in_f), guards[1][i][:out_f * ra].view(out_f, ra))
             else:
                 pool.set_grad(i, dA[i], dB[i])
-    b = S.Batch.from_synth(batch)
+    b = S.Batch.from_synth(batch) if dropout is None else S.Batch.from_synth(batch, dropout[0], dropout[1])
     Xd = X.to(dev).contiguous()
     Wd = w.W.to(dev).contiguous()
     if w_null:
