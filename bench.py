@@ -228,6 +228,23 @@ class Workload:
                 comm(self.buckets[L])
 
 
+    def use_peer_reduce(self, dist):
+        """Fused cross-rank reduction: every layer bucket becomes a view of this rank's
+        slot in a dp.PeerReduce staging buffer; every pool fans its dA/dB out to the peers."""
+        from paper_2511_00101_b200.dp import PeerReduce
+        sizes = [lb.flat.numel() for lb in self.buckets]
+        self._peer_off = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
+        self.peer = PeerReduce(dist, int(self._peer_off[-1]), self.dev)
+        self.peer.set_fanout([self.layers[L][p]["pool"] for L in range(N_LAYERS) for p in synth.PROJECTIONS])
+        self.bind_peer_slots(0)
+        return self.peer
+
+    def bind_peer_slots(self, parity):
+        slot = self.peer.slot(parity)
+        for L, lb in enumerate(self.buckets):
+            lb.rebind(slot[int(self._peer_off[L]):int(self._peer_off[L + 1])], self.layers[L])
+
+
 class LayerBucket:
     """One flat fp32 buffer per layer holding the fine-tune adapters' dA/dB of all 7 projections
     (one all-reduce bucket per layer, 20 MiB at C4/C5); each projection's grads are
@@ -238,6 +255,13 @@ class LayerBucket:
         n = sum(len(self.slots) * r * (i + o) for i, o in (synth.PROJ_SHAPES[p] for p in synth.PROJECTIONS))
         self.flat = torch.zeros(n, dtype=torch.float32, device=dev)
         self.r, self.off, self.views = r, 0, {}
+
+    def rebind(self, flat, layer):
+        """Move the bucket onto another buffer (e.g. a peer-reduction staging slot) and re-bind."""
+        self.flat, self.off = flat, 0
+        for p in synth.PROJECTIONS:
+            self.bind(p, layer[p]["pool"])
+            layer[p]["grad"] = self.views[p]
 
     def bind(self, p, pool):
         in_f, out_f = synth.PROJ_SHAPES[p]
@@ -362,6 +386,9 @@ def main():
     ap.add_argument("--dist-backend", default="nccl", help="nccl (production); gloo only to exercise the N>1 "
                     "path on a single-GPU box")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--dp-reduce", default="fanout", choices=["fanout", "nccl"],
+                    help="N > 1: fused peer-memory fan-out of dA/dB from the contraction kernel (SURVEY f3) or "
+                         "an NCCL all-reduce per layer bucket")
     ap.add_argument("--no-kernel-timing", action="store_true",
                     help="skip the per-kernel CUDA events (A/B check of their overhead)")
     ap.add_argument("--oracle-rows", type=int, default=48, help="cpu_baseline sample rows, all host cores")
@@ -419,16 +446,33 @@ def main():
     wl = Workload(k, rank, dev)
     stream = torch.cuda.current_stream(dev)
     comm = None
+    peer = None
+    dp_reduce = None
     if dist is not None:
-        allreduce = AllReduce(dist, dev)
+        dp_reduce = args.dp_reduce
+        if dp_reduce == "fanout":
+            # the dA/dB contraction stores every gradient into its slot of every peer's
+            # staging buffer over NVLink; the step ends when all ranks' slots have arrived
+            try:
+                peer = wl.use_peer_reduce(dist)
+            except Exception as ex:   # e.g. no peer access between the devices: NCCL instead
+                print(f"[bench] fan-out reduction unavailable ({ex!r:.120}); using NCCL all-reduce", file=sys.stderr)
+                dp_reduce = "nccl"
+        if dp_reduce == "nccl":
+            allreduce = AllReduce(dist, dev)
 
-        def comm(bucket):
-            allreduce(bucket, stream)
+            def comm(bucket):
+                allreduce(bucket, stream)
 
     def one_step(i):
+        if peer is not None:
+            wl.bind_peer_slots(i % 2)
         wl.step(stream, comm)
         if comm is not None:
             allreduce.join(stream)
+        if peer is not None:
+            peer.signal(stream)
+            peer.wait(stream)
 
     for i in range(args.warmup):
         one_step(i)
@@ -570,8 +614,12 @@ def main():
                                 f"(416 MiB each, {N_LAYERS} per step)",
                           "step": f"forward of the 7 projections of layers 0..{N_LAYERS - 1}, then the fine-tune "
                                   f"backward of layers {N_LAYERS - 1}..0"
-                                  + (" with one NCCL all-reduce of the layer's fine-tune dA/dB (20 MiB fp32 bucket) "
-                                     "per layer, overlapping the next layer's backward" if n > 1 else ""),
+                                  + ((" with one NCCL all-reduce of the layer's fine-tune dA/dB (20 MiB fp32 bucket) "
+                                      "per layer, overlapping the next layer's backward") if dp_reduce == "nccl" else
+                                     (" with the fine-tune dA/dB stored into every peer's staging slot by the dA/dB "
+                                      "contraction kernel itself (NVLink peer memory), then a device-side wait for all "
+                                      "ranks' slots") if dp_reduce == "fanout" else ""),
+                          "dp_reduce": dp_reduce,
                           "tokens_per_s": "rows x layers / step time (per-layer throughput, SURVEY §8(d))"},
                "step_stats": step_stats,
                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
@@ -649,6 +697,8 @@ def run_e2e(wl, stream, steps, n, dist):
 
     def compute(i):
         b = i % 2
+        if getattr(wl, "peer", None) is not None:
+            wl.bind_peer_slots(wl.peer.steps % 2)
         stream.wait_event(in_ready[b])
         if out_done[b] is not None:
             stream.wait_event(out_done[b])
@@ -678,13 +728,16 @@ def run_e2e(wl, stream, steps, n, dist):
             ev = torch.cuda.Event()
             ev.record(wl._s2)
             stream.wait_event(ev)
-            if dist is not None:
+            if dist is not None and getattr(wl, "peer", None) is None:
                 dist.all_reduce(wl.buckets[L].flat, op=dist.ReduceOp.SUM)
             ev = torch.cuda.Event()
             ev.record(stream)
             s_d2h.wait_event(ev)
             with torch.cuda.stream(s_d2h):
                 hG[L].copy_(wl.buckets[L].flat, non_blocking=True)
+        if getattr(wl, "peer", None) is not None:
+            wl.peer.signal(stream)
+            wl.peer.wait(stream)
         ev = torch.cuda.Event(enable_timing=diag is not None)
         ev.record(stream)
         in_free[b] = ev

@@ -276,6 +276,48 @@ SMLM_API int smlm_adamw_step(float *param, float *exp_avg, float *exp_avg_sq, fl
                              float weight_decay, float grad_scale, float max_grad_norm, int zero_grad,
                              void *ws, size_t ws_bytes, void *stream);
 
+/*
+ * Fused cross-rank reduction of the fine-tune gradients + optimizer (BASELINE.json
+ * north_star "the fine-tuning LoRA gradients are all-reduced ... over NVLink"; PAPER.md P:422 masking
+ * = only the trained adapters' gradients are reduced).  Data-parallel ranks replicate the adapters;
+ * rank r of N keeps a STAGING buffer of N gradient slots [N][n] fp32 (slot q = rank q's gradient,
+ * same flat layout), binds its pools' dA/dB to views of ITS slot r, and maps the peers' staging
+ * buffers over NVLink with the IPC calls below.  Then:
+ *   smlm_pool_set_grad_fanout(pool, N - 1, deltas): the dA/dB contraction kernel stores every
+ *     gradient value it writes at p AND at p + deltas[q] -- slot r of peer q's buffer (delta =
+ *     peer base - own base, bytes, a multiple of 4) -- so the transfer overlaps the contraction
+ *     tile by tile (plain stores: each rank is the only writer of its slot everywhere);
+ *   smlm_fanout_signal(N, ready, stream): after the step's backward (stream order), a system-scope
+ *     release increment of every rank's ready counter (an int in each rank's device memory,
+ *     zero-initialised, peer-mapped; ready[q] = rank q's counter as mapped here);
+ *   smlm_adamw_step_reduce(...): the AdamW step of smlm_adamw_step on g = sum_{q < n_slots} of
+ *     grad_slots[q * slot_stride + i] IN RANK ORDER (deterministic, the same on every rank, so the
+ *     replicas stay bit-identical), after waiting until *ready >= ready_target (= N x steps so far);
+ *     zero_grad clears only slot own_slot.
+ * Use two staging buffers alternating by step parity (a fast peer may write step t + 1 while this
+ * rank still reads step t); the wait itself keeps ranks within one step of each other.
+ * Errors: SMLM_E_INVALID (NULL, counts outside [1, 8], misaligned deltas / strides), SMLM_E_CUDA
+ * (IPC failures), SMLM_E_UNSUPPORTED (fan-out on an fp32 pool with gradients).
+ */
+#define SMLM_IPC_HANDLE_BYTES 64
+/* handle of the allocation that contains dev_ptr, and dev_ptr's byte offset in it; open returns the
+ * allocation BASE in this process (add the offset); close unmaps it */
+SMLM_API int smlm_ipc_get_handle(const void *dev_ptr, void *handle_out /* SMLM_IPC_HANDLE_BYTES, host */,
+                                 uint64_t *offset_out);
+SMLM_API int smlm_ipc_open_handle(const void *handle /* host */, void **base_out);
+SMLM_API int smlm_ipc_close_handle(void *dev_ptr);
+SMLM_API int smlm_pool_set_grad_fanout(smlm_pool pool, int n_peers, const int64_t *byte_deltas);
+SMLM_API int smlm_fanout_signal(int n_ranks, int *const *ready_counters, void *stream);
+/* the stream waits (device-side) until *ready >= target: every rank's slots of the step are in
+ * this rank's staging buffer (the all-reduce post-condition; the sum itself is folded into the
+ * consumer, e.g. smlm_adamw_step_reduce) */
+SMLM_API int smlm_fanout_wait(const int *ready, int target, void *stream);
+SMLM_API int smlm_adamw_step_reduce(float *param, float *exp_avg, float *exp_avg_sq, float *grad_slots, int n_slots,
+                                   size_t slot_stride, int own_slot, void *param_bf16, size_t n, int step, float lr,
+                                   float beta1, float beta2, float eps, float weight_decay, float grad_scale,
+                                   float max_grad_norm, int zero_grad, const int *ready, int ready_target, void *ws,
+                                   size_t ws_bytes, void *stream);
+
 SMLM_API const char *smlm_status_string(int status);
 SMLM_API const char *smlm_last_error(void);
 

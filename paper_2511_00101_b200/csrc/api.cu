@@ -50,7 +50,9 @@ int dec3_max_clusters(int r_pad);
 int launch_dec3(const Dec3Args &a, const Dec3Inline &in, int clusters, cudaStream_t st);
 int launch_plan_copy(void *dst, const void *src, size_t n, cudaStream_t st);
 int adamw_grid(int num_sms, size_t n);
-int launch_adamw_sumsq(const float *g, size_t n, float gscale, float *partial, int grid, cudaStream_t st);
+int launch_adamw_sumsq(const AdamwArgs &a, float *partial, int grid, cudaStream_t st);
+int launch_fanout_signal(const FanoutFlags &f, cudaStream_t st);
+int launch_fanout_wait(const int *ready, int target, cudaStream_t st);
 int launch_adamw_step(const AdamwArgs &a, int grid, cudaStream_t st);
 int launch_shrink_split(const __nv_bfloat16 *X, const SlotDev *slots, const DevBlock *blocks,
                         const DevShortRow *srows, int n_blocks, int in_f, int r, int r_pad, float *part,
@@ -270,6 +272,7 @@ struct smlm_pool_s {
     int dec_kernel = 1; // pure decode batches take the single-launch decode kernel (SMLM_OPT_DECODE_KERNEL)
     int dec_ksplit = 0; // decode W split-K factor, 0 = automatic (SMLM_OPT_DEC_KSPLIT)
     int dec_coop = 0;   // cooperative decode launches (SMLM_OPT_DEC_COOPERATIVE)
+    std::vector<long long> fanout;   // dA/dB also stored at p + delta (peer ranks' staging slots, f3)
     int num_sms = 148;
     std::vector<SlotHost> slots;
     std::vector<uint8_t> ok;
@@ -958,15 +961,20 @@ size_t smlm_adamw_workspace_size(void) {
     return (size_t)sms * 8 * sizeof(float);
 }
 
-int smlm_adamw_step(float *param, float *exp_avg, float *exp_avg_sq, float *grad, void *param_bf16, size_t n,
-                    int step, float lr, float beta1, float beta2, float eps, float weight_decay, float grad_scale,
-                    float max_grad_norm, int zero_grad, void *ws, size_t ws_bytes, void *stream) {
+static int adamw_impl(float *param, float *exp_avg, float *exp_avg_sq, float *grad, int n_slots, size_t slot_stride,
+                      int own_slot, void *param_bf16, size_t n, int step, float lr, float beta1, float beta2,
+                      float eps, float weight_decay, float grad_scale, float max_grad_norm, int zero_grad,
+                      const int *ready, int ready_target, void *ws, size_t ws_bytes, void *stream) {
     if (n == 0) return SMLM_OK;
     if (!param || !exp_avg || !exp_avg_sq || !grad) return set_err(SMLM_E_INVALID, "adamw: null buffer");
     if (step < 1) return set_err(SMLM_E_INVALID, "adamw: step must be >= 1");
     if (!(lr >= 0.f) || !(beta1 >= 0.f && beta1 < 1.f) || !(beta2 >= 0.f && beta2 < 1.f) || !(eps > 0.f) ||
         !(weight_decay >= 0.f) || !std::isfinite(grad_scale) || !std::isfinite(max_grad_norm))
         return set_err(SMLM_E_INVALID, "adamw: hyper-parameter out of range");
+    if (n_slots < 1 || n_slots > kMaxRanks || own_slot < 0 || own_slot >= n_slots ||
+        (n_slots > 1 && (slot_stride < n || slot_stride % 4)))
+        return set_err(SMLM_E_INVALID, "adamw: 1 <= n_slots <= 8, 0 <= own_slot < n_slots, slot_stride >= n and a "
+                                       "multiple of 4");
     auto al = [](const void *q, size_t b) { return (reinterpret_cast<uintptr_t>(q) % b) == 0; };
     if (!al(param, 16) || !al(exp_avg, 16) || !al(exp_avg_sq, 16) || !al(grad, 16) || (param_bf16 && !al(param_bf16, 8)))
         return set_err(SMLM_E_INVALID, "adamw: fp32 buffers must be 16-byte and the bf16 copy 8-byte aligned");
@@ -975,6 +983,7 @@ int smlm_adamw_step(float *param, float *exp_avg, float *exp_avg_sq, float *grad
     cudaStream_t st = (cudaStream_t)stream;
     const int grid = adamw_grid(sms, n);
     AdamwArgs a;
+    memset(&a, 0, sizeof(a));
     a.p = param;
     a.m = exp_avg;
     a.v = exp_avg_sq;
@@ -992,11 +1001,16 @@ int smlm_adamw_step(float *param, float *exp_avg, float *exp_avg_sq, float *grad
     a.zero_grad = zero_grad ? 1 : 0;
     a.partial = nullptr;
     a.n_partial = 0;
+    a.n_slots = n_slots;
+    a.slot_stride = n_slots > 1 ? slot_stride : 0;
+    a.zero_slot = own_slot;
+    a.ready = ready;
+    a.ready_target = ready_target;
     if (max_grad_norm > 0.f) {
         if (!ws || !al(ws, 4) || ws_bytes < (size_t)grid * sizeof(float))
             return set_err(SMLM_E_WORKSPACE, "adamw: clipping needs smlm_adamw_workspace_size() bytes of workspace");
         ProfScope ps(4, st);
-        CKL(launch_adamw_sumsq(grad, n, grad_scale, reinterpret_cast<float *>(ws), grid, st), 1);
+        CKL(launch_adamw_sumsq(a, reinterpret_cast<float *>(ws), grid, st), 1);
         a.partial = reinterpret_cast<const float *>(ws);
         a.n_partial = grid;
     }
@@ -1004,6 +1018,90 @@ int smlm_adamw_step(float *param, float *exp_avg, float *exp_avg_sq, float *grad
         ProfScope ps(4, st);
         CKL(launch_adamw_step(a, grid, st), 1);
     }
+    return SMLM_OK;
+}
+
+int smlm_adamw_step(float *param, float *exp_avg, float *exp_avg_sq, float *grad, void *param_bf16, size_t n,
+                    int step, float lr, float beta1, float beta2, float eps, float weight_decay, float grad_scale,
+                    float max_grad_norm, int zero_grad, void *ws, size_t ws_bytes, void *stream) {
+    return adamw_impl(param, exp_avg, exp_avg_sq, grad, 1, 0, 0, param_bf16, n, step, lr, beta1, beta2, eps,
+                      weight_decay, grad_scale, max_grad_norm, zero_grad, nullptr, 0, ws, ws_bytes, stream);
+}
+
+int smlm_adamw_step_reduce(float *param, float *exp_avg, float *exp_avg_sq, float *grad_slots, int n_slots,
+                           size_t slot_stride, int own_slot, void *param_bf16, size_t n, int step, float lr,
+                           float beta1, float beta2, float eps, float weight_decay, float grad_scale,
+                           float max_grad_norm, int zero_grad, const int *ready, int ready_target, void *ws,
+                           size_t ws_bytes, void *stream) {
+    return adamw_impl(param, exp_avg, exp_avg_sq, grad_slots, n_slots, slot_stride, own_slot, param_bf16, n, step, lr,
+                      beta1, beta2, eps, weight_decay, grad_scale, max_grad_norm, zero_grad, ready, ready_target, ws,
+                      ws_bytes, stream);
+}
+
+// ---- fused cross-rank reduction plumbing: IPC mappings, fan-out, completion ----
+int smlm_ipc_get_handle(const void *dev_ptr, void *handle_out, uint64_t *offset_out) {
+    if (!dev_ptr || !handle_out || !offset_out) return set_err(SMLM_E_INVALID, "NULL argument");
+    // the handle names the whole allocation (e.g. a caching-allocator block): report ptr's offset
+    static PFN_cuMemGetAddressRange_v3020 range = nullptr;
+    if (!range) {
+        void *fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn)
+            return set_err(SMLM_E_CUDA, "cuMemGetAddressRange entry point unavailable");
+        range = reinterpret_cast<PFN_cuMemGetAddressRange_v3020>(fn);
+    }
+    CUdeviceptr base = 0;
+    size_t size = 0;
+    if (range(&base, &size, (CUdeviceptr)dev_ptr) != CUDA_SUCCESS)
+        return set_err(SMLM_E_CUDA, "cuMemGetAddressRange failed");
+    cudaIpcMemHandle_t h;
+    CK(cudaIpcGetMemHandle(&h, reinterpret_cast<void *>(base)));
+    static_assert(sizeof(h) == SMLM_IPC_HANDLE_BYTES, "IPC handle size");
+    memcpy(handle_out, &h, sizeof(h));
+    *offset_out = (uint64_t)((CUdeviceptr)dev_ptr - base);
+    return SMLM_OK;
+}
+
+int smlm_ipc_open_handle(const void *handle, void **dev_ptr_out) {   // returns the allocation base
+    if (!handle || !dev_ptr_out) return set_err(SMLM_E_INVALID, "NULL argument");
+    cudaIpcMemHandle_t h;
+    memcpy(&h, handle, sizeof(h));
+    CK(cudaIpcOpenMemHandle(dev_ptr_out, h, cudaIpcMemLazyEnablePeerAccess));
+    return SMLM_OK;
+}
+
+int smlm_ipc_close_handle(void *dev_ptr) {
+    if (!dev_ptr) return SMLM_OK;
+    CK(cudaIpcCloseMemHandle(dev_ptr));
+    return SMLM_OK;
+}
+
+int smlm_pool_set_grad_fanout(smlm_pool p, int n_peers, const int64_t *byte_deltas) {
+    if (!p) return set_err(SMLM_E_INVALID, "pool is NULL");
+    if (n_peers < 0 || n_peers > kMaxRanks - 1 || (n_peers > 0 && !byte_deltas))
+        return set_err(SMLM_E_INVALID, "fan-out: 0 <= n_peers <= 7 byte deltas");
+    for (int q = 0; q < n_peers; ++q)
+        if (byte_deltas[q] % 4) return set_err(SMLM_E_INVALID, "fan-out deltas must be multiples of 4 bytes");
+    p->fanout.assign(byte_deltas, byte_deltas + n_peers);
+    return SMLM_OK;
+}
+
+int smlm_fanout_signal(int n_ranks, int *const *ready_counters, void *stream) {
+    if (n_ranks < 1 || n_ranks > kMaxRanks || !ready_counters) return set_err(SMLM_E_INVALID, "1 <= n_ranks <= 8");
+    FanoutFlags f;
+    memset(&f, 0, sizeof(f));
+    f.n = n_ranks;
+    for (int q = 0; q < n_ranks; ++q) {
+        if (!ready_counters[q]) return set_err(SMLM_E_INVALID, "NULL ready counter");
+        f.flag[q] = ready_counters[q];
+    }
+    CKL(launch_fanout_signal(f, (cudaStream_t)stream), 1);
+    return SMLM_OK;
+}
+
+int smlm_fanout_wait(const int *ready, int target, void *stream) {
+    if (!ready) return set_err(SMLM_E_INVALID, "NULL ready counter");
+    CKL(launch_fanout_wait(ready, target, (cudaStream_t)stream), 1);
     return SMLM_OK;
 }
 
@@ -1666,6 +1764,8 @@ static int bwd_tok(smlm_pool p, const smlm_batch *b, const void *X, const void *
     ta.mt_b = (p->out + 128 * ta.nh - 1) / (128 * ta.nh);
     ta.accumulate = accumulate ? 1 : 0;
     ta.drop = make_drop(b, p->in);
+    ta.n_fanout = (int)p->fanout.size();
+    for (int q = 0; q < ta.n_fanout; ++q) ta.fanout_delta[q] = p->fanout[q];
     CKL(launch_tok(ta, p->num_sms, st), 1);
     return SMLM_OK;
 }
@@ -1691,6 +1791,8 @@ int smlm_backward(smlm_pool p, const smlm_batch *b, const void *X, const void *W
     if ((rc = bwd_prepare(p, b, plan, L, dY, V_save, dX != nullptr, wsb, uctr, st, B))) return rc;
 
     if (p->dtype == SMLM_FP32) {
+        if (!p->fanout.empty() && B.n_grad)
+            return set_err(SMLM_E_UNSUPPORTED, "gradient fan-out (smlm_pool_set_grad_fanout) is a bf16-path feature");
         CKL(launch_rows_u<float>(B.tiles, B.nt, p->d_slots, (const float *)dY, p->out, p->r, B.Uf, nullptr, p->r_pad,
                                  st), 1);
         const DropArgs drop = make_drop(b, p->in);

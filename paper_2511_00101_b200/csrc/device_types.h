@@ -179,6 +179,10 @@ struct TokArgs {
     int accumulate;
     int stages;
     DropArgs drop;      // dA items: LoRA dropout of X (the mask of the forward), dA scaled by drop.scale
+    // fused cross-rank reduction: every dA/dB value is also stored at p + fanout_delta[q]
+    // (the same slot of peer rank q's staging buffer, mapped over NVLink), tile by tile
+    int n_fanout;
+    long long fanout_delta[8];
 };
 
 // ------------------------------------------------------------------------------------------
@@ -253,6 +257,21 @@ struct AdamwArgs {
     int zero_grad;
     const float *partial;   // per-CTA sum(g^2) of the clip pass, or nullptr
     int n_partial;
+    // fused cross-rank reduction: the gradient is the sum of n_slots slots
+    // g[q * slot_stride + i] in rank order q = 0.. (peer ranks wrote theirs over NVLink); the
+    // kernels start once *ready >= ready_target (system-scope counter the peers increment)
+    int n_slots;            // 1 = a plain gradient buffer
+    size_t slot_stride;     // elements between slots (multiple of 4)
+    int zero_slot;          // zero_grad clears only this slot (the caller's own)
+    const int *ready;
+    int ready_target;
+};
+
+// fused cross-rank gradient reduction: every rank's ready counter (peer-mapped)
+constexpr int kMaxRanks = 8;
+struct FanoutFlags {
+    int *flag[kMaxRanks];
+    int n;
 };
 
 constexpr int kDec3ChunkBytes = 128 * 32 * 4;   // one 32-column fp32 chunk of a CTA accumulator

@@ -634,7 +634,12 @@ __global__ void __launch_bounds__(kThreads, 1) smlm_tok_kernel(const __grid_cons
                     float *p = grp.dB + (size_t)col * grp.r;   // the adapter's own rank
 #pragma unroll
                     for (int j = 0; j < RP; ++j)
-                        if (j < grp.r) p[j] = args.accumulate ? p[j] + __uint_as_float(v[j]) : __uint_as_float(v[j]);
+                        if (j < grp.r) {
+                            const float dv = args.accumulate ? p[j] + __uint_as_float(v[j]) : __uint_as_float(v[j]);
+                            p[j] = dv;
+                            for (int q = 0; q < args.n_fanout; ++q)   // peers' copies of this rank's slot
+                                *reinterpret_cast<float *>(reinterpret_cast<char *>(p + j) + args.fanout_delta[q]) = dv;
+                        }
                 } else {
                     const float ds = args.drop.on ? args.drop.scale : 1.f;   // x~ = keep * x / (1 - p)
 #pragma unroll
@@ -642,7 +647,10 @@ __global__ void __launch_bounds__(kThreads, 1) smlm_tok_kernel(const __grid_cons
                         if (j < grp.r) {
                             float *p = grp.dA + (size_t)j * args.in_f + col;
                             const float dv = ds * __uint_as_float(v[j]);
-                            *p = args.accumulate ? *p + dv : dv;
+                            const float nv = args.accumulate ? *p + dv : dv;
+                            *p = nv;
+                            for (int q = 0; q < args.n_fanout; ++q)   // peers' copies of this rank's slot
+                                *reinterpret_cast<float *>(reinterpret_cast<char *>(p) + args.fanout_delta[q]) = nv;
                         }
                 }
             }

@@ -32,7 +32,8 @@ class AdapterParams:
     jobs[k] = the fine-tune job adapter k belongs to (default: one job per adapter).  The adapters
     of a job must be consecutive in `shapes` (one contiguous sub-range per job)."""
 
-    def __init__(self, shapes: Sequence[Tuple[int, int, int]], device="cuda", jobs: Optional[Sequence[int]] = None):
+    def __init__(self, shapes: Sequence[Tuple[int, int, int]], device="cuda", jobs: Optional[Sequence[int]] = None,
+                 grad: Optional[torch.Tensor] = None):
         self.shapes = [tuple(int(v) for v in s) for s in shapes]
         self.jobs = list(range(len(self.shapes))) if jobs is None else [int(j) for j in jobs]
         if len(self.jobs) != len(self.shapes):
@@ -56,7 +57,8 @@ class AdapterParams:
         self.master = torch.zeros(self.n, **f32)
         self.exp_avg = torch.zeros(self.n, **f32)
         self.exp_avg_sq = torch.zeros(self.n, **f32)
-        self.grad = torch.zeros(self.n, **f32)
+        # the gradient may live elsewhere (dp.PeerReduce: this rank's staging slot)
+        self.grad = torch.zeros(self.n, **f32) if grad is None else grad
         self.bf16 = torch.zeros(self.n, dtype=torch.bfloat16, device=device)
 
     def _view(self, buf, k: int, which: str):
@@ -105,11 +107,21 @@ class AdamW:
         self.ws = torch.empty(max(nws, 1), dtype=torch.float32, device=params.master.device)
 
     def step(self, jobs: Optional[Iterable[int]] = None, grad_scale: float = 1.0, zero_grad: bool = True,
-             lr: Optional[float] = None, stream=None):
+             lr: Optional[float] = None, stream=None, peer=None, parity: int = 0):
         """One step of each listed job (default: all) on its accumulated gradient (grad_scale: e.g.
-        1/(world * accumulation)); a job steps when ITS accumulation window closes."""
+        1/(world * accumulation)); a job steps when ITS accumulation window closes.
+        peer: a dp.PeerReduce -- the gradient is the rank-ordered sum of the peer slots of the given
+        step parity (store.grad must be peer.slot(parity)), reduced inside the step."""
         for j in (sorted(self.p.job_range) if jobs is None else jobs):
             self.t[j] += 1
             m, ea, es, g, pb = self.p.job(j)
-            S.smlm_adamw_step(m, ea, es, g, pb, self.t[j], self.lr if lr is None else lr, self.betas[0],
-                              self.betas[1], self.eps, self.wd, grad_scale, self.max_norm, zero_grad, self.ws, stream)
+            lr_j = self.lr if lr is None else lr
+            if peer is None:
+                S.smlm_adamw_step(m, ea, es, g, pb, self.t[j], lr_j, self.betas[0], self.betas[1], self.eps, self.wd,
+                                  grad_scale, self.max_norm, zero_grad, self.ws, stream)
+            else:
+                lo, hi = self.p.job_range[j]
+                S.smlm_adamw_step_reduce(m, ea, es, peer.stage[parity, 0, lo:], peer.world, peer.stride, peer.rank,
+                                         pb, hi - lo, self.t[j], lr_j, self.betas[0], self.betas[1], self.eps, self.wd,
+                                         grad_scale, self.max_norm, zero_grad, peer.ready, peer.ready_target(),
+                                         self.ws, stream)

@@ -33,6 +33,8 @@ EXPORTED = [
     "smlm_launch_count", "smlm_profile_enable", "smlm_profile_read", "smlm_workspace_size_multi",
     "smlm_forward_multi", "smlm_adamw_workspace_size", "smlm_adamw_step", "smlm_adapter_register_rank",
     "smlm_workspace_size_backward_multi", "smlm_backward_multi",
+    "smlm_ipc_get_handle", "smlm_ipc_open_handle", "smlm_ipc_close_handle", "smlm_pool_set_grad_fanout",
+    "smlm_fanout_signal", "smlm_fanout_wait", "smlm_adamw_step_reduce",
 ]
 
 
@@ -79,6 +81,13 @@ def _load():
         "smlm_profile_read": ([I, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(I)], I),
         "smlm_adamw_workspace_size": ([], Z),
         "smlm_adamw_step": ([P, P, P, P, P, Z, I] + [ctypes.c_float] * 7 + [I, P, Z, P], I),
+        "smlm_adamw_step_reduce": ([P, P, P, P, I, Z, I, P, Z, I] + [ctypes.c_float] * 7 + [I, P, I, P, Z, P], I),
+        "smlm_ipc_get_handle": ([P, P, ctypes.POINTER(ctypes.c_uint64)], I),
+        "smlm_ipc_open_handle": ([P, ctypes.POINTER(P)], I),
+        "smlm_ipc_close_handle": ([P], I),
+        "smlm_pool_set_grad_fanout": ([P, I, P], I),
+        "smlm_fanout_signal": ([I, P, P], I),
+        "smlm_fanout_wait": ([P, I, P], I),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)
@@ -275,6 +284,62 @@ def smlm_adamw_step(param, exp_avg, exp_avg_sq, grad, param_bf16, step: int, lr:
                                 int(step), lr, beta1, beta2, eps, weight_decay, grad_scale, max_grad_norm,
                                 int(bool(zero_grad)), _ptr(ws), 0 if ws is None else ws.numel() * ws.element_size(),
                                 _stream(stream, param.device)), "smlm_adamw_step")
+
+
+def smlm_adamw_step_reduce(param, exp_avg, exp_avg_sq, grad_slots, n_slots: int, slot_stride: int, own_slot: int,
+                           param_bf16, n: int, step: int, lr: float, beta1: float = 0.9, beta2: float = 0.999,
+                           eps: float = 1e-8, weight_decay: float = 0.0, grad_scale: float = 1.0,
+                           max_grad_norm: float = 0.0, zero_grad: bool = False, ready=None, ready_target: int = 0,
+                           ws=None, stream=None):
+    """AdamW on the rank-ordered sum of n_slots gradient slots (include/smlm.h smlm_adamw_step_reduce).
+    grad_slots: a tensor (or view) whose element 0 is slot 0's first element; ready: int32 tensor."""
+    _check(_lib.smlm_adamw_step_reduce(_ptr(param), _ptr(exp_avg), _ptr(exp_avg_sq), _ptr(grad_slots), int(n_slots),
+                                       int(slot_stride), int(own_slot), _ptr(param_bf16), int(n), int(step), lr, beta1,
+                                       beta2, eps, weight_decay, grad_scale, max_grad_norm, int(bool(zero_grad)),
+                                       _ptr(ready), int(ready_target), _ptr(ws),
+                                       0 if ws is None else ws.numel() * ws.element_size(),
+                                       _stream(stream, param.device)), "smlm_adamw_step_reduce")
+
+
+IPC_HANDLE_BYTES = 64
+
+
+def smlm_ipc_get_handle(t):
+    """(CUDA IPC handle (64 bytes) of the allocation holding tensor t, t's byte offset in it)."""
+    buf = ctypes.create_string_buffer(IPC_HANDLE_BYTES)
+    off = ctypes.c_uint64(0)
+    _check(_lib.smlm_ipc_get_handle(_ptr(t), buf, ctypes.byref(off)), "smlm_ipc_get_handle")
+    return buf.raw, int(off.value)
+
+
+def smlm_ipc_open_handle(handle: bytes) -> int:
+    """Map a peer allocation; returns its base address in this process."""
+    out = ctypes.c_void_p(0)
+    _check(_lib.smlm_ipc_open_handle(ctypes.create_string_buffer(handle, IPC_HANDLE_BYTES), ctypes.byref(out)),
+           "smlm_ipc_open_handle")
+    return int(out.value)
+
+
+def smlm_ipc_close_handle(ptr: int):
+    _check(_lib.smlm_ipc_close_handle(ptr), "smlm_ipc_close_handle")
+
+
+def smlm_pool_set_grad_fanout(pool: int, deltas):
+    arr = (ctypes.c_int64 * max(len(deltas), 1))(*[int(d) for d in deltas])
+    _check(_lib.smlm_pool_set_grad_fanout(pool, len(deltas), ctypes.cast(arr, ctypes.c_void_p)),
+           "smlm_pool_set_grad_fanout")
+
+
+def smlm_fanout_wait(ready, target: int, stream=None):
+    _check(_lib.smlm_fanout_wait(_ptr(ready), int(target), _stream(stream, ready.device)), "smlm_fanout_wait")
+
+
+def smlm_fanout_signal(ready_ptrs, stream=None, device=None):
+    """ready_ptrs: device addresses (ints) of every rank's ready counter as mapped in this process."""
+    arr = (ctypes.c_void_p * len(ready_ptrs))(*[int(p) for p in ready_ptrs])
+    import torch
+    st = _stream(stream, device if device is not None else torch.device("cuda", torch.cuda.current_device()))
+    _check(_lib.smlm_fanout_signal(len(ready_ptrs), ctypes.cast(arr, ctypes.c_void_p), st), "smlm_fanout_signal")
 
 
 def smlm_launch_count() -> int:
