@@ -6,6 +6,8 @@ it and shares no code with it (no kernels, headers, helpers or constants).
 
 * `smlm_oracle.c`  -- fp64 per-row loops of the plain SMLM definition
                       (SURVEY.md §8(c)).
+* `attention.py`   -- the Alg. 1 attention branch: causal segment-wise
+                      attention with KV-cache init / append, fp64 (numpy).
 * `plan.py`        -- independent Python re-derivation of the canonical work plan
                       (DESIGN.md "Canonical plan").
 
