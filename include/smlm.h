@@ -318,6 +318,37 @@ SMLM_API int smlm_adamw_step_reduce(float *param, float *exp_avg, float *exp_avg
                                    float max_grad_norm, int zero_grad, const int *ready, int ready_target, void *ws,
                                    size_t ws_bytes, void *stream);
 
+/*
+ * The Alg. 1 attention branch (reading R14): for a
+ * packed batch of segments, causal scaled-dot-product attention of every row over the keys of its
+ * own request, grouped-query heads (query head h reads KV head h / (n_heads / n_kv_heads)):
+ *   FINETUNE / EVAL / PREFILL segment (a fresh sequence): row i attends to the segment's rows 0..i;
+ *     a PREFILL segment with seg_cache[g] >= 0 also writes its K/V rows to cache positions [0, L)
+ *     ("Initialize KVCache for prefills");
+ *   DECODE segment: row i is appended at cache position seg_past[g] + i ("Append KVCache for
+ *     decodes") and attends to cache positions [0, seg_past[g] + i].
+ *   Q [S, n_heads, 128], K / V [S, n_kv_heads, 128], O [S, n_heads, 128] bf16 (the projections'
+ *   outputs: position encoding, e.g. RoPE, is applied by the caller); K_cache / V_cache
+ *   [cache_slots, cache_capacity, n_kv_heads, 128] bf16; scale = softmax scale (1/sqrt(128)).
+ *   head_dim must be 128; n_heads / n_kv_heads <= 8; decode: group * (past + L) * 4 <= 200 KB.
+ *   Host arrays: seg_offsets [G+1], seg_mode [G], seg_cache [G] (or NULL: no cache use),
+ *   seg_past [G] (or NULL: 0).  ws: >= smlm_attention_workspace_size(batch) bytes (device).
+ * Forward only (fine-tune rows' attention gradients are outside the SMLM path).
+ * Errors: SMLM_E_INVALID, SMLM_E_SHAPE, SMLM_E_UNSUPPORTED, SMLM_E_WORKSPACE, SMLM_E_CUDA.
+ */
+typedef struct {
+    int S;
+    int G;
+    const int32_t *seg_offsets;
+    const int8_t *seg_mode;
+    const int32_t *seg_cache;
+    const int32_t *seg_past;
+} smlm_attn_batch;
+SMLM_API size_t smlm_attention_workspace_size(const smlm_attn_batch *batch);
+SMLM_API int smlm_attention(const smlm_attn_batch *batch, int n_heads, int n_kv_heads, int head_dim, const void *Q,
+                            const void *K, const void *V, void *O, void *K_cache, void *V_cache, int cache_slots,
+                            int cache_capacity, float scale, void *ws, size_t ws_bytes, void *stream);
+
 SMLM_API const char *smlm_status_string(int status);
 SMLM_API const char *smlm_last_error(void);
 

@@ -24,8 +24,8 @@ BUILD = os.path.join(HERE, "_build")
 LIB = os.path.join(HERE, "libsmlm.so")
 BUILD_MEASURE = os.path.join(HERE, "_build_measure")
 LIB_MEASURE = os.path.join(HERE, "libsmlm_measure.so")
-SOURCES = ["api.cu", "planner.cpp", "kernels_tc.cu", "kernels_simt.cu", "kernels_dec.cu", "kernels_tc2.cu", "kernels_dec3.cu", "kernels_opt.cu", "kernels_plan.cu"]
-HEADERS = ["plan.h", "device_types.h", "sm100.cuh", "pdl.cuh"]
+SOURCES = ["api.cu", "planner.cpp", "kernels_tc.cu", "kernels_simt.cu", "kernels_dec.cu", "kernels_tc2.cu", "kernels_dec3.cu", "kernels_opt.cu", "kernels_plan.cu", "kernels_attn.cu"]
+HEADERS = ["plan.h", "device_types.h", "sm100.cuh", "pdl.cuh", "dropout.cuh"]
 NVCC = os.environ.get("NVCC", "nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",

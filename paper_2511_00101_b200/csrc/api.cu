@@ -53,6 +53,7 @@ int adamw_grid(int num_sms, size_t n);
 int launch_adamw_sumsq(const AdamwArgs &a, float *partial, int grid, cudaStream_t st);
 int launch_fanout_signal(const FanoutFlags &f, cudaStream_t st);
 int launch_fanout_wait(const int *ready, int target, cudaStream_t st);
+int launch_attn(const AttnArgs &a, int n_items, int n_rows, int n_drows, int max_dec_len, cudaStream_t st);
 int launch_adamw_step(const AdamwArgs &a, int grid, cudaStream_t st);
 int launch_shrink_split(const __nv_bfloat16 *X, const SlotDev *slots, const DevBlock *blocks,
                         const DevShortRow *srows, int n_blocks, int in_f, int r, int r_pad, float *part,
@@ -1955,6 +1956,117 @@ int smlm_backward_multi(int n_proj, const smlm_pool *pools, const smlm_batch *b,
     }
     for (int i = 0; i < n_proj; ++i)
         if ((rc = bwd_tok(pools[i], b, X, dY[i], V_save ? V_save[i] : nullptr, accumulate, B[i], st))) return rc;
+    return SMLM_OK;
+}
+
+// ---- the Alg. 1 attention branch (kernels_attn.cu) ----
+namespace {
+struct AttnPlan {
+    std::vector<AttnItem> items;
+    std::vector<AttnRow> rows, drows;
+    int max_dec_len = 0;
+};
+int attn_plan(const smlm_attn_batch *b, int n_heads, int n_kv_heads, int head_dim, int cache_slots, int capacity,
+              AttnPlan &P) {
+    if (!b) return set_err(SMLM_E_INVALID, "batch is NULL");
+    if (head_dim != 128) return set_err(SMLM_E_UNSUPPORTED, "attention: head_dim must be 128");
+    if (n_heads < 1 || n_kv_heads < 1 || n_heads % n_kv_heads || n_heads / n_kv_heads > 8)
+        return set_err(SMLM_E_SHAPE, "attention: n_heads must be a multiple of n_kv_heads, group <= 8");
+    if (b->S < 0 || b->G < 0 || (b->G > 0 && (!b->seg_offsets || !b->seg_mode)))
+        return set_err(SMLM_E_INVALID, "attention: bad batch arrays");
+    if (b->G == 0) return b->S == 0 ? SMLM_OK : set_err(SMLM_E_INVALID, "G == 0 but S != 0");
+    const int32_t *off = b->seg_offsets;
+    if (off[0] != 0 || off[b->G] != b->S) return set_err(SMLM_E_INVALID, "attention: offsets must run 0..S");
+    for (int g = 0; g < b->G; ++g) {
+        const int a0 = off[g], a1 = off[g + 1], L = a1 - a0, m = b->seg_mode[g];
+        if (L < 0) return set_err(SMLM_E_INVALID, "attention: offsets must be non-decreasing");
+        if (m < SMLM_FINETUNE || m > SMLM_DECODE) return set_err(SMLM_E_INVALID, "attention: mode outside 0..3");
+        const int slot = b->seg_cache ? b->seg_cache[g] : -1;
+        if (L == 0) continue;
+        if (m == SMLM_DECODE) {
+            const int past = b->seg_past ? b->seg_past[g] : 0;
+            if (slot < 0 || slot >= cache_slots || past < 0 || past + L > capacity)
+                return set_err(SMLM_E_INVALID, "attention: a DECODE segment needs a cache slot with room for its rows");
+            for (int i = 0; i < L; ++i) {
+                P.rows.push_back({a0 + i, slot, past + i, 0});
+                P.drows.push_back({a0 + i, slot, past + i, 0});
+            }
+            P.max_dec_len = std::max(P.max_dec_len, past + L);
+        } else {
+            if (m == SMLM_PREFILL && slot >= 0) {
+                if (slot >= cache_slots || L > capacity)
+                    return set_err(SMLM_E_INVALID, "attention: PREFILL cache slot out of range or too short");
+                for (int i = 0; i < L; ++i) P.rows.push_back({a0 + i, slot, i, 0});
+            }
+            for (int qb = 0; qb * 128 < L; ++qb) P.items.push_back({a0, L, qb, 0});
+        }
+    }
+    const size_t dec_smem = (size_t)(n_heads / n_kv_heads) * P.max_dec_len * sizeof(float);
+    if (dec_smem > 200 * 1024)
+        return set_err(SMLM_E_UNSUPPORTED, "attention: decode context too long for the one-pass decode kernel "
+                                           "(group * cache length * 4 bytes <= 200 KB)");
+    return SMLM_OK;
+}
+smlm_pool_s g_attn_stage;   // pinned staging of the attention plans (no adapter pool involved)
+}  // namespace
+
+size_t smlm_attention_workspace_size(const smlm_attn_batch *b) {
+    if (!b) return 0;
+    AttnPlan P;
+    if (attn_plan(b, 1, 1, 128, 1 << 30, 1 << 30, P) != SMLM_OK) return 0;
+    return align256(P.items.size() * sizeof(AttnItem) + 16) + align256(P.rows.size() * sizeof(AttnRow) + 16) +
+           align256(P.drows.size() * sizeof(AttnRow) + 16) + 256;
+}
+
+int smlm_attention(const smlm_attn_batch *b, int n_heads, int n_kv_heads, int head_dim, const void *Q, const void *K,
+                   const void *V, void *O, void *K_cache, void *V_cache, int cache_slots, int cache_capacity,
+                   float scale, void *ws, size_t ws_bytes, void *stream) {
+    AttnPlan P;
+    int rc = attn_plan(b, n_heads, n_kv_heads, head_dim, cache_slots, cache_capacity, P);
+    if (rc) return rc;
+    if (b->S == 0) return SMLM_OK;
+    if (!Q || !K || !V || !O) return set_err(SMLM_E_INVALID, "attention: Q, K, V and O must be non-NULL");
+    if ((!P.rows.empty() || !P.drows.empty()) && (!K_cache || !V_cache))
+        return set_err(SMLM_E_INVALID, "attention: prefill-with-cache / decode segments need K_cache and V_cache");
+    if (!(scale > 0.f) || !std::isfinite(scale)) return set_err(SMLM_E_INVALID, "attention: scale must be finite, > 0");
+    const size_t need = smlm_attention_workspace_size(b);
+    if (!ws || ws_bytes < need) return set_err(SMLM_E_WORKSPACE, "workspace too small");
+    int sms = 0;
+    if ((rc = current_sm100_sms(&sms))) return rc;
+    if ((rc = check_sticky())) return rc;
+    cudaStream_t st = (cudaStream_t)stream;
+    uint8_t *wsb = reinterpret_cast<uint8_t *>(ws);
+    std::vector<uint8_t> bytes;
+    append(bytes, P.items);
+    while (bytes.size() % 16) bytes.push_back(0);
+    const size_t rows_off = bytes.size();
+    append(bytes, P.rows);
+    const size_t drows_off = bytes.size();
+    append(bytes, P.drows);
+    if ((rc = stage_upload(&g_attn_stage, bytes, wsb, st))) return rc;
+    AttnArgs a;
+    memset(&a, 0, sizeof(a));
+    const uint64_t S = (uint64_t)b->S;
+    if (!P.items.empty()) {
+        if ((rc = make_map(&a.tmQ, Q, (uint64_t)n_heads * 128, S, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B))) return rc;
+        if ((rc = make_map(&a.tmK, K, (uint64_t)n_kv_heads * 128, S, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B))) return rc;
+        if ((rc = make_map(&a.tmV, V, (uint64_t)n_kv_heads * 128, S, 64, 64, CU_TENSOR_MAP_SWIZZLE_128B))) return rc;
+    }
+    a.items = reinterpret_cast<const AttnItem *>(wsb);
+    a.rows = reinterpret_cast<const AttnRow *>(wsb + rows_off);
+    a.drows = reinterpret_cast<const AttnRow *>(wsb + drows_off);
+    a.Q = Q;
+    a.K = K;
+    a.V = V;
+    a.O = O;
+    a.K_cache = K_cache;
+    a.V_cache = V_cache;
+    a.n_heads = n_heads;
+    a.n_kv_heads = n_kv_heads;
+    a.cache_capacity = cache_capacity;
+    a.scale = scale;
+    const int nl = (P.rows.empty() ? 0 : 1) + (P.items.empty() ? 0 : 1) + (P.drows.empty() ? 0 : 1);
+    CKL(launch_attn(a, (int)P.items.size(), (int)P.rows.size(), (int)P.drows.size(), P.max_dec_len, st), nl);
     return SMLM_OK;
 }
 

@@ -267,6 +267,34 @@ struct AdamwArgs {
     int ready_target;
 };
 
+// ---- the Alg. 1 attention branch (kernels_attn.cu) ----
+struct alignas(16) AttnItem {   // prefill kernel: one 128-query block of a FINETUNE / EVAL / PREFILL segment
+    int row0;    // first row of the segment
+    int len;     // segment length (keys and queries are the segment's own rows)
+    int qb;      // query block
+    int pad;
+};
+struct alignas(16) AttnRow {    // a row written to the KV cache (kv-write) / a decode row (decode)
+    int row;     // row of Q/K/V
+    int slot;    // cache slot (-1: no write)
+    int pos;     // cache position of this row (decode: it attends to cache[0 .. pos])
+    int pad;
+};
+struct AttnArgs {
+    CUtensorMap tmQ;   // Q [S, Hq*d] box {64, 128}
+    CUtensorMap tmK;   // K [S, Hkv*d] box {64, 128}
+    CUtensorMap tmV;   // V [S, Hkv*d] box {64, 64}
+    const AttnItem *items;
+    const AttnRow *rows;    // cache writes
+    const AttnRow *drows;   // decode rows
+    const void *Q, *K, *V;
+    void *O;
+    void *K_cache, *V_cache;   // [slots, capacity, Hkv, d] bf16
+    int n_heads, n_kv_heads;
+    int cache_capacity;
+    float scale;
+};
+
 // fused cross-rank gradient reduction: every rank's ready counter (peer-mapped)
 constexpr int kMaxRanks = 8;
 struct FanoutFlags {

@@ -1,0 +1,382 @@
+// kernels_attn.cu -- the Alg. 1 attention branch: segment-wise
+// causal attention for FINETUNE / EVAL / PREFILL rows, KV-cache initialisation for prefills and
+// append + attention over the cache for decodes (reading R14, oracle/attention.py).
+//
+//   attn_kv_write_kernel   : prefill rows -> cache[slot][0..L), decode rows -> cache[slot][past + i]
+//   attn_prefill_kernel    : one CTA per (segment, 128-query block, query head), tcgen05 with the
+//                            accumulators in TMEM: S = Q K_j^T (M=128, N=128 keys, K=d=128) ->
+//                            online softmax by 4 warps (thread = query row; running max / sum in
+//                            registers, O rescaled in TMEM when the max moves) -> P (bf16, smem) ->
+//                            O += P V_j (N=d, K=128 keys, V as the MN-major operand); K/V tiles by
+//                            TMA in a 2-deep ring; S_{j+1} is issued while the softmax of j runs.
+//   attn_decode_kernel     : one CTA per (decode row, KV head), HBM-bound: the G query heads of the
+//                            group (one warp each) score every cached key (each K row read once
+//                            for all G heads, 128-bit loads), softmax in fp32, then P V with lanes
+//                            over the head dimension (coalesced 256-byte V rows).
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <math.h>
+
+#include "device_types.h"
+#include "pdl.cuh"
+#include "sm100.cuh"
+
+namespace smlm {
+using namespace sm100;
+
+namespace {
+
+constexpr int kAT = 256;                 // prefill: 8 warps (0 TMA, 1 MMA, 2 TMEM alloc, 4-7 softmax)
+constexpr uint32_t kQBytes = 32768;      // 128 rows x 128 d bf16 (two 64-wide SW128 boxes)
+constexpr uint32_t kKVBytes = 65536;     // K tile (32 KB) + V tile (32 KB)
+constexpr uint32_t kPBytes = 32768;      // P: 128 rows x 128 keys bf16
+
+__device__ __forceinline__ float fast_exp2(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+__global__ void __launch_bounds__(kAT, 1) attn_prefill_kernel(const __grid_constant__ AttnArgs a) {
+    extern __shared__ uint8_t smem_raw[];
+    const uint32_t raw = smem_u32(smem_raw);
+    const uint32_t base = (raw + 1023u) & ~1023u;
+    uint8_t *base_ptr = smem_raw + (base - raw);
+    const uint32_t q_s = base;
+    auto kv_s = [&](int b) { return base + kQBytes + (uint32_t)b * kKVBytes; };
+    const uint32_t p_s = base + kQBytes + 2 * kKVBytes;
+    const uint32_t bar = p_s + kPBytes;
+    const uint32_t q_full = bar, s_full = bar + 8, s_free = bar + 16, p_full = bar + 24, o_done = bar + 32;
+    auto kv_full = [&](int b) { return bar + 40u + 8u * b; };
+    auto kv_empty = [&](int b) { return bar + 56u + 8u * b; };
+    const uint32_t tmem_slot = bar + 72;
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int head = blockIdx.x % a.n_heads;
+    const int kvh = head / (a.n_heads / a.n_kv_heads);
+    if (threadIdx.x == 0) {
+        mbar_init(q_full, 1);
+        mbar_init(s_full, 1);
+        mbar_init(s_free, 128);
+        mbar_init(p_full, 128);
+        mbar_init(o_done, 1);
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(kv_full(b), 1);
+            mbar_init(kv_empty(b), 1);
+        }
+        fence_mbar_init();
+        tma_prefetch_desc(&a.tmQ);
+        tma_prefetch_desc(&a.tmK);
+        tma_prefetch_desc(&a.tmV);
+    }
+    if (warp == 2) tmem_alloc(tmem_slot, 256);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *reinterpret_cast<volatile uint32_t *>(base_ptr + (tmem_slot - base));
+    const uint32_t S_t = tmem, O_t = tmem + 128;
+    pdl_wait();   // the item table is written by the stream's plan upload
+    pdl_trigger();
+    const AttnItem it = a.items[blockIdx.x / a.n_heads];
+    const int nkb = it.qb + 1;                 // block-causal key range
+    const int q0 = it.row0 + it.qb * 128;      // first query row of the block
+
+    if (warp == 0) {
+        // ---------------- TMA producer ----------------
+        if (lane == 0) {
+            mbar_expect_tx(q_full, kQBytes);
+            for (int db = 0; db < 2; ++db)
+                tma_load_2d(q_s + 16384u * db, &a.tmQ, q_full, head * 128 + 64 * db, q0);
+            for (int j = 0; j < nkb; ++j) {
+                const int b = j & 1;
+                mbar_wait(kv_empty(b), ((j >> 1) & 1) ^ 1);
+                mbar_expect_tx(kv_full(b), kKVBytes);
+                const int k0 = it.row0 + j * 128;
+                // K_j: B operand of S = Q K^T, K-major (rows = keys, 128 B of d per row)
+                for (int db = 0; db < 2; ++db)
+                    tma_load_2d(kv_s(b) + 16384u * db, &a.tmK, kv_full(b), kvh * 128 + 64 * db, k0);
+                // V_j: B operand of O += P V, MN-major (rows = keys, 64-wide d boxes)
+                for (int kb = 0; kb < 2; ++kb)
+                    for (int db = 0; db < 2; ++db)
+                        tma_load_2d(kv_s(b) + 32768u + 16384u * kb + 8192u * db, &a.tmV, kv_full(b),
+                                    kvh * 128 + 64 * db, k0 + 64 * kb);
+            }
+        }
+    } else if (warp == 1) {
+        // ---------------- MMA issuer ----------------
+        constexpr uint32_t idesc_s = idesc_bf16(128, 128, 0, 0);
+        constexpr uint32_t idesc_o = idesc_bf16(128, 128, 0, 1);
+        auto issue_s = [&](int j) {
+            const int b = j & 1;
+            mbar_wait(kv_full(b), (j >> 1) & 1);
+            tc_fence_after();
+            if (lane == 0) {
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    const uint32_t off = 16384u * (k >> 2) + 32u * (k & 3);
+                    mma_bf16(S_t, smem_desc(q_s + off, 16, 1024, kSw128), smem_desc(kv_s(b) + off, 16, 1024, kSw128),
+                             idesc_s, k > 0);
+                }
+                mma_commit(s_full);
+            }
+            __syncwarp();
+        };
+        mbar_wait(q_full, 0);
+        issue_s(0);
+        for (int j = 0; j < nkb; ++j) {
+            if (j + 1 < nkb) {
+                mbar_wait(s_free, j & 1);   // the softmax has read S_j
+                issue_s(j + 1);
+            }
+            mbar_wait(p_full, j & 1);       // P_j in smem, O rescaled
+            tc_fence_after();
+            const int b = j & 1;
+            if (lane == 0) {
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    const uint32_t pa = p_s + 16384u * (k >> 2) + 32u * (k & 3);
+                    const uint32_t vb = kv_s(b) + 32768u + 16384u * (k >> 2) + 2048u * (k & 3);
+                    mma_bf16(O_t, smem_desc(pa, 16, 1024, kSw128), smem_desc(vb, 8192, 1024, kSw128), idesc_o,
+                             (j > 0 || k > 0) ? 1u : 0u);
+                }
+                mma_commit(kv_empty(b));
+                mma_commit(o_done);
+            }
+            __syncwarp();
+        }
+    } else if (warp >= 4) {
+        // ---------------- online softmax + epilogue (thread = query row) ----------------
+        const int m = threadIdx.x - 128;
+        const uint32_t lane_base = (uint32_t)((warp - 4) * 32) << 16;
+        const int qi = it.qb * 128 + m;           // query position inside the segment
+        const float sl2 = a.scale * 1.4426950408889634f;
+        float mi = -INFINITY, li = 0.f;
+        uint8_t *pp = base_ptr + (p_s - base);
+        for (int j = 0; j < nkb; ++j) {
+            mbar_wait(s_full, j & 1);
+            tc_fence_after();
+            const int kbase = j * 128;
+            float mx = -INFINITY;
+#pragma unroll 1
+            for (int c = 0; c < 4; ++c) {
+                uint32_t r[32];
+                tmem_ld32(S_t + lane_base + 32u * c, r);
+                tmem_wait_ld();
+#pragma unroll
+                for (int e = 0; e < 32; ++e) {
+                    const int kj = kbase + 32 * c + e;
+                    if (kj <= qi && kj < it.len) mx = fmaxf(mx, __uint_as_float(r[e]) * sl2);
+                }
+            }
+            const float m_new = fmaxf(mi, mx);
+            const float alpha = fast_exp2(mi - m_new);   // 0 on the first block (mi = -inf)
+            float sum = 0.f;
+            if (j > 0) {
+                // P_{j-1} V_{j-1} has landed in O and the P buffer is free
+                mbar_wait(o_done, (j - 1) & 1);
+                tc_fence_after();
+            }
+#pragma unroll 1
+            for (int c = 0; c < 4; ++c) {
+                uint32_t r[32];
+                tmem_ld32(S_t + lane_base + 32u * c, r);
+                tmem_wait_ld();
+                uint32_t pk[16];
+#pragma unroll
+                for (int e = 0; e < 32; e += 2) {
+                    const int kj = kbase + 32 * c + e;
+                    const float p0 = (kj <= qi && kj < it.len) ? fast_exp2(__uint_as_float(r[e]) * sl2 - m_new) : 0.f;
+                    const float p1 = (kj + 1 <= qi && kj + 1 < it.len) ? fast_exp2(__uint_as_float(r[e + 1]) * sl2 - m_new)
+                                                                     : 0.f;
+                    const __nv_bfloat162 pb = __floats2bfloat162_rn(p0, p1);
+                    // the sum uses the rounded probabilities the MMA multiplies V with
+                    const float2 pr = __bfloat1622float2(pb);
+                    sum += pr.x + pr.y;
+                    pk[e >> 1] = *reinterpret_cast<const uint32_t *>(&pb);
+                }
+                // keys 32c .. 32c+31: 16-byte chunks 4c .. 4c+3 of the 128-key row (two 64-key blocks)
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const int ch = 4 * c + q, kb = ch >> 3, cc = ch & 7;
+                    *reinterpret_cast<uint4 *>(pp + kb * 16384 + m * 128 + ((cc ^ (m & 7)) << 4)) =
+                        make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+                }
+            }
+            tc_fence_before();
+            mbar_arrive(s_free);   // S may be overwritten by S_{j+1}
+            li = li * alpha + sum;
+            // tcgen05.ld / st are warp-collective: the rescale runs when any row of the warp needs it
+            if (j > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {
+#pragma unroll 1
+                for (int c = 0; c < 4; ++c) {
+                    uint32_t r[32];
+                    tmem_ld32(O_t + lane_base + 32u * c, r);
+                    tmem_wait_ld();
+#pragma unroll
+                    for (int e = 0; e < 32; ++e) r[e] = __float_as_uint(__uint_as_float(r[e]) * alpha);
+                    tmem_st32(O_t + lane_base + 32u * c, r);
+                }
+                tmem_wait_st();
+            }
+            mi = m_new;
+            fence_proxy_async_smem();   // P (generic stores) -> the MMA (async proxy)
+            tc_fence_before();
+            mbar_arrive(p_full);
+        }
+        mbar_wait(o_done, (nkb - 1) & 1);
+        tc_fence_after();
+        const float inv = 1.f / li;
+        const bool ok = qi < it.len;
+        __nv_bfloat16 *O = reinterpret_cast<__nv_bfloat16 *>(a.O) + ((size_t)(q0 + m) * a.n_heads + head) * 128;
+#pragma unroll 1
+        for (int c = 0; c < 4; ++c) {
+            uint32_t r[32];
+            tmem_ld32(O_t + lane_base + 32u * c, r);
+            tmem_wait_ld();
+            if (ok) {
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    uint4 v;
+                    v.x = pack_bf16x2(__uint_as_float(r[8 * q + 0]) * inv, __uint_as_float(r[8 * q + 1]) * inv);
+                    v.y = pack_bf16x2(__uint_as_float(r[8 * q + 2]) * inv, __uint_as_float(r[8 * q + 3]) * inv);
+                    v.z = pack_bf16x2(__uint_as_float(r[8 * q + 4]) * inv, __uint_as_float(r[8 * q + 5]) * inv);
+                    v.w = pack_bf16x2(__uint_as_float(r[8 * q + 6]) * inv, __uint_as_float(r[8 * q + 7]) * inv);
+                    *reinterpret_cast<uint4 *>(O + 32 * c + 8 * q) = v;
+                }
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 2) {
+        tc_fence_after();
+        tmem_dealloc(tmem, 256);
+    }
+}
+
+// ---- KV-cache writes: row t of K/V [S, Hkv, d] -> cache slot / position (plan: AttnRow) ----
+__global__ void __launch_bounds__(256) attn_kv_write_kernel(const AttnArgs a) {
+    pdl_wait();
+    pdl_trigger();
+    const AttnRow rw = a.rows[blockIdx.x];
+    if (rw.slot < 0) return;
+    const size_t row_elems = (size_t)a.n_kv_heads * 128;
+    const uint4 *ks = reinterpret_cast<const uint4 *>(reinterpret_cast<const __nv_bfloat16 *>(a.K) + (size_t)rw.row * row_elems);
+    const uint4 *vs = reinterpret_cast<const uint4 *>(reinterpret_cast<const __nv_bfloat16 *>(a.V) + (size_t)rw.row * row_elems);
+    const size_t dst = ((size_t)rw.slot * a.cache_capacity + rw.pos) * row_elems;
+    uint4 *kd = reinterpret_cast<uint4 *>(reinterpret_cast<__nv_bfloat16 *>(a.K_cache) + dst);
+    uint4 *vd = reinterpret_cast<uint4 *>(reinterpret_cast<__nv_bfloat16 *>(a.V_cache) + dst);
+    for (int i = threadIdx.x; i < (int)(row_elems / 8); i += blockDim.x) {
+        kd[i] = ks[i];
+        vd[i] = vs[i];
+    }
+}
+
+// ---- decode: one CTA per (decode row, KV head); warp g = query head kvh * G + g ----
+__global__ void __launch_bounds__(256) attn_decode_kernel(const AttnArgs a) {
+    extern __shared__ float sc[];   // [G][L] scores -> probabilities
+    pdl_wait();
+    pdl_trigger();
+    const int G = a.n_heads / a.n_kv_heads;
+    const AttnRow rw = a.drows[blockIdx.x / a.n_kv_heads];
+    const int kvh = blockIdx.x % a.n_kv_heads;
+    const int L = rw.pos + 1;   // the cache holds the row itself (appended by attn_kv_write_kernel)
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    __shared__ float qs[8][128];
+    const __nv_bfloat16 *Q = reinterpret_cast<const __nv_bfloat16 *>(a.Q) + ((size_t)rw.row * a.n_heads + kvh * G) * 128;
+    for (int e = threadIdx.x; e < G * 128; e += blockDim.x) qs[e / 128][e % 128] = __bfloat162float(Q[e]) * a.scale;
+    __syncthreads();
+    const size_t row_elems = (size_t)a.n_kv_heads * 128;
+    const __nv_bfloat16 *Kc = reinterpret_cast<const __nv_bfloat16 *>(a.K_cache) +
+                              (size_t)rw.slot * a.cache_capacity * row_elems + kvh * 128;
+    const __nv_bfloat16 *Vc = reinterpret_cast<const __nv_bfloat16 *>(a.V_cache) +
+                              (size_t)rw.slot * a.cache_capacity * row_elems + kvh * 128;
+    // scores: thread per key, all G heads from one read of the key row
+    for (int j = threadIdx.x; j < L; j += blockDim.x) {
+        const uint4 *kr = reinterpret_cast<const uint4 *>(Kc + (size_t)j * row_elems);
+        float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll 2
+        for (int v = 0; v < 16; ++v) {
+            const uint4 u = kr[v];
+            const __nv_bfloat162 *h2 = reinterpret_cast<const __nv_bfloat162 *>(&u);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const float2 kf = __bfloat1622float2(h2[i]);
+                const int d = 8 * v + 2 * i;
+#pragma unroll
+                for (int g = 0; g < 8; ++g)
+                    if (g < G) acc[g] = fmaf(kf.x, qs[g][d], fmaf(kf.y, qs[g][d + 1], acc[g]));
+            }
+        }
+#pragma unroll
+        for (int g = 0; g < 8; ++g)
+            if (g < G) sc[g * L + j] = acc[g];
+    }
+    __syncthreads();
+    if (warp < G) {
+        // softmax of head `warp` over the L scores (fp32), in place
+        float mx = -INFINITY;
+        for (int j = lane; j < L; j += 32) mx = fmaxf(mx, sc[warp * L + j]);
+#pragma unroll
+        for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        float sum = 0.f;
+        for (int j = lane; j < L; j += 32) {
+            const float p = __expf(sc[warp * L + j] - mx);
+            sc[warp * L + j] = p;
+            sum += p;
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+        __syncwarp();
+        // O = sum_j p_j v_j / sum: lane owns d = 4 lane .. 4 lane + 3 (256-byte V rows, coalesced)
+        float o[4] = {0.f, 0.f, 0.f, 0.f};
+        for (int j = 0; j < L; ++j) {
+            const float p = sc[warp * L + j];
+            const uint2 u = *reinterpret_cast<const uint2 *>(Vc + (size_t)j * row_elems + 4 * lane);
+            const __nv_bfloat162 *h2 = reinterpret_cast<const __nv_bfloat162 *>(&u);
+            const float2 v0 = __bfloat1622float2(h2[0]), v1 = __bfloat1622float2(h2[1]);
+            o[0] = fmaf(p, v0.x, o[0]);
+            o[1] = fmaf(p, v0.y, o[1]);
+            o[2] = fmaf(p, v1.x, o[2]);
+            o[3] = fmaf(p, v1.y, o[3]);
+        }
+        const float inv = 1.f / sum;
+        __nv_bfloat16 *O = reinterpret_cast<__nv_bfloat16 *>(a.O) + ((size_t)rw.row * a.n_heads + kvh * G + warp) * 128 + 4 * lane;
+        uint2 st;
+        st.x = pack_bf16x2(o[0] * inv, o[1] * inv);
+        st.y = pack_bf16x2(o[2] * inv, o[3] * inv);
+        *reinterpret_cast<uint2 *>(O) = st;
+    }
+}
+
+}  // namespace
+
+size_t attn_prefill_smem() { return 1024 + kQBytes + 2 * kKVBytes + kPBytes + 256; }
+
+int launch_attn(const AttnArgs &a, int n_items, int n_rows, int n_drows, int max_dec_len, cudaStream_t st) {
+    cudaError_t e = cudaSuccess;
+    if (n_rows) {
+        e = launch_pdl(attn_kv_write_kernel, dim3(n_rows), dim3(256), 0, st, a);
+        if (e != cudaSuccess) return (int)e;
+    }
+    if (n_items) {
+        static bool attr = false;
+        if (!attr) {
+            e = cudaFuncSetAttribute(attn_prefill_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)attn_prefill_smem());
+            if (e != cudaSuccess) return (int)e;
+            attr = true;
+        }
+        e = launch_pdl(attn_prefill_kernel, dim3(n_items * a.n_heads), dim3(kAT), attn_prefill_smem(), st, a);
+        if (e != cudaSuccess) return (int)e;
+    }
+    if (n_drows) {
+        const size_t smem = (size_t)(a.n_heads / a.n_kv_heads) * max_dec_len * sizeof(float);
+        e = cudaFuncSetAttribute(attn_decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return (int)e;
+        e = launch_pdl(attn_decode_kernel, dim3(n_drows * a.n_kv_heads), dim3(256), smem, st, a);
+    }
+    return (int)e;
+}
+
+}  // namespace smlm

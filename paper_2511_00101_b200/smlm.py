@@ -35,6 +35,7 @@ EXPORTED = [
     "smlm_workspace_size_backward_multi", "smlm_backward_multi",
     "smlm_ipc_get_handle", "smlm_ipc_open_handle", "smlm_ipc_close_handle", "smlm_pool_set_grad_fanout",
     "smlm_fanout_signal", "smlm_fanout_wait", "smlm_adamw_step_reduce",
+    "smlm_attention_workspace_size", "smlm_attention",
 ]
 
 
@@ -48,6 +49,11 @@ class smlm_batch(ctypes.Structure):
     _fields_ = [("S", ctypes.c_int), ("G", ctypes.c_int), ("seg_offsets", ctypes.c_void_p),
                 ("seg_slot", ctypes.c_void_p), ("seg_mode", ctypes.c_void_p), ("seg_scale", ctypes.c_void_p),
                 ("dropout_p", ctypes.c_float), ("dropout_seed", ctypes.c_uint64)]
+
+
+class smlm_attn_batch(ctypes.Structure):
+    _fields_ = [("S", ctypes.c_int), ("G", ctypes.c_int), ("seg_offsets", ctypes.c_void_p),
+                ("seg_mode", ctypes.c_void_p), ("seg_cache", ctypes.c_void_p), ("seg_past", ctypes.c_void_p)]
 
 
 def _load():
@@ -88,6 +94,9 @@ def _load():
         "smlm_pool_set_grad_fanout": ([P, I, P], I),
         "smlm_fanout_signal": ([I, P, P], I),
         "smlm_fanout_wait": ([P, I, P], I),
+        "smlm_attention_workspace_size": ([ctypes.POINTER(smlm_attn_batch)], Z),
+        "smlm_attention": ([ctypes.POINTER(smlm_attn_batch), I, I, I, P, P, P, P, P, P, I, I, ctypes.c_float, P, Z, P],
+                           I),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)
@@ -340,6 +349,38 @@ def smlm_fanout_signal(ready_ptrs, stream=None, device=None):
     import torch
     st = _stream(stream, device if device is not None else torch.device("cuda", torch.cuda.current_device()))
     _check(_lib.smlm_fanout_signal(len(ready_ptrs), ctypes.cast(arr, ctypes.c_void_p), st), "smlm_fanout_signal")
+
+
+class AttnBatch:
+    """Host segment arrays of an attention call (include/smlm.h smlm_attn_batch), kept alive."""
+
+    def __init__(self, offsets, modes, cache_slots=None, past=None):
+        self.offsets = np.ascontiguousarray(offsets, np.int32)
+        self.modes = np.ascontiguousarray(modes, np.int8)
+        self.cache = None if cache_slots is None else np.ascontiguousarray(cache_slots, np.int32)
+        self.past = None if past is None else np.ascontiguousarray(past, np.int32)
+        self.c = smlm_attn_batch(int(self.offsets[-1]) if len(self.offsets) else 0, len(self.modes),
+                                 self.offsets.ctypes.data, self.modes.ctypes.data,
+                                 None if self.cache is None else self.cache.ctypes.data,
+                                 None if self.past is None else self.past.ctypes.data)
+
+
+def smlm_attention_workspace_size(batch: AttnBatch) -> int:
+    return int(_lib.smlm_attention_workspace_size(ctypes.byref(batch.c)))
+
+
+def smlm_attention(batch: AttnBatch, Q, K, V, O, K_cache=None, V_cache=None, scale=None, ws=None, stream=None):
+    """Q [S, Hq, 128], K/V [S, Hkv, 128], O [S, Hq, 128]; caches [slots, capacity, Hkv, 128] (bf16)."""
+    import math
+    import torch
+    nh, nkv, d = Q.shape[1], K.shape[1], Q.shape[2]
+    if ws is None:
+        ws = torch.empty(max(smlm_attention_workspace_size(batch), 256), dtype=torch.uint8, device=Q.device)
+    slots = 0 if K_cache is None else K_cache.shape[0]
+    cap = 0 if K_cache is None else K_cache.shape[1]
+    _check(_lib.smlm_attention(ctypes.byref(batch.c), nh, nkv, d, _ptr(Q), _ptr(K), _ptr(V), _ptr(O), _ptr(K_cache),
+                               _ptr(V_cache), slots, cap, 1.0 / math.sqrt(d) if scale is None else scale, _ptr(ws),
+                               ws.numel() * ws.element_size(), _stream(stream, Q.device)), "smlm_attention")
 
 
 def smlm_launch_count() -> int:
