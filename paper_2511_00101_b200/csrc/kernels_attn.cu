@@ -17,6 +17,8 @@
 #include <cuda_runtime.h>
 #include <math.h>
 
+#include <algorithm>
+
 #include "device_types.h"
 #include "pdl.cuh"
 #include "sm100.cuh"
@@ -291,30 +293,48 @@ __global__ void __launch_bounds__(256) attn_decode_kernel(const AttnArgs a) {
                               (size_t)rw.slot * a.cache_capacity * row_elems + kvh * 128;
     const __nv_bfloat16 *Vc = reinterpret_cast<const __nv_bfloat16 *>(a.V_cache) +
                               (size_t)rw.slot * a.cache_capacity * row_elems + kvh * 128;
-    // scores: thread per key, all G heads from one read of the key row
-    for (int j = threadIdx.x; j < L; j += blockDim.x) {
-        const uint4 *kr = reinterpret_cast<const uint4 *>(Kc + (size_t)j * row_elems);
-        float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-#pragma unroll 2
-        for (int v = 0; v < 16; ++v) {
-            const uint4 u = kr[v];
-            const __nv_bfloat162 *h2 = reinterpret_cast<const __nv_bfloat162 *>(&u);
+    // scores: a warp takes 8 keys at a time (4 lanes per key, 64 bytes each), so the warp streams
+    // 2 KB of K coalesced; all G heads from that one read, the 4 lanes of a key reduce by shuffles
+    {
+        const int kq = lane >> 2, part = lane & 3;
+        for (int j0 = warp * 8; j0 < L; j0 += 64) {
+            const int j = j0 + kq;
+            float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+            if (j < L) {
+                // lane part p reads dims 8p + 32v .. +8 (v = 0..3): the 4 lanes of a key cover each
+                // 64-byte stretch of its row together, and their q reads fall in distinct banks
+                const uint4 *kr = reinterpret_cast<const uint4 *>(Kc + (size_t)j * row_elems + 8 * part);
+                uint4 u[4];
 #pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                const float2 kf = __bfloat1622float2(h2[i]);
-                const int d = 8 * v + 2 * i;
+                for (int v = 0; v < 4; ++v) u[v] = kr[4 * v];
 #pragma unroll
-                for (int g = 0; g < 8; ++g)
-                    if (g < G) acc[g] = fmaf(kf.x, qs[g][d], fmaf(kf.y, qs[g][d + 1], acc[g]));
+                for (int v = 0; v < 4; ++v) {
+                    const __nv_bfloat162 *h2 = reinterpret_cast<const __nv_bfloat162 *>(&u[v]);
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        const float2 kf = __bfloat1622float2(h2[i]);
+                        const int d = 8 * part + 32 * v + 2 * i;
+#pragma unroll
+                        for (int g = 0; g < 8; ++g)
+                            if (g < G) acc[g] = fmaf(kf.x, qs[g][d], fmaf(kf.y, qs[g][d + 1], acc[g]));
+                    }
+                }
+            }
+#pragma unroll
+            for (int g = 0; g < 8; ++g) {
+                if (g < G) {
+                    float v = acc[g];
+                    v += __shfl_xor_sync(0xffffffffu, v, 1);
+                    v += __shfl_xor_sync(0xffffffffu, v, 2);
+                    if (part == 0 && j < L) sc[g * L + j] = v;
+                }
             }
         }
-#pragma unroll
-        for (int g = 0; g < 8; ++g)
-            if (g < G) sc[g * L + j] = acc[g];
     }
     __syncthreads();
+    __shared__ float inv_sum[8];
     if (warp < G) {
-        // softmax of head `warp` over the L scores (fp32), in place
+        // softmax of head `warp` over the L scores (fp32), in place (unnormalised; 1 / sum kept)
         float mx = -INFINITY;
         for (int j = lane; j < L; j += 32) mx = fmaxf(mx, sc[warp * L + j]);
 #pragma unroll
@@ -327,25 +347,66 @@ __global__ void __launch_bounds__(256) attn_decode_kernel(const AttnArgs a) {
         }
 #pragma unroll
         for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
-        __syncwarp();
-        // O = sum_j p_j v_j / sum: lane owns d = 4 lane .. 4 lane + 3 (256-byte V rows, coalesced)
-        float o[4] = {0.f, 0.f, 0.f, 0.f};
-        for (int j = 0; j < L; ++j) {
-            const float p = sc[warp * L + j];
-            const uint2 u = *reinterpret_cast<const uint2 *>(Vc + (size_t)j * row_elems + 4 * lane);
+        if (lane == 0) inv_sum[warp] = 1.f / sum;
+    }
+    __syncthreads();
+    // O = sum_j p_j v_j for ALL G heads from one read of each V row: a half-warp per key (lane owns
+    // dims 8 (l % 16) .. +8, 16-byte loads, 256 contiguous bytes per key), warp w takes key pairs
+    // j = 2w, 2w + 16, ...; loads of the next pair are issued before the current pair's FMAs
+    float o[8][8];
+#pragma unroll
+    for (int g = 0; g < 8; ++g)
+#pragma unroll
+        for (int e = 0; e < 8; ++e) o[g][e] = 0.f;
+    {
+        const int hk = lane >> 4, dq = lane & 15;
+        int j = 2 * warp + hk;
+        uint4 u = j < L ? *reinterpret_cast<const uint4 *>(Vc + (size_t)j * row_elems + 8 * dq) : make_uint4(0, 0, 0, 0);
+        for (; j < L; j += 16) {
+            const int jn = j + 16;
+            const uint4 un = jn < L ? *reinterpret_cast<const uint4 *>(Vc + (size_t)jn * row_elems + 8 * dq)
+                                    : make_uint4(0, 0, 0, 0);
             const __nv_bfloat162 *h2 = reinterpret_cast<const __nv_bfloat162 *>(&u);
-            const float2 v0 = __bfloat1622float2(h2[0]), v1 = __bfloat1622float2(h2[1]);
-            o[0] = fmaf(p, v0.x, o[0]);
-            o[1] = fmaf(p, v0.y, o[1]);
-            o[2] = fmaf(p, v1.x, o[2]);
-            o[3] = fmaf(p, v1.y, o[3]);
+            float vf[8];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const float2 t = __bfloat1622float2(h2[i]);
+                vf[2 * i] = t.x;
+                vf[2 * i + 1] = t.y;
+            }
+#pragma unroll
+            for (int g = 0; g < 8; ++g)
+                if (g < G) {
+                    const float p = sc[g * L + j];
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) o[g][e] = fmaf(p, vf[e], o[g][e]);
+                }
+            u = un;
         }
-        const float inv = 1.f / sum;
-        __nv_bfloat16 *O = reinterpret_cast<__nv_bfloat16 *>(a.O) + ((size_t)rw.row * a.n_heads + kvh * G + warp) * 128 + 4 * lane;
-        uint2 st;
-        st.x = pack_bf16x2(o[0] * inv, o[1] * inv);
-        st.y = pack_bf16x2(o[2] * inv, o[3] * inv);
-        *reinterpret_cast<uint2 *>(O) = st;
+#pragma unroll
+        for (int g = 0; g < 8; ++g)
+#pragma unroll
+            for (int e = 0; e < 8; ++e) o[g][e] += __shfl_xor_sync(0xffffffffu, o[g][e], 16);   // the two keys
+    }
+    __syncthreads();   // the scores are no longer needed: reuse their shared memory for partials
+    float *red = sc;   // [8 warps][G][128]
+    if (lane < 16) {
+#pragma unroll
+        for (int g = 0; g < 8; ++g)
+            if (g < G) {
+                float4 *dst = reinterpret_cast<float4 *>(red + ((size_t)warp * G + g) * 128 + 8 * lane);
+                dst[0] = make_float4(o[g][0], o[g][1], o[g][2], o[g][3]);
+                dst[1] = make_float4(o[g][4], o[g][5], o[g][6], o[g][7]);
+            }
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < G * 128; e += blockDim.x) {
+        const int g = e / 128, d = e % 128;
+        float acc = 0.f;
+#pragma unroll
+        for (int w = 0; w < 8; ++w) acc += red[((size_t)w * G + g) * 128 + d];   // fixed order
+        __nv_bfloat16 *O = reinterpret_cast<__nv_bfloat16 *>(a.O) + ((size_t)rw.row * a.n_heads + kvh * G + g) * 128 + d;
+        *O = __float2bfloat16_rn(acc * inv_sum[g]);
     }
 }
 
@@ -371,7 +432,9 @@ int launch_attn(const AttnArgs &a, int n_items, int n_rows, int n_drows, int max
         if (e != cudaSuccess) return (int)e;
     }
     if (n_drows) {
-        const size_t smem = (size_t)(a.n_heads / a.n_kv_heads) * max_dec_len * sizeof(float);
+        // scores [G][L], later reused for the 8 warps' partial outputs [8][G][128]
+        const size_t G = (size_t)(a.n_heads / a.n_kv_heads);
+        const size_t smem = std::max(G * max_dec_len, 8 * G * 128) * sizeof(float);
         e = cudaFuncSetAttribute(attn_decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return (int)e;
         e = launch_pdl(attn_decode_kernel, dim3(n_drows * a.n_kv_heads), dim3(256), smem, st, a);

@@ -13,6 +13,7 @@ import os
 import statistics
 import sys
 
+import numpy as np
 import torch
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -233,6 +234,9 @@ def main():
         print(json.dumps({"config": "C3-prefill", "uniform_r64_ms": t_u, "hetero_64_32_16_8_ms": t_h,
                           "ratio": t_h / t_u}), flush=True)
         return
+    if "--attention" in sys.argv:
+        print(json.dumps(attention_step()), flush=True)
+        return
     print(json.dumps(c2_layer_step(graphs="--c2-only" not in sys.argv)), flush=True)
     if "--c2-only" in sys.argv:
         return
@@ -243,6 +247,71 @@ def main():
         print(json.dumps({"config": synth.CONFIGS[k].name, "total_ms": tot,
                           "rows_per_s": synth.config_batch(k).S / (tot / 1e3),
                           "roofline_frac": sum(r["roofline_ms"] for r in rows) / tot}), flush=True)
+
+
+
+
+def attention_step(iters=20, past=1024):
+    """the Alg. 1 attention branch on the C4 batch structure at Llama-3-8B heads
+    (32 query / 8 KV heads, d = 128): 4 fine-tune x 1024 + 8 prefill (512-2048, KV cache written) +
+    128 decode rows each over a `past`-token cache.  Reports the prefill kernel's causal-attention
+    tensor TF/s (4 * sum(L(L+1)/2) * d * Hq flops over the F/E/P segments) and the decode kernel's
+    HBM GB/s (K + V cache bytes read), each timed alone with CUDA events (L2 flushed)."""
+    from oracle.attention import DECODE, FINETUNE, PREFILL
+    dev = torch.device("cuda", 0)
+    batch = synth.config_batch(4)
+    lens = np.diff(batch.offsets)
+    modes = list(batch.modes)
+    hq, hkv = 32, 8
+    slots, pasts, slot = [], [], 0
+    for L, m in zip(lens, modes):
+        if m in (PREFILL, DECODE):
+            slots.append(slot)
+            slot += 1
+        else:
+            slots.append(-1)
+        pasts.append(past if m == DECODE else 0)
+    S_ = int(batch.S)
+    g = torch.Generator(device=dev).manual_seed(5)
+    Q = torch.randn(S_, hq, 128, generator=g, device=dev).to(torch.bfloat16)
+    K = torch.randn(S_, hkv, 128, generator=g, device=dev).to(torch.bfloat16)
+    V = torch.randn(S_, hkv, 128, generator=g, device=dev).to(torch.bfloat16)
+    cap = max(2048, past + 8)
+    Kc = torch.randn(slot, cap, hkv, 128, generator=g, device=dev).to(torch.bfloat16)
+    Vc = torch.randn(slot, cap, hkv, 128, generator=g, device=dev).to(torch.bfloat16)
+    O = torch.empty_like(Q)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    offs = batch.offsets
+
+    def timed(sel_modes):
+        keep = [m in sel_modes for m in modes]
+        lengths = [int(L) if k else 0 for L, k in zip(lens, keep)]
+        b = S.AttnBatch(offs, modes, slots, pasts) if keep.count(True) == len(keep) else \
+            S.AttnBatch(np.concatenate([[0], np.cumsum(lengths)]).astype(np.int32), modes, slots, pasts)
+        ws = torch.empty(max(S.smlm_attention_workspace_size(b), 256), dtype=torch.uint8, device=dev)
+        ts = []
+        for it in range(iters + 3):
+            flush.zero_()
+            e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
+            e0.record()
+            S.smlm_attention(b, Q, K, V, O, Kc, Vc, ws=ws)
+            e1.record()
+            e1.synchronize()
+            if it >= 3:
+                ts.append(e0.elapsed_time(e1))
+        return statistics.median(ts)
+
+    ms_pf = timed((FINETUNE, 1, PREFILL))
+    ms_dec = timed((DECODE,))
+    fe = [(int(L), m) for L, m in zip(lens, modes) if m != DECODE and L > 0]
+    flops = sum(4.0 * L * (L + 1) / 2 * 128 * hq for L, _ in fe)
+    n_dec = int(sum(L for L, m in zip(lens, modes) if m == DECODE))
+    dec_bytes = n_dec * hkv * (past + 1) * 128 * 2 * 2
+    return {"workload": f"C4 batch, Llama-3-8B heads 32/8 d=128; decode rows over {past}-token caches",
+            "prefill_ms": ms_pf, "prefill_tflops": flops / ms_pf / 1e9,
+            "prefill_tensor_frac": flops / ms_pf / 1e9 / PEAKS["bf16_tflops"],
+            "decode_ms": ms_dec, "decode_GBs": dec_bytes / ms_dec / 1e6,
+            "decode_hbm_frac": dec_bytes / ms_dec / 1e6 / PEAKS["hbm_gbs"]}
 
 
 if __name__ == "__main__":
