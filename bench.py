@@ -582,6 +582,12 @@ def main():
                                    "rows_per_s": synth.config_batch(3).S / (tot3 / 1e3),
                                    "tensor_roofline_frac": sum(r["roofline_ms"] for r in rows3) / tot3,
                                    "bound": "tensor"}}
+            at = bc.attention_step()
+            side["F4_attention"] = {"workload": at["workload"], "prefill_ms": at["prefill_ms"],
+                                    "prefill_tflops": at["prefill_tflops"],
+                                    "prefill_tensor_roofline_frac": at["prefill_tensor_frac"],
+                                    "decode_ms": at["decode_ms"], "decode_GBs": at["decode_GBs"],
+                                    "decode_hbm_roofline_frac": at["decode_hbm_frac"]}
             ad = bc.adamw_step(layers=32)
             side["F3_adamw"] = {"workload": "AdamW step (clip 1.0 per job) over the C4 fine-tune adapters: 4 jobs x "
                                             "r=16 x 7 projections x 32 layers, one step per job", "n": ad["n"],
