@@ -2001,6 +2001,8 @@ int attn_plan(const smlm_attn_batch *b, int n_heads, int n_kv_heads, int head_di
             for (int qb = 0; qb * 128 < L; ++qb) P.items.push_back({a0, L, qb, 0});
         }
     }
+    // the longest items (most key blocks) first: the persistent CTAs finish together
+    std::stable_sort(P.items.begin(), P.items.end(), [](const AttnItem &x, const AttnItem &y) { return x.qb > y.qb; });
     const size_t dec_smem = (size_t)(n_heads / n_kv_heads) * P.max_dec_len * sizeof(float);
     if (dec_smem > 200 * 1024)
         return set_err(SMLM_E_UNSUPPORTED, "attention: decode context too long for the one-pass decode kernel "

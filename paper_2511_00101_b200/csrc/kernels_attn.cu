@@ -31,7 +31,7 @@ namespace {
 constexpr int kAT = 256;                 // prefill: 8 warps (0 TMA, 1 MMA, 2 TMEM alloc, 4-7 softmax)
 constexpr uint32_t kQBytes = 32768;      // 128 rows x 128 d bf16 (two 64-wide SW128 boxes)
 constexpr uint32_t kKVBytes = 65536;     // K tile (32 KB) + V tile (32 KB)
-constexpr uint32_t kPBytes = 32768;      // P: 128 rows x 128 keys bf16
+constexpr uint32_t kPBytes = 32768;      // P: 128 rows x 128 keys bf16 (two buffers)
 
 __device__ __forceinline__ float fast_exp2(float x) {
     float y;
@@ -39,7 +39,10 @@ __device__ __forceinline__ float fast_exp2(float x) {
     return y;
 }
 
-__global__ void __launch_bounds__(kAT, 1) attn_prefill_kernel(const __grid_constant__ AttnArgs a) {
+__global__ void __launch_bounds__(kAT, 1) attn_prefill_kernel(const __grid_constant__ AttnArgs a, int n_units) {
+    // persistent: CTA c takes work units c, c + grid, ... (unit = (128-query block, query head),
+    // the items sorted by key-block count, longest first); block counters run across units so
+    // the TMA ring, the S buffer and the P buffers stream from one unit into the next
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw = smem_u32(smem_raw);
     const uint32_t base = (raw + 1023u) & ~1023u;
@@ -47,22 +50,23 @@ __global__ void __launch_bounds__(kAT, 1) attn_prefill_kernel(const __grid_const
     const uint32_t q_s = base;
     auto kv_s = [&](int b) { return base + kQBytes + (uint32_t)b * kKVBytes; };
     const uint32_t p_s = base + kQBytes + 2 * kKVBytes;
-    const uint32_t bar = p_s + kPBytes;
-    const uint32_t q_full = bar, s_full = bar + 8, s_free = bar + 16, p_full = bar + 24, o_done = bar + 32;
-    auto kv_full = [&](int b) { return bar + 40u + 8u * b; };
-    auto kv_empty = [&](int b) { return bar + 56u + 8u * b; };
-    const uint32_t tmem_slot = bar + 72;
+    const uint32_t bar = p_s + 2 * kPBytes;
+    const uint32_t q_full = bar, q_empty = bar + 8, s_full = bar + 16, s_free = bar + 24, p_full = bar + 32;
+    auto o_done = [&](int b) { return bar + 40u + 8u * b; };   // PV_G committed, G % 2 == b (P buffer b free)
+    auto kv_full = [&](int b) { return bar + 56u + 8u * b; };
+    auto kv_empty = [&](int b) { return bar + 72u + 8u * b; };
+    const uint32_t tmem_slot = bar + 88;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int head = blockIdx.x % a.n_heads;
-    const int kvh = head / (a.n_heads / a.n_kv_heads);
+    const int group = a.n_heads / a.n_kv_heads;
     if (threadIdx.x == 0) {
         mbar_init(q_full, 1);
+        mbar_init(q_empty, 1);
         mbar_init(s_full, 1);
         mbar_init(s_free, 128);
         mbar_init(p_full, 128);
-        mbar_init(o_done, 1);
         for (int b = 0; b < 2; ++b) {
+            mbar_init(o_done(b), 1);
             mbar_init(kv_full(b), 1);
             mbar_init(kv_empty(b), 1);
         }
@@ -79,173 +83,189 @@ __global__ void __launch_bounds__(kAT, 1) attn_prefill_kernel(const __grid_const
     const uint32_t S_t = tmem, O_t = tmem + 128;
     pdl_wait();   // the item table is written by the stream's plan upload
     pdl_trigger();
-    const AttnItem it = a.items[blockIdx.x / a.n_heads];
-    const int nkb = it.qb + 1;                 // block-causal key range
-    const int q0 = it.row0 + it.qb * 128;      // first query row of the block
 
     if (warp == 0) {
         // ---------------- TMA producer ----------------
         if (lane == 0) {
-            mbar_expect_tx(q_full, kQBytes);
-            for (int db = 0; db < 2; ++db)
-                tma_load_2d(q_s + 16384u * db, &a.tmQ, q_full, head * 128 + 64 * db, q0);
-            for (int j = 0; j < nkb; ++j) {
-                const int b = j & 1;
-                mbar_wait(kv_empty(b), ((j >> 1) & 1) ^ 1);
-                mbar_expect_tx(kv_full(b), kKVBytes);
-                const int k0 = it.row0 + j * 128;
-                // K_j: B operand of S = Q K^T, K-major (rows = keys, 128 B of d per row)
+            int G = 0, u = 0;
+            for (int w = blockIdx.x; w < n_units; w += gridDim.x, ++u) {
+                const AttnItem it = a.items[w / a.n_heads];
+                const int head = w % a.n_heads, kvh = head / group, nkb = it.qb + 1;
+                if (u > 0) mbar_wait(q_empty, (u - 1) & 1);   // the previous unit's S MMAs read Q
+                mbar_expect_tx(q_full, kQBytes);
                 for (int db = 0; db < 2; ++db)
-                    tma_load_2d(kv_s(b) + 16384u * db, &a.tmK, kv_full(b), kvh * 128 + 64 * db, k0);
-                // V_j: B operand of O += P V, MN-major (rows = keys, 64-wide d boxes)
-                for (int kb = 0; kb < 2; ++kb)
+                    tma_load_2d(q_s + 16384u * db, &a.tmQ, q_full, head * 128 + 64 * db, it.row0 + it.qb * 128);
+                for (int j = 0; j < nkb; ++j, ++G) {
+                    const int b = G & 1;
+                    mbar_wait(kv_empty(b), ((G >> 1) & 1) ^ 1);
+                    mbar_expect_tx(kv_full(b), kKVBytes);
+                    const int k0 = it.row0 + j * 128;
+                    // K_j: B operand of S = Q K^T, K-major (rows = keys, 128 B of d per row)
                     for (int db = 0; db < 2; ++db)
-                        tma_load_2d(kv_s(b) + 32768u + 16384u * kb + 8192u * db, &a.tmV, kv_full(b),
-                                    kvh * 128 + 64 * db, k0 + 64 * kb);
+                        tma_load_2d(kv_s(b) + 16384u * db, &a.tmK, kv_full(b), kvh * 128 + 64 * db, k0);
+                    // V_j: B operand of O += P V, MN-major (rows = keys, 64-wide d boxes)
+                    for (int kb = 0; kb < 2; ++kb)
+                        for (int db = 0; db < 2; ++db)
+                            tma_load_2d(kv_s(b) + 32768u + 16384u * kb + 8192u * db, &a.tmV, kv_full(b),
+                                        kvh * 128 + 64 * db, k0 + 64 * kb);
+                }
             }
         }
     } else if (warp == 1) {
         // ---------------- MMA issuer ----------------
+        // order per block G: S_G (after the softmax has read S_{G-1}), then PV_{G-1} -- so S_G
+        // overlaps the softmax of G-1 and PV_{G-1} overlaps the softmax of G
         constexpr uint32_t idesc_s = idesc_bf16(128, 128, 0, 0);
         constexpr uint32_t idesc_o = idesc_bf16(128, 128, 0, 1);
-        auto issue_s = [&](int j) {
-            const int b = j & 1;
-            mbar_wait(kv_full(b), (j >> 1) & 1);
+        auto issue_pv = [&](int Gp, bool first) {
+            mbar_wait(p_full, Gp & 1);       // P_Gp in smem, O rescaled
             tc_fence_after();
+            const int b = Gp & 1;
             if (lane == 0) {
 #pragma unroll
                 for (int k = 0; k < 8; ++k) {
-                    const uint32_t off = 16384u * (k >> 2) + 32u * (k & 3);
-                    mma_bf16(S_t, smem_desc(q_s + off, 16, 1024, kSw128), smem_desc(kv_s(b) + off, 16, 1024, kSw128),
-                             idesc_s, k > 0);
+                    const uint32_t pa = p_s + (uint32_t)b * kPBytes + 16384u * (k >> 2) + 32u * (k & 3);
+                    const uint32_t vb = kv_s(b) + 32768u + 16384u * (k >> 2) + 2048u * (k & 3);
+                    mma_bf16(O_t, smem_desc(pa, 16, 1024, kSw128), smem_desc(vb, 8192, 1024, kSw128), idesc_o,
+                             (!first || k > 0) ? 1u : 0u);
                 }
-                mma_commit(s_full);
+                mma_commit(kv_empty(b));
+                mma_commit(o_done(b));
             }
             __syncwarp();
         };
-        mbar_wait(q_full, 0);
-        issue_s(0);
-        for (int j = 0; j < nkb; ++j) {
-            if (j + 1 < nkb) {
-                mbar_wait(s_free, j & 1);   // the softmax has read S_j
-                issue_s(j + 1);
-            }
-            mbar_wait(p_full, j & 1);       // P_j in smem, O rescaled
-            tc_fence_after();
-            const int b = j & 1;
-            if (lane == 0) {
+        int G = 0, u = 0;
+        for (int w = blockIdx.x; w < n_units; w += gridDim.x, ++u) {
+            const AttnItem it = a.items[w / a.n_heads];
+            const int nkb = it.qb + 1;
+            mbar_wait(q_full, u & 1);
+            for (int j = 0; j < nkb; ++j, ++G) {
+                if (G > 0) mbar_wait(s_free, (G - 1) & 1);   // the softmax has read S_{G-1}
+                const int b = G & 1;
+                mbar_wait(kv_full(b), (G >> 1) & 1);
+                tc_fence_after();
+                if (lane == 0) {
 #pragma unroll
-                for (int k = 0; k < 8; ++k) {
-                    const uint32_t pa = p_s + 16384u * (k >> 2) + 32u * (k & 3);
-                    const uint32_t vb = kv_s(b) + 32768u + 16384u * (k >> 2) + 2048u * (k & 3);
-                    mma_bf16(O_t, smem_desc(pa, 16, 1024, kSw128), smem_desc(vb, 8192, 1024, kSw128), idesc_o,
-                             (j > 0 || k > 0) ? 1u : 0u);
+                    for (int k = 0; k < 8; ++k) {
+                        const uint32_t off = 16384u * (k >> 2) + 32u * (k & 3);
+                        mma_bf16(S_t, smem_desc(q_s + off, 16, 1024, kSw128),
+                                 smem_desc(kv_s(b) + off, 16, 1024, kSw128), idesc_s, k > 0);
+                    }
+                    mma_commit(s_full);
+                    if (j == nkb - 1) mma_commit(q_empty);
                 }
-                mma_commit(kv_empty(b));
-                mma_commit(o_done);
+                __syncwarp();
+                if (j > 0) issue_pv(G - 1, j == 1);
             }
-            __syncwarp();
+            issue_pv(G - 1, nkb == 1);   // the unit's last block
         }
     } else if (warp >= 4) {
         // ---------------- online softmax + epilogue (thread = query row) ----------------
         const int m = threadIdx.x - 128;
         const uint32_t lane_base = (uint32_t)((warp - 4) * 32) << 16;
-        const int qi = it.qb * 128 + m;           // query position inside the segment
         const float sl2 = a.scale * 1.4426950408889634f;
-        float mi = -INFINITY, li = 0.f;
         uint8_t *pp = base_ptr + (p_s - base);
-        for (int j = 0; j < nkb; ++j) {
-            mbar_wait(s_full, j & 1);
-            tc_fence_after();
-            const int kbase = j * 128;
-            float mx = -INFINITY;
-#pragma unroll 1
-            for (int c = 0; c < 4; ++c) {
-                uint32_t r[32];
-                tmem_ld32(S_t + lane_base + 32u * c, r);
-                tmem_wait_ld();
-#pragma unroll
-                for (int e = 0; e < 32; ++e) {
-                    const int kj = kbase + 32 * c + e;
-                    if (kj <= qi && kj < it.len) mx = fmaxf(mx, __uint_as_float(r[e]) * sl2);
-                }
-            }
-            const float m_new = fmaxf(mi, mx);
-            const float alpha = fast_exp2(mi - m_new);   // 0 on the first block (mi = -inf)
-            float sum = 0.f;
-            if (j > 0) {
-                // P_{j-1} V_{j-1} has landed in O and the P buffer is free
-                mbar_wait(o_done, (j - 1) & 1);
+        int G = 0;
+        for (int w = blockIdx.x; w < n_units; w += gridDim.x) {
+            const AttnItem it = a.items[w / a.n_heads];
+            const int head = w % a.n_heads, nkb = it.qb + 1;
+            const int qi = it.qb * 128 + m;           // query position inside the segment
+            float mi = -INFINITY, li = 0.f;           // running max (log2 units) and sum
+            for (int j = 0; j < nkb; ++j, ++G) {
+                mbar_wait(s_full, G & 1);
                 tc_fence_after();
-            }
-#pragma unroll 1
-            for (int c = 0; c < 4; ++c) {
-                uint32_t r[32];
-                tmem_ld32(S_t + lane_base + 32u * c, r);
-                tmem_wait_ld();
-                uint32_t pk[16];
+                const int kbase = j * 128;
+                // the whole S row into registers, then S is free for S_{G+1} (it overlaps the exps)
+                uint32_t sr[128];
 #pragma unroll
-                for (int e = 0; e < 32; e += 2) {
-                    const int kj = kbase + 32 * c + e;
-                    const float p0 = (kj <= qi && kj < it.len) ? fast_exp2(__uint_as_float(r[e]) * sl2 - m_new) : 0.f;
-                    const float p1 = (kj + 1 <= qi && kj + 1 < it.len) ? fast_exp2(__uint_as_float(r[e + 1]) * sl2 - m_new)
-                                                                     : 0.f;
-                    const __nv_bfloat162 pb = __floats2bfloat162_rn(p0, p1);
-                    // the sum uses the rounded probabilities the MMA multiplies V with
-                    const float2 pr = __bfloat1622float2(pb);
-                    sum += pr.x + pr.y;
-                    pk[e >> 1] = *reinterpret_cast<const uint32_t *>(&pb);
-                }
-                // keys 32c .. 32c+31: 16-byte chunks 4c .. 4c+3 of the 128-key row (two 64-key blocks)
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    const int ch = 4 * c + q, kb = ch >> 3, cc = ch & 7;
-                    *reinterpret_cast<uint4 *>(pp + kb * 16384 + m * 128 + ((cc ^ (m & 7)) << 4)) =
-                        make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
-                }
-            }
-            tc_fence_before();
-            mbar_arrive(s_free);   // S may be overwritten by S_{j+1}
-            li = li * alpha + sum;
-            // tcgen05.ld / st are warp-collective: the rescale runs when any row of the warp needs it
-            if (j > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {
-#pragma unroll 1
                 for (int c = 0; c < 4; ++c) {
                     uint32_t r[32];
-                    tmem_ld32(O_t + lane_base + 32u * c, r);
-                    tmem_wait_ld();
+                    tmem_ld32(S_t + lane_base + 32u * c, r);
 #pragma unroll
-                    for (int e = 0; e < 32; ++e) r[e] = __float_as_uint(__uint_as_float(r[e]) * alpha);
-                    tmem_st32(O_t + lane_base + 32u * c, r);
+                    for (int e = 0; e < 32; ++e) sr[32 * c + e] = r[e];
                 }
-                tmem_wait_st();
-            }
-            mi = m_new;
-            fence_proxy_async_smem();   // P (generic stores) -> the MMA (async proxy)
-            tc_fence_before();
-            mbar_arrive(p_full);
-        }
-        mbar_wait(o_done, (nkb - 1) & 1);
-        tc_fence_after();
-        const float inv = 1.f / li;
-        const bool ok = qi < it.len;
-        __nv_bfloat16 *O = reinterpret_cast<__nv_bfloat16 *>(a.O) + ((size_t)(q0 + m) * a.n_heads + head) * 128;
+                tmem_wait_ld();
+                tc_fence_before();
+                mbar_arrive(s_free);
+                // keys visible to this row: kj <= qi and kj < len  <=>  kj - kbase < lim
+                const int lim = min(qi + 1, it.len) - kbase;
+                float mx = -INFINITY;
+#pragma unroll
+                for (int e = 0; e < 128; ++e)
+                    if (e < lim) mx = fmaxf(mx, __uint_as_float(sr[e]));
+                const float m_new = fmaxf(mi, mx * sl2);
+                const float alpha = fast_exp2(mi - m_new);   // 0 on the first block (mi = -inf)
+                const uint32_t pb = G & 1;
+                if (G >= 2) mbar_wait(o_done(pb), ((G >> 1) - 1) & 1);   // PV_{G-2} has read P buffer pb
+                float sum = 0.f;
+                uint8_t *pbuf = pp + pb * kPBytes;
+#pragma unroll
+                for (int ch = 0; ch < 16; ++ch) {   // 16-byte chunks of 8 keys: chunk ch of key block ch / 8
+                    uint32_t pk[4];
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const int e = 8 * ch + 2 * q;
+                        const float p0 = e < lim ? fast_exp2(__uint_as_float(sr[e]) * sl2 - m_new) : 0.f;
+                        const float p1 = e + 1 < lim ? fast_exp2(__uint_as_float(sr[e + 1]) * sl2 - m_new) : 0.f;
+                        const __nv_bfloat162 b2 = __floats2bfloat162_rn(p0, p1);
+                        // the sum uses the rounded probabilities the MMA multiplies V with
+                        const float2 pr = __bfloat1622float2(b2);
+                        sum += pr.x + pr.y;
+                        pk[q] = *reinterpret_cast<const uint32_t *>(&b2);
+                    }
+                    const int kb = ch >> 3, cc = ch & 7;
+                    *reinterpret_cast<uint4 *>(pbuf + kb * 16384 + m * 128 + ((cc ^ (m & 7)) << 4)) =
+                        make_uint4(pk[0], pk[1], pk[2], pk[3]);
+                }
+                li = li * alpha + sum;
+                if (j > 0) {
+                    // P_{G-1} V_{G-1} has landed in O: rescale it (warp-collective tcgen05.ld / st,
+                    // so the warp rescales when any of its rows needs it)
+                    mbar_wait(o_done((G - 1) & 1), ((G - 1) >> 1) & 1);
+                    tc_fence_after();
+                    if (__any_sync(0xffffffffu, alpha != 1.f)) {
 #pragma unroll 1
-        for (int c = 0; c < 4; ++c) {
-            uint32_t r[32];
-            tmem_ld32(O_t + lane_base + 32u * c, r);
-            tmem_wait_ld();
-            if (ok) {
+                        for (int c = 0; c < 4; ++c) {
+                            uint32_t r[32];
+                            tmem_ld32(O_t + lane_base + 32u * c, r);
+                            tmem_wait_ld();
 #pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    uint4 v;
-                    v.x = pack_bf16x2(__uint_as_float(r[8 * q + 0]) * inv, __uint_as_float(r[8 * q + 1]) * inv);
-                    v.y = pack_bf16x2(__uint_as_float(r[8 * q + 2]) * inv, __uint_as_float(r[8 * q + 3]) * inv);
-                    v.z = pack_bf16x2(__uint_as_float(r[8 * q + 4]) * inv, __uint_as_float(r[8 * q + 5]) * inv);
-                    v.w = pack_bf16x2(__uint_as_float(r[8 * q + 6]) * inv, __uint_as_float(r[8 * q + 7]) * inv);
-                    *reinterpret_cast<uint4 *>(O + 32 * c + 8 * q) = v;
+                            for (int e = 0; e < 32; ++e) r[e] = __float_as_uint(__uint_as_float(r[e]) * alpha);
+                            tmem_st32(O_t + lane_base + 32u * c, r);
+                        }
+                        tmem_wait_st();
+                    }
+                }
+                mi = m_new;
+                fence_proxy_async_smem();   // P (generic stores) -> the MMA (async proxy)
+                tc_fence_before();
+                mbar_arrive(p_full);
+            }
+            // epilogue of the unit: O / l -> bf16 rows of O [S, Hq, d]
+            mbar_wait(o_done((G - 1) & 1), ((G - 1) >> 1) & 1);
+            tc_fence_after();
+            const float inv = 1.f / li;
+            const bool ok = qi < it.len;
+            __nv_bfloat16 *O = reinterpret_cast<__nv_bfloat16 *>(a.O) +
+                               ((size_t)(it.row0 + qi) * a.n_heads + head) * 128;
+#pragma unroll 1
+            for (int c = 0; c < 4; ++c) {
+                uint32_t r[32];
+                tmem_ld32(O_t + lane_base + 32u * c, r);
+                tmem_wait_ld();
+                if (ok) {
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        uint4 v;
+                        v.x = pack_bf16x2(__uint_as_float(r[8 * q + 0]) * inv, __uint_as_float(r[8 * q + 1]) * inv);
+                        v.y = pack_bf16x2(__uint_as_float(r[8 * q + 2]) * inv, __uint_as_float(r[8 * q + 3]) * inv);
+                        v.z = pack_bf16x2(__uint_as_float(r[8 * q + 4]) * inv, __uint_as_float(r[8 * q + 5]) * inv);
+                        v.w = pack_bf16x2(__uint_as_float(r[8 * q + 6]) * inv, __uint_as_float(r[8 * q + 7]) * inv);
+                        *reinterpret_cast<uint4 *>(O + 32 * c + 8 * q) = v;
+                    }
                 }
             }
+            tc_fence_before();   // the O reads are ordered before the next unit's p_full
         }
     }
     tc_fence_before();
@@ -412,7 +432,7 @@ __global__ void __launch_bounds__(256) attn_decode_kernel(const AttnArgs a) {
 
 }  // namespace
 
-size_t attn_prefill_smem() { return 1024 + kQBytes + 2 * kKVBytes + kPBytes + 256; }
+size_t attn_prefill_smem() { return 1024 + kQBytes + 2 * kKVBytes + 2 * kPBytes + 128; }
 
 int launch_attn(const AttnArgs &a, int n_items, int n_rows, int n_drows, int max_dec_len, cudaStream_t st) {
     cudaError_t e = cudaSuccess;
@@ -428,7 +448,12 @@ int launch_attn(const AttnArgs &a, int n_items, int n_rows, int n_drows, int max
             if (e != cudaSuccess) return (int)e;
             attr = true;
         }
-        e = launch_pdl(attn_prefill_kernel, dim3(n_items * a.n_heads), dim3(kAT), attn_prefill_smem(), st, a);
+        int sms = 0, dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        const int units = n_items * a.n_heads;
+        e = launch_pdl(attn_prefill_kernel, dim3(units < sms ? units : sms), dim3(kAT), attn_prefill_smem(), st, a,
+                       units);
         if (e != cudaSuccess) return (int)e;
     }
     if (n_drows) {
