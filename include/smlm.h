@@ -330,9 +330,10 @@ SMLM_API int smlm_adamw_step_reduce(float *param, float *exp_avg, float *exp_avg
  *   Q [S, n_heads, 128], K / V [S, n_kv_heads, 128], O [S, n_heads, 128] bf16 (the projections'
  *   outputs: position encoding, e.g. RoPE, is applied by the caller); K_cache / V_cache
  *   [cache_slots, cache_capacity, n_kv_heads, 128] bf16; scale = softmax scale (1/sqrt(128)).
- *   head_dim must be 128; n_heads / n_kv_heads <= 8; decode: group * (past + L) * 4 <= 200 KB.
+ *   head_dim must be 128; n_heads / n_kv_heads in {1, 2, 4, 8}.
  *   Host arrays: seg_offsets [G+1], seg_mode [G], seg_cache [G] (or NULL: no cache use),
- *   seg_past [G] (or NULL: 0).  ws: >= smlm_attention_workspace_size(batch) bytes (device).
+ *   seg_past [G] (or NULL: 0).  ws: >= smlm_attention_workspace_size(batch, n_heads, n_kv_heads)
+ *   bytes (device): the plan and the split-KV partials of the decode rows.
  * Forward only (fine-tune rows' attention gradients are outside the SMLM path).
  * Errors: SMLM_E_INVALID, SMLM_E_SHAPE, SMLM_E_UNSUPPORTED, SMLM_E_WORKSPACE, SMLM_E_CUDA.
  */
@@ -344,7 +345,7 @@ typedef struct {
     const int32_t *seg_cache;
     const int32_t *seg_past;
 } smlm_attn_batch;
-SMLM_API size_t smlm_attention_workspace_size(const smlm_attn_batch *batch);
+SMLM_API size_t smlm_attention_workspace_size(const smlm_attn_batch *batch, int n_heads, int n_kv_heads);
 SMLM_API int smlm_attention(const smlm_attn_batch *batch, int n_heads, int n_kv_heads, int head_dim, const void *Q,
                             const void *K, const void *V, void *O, void *K_cache, void *V_cache, int cache_slots,
                             int cache_capacity, float scale, void *ws, size_t ws_bytes, void *stream);

@@ -1970,8 +1970,9 @@ int attn_plan(const smlm_attn_batch *b, int n_heads, int n_kv_heads, int head_di
               AttnPlan &P) {
     if (!b) return set_err(SMLM_E_INVALID, "batch is NULL");
     if (head_dim != 128) return set_err(SMLM_E_UNSUPPORTED, "attention: head_dim must be 128");
-    if (n_heads < 1 || n_kv_heads < 1 || n_heads % n_kv_heads || n_heads / n_kv_heads > 8)
-        return set_err(SMLM_E_SHAPE, "attention: n_heads must be a multiple of n_kv_heads, group <= 8");
+    if (n_heads < 1 || n_kv_heads < 1 || n_heads % n_kv_heads ||
+        (n_heads / n_kv_heads != 1 && n_heads / n_kv_heads != 2 && n_heads / n_kv_heads != 4 && n_heads / n_kv_heads != 8))
+        return set_err(SMLM_E_SHAPE, "attention: n_heads must be 1, 2, 4 or 8 times n_kv_heads");
     if (b->S < 0 || b->G < 0 || (b->G > 0 && (!b->seg_offsets || !b->seg_mode)))
         return set_err(SMLM_E_INVALID, "attention: bad batch arrays");
     if (b->G == 0) return b->S == 0 ? SMLM_OK : set_err(SMLM_E_INVALID, "G == 0 but S != 0");
@@ -2003,21 +2004,25 @@ int attn_plan(const smlm_attn_batch *b, int n_heads, int n_kv_heads, int head_di
     }
     // the longest items (most key blocks) first: the persistent CTAs finish together
     std::stable_sort(P.items.begin(), P.items.end(), [](const AttnItem &x, const AttnItem &y) { return x.qb > y.qb; });
-    const size_t dec_smem = (size_t)(n_heads / n_kv_heads) * P.max_dec_len * sizeof(float);
-    if (dec_smem > 200 * 1024)
-        return set_err(SMLM_E_UNSUPPORTED, "attention: decode context too long for the one-pass decode kernel "
-                                           "(group * cache length * 4 bytes <= 200 KB)");
     return SMLM_OK;
 }
 smlm_pool_s g_attn_stage;   // pinned staging of the attention plans (no adapter pool involved)
 }  // namespace
 
-size_t smlm_attention_workspace_size(const smlm_attn_batch *b) {
-    if (!b) return 0;
+static size_t attn_plan_bytes(const AttnPlan &P) {
+    return align256(P.items.size() * sizeof(AttnItem) + P.rows.size() * sizeof(AttnRow) +
+                    P.drows.size() * sizeof(AttnRow) + 64);
+}
+static size_t attn_part_bytes(const AttnPlan &P, int n_heads, int n_kv_heads) {
+    const size_t splits = (size_t)(P.max_dec_len + 255) / 256;
+    return align256(P.drows.size() * (size_t)n_heads * splits * 130 * sizeof(float));
+}
+
+size_t smlm_attention_workspace_size(const smlm_attn_batch *b, int n_heads, int n_kv_heads) {
+    if (!b || n_heads < 1 || n_kv_heads < 1) return 0;
     AttnPlan P;
-    if (attn_plan(b, 1, 1, 128, 1 << 30, 1 << 30, P) != SMLM_OK) return 0;
-    return align256(P.items.size() * sizeof(AttnItem) + 16) + align256(P.rows.size() * sizeof(AttnRow) + 16) +
-           align256(P.drows.size() * sizeof(AttnRow) + 16) + 256;
+    if (attn_plan(b, n_heads, n_kv_heads, 128, 1 << 30, 1 << 30, P) != SMLM_OK) return 0;
+    return attn_plan_bytes(P) + attn_part_bytes(P, n_heads, n_kv_heads) + 256;
 }
 
 int smlm_attention(const smlm_attn_batch *b, int n_heads, int n_kv_heads, int head_dim, const void *Q, const void *K,
@@ -2031,7 +2036,7 @@ int smlm_attention(const smlm_attn_batch *b, int n_heads, int n_kv_heads, int he
     if ((!P.rows.empty() || !P.drows.empty()) && (!K_cache || !V_cache))
         return set_err(SMLM_E_INVALID, "attention: prefill-with-cache / decode segments need K_cache and V_cache");
     if (!(scale > 0.f) || !std::isfinite(scale)) return set_err(SMLM_E_INVALID, "attention: scale must be finite, > 0");
-    const size_t need = smlm_attention_workspace_size(b);
+    const size_t need = attn_plan_bytes(P) + attn_part_bytes(P, n_heads, n_kv_heads) + 256;
     if (!ws || ws_bytes < need) return set_err(SMLM_E_WORKSPACE, "workspace too small");
     int sms = 0;
     if ((rc = current_sm100_sms(&sms))) return rc;
@@ -2067,6 +2072,8 @@ int smlm_attention(const smlm_attn_batch *b, int n_heads, int n_kv_heads, int he
     a.n_kv_heads = n_kv_heads;
     a.cache_capacity = cache_capacity;
     a.scale = scale;
+    a.max_splits = (P.max_dec_len + 255) / 256;
+    a.dpart = reinterpret_cast<float *>(wsb + attn_plan_bytes(P));
     const int nl = (P.rows.empty() ? 0 : 1) + (P.items.empty() ? 0 : 1) + (P.drows.empty() ? 0 : 1);
     CKL(launch_attn(a, (int)P.items.size(), (int)P.rows.size(), (int)P.drows.size(), P.max_dec_len, st), nl);
     return SMLM_OK;

@@ -293,6 +293,8 @@ struct AttnArgs {
     int n_heads, n_kv_heads;
     int cache_capacity;
     float scale;
+    float *dpart;      // decode split partials [drows * n_kv_heads * max_splits][G][130] fp32
+    int max_splits;    // ceil(longest decode context / 256)
 };
 
 // fused cross-rank gradient reduction: every rank's ready counter (peer-mapped)

@@ -9,10 +9,10 @@
 //                            registers, O rescaled in TMEM when the max moves) -> P (bf16, smem) ->
 //                            O += P V_j (N=d, K=128 keys, V as the MN-major operand); K/V tiles by
 //                            TMA in a 2-deep ring; S_{j+1} is issued while the softmax of j runs.
-//   attn_decode_kernel     : one CTA per (decode row, KV head), HBM-bound: the G query heads of the
-//                            group (one warp each) score every cached key (each K row read once
-//                            for all G heads, 128-bit loads), softmax in fp32, then P V with lanes
-//                            over the head dimension (coalesced 256-byte V rows).
+//   attn_decode_split_kernel + attn_decode_combine_kernel : split-KV decode, HBM-bound: CTA per
+//                            (decode row, KV head, 256-key chunk) -- each K and V row read once for
+//                            all G query heads of the group, 64 KB of loads in flight per CTA --
+//                            then the splits merged in order (max, sum, o rescaled in fp32).
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <math.h>
@@ -294,139 +294,164 @@ __global__ void __launch_bounds__(256) attn_kv_write_kernel(const AttnArgs a) {
     }
 }
 
-// ---- decode: one CTA per (decode row, KV head); warp g = query head kvh * G + g ----
-__global__ void __launch_bounds__(256) attn_decode_kernel(const AttnArgs a) {
-    extern __shared__ float sc[];   // [G][L] scores -> probabilities
+// ---- decode (split-KV): CTA (decode row, KV head, split) scores its 256 cached keys for the G query
+// heads of the group (thread per key: the whole 256-byte K row requested at once, so each CTA has
+// 64 KB of loads in flight), takes the chunk's softmax statistics, and accumulates P V with 16
+// threads per V row (16-byte loads); partial (max, sum, o) per head go to the workspace and
+// attn_decode_combine_kernel merges the splits in split order ----
+constexpr int kDecChunk = 256;
+
+template <int G>
+__global__ void __launch_bounds__(256) attn_decode_split_kernel(const AttnArgs a) {
     pdl_wait();
     pdl_trigger();
-    const int G = a.n_heads / a.n_kv_heads;
-    const AttnRow rw = a.drows[blockIdx.x / a.n_kv_heads];
-    const int kvh = blockIdx.x % a.n_kv_heads;
+    const int s = blockIdx.x % a.max_splits;
+    const int rk = blockIdx.x / a.max_splits;
+    const AttnRow rw = a.drows[rk / a.n_kv_heads];
+    const int kvh = rk % a.n_kv_heads;
     const int L = rw.pos + 1;   // the cache holds the row itself (appended by attn_kv_write_kernel)
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    __shared__ float qs[8][128];
+    const int j0 = s * kDecChunk;
+    if (j0 >= L) return;
+    const int nk = min(kDecChunk, L - j0);
+    __shared__ float qs[G][128];
+    __shared__ float sc[G][kDecChunk];
+    __shared__ float red[8][G][128];   // [warp][head][128] partial outputs
+    __shared__ float mloc[G];
     const __nv_bfloat16 *Q = reinterpret_cast<const __nv_bfloat16 *>(a.Q) + ((size_t)rw.row * a.n_heads + kvh * G) * 128;
     for (int e = threadIdx.x; e < G * 128; e += blockDim.x) qs[e / 128][e % 128] = __bfloat162float(Q[e]) * a.scale;
     __syncthreads();
     const size_t row_elems = (size_t)a.n_kv_heads * 128;
     const __nv_bfloat16 *Kc = reinterpret_cast<const __nv_bfloat16 *>(a.K_cache) +
-                              (size_t)rw.slot * a.cache_capacity * row_elems + kvh * 128;
+                              ((size_t)rw.slot * a.cache_capacity + j0) * row_elems + kvh * 128;
     const __nv_bfloat16 *Vc = reinterpret_cast<const __nv_bfloat16 *>(a.V_cache) +
-                              (size_t)rw.slot * a.cache_capacity * row_elems + kvh * 128;
-    // scores: a warp takes 8 keys at a time (4 lanes per key, 64 bytes each), so the warp streams
-    // 2 KB of K coalesced; all G heads from that one read, the 4 lanes of a key reduce by shuffles
-    {
-        const int kq = lane >> 2, part = lane & 3;
-        for (int j0 = warp * 8; j0 < L; j0 += 64) {
-            const int j = j0 + kq;
-            float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-            if (j < L) {
-                // lane part p reads dims 8p + 32v .. +8 (v = 0..3): the 4 lanes of a key cover each
-                // 64-byte stretch of its row together, and their q reads fall in distinct banks
-                const uint4 *kr = reinterpret_cast<const uint4 *>(Kc + (size_t)j * row_elems + 8 * part);
-                uint4 u[4];
+                              ((size_t)rw.slot * a.cache_capacity + j0) * row_elems + kvh * 128;
+    const int t = threadIdx.x;
+    if (t < nk) {
+        const uint4 *kr = reinterpret_cast<const uint4 *>(Kc + (size_t)t * row_elems);
+        uint4 u[16];
 #pragma unroll
-                for (int v = 0; v < 4; ++v) u[v] = kr[4 * v];
+        for (int v = 0; v < 16; ++v) u[v] = kr[v];
+        float acc[G];
 #pragma unroll
-                for (int v = 0; v < 4; ++v) {
-                    const __nv_bfloat162 *h2 = reinterpret_cast<const __nv_bfloat162 *>(&u[v]);
+        for (int g = 0; g < G; ++g) acc[g] = 0.f;
 #pragma unroll
-                    for (int i = 0; i < 4; ++i) {
-                        const float2 kf = __bfloat1622float2(h2[i]);
-                        const int d = 8 * part + 32 * v + 2 * i;
-#pragma unroll
-                        for (int g = 0; g < 8; ++g)
-                            if (g < G) acc[g] = fmaf(kf.x, qs[g][d], fmaf(kf.y, qs[g][d + 1], acc[g]));
-                    }
-                }
-            }
-#pragma unroll
-            for (int g = 0; g < 8; ++g) {
-                if (g < G) {
-                    float v = acc[g];
-                    v += __shfl_xor_sync(0xffffffffu, v, 1);
-                    v += __shfl_xor_sync(0xffffffffu, v, 2);
-                    if (part == 0 && j < L) sc[g * L + j] = v;
-                }
-            }
-        }
-    }
-    __syncthreads();
-    __shared__ float inv_sum[8];
-    if (warp < G) {
-        // softmax of head `warp` over the L scores (fp32), in place (unnormalised; 1 / sum kept)
-        float mx = -INFINITY;
-        for (int j = lane; j < L; j += 32) mx = fmaxf(mx, sc[warp * L + j]);
-#pragma unroll
-        for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-        float sum = 0.f;
-        for (int j = lane; j < L; j += 32) {
-            const float p = __expf(sc[warp * L + j] - mx);
-            sc[warp * L + j] = p;
-            sum += p;
-        }
-#pragma unroll
-        for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
-        if (lane == 0) inv_sum[warp] = 1.f / sum;
-    }
-    __syncthreads();
-    // O = sum_j p_j v_j for ALL G heads from one read of each V row: a half-warp per key (lane owns
-    // dims 8 (l % 16) .. +8, 16-byte loads, 256 contiguous bytes per key), warp w takes key pairs
-    // j = 2w, 2w + 16, ...; loads of the next pair are issued before the current pair's FMAs
-    float o[8][8];
-#pragma unroll
-    for (int g = 0; g < 8; ++g)
-#pragma unroll
-        for (int e = 0; e < 8; ++e) o[g][e] = 0.f;
-    {
-        const int hk = lane >> 4, dq = lane & 15;
-        int j = 2 * warp + hk;
-        uint4 u = j < L ? *reinterpret_cast<const uint4 *>(Vc + (size_t)j * row_elems + 8 * dq) : make_uint4(0, 0, 0, 0);
-        for (; j < L; j += 16) {
-            const int jn = j + 16;
-            const uint4 un = jn < L ? *reinterpret_cast<const uint4 *>(Vc + (size_t)jn * row_elems + 8 * dq)
-                                    : make_uint4(0, 0, 0, 0);
-            const __nv_bfloat162 *h2 = reinterpret_cast<const __nv_bfloat162 *>(&u);
-            float vf[8];
+        for (int v = 0; v < 16; ++v) {
+            const __nv_bfloat162 *h2 = reinterpret_cast<const __nv_bfloat162 *>(&u[v]);
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
-                const float2 t = __bfloat1622float2(h2[i]);
-                vf[2 * i] = t.x;
-                vf[2 * i + 1] = t.y;
-            }
+                const float2 kf = __bfloat1622float2(h2[i]);
+                const int d = 8 * v + 2 * i;
 #pragma unroll
-            for (int g = 0; g < 8; ++g)
-                if (g < G) {
-                    const float p = sc[g * L + j];
+                for (int g = 0; g < G; ++g) acc[g] = fmaf(kf.x, qs[g][d], fmaf(kf.y, qs[g][d + 1], acc[g]));
+            }
+        }
+#pragma unroll
+        for (int g = 0; g < G; ++g) sc[g][t] = acc[g];
+    }
+    __syncthreads();
+    const int warp = t >> 5, lane = t & 31;
+    if (warp < G) {   // the chunk's max per head, then p = exp(s - max) in place
+        float mx = -INFINITY;
+        for (int j = lane; j < nk; j += 32) mx = fmaxf(mx, sc[warp][j]);
+#pragma unroll
+        for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        for (int j = lane; j < nk; j += 32) sc[warp][j] = __expf(sc[warp][j] - mx);
+        if (lane == 0) mloc[warp] = mx;
+    }
+    __syncthreads();
+    // P V: thread (key group kq, dims 8 dq .. 8 dq + 7); 16 keys per round, all 16 rounds' loads first
+    const int kq = t >> 4, dq = t & 15;
+    float o[G][8];
+#pragma unroll
+    for (int g = 0; g < G; ++g)
+#pragma unroll
+        for (int e = 0; e < 8; ++e) o[g][e] = 0.f;
+#pragma unroll 1
+    for (int r0 = 0; r0 < 16; r0 += 8) {
+        uint4 u[8];
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+            const int j = kq + 16 * (r0 + r);
+            u[r] = j < nk ? *reinterpret_cast<const uint4 *>(Vc + (size_t)j * row_elems + 8 * dq) : make_uint4(0, 0, 0, 0);
+        }
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+            const int j = kq + 16 * (r0 + r);
+            if (j < nk) {
+                const __nv_bfloat162 *h2 = reinterpret_cast<const __nv_bfloat162 *>(&u[r]);
+                float vf[8];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const float2 f2 = __bfloat1622float2(h2[i]);
+                    vf[2 * i] = f2.x;
+                    vf[2 * i + 1] = f2.y;
+                }
+#pragma unroll
+                for (int g = 0; g < G; ++g) {
+                    const float p = sc[g][j];
 #pragma unroll
                     for (int e = 0; e < 8; ++e) o[g][e] = fmaf(p, vf[e], o[g][e]);
                 }
-            u = un;
+            }
         }
-#pragma unroll
-        for (int g = 0; g < 8; ++g)
-#pragma unroll
-            for (int e = 0; e < 8; ++e) o[g][e] += __shfl_xor_sync(0xffffffffu, o[g][e], 16);   // the two keys
     }
-    __syncthreads();   // the scores are no longer needed: reuse their shared memory for partials
-    float *red = sc;   // [8 warps][G][128]
+    // the two key groups of a warp (lanes l and l + 16 share dims) by a shuffle, then per warp in smem
+#pragma unroll
+    for (int g = 0; g < G; ++g)
+#pragma unroll
+        for (int e = 0; e < 8; ++e) o[g][e] += __shfl_xor_sync(0xffffffffu, o[g][e], 16);
     if (lane < 16) {
 #pragma unroll
-        for (int g = 0; g < 8; ++g)
-            if (g < G) {
-                float4 *dst = reinterpret_cast<float4 *>(red + ((size_t)warp * G + g) * 128 + 8 * lane);
-                dst[0] = make_float4(o[g][0], o[g][1], o[g][2], o[g][3]);
-                dst[1] = make_float4(o[g][4], o[g][5], o[g][6], o[g][7]);
-            }
+        for (int g = 0; g < G; ++g) {
+            float4 *dst = reinterpret_cast<float4 *>(&red[warp][g][8 * dq]);
+            dst[0] = make_float4(o[g][0], o[g][1], o[g][2], o[g][3]);
+            dst[1] = make_float4(o[g][4], o[g][5], o[g][6], o[g][7]);
+        }
     }
     __syncthreads();
-    for (int e = threadIdx.x; e < G * 128; e += blockDim.x) {
+    // partial of this split: [g] {max, sum, o[128]} in fp32, key groups summed in order
+    float *part = a.dpart + (((size_t)rk * a.max_splits + s) * G) * 130;
+    for (int e = t; e < G * 128; e += blockDim.x) {
         const int g = e / 128, d = e % 128;
         float acc = 0.f;
 #pragma unroll
-        for (int w = 0; w < 8; ++w) acc += red[((size_t)w * G + g) * 128 + d];   // fixed order
-        __nv_bfloat16 *O = reinterpret_cast<__nv_bfloat16 *>(a.O) + ((size_t)rw.row * a.n_heads + kvh * G + g) * 128 + d;
-        *O = __float2bfloat16_rn(acc * inv_sum[g]);
+        for (int q = 0; q < 8; ++q) acc += red[q][g][d];
+        part[g * 130 + 2 + d] = acc;
+    }
+    if (warp < G) {
+        float l = 0.f;
+        for (int j = lane; j < nk; j += 32) l += sc[warp][j];
+#pragma unroll
+        for (int off = 16; off; off >>= 1) l += __shfl_xor_sync(0xffffffffu, l, off);
+        if (lane == 0) {
+            part[warp * 130 + 0] = mloc[warp];
+            part[warp * 130 + 1] = l;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(128) attn_decode_combine_kernel(const AttnArgs a) {
+    pdl_wait();
+    pdl_trigger();
+    const int G = a.n_heads / a.n_kv_heads;
+    const int rk = blockIdx.x;
+    const AttnRow rw = a.drows[rk / a.n_kv_heads];
+    const int kvh = rk % a.n_kv_heads;
+    const int ns = (rw.pos + 1 + kDecChunk - 1) / kDecChunk;
+    const int d = threadIdx.x;
+    for (int g = 0; g < G; ++g) {
+        const float *p0 = a.dpart + ((size_t)rk * a.max_splits * G + g) * 130;
+        float M = -INFINITY;
+        for (int s = 0; s < ns; ++s) M = fmaxf(M, p0[(size_t)s * G * 130]);
+        float l = 0.f, o = 0.f;
+        for (int s = 0; s < ns; ++s) {   // split order
+            const float *p = p0 + (size_t)s * G * 130;
+            const float w = __expf(p[0] - M);
+            l = fmaf(w, p[1], l);
+            o = fmaf(w, p[2 + d], o);
+        }
+        __nv_bfloat16 *O = reinterpret_cast<__nv_bfloat16 *>(a.O) + ((size_t)rw.row * a.n_heads + kvh * G + g) * 128;
+        O[d] = __float2bfloat16_rn(o / l);
     }
 }
 
@@ -457,12 +482,16 @@ int launch_attn(const AttnArgs &a, int n_items, int n_rows, int n_drows, int max
         if (e != cudaSuccess) return (int)e;
     }
     if (n_drows) {
-        // scores [G][L], later reused for the 8 warps' partial outputs [8][G][128]
-        const size_t G = (size_t)(a.n_heads / a.n_kv_heads);
-        const size_t smem = std::max(G * max_dec_len, 8 * G * 128) * sizeof(float);
-        e = cudaFuncSetAttribute(attn_decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        const dim3 grid(n_drows * a.n_kv_heads * a.max_splits);
+        switch (a.n_heads / a.n_kv_heads) {
+            case 1: e = launch_pdl(attn_decode_split_kernel<1>, grid, dim3(256), 0, st, a); break;
+            case 2: e = launch_pdl(attn_decode_split_kernel<2>, grid, dim3(256), 0, st, a); break;
+            case 4: e = launch_pdl(attn_decode_split_kernel<4>, grid, dim3(256), 0, st, a); break;
+            case 8: e = launch_pdl(attn_decode_split_kernel<8>, grid, dim3(256), 0, st, a); break;
+            default: return (int)cudaErrorInvalidValue;
+        }
         if (e != cudaSuccess) return (int)e;
-        e = launch_pdl(attn_decode_kernel, dim3(n_drows * a.n_kv_heads), dim3(256), smem, st, a);
+        e = launch_pdl(attn_decode_combine_kernel, dim3(n_drows * a.n_kv_heads), dim3(128), 0, st, a);
     }
     return (int)e;
 }

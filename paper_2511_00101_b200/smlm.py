@@ -94,7 +94,7 @@ def _load():
         "smlm_pool_set_grad_fanout": ([P, I, P], I),
         "smlm_fanout_signal": ([I, P, P], I),
         "smlm_fanout_wait": ([P, I, P], I),
-        "smlm_attention_workspace_size": ([ctypes.POINTER(smlm_attn_batch)], Z),
+        "smlm_attention_workspace_size": ([ctypes.POINTER(smlm_attn_batch), I, I], Z),
         "smlm_attention": ([ctypes.POINTER(smlm_attn_batch), I, I, I, P, P, P, P, P, P, I, I, ctypes.c_float, P, Z, P],
                            I),
     }
@@ -365,8 +365,8 @@ class AttnBatch:
                                  None if self.past is None else self.past.ctypes.data)
 
 
-def smlm_attention_workspace_size(batch: AttnBatch) -> int:
-    return int(_lib.smlm_attention_workspace_size(ctypes.byref(batch.c)))
+def smlm_attention_workspace_size(batch: AttnBatch, n_heads: int, n_kv_heads: int) -> int:
+    return int(_lib.smlm_attention_workspace_size(ctypes.byref(batch.c), n_heads, n_kv_heads))
 
 
 def smlm_attention(batch: AttnBatch, Q, K, V, O, K_cache=None, V_cache=None, scale=None, ws=None, stream=None):
@@ -375,7 +375,7 @@ def smlm_attention(batch: AttnBatch, Q, K, V, O, K_cache=None, V_cache=None, sca
     import torch
     nh, nkv, d = Q.shape[1], K.shape[1], Q.shape[2]
     if ws is None:
-        ws = torch.empty(max(smlm_attention_workspace_size(batch), 256), dtype=torch.uint8, device=Q.device)
+        ws = torch.empty(max(smlm_attention_workspace_size(batch, nh, nkv), 256), dtype=torch.uint8, device=Q.device)
     slots = 0 if K_cache is None else K_cache.shape[0]
     cap = 0 if K_cache is None else K_cache.shape[1]
     _check(_lib.smlm_attention(ctypes.byref(batch.c), nh, nkv, d, _ptr(Q), _ptr(K), _ptr(V), _ptr(O), _ptr(K_cache),

@@ -288,7 +288,7 @@ def attention_step(iters=20, past=1024):
         lengths = [int(L) if k else 0 for L, k in zip(lens, keep)]
         b = S.AttnBatch(offs, modes, slots, pasts) if keep.count(True) == len(keep) else \
             S.AttnBatch(np.concatenate([[0], np.cumsum(lengths)]).astype(np.int32), modes, slots, pasts)
-        ws = torch.empty(max(S.smlm_attention_workspace_size(b), 256), dtype=torch.uint8, device=dev)
+        ws = torch.empty(max(S.smlm_attention_workspace_size(b, hq, hkv), 256), dtype=torch.uint8, device=dev)
         ts = []
         for it in range(iters + 3):
             flush.zero_()
