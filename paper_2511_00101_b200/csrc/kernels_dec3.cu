@@ -125,6 +125,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT3, 1) smlm_dec3_ke
     auto a_addr = [&](int s) { return base + s * kStage3; };
     auto b_addr = [&](int s) { return base + s * kStage3 + kA3; };
 
+    if (threadIdx.x == 0) dbg_stamp(a, 10);   // entry (stamp 0: setup done, after the grid-dependency wait)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t rank = cluster_rank();
     const bool leader = rank == 0;

@@ -88,9 +88,7 @@ for name, ws, nn in (("qkv", wsq, nq), ("o", wso, no)):
     t = ws[nn - 148 * 128:nn].view(torch.int64).view(148, 16).cpu().numpy()
     used = t[:, 10] > 0
     absd[name] = (int(t[used, 10].min()), int(t[used][:, 6].max()))
-    sh = ws[nn - 148 * 128 - NSH:nn - 148 * 128].view(torch.int64).view(-1, 4).cpu().numpy()
-    sh = sh[sh[:, 0] > 0].astype(np.float64)
-    absd[name + "_sh"] = sh
+
     t = t[used].astype(np.float64)
     rel = (t - t[:, 10].min()) / 1e3
     out = {"call": name, "ctas": int(used.sum())}
@@ -101,7 +99,3 @@ for name, ws, nn in (("qkv", wsq, nq), ("o", wso, no)):
     print(json.dumps(out))
 print(json.dumps({"qkv_span_us": (absd["qkv"][1] - absd["qkv"][0]) / 1e3, "gap_qkv_end_to_o_entry_us": (absd["o"][0] - absd["qkv"][1]) / 1e3,
                   "o_span_us": (absd["o"][1] - absd["o"][0]) / 1e3}))
-for nm in ("qkv", "o"):
-    sh = absd[nm + "_sh"]
-    ref = absd["qkv"][1]   # qkv main's last Y store
-    print(json.dumps({nm + "_shrink_vs_qkv_end_us": {k: [round(float(np.min((sh[:, i] - ref) / 1e3)), 2), round(float(np.median((sh[:, i] - ref) / 1e3)), 2), round(float(np.max((sh[:, i] - ref) / 1e3)), 2)] for i, k in ((0, "entry"), (1, "loop_done"), (3, "end"))}}))
