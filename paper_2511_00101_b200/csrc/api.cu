@@ -870,6 +870,7 @@ static int gemm2_fwd_args(int n_proj, const smlm_pool *pools, const smlm_batch *
         }
         P.slots = pi->d_slots;
         P.Y = Y[i];
+        if ((rc = make_map_cached(p0, &P.tmY, Y[i], pi->out, b->S, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B))) return rc;
         P.N = pi->out;
         P.nt0 = nt0;
         nt0 += (pi->out + kBN - 1) / kBN;
@@ -880,6 +881,7 @@ static int gemm2_fwd_args(int n_proj, const smlm_pool *pools, const smlm_batch *
     g2.n_pairs = F[0].n_pairs;
     g2.n_nt = nt0;
     g2.group_m = (raster_group(p0->in) + 1) / 2;
+    g2.dbg = measure_flag("SMLM_GEMM2_DEBUG");
     g2.r = p0->r;
     g2.r_pad = p0->r_pad;
     g2.stages = gemm2_stages(p0->r_pad);

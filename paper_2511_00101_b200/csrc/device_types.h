@@ -94,6 +94,7 @@ struct alignas(64) Gemm2Proj {
                         // bwd: W box {64,64} (MN-major)
     CUtensorMap tmU;    // fwd: block-diagonal s*V of short tiles; bwd: tile-compact s*U; box {r_pad,128}
     CUtensorMap tmV;    // fwd: tile-compact s*V of the long tiles (pre-shrink); box {r_pad,128}
+    CUtensorMap tmY;    // fwd: Y [S,N] box {64,128} SW128 (TMA store of a 64-column chunk of a full tile)
     const SlotDev *slots;   // this projection's pool slot table
     void *Y;            // fwd: Y [S,N]; bwd: dX [S,N]
     int N;              // output width (fwd out, bwd in)
@@ -106,6 +107,7 @@ struct alignas(64) Gemm2Proj {
 
 struct Gemm2Args {
     Gemm2Proj proj[kGemm2MaxProj];
+    int dbg;                  // measure build only (SMLM_GEMM2_DEBUG): the MMA issuer prints its wait cycles
     DropArgs drop;            // backward: dX = W^T dy + keep * scale * (s A_a^T u) (separate LoRA accumulator)
     const DevPair *pairs;
     const DevBlock *blocks;   // fwd short tiles' adapter blocks
