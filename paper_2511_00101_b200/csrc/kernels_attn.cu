@@ -193,8 +193,11 @@ __global__ void __launch_bounds__(kAT, 1) attn_prefill_kernel(const __grid_const
 #pragma unroll
                 for (int e = 0; e < 128; ++e)
                     if (e < lim) mx = fmaxf(mx, __uint_as_float(sr[e]));
-                const float m_new = fmaxf(mi, mx * sl2);
-                const float alpha = fast_exp2(mi - m_new);   // 0 on the first block (mi = -inf)
+                // lazy rescaling: the reference max moves only when the block's max exceeds it by
+                // more than 2^8 (probabilities stay <= 256, exact in fp32 sums and bf16-rounded like
+                // any other P), so O is rarely rescaled in TMEM
+                const float m_new = (mx * sl2 > mi + 8.f) ? mx * sl2 : mi;
+                const float alpha = fast_exp2(mi - m_new);   // 0 on the first block (mi = -inf), else 1 unless moved
                 const uint32_t pb = G & 1;
                 if (G >= 2) mbar_wait(o_done(pb), ((G >> 1) - 1) & 1);   // PV_{G-2} has read P buffer pb
                 float sum = 0.f;
