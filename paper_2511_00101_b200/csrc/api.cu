@@ -2055,6 +2055,7 @@ int smlm_attention(const smlm_attn_batch *b, int n_heads, int n_kv_heads, int he
     if ((rc = stage_upload(&g_attn_stage, bytes, wsb, st))) return rc;
     AttnArgs a;
     memset(&a, 0, sizeof(a));
+    a.dbg = measure_flag("SMLM_ATTN_DEBUG");
     const uint64_t S = (uint64_t)b->S;
     if (!P.items.empty()) {
         if ((rc = make_map(&a.tmQ, Q, (uint64_t)n_heads * 128, S, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B))) return rc;

@@ -297,6 +297,7 @@ struct AttnArgs {
     float scale;
     float *dpart;      // decode split partials [drows * n_kv_heads * max_splits][G][130] fp32
     int max_splits;    // ceil(longest decode context / 256)
+    int dbg;           // measure build only (SMLM_ATTN_DEBUG): the softmax warps print their phase cycles
 };
 
 // fused cross-rank gradient reduction: every rank's ready counter (peer-mapped)

@@ -16,6 +16,8 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <math.h>
+#include <cstdio>
+
 
 #include <algorithm>
 
@@ -28,7 +30,7 @@ using namespace sm100;
 
 namespace {
 
-constexpr int kAT = 256;                 // prefill: 8 warps (0 TMA, 1 MMA, 2 TMEM alloc, 4-7 softmax)
+constexpr int kAT = 384;                 // prefill: 12 warps (0 TMA, 1 MMA, 2 TMEM alloc, 4-11 softmax)
 constexpr uint32_t kQBytes = 32768;      // 128 rows x 128 d bf16 (two 64-wide SW128 boxes)
 constexpr uint32_t kKVBytes = 65536;     // K tile (32 KB) + V tile (32 KB)
 constexpr uint32_t kPBytes = 32768;      // P: 128 rows x 128 keys bf16 (two buffers)
@@ -53,9 +55,12 @@ __global__ void __launch_bounds__(kAT, 1) attn_prefill_kernel(const __grid_const
     const uint32_t bar = p_s + 2 * kPBytes;
     const uint32_t q_full = bar, q_empty = bar + 8, s_full = bar + 16, s_free = bar + 24, p_full = bar + 32;
     auto o_done = [&](int b) { return bar + 40u + 8u * b; };   // PV_G committed, G % 2 == b (P buffer b free)
-    auto kv_full = [&](int b) { return bar + 56u + 8u * b; };
-    auto kv_empty = [&](int b) { return bar + 72u + 8u * b; };
-    const uint32_t tmem_slot = bar + 88;
+    // K and V of a key block have their own barriers: K_b is free once S has read it, V_b once PV has
+    auto k_full = [&](int b) { return bar + 56u + 8u * b; };
+    auto k_empty = [&](int b) { return bar + 72u + 8u * b; };
+    auto v_full = [&](int b) { return bar + 88u + 8u * b; };
+    auto v_empty = [&](int b) { return bar + 104u + 8u * b; };
+    const uint32_t tmem_slot = bar + 120;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int group = a.n_heads / a.n_kv_heads;
@@ -63,12 +68,14 @@ __global__ void __launch_bounds__(kAT, 1) attn_prefill_kernel(const __grid_const
         mbar_init(q_full, 1);
         mbar_init(q_empty, 1);
         mbar_init(s_full, 1);
-        mbar_init(s_free, 128);
-        mbar_init(p_full, 128);
+        mbar_init(s_free, 256);
+        mbar_init(p_full, 256);
         for (int b = 0; b < 2; ++b) {
             mbar_init(o_done(b), 1);
-            mbar_init(kv_full(b), 1);
-            mbar_init(kv_empty(b), 1);
+            mbar_init(k_full(b), 1);
+            mbar_init(k_empty(b), 1);
+            mbar_init(v_full(b), 1);
+            mbar_init(v_empty(b), 1);
         }
         fence_mbar_init();
         tma_prefetch_desc(&a.tmQ);
@@ -97,16 +104,18 @@ __global__ void __launch_bounds__(kAT, 1) attn_prefill_kernel(const __grid_const
                     tma_load_2d(q_s + 16384u * db, &a.tmQ, q_full, head * 128 + 64 * db, it.row0 + it.qb * 128);
                 for (int j = 0; j < nkb; ++j, ++G) {
                     const int b = G & 1;
-                    mbar_wait(kv_empty(b), ((G >> 1) & 1) ^ 1);
-                    mbar_expect_tx(kv_full(b), kKVBytes);
                     const int k0 = it.row0 + j * 128;
                     // K_j: B operand of S = Q K^T, K-major (rows = keys, 128 B of d per row)
+                    mbar_wait(k_empty(b), ((G >> 1) & 1) ^ 1);
+                    mbar_expect_tx(k_full(b), kKVBytes / 2);
                     for (int db = 0; db < 2; ++db)
-                        tma_load_2d(kv_s(b) + 16384u * db, &a.tmK, kv_full(b), kvh * 128 + 64 * db, k0);
+                        tma_load_2d(kv_s(b) + 16384u * db, &a.tmK, k_full(b), kvh * 128 + 64 * db, k0);
                     // V_j: B operand of O += P V, MN-major (rows = keys, 64-wide d boxes)
+                    mbar_wait(v_empty(b), ((G >> 1) & 1) ^ 1);
+                    mbar_expect_tx(v_full(b), kKVBytes / 2);
                     for (int kb = 0; kb < 2; ++kb)
                         for (int db = 0; db < 2; ++db)
-                            tma_load_2d(kv_s(b) + 32768u + 16384u * kb + 8192u * db, &a.tmV, kv_full(b),
+                            tma_load_2d(kv_s(b) + 32768u + 16384u * kb + 8192u * db, &a.tmV, v_full(b),
                                         kvh * 128 + 64 * db, k0 + 64 * kb);
                 }
             }
@@ -118,9 +127,10 @@ __global__ void __launch_bounds__(kAT, 1) attn_prefill_kernel(const __grid_const
         constexpr uint32_t idesc_s = idesc_bf16(128, 128, 0, 0);
         constexpr uint32_t idesc_o = idesc_bf16(128, 128, 0, 1);
         auto issue_pv = [&](int Gp, bool first) {
+            const int b = Gp & 1;
+            mbar_wait(v_full(b), (Gp >> 1) & 1);
             mbar_wait(p_full, Gp & 1);       // P_Gp in smem, O rescaled
             tc_fence_after();
-            const int b = Gp & 1;
             if (lane == 0) {
 #pragma unroll
                 for (int k = 0; k < 8; ++k) {
@@ -129,7 +139,7 @@ __global__ void __launch_bounds__(kAT, 1) attn_prefill_kernel(const __grid_const
                     mma_bf16(O_t, smem_desc(pa, 16, 1024, kSw128), smem_desc(vb, 8192, 1024, kSw128), idesc_o,
                              (!first || k > 0) ? 1u : 0u);
                 }
-                mma_commit(kv_empty(b));
+                mma_commit(v_empty(b));
                 mma_commit(o_done(b));
             }
             __syncwarp();
@@ -142,7 +152,7 @@ __global__ void __launch_bounds__(kAT, 1) attn_prefill_kernel(const __grid_const
             for (int j = 0; j < nkb; ++j, ++G) {
                 if (G > 0) mbar_wait(s_free, (G - 1) & 1);   // the softmax has read S_{G-1}
                 const int b = G & 1;
-                mbar_wait(kv_full(b), (G >> 1) & 1);
+                mbar_wait(k_full(b), (G >> 1) & 1);
                 tc_fence_after();
                 if (lane == 0) {
 #pragma unroll
@@ -152,6 +162,7 @@ __global__ void __launch_bounds__(kAT, 1) attn_prefill_kernel(const __grid_const
                                  smem_desc(kv_s(b) + off, 16, 1024, kSw128), idesc_s, k > 0);
                     }
                     mma_commit(s_full);
+                    mma_commit(k_empty(b));
                     if (j == nkb - 1) mma_commit(q_empty);
                 }
                 __syncwarp();
@@ -160,81 +171,126 @@ __global__ void __launch_bounds__(kAT, 1) attn_prefill_kernel(const __grid_const
             issue_pv(G - 1, nkb == 1);   // the unit's last block
         }
     } else if (warp >= 4) {
-        // ---------------- online softmax + epilogue (thread = query row) ----------------
-        const int m = threadIdx.x - 128;
-        const uint32_t lane_base = (uint32_t)((warp - 4) * 32) << 16;
+        // ---------------- online softmax + epilogue ----------------
+        // two warpgroups: warpgroup wg takes key columns [64 wg, 64 wg + 64) of every S block and
+        // output columns [64 wg, 64 wg + 64) of O; thread = query row (TMEM lane).  The row's max
+        // is combined through shared memory each block; each warpgroup keeps the sum of its own
+        // columns (both use the same reference max), added at the unit's end.
+        const int wg = (warp - 4) >> 2;
+        const int m = (threadIdx.x - 128) & 127;
+        const int tid_s = threadIdx.x - 128;   // 0..255
+        const uint32_t lane_base = (uint32_t)(((warp - 4) & 3) * 32) << 16;
+        const uint32_t col0 = 64u * (uint32_t)wg;
         const float sl2 = a.scale * 1.4426950408889634f;
         uint8_t *pp = base_ptr + (p_s - base);
+        __shared__ float s_x[128];   // per row: warpgroup 1's max -> the new reference max; at the end l
         int G = 0;
+#ifdef SMLM_MEASURE
+        long long c_ws = 0, c_ld = 0, c_exp = 0, c_wo = 0, c_rs = 0, c_ep = 0, c0, c_begin = clock64();
+#define TSTAMP() (c0 = clock64())
+#define TACC(x) (x += clock64() - c0)
+#else
+#define TSTAMP()
+#define TACC(x)
+#endif
         for (int w = blockIdx.x; w < n_units; w += gridDim.x) {
             const AttnItem it = a.items[w / a.n_heads];
             const int head = w % a.n_heads, nkb = it.qb + 1;
             const int qi = it.qb * 128 + m;           // query position inside the segment
-            float mi = -INFINITY, li = 0.f;           // running max (log2 units) and sum
+            float mi = -INFINITY, li = 0.f;           // reference max (log2 units), this half's sum
             for (int j = 0; j < nkb; ++j, ++G) {
+                TSTAMP();
                 mbar_wait(s_full, G & 1);
+                TACC(c_ws);
+                TSTAMP();
                 tc_fence_after();
-                const int kbase = j * 128;
-                // the whole S row into registers, then S is free for S_{G+1} (it overlaps the exps)
-                uint32_t sr[128];
+                const int kbase = j * 128 + (int)col0;
+                // this half of the S row into registers, then S is free for S_{G+1}
+                uint32_t sr[64];
 #pragma unroll
-                for (int c = 0; c < 4; ++c) {
+                for (int c = 0; c < 2; ++c) {
                     uint32_t r[32];
-                    tmem_ld32(S_t + lane_base + 32u * c, r);
+                    tmem_ld32(S_t + lane_base + col0 + 32u * c, r);
 #pragma unroll
                     for (int e = 0; e < 32; ++e) sr[32 * c + e] = r[e];
                 }
                 tmem_wait_ld();
                 tc_fence_before();
                 mbar_arrive(s_free);
+                TACC(c_ld);
+                TSTAMP();
                 // keys visible to this row: kj <= qi and kj < len  <=>  kj - kbase < lim
                 const int lim = min(qi + 1, it.len) - kbase;
+                // every key of this half visible to every row of the warp (all but the diagonal and
+                // segment-end blocks): no per-key predicates
+                const bool whole = __all_sync(0xffffffffu, lim >= 64);
                 float mx = -INFINITY;
+                if (whole) {
 #pragma unroll
-                for (int e = 0; e < 128; ++e)
-                    if (e < lim) mx = fmaxf(mx, __uint_as_float(sr[e]));
-                // lazy rescaling: the reference max moves only when the block's max exceeds it by
-                // more than 2^8 (probabilities stay <= 256, exact in fp32 sums and bf16-rounded like
-                // any other P), so O is rarely rescaled in TMEM
-                const float m_new = (mx * sl2 > mi + 8.f) ? mx * sl2 : mi;
+                    for (int e = 0; e < 64; ++e) mx = fmaxf(mx, __uint_as_float(sr[e]));
+                } else {
+#pragma unroll
+                    for (int e = 0; e < 64; ++e)
+                        if (e < lim) mx = fmaxf(mx, __uint_as_float(sr[e]));
+                }
+                // the row's max: warpgroup 1 publishes its half, warpgroup 0 combines and publishes the
+                // new reference.  Lazy rescaling: the reference max moves only when the block's max
+                // exceeds it by more than 2^8 (probabilities stay <= 256), so O is rarely rescaled
+                if (wg == 1) s_x[m] = mx;
+                named_bar_sync(1, 256);
+                float m_new;
+                if (wg == 0) {
+                    mx = fmaxf(mx, s_x[m]);
+                    m_new = (mx * sl2 > mi + 8.f) ? mx * sl2 : mi;
+                    s_x[m] = m_new;
+                }
+                named_bar_sync(1, 256);
+                if (wg == 1) m_new = s_x[m];
                 const float alpha = fast_exp2(mi - m_new);   // 0 on the first block (mi = -inf), else 1 unless moved
                 const uint32_t pb = G & 1;
+                TACC(c_exp);
+                TSTAMP();
                 if (G >= 2) mbar_wait(o_done(pb), ((G >> 1) - 1) & 1);   // PV_{G-2} has read P buffer pb
-                float sum = 0.f;
-                uint8_t *pbuf = pp + pb * kPBytes;
+                TACC(c_wo);
+                TSTAMP();
+                float sum = 0.f;   // of the fp32 probabilities (P itself is rounded to bf16 for the MMA)
+                uint8_t *pbuf = pp + pb * kPBytes + wg * 16384;   // key half wg of P (64 keys, SW128)
+                const float nm = -m_new;
 #pragma unroll
-                for (int ch = 0; ch < 16; ++ch) {   // 16-byte chunks of 8 keys: chunk ch of key block ch / 8
+                for (int ch = 0; ch < 8; ++ch) {   // 16-byte chunks of 8 keys
                     uint32_t pk[4];
 #pragma unroll
                     for (int q = 0; q < 4; ++q) {
                         const int e = 8 * ch + 2 * q;
-                        const float p0 = e < lim ? fast_exp2(__uint_as_float(sr[e]) * sl2 - m_new) : 0.f;
-                        const float p1 = e + 1 < lim ? fast_exp2(__uint_as_float(sr[e + 1]) * sl2 - m_new) : 0.f;
+                        float p0 = fast_exp2(fmaf(__uint_as_float(sr[e]), sl2, nm));
+                        float p1 = fast_exp2(fmaf(__uint_as_float(sr[e + 1]), sl2, nm));
+                        if (!whole) {
+                            p0 = e < lim ? p0 : 0.f;
+                            p1 = e + 1 < lim ? p1 : 0.f;
+                        }
+                        sum += p0 + p1;
                         const __nv_bfloat162 b2 = __floats2bfloat162_rn(p0, p1);
-                        // the sum uses the rounded probabilities the MMA multiplies V with
-                        const float2 pr = __bfloat1622float2(b2);
-                        sum += pr.x + pr.y;
                         pk[q] = *reinterpret_cast<const uint32_t *>(&b2);
                     }
-                    const int kb = ch >> 3, cc = ch & 7;
-                    *reinterpret_cast<uint4 *>(pbuf + kb * 16384 + m * 128 + ((cc ^ (m & 7)) << 4)) =
-                        make_uint4(pk[0], pk[1], pk[2], pk[3]);
+                    *reinterpret_cast<uint4 *>(pbuf + m * 128 + ((ch ^ (m & 7)) << 4)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
                 }
                 li = li * alpha + sum;
+                TACC(c_exp);
+                TSTAMP();
                 if (j > 0) {
-                    // P_{G-1} V_{G-1} has landed in O: rescale it (warp-collective tcgen05.ld / st,
-                    // so the warp rescales when any of its rows needs it)
+                    // P_{G-1} V_{G-1} has landed in O: rescale this warpgroup's 64 columns of it
+                    // (warp-collective tcgen05.ld / st: the warp rescales when any of its rows needs it)
                     mbar_wait(o_done((G - 1) & 1), ((G - 1) >> 1) & 1);
                     tc_fence_after();
                     if (__any_sync(0xffffffffu, alpha != 1.f)) {
 #pragma unroll 1
-                        for (int c = 0; c < 4; ++c) {
+                        for (int c = 0; c < 2; ++c) {
                             uint32_t r[32];
-                            tmem_ld32(O_t + lane_base + 32u * c, r);
+                            tmem_ld32(O_t + lane_base + col0 + 32u * c, r);
                             tmem_wait_ld();
 #pragma unroll
                             for (int e = 0; e < 32; ++e) r[e] = __float_as_uint(__uint_as_float(r[e]) * alpha);
-                            tmem_st32(O_t + lane_base + 32u * c, r);
+                            tmem_st32(O_t + lane_base + col0 + 32u * c, r);
                         }
                         tmem_wait_st();
                     }
@@ -243,33 +299,65 @@ __global__ void __launch_bounds__(kAT, 1) attn_prefill_kernel(const __grid_const
                 fence_proxy_async_smem();   // P (generic stores) -> the MMA (async proxy)
                 tc_fence_before();
                 mbar_arrive(p_full);
+                TACC(c_rs);
             }
-            // epilogue of the unit: O / l -> bf16 rows of O [S, Hq, d]
+            TSTAMP();
+            // epilogue of the unit: O / l -> bf16 rows of O [S, Hq, d], l = the two halves' sums
+            // (added in the same order by both warpgroups)
+            named_bar_sync(1, 256);   // warpgroup 1 has read the last block's reference max
+            if (wg == 1) s_x[m] = li;
             mbar_wait(o_done((G - 1) & 1), ((G - 1) >> 1) & 1);
             tc_fence_after();
-            const float inv = 1.f / li;
-            const bool ok = qi < it.len;
-            __nv_bfloat16 *O = reinterpret_cast<__nv_bfloat16 *>(a.O) +
-                               ((size_t)(it.row0 + qi) * a.n_heads + head) * 128;
+            named_bar_sync(1, 256);
+            if (wg == 0) s_x[m] = li + s_x[m];
+            named_bar_sync(1, 256);
+            const float invl = 1.f / s_x[m];
+            // stage the O rows in P buffer 0 (free: the unit's last PV has completed, the next
+            // unit's softmax has not started) so the global stores are whole 256-byte rows
+            uint8_t *ostage = pp;   // 128 rows x 256 B, 16-byte units XOR-swizzled by row
 #pragma unroll 1
-            for (int c = 0; c < 4; ++c) {
+            for (int c = 0; c < 2; ++c) {
                 uint32_t r[32];
-                tmem_ld32(O_t + lane_base + 32u * c, r);
+                tmem_ld32(O_t + lane_base + col0 + 32u * c, r);
                 tmem_wait_ld();
-                if (ok) {
 #pragma unroll
-                    for (int q = 0; q < 4; ++q) {
-                        uint4 v;
-                        v.x = pack_bf16x2(__uint_as_float(r[8 * q + 0]) * inv, __uint_as_float(r[8 * q + 1]) * inv);
-                        v.y = pack_bf16x2(__uint_as_float(r[8 * q + 2]) * inv, __uint_as_float(r[8 * q + 3]) * inv);
-                        v.z = pack_bf16x2(__uint_as_float(r[8 * q + 4]) * inv, __uint_as_float(r[8 * q + 5]) * inv);
-                        v.w = pack_bf16x2(__uint_as_float(r[8 * q + 6]) * inv, __uint_as_float(r[8 * q + 7]) * inv);
-                        *reinterpret_cast<uint4 *>(O + 32 * c + 8 * q) = v;
-                    }
+                for (int q = 0; q < 4; ++q) {
+                    uint4 v;
+                    v.x = pack_bf16x2(__uint_as_float(r[8 * q + 0]) * invl, __uint_as_float(r[8 * q + 1]) * invl);
+                    v.y = pack_bf16x2(__uint_as_float(r[8 * q + 2]) * invl, __uint_as_float(r[8 * q + 3]) * invl);
+                    v.z = pack_bf16x2(__uint_as_float(r[8 * q + 4]) * invl, __uint_as_float(r[8 * q + 5]) * invl);
+                    v.w = pack_bf16x2(__uint_as_float(r[8 * q + 6]) * invl, __uint_as_float(r[8 * q + 7]) * invl);
+                    const int u = 8 * wg + 4 * c + q;   // 16-byte unit of the row (16 per row)
+                    *reinterpret_cast<uint4 *>(ostage + m * 256 + ((u ^ (m & 15)) << 4)) = v;
+                }
+            }
+            named_bar_sync(1, 256);
+            {
+                const int rsub = tid_s >> 4, u = tid_s & 15;   // 16 rows per pass, 16 threads per row
+                __nv_bfloat16 *Ob = reinterpret_cast<__nv_bfloat16 *>(a.O);
+#pragma unroll 2
+                for (int r0 = 0; r0 < 128; r0 += 16) {
+                    const int rr = r0 + rsub;
+                    const int qr = it.qb * 128 + rr;
+                    if (qr < it.len)
+                        *reinterpret_cast<uint4 *>(Ob + ((size_t)(it.row0 + qr) * a.n_heads + head) * 128 + 8 * u) =
+                            *reinterpret_cast<const uint4 *>(ostage + rr * 256 + ((u ^ (rr & 15)) << 4));
                 }
             }
             tc_fence_before();   // the O reads are ordered before the next unit's p_full
+            named_bar_sync(1, 256);   // the staging buffer is P buffer 0 of the next unit; s_x reused
+            TACC(c_ep);
         }
+#ifdef SMLM_MEASURE
+        if (a.dbg && tid_s == 0 && blockIdx.x % 16 == 0) {
+            const double T = (double)(clock64() - c_begin);
+            printf("[attn prefill] cta %d blocks %d cycles %.0f wait_S %.1f%% ld_S %.1f%% max+exp+P %.1f%% wait_Pfree %.1f%% "
+                   "wait_PV+rescale %.1f%% epilogue %.1f%%\n",
+                   blockIdx.x, G, T, 100 * c_ws / T, 100 * c_ld / T, 100 * c_exp / T, 100 * c_wo / T, 100 * c_rs / T, 100 * c_ep / T);
+        }
+#endif
+#undef TSTAMP
+#undef TACC
     }
     tc_fence_before();
     __syncthreads();
@@ -461,6 +549,7 @@ __global__ void __launch_bounds__(128) attn_decode_combine_kernel(const AttnArgs
 }  // namespace
 
 size_t attn_prefill_smem() { return 1024 + kQBytes + 2 * kKVBytes + 2 * kPBytes + 128; }
+static_assert(120 + 4 <= 128, "prefill barriers exceed their area");
 
 int launch_attn(const AttnArgs &a, int n_items, int n_rows, int n_drows, int max_dec_len, cudaStream_t st) {
     cudaError_t e = cudaSuccess;
