@@ -208,12 +208,16 @@ class Workload:
         two streams so one group's GEMM tail and small kernels overlap the next one's; both
         streams join before the layer's bucket is reduced."""
         S = self.S
+        nvtx = torch.cuda.nvtx
         order = list(range(N_LAYERS)) if layers is None else list(layers)
         for L in order:
+            nvtx.range_push(f"smlm fwd L{L}")   # NVTX ranges: phase markers for nsys / ncu --nvtx
             forward_groups(S, self.layers[L], self.b, lambda p: self.X[GROUP_OF[p]], self.Y, self.V[L], stream)
+            nvtx.range_pop()
         if getattr(self, "_s2", None) is None:
             self._s2 = torch.cuda.Stream(self.dev)
         for L in reversed(order):
+            nvtx.range_push(f"smlm bwd L{L}")
             layer = self.layers[L]
             ev = torch.cuda.Event()
             ev.record(stream)
@@ -224,8 +228,11 @@ class Workload:
             ev2 = torch.cuda.Event()
             ev2.record(self._s2)
             stream.wait_event(ev2)
+            nvtx.range_pop()
             if comm is not None:
+                nvtx.range_push(f"smlm grad reduce L{L}")
                 comm(self.buckets[L])
+                nvtx.range_pop()
 
 
     def use_peer_reduce(self, dist):
@@ -546,7 +553,7 @@ def main():
     step_tflops = (f_alg + b_alg) * N_LAYERS / (ms / 1000.0) / 1e12
     roofline = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                 "frac": achieved / peak if peak else None, "traffic": traffic,
-                "kernel": "smlm_gemm2_kernel<fwd, pre-shrunk> (tcgen05 cta_group::2; full 256-column W tiles + s*V expand K-block)",
+                "kernel": "smlm_gemm2w_kernel<fwd> (tcgen05 cta_group::2; 256 x 512 items over both TMEM halves, full W tiles + s*V expand K-block, TMA-store epilogue)",
                 "peak_source": peaks["source"] + (" bf16_tflops (burst: the timed region ran at max SM clock)" if at_max
                                                   else " bf16_tflops_sustained (the timed region ran below max SM "
                                                        "clock under the power cap)"),

@@ -10,9 +10,9 @@ OUT=${1:-gpurun_out}
 mkdir -p $OUT
 NCU=/usr/local/cuda/bin/ncu
 $NCU --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
-     -k regex:smlm_gemm2_kernel -s 8 -c 8 --csv --log-file $OUT/gemm_traffic.csv python scripts/prof_step.py > /dev/null 2>&1
-$NCU --set full --clock-control none --import-source on -k regex:smlm_gemm2_kernel -s 8 -c 1 -o $OUT/prof_fwd_qkv -f python scripts/prof_step.py > /dev/null 2>&1
-$NCU --set full --clock-control none --import-source on -k regex:smlm_gemm2_kernel -s 13 -c 1 -o $OUT/prof_bwd_gateup -f python scripts/prof_step.py > /dev/null 2>&1
+     -k regex:smlm_gemm2 -s 8 -c 8 --csv --log-file $OUT/gemm_traffic.csv python scripts/prof_step.py > /dev/null 2>&1
+$NCU --set full --clock-control none --import-source on -k regex:smlm_gemm2 -s 8 -c 1 -o $OUT/prof_fwd_qkv -f python scripts/prof_step.py > /dev/null 2>&1
+$NCU --set full --clock-control none --import-source on -k regex:smlm_gemm2 -s 13 -c 1 -o $OUT/prof_bwd_gateup -f python scripts/prof_step.py > /dev/null 2>&1
 $NCU --set full --clock-control none --import-source on -k regex:smlm_tok_kernel -s 9 -c 1 -o $OUT/prof_tok -f python scripts/prof_step.py > /dev/null 2>&1
 $NCU --set full --clock-control none --import-source on -k regex:smlm_dec3 -s 2 -c 1 -o $OUT/prof_dec3_qkv -f python scripts/dec_layer_phases.py > /dev/null 2>&1
 $NCU --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file $OUT/dec_launches.csv python scripts/bench_configs.py --c2-only > /dev/null 2>&1

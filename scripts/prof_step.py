@@ -1,7 +1,7 @@
 """Tiny driver for ncu: the bench's C4 step restricted to ONE layer (layers=[0]), run twice (the
 first is the warm-up).  Per step the CTA-pair GEMM launches are, in order: forward q/k/v (one
 merged launch), o, gate/up (merged), down; backward down, gate/up (smlm_backward_multi), o,
-q/k/v -- 8 per step, so `-k regex:smlm_gemm2_kernel -s 8 -c 8` captures the second step."""
+q/k/v -- 8 per step, so `-k regex:smlm_gemm2 -s 8 -c 8` (forward: smlm_gemm2w_kernel, backward: smlm_gemm2_kernel) captures the second step."""
 import os
 import sys
 
