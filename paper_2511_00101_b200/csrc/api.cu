@@ -262,6 +262,17 @@ int raster_group(int K) {
     if (g > 64) g = 64;
     return (int)g;
 }
+// CTA-pair GEMMs: pairs per raster group -- a ~64 MB budget of X tiles, then the groups
+// balanced (53 pairs at K = 4096: 2 groups of 27 / 26 instead of 24 + 24 + 5, so W is streamed
+// from HBM twice instead of three times)
+int raster_group_pairs(int K, int n_pairs) {
+    const long pair = 256L * K * 2;
+    long g = (64L << 20) / pair;
+    if (g < 2) g = 2;
+    if (g > 64) g = 64;
+    const long groups = (n_pairs + g - 1) / g;
+    return (int)std::max<long>(1, (n_pairs + groups - 1) / groups);
+}
 
 }  // namespace
 
@@ -880,7 +891,7 @@ static int gemm2_fwd_args(int n_proj, const smlm_pool *pools, const smlm_batch *
     g2.n_proj = n_proj;
     g2.n_pairs = F[0].n_pairs;
     g2.n_nt = nt0;
-    g2.group_m = (raster_group(p0->in) + 1) / 2;
+    g2.group_m = raster_group_pairs(p0->in, F[0].n_pairs);
     g2.dbg = measure_flag("SMLM_GEMM2_DEBUG");
     g2.r = p0->r;
     g2.r_pad = p0->r_pad;

@@ -31,9 +31,12 @@ def us(d):
 
 # per-kernel shares of one layer (launch list)
 data = launches(os.path.join(src, "launches_layer.csv"))
+# the library's kernels only (not the workload set-up), of the second of the two steps
+data = [d for d in data if "smlm::" in d["Kernel Name"]]
+data = data[len(data) // 2:]
 agg = collections.OrderedDict()
 for d in data:
-    k = re.sub(r"\(.*", "", d["Kernel Name"]).replace("void ", "").replace("unnamed>::", "")
+    k = re.sub(r"\(.*", "", d["Kernel Name"]).replace("void ", "").replace("unnamed>::", "").replace("smlm::<", "")
     a = agg.setdefault(k, [0, 0.0])
     a[0] += 1
     a[1] += us(d)
