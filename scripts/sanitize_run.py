@@ -6,7 +6,8 @@
 Covers: the CTA-pair forward GEMM (pre-shrink, short tiles, fine-tune V_save), the SIMT short-row
 shrink, the U pass + dX GEMM + dA/dB token contraction (backward), the single-launch decode
 kernel (one projection and q/k/v fused), the multi-projection pre-shrink of a mixed batch, the
-1-CTA GEMM (SMLM_OPT_CTA_PAIR = 0), the fp32 test-mode kernels and the AdamW step.
+1-CTA GEMM (SMLM_OPT_CTA_PAIR = 0), the fp32 test-mode kernels, the attention branch (prefill,
+cache writes, split-KV decode) and the AdamW step.
 No parity checks here (the tests do that): this only exercises the launches."""
 import os
 import sys
@@ -82,6 +83,22 @@ def decode_and_multi():
         p.close()
 
 
+def attention():
+    # the Alg. 1 attention branch: a 300-row prefill (three query blocks, the last partial) with
+    # KV-cache init, a 128-row fine-tune segment (one full block), and two decode rows
+    g = torch.Generator().manual_seed(3)
+    S_ = 430
+    Q = torch.randn(S_, 8, 128, generator=g).to(torch.bfloat16).to(dev)
+    K = torch.randn(S_, 2, 128, generator=g).to(torch.bfloat16).to(dev)
+    V = torch.randn(S_, 2, 128, generator=g).to(torch.bfloat16).to(dev)
+    Kc = torch.zeros(2, 512, 2, 128, dtype=torch.bfloat16, device=dev)
+    Vc = torch.zeros_like(Kc)
+    offs, modes, cs, past = [0, 300, 428, 429, 430], [PREFILL, FINETUNE, DECODE, DECODE], [0, -1, 0, 1], [0, 0, 300, 7]
+    O = torch.empty(S_, 8, 128, dtype=torch.bfloat16, device=dev)
+    S.smlm_attention(S.AttnBatch(offs, modes, cs, past), Q, K, V, O, Kc, Vc)
+    torch.cuda.synchronize()
+
+
 def adamw():
     n = 70001
     P, M, V, G = (torch.randn(n, device=dev) for _ in range(4))
@@ -97,5 +114,6 @@ if __name__ == "__main__":
     mixed(S.SMLM_BF16, cta_pair=0)
     mixed(S.SMLM_FP32)
     decode_and_multi()
+    attention()
     adamw()
     print("sanitize_run: ok, launches", S.smlm_launch_count())
