@@ -223,16 +223,17 @@ __global__ void __launch_bounds__(kAT, 1) attn_prefill_kernel(const __grid_const
                 const int lim = min(qi + 1, it.len) - kbase;
                 // every key of this half visible to every row of the warp (all but the diagonal and
                 // segment-end blocks): no per-key predicates
-                const bool whole = __all_sync(0xffffffffu, lim >= 64);
-                float mx = -INFINITY;
-                if (whole) {
-#pragma unroll
-                    for (int e = 0; e < 64; ++e) mx = fmaxf(mx, __uint_as_float(sr[e]));
-                } else {
+                // masked keys become -inf in the registers (only in the diagonal / segment-end
+                // blocks: a warp-uniform branch), so the max and exp loops below carry no per-key
+                // predicate (exp2(-inf) = 0)
+                if (!__all_sync(0xffffffffu, lim >= 64)) {
 #pragma unroll
                     for (int e = 0; e < 64; ++e)
-                        if (e < lim) mx = fmaxf(mx, __uint_as_float(sr[e]));
+                        if (e >= lim) sr[e] = 0xff800000u;   // -inf
                 }
+                float mx = -INFINITY;
+#pragma unroll
+                for (int e = 0; e < 64; ++e) mx = fmaxf(mx, __uint_as_float(sr[e]));
                 // the row's max: warpgroup 1 publishes its half, warpgroup 0 combines and publishes the
                 // new reference.  Lazy rescaling: the reference max moves only when the block's max
                 // exceeds it by more than 2^8 (probabilities stay <= 256), so O is rarely rescaled
@@ -262,12 +263,8 @@ __global__ void __launch_bounds__(kAT, 1) attn_prefill_kernel(const __grid_const
 #pragma unroll
                     for (int q = 0; q < 4; ++q) {
                         const int e = 8 * ch + 2 * q;
-                        float p0 = fast_exp2(fmaf(__uint_as_float(sr[e]), sl2, nm));
-                        float p1 = fast_exp2(fmaf(__uint_as_float(sr[e + 1]), sl2, nm));
-                        if (!whole) {
-                            p0 = e < lim ? p0 : 0.f;
-                            p1 = e + 1 < lim ? p1 : 0.f;
-                        }
+                        const float p0 = fast_exp2(fmaf(__uint_as_float(sr[e]), sl2, nm));
+                        const float p1 = fast_exp2(fmaf(__uint_as_float(sr[e + 1]), sl2, nm));
                         sum += p0 + p1;
                         const __nv_bfloat162 b2 = __floats2bfloat162_rn(p0, p1);
                         pk[q] = *reinterpret_cast<const uint32_t *>(&b2);
