@@ -133,6 +133,8 @@ def c2_layer_step(iters=40, graphs=True):
             A = (torch.randn(U, r, in_f, generator=g, device=dev) / math.sqrt(in_f)).to(torch.bfloat16)
             B = (torch.randn(U, out_f, r, generator=g, device=dev) / (4 * math.sqrt(r))).to(torch.bfloat16)
             pool = S.Pool(in_f, out_f, r, U, S.SMLM_BF16, 0)
+            if os.environ.get("DEC_KSPLIT"):   # measurement sweep of the decode split-K factor
+                pool.set_option(S.SMLM_OPT_DEC_KSPLIT, int(os.environ["DEC_KSPLIT"]))
             for a in range(U):
                 pool.register(A[a], B[a], 2.0)
             Y = torch.empty(batch.S, out_f, dtype=torch.bfloat16, device=dev)
