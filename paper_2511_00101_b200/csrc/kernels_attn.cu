@@ -364,6 +364,286 @@ __global__ void __launch_bounds__(kAT, 1) attn_prefill_kernel(const __grid_const
     }
 }
 
+// ---- prefill, two query heads of one KV group per CTA (GQA group even) ----
+// Unit = (128-query block, KV head, head pair): the two heads' 128-row tiles share every K / V
+// block, so the tensor pipe always has the other tile's S / PV MMAs while a softmax warpgroup
+// works (FA4-style ping-pong of two tiles).  12 warps: 0 TMA (Q, K), 1 MMA issuer, 2 TMEM
+// allocator, 3 TMA (V), 4-7 softmax of tile 0, 8-11 softmax of tile 1 (thread = query row).
+// Shared memory: Q0 Q1 | K ring 2 | V (one buffer) | P0 P1 (one buffer per tile) = 224 KB.
+// TMEM: S0 S1 O0 O1 (128 columns each).
+constexpr int kAT2 = 384;
+size_t attn_prefill2_smem() { return 1024 + 2 * kQBytes + 2 * (kKVBytes / 2) + kKVBytes / 2 + 2 * kPBytes + 256; }
+
+__global__ void __launch_bounds__(kAT2, 1) attn_prefill2_kernel(const __grid_constant__ AttnArgs a, int n_units) {
+    extern __shared__ uint8_t smem_raw[];
+    const uint32_t raw = smem_u32(smem_raw);
+    const uint32_t base = (raw + 1023u) & ~1023u;
+    uint8_t *base_ptr = smem_raw + (base - raw);
+    auto q_s = [&](int t) { return base + (uint32_t)t * kQBytes; };
+    auto k_s = [&](int b) { return base + 2u * kQBytes + (uint32_t)b * 32768u; };
+    const uint32_t v_s = base + 2u * kQBytes + 65536u;
+    auto p_s = [&](int t) { return base + 2u * kQBytes + 98304u + (uint32_t)t * kPBytes; };
+    const uint32_t bar = base + 2u * kQBytes + 98304u + 2u * kPBytes;
+    const uint32_t q_full = bar, q_empty = bar + 8, v_full = bar + 16, v_empty = bar + 24;
+    auto k_full = [&](int b) { return bar + 32u + 8u * b; };
+    auto k_empty = [&](int b) { return bar + 48u + 8u * b; };
+    auto s_full = [&](int t) { return bar + 64u + 8u * t; };
+    auto s_free = [&](int t) { return bar + 80u + 8u * t; };
+    auto p_full = [&](int t) { return bar + 96u + 8u * t; };
+    auto o_done = [&](int t) { return bar + 112u + 8u * t; };   // PV of tile t committed (P_t free, O_t updated)
+    const uint32_t tmem_slot = bar + 128;
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int group = a.n_heads / a.n_kv_heads;
+    const int hpairs = a.n_heads / 2;
+    if (threadIdx.x == 0) {
+        mbar_init(q_full, 1);
+        mbar_init(q_empty, 1);
+        mbar_init(v_full, 1);
+        mbar_init(v_empty, 1);
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(k_full(b), 1);
+            mbar_init(k_empty(b), 1);
+            mbar_init(s_full(b), 1);
+            mbar_init(s_free(b), 128);
+            mbar_init(p_full(b), 128);
+            mbar_init(o_done(b), 1);
+        }
+        fence_mbar_init();
+        tma_prefetch_desc(&a.tmQ);
+        tma_prefetch_desc(&a.tmK);
+        tma_prefetch_desc(&a.tmV);
+    }
+    if (warp == 2) tmem_alloc(tmem_slot, 512);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *reinterpret_cast<volatile uint32_t *>(base_ptr + (tmem_slot - base));
+    auto S_t = [&](int t) { return tmem + 128u * (uint32_t)t; };
+    auto O_t = [&](int t) { return tmem + 256u + 128u * (uint32_t)t; };
+    pdl_wait();   // the item table is written by the stream's plan upload
+    pdl_trigger();
+
+    if (warp == 0) {
+        // ---------------- TMA: Q of both heads, K ring ----------------
+        if (lane == 0) {
+            int G = 0, u = 0;
+            for (int w = blockIdx.x; w < n_units; w += gridDim.x, ++u) {
+                const AttnItem it = a.items[w / hpairs];
+                const int h0 = 2 * (w % hpairs), kvh = h0 / group, nkb = it.qb + 1;
+                if (u > 0) mbar_wait(q_empty, (u - 1) & 1);   // the previous unit's S MMAs read Q
+                mbar_expect_tx(q_full, 2 * kQBytes);
+                for (int t = 0; t < 2; ++t)
+                    for (int db = 0; db < 2; ++db)
+                        tma_load_2d(q_s(t) + 16384u * db, &a.tmQ, q_full, (h0 + t) * 128 + 64 * db, it.row0 + it.qb * 128);
+                for (int j = 0; j < nkb; ++j, ++G) {
+                    const int b = G & 1;
+                    mbar_wait(k_empty(b), ((G >> 1) & 1) ^ 1);
+                    mbar_expect_tx(k_full(b), 32768u);
+                    for (int db = 0; db < 2; ++db)
+                        tma_load_2d(k_s(b) + 16384u * db, &a.tmK, k_full(b), kvh * 128 + 64 * db, it.row0 + j * 128);
+                }
+            }
+        }
+    } else if (warp == 3) {
+        // ---------------- TMA: V (one buffer; free once both tiles' PV have read it) ----------------
+        if (lane == 0) {
+            int G = 0;
+            for (int w = blockIdx.x; w < n_units; w += gridDim.x) {
+                const AttnItem it = a.items[w / hpairs];
+                const int kvh = 2 * (w % hpairs) / group, nkb = it.qb + 1;
+                for (int j = 0; j < nkb; ++j, ++G) {
+                    mbar_wait(v_empty, (G & 1) ^ 1);
+                    mbar_expect_tx(v_full, 32768u);
+                    for (int kb = 0; kb < 2; ++kb)
+                        for (int db = 0; db < 2; ++db)
+                            tma_load_2d(v_s + 16384u * kb + 8192u * db, &a.tmV, v_full, kvh * 128 + 64 * db,
+                                        it.row0 + j * 128 + 64 * kb);
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ---------------- MMA issuer ----------------
+        // per key block G: S_0(G), S_1(G) (each after its softmax has read S_t(G-1)), then
+        // PV_0(G-1), PV_1(G-1) -- a tile's MMAs run while the other tile's softmax works
+        constexpr uint32_t idesc_s = idesc_bf16(128, 128, 0, 0);
+        constexpr uint32_t idesc_o = idesc_bf16(128, 128, 0, 1);
+        auto issue_pv = [&](int Gp, bool first) {
+            mbar_wait(v_full, Gp & 1);
+            for (int t = 0; t < 2; ++t) {
+                mbar_wait(p_full(t), Gp & 1);   // P_t in smem, O_t rescaled
+                tc_fence_after();
+                if (lane == 0) {
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) {
+                        const uint32_t pa = p_s(t) + 16384u * (k >> 2) + 32u * (k & 3);
+                        const uint32_t vb = v_s + 16384u * (k >> 2) + 2048u * (k & 3);
+                        mma_bf16(O_t(t), smem_desc(pa, 16, 1024, kSw128), smem_desc(vb, 8192, 1024, kSw128), idesc_o,
+                                 (!first || k > 0) ? 1u : 0u);
+                    }
+                    mma_commit(o_done(t));
+                }
+                __syncwarp();
+            }
+            if (lane == 0) mma_commit(v_empty);
+            __syncwarp();
+        };
+        int G = 0, u = 0;
+        for (int w = blockIdx.x; w < n_units; w += gridDim.x, ++u) {
+            const AttnItem it = a.items[w / hpairs];
+            const int nkb = it.qb + 1;
+            mbar_wait(q_full, u & 1);
+            for (int j = 0; j < nkb; ++j, ++G) {
+                const int b = G & 1;
+                mbar_wait(k_full(b), (G >> 1) & 1);
+                for (int t = 0; t < 2; ++t) {
+                    if (G > 0) mbar_wait(s_free(t), (G - 1) & 1);   // softmax t has read S_t(G-1)
+                    tc_fence_after();
+                    if (lane == 0) {
+#pragma unroll
+                        for (int k = 0; k < 8; ++k) {
+                            const uint32_t off = 16384u * (k >> 2) + 32u * (k & 3);
+                            mma_bf16(S_t(t), smem_desc(q_s(t) + off, 16, 1024, kSw128), smem_desc(k_s(b) + off, 16, 1024, kSw128),
+                                     idesc_s, k > 0);
+                        }
+                        mma_commit(s_full(t));
+                    }
+                    __syncwarp();
+                }
+                if (lane == 0) {
+                    mma_commit(k_empty(b));
+                    if (j == nkb - 1) mma_commit(q_empty);
+                }
+                __syncwarp();
+                if (j > 0) issue_pv(G - 1, j == 1);
+            }
+            issue_pv(G - 1, nkb == 1);   // the unit's last block
+        }
+    } else if (warp >= 4) {
+        // ---------------- online softmax + epilogue of tile t (thread = query row) ----------------
+        const int t = (warp - 4) >> 2;
+        const int m = (threadIdx.x - 128) & 127;
+        const uint32_t lane_base = (uint32_t)(((warp - 4) & 3) * 32) << 16;
+        const float sl2 = a.scale * 1.4426950408889634f;
+        uint8_t *pbuf = base_ptr + (p_s(t) - base);   // P_t: two 64-key halves, SW128
+        int G = 0;
+        for (int w = blockIdx.x; w < n_units; w += gridDim.x) {
+            const AttnItem it = a.items[w / hpairs];
+            const int head = 2 * (w % hpairs) + t, nkb = it.qb + 1;
+            const int qi = it.qb * 128 + m;   // query position inside the segment
+            float mi = -INFINITY, li = 0.f;   // reference max (log2 units), row sum
+            for (int j = 0; j < nkb; ++j, ++G) {
+                mbar_wait(s_full(t), G & 1);
+                tc_fence_after();
+                uint32_t sr[128];
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    uint32_t r[32];
+                    tmem_ld32(S_t(t) + lane_base + 32u * c, r);
+#pragma unroll
+                    for (int e = 0; e < 32; ++e) sr[32 * c + e] = r[e];
+                }
+                tmem_wait_ld();
+                tc_fence_before();
+                mbar_arrive(s_free(t));
+                // keys visible to this row: kj <= qi and kj < len; masked keys -> -inf (warp-uniform
+                // branch: only the diagonal and segment-end blocks)
+                const int lim = min(qi + 1, it.len) - j * 128;
+                if (!__all_sync(0xffffffffu, lim >= 128)) {
+#pragma unroll
+                    for (int e = 0; e < 128; ++e)
+                        if (e >= lim) sr[e] = 0xff800000u;
+                }
+                float mx = -INFINITY;
+#pragma unroll
+                for (int e = 0; e < 128; ++e) mx = fmaxf(mx, __uint_as_float(sr[e]));
+                // lazy rescaling: the reference max moves only past 2^8 (probabilities <= 256)
+                const float m_new = (mx * sl2 > mi + 8.f) ? mx * sl2 : mi;
+                const float alpha = fast_exp2(mi - m_new);   // 0 on the first block, else 1 unless moved
+                // PV_t(G-1) has read P_t and updated O_t (also the previous unit's last block)
+                if (G > 0) mbar_wait(o_done(t), (G - 1) & 1);
+                tc_fence_after();
+                float sum = 0.f;
+                const float nm = -m_new;
+#pragma unroll
+                for (int ch = 0; ch < 16; ++ch) {   // 16-byte chunks of 8 keys: chunk ch of key half ch / 8
+                    uint32_t pk[4];
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const int e = 8 * ch + 2 * q;
+                        const float p0 = fast_exp2(fmaf(__uint_as_float(sr[e]), sl2, nm));
+                        const float p1 = fast_exp2(fmaf(__uint_as_float(sr[e + 1]), sl2, nm));
+                        sum += p0 + p1;
+                        const __nv_bfloat162 b2 = __floats2bfloat162_rn(p0, p1);
+                        pk[q] = *reinterpret_cast<const uint32_t *>(&b2);
+                    }
+                    const int kh = ch >> 3, cc = ch & 7;
+                    *reinterpret_cast<uint4 *>(pbuf + kh * 16384 + m * 128 + ((cc ^ (m & 7)) << 4)) =
+                        make_uint4(pk[0], pk[1], pk[2], pk[3]);
+                }
+                li = li * alpha + sum;
+                if (j > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {
+#pragma unroll 1
+                    for (int c = 0; c < 4; ++c) {
+                        uint32_t r[32];
+                        tmem_ld32(O_t(t) + lane_base + 32u * c, r);
+                        tmem_wait_ld();
+#pragma unroll
+                        for (int e = 0; e < 32; ++e) r[e] = __float_as_uint(__uint_as_float(r[e]) * alpha);
+                        tmem_st32(O_t(t) + lane_base + 32u * c, r);
+                    }
+                    tmem_wait_st();
+                }
+                mi = m_new;
+                fence_proxy_async_smem();   // P (generic stores) -> the MMA (async proxy)
+                tc_fence_before();
+                mbar_arrive(p_full(t));
+            }
+            // epilogue: O_t / l -> bf16 rows of O [S, Hq, d], staged in P_t (its last PV is done)
+            mbar_wait(o_done(t), (G - 1) & 1);
+            tc_fence_after();
+            const float inv = 1.f / li;
+#pragma unroll 1
+            for (int c = 0; c < 4; ++c) {
+                uint32_t r[32];
+                tmem_ld32(O_t(t) + lane_base + 32u * c, r);
+                tmem_wait_ld();
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    uint4 v;
+                    v.x = pack_bf16x2(__uint_as_float(r[8 * q + 0]) * inv, __uint_as_float(r[8 * q + 1]) * inv);
+                    v.y = pack_bf16x2(__uint_as_float(r[8 * q + 2]) * inv, __uint_as_float(r[8 * q + 3]) * inv);
+                    v.z = pack_bf16x2(__uint_as_float(r[8 * q + 4]) * inv, __uint_as_float(r[8 * q + 5]) * inv);
+                    v.w = pack_bf16x2(__uint_as_float(r[8 * q + 6]) * inv, __uint_as_float(r[8 * q + 7]) * inv);
+                    const int uu = 4 * c + q;   // 16-byte unit of the 256-byte row
+                    *reinterpret_cast<uint4 *>(pbuf + m * 256 + ((uu ^ (m & 15)) << 4)) = v;
+                }
+            }
+            named_bar_sync(1 + t, 128);
+            {
+                const int rsub = m >> 4, uu = m & 15;   // 8 rows per pass, 16 threads per row
+                __nv_bfloat16 *Ob = reinterpret_cast<__nv_bfloat16 *>(a.O);
+#pragma unroll 2
+                for (int r0 = 0; r0 < 128; r0 += 8) {
+                    const int rr = r0 + rsub;
+                    const int qr = it.qb * 128 + rr;
+                    if (qr < it.len)
+                        *reinterpret_cast<uint4 *>(Ob + ((size_t)(it.row0 + qr) * a.n_heads + head) * 128 + 8 * uu) =
+                            *reinterpret_cast<const uint4 *>(pbuf + rr * 256 + ((uu ^ (rr & 15)) << 4));
+                }
+            }
+            tc_fence_before();          // the O reads are ordered before the next unit's PV
+            named_bar_sync(1 + t, 128);   // the staging buffer is P_t of the next unit's first block
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 2) {
+        tc_fence_after();
+        tmem_dealloc(tmem, 512);
+    }
+}
+
 // ---- KV-cache writes: row t of K/V [S, Hkv, d] -> cache slot / position (plan: AttnRow) ----
 __global__ void __launch_bounds__(256) attn_kv_write_kernel(const AttnArgs a) {
     pdl_wait();
@@ -565,9 +845,23 @@ int launch_attn(const AttnArgs &a, int n_items, int n_rows, int n_drows, int max
         int sms = 0, dev = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        const int units = n_items * a.n_heads;
-        e = launch_pdl(attn_prefill_kernel, dim3(units < sms ? units : sms), dim3(kAT), attn_prefill_smem(), st, a,
-                       units);
+        const int group = a.n_heads / a.n_kv_heads;
+        if (group % 2 == 0) {   // two query heads of one KV group per CTA
+            static bool attr2 = false;
+            if (!attr2) {
+                e = cudaFuncSetAttribute(attn_prefill2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)attn_prefill2_smem());
+                if (e != cudaSuccess) return (int)e;
+                attr2 = true;
+            }
+            const int units = n_items * (a.n_heads / 2);
+            e = launch_pdl(attn_prefill2_kernel, dim3(units < sms ? units : sms), dim3(kAT2), attn_prefill2_smem(), st,
+                           a, units);
+        } else {
+            const int units = n_items * a.n_heads;
+            e = launch_pdl(attn_prefill_kernel, dim3(units < sms ? units : sms), dim3(kAT), attn_prefill_smem(), st, a,
+                           units);
+        }
         if (e != cudaSuccess) return (int)e;
     }
     if (n_drows) {
