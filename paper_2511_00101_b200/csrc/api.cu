@@ -2072,6 +2072,7 @@ int smlm_attention(const smlm_attn_batch *b, int n_heads, int n_kv_heads, int he
         if ((rc = make_map(&a.tmQ, Q, (uint64_t)n_heads * 128, S, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B))) return rc;
         if ((rc = make_map(&a.tmK, K, (uint64_t)n_kv_heads * 128, S, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B))) return rc;
         if ((rc = make_map(&a.tmV, V, (uint64_t)n_kv_heads * 128, S, 64, 64, CU_TENSOR_MAP_SWIZZLE_128B))) return rc;
+        if ((rc = make_map(&a.tmO, O, (uint64_t)n_heads * 128, S, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B))) return rc;
     }
     a.items = reinterpret_cast<const AttnItem *>(wsb);
     a.rows = reinterpret_cast<const AttnRow *>(wsb + rows_off);

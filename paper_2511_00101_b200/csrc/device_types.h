@@ -286,6 +286,7 @@ struct AttnArgs {
     CUtensorMap tmQ;   // Q [S, Hq*d] box {64, 128}
     CUtensorMap tmK;   // K [S, Hkv*d] box {64, 128}
     CUtensorMap tmV;   // V [S, Hkv*d] box {64, 64}
+    CUtensorMap tmO;   // O [S, Hq*d] box {64, 128} SW128 (TMA store of a full 128-row tile)
     const AttnItem *items;
     const AttnRow *rows;    // cache writes
     const AttnRow *drows;   // decode rows

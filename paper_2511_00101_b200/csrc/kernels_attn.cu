@@ -527,13 +527,24 @@ __global__ void __launch_bounds__(kAT2, 1) attn_prefill2_kernel(const __grid_con
         const float sl2 = a.scale * 1.4426950408889634f;
         uint8_t *pbuf = base_ptr + (p_s(t) - base);   // P_t: two 64-key halves, SW128
         int G = 0;
+#ifdef SMLM_MEASURE
+        long long c_ws = 0, c_ld = 0, c_mx = 0, c_wo = 0, c_exp = 0, c_rs = 0, c_ep = 0, c0, c_begin = clock64();
+#define TSTAMP() (c0 = clock64())
+#define TACC(x) (x += clock64() - c0)
+#else
+#define TSTAMP()
+#define TACC(x)
+#endif
         for (int w = blockIdx.x; w < n_units; w += gridDim.x) {
             const AttnItem it = a.items[w / hpairs];
             const int head = 2 * (w % hpairs) + t, nkb = it.qb + 1;
             const int qi = it.qb * 128 + m;   // query position inside the segment
             float mi = -INFINITY, li = 0.f;   // reference max (log2 units), row sum
             for (int j = 0; j < nkb; ++j, ++G) {
+                TSTAMP();
                 mbar_wait(s_full(t), G & 1);
+                TACC(c_ws);
+                TSTAMP();
                 tc_fence_after();
                 uint32_t sr[128];
 #pragma unroll
@@ -546,6 +557,8 @@ __global__ void __launch_bounds__(kAT2, 1) attn_prefill2_kernel(const __grid_con
                 tmem_wait_ld();
                 tc_fence_before();
                 mbar_arrive(s_free(t));
+                TACC(c_ld);
+                TSTAMP();
                 // keys visible to this row: kj <= qi and kj < len; masked keys -> -inf (warp-uniform
                 // branch: only the diagonal and segment-end blocks)
                 const int lim = min(qi + 1, it.len) - j * 128;
@@ -554,16 +567,21 @@ __global__ void __launch_bounds__(kAT2, 1) attn_prefill2_kernel(const __grid_con
                     for (int e = 0; e < 128; ++e)
                         if (e >= lim) sr[e] = 0xff800000u;
                 }
-                float mx = -INFINITY;
+                float mx4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};   // independent chains
 #pragma unroll
-                for (int e = 0; e < 128; ++e) mx = fmaxf(mx, __uint_as_float(sr[e]));
+                for (int e = 0; e < 128; ++e) mx4[e & 3] = fmaxf(mx4[e & 3], __uint_as_float(sr[e]));
+                const float mx = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3]));
                 // lazy rescaling: the reference max moves only past 2^8 (probabilities <= 256)
                 const float m_new = (mx * sl2 > mi + 8.f) ? mx * sl2 : mi;
                 const float alpha = fast_exp2(mi - m_new);   // 0 on the first block, else 1 unless moved
                 // PV_t(G-1) has read P_t and updated O_t (also the previous unit's last block)
+                TACC(c_mx);
+                TSTAMP();
                 if (G > 0) mbar_wait(o_done(t), (G - 1) & 1);
+                TACC(c_wo);
+                TSTAMP();
                 tc_fence_after();
-                float sum = 0.f;
+                float sum4[4] = {0.f, 0.f, 0.f, 0.f};   // independent chains
                 const float nm = -m_new;
 #pragma unroll
                 for (int ch = 0; ch < 16; ++ch) {   // 16-byte chunks of 8 keys: chunk ch of key half ch / 8
@@ -573,7 +591,7 @@ __global__ void __launch_bounds__(kAT2, 1) attn_prefill2_kernel(const __grid_con
                         const int e = 8 * ch + 2 * q;
                         const float p0 = fast_exp2(fmaf(__uint_as_float(sr[e]), sl2, nm));
                         const float p1 = fast_exp2(fmaf(__uint_as_float(sr[e + 1]), sl2, nm));
-                        sum += p0 + p1;
+                        sum4[q] += p0 + p1;
                         const __nv_bfloat162 b2 = __floats2bfloat162_rn(p0, p1);
                         pk[q] = *reinterpret_cast<const uint32_t *>(&b2);
                     }
@@ -581,7 +599,9 @@ __global__ void __launch_bounds__(kAT2, 1) attn_prefill2_kernel(const __grid_con
                     *reinterpret_cast<uint4 *>(pbuf + kh * 16384 + m * 128 + ((cc ^ (m & 7)) << 4)) =
                         make_uint4(pk[0], pk[1], pk[2], pk[3]);
                 }
-                li = li * alpha + sum;
+                li = li * alpha + ((sum4[0] + sum4[1]) + (sum4[2] + sum4[3]));
+                TACC(c_exp);
+                TSTAMP();
                 if (j > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {
 #pragma unroll 1
                     for (int c = 0; c < 4; ++c) {
@@ -598,29 +618,49 @@ __global__ void __launch_bounds__(kAT2, 1) attn_prefill2_kernel(const __grid_con
                 fence_proxy_async_smem();   // P (generic stores) -> the MMA (async proxy)
                 tc_fence_before();
                 mbar_arrive(p_full(t));
+                TACC(c_rs);
             }
+            TSTAMP();
             // epilogue: O_t / l -> bf16 rows of O [S, Hq, d], staged in P_t (its last PV is done)
             mbar_wait(o_done(t), (G - 1) & 1);
             tc_fence_after();
             const float inv = 1.f / li;
-#pragma unroll 1
-            for (int c = 0; c < 4; ++c) {
-                uint32_t r[32];
-                tmem_ld32(O_t(t) + lane_base + 32u * c, r);
+            const bool full = it.qb * 128 + 128 <= it.len;   // every row of the tile is stored
+            {
+                uint32_t r[4][32];   // the whole O row behind one wait
+#pragma unroll
+                for (int c = 0; c < 4; ++c) tmem_ld32(O_t(t) + lane_base + 32u * c, r[c]);
                 tmem_wait_ld();
 #pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    uint4 v;
-                    v.x = pack_bf16x2(__uint_as_float(r[8 * q + 0]) * inv, __uint_as_float(r[8 * q + 1]) * inv);
-                    v.y = pack_bf16x2(__uint_as_float(r[8 * q + 2]) * inv, __uint_as_float(r[8 * q + 3]) * inv);
-                    v.z = pack_bf16x2(__uint_as_float(r[8 * q + 4]) * inv, __uint_as_float(r[8 * q + 5]) * inv);
-                    v.w = pack_bf16x2(__uint_as_float(r[8 * q + 6]) * inv, __uint_as_float(r[8 * q + 7]) * inv);
-                    const int uu = 4 * c + q;   // 16-byte unit of the 256-byte row
-                    *reinterpret_cast<uint4 *>(pbuf + m * 256 + ((uu ^ (m & 15)) << 4)) = v;
-                }
+                for (int c = 0; c < 4; ++c)
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        uint4 v;
+                        v.x = pack_bf16x2(__uint_as_float(r[c][8 * q + 0]) * inv, __uint_as_float(r[c][8 * q + 1]) * inv);
+                        v.y = pack_bf16x2(__uint_as_float(r[c][8 * q + 2]) * inv, __uint_as_float(r[c][8 * q + 3]) * inv);
+                        v.z = pack_bf16x2(__uint_as_float(r[c][8 * q + 4]) * inv, __uint_as_float(r[c][8 * q + 5]) * inv);
+                        v.w = pack_bf16x2(__uint_as_float(r[c][8 * q + 6]) * inv, __uint_as_float(r[c][8 * q + 7]) * inv);
+                        const int uu = 4 * c + q;   // 16-byte unit of the 256-byte row
+                        if (full)   // two 64-column SW128 halves (the TMA store's layout, = P's)
+                            *reinterpret_cast<uint4 *>(pbuf + (uu >> 3) * 16384 + m * 128 + (((uu & 7) ^ (m & 7)) << 4)) = v;
+                        else
+                            *reinterpret_cast<uint4 *>(pbuf + m * 256 + ((uu ^ (m & 15)) << 4)) = v;
+                    }
             }
-            named_bar_sync(1 + t, 128);
-            {
+            if (full) {
+                fence_proxy_async_smem();
+                named_bar_sync(1 + t, 128);
+                if (m == 0) {
+                    for (int h = 0; h < 2; ++h)
+                        asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                                         reinterpret_cast<uint64_t>(&a.tmO)),
+                                     "r"(p_s(t) + 16384u * h), "r"(head * 128 + 64 * h), "r"(it.row0 + it.qb * 128)
+                                     : "memory");
+                    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");   // P_t reusable
+                }
+            } else {
+                named_bar_sync(1 + t, 128);
                 const int rsub = m >> 4, uu = m & 15;   // 8 rows per pass, 16 threads per row
                 __nv_bfloat16 *Ob = reinterpret_cast<__nv_bfloat16 *>(a.O);
 #pragma unroll 2
@@ -634,7 +674,19 @@ __global__ void __launch_bounds__(kAT2, 1) attn_prefill2_kernel(const __grid_con
             }
             tc_fence_before();          // the O reads are ordered before the next unit's PV
             named_bar_sync(1 + t, 128);   // the staging buffer is P_t of the next unit's first block
+            TACC(c_ep);
         }
+#ifdef SMLM_MEASURE
+        if (a.dbg && m == 0 && blockIdx.x % 16 == 0) {
+            const double T = (double)(clock64() - c_begin);
+            printf("[attn prefill2] cta %d tile %d blocks %d cycles %.0f wait_S %.1f%% ld_S %.1f%% mask+max %.1f%% wait_PVdone %.1f%% "
+                   "exp+P %.1f%% rescale+arrive %.1f%% epilogue %.1f%%\n",
+                   blockIdx.x, t, G, T, 100 * c_ws / T, 100 * c_ld / T, 100 * c_mx / T, 100 * c_wo / T, 100 * c_exp / T,
+                   100 * c_rs / T, 100 * c_ep / T);
+        }
+#endif
+#undef TSTAMP
+#undef TACC
     }
     tc_fence_before();
     __syncthreads();
