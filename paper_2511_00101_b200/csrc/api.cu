@@ -2027,7 +2027,7 @@ static size_t attn_plan_bytes(const AttnPlan &P) {
                     P.drows.size() * sizeof(AttnRow) + 64);
 }
 static size_t attn_part_bytes(const AttnPlan &P, int n_heads, int n_kv_heads) {
-    const size_t splits = (size_t)(P.max_dec_len + 255) / 256;
+    const size_t splits = (size_t)(P.max_dec_len + kAttnDecChunk - 1) / kAttnDecChunk;
     return align256(P.drows.size() * (size_t)n_heads * splits * 130 * sizeof(float));
 }
 
@@ -2087,7 +2087,7 @@ int smlm_attention(const smlm_attn_batch *b, int n_heads, int n_kv_heads, int he
     a.n_kv_heads = n_kv_heads;
     a.cache_capacity = cache_capacity;
     a.scale = scale;
-    a.max_splits = (P.max_dec_len + 255) / 256;
+    a.max_splits = (P.max_dec_len + kAttnDecChunk - 1) / kAttnDecChunk;
     a.dpart = reinterpret_cast<float *>(wsb + attn_plan_bytes(P));
     const int nl = (P.rows.empty() ? 0 : 1) + (P.items.empty() ? 0 : 1) + (P.drows.empty() ? 0 : 1);
     CKL(launch_attn(a, (int)P.items.size(), (int)P.rows.size(), (int)P.drows.size(), P.max_dec_len, st), nl);

@@ -270,6 +270,7 @@ struct AdamwArgs {
 };
 
 // ---- the Alg. 1 attention branch (kernels_attn.cu) ----
+constexpr int kAttnDecChunk = 128;   // decode attention: cached keys per split CTA
 struct alignas(16) AttnItem {   // prefill kernel: one 128-query block of a FINETUNE / EVAL / PREFILL segment
     int row0;    // first row of the segment
     int len;     // segment length (keys and queries are the segment's own rows)
@@ -297,7 +298,7 @@ struct AttnArgs {
     int cache_capacity;
     float scale;
     float *dpart;      // decode split partials [drows * n_kv_heads * max_splits][G][130] fp32
-    int max_splits;    // ceil(longest decode context / 256)
+    int max_splits;    // ceil(longest decode context / kAttnDecChunk)
     int dbg;           // measure build only (SMLM_ATTN_DEBUG): the softmax warps print their phase cycles
 };
 

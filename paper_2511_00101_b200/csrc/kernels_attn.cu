@@ -714,15 +714,19 @@ __global__ void __launch_bounds__(256) attn_kv_write_kernel(const AttnArgs a) {
     }
 }
 
-// ---- decode (split-KV): CTA (decode row, KV head, split) scores its 256 cached keys for the G query
-// heads of the group (thread per key: the whole 256-byte K row requested at once, so each CTA has
-// 64 KB of loads in flight), takes the chunk's softmax statistics, and accumulates P V with 16
-// threads per V row (16-byte loads); partial (max, sum, o) per head go to the workspace and
-// attn_decode_combine_kernel merges the splits in split order ----
-constexpr int kDecChunk = 256;
+// ---- decode (split-KV): CTA (decode row, KV head, split) takes kAttnDecChunk = 128 cached keys.
+// The chunk's K and V rows go to shared memory by row-coalesced cp.async (16 threads per 256-byte
+// row; K rows padded to 272 bytes so a thread per key reads its row conflict-free); the keys are
+// scored for the G query heads of the group, the chunk's softmax statistics taken, and P V
+// accumulated with 16 threads per V row; partial (max, sum, o) per head go to the workspace and
+// attn_decode_combine_kernel merges the splits in split order.  ~70 KB of shared memory: 3 CTAs
+// per SM (G <= 4) keep ~200 KB of loads in flight per SM ----
+constexpr int kDecChunk = kAttnDecChunk;
+constexpr int kKRowU = 17;   // 16-byte units per padded K row in shared memory
+constexpr size_t kDecSmem = (size_t)kDecChunk * kKRowU * 16 + (size_t)kDecChunk * 16 * 16;
 
 template <int G>
-__global__ void __launch_bounds__(256) attn_decode_split_kernel(const AttnArgs a) {
+__global__ void __launch_bounds__(256, G <= 4 ? 3 : 2) attn_decode_split_kernel(const AttnArgs a) {
     pdl_wait();
     pdl_trigger();
     const int s = blockIdx.x % a.max_splits;
@@ -733,30 +737,41 @@ __global__ void __launch_bounds__(256) attn_decode_split_kernel(const AttnArgs a
     const int j0 = s * kDecChunk;
     if (j0 >= L) return;
     const int nk = min(kDecChunk, L - j0);
+    extern __shared__ __align__(16) uint8_t dsm_raw[];
+    uint4 *ksm = reinterpret_cast<uint4 *>(dsm_raw);                       // [kDecChunk][17]
+    uint4 *vsm = ksm + kDecChunk * kKRowU;                                 // [kDecChunk][16]
+    float(*red)[G][128] = reinterpret_cast<float(*)[G][128]>(dsm_raw);    // [8 warps][G][128], over K after the scores
     __shared__ float qs[G][128];
     __shared__ float sc[G][kDecChunk];
-    __shared__ float red[8][G][128];   // [warp][head][128] partial outputs
     __shared__ float mloc[G];
-    const __nv_bfloat16 *Q = reinterpret_cast<const __nv_bfloat16 *>(a.Q) + ((size_t)rw.row * a.n_heads + kvh * G) * 128;
-    for (int e = threadIdx.x; e < G * 128; e += blockDim.x) qs[e / 128][e % 128] = __bfloat162float(Q[e]) * a.scale;
-    __syncthreads();
     const size_t row_elems = (size_t)a.n_kv_heads * 128;
     const __nv_bfloat16 *Kc = reinterpret_cast<const __nv_bfloat16 *>(a.K_cache) +
                               ((size_t)rw.slot * a.cache_capacity + j0) * row_elems + kvh * 128;
     const __nv_bfloat16 *Vc = reinterpret_cast<const __nv_bfloat16 *>(a.V_cache) +
                               ((size_t)rw.slot * a.cache_capacity + j0) * row_elems + kvh * 128;
     const int t = threadIdx.x;
-    if (t < nk) {
-        const uint4 *kr = reinterpret_cast<const uint4 *>(Kc + (size_t)t * row_elems);
-        uint4 u[16];
-#pragma unroll
-        for (int v = 0; v < 16; ++v) u[v] = kr[v];
+    for (int i = t; i < nk * 16; i += blockDim.x) {
+        const int row = i >> 4, u = i & 15;
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(ksm + row * kKRowU + u)),
+                     "l"(reinterpret_cast<const uint4 *>(Kc + (size_t)row * row_elems) + u)
+                     : "memory");
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(vsm + i)),
+                     "l"(reinterpret_cast<const uint4 *>(Vc + (size_t)row * row_elems) + u)
+                     : "memory");
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    const __nv_bfloat16 *Q = reinterpret_cast<const __nv_bfloat16 *>(a.Q) + ((size_t)rw.row * a.n_heads + kvh * G) * 128;
+    for (int e = t; e < G * 128; e += blockDim.x) qs[e / 128][e % 128] = __bfloat162float(Q[e]) * a.scale;
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncthreads();
+    if (t < nk) {   // thread per key
         float acc[G];
 #pragma unroll
         for (int g = 0; g < G; ++g) acc[g] = 0.f;
-#pragma unroll
+#pragma unroll 4
         for (int v = 0; v < 16; ++v) {
-            const __nv_bfloat162 *h2 = reinterpret_cast<const __nv_bfloat162 *>(&u[v]);
+            const uint4 u = ksm[t * kKRowU + v];
+            const __nv_bfloat162 *h2 = reinterpret_cast<const __nv_bfloat162 *>(&u);
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
                 const float2 kf = __bfloat1622float2(h2[i]);
@@ -768,7 +783,7 @@ __global__ void __launch_bounds__(256) attn_decode_split_kernel(const AttnArgs a
 #pragma unroll
         for (int g = 0; g < G; ++g) sc[g][t] = acc[g];
     }
-    __syncthreads();
+    __syncthreads();   // K is dead from here on: its space takes the per-warp partial outputs
     const int warp = t >> 5, lane = t & 31;
     if (warp < G) {   // the chunk's max per head, then p = exp(s - max) in place
         float mx = -INFINITY;
@@ -779,39 +794,31 @@ __global__ void __launch_bounds__(256) attn_decode_split_kernel(const AttnArgs a
         if (lane == 0) mloc[warp] = mx;
     }
     __syncthreads();
-    // P V: thread (key group kq, dims 8 dq .. 8 dq + 7); 16 keys per round, all 16 rounds' loads first
+    // P V: thread (key group kq, dims 8 dq .. 8 dq + 7): keys kq + 16 r
     const int kq = t >> 4, dq = t & 15;
     float o[G][8];
 #pragma unroll
     for (int g = 0; g < G; ++g)
 #pragma unroll
         for (int e = 0; e < 8; ++e) o[g][e] = 0.f;
-#pragma unroll 1
-    for (int r0 = 0; r0 < 16; r0 += 8) {
-        uint4 u[8];
+#pragma unroll 2
+    for (int r = 0; r < kDecChunk / 16; ++r) {
+        const int j = kq + 16 * r;
+        if (j < nk) {
+            const uint4 u = vsm[j * 16 + dq];
+            const __nv_bfloat162 *h2 = reinterpret_cast<const __nv_bfloat162 *>(&u);
+            float vf[8];
 #pragma unroll
-        for (int r = 0; r < 8; ++r) {
-            const int j = kq + 16 * (r0 + r);
-            u[r] = j < nk ? *reinterpret_cast<const uint4 *>(Vc + (size_t)j * row_elems + 8 * dq) : make_uint4(0, 0, 0, 0);
-        }
+            for (int i = 0; i < 4; ++i) {
+                const float2 f2 = __bfloat1622float2(h2[i]);
+                vf[2 * i] = f2.x;
+                vf[2 * i + 1] = f2.y;
+            }
 #pragma unroll
-        for (int r = 0; r < 8; ++r) {
-            const int j = kq + 16 * (r0 + r);
-            if (j < nk) {
-                const __nv_bfloat162 *h2 = reinterpret_cast<const __nv_bfloat162 *>(&u[r]);
-                float vf[8];
+            for (int g = 0; g < G; ++g) {
+                const float p = sc[g][j];
 #pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                    const float2 f2 = __bfloat1622float2(h2[i]);
-                    vf[2 * i] = f2.x;
-                    vf[2 * i + 1] = f2.y;
-                }
-#pragma unroll
-                for (int g = 0; g < G; ++g) {
-                    const float p = sc[g][j];
-#pragma unroll
-                    for (int e = 0; e < 8; ++e) o[g][e] = fmaf(p, vf[e], o[g][e]);
-                }
+                for (int e = 0; e < 8; ++e) o[g][e] = fmaf(p, vf[e], o[g][e]);
             }
         }
     }
@@ -918,11 +925,19 @@ int launch_attn(const AttnArgs &a, int n_items, int n_rows, int n_drows, int max
     }
     if (n_drows) {
         const dim3 grid(n_drows * a.n_kv_heads * a.max_splits);
+        static bool dattr = false;
+        if (!dattr) {
+            cudaFuncSetAttribute(attn_decode_split_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDecSmem);
+            cudaFuncSetAttribute(attn_decode_split_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDecSmem);
+            cudaFuncSetAttribute(attn_decode_split_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDecSmem);
+            cudaFuncSetAttribute(attn_decode_split_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDecSmem);
+            dattr = true;
+        }
         switch (a.n_heads / a.n_kv_heads) {
-            case 1: e = launch_pdl(attn_decode_split_kernel<1>, grid, dim3(256), 0, st, a); break;
-            case 2: e = launch_pdl(attn_decode_split_kernel<2>, grid, dim3(256), 0, st, a); break;
-            case 4: e = launch_pdl(attn_decode_split_kernel<4>, grid, dim3(256), 0, st, a); break;
-            case 8: e = launch_pdl(attn_decode_split_kernel<8>, grid, dim3(256), 0, st, a); break;
+            case 1: e = launch_pdl(attn_decode_split_kernel<1>, grid, dim3(256), kDecSmem, st, a); break;
+            case 2: e = launch_pdl(attn_decode_split_kernel<2>, grid, dim3(256), kDecSmem, st, a); break;
+            case 4: e = launch_pdl(attn_decode_split_kernel<4>, grid, dim3(256), kDecSmem, st, a); break;
+            case 8: e = launch_pdl(attn_decode_split_kernel<8>, grid, dim3(256), kDecSmem, st, a); break;
             default: return (int)cudaErrorInvalidValue;
         }
         if (e != cudaSuccess) return (int)e;
