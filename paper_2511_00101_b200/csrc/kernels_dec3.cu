@@ -346,6 +346,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT3, 1) smlm_dec3_ke
             return reinterpret_cast<float4 *>(a.kpart) +
                    ((((size_t)(it.item0 + s2) * 2 + rank) * 8 + c) * 8) * 128 + m;
         };
+        // W tiles exchange their split partials in bf16 (each split accumulated in fp32 in TMEM; the
+        // owner adds its own fp32 chunk to the peers' bf16 ones in split order): [4 q][128 m] uint4
+        auto part_w = [&](int s2, int c) {
+            return reinterpret_cast<uint4 *>(a.kpart) + ((((size_t)(it.item0 + s2) * 2 + rank) * 8 + c) * 4) * 128 + m;
+        };
+        constexpr uint32_t kPartW = 128u * 32u * 2u;   // bytes of one bf16 chunk partial
         if (it.vtile) {
             // ---- V tile: only each row's own-adapter columns matter, so the split-K reduction moves
             // r_pad floats per row (not the whole 256-column accumulator) ----
@@ -470,11 +476,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT3, 1) smlm_dec3_ke
                     uint32_t rr[32];
                     tmem_ld32(tmem_base + lane_base + 32u * c, rr);
                     tmem_wait_ld();
-                    float4 *dst = part(it.s, c);
+                    uint4 *dst = part_w(it.s, c);
     #pragma unroll
-                    for (int q = 0; q < 8; ++q)
-                        __stcg(dst + q * 128, make_float4(__uint_as_float(rr[4 * q]), __uint_as_float(rr[4 * q + 1]),
-                                                          __uint_as_float(rr[4 * q + 2]), __uint_as_float(rr[4 * q + 3])));
+                    for (int q = 0; q < 4; ++q)
+                        __stcg(dst + q * 128, make_uint4(pack_bf16x2(__uint_as_float(rr[8 * q]), __uint_as_float(rr[8 * q + 1])),
+                                                         pack_bf16x2(__uint_as_float(rr[8 * q + 2]), __uint_as_float(rr[8 * q + 3])),
+                                                         pack_bf16x2(__uint_as_float(rr[8 * q + 4]), __uint_as_float(rr[8 * q + 5])),
+                                                         pack_bf16x2(__uint_as_float(rr[8 * q + 6]), __uint_as_float(rr[8 * q + 7]))));
                 }
                 named_bar_sync(1, 128);
                 if (tid_e == 0) {
@@ -490,12 +498,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT3, 1) smlm_dec3_ke
                 if (tid_e == 0) {
                     fence_proxy_async_global();
                     const int n_own = (8 - it.s + ks - 1) / ks;
-                    mbar_expect_tx(xbar, (uint32_t)(n_own * (ks - 1)) * 16384u);
+                    mbar_expect_tx(xbar, (uint32_t)(n_own * (ks - 1)) * kPartW);
                     int slot = 0;
                     for (int c = it.s; c < 8; c += ks)
                         for (int s2 = 0; s2 < ks; ++s2) {
                             if (s2 == it.s) continue;
-                            bulk_load(base + (uint32_t)slot * 16384u, part(s2, c) - m, 16384u, xbar);
+                            bulk_load(base + (uint32_t)slot * kPartW, part_w(s2, c) - m, kPartW, xbar);
                             ++slot;
                         }
                 }
@@ -519,14 +527,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT3, 1) smlm_dec3_ke
 #pragma unroll
                             for (int e = 0; e < 32; ++e) t[e] = __uint_as_float(rr[e]);
                         } else {
-                            const float4 *src = reinterpret_cast<const float4 *>(base_ptr + (size_t)(oi * (ks - 1) + j) * 16384u) + m;
+                            const uint4 *src = reinterpret_cast<const uint4 *>(base_ptr + (size_t)(oi * (ks - 1) + j) * kPartW) + m;
 #pragma unroll
-                            for (int q = 0; q < 8; ++q) {
-                                const float4 f = src[q * 128];
-                                t[4 * q] = f.x;
-                                t[4 * q + 1] = f.y;
-                                t[4 * q + 2] = f.z;
-                                t[4 * q + 3] = f.w;
+                            for (int q = 0; q < 4; ++q) {
+                                const uint4 f = src[q * 128];
+                                const __nv_bfloat162 *h = reinterpret_cast<const __nv_bfloat162 *>(&f);
+#pragma unroll
+                                for (int i = 0; i < 4; ++i) {
+                                    const float2 x = __bfloat1622float2(h[i]);
+                                    t[8 * q + 2 * i] = x.x;
+                                    t[8 * q + 2 * i + 1] = x.y;
+                                }
                             }
                             ++j;
                         }
