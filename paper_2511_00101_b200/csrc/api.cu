@@ -53,7 +53,7 @@ int adamw_grid(int num_sms, size_t n);
 int launch_adamw_sumsq(const AdamwArgs &a, float *partial, int grid, cudaStream_t st);
 int launch_fanout_signal(const FanoutFlags &f, cudaStream_t st);
 int launch_fanout_wait(const int *ready, int target, cudaStream_t st);
-int launch_attn(const AttnArgs &a, int n_items, int n_rows, int n_drows, int max_dec_len, cudaStream_t st);
+int launch_attn(const AttnArgs &a, int n_items, int n_rows, int n_drows, int n_dgroups, cudaStream_t st);
 int launch_adamw_step(const AdamwArgs &a, int grid, cudaStream_t st);
 int launch_shrink_split(const __nv_bfloat16 *X, const SlotDev *slots, const DevBlock *blocks,
                         const DevShortRow *srows, int n_blocks, int in_f, int r, int r_pad, float *part,
@@ -1977,6 +1977,7 @@ namespace {
 struct AttnPlan {
     std::vector<AttnItem> items;
     std::vector<AttnRow> rows, drows;
+    std::vector<AttnDGroup> dgroups;
     int max_dec_len = 0;
 };
 int attn_plan(const smlm_attn_batch *b, int n_heads, int n_kv_heads, int head_dim, int cache_slots, int capacity,
@@ -2001,7 +2002,10 @@ int attn_plan(const smlm_attn_batch *b, int n_heads, int n_kv_heads, int head_di
             const int past = b->seg_past ? b->seg_past[g] : 0;
             if (slot < 0 || slot >= cache_slots || past < 0 || past + L > capacity)
                 return set_err(SMLM_E_INVALID, "attention: a DECODE segment needs a cache slot with room for its rows");
+            // groups of up to kAttnDecCols / G rows share one read of the slot's K / V
+            const int rg = kAttnDecCols / (n_heads / n_kv_heads);
             for (int i = 0; i < L; ++i) {
+                if (i % rg == 0) P.dgroups.push_back({(int)P.drows.size(), std::min(rg, L - i), past + i, slot});
                 P.rows.push_back({a0 + i, slot, past + i, 0});
                 P.drows.push_back({a0 + i, slot, past + i, 0});
             }
@@ -2024,7 +2028,7 @@ smlm_pool_s g_attn_stage;   // pinned staging of the attention plans (no adapter
 
 static size_t attn_plan_bytes(const AttnPlan &P) {
     return align256(P.items.size() * sizeof(AttnItem) + P.rows.size() * sizeof(AttnRow) +
-                    P.drows.size() * sizeof(AttnRow) + 64);
+                    P.drows.size() * sizeof(AttnRow) + P.dgroups.size() * sizeof(AttnDGroup) + 64);
 }
 static size_t attn_part_bytes(const AttnPlan &P, int n_heads, int n_kv_heads) {
     const size_t splits = (size_t)(P.max_dec_len + kAttnDecChunk - 1) / kAttnDecChunk;
@@ -2063,6 +2067,8 @@ int smlm_attention(const smlm_attn_batch *b, int n_heads, int n_kv_heads, int he
     append(bytes, P.rows);
     const size_t drows_off = bytes.size();
     append(bytes, P.drows);
+    const size_t dgroups_off = bytes.size();
+    append(bytes, P.dgroups);
     if ((rc = stage_upload(&g_attn_stage, bytes, wsb, st))) return rc;
     AttnArgs a;
     memset(&a, 0, sizeof(a));
@@ -2074,9 +2080,15 @@ int smlm_attention(const smlm_attn_batch *b, int n_heads, int n_kv_heads, int he
         if ((rc = make_map(&a.tmV, V, (uint64_t)n_kv_heads * 128, S, 64, 64, CU_TENSOR_MAP_SWIZZLE_128B))) return rc;
         if ((rc = make_map(&a.tmO, O, (uint64_t)n_heads * 128, S, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B))) return rc;
     }
+    if (!P.drows.empty()) {
+        const uint64_t crow = (uint64_t)cache_slots * (uint64_t)cache_capacity;
+        if ((rc = make_map(&a.tmKc, K_cache, (uint64_t)n_kv_heads * 128, crow, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B))) return rc;
+        if ((rc = make_map(&a.tmVc, V_cache, (uint64_t)n_kv_heads * 128, crow, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B))) return rc;
+    }
     a.items = reinterpret_cast<const AttnItem *>(wsb);
     a.rows = reinterpret_cast<const AttnRow *>(wsb + rows_off);
     a.drows = reinterpret_cast<const AttnRow *>(wsb + drows_off);
+    a.dgroups = reinterpret_cast<const AttnDGroup *>(wsb + dgroups_off);
     a.Q = Q;
     a.K = K;
     a.V = V;
@@ -2090,7 +2102,7 @@ int smlm_attention(const smlm_attn_batch *b, int n_heads, int n_kv_heads, int he
     a.max_splits = (P.max_dec_len + kAttnDecChunk - 1) / kAttnDecChunk;
     a.dpart = reinterpret_cast<float *>(wsb + attn_plan_bytes(P));
     const int nl = (P.rows.empty() ? 0 : 1) + (P.items.empty() ? 0 : 1) + (P.drows.empty() ? 0 : 1);
-    CKL(launch_attn(a, (int)P.items.size(), (int)P.rows.size(), (int)P.drows.size(), P.max_dec_len, st), nl);
+    CKL(launch_attn(a, (int)P.items.size(), (int)P.rows.size(), (int)P.drows.size(), (int)P.dgroups.size(), st), nl);
     return SMLM_OK;
 }
 

@@ -283,14 +283,24 @@ struct alignas(16) AttnRow {    // a row written to the KV cache (kv-write) / a 
     int pos;     // cache position of this row (decode: it attends to cache[0 .. pos])
     int pad;
 };
+struct alignas(16) AttnDGroup {   // consecutive decode rows of one DECODE segment (one cache slot)
+    int d0;      // first decode row (index into drows)
+    int n;       // rows (n * G <= kAttnDecCols query columns)
+    int pos0;    // cache position of the first row (row i attends to cache[0 .. pos0 + i])
+    int slot;
+};
+constexpr int kAttnDecCols = 32;   // query columns (rows x GQA heads) of one decode CTA
 struct AttnArgs {
     CUtensorMap tmQ;   // Q [S, Hq*d] box {64, 128}
     CUtensorMap tmK;   // K [S, Hkv*d] box {64, 128}
     CUtensorMap tmV;   // V [S, Hkv*d] box {64, 64}
     CUtensorMap tmO;   // O [S, Hq*d] box {64, 128} SW128 (TMA store of a full 128-row tile)
+    CUtensorMap tmKc;  // K cache [slots * capacity, Hkv*d] box {64, 128} SW128 (decode chunks)
+    CUtensorMap tmVc;  // V cache, same
     const AttnItem *items;
     const AttnRow *rows;    // cache writes
     const AttnRow *drows;   // decode rows
+    const AttnDGroup *dgroups;   // decode row groups (a CTA reads its chunk of the slot's K / V once for them)
     const void *Q, *K, *V;
     void *O;
     void *K_cache, *V_cache;   // [slots, capacity, Hkv, d] bf16

@@ -714,150 +714,212 @@ __global__ void __launch_bounds__(256) attn_kv_write_kernel(const AttnArgs a) {
     }
 }
 
-// ---- decode (split-KV): CTA (decode row, KV head, split) takes kAttnDecChunk = 128 cached keys.
-// The chunk's K and V rows go to shared memory by row-coalesced cp.async (16 threads per 256-byte
-// row; K rows padded to 272 bytes so a thread per key reads its row conflict-free); the keys are
-// scored for the G query heads of the group, the chunk's softmax statistics taken, and P V
-// accumulated with 16 threads per V row; partial (max, sum, o) per head go to the workspace and
-// attn_decode_combine_kernel merges the splits in split order.  ~70 KB of shared memory: 3 CTAs
-// per SM (G <= 4) keep ~200 KB of loads in flight per SM ----
+// ---- decode (split-KV): CTA (decode row group, KV head, split) takes kAttnDecChunk = 128 cached
+// keys of the group's cache slot.  HBM-bound: the slot's K / V bytes are read once for all rows of
+// the group (the rows of one DECODE segment, up to kAttnDecCols / G of them) and the CTA's work
+// beside its 64 KB of loads is kept small so that three CTAs per SM keep ~190 KB in flight.  The
+// chunk's K and V arrive by TMA (SW128 boxes: ldmatrix conflict-free); the scores
+// S^T = K_chunk Q^T and O^T = V_chunk^T P run on mma.sync m16n8k16 (keys x query columns, column =
+// row * G + head, up to 32 columns; the tensor work is negligible, it only replaces CUDA-core dot
+// products); the chunk's max / sum / o (fp32) per (row, head) go to the workspace and
+// attn_decode_combine_kernel merges the splits in split order.  P is rounded to bf16 for the PV
+// product (as in the prefill kernel); the row sum is taken over the fp32 p ----
 constexpr int kDecChunk = kAttnDecChunk;
-constexpr int kKRowU = 17;   // 16-byte units per padded K row in shared memory
-constexpr size_t kDecSmem = (size_t)kDecChunk * kKRowU * 16 + (size_t)kDecChunk * 16 * 16;
-
-template <int G>
-__global__ void __launch_bounds__(256, G <= 4 ? 3 : 2) attn_decode_split_kernel(const AttnArgs a) {
-    pdl_wait();
-    pdl_trigger();
-    const int s = blockIdx.x % a.max_splits;
-    const int rk = blockIdx.x / a.max_splits;
-    const AttnRow rw = a.drows[rk / a.n_kv_heads];
-    const int kvh = rk % a.n_kv_heads;
-    const int L = rw.pos + 1;   // the cache holds the row itself (appended by attn_kv_write_kernel)
-    const int j0 = s * kDecChunk;
-    if (j0 >= L) return;
-    const int nk = min(kDecChunk, L - j0);
-    extern __shared__ __align__(16) uint8_t dsm_raw[];
-    uint4 *ksm = reinterpret_cast<uint4 *>(dsm_raw);                       // [kDecChunk][17]
-    uint4 *vsm = ksm + kDecChunk * kKRowU;                                 // [kDecChunk][16]
-    float(*red)[G][128] = reinterpret_cast<float(*)[G][128]>(dsm_raw);    // [8 warps][G][128], over K after the scores
-    __shared__ float qs[G][128];
-    __shared__ float sc[G][kDecChunk];
-    __shared__ float mloc[G];
-    const size_t row_elems = (size_t)a.n_kv_heads * 128;
-    const __nv_bfloat16 *Kc = reinterpret_cast<const __nv_bfloat16 *>(a.K_cache) +
-                              ((size_t)rw.slot * a.cache_capacity + j0) * row_elems + kvh * 128;
-    const __nv_bfloat16 *Vc = reinterpret_cast<const __nv_bfloat16 *>(a.V_cache) +
-                              ((size_t)rw.slot * a.cache_capacity + j0) * row_elems + kvh * 128;
-    const int t = threadIdx.x;
-    for (int i = t; i < nk * 16; i += blockDim.x) {
-        const int row = i >> 4, u = i & 15;
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(ksm + row * kKRowU + u)),
-                     "l"(reinterpret_cast<const uint4 *>(Kc + (size_t)row * row_elems) + u)
-                     : "memory");
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(vsm + i)),
-                     "l"(reinterpret_cast<const uint4 *>(Vc + (size_t)row * row_elems) + u)
-                     : "memory");
-    }
-    asm volatile("cp.async.commit_group;" ::: "memory");
-    const __nv_bfloat16 *Q = reinterpret_cast<const __nv_bfloat16 *>(a.Q) + ((size_t)rw.row * a.n_heads + kvh * G) * 128;
-    for (int e = t; e < G * 128; e += blockDim.x) qs[e / 128][e % 128] = __bfloat162float(Q[e]) * a.scale;
-    asm volatile("cp.async.wait_all;" ::: "memory");
-    __syncthreads();
-    if (t < nk) {   // thread per key
-        float acc[G];
-#pragma unroll
-        for (int g = 0; g < G; ++g) acc[g] = 0.f;
-#pragma unroll 4
-        for (int v = 0; v < 16; ++v) {
-            const uint4 u = ksm[t * kKRowU + v];
-            const __nv_bfloat162 *h2 = reinterpret_cast<const __nv_bfloat162 *>(&u);
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                const float2 kf = __bfloat1622float2(h2[i]);
-                const int d = 8 * v + 2 * i;
-#pragma unroll
-                for (int g = 0; g < G; ++g) acc[g] = fmaf(kf.x, qs[g][d], fmaf(kf.y, qs[g][d + 1], acc[g]));
-            }
-        }
-#pragma unroll
-        for (int g = 0; g < G; ++g) sc[g][t] = acc[g];
-    }
-    __syncthreads();   // K is dead from here on: its space takes the per-warp partial outputs
-    const int warp = t >> 5, lane = t & 31;
-    if (warp < G) {   // the chunk's max per head, then p = exp(s - max) in place
-        float mx = -INFINITY;
-        for (int j = lane; j < nk; j += 32) mx = fmaxf(mx, sc[warp][j]);
-#pragma unroll
-        for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-        for (int j = lane; j < nk; j += 32) sc[warp][j] = __expf(sc[warp][j] - mx);
-        if (lane == 0) mloc[warp] = mx;
-    }
-    __syncthreads();
-    // P V: thread (key group kq, dims 8 dq .. 8 dq + 7): keys kq + 16 r
-    const int kq = t >> 4, dq = t & 15;
-    float o[G][8];
-#pragma unroll
-    for (int g = 0; g < G; ++g)
-#pragma unroll
-        for (int e = 0; e < 8; ++e) o[g][e] = 0.f;
-#pragma unroll 2
-    for (int r = 0; r < kDecChunk / 16; ++r) {
-        const int j = kq + 16 * r;
-        if (j < nk) {
-            const uint4 u = vsm[j * 16 + dq];
-            const __nv_bfloat162 *h2 = reinterpret_cast<const __nv_bfloat162 *>(&u);
-            float vf[8];
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                const float2 f2 = __bfloat1622float2(h2[i]);
-                vf[2 * i] = f2.x;
-                vf[2 * i + 1] = f2.y;
-            }
-#pragma unroll
-            for (int g = 0; g < G; ++g) {
-                const float p = sc[g][j];
-#pragma unroll
-                for (int e = 0; e < 8; ++e) o[g][e] = fmaf(p, vf[e], o[g][e]);
-            }
-        }
-    }
-    // the two key groups of a warp (lanes l and l + 16 share dims) by a shuffle, then per warp in smem
-#pragma unroll
-    for (int g = 0; g < G; ++g)
-#pragma unroll
-        for (int e = 0; e < 8; ++e) o[g][e] += __shfl_xor_sync(0xffffffffu, o[g][e], 16);
-    if (lane < 16) {
-#pragma unroll
-        for (int g = 0; g < G; ++g) {
-            float4 *dst = reinterpret_cast<float4 *>(&red[warp][g][8 * dq]);
-            dst[0] = make_float4(o[g][0], o[g][1], o[g][2], o[g][3]);
-            dst[1] = make_float4(o[g][4], o[g][5], o[g][6], o[g][7]);
-        }
-    }
-    __syncthreads();
-    // partial of this split: [g] {max, sum, o[128]} in fp32, key groups summed in order
-    float *part = a.dpart + (((size_t)rk * a.max_splits + s) * G) * 130;
-    for (int e = t; e < G * 128; e += blockDim.x) {
-        const int g = e / 128, d = e % 128;
-        float acc = 0.f;
-#pragma unroll
-        for (int q = 0; q < 8; ++q) acc += red[q][g][d];
-        part[g * 130 + 2 + d] = acc;
-    }
-    if (warp < G) {
-        float l = 0.f;
-        for (int j = lane; j < nk; j += 32) l += sc[warp][j];
-#pragma unroll
-        for (int off = 16; off; off >>= 1) l += __shfl_xor_sync(0xffffffffu, l, off);
-        if (lane == 0) {
-            part[warp * 130 + 0] = mloc[warp];
-            part[warp * 130 + 1] = l;
-        }
-    }
+constexpr size_t kDecSmem = 1024 + 2 * 32768;   // K and V chunks, each two 64-column SW128 halves
+// byte offset of 16-byte unit c (0..15, 8 bf16 of d) of key row r in a SW128 chunk
+__device__ __forceinline__ uint32_t dec_sw(int r, int c) {
+    return (uint32_t)((c >> 3) * 16384 + r * 128 + (((c & 7) ^ (r & 7)) << 4));
 }
 
-__global__ void __launch_bounds__(128) attn_decode_combine_kernel(const AttnArgs a) {
+__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t &r0, uint32_t &r1, uint32_t &r2, uint32_t &r3) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3) : "r"(addr));
+}
+__device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t &r0, uint32_t &r1, uint32_t &r2, uint32_t &r3) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3) : "r"(addr));
+}
+__device__ __forceinline__ void mma16816(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t b0,
+                                         uint32_t b1) {
+    asm volatile("mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, {%8, %9}, "
+                 "{%0, %1, %2, %3};"
+                 : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+                 : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+
+template <int G>
+__global__ void __launch_bounds__(128, 3) attn_decode_split_kernel(const __grid_constant__ AttnArgs a) {
+    pdl_wait();
+    pdl_trigger();
+    constexpr int NT = kAttnDecCols / 8;   // n8 tiles of query columns (column = row * G + head)
+    const int s = blockIdx.x % a.max_splits;
+    const int kvh = (blockIdx.x / a.max_splits) % a.n_kv_heads;
+    const AttnDGroup grp = a.dgroups[blockIdx.x / (a.max_splits * a.n_kv_heads)];
+    const int Lmax = grp.pos0 + grp.n;   // keys of the group's last row (the cache holds the rows themselves)
+    const int j0 = s * kDecChunk;
+    if (j0 >= Lmax) return;
+    const int nk = min(kDecChunk, Lmax - j0);
+    const int ncol = grp.n * G, ntiles = (ncol + 7) >> 3;
+    extern __shared__ __align__(16) uint8_t dsm_raw0[];
+    uint8_t *dsm_raw = dsm_raw0 + ((1024u - (smem_u32(dsm_raw0) & 1023u)) & 1023u);   // SW128: 1 KB aligned
+    uint8_t *ksm = dsm_raw;              // K chunk [128 keys][128 d], two SW128 halves of 64 d
+    uint8_t *vsm = dsm_raw + 32768;      // V chunk, same
+    __nv_bfloat16(*pb)[136] = reinterpret_cast<__nv_bfloat16(*)[136]>(dsm_raw);   // P [32 columns][136] over K after S
+    __shared__ __align__(8) uint64_t bars[2];
+    const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+    // the chunk's K and V rows by TMA (one 2-D box per 64 d; rows past the chunk are the slot's later
+    // positions or the next slot's: masked in S, zeroed in V before P V)
+    const int crow = grp.slot * a.cache_capacity + j0;
+    if (t == 0) {
+        mbar_init(smem_u32(&bars[0]), 1);
+        mbar_init(smem_u32(&bars[1]), 1);
+        fence_mbar_init();
+        mbar_expect_tx(smem_u32(&bars[0]), 32768u);
+        for (int h = 0; h < 2; ++h) tma_load_2d(smem_u32(ksm) + 16384u * h, &a.tmKc, smem_u32(&bars[0]), kvh * 128 + 64 * h, crow);
+        mbar_expect_tx(smem_u32(&bars[1]), 32768u);
+        for (int h = 0; h < 2; ++h) tma_load_2d(smem_u32(vsm) + 16384u * h, &a.tmVc, smem_u32(&bars[1]), kvh * 128 + 64 * h, crow);
+    }
+    // Q^T as the B operand (k = d, n = column): n = 8 nt + lane / 4, k pairs 2 (lane % 4) (+ 8)
+    const int gq = lane >> 2, tq = lane & 3;
+    uint32_t qb[NT][8][2];
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+        const int n = 8 * nt + gq;
+        const bool in = n < ncol;
+        const int drow = grp.d0 + (in ? n / G : 0);
+        const uint32_t *Qh = reinterpret_cast<const uint32_t *>(
+            reinterpret_cast<const __nv_bfloat16 *>(a.Q) + ((size_t)a.drows[drow].row * a.n_heads + kvh * G + n % G) * 128);
+#pragma unroll
+        for (int ks = 0; ks < 8; ++ks) {
+            qb[nt][ks][0] = (in && nt < ntiles) ? Qh[8 * ks + tq] : 0u;
+            qb[nt][ks][1] = (in && nt < ntiles) ? Qh[8 * ks + 4 + tq] : 0u;
+        }
+    }
+    __syncthreads();   // barrier init visible
+    mbar_wait(smem_u32(&bars[0]), 0);   // K
+    // S^T (keys x columns): warp w takes keys 32 w .. 32 w + 31 (two m16 tiles), 8 k16 steps over d
+    float c[2][NT][4] = {};
+    {
+        const uint32_t kb = smem_u32(ksm);
+#pragma unroll
+        for (int ks = 0; ks < 8; ++ks)
+#pragma unroll
+            for (int mt = 0; mt < 2; ++mt) {
+                uint32_t a0, a1, a2, a3;
+                ldsm_x4(kb + dec_sw(32 * warp + 16 * mt + (lane & 15), 2 * ks + (lane >> 4)), a0, a1, a2, a3);
+#pragma unroll
+                for (int nt = 0; nt < NT; ++nt)
+                    if (nt < ntiles) mma16816(c[mt][nt], a0, a1, a2, a3, qb[nt][ks][0], qb[nt][ks][1]);
+            }
+    }
+    // the chunk's softmax per query column n (row r = n / G sees cache positions <= pos0 + r), in
+    // registers: column max and sum over the warp's 32 keys by shuffles (lanes of equal lane % 4),
+    // across the 4 warps through shared memory
+    __shared__ float red_m[4][kAttnDecCols], red_l[4][kAttnDecCols];
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt)
+        if (nt < ntiles)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int n = 8 * nt + 2 * tq + e;
+                const int last = min(nk - 1, grp.pos0 + n / G - j0);   // last visible key of the chunk
+                float m = -INFINITY;
+#pragma unroll
+                for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const int key = 32 * warp + 16 * mt + gq + 8 * h;
+                        const float v = key <= last ? c[mt][nt][2 * h + e] * a.scale : -INFINITY;
+                        c[mt][nt][2 * h + e] = v;
+                        m = fmaxf(m, v);
+                    }
+                m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 4));
+                m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 8));
+                m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 16));
+                if (gq == 0) red_m[warp][n] = m;
+            }
+    __syncthreads();   // every warp is past S: K's space takes P
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt)
+        if (nt < ntiles)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int n = 8 * nt + 2 * tq + e;
+                const float M = fmaxf(fmaxf(red_m[0][n], red_m[1][n]), fmaxf(red_m[2][n], red_m[3][n]));
+                float l = 0.f;
+#pragma unroll
+                for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const float v = c[mt][nt][2 * h + e];
+                        const float p = v > -INFINITY ? __expf(v - M) : 0.f;
+                        l += p;
+                        pb[n][32 * warp + 16 * mt + gq + 8 * h] = __float2bfloat16_rn(p);
+                    }
+                l += __shfl_xor_sync(0xffffffffu, l, 4);
+                l += __shfl_xor_sync(0xffffffffu, l, 8);
+                l += __shfl_xor_sync(0xffffffffu, l, 16);
+                if (gq == 0) red_l[warp][n] = l;
+            }
+    mbar_wait(smem_u32(&bars[1]), 0);   // V
+    for (int i = nk * 16 + t; i < kDecChunk * 16; i += blockDim.x)   // V rows past the chunk: zero (p = 0 there)
+        *reinterpret_cast<uint4 *>(vsm + dec_sw(i >> 4, i & 15)) = make_uint4(0, 0, 0, 0);
+    __syncthreads();
+    // the partial records of the columns whose row sees keys of this chunk: {max, sum, o[128]}
+    auto rec = [&](int n) -> float * {
+        const int r = n / G;
+        return (n < ncol && j0 <= grp.pos0 + r)
+                   ? a.dpart + ((((size_t)(grp.d0 + r) * a.n_kv_heads + kvh) * a.max_splits + s) * G + n % G) * 130
+                   : nullptr;
+    };
+    if (t < ncol) {
+        float *pr = rec(t);
+        if (pr) {
+            pr[0] = fmaxf(fmaxf(red_m[0][t], red_m[1][t]), fmaxf(red_m[2][t], red_m[3][t]));
+            pr[1] = (red_l[0][t] + red_l[1][t]) + (red_l[2][t] + red_l[3][t]);
+        }
+    }
+    // O^T (d x columns) = V^T P: warp w takes d = 32 w .. 32 w + 31 (two m16 tiles), 8 k16 steps over keys
+    float o[2][NT][4] = {};
+    {
+        const uint32_t vb = smem_u32(vsm);
+        const int vr = (lane & 7) + ((lane >> 4) & 1) * 8, vc = 4 * warp + ((lane >> 3) & 1);
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+            uint32_t b[NT][2];
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt) {
+                const uint32_t *pw = reinterpret_cast<const uint32_t *>(&pb[8 * nt + gq][0]);
+                b[nt][0] = nt < ntiles ? pw[8 * kk + tq] : 0u;
+                b[nt][1] = nt < ntiles ? pw[8 * kk + 4 + tq] : 0u;
+            }
+#pragma unroll
+            for (int mt = 0; mt < 2; ++mt) {
+                uint32_t a0, a1, a2, a3;
+                ldsm_x4_t(vb + dec_sw(16 * kk + vr, vc + 2 * mt), a0, a1, a2, a3);
+#pragma unroll
+                for (int nt = 0; nt < NT; ++nt)
+                    if (nt < ntiles) mma16816(o[mt][nt], a0, a1, a2, a3, b[nt][0], b[nt][1]);
+            }
+        }
+    }
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt)
+        if (nt < ntiles)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                float *pr = rec(8 * nt + 2 * tq + e);
+                if (pr) {
+#pragma unroll
+                    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+                        for (int h = 0; h < 2; ++h) pr[2 + 32 * warp + 16 * mt + gq + 8 * h] = o[mt][nt][2 * h + e];
+                }
+            }
+}
+
+// thread (head g, dim d) of decode row rk / n_kv_heads: the splits merged in split order
+__global__ void __launch_bounds__(1024) attn_decode_combine_kernel(const AttnArgs a) {
     pdl_wait();
     pdl_trigger();
     const int G = a.n_heads / a.n_kv_heads;
@@ -865,21 +927,21 @@ __global__ void __launch_bounds__(128) attn_decode_combine_kernel(const AttnArgs
     const AttnRow rw = a.drows[rk / a.n_kv_heads];
     const int kvh = rk % a.n_kv_heads;
     const int ns = (rw.pos + 1 + kDecChunk - 1) / kDecChunk;
-    const int d = threadIdx.x;
-    for (int g = 0; g < G; ++g) {
-        const float *p0 = a.dpart + ((size_t)rk * a.max_splits * G + g) * 130;
-        float M = -INFINITY;
-        for (int s = 0; s < ns; ++s) M = fmaxf(M, p0[(size_t)s * G * 130]);
-        float l = 0.f, o = 0.f;
-        for (int s = 0; s < ns; ++s) {   // split order
-            const float *p = p0 + (size_t)s * G * 130;
-            const float w = __expf(p[0] - M);
-            l = fmaf(w, p[1], l);
-            o = fmaf(w, p[2 + d], o);
-        }
-        __nv_bfloat16 *O = reinterpret_cast<__nv_bfloat16 *>(a.O) + ((size_t)rw.row * a.n_heads + kvh * G + g) * 128;
-        O[d] = __float2bfloat16_rn(o / l);
+    const int g = threadIdx.x >> 7, d = threadIdx.x & 127;
+    const float *p0 = a.dpart + ((size_t)rk * a.max_splits * G + g) * 130;
+    float M = -INFINITY;
+#pragma unroll 4
+    for (int s = 0; s < ns; ++s) M = fmaxf(M, p0[(size_t)s * G * 130]);
+    float l = 0.f, o = 0.f;
+#pragma unroll 4
+    for (int s = 0; s < ns; ++s) {   // split order
+        const float *p = p0 + (size_t)s * G * 130;
+        const float w = __expf(p[0] - M);
+        l = fmaf(w, p[1], l);
+        o = fmaf(w, p[2 + d], o);
     }
+    __nv_bfloat16 *O = reinterpret_cast<__nv_bfloat16 *>(a.O) + ((size_t)rw.row * a.n_heads + kvh * G + g) * 128;
+    O[d] = __float2bfloat16_rn(o / l);
 }
 
 }  // namespace
@@ -887,7 +949,7 @@ __global__ void __launch_bounds__(128) attn_decode_combine_kernel(const AttnArgs
 size_t attn_prefill_smem() { return 1024 + kQBytes + 2 * kKVBytes + 2 * kPBytes + 128; }
 static_assert(120 + 4 <= 128, "prefill barriers exceed their area");
 
-int launch_attn(const AttnArgs &a, int n_items, int n_rows, int n_drows, int max_dec_len, cudaStream_t st) {
+int launch_attn(const AttnArgs &a, int n_items, int n_rows, int n_drows, int n_dgroups, cudaStream_t st) {
     cudaError_t e = cudaSuccess;
     if (n_rows) {
         e = launch_pdl(attn_kv_write_kernel, dim3(n_rows), dim3(256), 0, st, a);
@@ -924,7 +986,7 @@ int launch_attn(const AttnArgs &a, int n_items, int n_rows, int n_drows, int max
         if (e != cudaSuccess) return (int)e;
     }
     if (n_drows) {
-        const dim3 grid(n_drows * a.n_kv_heads * a.max_splits);
+        const dim3 grid(n_dgroups * a.n_kv_heads * a.max_splits);
         static bool dattr = false;
         if (!dattr) {
             cudaFuncSetAttribute(attn_decode_split_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDecSmem);
@@ -934,14 +996,15 @@ int launch_attn(const AttnArgs &a, int n_items, int n_rows, int n_drows, int max
             dattr = true;
         }
         switch (a.n_heads / a.n_kv_heads) {
-            case 1: e = launch_pdl(attn_decode_split_kernel<1>, grid, dim3(256), kDecSmem, st, a); break;
-            case 2: e = launch_pdl(attn_decode_split_kernel<2>, grid, dim3(256), kDecSmem, st, a); break;
-            case 4: e = launch_pdl(attn_decode_split_kernel<4>, grid, dim3(256), kDecSmem, st, a); break;
-            case 8: e = launch_pdl(attn_decode_split_kernel<8>, grid, dim3(256), kDecSmem, st, a); break;
+            case 1: e = launch_pdl(attn_decode_split_kernel<1>, grid, dim3(128), kDecSmem, st, a); break;
+            case 2: e = launch_pdl(attn_decode_split_kernel<2>, grid, dim3(128), kDecSmem, st, a); break;
+            case 4: e = launch_pdl(attn_decode_split_kernel<4>, grid, dim3(128), kDecSmem, st, a); break;
+            case 8: e = launch_pdl(attn_decode_split_kernel<8>, grid, dim3(128), kDecSmem, st, a); break;
             default: return (int)cudaErrorInvalidValue;
         }
         if (e != cudaSuccess) return (int)e;
-        e = launch_pdl(attn_decode_combine_kernel, dim3(n_drows * a.n_kv_heads), dim3(128), 0, st, a);
+        e = launch_pdl(attn_decode_combine_kernel, dim3(n_drows * a.n_kv_heads), dim3(128 * (a.n_heads / a.n_kv_heads)), 0,
+                       st, a);
     }
     return (int)e;
 }

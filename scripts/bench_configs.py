@@ -307,8 +307,9 @@ def attention_step(iters=20, past=1024):
     ms_dec = timed((DECODE,))
     fe = [(int(L), m) for L, m in zip(lens, modes) if m != DECODE and L > 0]
     flops = sum(4.0 * L * (L + 1) / 2 * 128 * hq for L, _ in fe)
-    n_dec = int(sum(L for L, m in zip(lens, modes) if m == DECODE))
-    dec_bytes = n_dec * hkv * (past + 1) * 128 * 2 * 2
+    # algorithmic decode bytes: each decode segment's cache (its past + its own rows) read once per
+    # KV head -- the rows of one segment share the slot's K / V (not once per decode row)
+    dec_bytes = sum((past + int(L)) * hkv * 128 * 2 * 2 for L, m in zip(lens, modes) if m == DECODE and L > 0)
     return {"workload": f"C4 batch, Llama-3-8B heads 32/8 d=128; decode rows over {past}-token caches",
             "prefill_ms": ms_pf, "prefill_tflops": flops / ms_pf / 1e9,
             "prefill_tensor_frac": flops / ms_pf / 1e9 / PEAKS["bf16_tflops"],

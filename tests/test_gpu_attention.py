@@ -38,7 +38,7 @@ def _run(offs, modes, slots, past, Q, K, V, Kc, Vc):
     return O.cpu(), Kd.cpu(), Vd.cpu()
 
 
-@pytest.mark.parametrize("hq,hkv", [(8, 2), (4, 4), (32, 8)])
+@pytest.mark.parametrize("hq,hkv", [(8, 2), (4, 4), (32, 8), (8, 4), (16, 2)])
 def test_mixed_batch_attention(hq, hkv):
     lengths = [200, 70, 300, 1, 3, 129, 1]
     modes = [FINETUNE, EVAL, PREFILL, DECODE, DECODE, PREFILL, DECODE]
@@ -52,6 +52,25 @@ def test_mixed_batch_attention(hq, hkv):
         a, bnd = offs[g], offs[g + 1]
         assert parity_err(O[a:bnd], Or[a:bnd]) <= BF16_TOL, (g, parity_err(O[a:bnd], Or[a:bnd]))
     # the cache writes are copies: bit-exact, and nothing else in the caches moved
+    assert np.array_equal(Kd.double().numpy(), Kr) and np.array_equal(Vd.double().numpy(), Vr)
+
+
+@pytest.mark.parametrize("hq,hkv", [(8, 2), (4, 4), (16, 2)])
+def test_multi_row_decode_segments(hq, hkv):
+    """DECODE segments of many rows (several row groups per segment: kAttnDecCols / G rows share one
+    read of the slot's K / V) whose rows straddle 128-key chunk boundaries: row i of a segment sees
+    cache[0 .. past + i], so rows of one group see different key counts in the boundary chunk."""
+    lengths = [37, 5, 70, 9]
+    modes = [DECODE, DECODE, DECODE, DECODE]
+    slots = [0, 1, 2, 3]
+    past = [120, 0, 250, 380]
+    offs, Q, K, V, Kc, Vc = _case(17 + hq, lengths, modes, slots, past, hq, hkv)
+    O, Kd, Vd = _run(offs, modes, slots, past, Q, K, V, Kc, Vc)
+    Or, Kr, Vr = OA.attention(offs, modes, slots, past, Q, K, V, Kc, Vc, 1.0 / math.sqrt(128))
+    assert not torch.isnan(O).any()
+    for g in range(len(modes)):
+        a, bnd = offs[g], offs[g + 1]
+        assert parity_err(O[a:bnd], Or[a:bnd]) <= BF16_TOL, (g, parity_err(O[a:bnd], Or[a:bnd]))
     assert np.array_equal(Kd.double().numpy(), Kr) and np.array_equal(Vd.double().numpy(), Vr)
 
 
