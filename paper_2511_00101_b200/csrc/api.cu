@@ -88,8 +88,13 @@ static bool measure_flag(const char *name) {
     const char *e = getenv(name);
     return e && *e && strcmp(e, "0") != 0;
 }
+static int measure_int(const char *name, int dflt) {
+    const char *e = getenv(name);
+    return e && *e ? atoi(e) : dflt;
+}
 #else
 static constexpr bool measure_flag(const char *) { return false; }
+static constexpr int measure_int(const char *, int dflt) { return dflt; }
 #endif
 struct HostProf {
     bool on = measure_flag("SMLM_HOST_PROF");
@@ -257,17 +262,19 @@ size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 // the CTAs sweep every n-tile, so each W n-tile is fetched from HBM once per group (~48 MB budget)
 int raster_group(int K) {
     const long tile = 128L * K * 2;
-    long g = (48L << 20) / tile;
+    long g = ((long)measure_int("SMLM_RASTER_BWD_MB", 48) << 20) / tile;
     if (g < 4) g = 4;
     if (g > 64) g = 64;
     return (int)g;
 }
-// CTA-pair GEMMs: pairs per raster group -- a ~64 MB budget of X tiles, then the groups
-// balanced (53 pairs at K = 4096: 2 groups of 27 / 26 instead of 24 + 24 + 5, so W is streamed
-// from HBM twice instead of three times)
+// CTA-pair GEMMs: pairs per raster group -- a ~24 MB budget of X tiles, then the groups
+// balanced (53 pairs at K = 4096: 5 groups of 11 / 10).  The L2 is two ~63 MB halves, one per
+// die, and the X band of a group is read from both: a 64 MB band (2 W passes on paper) measured
+// 3.2 GB of DRAM traffic for the C4 gate/up launch and 2.13 M tokens/s, 24 MB 2.4 GB and
+// 2.18-2.19 M (same box, scripts/sweep_raster.sh)
 int raster_group_pairs(int K, int n_pairs) {
     const long pair = 256L * K * 2;
-    long g = (64L << 20) / pair;
+    long g = ((long)measure_int("SMLM_RASTER_MB", 24) << 20) / pair;
     if (g < 2) g = 2;
     if (g > 64) g = 64;
     const long groups = (n_pairs + g - 1) / g;

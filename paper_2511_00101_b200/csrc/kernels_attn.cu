@@ -581,25 +581,28 @@ __global__ void __launch_bounds__(kAT2, 1) attn_prefill2_kernel(const __grid_con
                 TACC(c_wo);
                 TSTAMP();
                 tc_fence_after();
-                float sum4[4] = {0.f, 0.f, 0.f, 0.f};   // independent chains
-                const float nm = -m_new;
+                // packed fp32 pairs (FFMA2 / FADD2): the scale-and-shift and the row sum take one
+                // instruction per two keys
+                float2 sum2[4] = {{0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}};   // independent chains
+                const float2 sl2v = make_float2(sl2, sl2), nmv = make_float2(-m_new, -m_new);
 #pragma unroll
                 for (int ch = 0; ch < 16; ++ch) {   // 16-byte chunks of 8 keys: chunk ch of key half ch / 8
                     uint32_t pk[4];
 #pragma unroll
                     for (int q = 0; q < 4; ++q) {
                         const int e = 8 * ch + 2 * q;
-                        const float p0 = fast_exp2(fmaf(__uint_as_float(sr[e]), sl2, nm));
-                        const float p1 = fast_exp2(fmaf(__uint_as_float(sr[e + 1]), sl2, nm));
-                        sum4[q] += p0 + p1;
-                        const __nv_bfloat162 b2 = __floats2bfloat162_rn(p0, p1);
+                        const float2 x = __ffma2_rn(make_float2(__uint_as_float(sr[e]), __uint_as_float(sr[e + 1])), sl2v, nmv);
+                        const float2 p = make_float2(fast_exp2(x.x), fast_exp2(x.y));
+                        sum2[q] = __fadd2_rn(sum2[q], p);
+                        const __nv_bfloat162 b2 = __floats2bfloat162_rn(p.x, p.y);
                         pk[q] = *reinterpret_cast<const uint32_t *>(&b2);
                     }
                     const int kh = ch >> 3, cc = ch & 7;
                     *reinterpret_cast<uint4 *>(pbuf + kh * 16384 + m * 128 + ((cc ^ (m & 7)) << 4)) =
                         make_uint4(pk[0], pk[1], pk[2], pk[3]);
                 }
-                li = li * alpha + ((sum4[0] + sum4[1]) + (sum4[2] + sum4[3]));
+                const float2 s01 = __fadd2_rn(sum2[0], sum2[1]), s23 = __fadd2_rn(sum2[2], sum2[3]);
+                li = li * alpha + ((s01.x + s23.x) + (s01.y + s23.y));
                 TACC(c_exp);
                 TSTAMP();
                 if (j > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {
@@ -635,11 +638,15 @@ __global__ void __launch_bounds__(kAT2, 1) attn_prefill2_kernel(const __grid_con
                 for (int c = 0; c < 4; ++c)
 #pragma unroll
                     for (int q = 0; q < 4; ++q) {
-                        uint4 v;
-                        v.x = pack_bf16x2(__uint_as_float(r[c][8 * q + 0]) * inv, __uint_as_float(r[c][8 * q + 1]) * inv);
-                        v.y = pack_bf16x2(__uint_as_float(r[c][8 * q + 2]) * inv, __uint_as_float(r[c][8 * q + 3]) * inv);
-                        v.z = pack_bf16x2(__uint_as_float(r[c][8 * q + 4]) * inv, __uint_as_float(r[c][8 * q + 5]) * inv);
-                        v.w = pack_bf16x2(__uint_as_float(r[c][8 * q + 6]) * inv, __uint_as_float(r[c][8 * q + 7]) * inv);
+                        uint32_t vv[4];
+#pragma unroll
+                        for (int h = 0; h < 4; ++h) {   // FMUL2: two columns per instruction
+                            const float2 o2 = __fmul2_rn(make_float2(__uint_as_float(r[c][8 * q + 2 * h]),
+                                                                     __uint_as_float(r[c][8 * q + 2 * h + 1])),
+                                                         make_float2(inv, inv));
+                            vv[h] = pack_bf16x2(o2.x, o2.y);
+                        }
+                        const uint4 v = make_uint4(vv[0], vv[1], vv[2], vv[3]);
                         const int uu = 4 * c + q;   // 16-byte unit of the 256-byte row
                         if (full)   // two 64-column SW128 halves (the TMA store's layout, = P's)
                             *reinterpret_cast<uint4 *>(pbuf + (uu >> 3) * 16384 + m * 128 + (((uu & 7) ^ (m & 7)) << 4)) = v;
