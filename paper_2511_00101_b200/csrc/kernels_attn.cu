@@ -925,8 +925,9 @@ __global__ void __launch_bounds__(128, 3) attn_decode_split_kernel(const __grid_
             }
 }
 
-// thread (head g, dim d) of decode row rk / n_kv_heads: the splits merged in split order
-__global__ void __launch_bounds__(1024) attn_decode_combine_kernel(const AttnArgs a) {
+// thread (head g, dims 4 q .. 4 q + 3) of decode row rk / n_kv_heads: the splits merged in split
+// order.  32 threads per head: every CTA of the launch is resident in one wave
+__global__ void __launch_bounds__(256) attn_decode_combine_kernel(const AttnArgs a) {
     pdl_wait();
     pdl_trigger();
     const int G = a.n_heads / a.n_kv_heads;
@@ -934,21 +935,27 @@ __global__ void __launch_bounds__(1024) attn_decode_combine_kernel(const AttnArg
     const AttnRow rw = a.drows[rk / a.n_kv_heads];
     const int kvh = rk % a.n_kv_heads;
     const int ns = (rw.pos + 1 + kDecChunk - 1) / kDecChunk;
-    const int g = threadIdx.x >> 7, d = threadIdx.x & 127;
+    const int g = threadIdx.x >> 5, q = threadIdx.x & 31;
     const float *p0 = a.dpart + ((size_t)rk * a.max_splits * G + g) * 130;
     float M = -INFINITY;
 #pragma unroll 4
     for (int s = 0; s < ns; ++s) M = fmaxf(M, p0[(size_t)s * G * 130]);
-    float l = 0.f, o = 0.f;
+    float l = 0.f, o[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll 4
     for (int s = 0; s < ns; ++s) {   // split order
         const float *p = p0 + (size_t)s * G * 130;
         const float w = __expf(p[0] - M);
         l = fmaf(w, p[1], l);
-        o = fmaf(w, p[2 + d], o);
+        const float2 o01 = *reinterpret_cast<const float2 *>(p + 2 + 4 * q);   // 8-byte aligned (130 floats per record)
+        const float2 o23 = *reinterpret_cast<const float2 *>(p + 4 + 4 * q);
+        o[0] = fmaf(w, o01.x, o[0]);
+        o[1] = fmaf(w, o01.y, o[1]);
+        o[2] = fmaf(w, o23.x, o[2]);
+        o[3] = fmaf(w, o23.y, o[3]);
     }
-    __nv_bfloat16 *O = reinterpret_cast<__nv_bfloat16 *>(a.O) + ((size_t)rw.row * a.n_heads + kvh * G + g) * 128;
-    O[d] = __float2bfloat16_rn(o / l);
+    __nv_bfloat16 *O = reinterpret_cast<__nv_bfloat16 *>(a.O) + ((size_t)rw.row * a.n_heads + kvh * G + g) * 128 + 4 * q;
+    const float inv = 1.f / l;
+    *reinterpret_cast<uint2 *>(O) = make_uint2(pack_bf16x2(o[0] * inv, o[1] * inv), pack_bf16x2(o[2] * inv, o[3] * inv));
 }
 
 }  // namespace
@@ -1010,7 +1017,7 @@ int launch_attn(const AttnArgs &a, int n_items, int n_rows, int n_drows, int n_d
             default: return (int)cudaErrorInvalidValue;
         }
         if (e != cudaSuccess) return (int)e;
-        e = launch_pdl(attn_decode_combine_kernel, dim3(n_drows * a.n_kv_heads), dim3(128 * (a.n_heads / a.n_kv_heads)), 0,
+        e = launch_pdl(attn_decode_combine_kernel, dim3(n_drows * a.n_kv_heads), dim3(32 * (a.n_heads / a.n_kv_heads)), 0,
                        st, a);
     }
     return (int)e;
