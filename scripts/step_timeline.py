@@ -1,6 +1,9 @@
-"""Kernel timeline of one C4 layer-step via torch.profiler (CUPTI): busy time, memcpy time and
-idle gaps between consecutive device activities on the compute stream."""
+"""Kernel timeline of one C4 step via torch.profiler (CUPTI): busy time per kernel and the idle
+gaps between consecutive device activities.  With PDL a kernel's interval starts at its early
+launch (it waits in griddepcontrol.wait), so per-kernel busy times overlap and add up to more
+than the span: use the gaps (device idle) here and the ncu launch list for shares."""
 import json
+import re
 import os
 import sys
 
@@ -27,7 +30,8 @@ busy = {}
 gaps = []
 prev_end = None
 for e in ev:
-    k = e.name.split("(")[0][:60]
+    k = re.sub(r"^void ", "", e.name.replace("(anonymous namespace)::", "")).split("(")[0]
+    k = re.sub(r"^.*::(?=[A-Za-z_]\w*(<|$))", "", k)[:60]   # the kernel's own name (+ template args)
     busy[k] = busy.get(k, 0) + (e.time_range.end - e.time_range.start)
     if prev_end is not None and e.time_range.start > prev_end:
         gaps.append(e.time_range.start - prev_end)
