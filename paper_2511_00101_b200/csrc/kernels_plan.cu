@@ -25,10 +25,23 @@ struct PlanBlob {
 
 template <int N>
 __global__ void __launch_bounds__(256) plan_copy_kernel(uint4 *__restrict__ dst, const __grid_constant__ PlanBlob<N> b) {
-    pdl_wait();   // the previous call's kernels may still read this workspace (WAR)
-    pdl_trigger();
+    // the parameter reads go ahead of the grid-dependency wait (they touch no global memory):
+    // only the stores wait for the previous call's kernels, which may still read this workspace
+    constexpr int kPer = (N / 16 + 255) / 256;
     const uint32_t n16 = (b.n + 15) / 16;
-    for (uint32_t i = threadIdx.x; i < n16; i += blockDim.x) dst[i] = b.data[i];
+    uint4 v[kPer];
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) {
+        const uint32_t i = threadIdx.x + 256u * k;
+        if (i < n16) v[k] = b.data[i];
+    }
+    pdl_wait();
+    pdl_trigger();
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) {
+        const uint32_t i = threadIdx.x + 256u * k;
+        if (i < n16) dst[i] = v[k];
+    }
 }
 
 template <int N>
