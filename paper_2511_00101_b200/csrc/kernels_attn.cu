@@ -728,11 +728,15 @@ __global__ void __launch_bounds__(256) attn_kv_write_kernel(const AttnArgs a) {
 // chunk's K and V arrive by TMA (SW128 boxes: ldmatrix conflict-free); the scores
 // S^T = K_chunk Q^T and O^T = V_chunk^T P run on mma.sync m16n8k16 (keys x query columns, column =
 // row * G + head, up to 32 columns; the tensor work is negligible, it only replaces CUDA-core dot
-// products); the chunk's max / sum / o (fp32) per (row, head) go to the workspace and
+// products); K and V share one 32 KB buffer -- V is loaded into it once every warp is past S, so
+// its load overlaps the softmax and four CTAs fit an SM (42 KB each); the chunk's max / sum /
+// o (fp32) per (row, head) go to the workspace and
 // attn_decode_combine_kernel merges the splits in split order.  P is rounded to bf16 for the PV
 // product (as in the prefill kernel); the row sum is taken over the fp32 p ----
 constexpr int kDecChunk = kAttnDecChunk;
-constexpr size_t kDecSmem = 1024 + 2 * 32768;   // K and V chunks, each two 64-column SW128 halves
+// one 32 KB chunk buffer (K, then V once every warp is past S: the V load overlaps the softmax)
+// and P [32 columns][136] beside it: 42 KB, four CTAs per SM
+constexpr size_t kDecSmem = 1024 + 32768 + 32 * 136 * 2;
 // byte offset of 16-byte unit c (0..15, 8 bf16 of d) of key row r in a SW128 chunk
 __device__ __forceinline__ uint32_t dec_sw(int r, int c) {
     return (uint32_t)((c >> 3) * 16384 + r * 128 + (((c & 7) ^ (r & 7)) << 4));
@@ -755,7 +759,7 @@ __device__ __forceinline__ void mma16816(float (&d)[4], uint32_t a0, uint32_t a1
 }
 
 template <int G>
-__global__ void __launch_bounds__(128, 3) attn_decode_split_kernel(const __grid_constant__ AttnArgs a) {
+__global__ void __launch_bounds__(128, 4) attn_decode_split_kernel(const __grid_constant__ AttnArgs a) {
     pdl_wait();
     pdl_trigger();
     constexpr int NT = kAttnDecCols / 8;   // n8 tiles of query columns (column = row * G + head)
@@ -770,8 +774,8 @@ __global__ void __launch_bounds__(128, 3) attn_decode_split_kernel(const __grid_
     extern __shared__ __align__(16) uint8_t dsm_raw0[];
     uint8_t *dsm_raw = dsm_raw0 + ((1024u - (smem_u32(dsm_raw0) & 1023u)) & 1023u);   // SW128: 1 KB aligned
     uint8_t *ksm = dsm_raw;              // K chunk [128 keys][128 d], two SW128 halves of 64 d
-    uint8_t *vsm = dsm_raw + 32768;      // V chunk, same
-    __nv_bfloat16(*pb)[136] = reinterpret_cast<__nv_bfloat16(*)[136]>(dsm_raw);   // P [32 columns][136] over K after S
+    uint8_t *vsm = dsm_raw;              // V chunk, same layout, in K's buffer after S
+    __nv_bfloat16(*pb)[136] = reinterpret_cast<__nv_bfloat16(*)[136]>(dsm_raw + 32768);   // P [32 columns][136]
     __shared__ __align__(8) uint64_t bars[2];
     const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
     // the chunk's K and V rows by TMA (one 2-D box per 64 d; rows past the chunk are the slot's later
@@ -783,8 +787,6 @@ __global__ void __launch_bounds__(128, 3) attn_decode_split_kernel(const __grid_
         fence_mbar_init();
         mbar_expect_tx(smem_u32(&bars[0]), 32768u);
         for (int h = 0; h < 2; ++h) tma_load_2d(smem_u32(ksm) + 16384u * h, &a.tmKc, smem_u32(&bars[0]), kvh * 128 + 64 * h, crow);
-        mbar_expect_tx(smem_u32(&bars[1]), 32768u);
-        for (int h = 0; h < 2; ++h) tma_load_2d(smem_u32(vsm) + 16384u * h, &a.tmVc, smem_u32(&bars[1]), kvh * 128 + 64 * h, crow);
     }
     // Q^T as the B operand (k = d, n = column): n = 8 nt + lane / 4, k pairs 2 (lane % 4) (+ 8)
     const int gq = lane >> 2, tq = lane & 3;
@@ -845,7 +847,12 @@ __global__ void __launch_bounds__(128, 3) attn_decode_split_kernel(const __grid_
                 m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 16));
                 if (gq == 0) red_m[warp][n] = m;
             }
-    __syncthreads();   // every warp is past S: K's space takes P
+    __syncthreads();   // every warp is past S: K's buffer takes V
+    if (t == 0) {
+        fence_proxy_async_smem();   // the K reads (generic) before the async-proxy V writes
+        mbar_expect_tx(smem_u32(&bars[1]), 32768u);
+        for (int h = 0; h < 2; ++h) tma_load_2d(smem_u32(vsm) + 16384u * h, &a.tmVc, smem_u32(&bars[1]), kvh * 128 + 64 * h, crow);
+    }
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt)
         if (nt < ntiles)
