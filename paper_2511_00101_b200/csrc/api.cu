@@ -2013,8 +2013,8 @@ int attn_plan(const smlm_attn_batch *b, int n_heads, int n_kv_heads, int head_di
             const int rg = kAttnDecCols / (n_heads / n_kv_heads);
             for (int i = 0; i < L; ++i) {
                 if (i % rg == 0) P.dgroups.push_back({(int)P.drows.size(), std::min(rg, L - i), past + i, slot});
-                P.rows.push_back({a0 + i, slot, past + i, 0});
-                P.drows.push_back({a0 + i, slot, past + i, 0});
+                // appended to the cache by the decode kernel; pad = the segment's first new position
+                P.drows.push_back({a0 + i, slot, past + i, past});
             }
             P.max_dec_len = std::max(P.max_dec_len, past + L);
         } else {
@@ -2108,7 +2108,8 @@ int smlm_attention(const smlm_attn_batch *b, int n_heads, int n_kv_heads, int he
     a.scale = scale;
     a.max_splits = (P.max_dec_len + kAttnDecChunk - 1) / kAttnDecChunk;
     a.dpart = reinterpret_cast<float *>(wsb + attn_plan_bytes(P));
-    const int nl = (P.rows.empty() ? 0 : 1) + (P.items.empty() ? 0 : 1) + (P.drows.empty() ? 0 : 1);
+    // launches: the cache write of PREFILL rows, the prefill kernel, the decode split + combine
+    const int nl = (P.rows.empty() ? 0 : 1) + (P.items.empty() ? 0 : 1) + (P.drows.empty() ? 0 : 2);
     CKL(launch_attn(a, (int)P.items.size(), (int)P.rows.size(), (int)P.drows.size(), (int)P.dgroups.size(), st), nl);
     return SMLM_OK;
 }

@@ -281,7 +281,7 @@ struct alignas(16) AttnRow {    // a row written to the KV cache (kv-write) / a 
     int row;     // row of Q/K/V
     int slot;    // cache slot (-1: no write)
     int pos;     // cache position of this row (decode: it attends to cache[0 .. pos])
-    int pad;
+    int pad;     // decode rows: the segment's first new cache position (its rows are appended in-kernel)
 };
 struct alignas(16) AttnDGroup {   // consecutive decode rows of one DECODE segment (one cache slot)
     int d0;      // first decode row (index into drows)

@@ -2,7 +2,8 @@
 // causal attention for FINETUNE / EVAL / PREFILL rows, KV-cache initialisation for prefills and
 // append + attention over the cache for decodes (reading R14, oracle/attention.py).
 //
-//   attn_kv_write_kernel   : prefill rows -> cache[slot][0..L), decode rows -> cache[slot][past + i]
+//   attn_kv_write_kernel   : prefill rows -> cache[slot][0..L) (decode rows are appended by the
+//                            decode kernel: cache[slot][past + i])
 //   attn_prefill_kernel    : one CTA per (segment, 128-query block, query head), tcgen05 with the
 //                            accumulators in TMEM: S = Q K_j^T (M=128, N=128 keys, K=d=128) ->
 //                            online softmax by 4 warps (thread = query row; running max / sum in
@@ -805,7 +806,29 @@ __global__ void __launch_bounds__(128, 4) attn_decode_split_kernel(const __grid_
         }
     }
     __syncthreads();   // barrier init visible
+    // this call's rows of the segment up to the group's last one (cache positions seg_past ..
+    // pos0 + n - 1, the earlier groups' rows included) are not in the cache yet: they are appended
+    // by this kernel, not by a separate cache-write launch -- the CTAs of the chunk(s) holding
+    // those positions patch the fresh K / V rows of their KV head into the staged chunk and store
+    // them into the cache (rows of earlier groups are stored by several groups: the same bytes)
+    const int seg_past = a.drows[grp.d0].pad;
+    const int q0 = max(seg_past, j0), q1 = min(grp.pos0 + grp.n, j0 + kDecChunk);
+    auto append_rows = [&](const void *src, void *cache, uint8_t *buf) {
+        for (int i = t; i < (q1 - q0) * 16; i += blockDim.x) {
+            const int pos = q0 + (i >> 4), u = i & 15;
+            const int row = a.drows[grp.d0 + pos - grp.pos0].row;
+            const uint4 v = *(reinterpret_cast<const uint4 *>(reinterpret_cast<const __nv_bfloat16 *>(src) +
+                                                             ((size_t)row * a.n_kv_heads + kvh) * 128) + u);
+            *reinterpret_cast<uint4 *>(buf + dec_sw(pos - j0, u)) = v;
+            *(reinterpret_cast<uint4 *>(reinterpret_cast<__nv_bfloat16 *>(cache) +
+                                        (((size_t)grp.slot * a.cache_capacity + pos) * a.n_kv_heads + kvh) * 128) + u) = v;
+        }
+    };
     mbar_wait(smem_u32(&bars[0]), 0);   // K
+    if (q0 < q1) {
+        append_rows(a.K, a.K_cache, ksm);
+        __syncthreads();
+    }
     // S^T (keys x columns): warp w takes keys 32 w .. 32 w + 31 (two m16 tiles), 8 k16 steps over d
     float c[2][NT][4] = {};
     {
@@ -878,6 +901,7 @@ __global__ void __launch_bounds__(128, 4) attn_decode_split_kernel(const __grid_
     mbar_wait(smem_u32(&bars[1]), 0);   // V
     for (int i = nk * 16 + t; i < kDecChunk * 16; i += blockDim.x)   // V rows past the chunk: zero (p = 0 there)
         *reinterpret_cast<uint4 *>(vsm + dec_sw(i >> 4, i & 15)) = make_uint4(0, 0, 0, 0);
+    if (q0 < q1) append_rows(a.V, a.V_cache, vsm);
     __syncthreads();
     // the partial records of the columns whose row sees keys of this chunk: {max, sum, o[128]}
     auto rec = [&](int n) -> float * {
