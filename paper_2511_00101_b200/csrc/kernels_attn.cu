@@ -782,12 +782,19 @@ __global__ void __launch_bounds__(128, 4) attn_decode_split_kernel(const __grid_
     // the chunk's K and V rows by TMA (one 2-D box per 64 d; rows past the chunk are the slot's later
     // positions or the next slot's: masked in S, zeroed in V before P V)
     const int crow = grp.slot * a.cache_capacity + j0;
+    // a chunk that starts at or after the segment's first new position holds no cached row: all its
+    // visible rows are this call's, appended below from K / V -- no cache load at all
+    const int seg_past = a.drows[grp.d0].pad;
+    const bool cached = j0 < seg_past;
     if (t == 0) {
         mbar_init(smem_u32(&bars[0]), 1);
         mbar_init(smem_u32(&bars[1]), 1);
         fence_mbar_init();
-        mbar_expect_tx(smem_u32(&bars[0]), 32768u);
-        for (int h = 0; h < 2; ++h) tma_load_2d(smem_u32(ksm) + 16384u * h, &a.tmKc, smem_u32(&bars[0]), kvh * 128 + 64 * h, crow);
+        if (cached) {
+            mbar_expect_tx(smem_u32(&bars[0]), 32768u);
+            for (int h = 0; h < 2; ++h)
+                tma_load_2d(smem_u32(ksm) + 16384u * h, &a.tmKc, smem_u32(&bars[0]), kvh * 128 + 64 * h, crow);
+        }
     }
     // Q^T as the B operand (k = d, n = column): n = 8 nt + lane / 4, k pairs 2 (lane % 4) (+ 8)
     const int gq = lane >> 2, tq = lane & 3;
@@ -811,7 +818,6 @@ __global__ void __launch_bounds__(128, 4) attn_decode_split_kernel(const __grid_
     // by this kernel, not by a separate cache-write launch -- the CTAs of the chunk(s) holding
     // those positions patch the fresh K / V rows of their KV head into the staged chunk and store
     // them into the cache (rows of earlier groups are stored by several groups: the same bytes)
-    const int seg_past = a.drows[grp.d0].pad;
     const int q0 = max(seg_past, j0), q1 = min(grp.pos0 + grp.n, j0 + kDecChunk);
     auto append_rows = [&](const void *src, void *cache, uint8_t *buf) {
         for (int i = t; i < (q1 - q0) * 16; i += blockDim.x) {
@@ -824,7 +830,7 @@ __global__ void __launch_bounds__(128, 4) attn_decode_split_kernel(const __grid_
                                         (((size_t)grp.slot * a.cache_capacity + pos) * a.n_kv_heads + kvh) * 128) + u) = v;
         }
     };
-    mbar_wait(smem_u32(&bars[0]), 0);   // K
+    if (cached) mbar_wait(smem_u32(&bars[0]), 0);   // K
     if (q0 < q1) {
         append_rows(a.K, a.K_cache, ksm);
         __syncthreads();
@@ -871,7 +877,7 @@ __global__ void __launch_bounds__(128, 4) attn_decode_split_kernel(const __grid_
                 if (gq == 0) red_m[warp][n] = m;
             }
     __syncthreads();   // every warp is past S: K's buffer takes V
-    if (t == 0) {
+    if (t == 0 && cached) {
         fence_proxy_async_smem();   // the K reads (generic) before the async-proxy V writes
         mbar_expect_tx(smem_u32(&bars[1]), 32768u);
         for (int h = 0; h < 2; ++h) tma_load_2d(smem_u32(vsm) + 16384u * h, &a.tmVc, smem_u32(&bars[1]), kvh * 128 + 64 * h, crow);
@@ -898,7 +904,7 @@ __global__ void __launch_bounds__(128, 4) attn_decode_split_kernel(const __grid_
                 l += __shfl_xor_sync(0xffffffffu, l, 16);
                 if (gq == 0) red_l[warp][n] = l;
             }
-    mbar_wait(smem_u32(&bars[1]), 0);   // V
+    if (cached) mbar_wait(smem_u32(&bars[1]), 0);   // V
     for (int i = nk * 16 + t; i < kDecChunk * 16; i += blockDim.x)   // V rows past the chunk: zero (p = 0 there)
         *reinterpret_cast<uint4 *>(vsm + dec_sw(i >> 4, i & 15)) = make_uint4(0, 0, 0, 0);
     if (q0 < q1) append_rows(a.V, a.V_cache, vsm);
