@@ -74,6 +74,26 @@ def test_multi_row_decode_segments(hq, hkv):
     assert np.array_equal(Kd.double().numpy(), Kr) and np.array_equal(Vd.double().numpy(), Vr)
 
 
+@pytest.mark.parametrize("hq,hkv", [(32, 8), (8, 2)])
+def test_decode_chunk_aligned_and_capacity_edge(hq, hkv):
+    """DECODE segments whose new rows start exactly at a 128-key chunk boundary (that chunk holds
+    no cached row: the kernel skips its cache load and takes every visible row from K / V), span
+    two chunks, or end at the last cache position; the caches must equal the oracle's bit for bit
+    (the appended rows written once per KV head, nothing else touched)."""
+    lengths = [9, 40, 12, 1, 3]
+    modes = [DECODE] * 5
+    slots = [0, 1, 2, 3, 4]
+    past = [256, 100, 500, 384, 0]   # chunk-aligned, straddling 128, up to cap - 1, aligned single, empty cache
+    offs, Q, K, V, Kc, Vc = _case(29 + hq, lengths, modes, slots, past, hq, hkv, cap=512, n_slots=5)
+    O, Kd, Vd = _run(offs, modes, slots, past, Q, K, V, Kc, Vc)
+    Or, Kr, Vr = OA.attention(offs, modes, slots, past, Q, K, V, Kc, Vc, 1.0 / math.sqrt(128))
+    assert not torch.isnan(O).any()
+    for g in range(len(modes)):
+        a, bnd = offs[g], offs[g + 1]
+        assert parity_err(O[a:bnd], Or[a:bnd]) <= BF16_TOL, (g, parity_err(O[a:bnd], Or[a:bnd]))
+    assert np.array_equal(Kd.double().numpy(), Kr) and np.array_equal(Vd.double().numpy(), Vr)
+
+
 def test_long_prefill_many_blocks_and_empty_segments():
     lengths = [0, 777, 0, 5]
     modes = [PREFILL, FINETUNE, DECODE, EVAL]
