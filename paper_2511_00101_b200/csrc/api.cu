@@ -53,7 +53,8 @@ int adamw_grid(int num_sms, size_t n);
 int launch_adamw_sumsq(const AdamwArgs &a, float *partial, int grid, cudaStream_t st);
 int launch_fanout_signal(const FanoutFlags &f, cudaStream_t st);
 int launch_fanout_wait(const int *ready, int target, cudaStream_t st);
-int launch_attn(const AttnArgs &a, int n_items, int n_rows, int n_drows, int n_dgroups, cudaStream_t st);
+int launch_attn(const AttnArgs &a, const AttnDecInline &dinl, int n_items, int n_rows, int n_drows, int n_dgroups,
+                cudaStream_t st);
 int launch_adamw_step(const AdamwArgs &a, int grid, cudaStream_t st);
 int launch_shrink_split(const __nv_bfloat16 *X, const SlotDev *slots, const DevBlock *blocks,
                         const DevShortRow *srows, int n_blocks, int in_f, int r, int r_pad, float *part,
@@ -2076,7 +2077,16 @@ int smlm_attention(const smlm_attn_batch *b, int n_heads, int n_kv_heads, int he
     append(bytes, P.drows);
     const size_t dgroups_off = bytes.size();
     append(bytes, P.dgroups);
-    if ((rc = stage_upload(&g_attn_stage, bytes, wsb, st))) return rc;
+    // a small decode plan rides in the decode kernels' parameters; nothing to upload for a
+    // decode-only call then
+    const bool dec_inline = P.drows.size() <= (size_t)kAttnDecInline && P.dgroups.size() <= (size_t)kAttnDecInline;
+    static thread_local AttnDecInline dinl;
+    if (dec_inline) {
+        std::copy(P.drows.begin(), P.drows.end(), dinl.drows);
+        std::copy(P.dgroups.begin(), P.dgroups.end(), dinl.dgroups);
+    }
+    const bool upload = !(dec_inline && P.items.empty() && P.rows.empty());
+    if (upload && (rc = stage_upload(&g_attn_stage, bytes, wsb, st))) return rc;
     AttnArgs a;
     memset(&a, 0, sizeof(a));
     a.dbg = measure_flag("SMLM_ATTN_DEBUG");
@@ -2110,7 +2120,8 @@ int smlm_attention(const smlm_attn_batch *b, int n_heads, int n_kv_heads, int he
     a.dpart = reinterpret_cast<float *>(wsb + attn_plan_bytes(P));
     // launches: the cache write of PREFILL rows, the prefill kernel, the decode split + combine
     const int nl = (P.rows.empty() ? 0 : 1) + (P.items.empty() ? 0 : 1) + (P.drows.empty() ? 0 : 2);
-    CKL(launch_attn(a, (int)P.items.size(), (int)P.rows.size(), (int)P.drows.size(), (int)P.dgroups.size(), st), nl);
+    a.dec_inline = dec_inline ? 1 : 0;
+    CKL(launch_attn(a, dinl, (int)P.items.size(), (int)P.rows.size(), (int)P.drows.size(), (int)P.dgroups.size(), st), nl);
     return SMLM_OK;
 }
 

@@ -290,6 +290,13 @@ struct alignas(16) AttnDGroup {   // consecutive decode rows of one DECODE segme
     int slot;
 };
 constexpr int kAttnDecCols = 32;   // query columns (rows x GQA heads) of one decode CTA
+// a decode plan of up to kAttnDecInline rows / groups rides in the decode kernels' parameters (no
+// plan upload launch before them)
+constexpr int kAttnDecInline = 256;
+struct AttnDecInline {
+    AttnRow drows[kAttnDecInline];
+    AttnDGroup dgroups[kAttnDecInline];
+};
 struct AttnArgs {
     CUtensorMap tmQ;   // Q [S, Hq*d] box {64, 128}
     CUtensorMap tmK;   // K [S, Hkv*d] box {64, 128}
@@ -309,6 +316,7 @@ struct AttnArgs {
     float scale;
     float *dpart;      // decode split partials [drows * n_kv_heads * max_splits][G][130] fp32
     int max_splits;    // ceil(longest decode context / kAttnDecChunk)
+    int dec_inline;    // drows / dgroups are in the decode kernels' AttnDecInline parameter
     int dbg;           // measure build only (SMLM_ATTN_DEBUG): the softmax warps print their phase cycles
 };
 

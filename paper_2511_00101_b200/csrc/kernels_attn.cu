@@ -760,13 +760,16 @@ __device__ __forceinline__ void mma16816(float (&d)[4], uint32_t a0, uint32_t a1
 }
 
 template <int G>
-__global__ void __launch_bounds__(128, 4) attn_decode_split_kernel(const __grid_constant__ AttnArgs a) {
+__global__ void __launch_bounds__(128, 4) attn_decode_split_kernel(const __grid_constant__ AttnArgs a,
+                                                                    const __grid_constant__ AttnDecInline dinl) {
+    const AttnRow *drows = a.dec_inline ? dinl.drows : a.drows;
+    const AttnDGroup *dgroups = a.dec_inline ? dinl.dgroups : a.dgroups;
     pdl_wait();
     pdl_trigger();
     constexpr int NT = kAttnDecCols / 8;   // n8 tiles of query columns (column = row * G + head)
     const int s = blockIdx.x % a.max_splits;
     const int kvh = (blockIdx.x / a.max_splits) % a.n_kv_heads;
-    const AttnDGroup grp = a.dgroups[blockIdx.x / (a.max_splits * a.n_kv_heads)];
+    const AttnDGroup grp = dgroups[blockIdx.x / (a.max_splits * a.n_kv_heads)];
     const int Lmax = grp.pos0 + grp.n;   // keys of the group's last row (the cache holds the rows themselves)
     const int j0 = s * kDecChunk;
     if (j0 >= Lmax) return;
@@ -784,7 +787,7 @@ __global__ void __launch_bounds__(128, 4) attn_decode_split_kernel(const __grid_
     const int crow = grp.slot * a.cache_capacity + j0;
     // a chunk that starts at or after the segment's first new position holds no cached row: all its
     // visible rows are this call's, appended below from K / V -- no cache load at all
-    const int seg_past = a.drows[grp.d0].pad;
+    const int seg_past = drows[grp.d0].pad;
     const bool cached = j0 < seg_past;
     if (t == 0) {
         mbar_init(smem_u32(&bars[0]), 1);
@@ -805,7 +808,7 @@ __global__ void __launch_bounds__(128, 4) attn_decode_split_kernel(const __grid_
         const bool in = n < ncol;
         const int drow = grp.d0 + (in ? n / G : 0);
         const uint32_t *Qh = reinterpret_cast<const uint32_t *>(
-            reinterpret_cast<const __nv_bfloat16 *>(a.Q) + ((size_t)a.drows[drow].row * a.n_heads + kvh * G + n % G) * 128);
+            reinterpret_cast<const __nv_bfloat16 *>(a.Q) + ((size_t)drows[drow].row * a.n_heads + kvh * G + n % G) * 128);
 #pragma unroll
         for (int ks = 0; ks < 8; ++ks) {
             qb[nt][ks][0] = (in && nt < ntiles) ? Qh[8 * ks + tq] : 0u;
@@ -822,7 +825,7 @@ __global__ void __launch_bounds__(128, 4) attn_decode_split_kernel(const __grid_
     auto append_rows = [&](const void *src, void *cache, uint8_t *buf) {
         for (int i = t; i < (q1 - q0) * 16; i += blockDim.x) {
             const int pos = q0 + (i >> 4), u = i & 15;
-            const int row = a.drows[grp.d0 + pos - grp.pos0].row;
+            const int row = drows[grp.d0 + pos - grp.pos0].row;
             const uint4 v = *(reinterpret_cast<const uint4 *>(reinterpret_cast<const __nv_bfloat16 *>(src) +
                                                              ((size_t)row * a.n_kv_heads + kvh) * 128) + u);
             *reinterpret_cast<uint4 *>(buf + dec_sw(pos - j0, u)) = v;
@@ -964,12 +967,13 @@ __global__ void __launch_bounds__(128, 4) attn_decode_split_kernel(const __grid_
 
 // thread (head g, dims 4 q .. 4 q + 3) of decode row rk / n_kv_heads: the splits merged in split
 // order.  32 threads per head: every CTA of the launch is resident in one wave
-__global__ void __launch_bounds__(256) attn_decode_combine_kernel(const AttnArgs a) {
+__global__ void __launch_bounds__(256) attn_decode_combine_kernel(const __grid_constant__ AttnArgs a,
+                                                                  const __grid_constant__ AttnDecInline dinl) {
     pdl_wait();
     pdl_trigger();
     const int G = a.n_heads / a.n_kv_heads;
     const int rk = blockIdx.x;
-    const AttnRow rw = a.drows[rk / a.n_kv_heads];
+    const AttnRow rw = (a.dec_inline ? dinl.drows : a.drows)[rk / a.n_kv_heads];
     const int kvh = rk % a.n_kv_heads;
     const int ns = (rw.pos + 1 + kDecChunk - 1) / kDecChunk;
     const int g = threadIdx.x >> 5, q = threadIdx.x & 31;
@@ -1000,7 +1004,8 @@ __global__ void __launch_bounds__(256) attn_decode_combine_kernel(const AttnArgs
 size_t attn_prefill_smem() { return 1024 + kQBytes + 2 * kKVBytes + 2 * kPBytes + 128; }
 static_assert(120 + 4 <= 128, "prefill barriers exceed their area");
 
-int launch_attn(const AttnArgs &a, int n_items, int n_rows, int n_drows, int n_dgroups, cudaStream_t st) {
+int launch_attn(const AttnArgs &a, const AttnDecInline &dinl, int n_items, int n_rows, int n_drows, int n_dgroups,
+                cudaStream_t st) {
     cudaError_t e = cudaSuccess;
     if (n_rows) {
         e = launch_pdl(attn_kv_write_kernel, dim3(n_rows), dim3(256), 0, st, a);
@@ -1047,15 +1052,15 @@ int launch_attn(const AttnArgs &a, int n_items, int n_rows, int n_drows, int n_d
             dattr = true;
         }
         switch (a.n_heads / a.n_kv_heads) {
-            case 1: e = launch_pdl(attn_decode_split_kernel<1>, grid, dim3(128), kDecSmem, st, a); break;
-            case 2: e = launch_pdl(attn_decode_split_kernel<2>, grid, dim3(128), kDecSmem, st, a); break;
-            case 4: e = launch_pdl(attn_decode_split_kernel<4>, grid, dim3(128), kDecSmem, st, a); break;
-            case 8: e = launch_pdl(attn_decode_split_kernel<8>, grid, dim3(128), kDecSmem, st, a); break;
+            case 1: e = launch_pdl(attn_decode_split_kernel<1>, grid, dim3(128), kDecSmem, st, a, dinl); break;
+            case 2: e = launch_pdl(attn_decode_split_kernel<2>, grid, dim3(128), kDecSmem, st, a, dinl); break;
+            case 4: e = launch_pdl(attn_decode_split_kernel<4>, grid, dim3(128), kDecSmem, st, a, dinl); break;
+            case 8: e = launch_pdl(attn_decode_split_kernel<8>, grid, dim3(128), kDecSmem, st, a, dinl); break;
             default: return (int)cudaErrorInvalidValue;
         }
         if (e != cudaSuccess) return (int)e;
         e = launch_pdl(attn_decode_combine_kernel, dim3(n_drows * a.n_kv_heads), dim3(32 * (a.n_heads / a.n_kv_heads)), 0,
-                       st, a);
+                       st, a, dinl);
     }
     return (int)e;
 }
