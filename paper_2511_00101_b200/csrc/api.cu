@@ -2119,8 +2119,10 @@ int smlm_attention(const smlm_attn_batch *b, int n_heads, int n_kv_heads, int he
     a.max_splits = (P.max_dec_len + kAttnDecChunk - 1) / kAttnDecChunk;
     a.dpart = reinterpret_cast<float *>(wsb + attn_plan_bytes(P));
     // launches: the cache write of PREFILL rows, the prefill kernel, the decode split + combine
-    const int nl = (P.rows.empty() ? 0 : 1) + (P.items.empty() ? 0 : 1) + (P.drows.empty() ? 0 : 2);
+    const bool fused_rows = !P.items.empty() && (n_heads / n_kv_heads) % 2 == 0 && n_kv_heads <= 8;   // prefill warp 2
+    const int nl = (P.rows.empty() || fused_rows ? 0 : 1) + (P.items.empty() ? 0 : 1) + (P.drows.empty() ? 0 : 2);
     a.dec_inline = dec_inline ? 1 : 0;
+    a.n_rows = (int)P.rows.size();
     CKL(launch_attn(a, dinl, (int)P.items.size(), (int)P.rows.size(), (int)P.drows.size(), (int)P.dgroups.size(), st), nl);
     return SMLM_OK;
 }

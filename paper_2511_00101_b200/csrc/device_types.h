@@ -312,6 +312,7 @@ struct AttnArgs {
     void *O;
     void *K_cache, *V_cache;   // [slots, capacity, Hkv, d] bf16
     int n_heads, n_kv_heads;
+    int n_rows;        // cache writes (rows); the two-tile prefill kernel's warp 2 copies them
     int cache_capacity;
     float scale;
     float *dpart;      // decode split partials [drows * n_kv_heads * max_splits][G][130] fp32

@@ -446,6 +446,44 @@ __global__ void __launch_bounds__(kAT2, 1) attn_prefill2_kernel(const __grid_con
                 }
             }
         }
+    } else if (warp == 2) {
+        // ---------------- KV-cache writes of the PREFILL rows (no separate launch) ----------------
+        // this warp is idle after the TMEM allocation: rows b, b + grid, ... of the cache-write list
+        // are copied with 16-byte loads / stores while the tensor pipe and the softmax run
+        // (loads of several rows in flight before their stores: one warp must keep ~16 KB moving)
+        const int re = a.n_kv_heads * 16;   // uint4 per K (or V) row
+        constexpr int kR = 4;               // rows per batch
+        for (int r0 = blockIdx.x; a.n_kv_heads <= 8 && r0 < a.n_rows; r0 += kR * gridDim.x) {
+            uint4 kv[kR][2][4];
+            AttnRow rw[kR];
+#pragma unroll
+            for (int q = 0; q < kR; ++q) {
+                const int rr = r0 + q * gridDim.x;
+                rw[q] = rr < a.n_rows ? a.rows[rr] : AttnRow{0, -1, 0, 0};
+            }
+#pragma unroll
+            for (int q = 0; q < kR; ++q)
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int i = lane + 32 * u;
+                    if (rw[q].slot >= 0 && i < re) {
+                        kv[q][0][u] = reinterpret_cast<const uint4 *>(a.K)[(size_t)rw[q].row * re + i];
+                        kv[q][1][u] = reinterpret_cast<const uint4 *>(a.V)[(size_t)rw[q].row * re + i];
+                    }
+                }
+#pragma unroll
+            for (int q = 0; q < kR; ++q)
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int i = lane + 32 * u;
+                    if (rw[q].slot >= 0 && i < re) {
+                        const size_t dst = ((size_t)rw[q].slot * a.cache_capacity + rw[q].pos) * re + i;
+                        reinterpret_cast<uint4 *>(a.K_cache)[dst] = kv[q][0][u];
+                        reinterpret_cast<uint4 *>(a.V_cache)[dst] = kv[q][1][u];
+                    }
+                }
+        }
+        // (n_kv_heads <= 8: a K row is at most 128 uint4 = 4 per lane)
     } else if (warp == 3) {
         // ---------------- TMA: V (one buffer; free once both tiles' PV have read it) ----------------
         if (lane == 0) {
@@ -1007,7 +1045,9 @@ static_assert(120 + 4 <= 128, "prefill barriers exceed their area");
 int launch_attn(const AttnArgs &a, const AttnDecInline &dinl, int n_items, int n_rows, int n_drows, int n_dgroups,
                 cudaStream_t st) {
     cudaError_t e = cudaSuccess;
-    if (n_rows) {
+    // the two-tile prefill kernel (even GQA groups) writes the cache rows itself (warp 2)
+    const bool fused_rows = n_items && (a.n_heads / a.n_kv_heads) % 2 == 0 && a.n_kv_heads <= 8;
+    if (n_rows && !fused_rows) {
         e = launch_pdl(attn_kv_write_kernel, dim3(n_rows), dim3(256), 0, st, a);
         if (e != cudaSuccess) return (int)e;
     }
