@@ -1987,6 +1987,7 @@ struct AttnPlan {
     std::vector<AttnRow> rows, drows;
     std::vector<AttnDGroup> dgroups;
     int max_dec_len = 0;
+    int n_cache_rows = 0;   // PREFILL rows written to the cache
 };
 int attn_plan(const smlm_attn_batch *b, int n_heads, int n_kv_heads, int head_dim, int cache_slots, int capacity,
               AttnPlan &P) {
@@ -2022,7 +2023,14 @@ int attn_plan(const smlm_attn_batch *b, int n_heads, int n_kv_heads, int head_di
             if (m == SMLM_PREFILL && slot >= 0) {
                 if (slot >= cache_slots || L > capacity)
                     return set_err(SMLM_E_INVALID, "attention: PREFILL cache slot out of range or too short");
-                for (int i = 0; i < L; ++i) P.rows.push_back({a0 + i, slot, i, 0});
+                if ((n_heads / n_kv_heads) % 2 == 0 && n_kv_heads <= 8) {
+                    // the two-tile prefill kernel writes the cache: one record per segment
+                    // {first row, slot, rows before it in the write list, length}
+                    P.rows.push_back({a0, slot, P.n_cache_rows, L});
+                } else {
+                    for (int i = 0; i < L; ++i) P.rows.push_back({a0 + i, slot, i, 0});
+                }
+                P.n_cache_rows += L;
             }
             for (int qb = 0; qb * 128 < L; ++qb) P.items.push_back({a0, L, qb, 0});
         }
@@ -2123,6 +2131,7 @@ int smlm_attention(const smlm_attn_batch *b, int n_heads, int n_kv_heads, int he
     const int nl = (P.rows.empty() || fused_rows ? 0 : 1) + (P.items.empty() ? 0 : 1) + (P.drows.empty() ? 0 : 2);
     a.dec_inline = dec_inline ? 1 : 0;
     a.n_rows = (int)P.rows.size();
+    a.n_cache_rows = P.n_cache_rows;
     CKL(launch_attn(a, dinl, (int)P.items.size(), (int)P.rows.size(), (int)P.drows.size(), (int)P.dgroups.size(), st), nl);
     return SMLM_OK;
 }

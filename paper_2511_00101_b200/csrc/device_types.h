@@ -312,7 +312,9 @@ struct AttnArgs {
     void *O;
     void *K_cache, *V_cache;   // [slots, capacity, Hkv, d] bf16
     int n_heads, n_kv_heads;
-    int n_rows;        // cache writes (rows); the two-tile prefill kernel's warp 2 copies them
+    int n_rows;        // cache-write records: rows (attn_kv_write_kernel) or, for the two-tile prefill
+                       // kernel (its warp 2 copies them), segments {row0, slot, list offset, length}
+    int n_cache_rows;  // rows written to the cache
     int cache_capacity;
     float scale;
     float *dpart;      // decode split partials [drows * n_kv_heads * max_splits][G][130] fp32

@@ -451,24 +451,36 @@ __global__ void __launch_bounds__(kAT2, 1) attn_prefill2_kernel(const __grid_con
         // this warp is idle after the TMEM allocation: rows b, b + grid, ... of the cache-write list
         // are copied with 16-byte loads / stores while the tensor pipe and the softmax run
         // (loads of several rows in flight before their stores: one warp must keep ~16 KB moving)
+        // the write list is per segment {first row, slot, offset in the list, length}: row rr of the
+        // list is found by a scan over the (few) segments
         const int re = a.n_kv_heads * 16;   // uint4 per K (or V) row
         constexpr int kR = 4;               // rows per batch
-        for (int r0 = blockIdx.x; a.n_kv_heads <= 8 && r0 < a.n_rows; r0 += kR * gridDim.x) {
+        int sg = 0;                         // segment of the batch's first row (rows increase)
+        for (int r0 = blockIdx.x; a.n_kv_heads <= 8 && r0 < a.n_cache_rows; r0 += kR * gridDim.x) {
             uint4 kv[kR][2][4];
-            AttnRow rw[kR];
+            int src[kR], dst[kR];   // input row, cache row (slot * capacity + position); -1: none
 #pragma unroll
             for (int q = 0; q < kR; ++q) {
                 const int rr = r0 + q * gridDim.x;
-                rw[q] = rr < a.n_rows ? a.rows[rr] : AttnRow{0, -1, 0, 0};
+                src[q] = -1;
+                dst[q] = 0;
+                if (rr < a.n_cache_rows) {
+                    int g2 = sg;
+                    while (g2 + 1 < a.n_rows && a.rows[g2 + 1].pos <= rr) ++g2;
+                    if (q == 0) sg = g2;
+                    const AttnRow seg = a.rows[g2];
+                    src[q] = seg.row + (rr - seg.pos);
+                    dst[q] = seg.slot * a.cache_capacity + (rr - seg.pos);
+                }
             }
 #pragma unroll
             for (int q = 0; q < kR; ++q)
 #pragma unroll
                 for (int u = 0; u < 4; ++u) {
                     const int i = lane + 32 * u;
-                    if (rw[q].slot >= 0 && i < re) {
-                        kv[q][0][u] = reinterpret_cast<const uint4 *>(a.K)[(size_t)rw[q].row * re + i];
-                        kv[q][1][u] = reinterpret_cast<const uint4 *>(a.V)[(size_t)rw[q].row * re + i];
+                    if (src[q] >= 0 && i < re) {
+                        kv[q][0][u] = reinterpret_cast<const uint4 *>(a.K)[(size_t)src[q] * re + i];
+                        kv[q][1][u] = reinterpret_cast<const uint4 *>(a.V)[(size_t)src[q] * re + i];
                     }
                 }
 #pragma unroll
@@ -476,10 +488,9 @@ __global__ void __launch_bounds__(kAT2, 1) attn_prefill2_kernel(const __grid_con
 #pragma unroll
                 for (int u = 0; u < 4; ++u) {
                     const int i = lane + 32 * u;
-                    if (rw[q].slot >= 0 && i < re) {
-                        const size_t dst = ((size_t)rw[q].slot * a.cache_capacity + rw[q].pos) * re + i;
-                        reinterpret_cast<uint4 *>(a.K_cache)[dst] = kv[q][0][u];
-                        reinterpret_cast<uint4 *>(a.V_cache)[dst] = kv[q][1][u];
+                    if (src[q] >= 0 && i < re) {
+                        reinterpret_cast<uint4 *>(a.K_cache)[(size_t)dst[q] * re + i] = kv[q][0][u];
+                        reinterpret_cast<uint4 *>(a.V_cache)[(size_t)dst[q] * re + i] = kv[q][1][u];
                     }
                 }
         }
