@@ -2023,13 +2023,9 @@ int attn_plan(const smlm_attn_batch *b, int n_heads, int n_kv_heads, int head_di
             if (m == SMLM_PREFILL && slot >= 0) {
                 if (slot >= cache_slots || L > capacity)
                     return set_err(SMLM_E_INVALID, "attention: PREFILL cache slot out of range or too short");
-                if ((n_heads / n_kv_heads) % 2 == 0 && n_kv_heads <= 8) {
-                    // the two-tile prefill kernel writes the cache: one record per segment
-                    // {first row, slot, rows before it in the write list, length}
-                    P.rows.push_back({a0, slot, P.n_cache_rows, L});
-                } else {
-                    for (int i = 0; i < L; ++i) P.rows.push_back({a0 + i, slot, i, 0});
-                }
+                // one cache-write record per segment {first row, slot, rows before it in the
+                // write list, length}: a small plan (the parameter-blob upload, not a memcpy)
+                P.rows.push_back({a0, slot, P.n_cache_rows, L});
                 P.n_cache_rows += L;
             }
             for (int qb = 0; qb * 128 < L; ++qb) P.items.push_back({a0, L, qb, 0});

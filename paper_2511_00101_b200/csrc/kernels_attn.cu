@@ -757,7 +757,16 @@ __global__ void __launch_bounds__(kAT2, 1) attn_prefill2_kernel(const __grid_con
 __global__ void __launch_bounds__(256) attn_kv_write_kernel(const AttnArgs a) {
     pdl_wait();
     pdl_trigger();
-    const AttnRow rw = a.rows[blockIdx.x];
+    // row blockIdx.x of the write list: its segment record by binary search over the offsets
+    const int rr = blockIdx.x;
+    int lo = 0, hi = a.n_rows - 1;
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (a.rows[mid].pos <= rr) lo = mid;
+        else hi = mid - 1;
+    }
+    const AttnRow sg = a.rows[lo];
+    const AttnRow rw{sg.row + (rr - sg.pos), sg.slot, rr - sg.pos, 0};
     if (rw.slot < 0) return;
     const size_t row_elems = (size_t)a.n_kv_heads * 128;
     const uint4 *ks = reinterpret_cast<const uint4 *>(reinterpret_cast<const __nv_bfloat16 *>(a.K) + (size_t)rw.row * row_elems);
@@ -1059,7 +1068,7 @@ int launch_attn(const AttnArgs &a, const AttnDecInline &dinl, int n_items, int n
     // the two-tile prefill kernel (even GQA groups) writes the cache rows itself (warp 2)
     const bool fused_rows = n_items && (a.n_heads / a.n_kv_heads) % 2 == 0 && a.n_kv_heads <= 8;
     if (n_rows && !fused_rows) {
-        e = launch_pdl(attn_kv_write_kernel, dim3(n_rows), dim3(256), 0, st, a);
+        e = launch_pdl(attn_kv_write_kernel, dim3(a.n_cache_rows), dim3(256), 0, st, a);
         if (e != cudaSuccess) return (int)e;
     }
     if (n_items) {
