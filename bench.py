@@ -20,6 +20,7 @@ sample of the same workload on this box's host cores (rank 0 only).
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import math
 import os
@@ -571,6 +572,14 @@ def main():
     if not args.no_e2e:
         e2e = run_e2e(wl, stream, max(4, min(args.steps, 8)), n, dist)
 
+    # the headline workload's device memory (8 layer sets, ~20 GB) is released before the side
+    # measurements, which then run on their own allocations as a standalone run would
+    wl_rows, wl_ft_rows = wl.rows, wl.ft_rows
+    del wl
+    gc.collect()
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+
     # ---- the other BASELINE.json configs as side measurements (rank 0, N=1): C2 decode layer-step
     # (q/k/v in one smlm_forward_multi launch + o; CUDA-graph replay) and C3 prefill ----
     side = None
@@ -621,7 +630,7 @@ def main():
                "config": {"workload": spec.name + ": Llama-3-8B projections q,k,v,o,gate,up,down; r=16; "
                           f"{spec.n_adapters} adapters; 4 fine-tune x 1024 rows (fwd+bwd) + 8 prefill "
                           "(512-2048) + 128 decode rows",
-                          "rows_per_layer_per_gpu": wl.rows, "finetune_rows": wl.ft_rows, "rank": spec.rank,
+                          "rows_per_layer_per_gpu": wl_rows, "finetune_rows": wl_ft_rows, "rank": spec.rank,
                           "adapters": spec.n_adapters, "parallelism": f"dp{n}", "layers_per_step": N_LAYERS,
                           "l2": f"inputs larger than L2: every layer of the step has its own weight set "
                                 f"(416 MiB each, {N_LAYERS} per step)",
