@@ -587,6 +587,7 @@ def main():
         try:
             sys.path.insert(0, os.path.join(ROOT, "scripts"))
             import bench_configs as bc
+            at = bc.attention_step()   # first: the smallest side workloads on a clean heap
             c2 = bc.c2_layer_step()
             rows3, tot3 = bc.run_config(3, iters=10)
             side = {"C2_decode": {"workload": c2["config"], "rows": c2["S"], "ms_graph_replay": c2["ms_graph_replay"],
@@ -598,7 +599,6 @@ def main():
                                    "rows_per_s": synth.config_batch(3).S / (tot3 / 1e3),
                                    "tensor_roofline_frac": sum(r["roofline_ms"] for r in rows3) / tot3,
                                    "bound": "tensor"}}
-            at = bc.attention_step()
             side["F4_attention"] = {"workload": at["workload"], "prefill_ms": at["prefill_ms"],
                                     "prefill_tflops": at["prefill_tflops"],
                                     "prefill_tensor_roofline_frac": at["prefill_tensor_frac"],
